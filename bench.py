@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the MPLD hot path (BASELINE.json metric: components/s and ms per
+layout; cost bit-exact vs the CPU oracle).
+
+One step = one pass of the whole hot path (validate -> simplify -> components ->
+exact-cover search -> recover -> evaluate) over one batch of synthetic layouts:
+the ten ISCAS-85-shaped layouts of BASELINE.json configs[1] (Table 1
+|V|/|E| for c432..c7552, k = 3, alpha = 0.1, stitch candidates), replicated
+with `--replicas` seeds, resident in HBM.  Under torchrun every rank decomposes
+its own batch (different seeds, no collective on the data path: components and
+layouts are independent) and `value` is all components of all
+ranks over the max-over-ranks device time (weak scaling).
+
+`--impl reference` times the CPU oracle (oracle/, the "reference arm" of this
+tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "components/s"
+MAX_STEPS = 1 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mpld", choices=["mpld", "reference"])
+    ap.add_argument("--replicas", type=int, default=16, help="ISCAS-85 suites per step per rank")
+    ap.add_argument("--max-steps", type=int, default=MAX_STEPS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--profile-launches", action="store_true", help="short run for ncu (no clocks / baselines)")
+    return ap.parse_args()
+
+
+def workload(rank: int, replicas: int):
+    graphs = []
+    for r in range(replicas):
+        gs, k, alpha = synth.config_graphs(1, seed=1000 * rank + 10 * r)
+        graphs += gs
+    return synth.concat(graphs, name="iscas85_x%d" % replicas), k, alpha
+
+
+def config_dict(b, replicas, n_gpus, extra=None):
+    d = {"workload": "configs[1]: ISCAS-85-shaped TPLD suite c432..c7552 (Table 1 |V|,|E|) x%d seeds per rank,"
+                     " k=3, alpha=0.1, stitch candidates" % replicas,
+         "layouts_per_step": int(b.n_layouts), "vertices_per_step": int(b.n),
+         "ce_edges_per_step": int(b.n_ce), "se_edges_per_step": int(b.n_se),
+         "max_steps": MAX_STEPS, "l2": "flushed between timed steps (256 MiB write)",
+         "parallelism": "dp%d (independent layouts per rank)" % n_gpus}
+    if extra:
+        d.update(extra)
+    return d
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def kernel_bytes(b):
+    """Algorithmic bytes per launch of each kernel: the CSR it must
+    read once plus the per-vertex outputs it must write once."""
+    n, m_ce, m_se = b.n, b.ce_col.size, b.se_col.size
+    rowptrs = 8 * (n + 1)
+    return {
+        "mpld_simplify_components": rowptrs + 4 * m_ce + 4 * m_se + 4 * n,  # CSR + hround
+        "mpld_exact_cover_search": None,  # ALU-bound search
+        "mpld_recover": None,
+        "mpld_evaluate": rowptrs + 4 * m_ce + 4 * m_se + 4 * n,  # CSR + colours
+        "mpld_validate": rowptrs + 4 * m_ce + 4 * m_se,
+    }
+
+
+def run_cpu_baseline(b, k, alpha, seconds):
+    import oracle
+    offs = b.layout_offsets.tolist()
+    graphs = []
+    for li in range(b.n_layouts):
+        a, e = offs[li], offs[li + 1]
+        graphs.append((a, e))
+    comps = layouts = 0
+    t0 = time.perf_counter()
+    names = []
+    for li, (a, e) in enumerate(graphs):
+        sub = synth.from_edges(e - a, b.ce_edges()[(b.ce_edges()[:, 0] >= a) & (b.ce_edges()[:, 0] < e)] - a,
+                               b.se_edges()[(b.se_edges()[:, 0] >= a) & (b.se_edges()[:, 0] < e)] - a)
+        r = oracle.decompose(sub, k, alpha, max_steps=MAX_STEPS, check=False)
+        comps += len(r["components"])
+        layouts += 1
+        names.append(li)
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": comps / dt, "unit": METRIC, "cores": 1, "kind": "oracle",
+            "sample": f"first {layouts} layouts of the rank-0 batch ({comps} components, {dt:.1f} s, "
+                      f"single-threaded CPython oracle/mpld.py incl. simplification and recovery)",
+            "ms_per_layout": 1e3 * dt / layouts}
+
+
+def main_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    b, k, alpha = workload(0, args.replicas)
+    import oracle
+    offs = b.layout_offsets.tolist()
+    ce_all, se_all = b.ce_edges(), b.se_edges()
+    subs = []
+    for li in range(b.n_layouts):
+        a, e = offs[li], offs[li + 1]
+        subs.append(synth.from_edges(e - a, ce_all[(ce_all[:, 0] >= a) & (ce_all[:, 0] < e)] - a,
+                                     se_all[(se_all[:, 0] >= a) & (se_all[:, 0] < e)] - a))
+    # each step: a bounded sample (one ISCAS-85 suite = 10 layouts, about 1 s of CPU work)
+    per_step = subs[:10]
+    for _ in range(args.warmup):
+        for g in per_step[:2]:
+            oracle.decompose(g, k, alpha, max_steps=MAX_STEPS, check=False)
+    comps = 0
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        for g in per_step:
+            comps += len(oracle.decompose(g, k, alpha, max_steps=MAX_STEPS, check=False)["components"])
+    dt = time.perf_counter() - t0
+    val = comps / dt
+    out = {"metric": METRIC, "value": val, "unit": METRIC, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+           "ms_per_layout": 1e3 * dt / (args.steps * len(per_step)), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+           "config": config_dict(b, args.replicas, args.gpus,
+                                 {"reference_sample": "one ISCAS-85 suite (10 layouts) per step"}),
+           "cpu_baseline": {"value": val, "unit": METRIC, "cores": 1, "kind": "oracle",
+                            "sample": "10 layouts (c432..c7552, seed 0..9) per step, CPython oracle"},
+           "e2e": {"value": val, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return main_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_14335_b200 as mp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    mp.lib()
+    b, k, alpha = workload(rank, args.replicas)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    d_lo, d_cr, d_cc, d_sr, d_sc = (T(b.layout_offsets), T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr),
+                                    T(b.se_col))
+    L = b.n_layouts
+    colors = torch.empty(b.n, dtype=torch.int32, device=dev)
+    counts = torch.empty(2 * L, dtype=torch.int64, device=dev)
+    cost = torch.empty(L, dtype=torch.float64, device=dev)
+    stats = torch.empty(len(mp.STAT_NAMES), dtype=torch.int64, device=dev)
+    ctx = mp.Context(local, b.n, L)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flags = mp.MPLD_FLAG_VALIDATE
+
+    def step():
+        ctx.decompose_device(d_lo, b.n, d_cr, d_cc, d_sr, d_sc, k, alpha, args.max_steps, colors, counts, cost,
+                             stats, flags=flags, stream=stream)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    st = dict(zip(mp.STAT_NAMES, stats.cpu().tolist()))
+    assert st["error"] == 0, st
+    comps_per_step = st["components"]
+
+    if args.profile_launches:
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        print(json.dumps({"profile_run": True, "stats": st}))
+        return
+
+    ctx.reset_timing()
+    ctx.set_timing(True)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx.set_timing(False)
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    ktimes = ctx.kernel_times()
+    st = dict(zip(mp.STAT_NAMES, stats.cpu().tolist()))
+    assert st["error"] == 0, st
+    launches = sum(v[1] for v in ktimes.values())
+
+    # e2e: the host C-ABI call on pinned host buffers (H2D + kernels + D2H inside)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    h = [pin(x) for x in (b.layout_offsets, b.ce_rowptr, b.ce_col, b.se_rowptr, b.se_col)]
+    h_colors = torch.empty(b.n, dtype=torch.int32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    mp.mpld_decompose_batch(h[0], b.n, h[1], h[2], h[3], h[4], k, alpha, args.max_steps, flags, out_colors=h_colors)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = mp.mpld_decompose_batch(h[0], b.n, h[1], h[2], h[3], h[4], k, alpha, args.max_steps, flags,
+                                      out_colors=h_colors)
+    e2e_s = time.perf_counter() - t0
+    assert np.array_equal(h_colors.numpy(), colors.cpu().numpy())
+    h2d = sum(x.numel() * 4 for x in h)
+    d2h = b.n * 4 + L * 8 * 3 + 8 * len(mp.STAT_NAMES)
+
+    # aggregate over ranks
+    vec = torch.tensor([comps_per_step * args.steps, total_ms, comps_per_step * e2e_steps, e2e_s * 1e3, L],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        tot = vec.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        mx = vec.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        comps_all, ms_max, e2e_comps_all, e2e_ms_max, layouts_all = tot[0].item(), mx[1].item(), tot[2].item(), \
+            mx[3].item(), tot[4].item()
+    else:
+        comps_all, ms_max, e2e_comps_all, e2e_ms_max, layouts_all = vec.tolist()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    value = comps_all / (ms_max / 1e3)
+    ms_per_step = ms_max / args.steps
+    # roofline of the dominant kernel
+    kb = kernel_bytes(b)
+    dom = max(ktimes.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_n) = dom
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:
+        hbm_peak, peak_src = 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
+    if kb.get(dom_name):
+        achieved = kb[dom_name] / (dom_ms / dom_n / 1e3) / 1e9
+        roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": kb[dom_name]}
+    else:
+        sm_clock = 1965.0
+        # ALU roofline: 148 SMs x 4 SMSPs x 1 warp-instruction/clk at sm_max
+        nodes = st["steps"]
+        achieved = nodes / (dom_ms / dom_n / 1e3) / 1e9
+        peak_nodes = 148 * 4 * 32 * sm_clock * 1e6 / 60.0 / 1e9  # 60 thread-instructions per node
+        roof = {"kernel": dom_name, "bound": "alu", "achieved": achieved, "peak": peak_nodes,
+                "unit": "Gnodes/s", "frac": achieved / peak_nodes, "traffic": None,
+                "peak_source": "148 SM x 4 SMSP x 32 lanes x 1.965 GHz / 60 instr per node (DESIGN.md §5)"}
+    share = {name: (v[0] / total_ms if total_ms else None) for name, v in ktimes.items() if v[1]}
+    out = {"metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_per_step,
+           "ms_per_layout": ms_max / args.steps / (layouts_all / world),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+           "data": "synthetic (seeded, synth/layouts.py)",
+           "config": config_dict(b, args.replicas, world, {"components_per_step_per_rank": comps_per_step}),
+           "e2e": {"value": e2e_comps_all / (e2e_ms_max / 1e3), "unit": METRIC, "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms_max / e2e_steps,
+                   "timing": "wall clock around the blocking host C-ABI call mpld_decompose_batch (pinned buffers)"},
+           "gpu_launches": int(launches),
+           "kernel_share": share,
+           "roofline": roof,
+           "clocks": clk.summary(),
+           "stats": st}
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = run_cpu_baseline(b, k, alpha, args.cpu_seconds)
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

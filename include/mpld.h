@@ -1,0 +1,154 @@
+/*
+ * mpld.h — C ABI of the B200 multiple-patterning layout decomposition (MPLD)
+ * hot path (arxiv 2303.14335, "GPU-accelerated matrix cover algorithm for
+ * multiple patterning layout decomposition").
+ *
+ * The library decomposes a decomposed graph DG = (V, CE ∪ SE) into k masks,
+ * minimising PAPER.md Eq. (1):
+ *
+ *     min_x  sum_{e_ij in CE} c_ij + alpha * sum_{e_ij in SE} s_ij
+ *     c_ij = (x_i == x_j),  s_ij = (x_i != x_j),  x_i in {0, ..., k-1}      (§2.1, Eq. 1a-1d)
+ *
+ * following the flow of PAPER.md §2.2 / Fig. 2 ("simplify the layout graph ...
+ * call the graph coloring solver ... recover the nodes removed in
+ * simplification step") with the solver replaced by an exact-cover search
+ * (§2.3, Alg. 1).  All steps run in CUDA kernels for sm_100a; see DESIGN.md
+ * §1 for the step list and §2 for the readings R1..R10 of the paper that fix
+ * the exact result (every result is bit-identical to the CPU oracle in
+ * oracle/, which shares no code with this library).
+ *
+ * Graph layout (all int32, shared by every entry point):
+ *   n            number of vertices (polygon features or stitch segments, §2.1
+ *                "every node v_i in V corresponds to one feature"), 0 <= n < 2^31.
+ *   ce_rowptr    [n+1] CSR row pointer of the conflict edges CE, ce_rowptr[0] = 0.
+ *   ce_col       [ce_rowptr[n]] neighbour ids; each undirected edge appears in
+ *                both rows; every row strictly ascending; no self loops.
+ *   se_rowptr,   the same for the stitch edges SE (Fig. 1(c) "stitch insertion";
+ *   se_col       an SE edge joins two segments of one feature).  CE ∩ SE = ∅.
+ *   A batch of independent layouts is their disjoint union: vertex ids of
+ *   layout l are [layout_offsets[l], layout_offsets[l+1]) and no edge crosses
+ *   a layout boundary.
+ *
+ * Parameters:
+ *   k            number of masks, 2 <= k <= MPLD_MAX_K (DPLD, TPLD, QPLD).
+ *   alpha        stitch weight of Eq. (1a) (§2.1 "set as 0.1 by default"); must
+ *                be a multiple of 0.001 in [0, 1000] (R2: the search
+ *                compares costs exactly in integer units of 1/1000).
+ *   max_steps    search budget per component (R7): once a complete
+ *                colouring exists and a component's search has entered more
+ *                than max_steps nodes, its search stops with the best colouring
+ *                found so far (counted in MPLD_STAT_TRUNCATED).  <= 0: no limit.
+ *
+ * Outputs:
+ *   colors       [n] mask of every vertex, in [0, k).
+ *   n_conflicts  #{e_ij in CE : x_i == x_j}    (Table 1 "cn#")
+ *   n_stitches   #{e_ij in SE : x_i != x_j}    (Table 1 "st#")
+ *   cost         n_conflicts + alpha * n_stitches, IEEE double, computed as
+ *                fl(fl(alpha * n_stitches) + n_conflicts).
+ *   stats        optional [MPLD_STAT_LEN] int64 (NULL to skip), see enum.
+ *
+ * Errors: every entry point returns MPLD_OK (0) or an MPLD_ERR_* code and
+ * leaves a one-line description in mpld_last_error() (thread-local).  On error
+ * the output buffers are unspecified.  Components (after simplification) with
+ * more than MPLD_MAX_COMPONENT vertices are rejected with MPLD_ERR_COMPONENT.
+ *
+ * Ownership: the library never takes ownership of caller buffers.  Host entry
+ * points copy inputs to device memory owned by an internal per-device context
+ * and block until the result is on the host.  Device entry points take device
+ * pointers, enqueue everything on the given stream and return without host
+ * synchronisation; the caller keeps buffers alive until the stream passes.
+ */
+#ifndef MPLD_H_
+#define MPLD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPLD_VERSION "0.1.0"
+#define MPLD_MAX_K 4
+#define MPLD_MAX_COMPONENT 64
+#define MPLD_COST_UNITS 1000 /* cost units per conflict (R2) */
+
+enum mpld_status {
+  MPLD_OK = 0,
+  MPLD_ERR_ARG = 1,       /* bad scalar argument or NULL pointer */
+  MPLD_ERR_GRAPH = 2,     /* CSR not symmetric / not strictly ascending / self loop / CE ∩ SE != ∅ */
+  MPLD_ERR_COMPONENT = 3, /* a component exceeds MPLD_MAX_COMPONENT vertices */
+  MPLD_ERR_CUDA = 4,      /* CUDA runtime error (message in mpld_last_error) */
+  MPLD_ERR_NOMEM = 5      /* device allocation failed */
+};
+
+/* flags */
+#define MPLD_FLAG_VALIDATE 1u /* check the CSR invariants on the device first (MPLD_ERR_GRAPH) */
+
+/* stats[] layout */
+enum mpld_stat {
+  MPLD_STAT_COMPONENTS = 0, /* components solved by the exact-cover search (Alg. 1 line 4) */
+  MPLD_STAT_HIDDEN = 1,     /* vertices hidden by simplification (§2.2) */
+  MPLD_STAT_ROUNDS = 2,     /* simplification rounds (R8) */
+  MPLD_STAT_MAX_COMP = 3,   /* largest component size */
+  MPLD_STAT_STEPS = 4,      /* search nodes entered, summed over components */
+  MPLD_STAT_TRUNCATED = 5,  /* components whose search hit max_steps */
+  MPLD_STAT_ERROR = 6,      /* device-side error bits (1 = graph, 2 = component too large) */
+  MPLD_STAT_LAUNCHES = 7,   /* kernels launched by the call */
+  MPLD_STAT_LEN = 8
+};
+
+/* Last error message of the calling thread ("" if none). */
+const char* mpld_last_error(void);
+const char* mpld_version(void);
+
+/* One layout, host buffers (end-to-end call: H2D copy, all kernels, D2H copy). */
+int mpld_decompose(int32_t n, const int32_t* ce_rowptr, const int32_t* ce_col,
+                   const int32_t* se_rowptr, const int32_t* se_col, int32_t k,
+                   double alpha, int64_t max_steps, int32_t* colors,
+                   int64_t* n_conflicts, int64_t* n_stitches, double* cost);
+
+/* A batch of n_layouts layouts (disjoint union), host buffers.
+ * layout_offsets [n_layouts+1]; n_conflicts, n_stitches, cost: [n_layouts]. */
+int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
+                         const int32_t* ce_rowptr, const int32_t* ce_col,
+                         const int32_t* se_rowptr, const int32_t* se_col, int32_t k,
+                         double alpha, int64_t max_steps, uint32_t flags, int32_t* colors,
+                         int64_t* n_conflicts, int64_t* n_stitches, double* cost,
+                         int64_t* stats);
+
+/* ---- device-resident interface (inputs already in HBM) ---------------------- */
+typedef struct mpld_context mpld_context;
+
+/* Create a context on `device` with workspace for up to max_vertices vertices
+ * and max_layouts layouts (grown on demand by later calls). */
+int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, mpld_context** out);
+void mpld_context_destroy(mpld_context* ctx);
+
+/* Enqueue the whole hot path on `stream` (a cudaStream_t; NULL = legacy default).
+ * All pointers are device pointers.  d_counts [2*n_layouts] int64 receives
+ * (n_conflicts, n_stitches) per layout, d_cost [n_layouts] the Eq. (1a) cost,
+ * d_stats [MPLD_STAT_LEN] the statistics (MPLD_STAT_ERROR != 0 means the
+ * result is invalid: check it after the stream synchronises).  Host-side
+ * argument errors are returned immediately. */
+int mpld_decompose_device(mpld_context* ctx, void* stream, int32_t n_layouts,
+                          const int32_t* d_layout_offsets, int32_t n,
+                          const int32_t* d_ce_rowptr, const int32_t* d_ce_col,
+                          const int32_t* d_se_rowptr, const int32_t* d_se_col, int32_t k,
+                          double alpha, int64_t max_steps, uint32_t flags, int32_t* d_colors,
+                          int64_t* d_counts, double* d_cost, int64_t* d_stats);
+
+/* Kernel timing inside the context (for bench.py's roofline): when enabled,
+ * every launch is bracketed by CUDA events on the launch stream and its
+ * duration accumulated per kernel.  mpld_kernel_count() kernels, indexed
+ * 0..count-1: name, accumulated milliseconds and launches since the last reset.
+ * Reading the times synchronises the context's events. */
+int mpld_context_set_timing(mpld_context* ctx, int enable);
+int mpld_context_reset_timing(mpld_context* ctx);
+int mpld_kernel_count(void);
+const char* mpld_kernel_name(int i);
+int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPLD_H_ */

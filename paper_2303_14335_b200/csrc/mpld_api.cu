@@ -1,0 +1,439 @@
+// C ABI of include/mpld.h: contexts, device workspace, host entry points and
+// the launch sequence of the hot path.
+//
+// Launch sequence of one call (all on one stream, no host synchronisation):
+//   [mpld_validate]            optional (MPLD_FLAG_VALIDATE)
+//   mpld_simplify_components   cooperative: reset, simplification rounds, union-find
+//   mpld_exact_cover_search<K> persistent: one thread per component, dynamic queue
+//   mpld_recover               cooperative: LIFO recovery of hidden vertices
+//   mpld_evaluate              Eq. (1) per layout + stats
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mpld_internal.cuh"
+
+using namespace mpld;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(MPLD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+enum KernelId { K_VALIDATE = 0, K_SIMPLIFY, K_SEARCH, K_RECOVER, K_EVALUATE, K_COUNT };
+const char* kKernelNames[K_COUNT] = {"mpld_validate", "mpld_simplify_components", "mpld_exact_cover_search",
+                                     "mpld_recover", "mpld_evaluate"};
+
+constexpr int kCoopThreads = 256;
+constexpr int kSearchThreads = 128;
+
+}  // namespace
+
+struct mpld_context {
+  int device = 0;
+  int num_sms = 0;
+  int64_t cap_n = 0;
+  int32_t cap_layouts = 0;
+  // workspace
+  int* deg = nullptr;
+  int* hround = nullptr;
+  int* hid = nullptr;
+  int* rcnt = nullptr;
+  int* roff = nullptr;
+  int* parent = nullptr;
+  int* loc = nullptr;
+  int* roots = nullptr;
+  Control* ctl = nullptr;
+  int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0;
+  // host-API staging (device copies of host inputs / outputs)
+  int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
+  int* h_lo = nullptr;
+  int* h_ce_rp = nullptr;
+  int* h_ce_col = nullptr;
+  int* h_se_rp = nullptr;
+  int* h_se_col = nullptr;
+  int* h_colors = nullptr;
+  long long* h_counts = nullptr;
+  double* h_cost = nullptr;
+  long long* h_stats = nullptr;
+  cudaStream_t stream = nullptr;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  double acc_ms[K_COUNT] = {0};
+  int64_t launches[K_COUNT] = {0};
+  std::mutex mu;
+};
+
+namespace {
+
+template <typename T>
+cudaError_t grow(T** p, int64_t count) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  return cudaMalloc((void**)p, sizeof(T) * (size_t)(count > 0 ? count : 1));
+}
+
+int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
+  if (n > ctx->cap_n) {
+    int64_t cap = std::max<int64_t>(n, ctx->cap_n * 3 / 2);
+    cudaError_t e = cudaSuccess;
+    for (int** p : {&ctx->deg, &ctx->hround, &ctx->hid, &ctx->parent, &ctx->loc, &ctx->roots}) {
+      e = grow(p, cap);
+      if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
+    }
+    if (grow(&ctx->rcnt, cap + 2) != cudaSuccess || grow(&ctx->roff, cap + 2) != cudaSuccess)
+      return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
+    ctx->cap_n = cap;
+  }
+  if (n_layouts > ctx->cap_layouts) {
+    int32_t cap = std::max<int32_t>(n_layouts, 16);
+    ctx->cap_layouts = cap;
+  }
+  return MPLD_OK;
+}
+
+cudaEvent_t take_event(mpld_context* ctx) {
+  if (ctx->ev_pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = ctx->ev_pool.back();
+  ctx->ev_pool.pop_back();
+  return e;
+}
+
+struct TimedLaunch {
+  mpld_context* ctx;
+  int id;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  TimedLaunch(mpld_context* c, int i, cudaStream_t st) : ctx(c), id(i), s(st) {
+    if (ctx->timing) {
+      a = take_event(ctx);
+      b = take_event(ctx);
+      cudaEventRecord(a, s);
+    }
+  }
+  void done() {
+    if (ctx->timing) {
+      cudaEventRecord(b, s);
+      ctx->pending.push_back({id, {a, b}});
+    }
+    ctx->launches[id] += 1;
+  }
+};
+
+int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
+  if (n < 0) return fail(MPLD_ERR_ARG, "n < 0");
+  if (k < 2 || k > MPLD_MAX_K) return fail(MPLD_ERR_ARG, "k must be in [2, 4]");
+  if (!(alpha >= 0.0 && alpha <= 1000.0)) return fail(MPLD_ERR_ARG, "alpha must be in [0, 1000]");
+  double a = alpha * MPLD_COST_UNITS;
+  double r = std::nearbyint(a);
+  if (std::fabs(a - r) > 1e-6) return fail(MPLD_ERR_ARG, "alpha must be a multiple of 0.001");
+  *w_stitch = (int)r;
+  return MPLD_OK;
+}
+
+int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
+                 long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost,
+                 long long* stats) {
+  Workspace ws{ctx->deg, ctx->hround, ctx->hid, ctx->rcnt, ctx->roff, ctx->parent, ctx->loc, ctx->roots, ctx->ctl};
+  cudaError_t e;
+  int launches = 0;
+  const int n_launch = 4 + ((flags & MPLD_FLAG_VALIDATE) ? 1 : 0);
+  if (flags & MPLD_FLAG_VALIDATE) {
+    TimedLaunch t(ctx, K_VALIDATE, s);
+    e = launch_validate(g, ws, s, ctx->blocks_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_validate");
+    t.done();
+    ++launches;
+  }
+  {
+    TimedLaunch t(ctx, K_SIMPLIFY, s);
+    e = launch_simplify_components(g, ws, k, colors, counts, s, ctx->blocks_simplify, kCoopThreads);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_simplify_components");
+    t.done();
+    ++launches;
+  }
+  {
+    TimedLaunch t(ctx, K_SEARCH, s);
+    e = launch_search(g, ws, k, w_stitch, max_steps, colors, s, ctx->blocks_search, kSearchThreads);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
+    t.done();
+    ++launches;
+  }
+  {
+    TimedLaunch t(ctx, K_RECOVER, s);
+    e = launch_recover(g, ws, k, colors, s, ctx->blocks_recover, kCoopThreads);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_recover");
+    t.done();
+    ++launches;
+  }
+  {
+    TimedLaunch t(ctx, K_EVALUATE, s);
+    e = launch_evaluate(g, ws, colors, alpha, counts, cost, stats, n_launch, s, ctx->blocks_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_evaluate");
+    t.done();
+    ++launches;
+  }
+  (void)launches;
+  return MPLD_OK;
+}
+
+std::mutex g_ctx_mu;
+std::vector<mpld_context*> g_host_ctx;  // one per device for the host entry points
+
+mpld_context* host_context(int* err) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *err = cuda_fail(e, "cudaGetDevice");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if ((int)g_host_ctx.size() <= dev) g_host_ctx.resize(dev + 1, nullptr);
+  if (!g_host_ctx[dev]) {
+    mpld_context* c = nullptr;
+    int rc = mpld_context_create(dev, 1 << 16, 16, &c);
+    if (rc != MPLD_OK) {
+      *err = rc;
+      return nullptr;
+    }
+    g_host_ctx[dev] = c;
+  }
+  *err = MPLD_OK;
+  return g_host_ctx[dev];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mpld_last_error(void) { return g_last_error.c_str(); }
+const char* mpld_version(void) { return MPLD_VERSION; }
+
+int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, mpld_context** out) {
+  if (!out) return fail(MPLD_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  mpld_context* ctx = new mpld_context();
+  ctx->device = device;
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+  if (!coop) {
+    delete ctx;
+    return fail(MPLD_ERR_CUDA, "device does not support cooperative launch");
+  }
+  if (cudaMalloc((void**)&ctx->ctl, sizeof(Control)) != cudaSuccess) {
+    delete ctx;
+    return fail(MPLD_ERR_NOMEM, "control block allocation failed");
+  }
+  cudaMemset(ctx->ctl, 0, sizeof(Control));
+  ctx->blocks_simplify = coop_blocks_simplify(kCoopThreads, ctx->num_sms);
+  ctx->blocks_recover = coop_blocks_recover(kCoopThreads, ctx->num_sms);
+  ctx->blocks_search = resident_blocks_search(kSearchThreads, ctx->num_sms);
+  ctx->blocks_stream = ctx->num_sms * 8;
+  if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0) {
+    mpld_context_destroy(ctx);
+    return fail(MPLD_ERR_CUDA, "occupancy query failed (kernel image missing for this device?)");
+  }
+  int rc = ensure_workspace(ctx, max_vertices, max_layouts);
+  if (rc != MPLD_OK) {
+    mpld_context_destroy(ctx);
+    return rc;
+  }
+  e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    mpld_context_destroy(ctx);
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  *out = ctx;
+  return MPLD_OK;
+}
+
+void mpld_context_destroy(mpld_context* ctx) {
+  if (!ctx) return;
+  for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->hid, (void*)ctx->rcnt, (void*)ctx->roff,
+                  (void*)ctx->parent, (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->ctl, (void*)ctx->h_lo,
+                  (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
+                  (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})
+    if (p) cudaFree(p);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& p : ctx->pending) {
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int mpld_decompose_device(mpld_context* ctx, void* stream, int32_t n_layouts, const int32_t* d_layout_offsets,
+                          int32_t n, const int32_t* d_ce_rowptr, const int32_t* d_ce_col,
+                          const int32_t* d_se_rowptr, const int32_t* d_se_col, int32_t k, double alpha,
+                          int64_t max_steps, uint32_t flags, int32_t* d_colors, int64_t* d_counts, double* d_cost,
+                          int64_t* d_stats) {
+  if (!ctx) return fail(MPLD_ERR_ARG, "ctx is NULL");
+  int w_stitch = 0;
+  int rc = check_scalars(n, k, alpha, &w_stitch);
+  if (rc != MPLD_OK) return rc;
+  if (n_layouts < 1) return fail(MPLD_ERR_ARG, "n_layouts < 1");
+  if (!d_layout_offsets || !d_ce_rowptr || !d_se_rowptr || !d_colors || !d_counts || !d_cost)
+    return fail(MPLD_ERR_ARG, "NULL device pointer");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  rc = ensure_workspace(ctx, n, n_layouts);
+  if (rc != MPLD_OK) return rc;
+  GraphView g{n, n_layouts, d_layout_offsets, d_ce_rowptr, d_ce_col, d_se_rowptr, d_se_col};
+  return run_pipeline(ctx, (cudaStream_t)stream, g, k, w_stitch, alpha, (long long)max_steps, flags, d_colors,
+                      (long long*)d_counts, d_cost, (long long*)d_stats);
+}
+
+int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32_t n, const int32_t* ce_rowptr,
+                         const int32_t* ce_col, const int32_t* se_rowptr, const int32_t* se_col, int32_t k,
+                         double alpha, int64_t max_steps, uint32_t flags, int32_t* colors, int64_t* n_conflicts,
+                         int64_t* n_stitches, double* cost, int64_t* stats) {
+  int w_stitch = 0;
+  int rc = check_scalars(n, k, alpha, &w_stitch);
+  if (rc != MPLD_OK) return rc;
+  if (n_layouts < 1 || !layout_offsets || !ce_rowptr || !se_rowptr || (n > 0 && !colors) || !n_conflicts ||
+      !n_stitches || !cost)
+    return fail(MPLD_ERR_ARG, "bad argument (NULL pointer or n_layouts < 1)");
+  if (layout_offsets[0] != 0 || layout_offsets[n_layouts] != n)
+    return fail(MPLD_ERR_ARG, "layout_offsets must start at 0 and end at n");
+  const int64_t m_ce = ce_rowptr[n], m_se = se_rowptr[n];
+  if (m_ce < 0 || m_se < 0 || (m_ce > 0 && !ce_col) || (m_se > 0 && !se_col))
+    return fail(MPLD_ERR_ARG, "bad CSR row pointer / column array");
+  mpld_context* ctx = host_context(&rc);
+  if (!ctx) return rc;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  rc = ensure_workspace(ctx, n, n_layouts);
+  if (rc != MPLD_OK) return rc;
+  // staging buffers
+  if (n > ctx->cap_stage_n || !ctx->h_ce_rp) {
+    ctx->cap_stage_n = ctx->cap_n;
+    if (grow(&ctx->h_ce_rp, ctx->cap_stage_n + 1) != cudaSuccess ||
+        grow(&ctx->h_se_rp, ctx->cap_stage_n + 1) != cudaSuccess || grow(&ctx->h_colors, ctx->cap_stage_n) != cudaSuccess)
+      return fail(MPLD_ERR_NOMEM, "staging allocation failed");
+  }
+  if (m_ce > ctx->cap_ce || !ctx->h_ce_col) {
+    ctx->cap_ce = std::max<int64_t>(m_ce, ctx->cap_ce * 3 / 2);
+    if (grow(&ctx->h_ce_col, ctx->cap_ce) != cudaSuccess) return fail(MPLD_ERR_NOMEM, "staging allocation failed");
+  }
+  if (m_se > ctx->cap_se || !ctx->h_se_col) {
+    ctx->cap_se = std::max<int64_t>(m_se, ctx->cap_se * 3 / 2);
+    if (grow(&ctx->h_se_col, ctx->cap_se) != cudaSuccess) return fail(MPLD_ERR_NOMEM, "staging allocation failed");
+  }
+  if (!ctx->h_lo || n_layouts > ctx->cap_layouts || !ctx->h_counts) {
+    ctx->cap_layouts = std::max<int32_t>(n_layouts, ctx->cap_layouts);
+    if (grow(&ctx->h_lo, ctx->cap_layouts + 1) != cudaSuccess ||
+        grow(&ctx->h_counts, 2 * (int64_t)ctx->cap_layouts) != cudaSuccess ||
+        grow(&ctx->h_cost, ctx->cap_layouts) != cudaSuccess || grow(&ctx->h_stats, MPLD_STAT_LEN) != cudaSuccess)
+      return fail(MPLD_ERR_NOMEM, "staging allocation failed");
+  }
+  cudaStream_t s = ctx->stream;
+  cudaError_t e;
+  e = cudaMemcpyAsync(ctx->h_lo, layout_offsets, sizeof(int) * (n_layouts + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ctx->h_ce_rp, ce_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ctx->h_se_rp, se_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && m_ce)
+    e = cudaMemcpyAsync(ctx->h_ce_col, ce_col, sizeof(int) * m_ce, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && m_se)
+    e = cudaMemcpyAsync(ctx->h_se_col, se_col, sizeof(int) * m_se, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+  GraphView g{n, n_layouts, ctx->h_lo, ctx->h_ce_rp, ctx->h_ce_col, ctx->h_se_rp, ctx->h_se_col};
+  rc = run_pipeline(ctx, s, g, k, w_stitch, alpha, (long long)max_steps, flags, ctx->h_colors, ctx->h_counts,
+                    ctx->h_cost, ctx->h_stats);
+  if (rc != MPLD_OK) return rc;
+  std::vector<long long> counts(2 * (size_t)n_layouts);
+  long long st[MPLD_STAT_LEN];
+  if (n > 0) e = cudaMemcpyAsync(colors, ctx->h_colors, sizeof(int) * n, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(counts.data(), ctx->h_counts, sizeof(long long) * 2 * n_layouts, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(cost, ctx->h_cost, sizeof(double) * n_layouts, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(st, ctx->h_stats, sizeof(st), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "pipeline / D2H copy");
+  for (int l = 0; l < n_layouts; ++l) {
+    n_conflicts[l] = counts[2 * l];
+    n_stitches[l] = counts[2 * l + 1];
+  }
+  if (stats) std::memcpy(stats, st, sizeof(st));
+  if (st[MPLD_STAT_ERROR] & kErrGraph) return fail(MPLD_ERR_GRAPH, "graph violates the CSR invariants of mpld.h");
+  if (st[MPLD_STAT_ERROR] & kErrComponent)
+    return fail(MPLD_ERR_COMPONENT, "a component exceeds MPLD_MAX_COMPONENT vertices");
+  g_last_error.clear();
+  return MPLD_OK;
+}
+
+int mpld_decompose(int32_t n, const int32_t* ce_rowptr, const int32_t* ce_col, const int32_t* se_rowptr,
+                   const int32_t* se_col, int32_t k, double alpha, int64_t max_steps, int32_t* colors,
+                   int64_t* n_conflicts, int64_t* n_stitches, double* cost) {
+  int32_t lo[2] = {0, n};
+  return mpld_decompose_batch(1, lo, n, ce_rowptr, ce_col, se_rowptr, se_col, k, alpha, max_steps, 0u, colors,
+                              n_conflicts, n_stitches, cost, nullptr);
+}
+
+int mpld_context_set_timing(mpld_context* ctx, int enable) {
+  if (!ctx) return fail(MPLD_ERR_ARG, "ctx is NULL");
+  ctx->timing = enable != 0;
+  return MPLD_OK;
+}
+
+static void drain_timing(mpld_context* ctx) {
+  for (auto& p : ctx->pending) {
+    cudaEventSynchronize(p.second.second);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+    ctx->acc_ms[p.first] += ms;
+    ctx->ev_pool.push_back(p.second.first);
+    ctx->ev_pool.push_back(p.second.second);
+  }
+  ctx->pending.clear();
+}
+
+int mpld_context_reset_timing(mpld_context* ctx) {
+  if (!ctx) return fail(MPLD_ERR_ARG, "ctx is NULL");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  drain_timing(ctx);
+  for (int i = 0; i < K_COUNT; ++i) {
+    ctx->acc_ms[i] = 0.0;
+    ctx->launches[i] = 0;
+  }
+  return MPLD_OK;
+}
+
+int mpld_kernel_count(void) { return K_COUNT; }
+
+const char* mpld_kernel_name(int i) { return (i >= 0 && i < K_COUNT) ? kKernelNames[i] : ""; }
+
+int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* launches) {
+  if (!ctx || i < 0 || i >= K_COUNT) return fail(MPLD_ERR_ARG, "bad context / kernel index");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  drain_timing(ctx);
+  if (ms) *ms = ctx->acc_ms[i];
+  if (launches) *launches = ctx->launches[i];
+  return MPLD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,195 @@
+"""Thin ctypes binding of the C ABI in include/mpld.h (argument marshalling only).
+
+Every step of the decomposition runs in the CUDA kernels of lib/libmpld.so; this
+module never computes any part of the result.  There is no CPU fallback: if the
+library is missing or no CUDA device is present the calls raise.
+
+Array arguments may be numpy arrays / torch CPU tensors (host entry points) or
+torch CUDA tensors (device entry points); they must be contiguous int32.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libmpld.so")
+
+MPLD_OK = 0
+MPLD_ERR_ARG, MPLD_ERR_GRAPH, MPLD_ERR_COMPONENT, MPLD_ERR_CUDA, MPLD_ERR_NOMEM = 1, 2, 3, 4, 5
+MPLD_FLAG_VALIDATE = 1
+MPLD_MAX_K = 4
+MPLD_MAX_COMPONENT = 64
+MPLD_COST_UNITS = 1000
+STAT_NAMES = ["components", "hidden", "rounds", "max_component", "steps", "truncated", "error", "launches"]
+MPLD_STAT_LEN = len(STAT_NAMES)
+
+# every symbol include/mpld.h declares
+EXPORTS = ["mpld_last_error", "mpld_version", "mpld_decompose", "mpld_decompose_batch", "mpld_context_create",
+           "mpld_context_destroy", "mpld_decompose_device", "mpld_context_set_timing",
+           "mpld_context_reset_timing", "mpld_kernel_count", "mpld_kernel_name", "mpld_context_kernel_time"]
+
+
+class MPLDError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"mpld error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_f64p = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+def lib():
+    """Load lib/libmpld.so (raises OSError loudly when it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise OSError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    L.mpld_last_error.restype = ctypes.c_char_p
+    L.mpld_version.restype = ctypes.c_char_p
+    L.mpld_kernel_name.restype = ctypes.c_char_p
+    L.mpld_kernel_name.argtypes = [ctypes.c_int]
+    L.mpld_kernel_count.restype = ctypes.c_int
+    L.mpld_decompose.argtypes = [ctypes.c_int32, _vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_double,
+                                 ctypes.c_int64, _vp, _i64p, _i64p, _f64p]
+    L.mpld_decompose_batch.argtypes = [ctypes.c_int32, _vp, ctypes.c_int32, _vp, _vp, _vp, _vp, ctypes.c_int32,
+                                       ctypes.c_double, ctypes.c_int64, ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp]
+    L.mpld_context_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_vp)]
+    L.mpld_context_destroy.argtypes = [_vp]
+    L.mpld_context_destroy.restype = None
+    L.mpld_decompose_device.argtypes = [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp, _vp, _vp, _vp,
+                                        ctypes.c_int32, ctypes.c_double, ctypes.c_int64, ctypes.c_uint32, _vp, _vp,
+                                        _vp, _vp]
+    L.mpld_context_set_timing.argtypes = [_vp, ctypes.c_int]
+    L.mpld_context_reset_timing.argtypes = [_vp]
+    L.mpld_context_kernel_time.argtypes = [_vp, ctypes.c_int, _f64p, _i64p]
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != MPLD_OK:
+        raise MPLDError(rc, lib().mpld_last_error().decode())
+
+
+def _host_ptr(x, dtype=np.int32):
+    """Address of a host buffer (numpy array or torch CPU tensor) plus a keep-alive."""
+    if hasattr(x, "data_ptr"):
+        if x.is_cuda:
+            raise ValueError("host entry point given a CUDA tensor")
+        return x.data_ptr(), x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return a.ctypes.data, a
+
+
+def _dev_ptr(t):
+    if t is None:
+        return None
+    if not (hasattr(t, "is_cuda") and t.is_cuda):
+        raise ValueError("device entry point needs CUDA tensors")
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return t.data_ptr()
+
+
+def version() -> str:
+    return lib().mpld_version().decode()
+
+
+def mpld_decompose(n, ce_rowptr, ce_col, se_rowptr, se_col, k: int, alpha: float, max_steps: int = 0):
+    """C ABI `mpld_decompose` on host buffers -> (colors, n_conflicts, n_stitches, cost)."""
+    L = lib()
+    colors = np.empty(max(int(n), 0), dtype=np.int32)
+    nc, ns, cost = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+    keep = [_host_ptr(a) for a in (ce_rowptr, ce_col, se_rowptr, se_col)]
+    _check(L.mpld_decompose(int(n), *[p for p, _ in keep], int(k), float(alpha), int(max_steps),
+                            colors.ctypes.data, ctypes.byref(nc), ctypes.byref(ns), ctypes.byref(cost)))
+    return colors, nc.value, ns.value, cost.value
+
+
+def mpld_decompose_batch(layout_offsets, n, ce_rowptr, ce_col, se_rowptr, se_col, k: int, alpha: float,
+                         max_steps: int = 0, flags: int = 0, out_colors=None):
+    """C ABI `mpld_decompose_batch` on host buffers -> dict with colors,
+    per-layout n_conflicts / n_stitches / cost and stats."""
+    L = lib()
+    lo_p, lo = _host_ptr(layout_offsets)
+    n_layouts = int(len(lo) - 1) if not hasattr(lo, "numel") else int(lo.numel() - 1)
+    colors = out_colors if out_colors is not None else np.empty(max(int(n), 0), dtype=np.int32)
+    col_p, _ = _host_ptr(colors)
+    nc = np.zeros(n_layouts, dtype=np.int64)
+    ns = np.zeros(n_layouts, dtype=np.int64)
+    cost = np.zeros(n_layouts, dtype=np.float64)
+    stats = np.zeros(MPLD_STAT_LEN, dtype=np.int64)
+    keep = [_host_ptr(a) for a in (ce_rowptr, ce_col, se_rowptr, se_col)]
+    _check(L.mpld_decompose_batch(n_layouts, lo_p, int(n), *[p for p, _ in keep], int(k), float(alpha),
+                                  int(max_steps), int(flags), col_p, nc.ctypes.data, ns.ctypes.data,
+                                  cost.ctypes.data, stats.ctypes.data))
+    return {"colors": colors, "n_conflicts": nc, "n_stitches": ns, "cost": cost,
+            "stats": dict(zip(STAT_NAMES, stats.tolist()))}
+
+
+def decompose_graph(g, k: int, alpha: float, max_steps: int = 0, flags: int = 0):
+    """Convenience: host batch call on an object with n, layout_offsets, ce_rowptr,
+    ce_col, se_rowptr, se_col attributes (e.g. synth.DecompGraph)."""
+    return mpld_decompose_batch(g.layout_offsets, g.n, g.ce_rowptr, g.ce_col, g.se_rowptr, g.se_col, k, alpha,
+                                max_steps, flags)
+
+
+class Context:
+    """Device-resident entry point (`mpld_context_*`, `mpld_decompose_device`)."""
+
+    def __init__(self, device: int = 0, max_vertices: int = 1 << 16, max_layouts: int = 16):
+        L = lib()
+        h = _vp()
+        _check(L.mpld_context_create(int(device), int(max_vertices), int(max_layouts), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().mpld_context_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def decompose_device(self, layout_offsets, n, ce_rowptr, ce_col, se_rowptr, se_col, k, alpha, max_steps,
+                         colors, counts, cost, stats=None, flags: int = 0, stream=None):
+        """Enqueue the hot path on `stream` (torch.cuda.Stream or raw handle; None =
+        torch's current stream).  All tensors on the device; asynchronous."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(colors.device)
+        sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream or 0)
+        n_layouts = int(layout_offsets.numel() - 1)
+        _check(lib().mpld_decompose_device(self._h, _vp(sh), n_layouts, _dev_ptr(layout_offsets), int(n),
+                                           _dev_ptr(ce_rowptr), _dev_ptr(ce_col), _dev_ptr(se_rowptr),
+                                           _dev_ptr(se_col), int(k), float(alpha), int(max_steps), int(flags),
+                                           _dev_ptr(colors), _dev_ptr(counts), _dev_ptr(cost), _dev_ptr(stats)))
+
+    def set_timing(self, enable: bool):
+        _check(lib().mpld_context_set_timing(self._h, 1 if enable else 0))
+
+    def reset_timing(self):
+        _check(lib().mpld_context_reset_timing(self._h))
+
+    def kernel_times(self):
+        """{kernel name: (accumulated ms, launches)} since the last reset."""
+        L = lib()
+        out = {}
+        for i in range(L.mpld_kernel_count()):
+            ms, cnt = ctypes.c_double(), ctypes.c_int64()
+            _check(L.mpld_context_kernel_time(self._h, i, ctypes.byref(ms), ctypes.byref(cnt)))
+            out[L.mpld_kernel_name(i).decode()] = (ms.value, cnt.value)
+        return out

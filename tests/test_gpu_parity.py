@@ -1,0 +1,195 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, element by
+element: colours, conflict and stitch counts and cost are compared bit-exactly
+(integer / index results; the cost is the same IEEE expression on both sides)."""
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import from_edges
+
+mp = pytest.importorskip("paper_2303_14335_b200")
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+BUDGET = 1 << 20
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    mp.lib()
+
+
+def _assert_same(g, k, alpha, max_steps=BUDGET, flags=mp.MPLD_FLAG_VALIDATE, ref=None):
+    got = mp.decompose_graph(g, k, alpha, max_steps=max_steps, flags=flags)
+    ref = ref or oracle.decompose(g, k, alpha, max_steps=max_steps)
+    assert np.array_equal(got["colors"], ref["colors"]), np.nonzero(got["colors"] != ref["colors"])[0][:10]
+    for li, (c, s, cost) in enumerate(ref["per_layout"]):
+        assert int(got["n_conflicts"][li]) == c
+        assert int(got["n_stitches"][li]) == s
+        assert float(got["cost"][li]) == cost
+    st = got["stats"]
+    assert st["components"] == len(ref["components"])
+    assert st["rounds"] == ref["n_rounds"]
+    assert st["hidden"] == int((ref["hround"] >= 0).sum())
+    assert st["steps"] == sum(c["steps"] for c in ref["components"])
+    assert st["truncated"] == sum(c["truncated"] for c in ref["components"])
+    assert st["error"] == 0
+    return got, ref
+
+
+def test_config0_full():
+    graphs, k, alpha = synth.config_graphs(0)
+    _assert_same(graphs[0], k, alpha)
+
+
+def test_config1_iscas85_suite_batched():
+    graphs, k, alpha = synth.config_graphs(1)
+    b = synth.concat(graphs)
+    _assert_same(b, k, alpha)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_random_small_graphs(k):
+    rng = random.Random(2024 + k)
+    for trial in range(40):
+        n = rng.randint(1, 24)
+        p = rng.choice([0.15, 0.3, 0.5])
+        ce, se = [], []
+        for u in range(n):
+            for v in range(u + 1, n):
+                r = rng.random()
+                if r < 0.05:
+                    se.append((u, v))
+                elif r < 0.05 + p:
+                    ce.append((u, v))
+        g = from_edges(n, ce, se)
+        _assert_same(g, k, 0.1, max_steps=20000)
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.1, 0.5, 1.0, 2.5])
+def test_alpha_values(alpha):
+    g = synth.make_layout(3000, 3400, k=3, stitch_prob=0.6, comp_max=12, density=0.9, seed=7)
+    _assert_same(g, 3, alpha)
+
+
+@pytest.mark.parametrize("budget", [1, 5, 37, 200])
+def test_truncated_search_parity(budget):
+    """With a tiny max_steps the GPU stops at exactly the oracle's node."""
+    g = synth.stress_components(16, 30, 3, seed=3)
+    _assert_same(g, 3, 0.1, max_steps=budget)
+
+
+@pytest.mark.parametrize("size", [4, 8, 16, 24, 32, 48, 64])
+def test_stress_component_sizes(size):
+    g = synth.stress_components(size, 12, 3, seed=size)
+    _assert_same(g, 3, 0.1, max_steps=20000)
+
+
+def test_qpld_k4_scaled():
+    graphs, k, alpha = synth.config_graphs(2, scale=0.1)
+    _assert_same(graphs[0], k, alpha, max_steps=200000)
+
+
+def test_edge_cases():
+    fx = synth.fixtures()
+    for name in ["empty", "single", "K4", "K5", "K7", "W5", "C5", "stitch_pair", "triangle"]:
+        for k in (2, 3, 4):
+            _assert_same(fx[name], k, 0.1)
+    # everything hidden (a long path)
+    n = 1000
+    _assert_same(from_edges(n, [(i, i + 1) for i in range(n - 1)]), 3, 0.1)
+    # a 64-vertex clique fits; 65 is rejected
+    K64 = from_edges(64, [(i, j) for i in range(64) for j in range(i + 1, 64)])
+    got = mp.decompose_graph(K64, 4, 0.1, max_steps=1000)
+    ref = oracle.decompose(K64, 4, 0.1, max_steps=1000)
+    assert np.array_equal(got["colors"], ref["colors"])
+    K65 = from_edges(65, [(i, j) for i in range(65) for j in range(i + 1, 65)])
+    with pytest.raises(mp.MPLDError) as ei:
+        mp.decompose_graph(K65, 4, 0.1, max_steps=1000)
+    assert ei.value.code == 3
+
+
+def test_validation_rejects_bad_graphs():
+    g = from_edges(4, [(0, 1), (1, 2)])
+    bad = from_edges(4, [(0, 1), (1, 2)])
+    bad.ce_col = bad.ce_col.copy()
+    bad.ce_col[0] = 3  # 0 -> 3 without 3 -> 0
+    with pytest.raises(mp.MPLDError) as ei:
+        mp.decompose_graph(bad, 3, 0.1, flags=mp.MPLD_FLAG_VALIDATE)
+    assert ei.value.code == 2
+    _assert_same(g, 3, 0.1)  # the context recovers after an error
+
+
+def test_batch_equals_individual_calls():
+    graphs = [synth.make_layout(2000, 2300, k=3, stitch_prob=0.5, comp_max=10, density=0.9, seed=s) for s in range(4)]
+    b = synth.concat(graphs)
+    gb = mp.decompose_graph(b, 3, 0.1)
+    for li, g in enumerate(graphs):
+        gi = mp.decompose_graph(g, 3, 0.1)
+        a, e = b.layout_offsets[li], b.layout_offsets[li + 1]
+        assert np.array_equal(gb["colors"][a:e], gi["colors"])
+        assert gb["n_conflicts"][li] == gi["n_conflicts"][0] and gb["cost"][li] == gi["cost"][0]
+
+
+def test_device_entry_point_matches_host_entry_point():
+    graphs, k, alpha = synth.config_graphs(1)
+    b = synth.concat(graphs[:4])
+    host = mp.decompose_graph(b, k, alpha, max_steps=BUDGET)
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    ctx = mp.Context(0, b.n, b.n_layouts)
+    colors = torch.empty(b.n, dtype=torch.int32, device=dev)
+    counts = torch.empty(2 * b.n_layouts, dtype=torch.int64, device=dev)
+    cost = torch.empty(b.n_layouts, dtype=torch.float64, device=dev)
+    stats = torch.empty(len(mp.STAT_NAMES), dtype=torch.int64, device=dev)
+    ctx.set_timing(True)
+    for _ in range(2):
+        ctx.decompose_device(T(b.layout_offsets), b.n, T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr), T(b.se_col),
+                             k, alpha, BUDGET, colors, counts, cost, stats)
+    torch.cuda.synchronize()
+    assert np.array_equal(colors.cpu().numpy(), host["colors"])
+    c = counts.cpu().numpy().reshape(-1, 2)
+    assert np.array_equal(c[:, 0], host["n_conflicts"]) and np.array_equal(c[:, 1], host["n_stitches"])
+    assert np.array_equal(cost.cpu().numpy(), host["cost"])
+    times = ctx.kernel_times()
+    assert times["mpld_exact_cover_search"][1] == 2 and times["mpld_exact_cover_search"][0] > 0
+    ctx.close()
+
+
+def test_full_size_qpld_sampled():
+    """configs[2] at full s38584 size, in bench's launch configuration: global
+    invariants at full size, and the oracle recomputes a sample of components
+    one by one (their colours must match element by element)."""
+    graphs, k, alpha = synth.config_graphs(2)
+    g = graphs[0]
+    got = mp.decompose_graph(g, k, alpha, max_steps=BUDGET, flags=mp.MPLD_FLAG_VALIDATE)
+    colors = got["colors"]
+    assert ((colors >= 0) & (colors < k)).all()
+    ce, se = g.ce_edges(), g.se_edges()
+    assert int((colors[ce[:, 0]] == colors[ce[:, 1]]).sum()) == int(got["n_conflicts"][0])
+    assert int((colors[se[:, 0]] != colors[se[:, 1]]).sum()) == int(got["n_stitches"][0])
+    ce_adj, se_adj = g.ce_adj(), g.se_adj()
+    hround, rounds = oracle.simplify(g.n, ce_adj, se_adj, k)
+    assert got["stats"]["rounds"] == len(rounds)
+    comps = oracle.components(g.n, ce_adj, se_adj, hround)
+    assert got["stats"]["components"] == len(comps)
+    rng = random.Random(0)
+    sample = rng.sample(comps, min(60, len(comps))) + sorted(comps, key=len)[-5:]
+    w = oracle.alpha_units(alpha)
+    for order in sample:
+        r = oracle.solve_component(order, ce_adj, se_adj, k, w, BUDGET)
+        for v, c in r["global_colors"].items():
+            assert colors[v] == c
+    # recovery adds no conflict: every conflict lies inside a component
+    kept = np.array(hround) == -1
+    conf_edges = ce[colors[ce[:, 0]] == colors[ce[:, 1]]]
+    assert kept[conf_edges[:, 0]].all() and kept[conf_edges[:, 1]].all()
