@@ -94,7 +94,8 @@ enum mpld_stat {
   MPLD_STAT_TRUNCATED = 5,  /* components whose search hit max_steps */
   MPLD_STAT_ERROR = 6,      /* device-side error bits (1 = graph, 2 = component too large) */
   MPLD_STAT_LAUNCHES = 7,   /* kernels launched by the call */
-  MPLD_STAT_LEN = 8
+  MPLD_STAT_MAX_STEPS = 8,  /* largest per-component step count */
+  MPLD_STAT_LEN = 9
 };
 
 /* Last error message of the calling thread ("" if none). */
@@ -147,6 +148,12 @@ int mpld_context_reset_timing(mpld_context* ctx);
 int mpld_kernel_count(void);
 const char* mpld_kernel_name(int i);
 int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* launches);
+
+/* Diagnostics of the last call (synchronous copy): out[0..15] device
+ * %globaltimer stamps (ns) at phase boundaries, out[16] recovery levels
+ * (depth of the pop-order DAG + 1), out[17] hidden vertices, out[18] rounds,
+ * out[19] largest per-component step count.  Copies min(n, 20) values. */
+int mpld_context_debug(mpld_context* ctx, int64_t* out, int n);
 
 #ifdef __cplusplus
 }

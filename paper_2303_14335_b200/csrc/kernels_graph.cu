@@ -6,16 +6,15 @@
 //
 // The two persistent kernels are launched cooperatively (one wave of resident
 // CTAs, grid-wide barriers between rounds) so that the whole path is enqueued
-// without a host synchronisation.
-#include <cooperative_groups.h>
-
+// without a host synchronisation.  Queue appends reserve space with one atomic
+// per CTA (a single hot counter serialises at the L2).
 #include "mpld_internal.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace mpld {
 
 namespace {
+
+constexpr int kAppend = 8;  // items one thread may append per call before spilling to direct atomics
 
 __device__ __forceinline__ bool row_contains(const int* __restrict__ col, int a, int b, int x) {
   // binary search in the strictly ascending row col[a..b)
@@ -28,24 +27,60 @@ __device__ __forceinline__ bool row_contains(const int* __restrict__ col, int a,
   return false;
 }
 
-__device__ __forceinline__ int layout_base(const GraphView& g, int v) {
-  if (g.n_layouts <= 1) return 0;
-  int lo = 0, hi = g.n_layouts;  // find l with off[l] <= v < off[l+1]
-  while (hi - lo > 1) {
-    int m = (lo + hi) >> 1;
-    if (__ldg(&g.layout_off[m]) <= v) lo = m; else hi = m;
-  }
-  return __ldg(&g.layout_off[lo]);
-}
-
 __device__ __forceinline__ int layout_index(const GraphView& g, int v) {
   if (g.n_layouts <= 1) return 0;
-  int lo = 0, hi = g.n_layouts;
+  int lo = 0, hi = g.n_layouts;  // off[lo] <= v < off[lo+1]
   while (hi - lo > 1) {
     int m = (lo + hi) >> 1;
     if (__ldg(&g.layout_off[m]) <= v) lo = m; else hi = m;
   }
   return lo;
+}
+
+__device__ __forceinline__ void stamp(Control* ctl, int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ctl->t[i] = t;
+  }
+}
+
+// Block-wide append: thread i contributes cnt_i items; the CTA reserves its
+// range with one atomicAdd.  Every thread of the CTA must call it (uniform
+// control flow); blockDim.x must be a multiple of 32.
+__device__ __forceinline__ void cta_append(int cnt, const int* items, int* counter, int* out) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    const int t = lane < nw ? s_warp[lane] : 0;
+    int y = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
+    }
+    if (lane < nw) s_warp[lane] = y - t;  // exclusive prefix of the warp totals
+    if (lane == 31) s_base = y ? atomicAdd(counter, y) : 0;
+  }
+  __syncthreads();
+  const int pos = s_base + s_warp[wid] + x - cnt;
+  for (int i = 0; i < cnt; ++i) out[pos + i] = items[i];
+  __syncthreads();
+}
+
+// push into a per-thread append list, spilling to a direct atomic when full
+__device__ __forceinline__ void list_push(int* items, int& cnt, int v, int* counter, int* out) {
+  if (cnt < kAppend) items[cnt++] = v;
+  else out[atomicAdd(counter, 1)] = v;
 }
 
 __device__ __forceinline__ int find_root(int* parent, int x) {
@@ -87,8 +122,8 @@ __global__ void __launch_bounds__(256) mpld_validate(GraphView g, Workspace w) {
         int u = col[e];
         if (u < 0 || u >= g.n || u == v || u <= prev) { bad = 1; break; }
         prev = u;
-        if (!row_contains(col, rp[u], rp[u + 1], v)) bad = 1;         // symmetric
-        if (row_contains(ocol, orp[v], orp[v + 1], u)) bad = 1;       // CE ∩ SE = ∅
+        if (!row_contains(col, rp[u], rp[u + 1], v)) bad = 1;    // symmetric
+        if (row_contains(ocol, orp[v], orp[v + 1], u)) bad = 1;  // CE ∩ SE = ∅
       }
     }
   }
@@ -103,83 +138,98 @@ __global__ void __launch_bounds__(256) mpld_validate(GraphView g, Workspace w) {
 // ---------------------------------------------------------------------------
 // Simplification (R8, §2.2 "simplify the layout graph"):
 // round r hides every not-yet-hidden vertex without stitch edges whose
-// conflict degree among not-yet-hidden vertices is < k.  A vertex enters round
-// r+1 exactly when its live degree crosses k -> k-1 during round r, so each
-// round only touches the neighbours of the previous round (frontier queue).
+// conflict degree among not-yet-hidden vertices is < k.
+//   * rounds 0 and 1 need no barrier: round 0 is a property of each vertex,
+//     and the degree after round 0 is pulled from the neighbours' static data;
+//   * a vertex enters round r+1 (r >= 1) exactly when its live degree crosses
+//     k -> k-1 while round r is pushed, so each round only touches the
+//     neighbours of the previous round (frontier queue).
 // Then union-find connected components over CE ∪ SE of the kept vertices.
-__global__ void __launch_bounds__(256) mpld_simplify_components(GraphView g, Workspace w, int k,
-                                                                int* colors, long long* counts) {
-  cg::grid_group grid = cg::this_grid();
+__global__ void __launch_bounds__(1024) mpld_simplify_components(GraphView g, Workspace w, int k,
+                                                                 int* colors, long long* counts) {
+  GridBarrier grid(&w.ctl->bar[0]);
+  stamp(w.ctl, 12);
   const int n = g.n;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nth = gridDim.x * blockDim.x;
   Control* ctl = w.ctl;
-
-  // phase A: reset the workspace
-  for (int v = tid; v < n + 2; v += nth) w.rcnt[v] = 0;
-  for (int v = tid; v < n; v += nth) {
-    w.deg[v] = g.ce_rp[v + 1] - g.ce_rp[v];
-    w.hround[v] = -1;
-    w.parent[v] = v;
-    w.loc[v] = -1;
-    colors[v] = -1;
-  }
+  (void)colors;
   for (int l = tid; l < 2 * g.n_layouts; l += nth) counts[l] = 0;
-  if (tid == 0) {
-    ctl->n_rounds = 0;
-    ctl->n_hidden = 0;
-    ctl->n_comp = 0;
-    ctl->next_comp = 0;
-    ctl->max_comp = 0;
-    ctl->truncated = 0;
-    ctl->done_blocks = 0;
-    ctl->left[0] = ctl->left[1] = ctl->left[2] = 0;
-    ctl->steps = 0ull;
-  }
-  grid.sync();
 
-  // phase B: round 0 = all low-degree vertices without stitch edges
-  for (int v = tid; v < n; v += nth) {
-    if (g.se_rp[v + 1] == g.se_rp[v] && w.deg[v] < k) {
-      w.hround[v] = 0;
-      int p = atomicAdd(&w.rcnt[0], 1);
-      w.hid[p] = v;
+  // rounds 0 and 1, recovery priorities, union-find init
+  int hidden0 = 0;
+  for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += nth) {
+    const int v = v0 + threadIdx.x;
+    int take = 0;
+    if (v < n) {
+      const int a = g.ce_rp[v], b = g.ce_rp[v + 1];
+      const bool st = g.se_rp[v + 1] > g.se_rp[v];
+      const int lo = layout_index(g, v);
+      w.prio[v] = lowbias32((uint32_t)(v - (g.n_layouts > 1 ? __ldg(&g.layout_off[lo]) : 0)));
+      w.parent[v] = v;
+      int hr = -1;
+      if (!st && b - a < k) {
+        hr = 0;
+        ++hidden0;
+      } else {
+        int d0 = 0;  // live degree after round 0
+        for (int e = a; e < b; ++e) {
+          const int u = g.ce_col[e];
+          const bool u_st = g.se_rp[u + 1] > g.se_rp[u];
+          d0 += (u_st || g.ce_rp[u + 1] - g.ce_rp[u] >= k) ? 1 : 0;
+        }
+        w.deg[v] = d0;
+        if (!st && d0 < k) { hr = 1; take = 1; }
+      }
+      w.hround[v] = hr;
     }
+    int item = v;
+    cta_append(take, &item, &ctl->qcnt[1], w.q1);
   }
+  hidden0 = __reduce_add_sync(0xffffffffu, hidden0);
+  if ((threadIdx.x & 31) == 0 && hidden0) atomicAdd(&ctl->n_hidden, hidden0);
   grid.sync();
+  stamp(w.ctl, 0);
 
-  // phase C: rounds 1, 2, ... (frontier = vertices whose degree crossed k -> k-1)
-  int off = 0, r = 0;
+  // rounds r >= 1: push the frontier's decrements
+  int r = 1;
   while (true) {
-    const int cnt = __ldcg(&w.rcnt[r]);
+    const int cnt = __ldcg(&ctl->qcnt[r % 3]);
     if (cnt == 0) break;
-    if (tid == 0) w.roff[r] = off;
-    const int next_off = off + cnt;
-    for (int i = tid; i < cnt; i += nth) {
-      const int v = __ldcg(&w.hid[off + i]);
-      const int e1 = g.ce_rp[v + 1];
-      for (int e = g.ce_rp[v]; e < e1; ++e) {
-        const int u = g.ce_col[e];
-        if (__ldcg(&w.hround[u]) != -1) continue;  // already hidden: its degree no longer matters
-        const int old = atomicSub(&w.deg[u], 1);
-        if (old == k && g.se_rp[u + 1] == g.se_rp[u]) {
-          w.hround[u] = r + 1;
-          const int p = atomicAdd(&w.rcnt[r + 1], 1);
-          w.hid[next_off + p] = u;
+    if (tid == 0) {
+      ctl->qcnt[(r + 2) % 3] = 0;
+      ctl->n_hidden += cnt;
+    }
+    const int* cur = (r & 1) ? w.q1 : w.q0;
+    int* nxt = (r & 1) ? w.q0 : w.q1;
+    int* ncnt = &ctl->qcnt[(r + 1) % 3];
+    for (int i0 = blockIdx.x * blockDim.x; i0 < cnt; i0 += nth) {
+      const int i = i0 + threadIdx.x;
+      int items[kAppend];
+      int m = 0;
+      if (i < cnt) {
+        const int v = __ldcg(&cur[i]);
+        const int e1 = g.ce_rp[v + 1];
+        for (int e = g.ce_rp[v]; e < e1; ++e) {
+          const int u = g.ce_col[e];
+          if (__ldcg(&w.hround[u]) != -1) continue;  // already hidden: its degree no longer matters
+          const int old = atomicSub(&w.deg[u], 1);
+          if (old == k && g.se_rp[u + 1] == g.se_rp[u]) {
+            w.hround[u] = r + 1;
+            list_push(items, m, u, ncnt, nxt);
+          }
         }
       }
+      cta_append(m, items, ncnt, nxt);
     }
-    off = next_off;
     ++r;
     grid.sync();
+    stamp(w.ctl, 2);
   }
-  if (tid == 0) {
-    ctl->n_rounds = r;
-    ctl->n_hidden = off;
-    w.roff[r] = off;
-  }
+  if (tid == 0) ctl->n_rounds = __ldcg(&ctl->n_hidden) ? r : 0;
+  stamp(w.ctl, 1);
 
-  // phase D: union-find hooking over CE ∪ SE between kept vertices
+  // union-find hooking over CE ∪ SE between kept vertices
   for (int v = tid; v < n; v += nth) {
     if (__ldcg(&w.hround[v]) != -1) continue;
     for (int pass = 0; pass < 2; ++pass) {
@@ -193,16 +243,20 @@ __global__ void __launch_bounds__(256) mpld_simplify_components(GraphView g, Wor
     }
   }
   grid.sync();
+  stamp(w.ctl, 3);
 
-  // phase E: compress, list the roots (component order is irrelevant to the result)
-  for (int v = tid; v < n; v += nth) {
-    if (__ldcg(&w.hround[v]) != -1) continue;
-    const int root = find_root(w.parent, v);
-    w.parent[v] = root;
-    if (root == v) {
-      const int p = atomicAdd(&ctl->n_comp, 1);
-      w.roots[p] = v;
+  // compress, list the roots (component order is irrelevant to the result)
+  for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += nth) {
+    const int v = v0 + threadIdx.x;
+    int is_root = 0;
+    if (v < n && __ldcg(&w.hround[v]) == -1) {
+      const int root = find_root(w.parent, v);
+      w.parent[v] = root;
+      w.loc[v] = -1;  // BFS marker of the search kernel
+      is_root = root == v;
     }
+    int item = v;
+    cta_append(is_root, &item, &ctl->n_comp, w.roots);
   }
 }
 
@@ -211,58 +265,84 @@ __global__ void __launch_bounds__(256) mpld_simplify_components(GraphView g, Wor
 // simplification step"): the hidden stack is popped LIFO — rounds in reverse,
 // inside a round in descending lowbias32(layout-local id) — and each vertex
 // takes the smallest mask unused by its already-coloured conflict neighbours.
-// Inside a round the order is realised Jones-Plassmann style: a vertex is
-// coloured as soon as every same-round neighbour of higher priority is, which
-// yields exactly the sequential result.
-__global__ void __launch_bounds__(256) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
-  cg::grid_group grid = cg::this_grid();
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+//
+// Only the relative order of conflict-adjacent hidden vertices matters, so the
+// LIFO order is realised level-synchronously over the DAG "u before v" (u, v
+// adjacent, u popped first): level 0 = hidden vertices without a hidden
+// predecessor; a vertex joins the next level when its last predecessor is
+// coloured.  Every level is coloured in parallel, one grid barrier per level
+// (DAG depth ~ 10-20 on layout graphs); the result equals the sequential pop.
+__device__ __forceinline__ bool popped_before(int hu, uint32_t pu, int hv, uint32_t pv) {
+  return hu > hv || (hu == hv && pu > pv);
+}
+
+__global__ void __launch_bounds__(1024) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
+  GridBarrier grid(&w.ctl->bar[1]);
+  stamp(w.ctl, 13);
   const int nth = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Control* ctl = w.ctl;
-  const int R = __ldcg(&ctl->n_rounds);
-  int it = 0;
-  for (int r = R - 1; r >= 0; --r) {
-    const int off = __ldcg(&w.roff[r]);
-    const int cnt = __ldcg(&w.rcnt[r]);
-    while (true) {
-      if (tid == 0) ctl->left[(it + 1) % 3] = 0;
-      int left = 0;
-      for (int i = tid; i < cnt; i += nth) {
-        const int v = __ldcg(&w.hid[off + i]);
-        if (__ldcg(&colors[v]) >= 0) continue;
-        const int base = layout_base(g, v);
-        const uint32_t pv = lowbias32((uint32_t)(v - base));
-        bool ready = true;
-        unsigned used = 0;
-        const int e1 = g.ce_rp[v + 1];
-        for (int e = g.ce_rp[v]; e < e1; ++e) {
+  // level 0 and predecessor counts
+  for (int v0 = blockIdx.x * blockDim.x; v0 < g.n; v0 += nth) {
+    const int v = v0 + threadIdx.x;
+    int ready = 0;
+    if (v < g.n) {
+      const int hv = w.hround[v];
+      if (hv >= 0) {
+        const uint32_t pv = w.prio[v];
+        int cnt = 0;
+        for (int e = g.ce_rp[v], e1 = g.ce_rp[v + 1]; e < e1; ++e) {
           const int u = g.ce_col[e];
-          const int hu = __ldcg(&w.hround[u]);
-          if (hu == r) {
-            if (lowbias32((uint32_t)(u - base)) > pv) {
-              const int cu = *((volatile int*)&colors[u]);
-              if (cu < 0) { ready = false; break; }
-              used |= 1u << cu;
-            }
-          } else if (hu == -1 || hu > r) {
+          const int hu = w.hround[u];
+          if (hu >= 0 && popped_before(hu, w.prio[u], hv, pv)) ++cnt;
+        }
+        w.deg[v] = cnt;
+        ready = cnt == 0;
+      }
+    }
+    int item = v;
+    cta_append(ready, &item, &ctl->rq[0], w.q0);
+  }
+  grid.sync();
+  stamp(w.ctl, 8);
+  int L = 0;
+  while (true) {
+    const int cnt = __ldcg(&ctl->rq[L % 3]);
+    if (cnt == 0) break;
+    if (tid == 0) ctl->rq[(L + 2) % 3] = 0;
+    const int* cur = (L & 1) ? w.q1 : w.q0;
+    int* nxt = (L & 1) ? w.q0 : w.q1;
+    int* ncnt = &ctl->rq[(L + 1) % 3];
+    for (int i0 = blockIdx.x * blockDim.x; i0 < cnt; i0 += nth) {
+      const int i = i0 + threadIdx.x;
+      int items[kAppend];
+      int m = 0;
+      if (i < cnt) {
+        const int v = __ldcg(&cur[i]);
+        const int hv = w.hround[v];
+        const uint32_t pv = w.prio[v];
+        const int e0 = g.ce_rp[v], e1 = g.ce_rp[v + 1];
+        unsigned used = 0;
+        for (int e = e0; e < e1; ++e) {
+          const int u = g.ce_col[e];
+          const int hu = w.hround[u];
+          if (hu == -1 || popped_before(hu, w.prio[u], hv, pv)) {
             const int cu = __ldcg(&colors[u]);
             if (cu >= 0) used |= 1u << cu;
+          } else if (atomicSub(&w.deg[u], 1) == 1) {  // v was u's last predecessor
+            list_push(items, m, u, ncnt, nxt);
           }
         }
-        if (ready) {
-          const int c = __ffs(~used) - 1;
-          colors[v] = c < k ? c : 0;  // c < k by the simplification invariant
-        } else {
-          ++left;
-        }
+        const int c = __ffs(~used) - 1;
+        colors[v] = c < k ? c : 0;  // c < k by the simplification invariant
       }
-      if (left) atomicAdd(&ctl->left[it % 3], left);
-      grid.sync();
-      const int remaining = __ldcg(&ctl->left[it % 3]);
-      ++it;
-      if (remaining == 0) break;
+      cta_append(m, items, ncnt, nxt);
     }
+    ++L;
+    grid.sync();
+    stamp(w.ctl, 9);
   }
+  if (tid == 0) ctl->n_levels = L;
 }
 
 // ---------------------------------------------------------------------------
@@ -271,6 +351,7 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
                                                      long long* counts, double* cost, long long* stats,
                                                      int launches) {
   const int nth = gridDim.x * blockDim.x;
+  stamp(w.ctl, 15);
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += nth) {
     const int cv = colors[v];
     int nc = 0, ns = 0;
@@ -300,19 +381,17 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
     const long long ns = __ldcg(&counts[2 * l + 1]);
     cost[l] = __dadd_rn(__dmul_rn(alpha, (double)ns), (double)nc);
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && stats) {
     Control* ctl = w.ctl;
-    if (stats) {
-      stats[MPLD_STAT_COMPONENTS] = __ldcg(&ctl->n_comp);
-      stats[MPLD_STAT_HIDDEN] = __ldcg(&ctl->n_hidden);
-      stats[MPLD_STAT_ROUNDS] = __ldcg(&ctl->n_rounds);
-      stats[MPLD_STAT_MAX_COMP] = __ldcg(&ctl->max_comp);
-      stats[MPLD_STAT_STEPS] = (long long)__ldcg(&ctl->steps);
-      stats[MPLD_STAT_TRUNCATED] = __ldcg(&ctl->truncated);
-      stats[MPLD_STAT_ERROR] = __ldcg(&ctl->err);
-      stats[MPLD_STAT_LAUNCHES] = launches;
-    }
-    ctl->err = 0;  // the control block resets itself for the next call
+    stats[MPLD_STAT_COMPONENTS] = __ldcg(&ctl->n_comp);
+    stats[MPLD_STAT_HIDDEN] = __ldcg(&ctl->n_hidden);
+    stats[MPLD_STAT_ROUNDS] = __ldcg(&ctl->n_rounds);
+    stats[MPLD_STAT_MAX_COMP] = __ldcg(&ctl->max_comp);
+    stats[MPLD_STAT_STEPS] = (long long)__ldcg(&ctl->steps);
+    stats[MPLD_STAT_TRUNCATED] = __ldcg(&ctl->truncated);
+    stats[MPLD_STAT_ERROR] = __ldcg(&ctl->err);
+    stats[MPLD_STAT_LAUNCHES] = launches;
+    stats[MPLD_STAT_MAX_STEPS] = __ldcg(&ctl->max_steps_comp);
   }
 }
 
@@ -323,8 +402,8 @@ cudaError_t launch_validate(const GraphView& g, Workspace ws, cudaStream_t s, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors,
-                                       long long* counts, cudaStream_t s, int blocks, int threads) {
+cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors, long long* counts,
+                                       cudaStream_t s, int blocks, int threads) {
   GraphView gg = g;
   void* args[] = {&gg, &ws, &k, &colors, &counts};
   return cudaLaunchCooperativeKernel((void*)mpld_simplify_components, dim3(blocks), dim3(threads), args, 0, s);

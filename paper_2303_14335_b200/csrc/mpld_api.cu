@@ -37,7 +37,7 @@ enum KernelId { K_VALIDATE = 0, K_SIMPLIFY, K_SEARCH, K_RECOVER, K_EVALUATE, K_C
 const char* kKernelNames[K_COUNT] = {"mpld_validate", "mpld_simplify_components", "mpld_exact_cover_search",
                                      "mpld_recover", "mpld_evaluate"};
 
-constexpr int kCoopThreads = 256;
+constexpr int kCoopThreads = 1024;
 constexpr int kSearchThreads = 128;
 
 }  // namespace
@@ -50,9 +50,9 @@ struct mpld_context {
   // workspace
   int* deg = nullptr;
   int* hround = nullptr;
-  int* hid = nullptr;
-  int* rcnt = nullptr;
-  int* roff = nullptr;
+  unsigned* prio = nullptr;
+  int* q0 = nullptr;
+  int* q1 = nullptr;
   int* parent = nullptr;
   int* loc = nullptr;
   int* roots = nullptr;
@@ -92,12 +92,11 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
   if (n > ctx->cap_n) {
     int64_t cap = std::max<int64_t>(n, ctx->cap_n * 3 / 2);
     cudaError_t e = cudaSuccess;
-    for (int** p : {&ctx->deg, &ctx->hround, &ctx->hid, &ctx->parent, &ctx->loc, &ctx->roots}) {
+    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->parent, &ctx->loc, &ctx->roots}) {
       e = grow(p, cap);
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
-    if (grow(&ctx->rcnt, cap + 2) != cudaSuccess || grow(&ctx->roff, cap + 2) != cudaSuccess)
-      return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
+    if (grow(&ctx->prio, cap) != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     ctx->cap_n = cap;
   }
   if (n_layouts > ctx->cap_layouts) {
@@ -153,8 +152,10 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
                  long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost,
                  long long* stats) {
-  Workspace ws{ctx->deg, ctx->hround, ctx->hid, ctx->rcnt, ctx->roff, ctx->parent, ctx->loc, ctx->roots, ctx->ctl};
-  cudaError_t e;
+  Workspace ws{ctx->deg, ctx->hround, ctx->prio, ctx->q0, ctx->q1, ctx->parent, ctx->loc, ctx->roots, ctx->ctl};
+  // the control block (counters, barrier arrivals, error bits) starts every call at zero
+  cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
+  if (e != cudaSuccess) return cuda_fail(e, "control reset");
   int launches = 0;
   const int n_launch = 4 + ((flags & MPLD_FLAG_VALIDATE) ? 1 : 0);
   if (flags & MPLD_FLAG_VALIDATE) {
@@ -271,7 +272,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
 
 void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
-  for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->hid, (void*)ctx->rcnt, (void*)ctx->roff,
+  for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->parent, (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->ctl, (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
                   (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})
@@ -424,6 +425,21 @@ int mpld_context_reset_timing(mpld_context* ctx) {
 }
 
 int mpld_kernel_count(void) { return K_COUNT; }
+
+int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
+  if (!ctx || !out || n < 0) return fail(MPLD_ERR_ARG, "bad argument");
+  Control c;
+  cudaError_t e = cudaMemcpy(&c, ctx->ctl, sizeof(Control), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "debug copy");
+  int64_t v[20];
+  for (int i = 0; i < 16; ++i) v[i] = (int64_t)c.t[i];
+  v[16] = c.n_levels;
+  v[17] = c.n_hidden;
+  v[18] = c.n_rounds;
+  v[19] = c.max_steps_comp;
+  for (int i = 0; i < n && i < 20; ++i) out[i] = v[i];
+  return MPLD_OK;
+}
 
 const char* mpld_kernel_name(int i) { return (i >= 0 && i < K_COUNT) ? kKernelNames[i] : ""; }
 

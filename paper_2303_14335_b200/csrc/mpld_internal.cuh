@@ -20,21 +20,50 @@ constexpr int kCostUnits = MPLD_COST_UNITS;
 
 enum ErrBits : int { kErrGraph = 1, kErrComponent = 2 };
 
-// Device-resident control block, zeroed at the start of every call by the
-// simplification kernel (phase A) except `err`, which the validation kernel may
-// set first (the host zeroes it with the graph upload / a memset node).
+// Device-resident control block, zeroed by one memset node at the start of
+// every call (before the optional validation kernel).
 struct Control {
   int n_rounds;     // simplification rounds R (R8)
   int n_hidden;     // |hidden vertices|
   int n_comp;       // components found
-  int next_comp;    // dynamic work counter of the search kernel
   int max_comp;     // largest component
   int truncated;    // components whose search hit max_steps
   int err;          // ErrBits
   int done_blocks;  // last-block detection of the evaluation kernel
-  int left[3];      // recovery: uncoloured vertices per iteration (rotating)
+  int max_steps_comp;        // largest per-component step count
+  int qcnt[3];               // simplification frontier sizes (rotating by round)
+  int rq[3];                 // recovery level sizes (rotating by level)
+  int n_levels;              // recovery levels (DAG depth + 1)
   int pad;
   unsigned long long steps;  // search nodes entered
+  unsigned bar[2];           // grid-barrier arrival counters of the two cooperative kernels
+  unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
+};
+
+// Grid-wide barrier for the cooperatively launched persistent kernels.  Each
+// CTA arrives once per barrier on a monotonically increasing counter and polls
+// it with relaxed loads (no L1 invalidation inside the spin loop; one fence on
+// each side), so a barrier costs one L2 atomic per CTA plus the polling latency.
+struct GridBarrier {
+  unsigned* count;
+  unsigned nblocks;
+  unsigned epoch;
+  __device__ __forceinline__ GridBarrier(unsigned* c) : count(c), nblocks(gridDim.x), epoch(0) {}
+  __device__ __forceinline__ void sync() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ++epoch;
+      __threadfence();
+      atomicAdd(count, 1u);
+      const unsigned target = epoch * nblocks;
+      unsigned cur;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(count) : "memory");
+      } while ((int)(cur - target) < 0);
+      __threadfence();
+    }
+    __syncthreads();
+  }
 };
 
 struct GraphView {
@@ -48,14 +77,14 @@ struct GraphView {
 };
 
 struct Workspace {
-  int* deg;
-  int* hround;  // -1 kept, else the round the vertex was hidden in
-  int* hid;     // hidden vertices, grouped by round
-  int* rcnt;    // [n+2]
-  int* roff;    // [n+2]
-  int* parent;  // union-find
-  int* loc;     // local index of a kept vertex inside its component
-  int* roots;   // component roots (min vertex id of the component)
+  int* deg;        // live conflict degree (simplification), then hidden-predecessor count (recovery)
+  int* hround;     // -1 kept, else the round the vertex was hidden in
+  unsigned* prio;  // lowbias32(layout-local id), recovery priority (R9)
+  int* q0;         // frontier queues (double-buffered)
+  int* q1;
+  int* parent;     // union-find
+  int* loc;        // local index of a kept vertex inside its component
+  int* roots;      // component roots (min vertex id of the component)
   Control* ctl;
 };
 

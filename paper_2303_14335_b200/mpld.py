@@ -23,13 +23,15 @@ MPLD_FLAG_VALIDATE = 1
 MPLD_MAX_K = 4
 MPLD_MAX_COMPONENT = 64
 MPLD_COST_UNITS = 1000
-STAT_NAMES = ["components", "hidden", "rounds", "max_component", "steps", "truncated", "error", "launches"]
+STAT_NAMES = ["components", "hidden", "rounds", "max_component", "steps", "truncated", "error", "launches",
+              "max_steps"]
 MPLD_STAT_LEN = len(STAT_NAMES)
 
 # every symbol include/mpld.h declares
 EXPORTS = ["mpld_last_error", "mpld_version", "mpld_decompose", "mpld_decompose_batch", "mpld_context_create",
            "mpld_context_destroy", "mpld_decompose_device", "mpld_context_set_timing",
-           "mpld_context_reset_timing", "mpld_kernel_count", "mpld_kernel_name", "mpld_context_kernel_time"]
+           "mpld_context_reset_timing", "mpld_kernel_count", "mpld_kernel_name", "mpld_context_kernel_time",
+           "mpld_context_debug"]
 
 
 class MPLDError(RuntimeError):
@@ -71,6 +73,7 @@ def lib():
     L.mpld_context_set_timing.argtypes = [_vp, ctypes.c_int]
     L.mpld_context_reset_timing.argtypes = [_vp]
     L.mpld_context_kernel_time.argtypes = [_vp, ctypes.c_int, _f64p, _i64p]
+    L.mpld_context_debug.argtypes = [_vp, _vp, ctypes.c_int]
     _lib = L
     return L
 
@@ -183,6 +186,12 @@ class Context:
 
     def reset_timing(self):
         _check(lib().mpld_context_reset_timing(self._h))
+
+    def debug(self):
+        """Diagnostics of the last call (include/mpld.h mpld_context_debug)."""
+        out = np.zeros(20, dtype=np.int64)
+        _check(lib().mpld_context_debug(self._h, out.ctypes.data, 20))
+        return out
 
     def kernel_times(self):
         """{kernel name: (accumulated ms, launches)} since the last reset."""
