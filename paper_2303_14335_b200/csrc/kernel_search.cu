@@ -1,9 +1,9 @@
 // The exact-cover search of PAPER.md §2.3 / Alg. 1 on bit-packed matrices.
 //
-// One thread owns one component (n <= 64 vertices).  The exact-cover matrix
-// (rows r(v,c), primary columns = vertices, secondary columns = (e,c) for
-// e in CE) is never materialised as a 0/1 array: with columns = bit positions
-// of a machine word it is fully described by, per vertex v,
+// The exact-cover matrix of a component (rows r(v,c), primary columns =
+// vertices, secondary columns = (e,c) for e in CE) is never materialised as a
+// 0/1 array: with columns = bit positions of a machine word it is fully
+// described by, per vertex v,
 //     adj[v]  — CE neighbours (the secondary columns shared by r(v,c), r(u,c))
 //     sadj[v] — SE neighbours (stitch cost of Eq. 1c)
 // and the search state by, per mask c,
@@ -16,8 +16,19 @@
 //     stitches of selecting r(v,c)   = popc(sadj[v] & coloured & ~C[c])
 // Cover/uncover (Eq. 2) become mask AND/OR; backtracking pops a 32-byte frame.
 // Components of <= 32 vertices run on 32-bit words, larger ones on 64-bit.
-// The search order, bound and budget are DESIGN.md R4-R7, identical to the
-// oracle's dancing-links Algorithm X, so the result is bit-identical.
+//
+// Two kernels:
+//   mpld_exact_cover_search<K>        one thread per component (sequential DFS,
+//                                     the oracle's exact node order and budget, R7);
+//   mpld_exact_cover_search_heavy<K>  exact mode (max_steps <= 0) only: one warp
+//                                     per component whose thread-level search
+//                                     needed more than kLightSteps nodes.  The
+//                                     canonical tree is split level-synchronously
+//                                     into >= kTarget subtrees (DFS order kept),
+//                                     lanes search subtrees with a shared
+//                                     incumbent keyed (cost, subtree index); the
+//                                     first optimal leaf of R7 is recovered
+//                                     exactly.
 #include <climits>
 
 #include "mpld_internal.cuh"
@@ -25,6 +36,10 @@
 namespace mpld {
 
 namespace {
+
+constexpr unsigned kLightSteps = 96;  // exact mode: thread-level budget before a component turns heavy
+constexpr int kTarget = 96;           // heavy: frontier size that stops the level-synchronous split
+constexpr int kCap = 192;             // heavy: frontier capacity per level buffer
 
 template <typename W>
 struct WordOps;
@@ -44,11 +59,21 @@ struct WordOps<unsigned long long> {
 // One level of the explicit backtrack stack (Alg. 1 recursion, lines 13-18).
 template <typename W>
 struct __align__(16) Frame {
-  W saved;   // B[c] before r(v,c) was selected
-  W adj;     // adj[v]
-  W sadj;    // sadj[v]
-  int cost;  // cost when the node was entered
+  W saved;     // B[c] before r(v,c) was selected
+  W adj;       // adj[v]
+  W sadj;      // sadj[v]
+  int cost;    // cost when the node was entered
   int packed;  // v | (c+1) << 8 | (maxused+1) << 16
+};
+
+// A search-tree node (heavy split).
+template <int K, typename W>
+struct __align__(16) Node {
+  W C[K];
+  W B[K];
+  W U;
+  int cost;
+  int mu;
 };
 
 template <int K, typename W>
@@ -66,19 +91,60 @@ __device__ __forceinline__ void put(W (&a)[K], int c, W x) {
     if (c == i) a[i] = x;
 }
 
-// Relaxed Algorithm X with branch and bound (R4-R7).  am[i] =
-// (adj, sadj) of local vertex i.  Returns the steps taken; the best masks in bestC.
+// column-count reduction, bit-sliced over all columns: Z = no live row, O = one live row
 template <int K, typename W>
-__device__ unsigned search_component(const W* __restrict__ am_adj, const W* __restrict__ am_sadj, int n,
-                                     int w_stitch, unsigned max_steps, Frame<W>* __restrict__ stack,
-                                     W (&bestC)[K], bool& truncated) {
-  using O = WordOps<W>;
-  W C[K], B[K];
+__device__ __forceinline__ void live_counts(const W (&B)[K], W U, W& Z, W& O) {
+  W s1 = 0, s2 = 0;
 #pragma unroll
-  for (int c = 0; c < K; ++c) { C[c] = 0; B[c] = 0; bestC[c] = 0; }
-  W U = O::full(n);
-  int cost = 0, maxused = -1, depth = 0;
+  for (int c = 0; c < K; ++c) {
+    const W F = U & ~B[c];
+    s2 |= s1 & F;
+    s1 |= F;
+  }
+  Z = U & ~s1;
+  O = s1 & ~s2;
+}
+
+// Incumbent of the sequential search: strict improvement, prune on lb >= best.
+struct SeqIncumbent {
   int best = INT_MAX;
+  __device__ __forceinline__ bool has() const { return best != INT_MAX; }
+  __device__ __forceinline__ bool prune(int lb) const { return lb >= best; }
+  __device__ __forceinline__ bool improves(int cost) const { return cost < best; }
+  __device__ __forceinline__ void take(int cost) { best = cost; }
+};
+
+// Incumbent of the warp-parallel search: keys (cost << 32 | subtree + 1),
+// shared through a shared-memory atomicMin; a node of subtree f is pruned when
+// (lb, f+1) >= the best key, so equal-cost leaves of earlier
+// subtrees always win.
+struct ParIncumbent {
+  unsigned long long* shared_best;
+  unsigned long long fkey;  // f + 1
+  unsigned long long lane_best = ~0ull;
+  __device__ __forceinline__ bool has() const { return true; }
+  __device__ __forceinline__ bool prune(int lb) const {
+    const unsigned long long g = *((volatile unsigned long long*)shared_best);
+    return (((unsigned long long)lb << 32) | fkey) >= g;
+  }
+  __device__ __forceinline__ bool improves(int cost) const {
+    return (((unsigned long long)cost << 32) | fkey) < lane_best;
+  }
+  __device__ __forceinline__ void take(int cost) {
+    lane_best = ((unsigned long long)cost << 32) | fkey;
+    atomicMin(shared_best, lane_best);
+  }
+};
+
+// Relaxed Algorithm X with branch and bound (R4-R7) from the node
+// (C, B, U, cost, maxused).  am_adj[i] / am_sadj[i] = masks of local vertex i.
+// Returns the nodes entered; the best leaf's masks in bestC.
+template <int K, typename W, typename Inc>
+__device__ unsigned dfs(const W* __restrict__ am_adj, const W* __restrict__ am_sadj, W (&C)[K], W (&B)[K], W U,
+                        int cost, int maxused, int w_stitch, unsigned max_steps, Frame<W>* __restrict__ stack,
+                        Inc& inc, W (&bestC)[K], bool& truncated) {
+  using O = WordOps<W>;
+  int depth = 0;
   unsigned steps = 0;
   truncated = false;
   bool enter = true;
@@ -88,25 +154,17 @@ __device__ unsigned search_component(const W* __restrict__ am_adj, const W* __re
   while (true) {
     if (enter) {
       ++steps;
-      if (best != INT_MAX && steps > max_steps) { truncated = true; break; }
+      if (inc.has() && steps > max_steps) { truncated = true; break; }
       if (U == 0) {  // Alg. 1 line 5: every column covered -> a solution
-        if (cost < best) {
-          best = cost;
+        if (inc.improves(cost)) {
+          inc.take(cost);
 #pragma unroll
           for (int c = 0; c < K; ++c) bestC[c] = C[c];
         }
       } else {
-        // column-count reduction, bit-sliced over all columns at once
-        W s1 = 0, s2 = 0;
-#pragma unroll
-        for (int c = 0; c < K; ++c) {
-          const W F = U & ~B[c];  // live rows of mask c
-          s2 |= s1 & F;
-          s1 |= F;
-        }
-        const W Z = U & ~s1;  // columns with no live row
-        const W Ol = s1 & ~s2;  // columns with exactly one live row
-        if (cost + kCostUnits * O::popc(Z) < best) {  // bound (R7)
+        W Z, Ol;
+        live_counts<K, W>(B, U, Z, Ol);
+        if (!inc.prune(cost + kCostUnits * O::popc(Z))) {  // bound (R7)
           const W cand = Z ? Z : (Ol ? Ol : U);  // Alg. 1 line 8 (R5)
           const int v = O::ffs(cand);
           if (depth > 0) {  // spill the parent frame
@@ -154,15 +212,42 @@ __device__ unsigned search_component(const W* __restrict__ am_adj, const W* __re
     }
     const W Cc = pick<K, W>(C, c);
     const W Bc = pick<K, W>(B, c);
-    const int inc = kCostUnits * O::popc(f_adj & Cc) + w_stitch * O::popc(f_sadj & ~U & ~Cc);
+    cost = f_cost + kCostUnits * O::popc(f_adj & Cc) + w_stitch * O::popc(f_sadj & ~U & ~Cc);
     f_saved = Bc;
     f_c = c;
     put<K, W>(C, c, Cc | bit);  // select r(v,c) (line 14) and cover its secondary columns (line 15)
     put<K, W>(B, c, Bc | f_adj);
-    cost = f_cost + inc;
     maxused = max(f_mu, c);
     enter = true;
   }
+  return steps;
+}
+
+template <int K, typename W>
+__device__ __forceinline__ int colour_of(const W (&bestC)[K], int i) {
+  int c = 0;
+#pragma unroll
+  for (int cc = 1; cc < K; ++cc)
+    if ((bestC[cc] >> i) & W(1)) c = cc;
+  return c;
+}
+
+template <int K, typename W>
+__device__ unsigned run_light(const unsigned long long* adjm, const unsigned long long* sadjm, int n, int w_stitch,
+                              unsigned budget, Frame<W>* stack, int* cval, int& best_cost, bool& trunc) {
+  W a[kMaxComp], s[kMaxComp];
+  for (int i = 0; i < n; ++i) {
+    a[i] = (W)adjm[i];
+    s[i] = (W)sadjm[i];
+  }
+  W C[K], B[K], bestC[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) C[c] = B[c] = bestC[c] = 0;
+  SeqIncumbent inc;
+  const unsigned steps =
+      dfs<K, W, SeqIncumbent>(a, s, C, B, WordOps<W>::full(n), 0, -1, w_stitch, budget, stack, inc, bestC, trunc);
+  for (int i = 0; i < n; ++i) cval[i] = colour_of<K, W>(bestC, i);
+  best_cost = inc.best;
   return steps;
 }
 
@@ -176,7 +261,9 @@ __global__ void __launch_bounds__(128) mpld_exact_cover_search(GraphView g, Work
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     ctl->t[14] = t;
   }
-  const unsigned budget = (max_steps <= 0 || max_steps >= (long long)UINT_MAX) ? UINT_MAX : (unsigned)max_steps;
+  const bool exact = max_steps <= 0;
+  const unsigned budget = exact ? kLightSteps
+                                : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
   int order[kMaxComp];
   unsigned long long adjm[kMaxComp], sadjm[kMaxComp];
   union {
@@ -222,35 +309,222 @@ __global__ void __launch_bounds__(128) mpld_exact_cover_search(GraphView g, Work
     }
     unsigned steps;
     bool trunc;
+    int best_cost;
     int cval[kMaxComp];
-    if (n <= 32) {
-      unsigned a32[32], s32[32];
-      for (int i = 0; i < n; ++i) { a32[i] = (unsigned)adjm[i]; s32[i] = (unsigned)sadjm[i]; }
-      unsigned bestC[K];
-      steps = search_component<K, unsigned>(a32, s32, n, w_stitch, budget, stack.f32, bestC, trunc);
-      for (int i = 0; i < n; ++i) {
-        int c = 0;
-#pragma unroll
-        for (int cc = 1; cc < K; ++cc)
-          if ((bestC[cc] >> i) & 1u) c = cc;
-        cval[i] = c;
-      }
-    } else {
-      unsigned long long bestC[K];
-      steps = search_component<K, unsigned long long>(adjm, sadjm, n, w_stitch, budget, stack.f64, bestC, trunc);
-      for (int i = 0; i < n; ++i) {
-        int c = 0;
-#pragma unroll
-        for (int cc = 1; cc < K; ++cc)
-          if ((bestC[cc] >> i) & 1ull) c = cc;
-        cval[i] = c;
-      }
-    }
+    if (n <= 32)
+      steps = run_light<K, unsigned>(adjm, sadjm, n, w_stitch, budget, stack.f32, cval, best_cost, trunc);
+    else
+      steps = run_light<K, unsigned long long>(adjm, sadjm, n, w_stitch, budget, stack.f64, cval, best_cost, trunc);
     for (int i = 0; i < n; ++i) colors[order[i]] = cval[i];
     atomicAdd(&ctl->steps, (unsigned long long)steps);
     atomicMax(&ctl->max_comp, n);
-    atomicMax(&ctl->max_steps_comp, (int)min(steps, (unsigned)INT_MAX));
-    if (trunc) atomicAdd(&ctl->truncated, 1);
+    if (trunc && exact) {  // hand the component to the warp-parallel search
+      const int h = atomicAdd(&ctl->n_heavy, 1);
+      w.q0[h] = root;
+      w.q1[h] = best_cost;
+    } else {
+      atomicMax(&ctl->max_steps_comp, (int)min(steps, (unsigned)INT_MAX));
+      if (trunc) atomicAdd(&ctl->truncated, 1);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// warp-parallel exact search of one heavy component (block = one warp)
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y < x ? y : x;
+  }
+  return x;
+}
+
+__device__ __forceinline__ int warp_excl_scan(int x, int& total) {
+  const int lane = threadIdx.x & 31;
+  int y = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int z = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) y += z;
+  }
+  total = __shfl_sync(0xffffffffu, y, 31);
+  return y - x;
+}
+
+// Expand node nd: number of children (0 pruned, 1 for a leaf itself) and, if
+// out != nullptr, write them in DFS (colour) order.
+template <int K, typename W>
+__device__ int expand(const Node<K, W>& nd, const W* s_adj, const W* s_sadj, int w_stitch, int bound,
+                      Node<K, W>* out) {
+  using O = WordOps<W>;
+  if (nd.U == 0) {
+    if (out) *out = nd;
+    return 1;
+  }
+  W Z, Ol;
+  live_counts<K, W>(nd.B, nd.U, Z, Ol);
+  if (nd.cost + kCostUnits * O::popc(Z) >= bound) return 0;  // pruned against the light-phase incumbent
+  const W cand = Z ? Z : (Ol ? Ol : nd.U);
+  const int v = O::ffs(cand);
+  const W bit = W(1) << v;
+  const int lim = min(K - 1, nd.mu + 1);
+  if (out) {
+    const W a = s_adj[v], s = s_sadj[v];
+    const W U = nd.U & ~bit;
+    for (int c = 0; c <= lim; ++c) {
+      Node<K, W> ch = nd;
+      const W Cc = pick<K, W>(nd.C, c);
+      ch.U = U;
+      ch.cost = nd.cost + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(s & ~U & ~Cc);
+      put<K, W>(ch.C, c, Cc | bit);
+      put<K, W>(ch.B, c, pick<K, W>(nd.B, c) | a);
+      ch.mu = max(nd.mu, c);
+      out[c] = ch;
+    }
+  }
+  return lim + 1;
+}
+
+template <int K, typename W>
+__device__ void heavy_component(int n, const int* s_order, const unsigned long long* s_adj64,
+                                const unsigned long long* s_sadj64, unsigned char* smem, int w_stitch, int c1,
+                                int* colors, Control* ctl) {
+  const int lane = threadIdx.x;
+  W* s_adj = (W*)smem;
+  W* s_sadj = s_adj + kMaxComp;
+  Node<K, W>* lvl[2] = {(Node<K, W>*)(smem + 2 * kMaxComp * sizeof(unsigned long long)), nullptr};
+  lvl[1] = lvl[0] + kCap;
+  __shared__ unsigned long long s_best;
+  __shared__ int s_next;
+  for (int i = lane; i < n; i += 32) {
+    s_adj[i] = (W)s_adj64[i];
+    s_sadj[i] = (W)s_sadj64[i];
+  }
+  if (lane == 0) {
+    Node<K, W> root;
+#pragma unroll
+    for (int c = 0; c < K; ++c) root.C[c] = root.B[c] = 0;
+    root.U = WordOps<W>::full(n);
+    root.cost = 0;
+    root.mu = -1;
+    lvl[0][0] = root;
+    s_best = (unsigned long long)c1 << 32;  // the light-phase leaf precedes every subtree (key f+1 = 0)
+    s_next = 0;
+  }
+  __syncwarp();
+  // level-synchronous split of the canonical tree, DFS order preserved
+  int m = 1, cur = 0;
+  unsigned expanded = 0;
+  while (m < kTarget) {
+    int total = 0;
+    bool inner = false;  // some node still has uncovered columns
+    for (int i0 = 0; i0 < m; i0 += 32) {
+      const int i = i0 + lane;
+      const int cnt = i < m ? expand<K, W>(lvl[cur][i], s_adj, s_sadj, w_stitch, c1, nullptr) : 0;
+      inner |= __any_sync(0xffffffffu, i < m && lvl[cur][i].U != 0 && cnt > 0);
+      int t;
+      warp_excl_scan(cnt, t);
+      total += t;
+    }
+    if (total == 0) {
+      m = 0;
+      break;
+    }
+    if (total > kCap || !inner) break;
+    int base = 0;
+    for (int i0 = 0; i0 < m; i0 += 32) {
+      const int i = i0 + lane;
+      const int cnt = i < m ? expand<K, W>(lvl[cur][i], s_adj, s_sadj, w_stitch, c1, nullptr) : 0;
+      int t;
+      const int off = warp_excl_scan(cnt, t);
+      if (cnt) expand<K, W>(lvl[cur][i], s_adj, s_sadj, w_stitch, c1, &lvl[cur ^ 1][base + off]);
+      base += t;
+    }
+    expanded += m;
+    cur ^= 1;
+    m = total;
+    __syncwarp();
+  }
+  // lanes search the subtrees in DFS order with a shared incumbent
+  Frame<W> stack[kMaxComp];
+  W bestC[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) bestC[c] = 0;
+  unsigned long long my_best = ~0ull;
+  unsigned steps = 0;
+  while (true) {
+    const int f = atomicAdd(&s_next, 1);
+    if (f >= m) break;
+    Node<K, W> nd = lvl[cur][f];
+    ParIncumbent inc;
+    inc.shared_best = &s_best;
+    inc.fkey = (unsigned long long)(f + 1);
+    inc.lane_best = my_best;
+    bool trunc;
+    steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, nd.C, nd.B, nd.U, nd.cost, nd.mu, w_stitch, UINT_MAX, stack,
+                                     inc, bestC, trunc);
+    my_best = inc.lane_best;
+  }
+  const unsigned long long win = warp_min_u64(my_best);
+  const unsigned who = __ballot_sync(0xffffffffu, my_best == win && win != ~0ull);
+  if (who && lane == __ffs(who) - 1 && win < ((unsigned long long)c1 << 32)) {
+    for (int i = 0; i < n; ++i) colors[s_order[i]] = colour_of<K, W>(bestC, i);
+  }
+  unsigned total_steps = steps;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) total_steps += __shfl_xor_sync(0xffffffffu, total_steps, o);
+  if (lane == 0) {
+    atomicAdd(&ctl->steps, (unsigned long long)(total_steps + expanded));
+    atomicMax(&ctl->max_steps_comp, (int)min(total_steps + expanded, (unsigned)INT_MAX));
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
+                                                                    int* colors) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_order[kMaxComp];
+  __shared__ unsigned long long s_adj64[kMaxComp], s_sadj64[kMaxComp];
+  __shared__ int s_n;
+  Control* ctl = w.ctl;
+  const int n_heavy = __ldcg(&ctl->n_heavy);
+  for (int h = blockIdx.x; h < n_heavy; h += gridDim.x) {
+    const int root = __ldcg(&w.q0[h]);
+    const int c1 = __ldcg(&w.q1[h]);
+    if (threadIdx.x == 0) {
+      // rebuild the matrix: loc[] already holds every vertex's BFS index
+      int n = 1, head = 0;
+      s_order[0] = root;
+      while (head < n) {
+        const int v = s_order[head];
+        unsigned long long adj = 0ull, sadj = 0ull;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int* rp = pass ? g.se_rp : g.ce_rp;
+          const int* col = pass ? g.se_col : g.ce_col;
+          for (int e = rp[v], e1 = rp[v + 1]; e < e1; ++e) {
+            const int u = col[e];
+            if (w.hround[u] != -1) continue;
+            const int lu = w.loc[u];
+            s_order[lu] = u;  // every vertex is seen before the BFS head reaches its index
+            n = max(n, lu + 1);
+            if (pass) sadj |= 1ull << lu; else adj |= 1ull << lu;
+          }
+        }
+        s_adj64[head] = adj;
+        s_sadj64[head] = sadj;
+        ++head;
+      }
+      s_n = n;
+    }
+    __syncwarp();
+    const int n = s_n;
+    if (n <= 32)
+      heavy_component<K, unsigned>(n, s_order, s_adj64, s_sadj64, smem, w_stitch, c1, colors, ctl);
+    else
+      heavy_component<K, unsigned long long>(n, s_order, s_adj64, s_sadj64, smem, w_stitch, c1, colors, ctl);
+    __syncwarp();
   }
 }
 
@@ -265,6 +539,32 @@ cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch,
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+size_t heavy_smem_bytes() {
+  return 2 * kMaxComp * sizeof(unsigned long long) + 2 * kCap * sizeof(Node<MPLD_MAX_K, unsigned long long>);
+}
+
+cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
+                                int blocks) {
+  const size_t smem = heavy_smem_bytes();
+  switch (k) {
+    case 2: mpld_exact_cover_search_heavy<2><<<blocks, 32, smem, s>>>(g, ws, w_stitch, colors); break;
+    case 3: mpld_exact_cover_search_heavy<3><<<blocks, 32, smem, s>>>(g, ws, w_stitch, colors); break;
+    case 4: mpld_exact_cover_search_heavy<4><<<blocks, 32, smem, s>>>(g, ws, w_stitch, colors); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t configure_search_heavy() {
+  const int smem = (int)heavy_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return e;
 }
 
 int resident_blocks_search(int threads, int num_sms) {

@@ -14,7 +14,8 @@ namespace mpld {
 
 namespace {
 
-constexpr int kAppend = 8;  // items one thread may append per call before spilling to direct atomics
+constexpr int kAppend = 8;   // items one thread may append per call before spilling to direct atomics
+constexpr int kTail = 4096;  // frontiers up to this size are finished by a single CTA
 
 __device__ __forceinline__ bool row_contains(const int* __restrict__ col, int a, int b, int x) {
   // binary search in the strictly ascending row col[a..b)
@@ -42,6 +43,15 @@ __device__ __forceinline__ void stamp(Control* ctl, int i) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     ctl->t[i] = t;
+  }
+}
+
+__device__ __forceinline__ void dstamp(Control* ctl, int i, int cnt) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && i < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ctl->tr[i] = t;
+    ctl->nr[i] = cnt;
   }
 }
 
@@ -135,6 +145,34 @@ __global__ void __launch_bounds__(256) mpld_validate(GraphView g, Workspace w) {
   if (bad) atomicOr(&w.ctl->err, kErrGraph);
 }
 
+// One simplification round r >= 1: push the decrements of the frontier
+// (items [first, cnt) with the given stride; every thread of the CTA calls it).
+__device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r, int cnt, int first, int stride) {
+  Control* ctl = w.ctl;
+  const int* cur = (r & 1) ? w.q1 : w.q0;
+  int* nxt = (r & 1) ? w.q0 : w.q1;
+  int* ncnt = &ctl->qcnt[(r + 1) % 3];
+  for (int i0 = first; i0 < cnt; i0 += stride) {
+    const int i = i0 + threadIdx.x;
+    int items[kAppend];
+    int m = 0;
+    if (i < cnt) {
+      const int v = __ldcg(&cur[i]);
+      const int e1 = g.ce_rp[v + 1];
+      for (int e = g.ce_rp[v]; e < e1; ++e) {
+        const int u = g.ce_col[e];
+        if (__ldcg(&w.hround[u]) != -1) continue;  // already hidden: its degree no longer matters
+        const int old = atomicSub(&w.deg[u], 1);
+        if (old == k && g.se_rp[u + 1] == g.se_rp[u]) {
+          w.hround[u] = r + 1;
+          list_push(items, m, u, ncnt, nxt);
+        }
+      }
+    }
+    cta_append(m, items, ncnt, nxt);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Simplification (R8, §2.2 "simplify the layout graph"):
 // round r hides every not-yet-hidden vertex without stitch edges whose
@@ -196,32 +234,35 @@ __global__ void __launch_bounds__(1024) mpld_simplify_components(GraphView g, Wo
   while (true) {
     const int cnt = __ldcg(&ctl->qcnt[r % 3]);
     if (cnt == 0) break;
+    if (cnt <= kTail) {
+      // small frontier: CTA 0 runs the remaining rounds alone with block
+      // barriers (a grid barrier costs ~1.5 µs; the rounds only need the
+      // dependent-load latency)
+      if (blockIdx.x == 0) {
+        int rr = r, c = cnt;
+        while (c > 0) {
+          if (threadIdx.x == 0) {
+            ctl->qcnt[(rr + 2) % 3] = 0;
+            ctl->n_hidden += c;
+          }
+          dstamp(ctl, rr, c);
+          peel_round(g, w, k, rr, c, 0, blockDim.x);
+          ++rr;
+          __syncthreads();
+          c = __ldcg(&ctl->qcnt[rr % 3]);
+        }
+        if (threadIdx.x == 0) ctl->n_rounds = rr;
+      }
+      grid.sync();
+      r = __ldcg(&ctl->n_rounds);
+      break;
+    }
     if (tid == 0) {
       ctl->qcnt[(r + 2) % 3] = 0;
       ctl->n_hidden += cnt;
     }
-    const int* cur = (r & 1) ? w.q1 : w.q0;
-    int* nxt = (r & 1) ? w.q0 : w.q1;
-    int* ncnt = &ctl->qcnt[(r + 1) % 3];
-    for (int i0 = blockIdx.x * blockDim.x; i0 < cnt; i0 += nth) {
-      const int i = i0 + threadIdx.x;
-      int items[kAppend];
-      int m = 0;
-      if (i < cnt) {
-        const int v = __ldcg(&cur[i]);
-        const int e1 = g.ce_rp[v + 1];
-        for (int e = g.ce_rp[v]; e < e1; ++e) {
-          const int u = g.ce_col[e];
-          if (__ldcg(&w.hround[u]) != -1) continue;  // already hidden: its degree no longer matters
-          const int old = atomicSub(&w.deg[u], 1);
-          if (old == k && g.se_rp[u + 1] == g.se_rp[u]) {
-            w.hround[u] = r + 1;
-            list_push(items, m, u, ncnt, nxt);
-          }
-        }
-      }
-      cta_append(m, items, ncnt, nxt);
-    }
+    dstamp(ctl, r, cnt);
+    peel_round(g, w, k, r, cnt, blockIdx.x * blockDim.x, nth);
     ++r;
     grid.sync();
     stamp(w.ctl, 2);
@@ -308,6 +349,7 @@ __global__ void __launch_bounds__(1024) mpld_recover(GraphView g, Workspace w, i
   int L = 0;
   while (true) {
     const int cnt = __ldcg(&ctl->rq[L % 3]);
+    dstamp(ctl, 16 + L, cnt);
     if (cnt == 0) break;
     if (tid == 0) ctl->rq[(L + 2) % 3] = 0;
     const int* cur = (L & 1) ? w.q1 : w.q0;

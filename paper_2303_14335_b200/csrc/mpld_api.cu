@@ -33,9 +33,9 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(MPLD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-enum KernelId { K_VALIDATE = 0, K_SIMPLIFY, K_SEARCH, K_RECOVER, K_EVALUATE, K_COUNT };
+enum KernelId { K_VALIDATE = 0, K_SIMPLIFY, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_COUNT };
 const char* kKernelNames[K_COUNT] = {"mpld_validate", "mpld_simplify_components", "mpld_exact_cover_search",
-                                     "mpld_recover", "mpld_evaluate"};
+                                     "mpld_exact_cover_search_heavy", "mpld_recover", "mpld_evaluate"};
 
 constexpr int kCoopThreads = 1024;
 constexpr int kSearchThreads = 128;
@@ -157,7 +157,8 @@ int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, i
   cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
   if (e != cudaSuccess) return cuda_fail(e, "control reset");
   int launches = 0;
-  const int n_launch = 4 + ((flags & MPLD_FLAG_VALIDATE) ? 1 : 0);
+  const bool exact = max_steps <= 0;
+  const int n_launch = 4 + ((flags & MPLD_FLAG_VALIDATE) ? 1 : 0) + (exact ? 1 : 0);
   if (flags & MPLD_FLAG_VALIDATE) {
     TimedLaunch t(ctx, K_VALIDATE, s);
     e = launch_validate(g, ws, s, ctx->blocks_stream);
@@ -176,6 +177,13 @@ int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, i
     TimedLaunch t(ctx, K_SEARCH, s);
     e = launch_search(g, ws, k, w_stitch, max_steps, colors, s, ctx->blocks_search, kSearchThreads);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
+    t.done();
+    ++launches;
+  }
+  if (exact) {
+    TimedLaunch t(ctx, K_SEARCH_HEAVY, s);
+    e = launch_search_heavy(g, ws, k, w_stitch, colors, s, ctx->num_sms * 4);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_heavy");
     t.done();
     ++launches;
   }
@@ -252,6 +260,11 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   ctx->blocks_recover = coop_blocks_recover(kCoopThreads, ctx->num_sms);
   ctx->blocks_search = resident_blocks_search(kSearchThreads, ctx->num_sms);
   ctx->blocks_stream = ctx->num_sms * 8;
+  e = configure_search_heavy();
+  if (e != cudaSuccess) {
+    mpld_context_destroy(ctx);
+    return cuda_fail(e, "configure heavy search");
+  }
   if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_CUDA, "occupancy query failed (kernel image missing for this device?)");
@@ -431,13 +444,17 @@ int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
   Control c;
   cudaError_t e = cudaMemcpy(&c, ctx->ctl, sizeof(Control), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "debug copy");
-  int64_t v[20];
+  int64_t v[84];
   for (int i = 0; i < 16; ++i) v[i] = (int64_t)c.t[i];
+  for (int i = 0; i < 32; ++i) {
+    v[20 + i] = (int64_t)c.tr[i];
+    v[52 + i] = c.nr[i];
+  }
   v[16] = c.n_levels;
   v[17] = c.n_hidden;
   v[18] = c.n_rounds;
   v[19] = c.max_steps_comp;
-  for (int i = 0; i < n && i < 20; ++i) out[i] = v[i];
+  for (int i = 0; i < n && i < 84; ++i) out[i] = v[i];
   return MPLD_OK;
 }
 

@@ -34,10 +34,12 @@ struct Control {
   int qcnt[3];               // simplification frontier sizes (rotating by round)
   int rq[3];                 // recovery level sizes (rotating by level)
   int n_levels;              // recovery levels (DAG depth + 1)
-  int pad;
+  int n_heavy;               // exact mode: components handed to the warp-parallel search
   unsigned long long steps;  // search nodes entered
   unsigned bar[2];           // grid-barrier arrival counters of the two cooperative kernels
   unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
+  unsigned long long tr[32];  // diagnostics: per round / level start time (ns)
+  int nr[32];                // diagnostics: per round / level frontier size
 };
 
 // Grid-wide barrier for the cooperatively launched persistent kernels.  Each
@@ -105,6 +107,9 @@ cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, 
                                        long long* counts, cudaStream_t s, int blocks, int threads);
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
                           int* colors, cudaStream_t s, int blocks, int threads);
+cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
+                                int blocks);
+cudaError_t configure_search_heavy();
 cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, cudaStream_t s,
                            int blocks, int threads);
 cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors, double alpha,

@@ -49,6 +49,8 @@ def run(b, k, alpha, iters=10, flush=None, max_steps=1 << 20):
     print("  phases(us from simplify start): simplify r01/rounds-end/hook:", [rel(i) for i in (0, 1, 3)],
           "search start", rel(14), "recover start", rel(13), "recover level0/levels-end", [rel(i) for i in (8, 9)],
           "evaluate start", rel(15), "levels", int(d[16]), "rounds", int(d[18]))
+    rr = [(i, rel(20 + i), int(d[52 + i])) for i in range(32) if d[20 + i]]
+    print("  rounds/levels (index, us, frontier):", rr)
     st = dict(zip(mp.STAT_NAMES, stats.cpu().tolist()))
     ctx.close()
     return {name: round(1e3 * ms / max(n, 1), 1) for name, (ms, n) in t.items()}, st
@@ -58,6 +60,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--replicas", type=int, nargs="+", default=[1, 4, 16])
     ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--max-steps", type=int, default=0)
     a = ap.parse_args()
     flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda:0")
     for R in a.replicas:
@@ -66,11 +69,11 @@ def main():
             gs, k, alpha = synth.config_graphs(a.config, seed=10 * r)
             graphs += gs
         b = synth.concat(graphs)
-        us, st = run(b, k, alpha, flush=flush)
+        us, st = run(b, k, alpha, flush=flush, max_steps=a.max_steps)
         print(json.dumps({"replicas": R, "layouts": b.n_layouts, "n": b.n, "us_per_launch": us, "stats": st}))
         one = synth.concat(graphs)
         one.layout_offsets = np.array([0, one.n], dtype=np.int32)
-        us, st = run(one, k, alpha, flush=flush)
+        us, st = run(one, k, alpha, flush=flush, max_steps=a.max_steps)
         print(json.dumps({"replicas": R, "layouts": 1, "n": one.n, "us_per_launch": us}))
 
 
