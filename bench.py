@@ -117,44 +117,54 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def kernel_bytes(b):
-    """Algorithmic bytes per launch of each kernel: the CSR it must
-    read once plus the per-vertex outputs it must write once."""
+def kernel_bytes(b, st):
+    """Algorithmic bytes per launch of each HBM-side kernel: the
+    CSR rows it must read once plus the per-vertex words it must write once."""
     n, m_ce, m_se = b.n, b.ce_col.size, b.se_col.size
-    rowptrs = 8 * (n + 1)
+    csr = 8 * (n + 1) + 4 * m_ce + 4 * m_se
     return {
-        "mpld_simplify_components": rowptrs + 4 * m_ce + 4 * m_se + 4 * n,  # CSR + hround
-        "mpld_exact_cover_search": None,  # ALU-bound search (DESIGN.md §5)
-        "mpld_recover": None,
-        "mpld_evaluate": rowptrs + 4 * m_ce + 4 * m_se + 4 * n,  # CSR + colours
-        "mpld_validate": rowptrs + 4 * m_ce + 4 * m_se,
+        "mpld_validate": csr,
+        "mpld_simplify_components": csr + 4 * n,  # CSR + the round of every vertex
+        "mpld_recover": 8 * (n + 1) + 4 * m_ce + 4 * int(st["hidden"]),  # CE rows + colours of hidden vertices
+        "mpld_evaluate": csr + 4 * n,  # CSR + colours
     }
 
 
-def run_cpu_baseline(b, k, alpha, seconds):
+def aggregate(values, ops, world, device):
+    """Whole-job figures: per-rank values reduced with 'sum' (work) or 'max'
+    (device time, the slowest rank) over the process group."""
+    import torch
+    vals = torch.tensor(values, dtype=torch.float64, device=device)
+    if world > 1:
+        import torch.distributed as dist
+        tot, mx = vals.clone(), vals.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        return [(tot if op == "sum" else mx)[i].item() for i, op in enumerate(ops)]
+    return vals.tolist()
+
+
+def cpu_layouts(b):
+    return synth.split(b)
+
+
+def run_cpu_baseline(layouts, k, alpha, seconds):
+    """The oracle as it stands, single-threaded, on the first layouts of the batch
+    until `seconds` of CPU work (bounded sample)."""
     import oracle
-    offs = b.layout_offsets.tolist()
-    graphs = []
-    for li in range(b.n_layouts):
-        a, e = offs[li], offs[li + 1]
-        graphs.append((a, e))
-    comps = layouts = 0
+    comps = done = 0
     t0 = time.perf_counter()
-    names = []
-    for li, (a, e) in enumerate(graphs):
-        sub = synth.from_edges(e - a, b.ce_edges()[(b.ce_edges()[:, 0] >= a) & (b.ce_edges()[:, 0] < e)] - a,
-                               b.se_edges()[(b.se_edges()[:, 0] >= a) & (b.se_edges()[:, 0] < e)] - a)
-        r = oracle.decompose(sub, k, alpha, max_steps=MAX_STEPS, check=False)
+    for g in layouts:
+        r = oracle.decompose(g, k, alpha, max_steps=MAX_STEPS, check=False)
         comps += len(r["components"])
-        layouts += 1
-        names.append(li)
+        done += 1
         if time.perf_counter() - t0 > seconds:
             break
     dt = time.perf_counter() - t0
     return {"value": comps / dt, "unit": METRIC, "cores": 1, "kind": "oracle",
-            "sample": f"first {layouts} layouts of the rank-0 batch ({comps} components, {dt:.1f} s, "
-                      f"single-threaded CPython oracle/mpld.py incl. simplification and recovery)",
-            "ms_per_layout": 1e3 * dt / layouts}
+            "sample": f"first {done} layouts of the rank-0 batch ({comps} components, {dt:.1f} s, "
+                      f"single-threaded CPython oracle/ incl. simplification and recovery)",
+            "ms_per_layout": 1e3 * dt / done}
 
 
 def main_reference(args):
@@ -163,15 +173,8 @@ def main_reference(args):
         return
     b, k, alpha = workload(0, args.replicas)
     import oracle
-    offs = b.layout_offsets.tolist()
-    ce_all, se_all = b.ce_edges(), b.se_edges()
-    subs = []
-    for li in range(b.n_layouts):
-        a, e = offs[li], offs[li + 1]
-        subs.append(synth.from_edges(e - a, ce_all[(ce_all[:, 0] >= a) & (ce_all[:, 0] < e)] - a,
-                                     se_all[(se_all[:, 0] >= a) & (se_all[:, 0] < e)] - a))
-    # each step: a bounded sample (one ISCAS-85 suite = 10 layouts, about 1 s of CPU work)
-    per_step = subs[:10]
+    # each step: a bounded sample of the workload (one ISCAS-85 suite = 10 layouts, ~1 s of CPU work)
+    per_step = cpu_layouts(b)[:10]
     for _ in range(args.warmup):
         for g in per_step[:2]:
             oracle.decompose(g, k, alpha, max_steps=MAX_STEPS, check=False)
@@ -189,7 +192,7 @@ def main_reference(args):
            "config": config_dict(b, args.replicas, args.gpus,
                                  {"reference_sample": "one ISCAS-85 suite (10 layouts) per step"}),
            "cpu_baseline": {"value": val, "unit": METRIC, "cores": 1, "kind": "oracle",
-                            "sample": "10 layouts (c432..c7552, seed 0..9) per step, CPython oracle"},
+                            "sample": "10 layouts (c432..c7552, first suite of the batch) per step, CPython oracle"},
            "e2e": {"value": val, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -286,17 +289,9 @@ def main():
     d2h = b.n * 4 + L * 8 * 3 + 8 * len(mp.STAT_NAMES)
 
     # aggregate over ranks
-    vec = torch.tensor([comps_per_step * args.steps, total_ms, comps_per_step * e2e_steps, e2e_s * 1e3, L],
-                       dtype=torch.float64, device=dev)
-    if world > 1:
-        tot = vec.clone()
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        mx = vec.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        comps_all, ms_max, e2e_comps_all, e2e_ms_max, layouts_all = tot[0].item(), mx[1].item(), tot[2].item(), \
-            mx[3].item(), tot[4].item()
-    else:
-        comps_all, ms_max, e2e_comps_all, e2e_ms_max, layouts_all = vec.tolist()
+    comps_all, ms_max, e2e_comps_all, e2e_ms_max, layouts_all = aggregate(
+        [comps_per_step * args.steps, total_ms, comps_per_step * e2e_steps, e2e_s * 1e3, L],
+        ["sum", "max", "sum", "max", "sum"], world, dev)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -305,10 +300,8 @@ def main():
     value = comps_all / (ms_max / 1e3)
     ms_per_step = ms_max / args.steps
     # roofline of the dominant kernel
-    kb = kernel_bytes(b)
-    dom = max(ktimes.items(), key=lambda kv: kv[1][0])
-    dom_name, (dom_ms, dom_n) = dom
-    peaks = {}
+    kb = kernel_bytes(b, st)
+    dom_name, (dom_ms, dom_n) = max(ktimes.items(), key=lambda kv: kv[1][0])
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
@@ -318,13 +311,12 @@ def main():
         achieved = kb[dom_name] / (dom_ms / dom_n / 1e3) / 1e9
         roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": kb[dom_name]}
+                "algorithmic_bytes_per_launch": kb[dom_name],
+                "note": "dependency-latency bound in practice (one grid barrier per level), DESIGN.md §5"}
     else:
-        sm_clock = 1965.0
-        # ALU roofline: 148 SMs x 4 SMSPs x 1 warp-instruction/clk at sm_max
-        nodes = st["steps"]
-        achieved = nodes / (dom_ms / dom_n / 1e3) / 1e9
-        peak_nodes = 148 * 4 * 32 * sm_clock * 1e6 / 60.0 / 1e9  # 60 thread-instructions per node
+        # ALU roofline: 148 SMs x 4 SMSPs x 32 lanes x 1 instr/clk at sm_max, 60 instr per node
+        achieved = st["steps"] / (dom_ms / dom_n / 1e3) / 1e9
+        peak_nodes = 148 * 4 * 32 * 1965e6 / 60.0 / 1e9
         roof = {"kernel": dom_name, "bound": "alu", "achieved": achieved, "peak": peak_nodes,
                 "unit": "Gnodes/s", "frac": achieved / peak_nodes, "traffic": None,
                 "peak_source": "148 SM x 4 SMSP x 32 lanes x 1.965 GHz / 60 instr per node (DESIGN.md §5)"}
@@ -344,7 +336,7 @@ def main():
            "clocks": clk.summary(),
            "stats": st}
     if not args.no_cpu_baseline:
-        out["cpu_baseline"] = run_cpu_baseline(b, k, alpha, args.cpu_seconds)
+        out["cpu_baseline"] = run_cpu_baseline(cpu_layouts(b), k, alpha, args.cpu_seconds)
     print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

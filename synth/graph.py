@@ -95,6 +95,20 @@ def from_edges(n: int, ce_edges, se_edges=(), name: str = "") -> DecompGraph:
     return DecompGraph(n, cr, cc, sr, sc, name=name)
 
 
+def split(b: DecompGraph):
+    """Inverse of concat: the layouts of a batch as separate DecompGraphs."""
+    offs = b.layout_offsets.tolist()
+    out = []
+    for li in range(len(offs) - 1):
+        a, e = offs[li], offs[li + 1]
+        cr = b.ce_rowptr[a:e + 1].astype(np.int64)
+        sr = b.se_rowptr[a:e + 1].astype(np.int64)
+        out.append(DecompGraph(e - a, (cr - cr[0]).astype(np.int32), (b.ce_col[cr[0]:cr[-1]] - a).astype(np.int32),
+                               (sr - sr[0]).astype(np.int32), (b.se_col[sr[0]:sr[-1]] - a).astype(np.int32),
+                               name=f"{b.name}[{li}]"))
+    return out
+
+
 def concat(graphs, name: str = "batch") -> DecompGraph:
     """Disjoint union of several layouts (vertex ids offset), keeping layout boundaries."""
     offs = [0]
