@@ -15,7 +15,7 @@ namespace mpld {
 namespace {
 
 constexpr int kAppend = 8;   // items one thread may append per call before spilling to direct atomics
-constexpr int kTail = 4096;  // frontiers up to this size are finished by a single CTA
+constexpr int kTail = 1024;  // frontiers up to one item per thread of a CTA are finished by that CTA alone
 
 __device__ __forceinline__ bool row_contains(const int* __restrict__ col, int a, int b, int x) {
   // binary search in the strictly ascending row col[a..b)
@@ -53,6 +53,13 @@ __device__ __forceinline__ void dstamp(Control* ctl, int i, int cnt) {
     ctl->tr[i] = t;
     ctl->nr[i] = cnt;
   }
+}
+
+// Recovery pop-order key (R9): kept vertices (coloured by the search) sort above
+// every hidden vertex; hidden ones by (round, priority) — u is popped before v
+// iff key(u) > key(v).
+__device__ __forceinline__ unsigned long long pop_key(int h, uint32_t p) {
+  return h < 0 ? ~0ull : (((unsigned long long)(h + 1) << 32) | p);
 }
 
 // Block-wide append: thread i contributes cnt_i items; the CTA reserves its
@@ -290,6 +297,7 @@ __global__ void __launch_bounds__(1024) mpld_simplify_components(GraphView g, Wo
   for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += nth) {
     const int v = v0 + threadIdx.x;
     int is_root = 0;
+    if (v < n) w.key[v] = pop_key(__ldcg(&w.hround[v]), w.prio[v]);
     if (v < n && __ldcg(&w.hround[v]) == -1) {
       const int root = find_root(w.parent, v);
       w.parent[v] = root;
@@ -313,8 +321,36 @@ __global__ void __launch_bounds__(1024) mpld_simplify_components(GraphView g, Wo
 // predecessor; a vertex joins the next level when its last predecessor is
 // coloured.  Every level is coloured in parallel, one grid barrier per level
 // (DAG depth ~ 10-20 on layout graphs); the result equals the sequential pop.
-__device__ __forceinline__ bool popped_before(int hu, uint32_t pu, int hv, uint32_t pv) {
-  return hu > hv || (hu == hv && pu > pv);
+// One recovery level: colour the ready vertices cur[first..cnt) (stride),
+// queue the successors whose last predecessor this was.
+__device__ void recover_level(const GraphView& g, const Workspace& w, int k, int* colors, int L, int cnt, int first,
+                              int stride) {
+  Control* ctl = w.ctl;
+  const int* cur = (L & 1) ? w.q1 : w.q0;
+  int* nxt = (L & 1) ? w.q0 : w.q1;
+  int* ncnt = &ctl->rq[(L + 1) % 3];
+  for (int i0 = first; i0 < cnt; i0 += stride) {
+    const int i = i0 + threadIdx.x;
+    int items[kAppend];
+    int m = 0;
+    if (i < cnt) {
+      const int v = __ldcg(&cur[i]);
+      const unsigned long long kv = w.key[v];
+      unsigned used = 0;
+      for (int e = g.ce_rp[v], e1 = g.ce_rp[v + 1]; e < e1; ++e) {
+        const int u = g.ce_col[e];
+        if (w.key[u] > kv) {  // popped before v (or kept): coloured
+          const int cu = __ldcg(&colors[u]);
+          if (cu >= 0) used |= 1u << cu;
+        } else if (atomicSub(&w.deg[u], 1) == 1) {  // v was u's last predecessor
+          list_push(items, m, u, ncnt, nxt);
+        }
+      }
+      const int c = __ffs(~used) - 1;
+      colors[v] = c < k ? c : 0;  // c < k by the simplification invariant
+    }
+    cta_append(m, items, ncnt, nxt);
+  }
 }
 
 __global__ void __launch_bounds__(1024) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
@@ -328,14 +364,12 @@ __global__ void __launch_bounds__(1024) mpld_recover(GraphView g, Workspace w, i
     const int v = v0 + threadIdx.x;
     int ready = 0;
     if (v < g.n) {
-      const int hv = w.hround[v];
-      if (hv >= 0) {
-        const uint32_t pv = w.prio[v];
+      const unsigned long long kv = w.key[v];
+      if (kv != ~0ull) {
         int cnt = 0;
         for (int e = g.ce_rp[v], e1 = g.ce_rp[v + 1]; e < e1; ++e) {
-          const int u = g.ce_col[e];
-          const int hu = w.hround[u];
-          if (hu >= 0 && popped_before(hu, w.prio[u], hv, pv)) ++cnt;
+          const unsigned long long ku = w.key[g.ce_col[e]];
+          cnt += (ku > kv && ku != ~0ull) ? 1 : 0;
         }
         w.deg[v] = cnt;
         ready = cnt == 0;
@@ -350,41 +384,30 @@ __global__ void __launch_bounds__(1024) mpld_recover(GraphView g, Workspace w, i
   while (true) {
     const int cnt = __ldcg(&ctl->rq[L % 3]);
     dstamp(ctl, 16 + L, cnt);
-    if (cnt == 0) break;
-    if (tid == 0) ctl->rq[(L + 2) % 3] = 0;
-    const int* cur = (L & 1) ? w.q1 : w.q0;
-    int* nxt = (L & 1) ? w.q0 : w.q1;
-    int* ncnt = &ctl->rq[(L + 1) % 3];
-    for (int i0 = blockIdx.x * blockDim.x; i0 < cnt; i0 += nth) {
-      const int i = i0 + threadIdx.x;
-      int items[kAppend];
-      int m = 0;
-      if (i < cnt) {
-        const int v = __ldcg(&cur[i]);
-        const int hv = w.hround[v];
-        const uint32_t pv = w.prio[v];
-        const int e0 = g.ce_rp[v], e1 = g.ce_rp[v + 1];
-        unsigned used = 0;
-        for (int e = e0; e < e1; ++e) {
-          const int u = g.ce_col[e];
-          const int hu = w.hround[u];
-          if (hu == -1 || popped_before(hu, w.prio[u], hv, pv)) {
-            const int cu = __ldcg(&colors[u]);
-            if (cu >= 0) used |= 1u << cu;
-          } else if (atomicSub(&w.deg[u], 1) == 1) {  // v was u's last predecessor
-            list_push(items, m, u, ncnt, nxt);
-          }
-        }
-        const int c = __ffs(~used) - 1;
-        colors[v] = c < k ? c : 0;  // c < k by the simplification invariant
-      }
-      cta_append(m, items, ncnt, nxt);
+    if (cnt == 0) {
+      if (tid == 0) ctl->n_levels = L;
+      break;
     }
+    if (cnt <= kTail) {  // small level: CTA 0 finishes the remaining levels with block barriers
+      if (blockIdx.x == 0) {
+        int LL = L, c = cnt;
+        while (c > 0) {
+          if (threadIdx.x == 0) ctl->rq[(LL + 2) % 3] = 0;
+          recover_level(g, w, k, colors, LL, c, 0, blockDim.x);
+          ++LL;
+          __syncthreads();
+          c = __ldcg(&ctl->rq[LL % 3]);
+        }
+        if (threadIdx.x == 0) ctl->n_levels = LL;
+      }
+      break;  // no grid barrier needed: the kernel ends here
+    }
+    if (tid == 0) ctl->rq[(L + 2) % 3] = 0;
+    recover_level(g, w, k, colors, L, cnt, blockIdx.x * blockDim.x, nth);
     ++L;
     grid.sync();
     stamp(w.ctl, 9);
   }
-  if (tid == 0) ctl->n_levels = L;
 }
 
 // ---------------------------------------------------------------------------

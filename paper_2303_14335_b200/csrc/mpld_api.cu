@@ -51,6 +51,7 @@ struct mpld_context {
   int* deg = nullptr;
   int* hround = nullptr;
   unsigned* prio = nullptr;
+  unsigned long long* key = nullptr;
   int* q0 = nullptr;
   int* q1 = nullptr;
   int* parent = nullptr;
@@ -96,7 +97,8 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
       e = grow(p, cap);
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
-    if (grow(&ctx->prio, cap) != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
+    if (grow(&ctx->prio, cap) != cudaSuccess || grow(&ctx->key, cap) != cudaSuccess)
+      return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     ctx->cap_n = cap;
   }
   if (n_layouts > ctx->cap_layouts) {
@@ -152,7 +154,7 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
                  long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost,
                  long long* stats) {
-  Workspace ws{ctx->deg, ctx->hround, ctx->prio, ctx->q0, ctx->q1, ctx->parent, ctx->loc, ctx->roots, ctx->ctl};
+  Workspace ws{ctx->deg, ctx->hround, ctx->key, ctx->prio, ctx->q0, ctx->q1, ctx->parent, ctx->loc, ctx->roots, ctx->ctl};
   // the control block (counters, barrier arrivals, error bits) starts every call at zero
   cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
   if (e != cudaSuccess) return cuda_fail(e, "control reset");
@@ -285,7 +287,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
 
 void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
-  for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
+  for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->key, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->parent, (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->ctl, (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
                   (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})

@@ -81,6 +81,7 @@ struct GraphView {
 struct Workspace {
   int* deg;        // live conflict degree (simplification), then hidden-predecessor count (recovery)
   int* hround;     // -1 kept, else the round the vertex was hidden in
+  unsigned long long* key;  // recovery pop-order key (round, priority); ~0 for kept vertices
   unsigned* prio;  // lowbias32(layout-local id), recovery priority (R9)
   int* q0;         // frontier queues (double-buffered)
   int* q1;
