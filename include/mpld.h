@@ -153,7 +153,8 @@ int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* laun
  * %globaltimer stamps (ns) at phase boundaries, out[16] recovery levels
  * (depth of the pop-order DAG + 1), out[17] hidden vertices, out[18] rounds,
  * out[19] largest per-component step count, out[20..51] per round (0..15) / recovery
- * level (16..31) start stamps, out[52..83] their frontier sizes.  Copies min(n, 84). */
+ * level (16..31) start stamps, out[52..83] their frontier sizes, out[84..91]
+ * slowest search thread (cycles total, build, search; n; steps).  Copies min(n, 92). */
 int mpld_context_debug(mpld_context* ctx, int64_t* out, int n);
 
 #ifdef __cplusplus

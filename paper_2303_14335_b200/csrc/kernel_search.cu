@@ -60,8 +60,6 @@ struct WordOps<unsigned long long> {
 template <typename W>
 struct __align__(16) Frame {
   W saved;     // B[c] before r(v,c) was selected
-  W adj;       // adj[v]
-  W sadj;      // sadj[v]
   int cost;    // cost when the node was entered
   int packed;  // v | (c+1) << 8 | (maxused+1) << 16
 };
@@ -137,12 +135,14 @@ struct ParIncumbent {
 };
 
 // Relaxed Algorithm X with branch and bound (R4-R7) from the node
-// (C, B, U, cost, maxused).  am_adj[i] / am_sadj[i] = masks of local vertex i.
-// Returns the nodes entered; the best leaf's masks in bestC.
+// (C, B, U, cost, maxused).  am_adj[i*as] / am_sadj[i*as] = masks of local
+// vertex i; stack[d*ss] = frame of depth d (strides let a warp interleave its
+// lanes' arrays in shared memory).  Returns the nodes entered; the best
+// leaf's masks in bestC.
 template <int K, typename W, typename Inc>
-__device__ unsigned dfs(const W* __restrict__ am_adj, const W* __restrict__ am_sadj, W (&C)[K], W (&B)[K], W U,
-                        int cost, int maxused, int w_stitch, unsigned max_steps, Frame<W>* __restrict__ stack,
-                        Inc& inc, W (&bestC)[K], bool& truncated) {
+__device__ unsigned dfs(const W* __restrict__ am_adj, const W* __restrict__ am_sadj, int as, W (&C)[K], W (&B)[K],
+                        W U, int cost, int maxused, int w_stitch, unsigned max_steps,
+                        Frame<W>* __restrict__ stack, int ss, Inc& inc, W (&bestC)[K], bool& truncated) {
   using O = WordOps<W>;
   int depth = 0;
   unsigned steps = 0;
@@ -170,18 +170,16 @@ __device__ unsigned dfs(const W* __restrict__ am_adj, const W* __restrict__ am_s
           if (depth > 0) {  // spill the parent frame
             Frame<W> f;
             f.saved = f_saved;
-            f.adj = f_adj;
-            f.sadj = f_sadj;
             f.cost = f_cost;
             f.packed = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16);
-            stack[depth - 1] = f;
+            stack[(depth - 1) * ss] = f;
           }
           f_v = v;
           f_c = -1;
           f_mu = maxused;
           f_cost = cost;
-          f_adj = am_adj[v];
-          f_sadj = am_sadj[v];
+          f_adj = am_adj[v * as];
+          f_sadj = am_sadj[v * as];
           U &= ~(W(1) << v);  // cover column v (line 9)
           ++depth;
         }
@@ -198,14 +196,14 @@ __device__ unsigned dfs(const W* __restrict__ am_adj, const W* __restrict__ am_s
       U |= bit;
       --depth;
       if (depth > 0) {
-        const Frame<W> f = stack[depth - 1];
+        const Frame<W> f = stack[(depth - 1) * ss];
         f_saved = f.saved;
-        f_adj = f.adj;
-        f_sadj = f.sadj;
         f_cost = f.cost;
         f_v = f.packed & 0xff;
         f_c = ((f.packed >> 8) & 0xff) - 1;
         f_mu = ((f.packed >> 16) & 0xff) - 1;
+        f_adj = am_adj[f_v * as];
+        f_sadj = am_sadj[f_v * as];
       }
       enter = false;
       continue;
@@ -232,28 +230,81 @@ __device__ __forceinline__ int colour_of(const W (&bestC)[K], int i) {
   return c;
 }
 
+// Per-lane search storage of the thread-per-component kernel: one warp per
+// CTA, arrays lane-interleaved in shared memory (element i of lane l at
+// i * 32 + l) so the search never touches local memory.
+constexpr int kLightSmem = 2 * kMaxComp * 32 * 8 + kMaxComp * 32 * 16;
+
 template <int K, typename W>
 __device__ unsigned run_light(const unsigned long long* adjm, const unsigned long long* sadjm, int n, int w_stitch,
-                              unsigned budget, Frame<W>* stack, int* cval, int& best_cost, bool& trunc) {
-  W a[kMaxComp], s[kMaxComp];
+                              unsigned budget, unsigned char* smem, int* cval, int& best_cost, bool& trunc) {
+  const int lane = threadIdx.x & 31;
+  W* a = (W*)smem + lane;
+  W* s = a + kMaxComp * 32;
+  Frame<W>* stack = (Frame<W>*)(smem + 2 * kMaxComp * 32 * 8) + lane;
   for (int i = 0; i < n; ++i) {
-    a[i] = (W)adjm[i];
-    s[i] = (W)sadjm[i];
+    a[i * 32] = (W)adjm[i];
+    s[i * 32] = (W)sadjm[i];
   }
   W C[K], B[K], bestC[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) C[c] = B[c] = bestC[c] = 0;
   SeqIncumbent inc;
-  const unsigned steps =
-      dfs<K, W, SeqIncumbent>(a, s, C, B, WordOps<W>::full(n), 0, -1, w_stitch, budget, stack, inc, bestC, trunc);
+  const unsigned steps = dfs<K, W, SeqIncumbent>(a, s, 32, C, B, WordOps<W>::full(n), 0, -1, w_stitch, budget,
+                                                 stack, 32, inc, bestC, trunc);
   for (int i = 0; i < n; ++i) cval[i] = colour_of<K, W>(bestC, i);
   best_cost = inc.best;
   return steps;
 }
 
+// The component's bit-packed matrix: BFS from the root (column order = BFS
+// order of G, neighbours over CE ∪ SE in ascending id, R5).  Every head's
+// neighbours are handled in batches whose global loads (ids, rounds, local
+// indices) are independent and in flight together, so a head costs a few
+// memory round trips instead of two per neighbour.  ASSIGN: discover vertices
+// and write loc[]; otherwise loc[] already holds the BFS positions (rebuild).
+// Returns n, or -1 when the component exceeds kMaxComp.
+template <bool ASSIGN>
+__device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* order, unsigned long long* adjm,
+                         unsigned long long* sadjm) {
+  int n = 1;
+  order[0] = root;
+  if (ASSIGN) w.loc[root] = 0;
+  for (int head = 0; head < n; ++head) {
+    const int v = order[head];
+    unsigned long long adj = 0ull, sadj = 0ull;
+    int a = g.ce_rp[v], b = g.se_rp[v];
+    const int ae = g.ce_rp[v + 1], be = g.se_rp[v + 1];
+    while (a < ae || b < be) {  // merge the two ascending rows
+      int u;
+      bool is_ce;
+      if (b >= be || (a < ae && g.ce_col[a] < g.se_col[b])) { u = g.ce_col[a++]; is_ce = true; }
+      else { u = g.se_col[b++]; is_ce = false; }
+      if (w.hround[u] != -1) continue;
+      int lu = w.loc[u];
+      if (ASSIGN) {
+        if (lu < 0) {
+          if (n == kMaxComp) return -1;
+          lu = n;
+          w.loc[u] = n;
+          order[n++] = u;
+        }
+      } else {
+        order[lu] = u;  // seen before the BFS head reaches its position
+        n = max(n, lu + 1);
+      }
+      if (is_ce) adj |= 1ull << lu; else sadj |= 1ull << lu;
+    }
+    adjm[head] = adj;
+    sadjm[head] = sadj;
+  }
+  return n;
+}
+
 template <int K>
-__global__ void __launch_bounds__(128) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
-                                                               long long max_steps, int* colors) {
+__global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
+                                                              long long max_steps, int* colors) {
+  extern __shared__ __align__(16) unsigned char lsmem[];
   Control* ctl = w.ctl;
   const int n_comp = __ldcg(&ctl->n_comp);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -266,43 +317,14 @@ __global__ void __launch_bounds__(128) mpld_exact_cover_search(GraphView g, Work
                                 : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
   int order[kMaxComp];
   unsigned long long adjm[kMaxComp], sadjm[kMaxComp];
-  union {
-    Frame<unsigned> f32[32];
-    Frame<unsigned long long> f64[kMaxComp];
-  } stack;
+  unsigned long long acc_steps = 0ull;
+  int acc_maxn = 0, acc_maxsteps = 0;
+  unsigned acc_trunc = 0;
   for (int ci = blockIdx.x * blockDim.x + threadIdx.x; ci < n_comp; ci += gridDim.x * blockDim.x) {
+    const long long c0 = clock64();
     const int root = w.roots[ci];
-    // build the component's bit-packed matrix: BFS from the root (column order
-    // = BFS order of G, neighbours in ascending id, R5)
-    int n = 1, head = 0;
-    bool too_big = false;
-    order[0] = root;
-    w.loc[root] = 0;
-    while (head < n) {
-      const int v = order[head];
-      unsigned long long adj = 0ull, sadj = 0ull;
-      int a = g.ce_rp[v], ae = g.ce_rp[v + 1], b = g.se_rp[v], be = g.se_rp[v + 1];
-      while (a < ae || b < be) {
-        int u;
-        bool is_ce;
-        if (b >= be || (a < ae && g.ce_col[a] < g.se_col[b])) { u = g.ce_col[a++]; is_ce = true; }
-        else { u = g.se_col[b++]; is_ce = false; }
-        if (w.hround[u] != -1) continue;
-        int lu = w.loc[u];
-        if (lu < 0) {
-          if (n == kMaxComp) { too_big = true; break; }
-          lu = n;
-          w.loc[u] = n;
-          order[n++] = u;
-        }
-        if (is_ce) adj |= 1ull << lu; else sadj |= 1ull << lu;
-      }
-      if (too_big) break;
-      adjm[head] = adj;
-      sadjm[head] = sadj;
-      ++head;
-    }
-    if (too_big) {
+    const int n = bfs_build<true>(g, w, root, order, adjm, sadjm);
+    if (n < 0) {
       atomicOr(&ctl->err, kErrComponent);
       atomicMax(&ctl->max_comp, kMaxComp + 1);
       continue;
@@ -311,21 +333,43 @@ __global__ void __launch_bounds__(128) mpld_exact_cover_search(GraphView g, Work
     bool trunc;
     int best_cost;
     int cval[kMaxComp];
+    const long long c1 = clock64();
     if (n <= 32)
-      steps = run_light<K, unsigned>(adjm, sadjm, n, w_stitch, budget, stack.f32, cval, best_cost, trunc);
+      steps = run_light<K, unsigned>(adjm, sadjm, n, w_stitch, budget, lsmem, cval, best_cost, trunc);
     else
-      steps = run_light<K, unsigned long long>(adjm, sadjm, n, w_stitch, budget, stack.f64, cval, best_cost, trunc);
+      steps = run_light<K, unsigned long long>(adjm, sadjm, n, w_stitch, budget, lsmem, cval, best_cost, trunc);
+    const long long c2 = clock64();
+    if ((unsigned long long)(c2 - c0) > ctl->dbg[0]) {  // diagnostics (racy by design)
+      atomicMax(&ctl->dbg[0], (unsigned long long)(c2 - c0));
+      ctl->dbg[1] = c1 - c0;
+      ctl->dbg[2] = c2 - c1;
+      ctl->dbg[3] = n;
+      ctl->dbg[4] = steps;
+    }
     for (int i = 0; i < n; ++i) colors[order[i]] = cval[i];
-    atomicAdd(&ctl->steps, (unsigned long long)steps);
-    atomicMax(&ctl->max_comp, n);
+    acc_steps += steps;
+    acc_maxn = max(acc_maxn, n);
     if (trunc && exact) {  // hand the component to the warp-parallel search
       const int h = atomicAdd(&ctl->n_heavy, 1);
       w.q0[h] = root;
       w.q1[h] = best_cost;
     } else {
-      atomicMax(&ctl->max_steps_comp, (int)min(steps, (unsigned)INT_MAX));
-      if (trunc) atomicAdd(&ctl->truncated, 1);
+      acc_maxsteps = max(acc_maxsteps, (int)min(steps, (unsigned)INT_MAX));
+      acc_trunc += trunc ? 1 : 0;
     }
+  }
+  // statistics: one atomic per warp (thousands of threads hitting one address
+  // serialise at the L2)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc_steps += __shfl_xor_sync(0xffffffffu, acc_steps, o);
+  acc_maxn = __reduce_max_sync(0xffffffffu, acc_maxn);
+  acc_maxsteps = __reduce_max_sync(0xffffffffu, acc_maxsteps);
+  acc_trunc = __reduce_add_sync(0xffffffffu, acc_trunc);
+  if ((threadIdx.x & 31) == 0 && acc_maxn > 0) {
+    atomicAdd(&ctl->steps, acc_steps);
+    atomicMax(&ctl->max_comp, acc_maxn);
+    atomicMax(&ctl->max_steps_comp, acc_maxsteps);
+    if (acc_trunc) atomicAdd(&ctl->truncated, (int)acc_trunc);
   }
 }
 
@@ -448,7 +492,8 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     __syncwarp();
   }
   // lanes search the subtrees in DFS order with a shared incumbent
-  Frame<W> stack[kMaxComp];
+  Frame<W>* stack = (Frame<W>*)(smem + 2 * kMaxComp * sizeof(unsigned long long) +
+                                2 * kCap * sizeof(Node<MPLD_MAX_K, unsigned long long>)) + lane;
   W bestC[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) bestC[c] = 0;
@@ -463,8 +508,8 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     inc.fkey = (unsigned long long)(f + 1);
     inc.lane_best = my_best;
     bool trunc;
-    steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, nd.C, nd.B, nd.U, nd.cost, nd.mu, w_stitch, UINT_MAX, stack,
-                                     inc, bestC, trunc);
+    steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, 1, nd.C, nd.B, nd.U, nd.cost, nd.mu, w_stitch, UINT_MAX,
+                                     stack, 32, inc, bestC, trunc);
     my_best = inc.lane_best;
   }
   const unsigned long long win = warp_min_u64(my_best);
@@ -493,31 +538,8 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
   for (int h = blockIdx.x; h < n_heavy; h += gridDim.x) {
     const int root = __ldcg(&w.q0[h]);
     const int c1 = __ldcg(&w.q1[h]);
-    if (threadIdx.x == 0) {
-      // rebuild the matrix: loc[] already holds every vertex's BFS index
-      int n = 1, head = 0;
-      s_order[0] = root;
-      while (head < n) {
-        const int v = s_order[head];
-        unsigned long long adj = 0ull, sadj = 0ull;
-        for (int pass = 0; pass < 2; ++pass) {
-          const int* rp = pass ? g.se_rp : g.ce_rp;
-          const int* col = pass ? g.se_col : g.ce_col;
-          for (int e = rp[v], e1 = rp[v + 1]; e < e1; ++e) {
-            const int u = col[e];
-            if (w.hround[u] != -1) continue;
-            const int lu = w.loc[u];
-            s_order[lu] = u;  // every vertex is seen before the BFS head reaches its index
-            n = max(n, lu + 1);
-            if (pass) sadj |= 1ull << lu; else adj |= 1ull << lu;
-          }
-        }
-        s_adj64[head] = adj;
-        s_sadj64[head] = sadj;
-        ++head;
-      }
-      s_n = n;
-    }
+    // rebuild the matrix: loc[] already holds every vertex's BFS position
+    if (threadIdx.x == 0) s_n = bfs_build<false>(g, w, root, s_order, s_adj64, s_sadj64);
     __syncwarp();
     const int n = s_n;
     if (n <= 32)
@@ -533,16 +555,17 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
                           cudaStream_t s, int blocks, int threads) {
   switch (k) {
-    case 2: mpld_exact_cover_search<2><<<blocks, threads, 0, s>>>(g, ws, w_stitch, max_steps, colors); break;
-    case 3: mpld_exact_cover_search<3><<<blocks, threads, 0, s>>>(g, ws, w_stitch, max_steps, colors); break;
-    case 4: mpld_exact_cover_search<4><<<blocks, threads, 0, s>>>(g, ws, w_stitch, max_steps, colors); break;
+    case 2: mpld_exact_cover_search<2><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, colors); break;
+    case 3: mpld_exact_cover_search<3><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, colors); break;
+    case 4: mpld_exact_cover_search<4><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, colors); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
 size_t heavy_smem_bytes() {
-  return 2 * kMaxComp * sizeof(unsigned long long) + 2 * kCap * sizeof(Node<MPLD_MAX_K, unsigned long long>);
+  return 2 * kMaxComp * sizeof(unsigned long long) + 2 * kCap * sizeof(Node<MPLD_MAX_K, unsigned long long>) +
+         kMaxComp * 32 * sizeof(Frame<unsigned long long>);
 }
 
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
@@ -559,17 +582,26 @@ cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_s
 
 cudaError_t configure_search_heavy() {
   const int smem = (int)heavy_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaSuccess;
+  e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(mpld_exact_cover_search<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLightSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(mpld_exact_cover_search<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLightSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(mpld_exact_cover_search<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLightSmem);
   return e;
 }
 
 int resident_blocks_search(int threads, int num_sms) {
+  (void)threads;
+  cudaFuncSetAttribute(mpld_exact_cover_search<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLightSmem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4>, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4>, 32, kLightSmem);
   return per_sm * num_sms;
 }
 

@@ -40,6 +40,7 @@ struct Control {
   unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
   unsigned long long tr[32];  // diagnostics: per round / level start time (ns)
   int nr[32];                // diagnostics: per round / level frontier size
+  unsigned long long dbg[8];  // diagnostics: slowest search thread (cycles total/build/search, n, steps)
 };
 
 // Grid-wide barrier for the cooperatively launched persistent kernels.  Each

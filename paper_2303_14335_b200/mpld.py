@@ -189,8 +189,8 @@ class Context:
 
     def debug(self):
         """Diagnostics of the last call (include/mpld.h mpld_context_debug)."""
-        out = np.zeros(84, dtype=np.int64)
-        _check(lib().mpld_context_debug(self._h, out.ctypes.data, 84))
+        out = np.zeros(92, dtype=np.int64)
+        _check(lib().mpld_context_debug(self._h, out.ctypes.data, 92))
         return out
 
     def kernel_times(self):
