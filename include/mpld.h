@@ -37,7 +37,13 @@
  *   max_steps    search budget per component (R7): once a complete
  *                colouring exists and a component's search has entered more
  *                than max_steps nodes, its search stops with the best colouring
- *                found so far (counted in MPLD_STAT_TRUNCATED).  <= 0: no limit.
+ *                found so far (counted in MPLD_STAT_TRUNCATED); the node order is
+ *                the sequential one of R5-R7, so truncated results are still
+ *                reproducible.  <= 0: exact mode — no budget; components whose
+ *                thread-level search needs more than 96 nodes are finished by a
+ *                warp-parallel search that returns the same first optimal leaf
+ *                (R7).  A safety cap of 2^22 nodes per lane bounds exact mode;
+ *                components hitting it are counted in MPLD_STAT_TRUNCATED.
  *
  * Outputs:
  *   colors       [n] mask of every vertex, in [0, k).

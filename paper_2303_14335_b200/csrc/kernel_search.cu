@@ -40,6 +40,7 @@ namespace {
 constexpr unsigned kLightSteps = 96;  // exact mode: thread-level budget before a component turns heavy
 constexpr int kTarget = 96;           // heavy: frontier size that stops the level-synchronous split
 constexpr int kCap = 192;             // heavy: frontier capacity per level buffer
+constexpr unsigned kHeavyLaneCap = 1u << 22;  // exact mode safety cap: search nodes per lane per component
 
 template <typename W>
 struct WordOps;
@@ -499,19 +500,26 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
   for (int c = 0; c < K; ++c) bestC[c] = 0;
   unsigned long long my_best = ~0ull;
   unsigned steps = 0;
+  bool capped = false;
   while (true) {
     const int f = atomicAdd(&s_next, 1);
     if (f >= m) break;
+    if (steps >= kHeavyLaneCap) {  // safety cap of exact mode: skip, flag as truncated
+      capped = true;
+      continue;
+    }
     Node<K, W> nd = lvl[cur][f];
     ParIncumbent inc;
     inc.shared_best = &s_best;
     inc.fkey = (unsigned long long)(f + 1);
     inc.lane_best = my_best;
     bool trunc;
-    steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, 1, nd.C, nd.B, nd.U, nd.cost, nd.mu, w_stitch, UINT_MAX,
-                                     stack, 32, inc, bestC, trunc);
+    steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, 1, nd.C, nd.B, nd.U, nd.cost, nd.mu, w_stitch,
+                                     kHeavyLaneCap - steps, stack, 32, inc, bestC, trunc);
     my_best = inc.lane_best;
+    capped |= trunc;
   }
+  const bool any_capped = __any_sync(0xffffffffu, capped);
   const unsigned long long win = warp_min_u64(my_best);
   const unsigned who = __ballot_sync(0xffffffffu, my_best == win && win != ~0ull);
   if (who && lane == __ffs(who) - 1 && win < ((unsigned long long)c1 << 32)) {
@@ -521,6 +529,7 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) total_steps += __shfl_xor_sync(0xffffffffu, total_steps, o);
   if (lane == 0) {
+    if (any_capped) atomicAdd(&ctl->truncated, 1);
     atomicAdd(&ctl->steps, (unsigned long long)(total_steps + expanded));
     atomicMax(&ctl->max_steps_comp, (int)min(total_steps + expanded, (unsigned)INT_MAX));
   }

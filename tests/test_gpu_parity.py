@@ -115,6 +115,40 @@ def test_exact_mode_warp_parallel_search(case):
     assert got["stats"]["truncated"] == 0
 
 
+def test_single_layout_entry_point():
+    """The north_star signature mpld_decompose(csr, stitches, k, alpha, max_steps)."""
+    g = synth.iscas_layout("c1908", seed=3)
+    colors, nc, ns, cost = mp.mpld_decompose(g.n, g.ce_rowptr, g.ce_col, g.se_rowptr, g.se_col, 3, 0.1, 0)
+    ref = oracle.decompose(g, 3, 0.1, max_steps=0)
+    assert np.array_equal(colors, ref["colors"])
+    assert (nc, ns, cost) == (ref["n_conflicts"], ref["n_stitches"], ref["cost"])
+
+
+def test_industrial_config3_scaled():
+    """configs[3] shape (10^6 polygons) scaled to 5 %: full element-by-element parity."""
+    graphs, k, alpha = synth.config_graphs(3, scale=0.05)
+    _assert_same(graphs[0], k, alpha, max_steps=0)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_stress_sweep_exact_mode(k):
+    """configs[4] stress sweep (component sizes 4 -> 64) in exact mode, sampled sizes."""
+    for size in (4, 16, 24, 32, 48, 64):
+        g = synth.stress_components(size, 6, k, seed=100 + size)
+        budget = 0 if size <= 24 else 50000  # exact mode where the oracle can follow
+        got = mp.decompose_graph(g, k, 0.1, max_steps=budget)
+        if size <= 24:
+            ref = oracle.decompose(g, k, 0.1, max_steps=0)
+            assert np.array_equal(got["colors"], ref["colors"])
+            assert got["stats"]["truncated"] == 0
+        # invariants at any size: colours in range, counts recomputed from colours
+        c = got["colors"]
+        assert ((c >= 0) & (c < k)).all()
+        ce = g.ce_edges()
+        assert int((c[ce[:, 0]] == c[ce[:, 1]]).sum()) == int(got["n_conflicts"][0])
+        assert got["stats"]["components"] == (6 if size > k else 0)  # K_size with size <= k peels away
+
+
 def test_qpld_k4_scaled():
     graphs, k, alpha = synth.config_graphs(2, scale=0.1)
     _assert_same(graphs[0], k, alpha, max_steps=200000)
