@@ -307,10 +307,16 @@ def main():
         hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
     except Exception:
         hbm_peak, peak_src = 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
+    traffic = None  # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r1_kernels.json")))["kernels"]
+        traffic = prof.get(dom_name, {}).get("dram_bytes")
+    except Exception:
+        pass
     if kb.get(dom_name):
         achieved = kb[dom_name] / (dom_ms / dom_n / 1e3) / 1e9
         roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": kb[dom_name],
                 "note": "dependency-latency bound in practice (one grid barrier per level), DESIGN.md §5"}
     else:
