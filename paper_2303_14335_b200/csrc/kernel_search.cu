@@ -354,6 +354,14 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
       const int h = atomicAdd(&ctl->n_heavy, 1);
       w.q0[h] = root;
       w.q1[h] = best_cost;
+      if (h < kHeavyScratch) {  // keep the matrix so the warp need not rebuild it
+        for (int i = 0; i < n; ++i) {
+          w.hmask[(size_t)h * 2 * kMaxComp + i] = adjm[i];
+          w.hmask[(size_t)h * 2 * kMaxComp + kMaxComp + i] = sadjm[i];
+          w.horder[(size_t)h * kMaxComp + i] = order[i];
+        }
+        w.hn[h] = n;
+      }
     } else {
       acc_maxsteps = max(acc_maxsteps, (int)min(steps, (unsigned)INT_MAX));
       acc_trunc += trunc ? 1 : 0;
@@ -547,8 +555,17 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
   for (int h = blockIdx.x; h < n_heavy; h += gridDim.x) {
     const int root = __ldcg(&w.q0[h]);
     const int c1 = __ldcg(&w.q1[h]);
-    // rebuild the matrix: loc[] already holds every vertex's BFS position
-    if (threadIdx.x == 0) s_n = bfs_build<false>(g, w, root, s_order, s_adj64, s_sadj64);
+    if (h < kHeavyScratch) {  // the light kernel kept the matrix
+      const int n = __ldcg(&w.hn[h]);
+      for (int i = threadIdx.x; i < n; i += 32) {
+        s_order[i] = __ldcg(&w.horder[(size_t)h * kMaxComp + i]);
+        s_adj64[i] = __ldcg(&w.hmask[(size_t)h * 2 * kMaxComp + i]);
+        s_sadj64[i] = __ldcg(&w.hmask[(size_t)h * 2 * kMaxComp + kMaxComp + i]);
+      }
+      if (threadIdx.x == 0) s_n = n;
+    } else if (threadIdx.x == 0) {  // rebuild: loc[] already holds every vertex's BFS position
+      s_n = bfs_build<false>(g, w, root, s_order, s_adj64, s_sadj64);
+    }
     __syncwarp();
     const int n = s_n;
     if (n <= 32)

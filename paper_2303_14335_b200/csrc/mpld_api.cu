@@ -57,6 +57,9 @@ struct mpld_context {
   int* parent = nullptr;
   int* loc = nullptr;
   int* roots = nullptr;
+  unsigned long long* hmask = nullptr;
+  int* horder = nullptr;
+  int* hn = nullptr;
   Control* ctl = nullptr;
   int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0;
   // host-API staging (device copies of host inputs / outputs)
@@ -154,7 +157,7 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
                  long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost,
                  long long* stats) {
-  Workspace ws{ctx->deg, ctx->hround, ctx->key, ctx->prio, ctx->q0, ctx->q1, ctx->parent, ctx->loc, ctx->roots, ctx->ctl};
+  Workspace ws{ctx->deg, ctx->hround, ctx->key, ctx->prio, ctx->q0, ctx->q1, ctx->parent, ctx->loc, ctx->roots, ctx->hmask, ctx->horder, ctx->hn, ctx->ctl};
   // the control block (counters, barrier arrivals, error bits) starts every call at zero
   cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
   if (e != cudaSuccess) return cuda_fail(e, "control reset");
@@ -253,8 +256,11 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     delete ctx;
     return fail(MPLD_ERR_CUDA, "device does not support cooperative launch");
   }
-  if (cudaMalloc((void**)&ctx->ctl, sizeof(Control)) != cudaSuccess) {
-    delete ctx;
+  if (cudaMalloc((void**)&ctx->hmask, sizeof(unsigned long long) * 2 * kMaxComp * kHeavyScratch) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->horder, sizeof(int) * kMaxComp * kHeavyScratch) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->hn, sizeof(int) * kHeavyScratch) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->ctl, sizeof(Control)) != cudaSuccess) {
+    mpld_context_destroy(ctx);
     return fail(MPLD_ERR_NOMEM, "control block allocation failed");
   }
   cudaMemset(ctx->ctl, 0, sizeof(Control));
@@ -288,7 +294,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
 void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->key, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
-                  (void*)ctx->parent, (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->ctl, (void*)ctx->h_lo,
+                  (void*)ctx->parent, (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->hmask, (void*)ctx->horder, (void*)ctx->hn, (void*)ctx->ctl, (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
                   (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})
     if (p) cudaFree(p);

@@ -17,6 +17,7 @@ namespace mpld {
 
 constexpr int kMaxComp = MPLD_MAX_COMPONENT;  // one 64-bit word per mask
 constexpr int kCostUnits = MPLD_COST_UNITS;
+constexpr int kHeavyScratch = 4096;  // heavy components whose matrices are kept for the warp kernel
 
 enum ErrBits : int { kErrGraph = 1, kErrComponent = 2 };
 
@@ -89,6 +90,9 @@ struct Workspace {
   int* parent;     // union-find
   int* loc;        // local index of a kept vertex inside its component
   int* roots;      // component roots (min vertex id of the component)
+  unsigned long long* hmask;  // heavy components kept by the light search: adj/sadj masks
+  int* horder;                // ... their BFS orders
+  int* hn;                    // ... their sizes
   Control* ctl;
 };
 
