@@ -15,6 +15,7 @@ namespace mpld {
 namespace {
 
 constexpr int kAppend = 8;   // items one thread may append per call before spilling to direct atomics
+constexpr int kNb = 4;       // neighbours processed per batch of independent memory operations
 constexpr int kTail = 1024;  // frontiers up to one item per thread of a CTA are finished by that CTA alone
 
 __device__ __forceinline__ bool row_contains(const int* __restrict__ col, int a, int b, int x) {
@@ -166,13 +167,24 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
     if (i < cnt) {
       const int v = __ldcg(&cur[i]);
       const int e1 = g.ce_rp[v + 1];
-      for (int e = g.ce_rp[v]; e < e1; ++e) {
-        const int u = g.ce_col[e];
-        if (__ldcg(&w.hround[u]) != -1) continue;  // already hidden: its degree no longer matters
-        const int old = atomicSub(&w.deg[u], 1);
-        if (old == k && g.se_rp[u + 1] == g.se_rp[u]) {
-          w.hround[u] = r + 1;
-          list_push(items, m, u, ncnt, nxt);
+      // neighbours in batches of kNb: ids, rounds and decrements of a batch are
+      // independent and in flight together (a few memory round trips per batch
+      // instead of three per neighbour)
+      for (int e0 = g.ce_rp[v]; e0 < e1; e0 += kNb) {
+        int u[kNb], hu[kNb], old[kNb];
+#pragma unroll
+        for (int j = 0; j < kNb; ++j) u[j] = e0 + j < e1 ? g.ce_col[e0 + j] : -1;
+#pragma unroll
+        for (int j = 0; j < kNb; ++j) hu[j] = u[j] >= 0 ? __ldcg(&w.hround[u[j]]) : 0;
+#pragma unroll
+        for (int j = 0; j < kNb; ++j)  // already-hidden neighbours' degrees no longer matter
+          old[j] = hu[j] == -1 ? atomicSub(&w.deg[u[j]], 1) : 0;
+#pragma unroll
+        for (int j = 0; j < kNb; ++j) {
+          if (old[j] == k && g.se_rp[u[j] + 1] == g.se_rp[u[j]]) {
+            w.hround[u[j]] = r + 1;
+            list_push(items, m, u[j], ncnt, nxt);
+          }
         }
       }
     }
@@ -190,7 +202,7 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 //     k -> k-1 while round r is pushed, so each round only touches the
 //     neighbours of the previous round (frontier queue).
 // Then union-find connected components over CE ∪ SE of the kept vertices.
-__global__ void __launch_bounds__(1024) mpld_simplify_components(GraphView g, Workspace w, int k,
+__global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g, Workspace w, int k,
                                                                  int* colors, long long* counts) {
   GridBarrier grid(&w.ctl->bar[0]);
   stamp(w.ctl, 12);
@@ -220,8 +232,7 @@ __global__ void __launch_bounds__(1024) mpld_simplify_components(GraphView g, Wo
         int d0 = 0;  // live degree after round 0
         for (int e = a; e < b; ++e) {
           const int u = g.ce_col[e];
-          const bool u_st = g.se_rp[u + 1] > g.se_rp[u];
-          d0 += (u_st || g.ce_rp[u + 1] - g.ce_rp[u] >= k) ? 1 : 0;
+          d0 += (g.se_rp[u + 1] > g.se_rp[u] || g.ce_rp[u + 1] - g.ce_rp[u] >= k) ? 1 : 0;
         }
         w.deg[v] = d0;
         if (!st && d0 < k) { hr = 1; take = 1; }
@@ -337,13 +348,25 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
       const int v = __ldcg(&cur[i]);
       const unsigned long long kv = w.key[v];
       unsigned used = 0;
-      for (int e = g.ce_rp[v], e1 = g.ce_rp[v + 1]; e < e1; ++e) {
-        const int u = g.ce_col[e];
-        if (w.key[u] > kv) {  // popped before v (or kept): coloured
-          const int cu = __ldcg(&colors[u]);
-          if (cu >= 0) used |= 1u << cu;
-        } else if (atomicSub(&w.deg[u], 1) == 1) {  // v was u's last predecessor
-          list_push(items, m, u, ncnt, nxt);
+      const int e1 = g.ce_rp[v + 1];
+      for (int e0 = g.ce_rp[v]; e0 < e1; e0 += kNb) {  // batches with independent loads / atomics
+        int u[kNb], x[kNb];
+        bool before[kNb];
+#pragma unroll
+        for (int j = 0; j < kNb; ++j) u[j] = e0 + j < e1 ? g.ce_col[e0 + j] : -1;
+#pragma unroll
+        for (int j = 0; j < kNb; ++j) before[j] = u[j] >= 0 && w.key[u[j]] > kv;  // popped before v (or kept)
+#pragma unroll
+        for (int j = 0; j < kNb; ++j)
+          x[j] = u[j] < 0 ? -1 : (before[j] ? __ldcg(&colors[u[j]]) : atomicSub(&w.deg[u[j]], 1));
+#pragma unroll
+        for (int j = 0; j < kNb; ++j) {
+          if (u[j] < 0) continue;
+          if (before[j]) {
+            if (x[j] >= 0) used |= 1u << x[j];
+          } else if (x[j] == 1) {  // v was u's last predecessor
+            list_push(items, m, u[j], ncnt, nxt);
+          }
         }
       }
       const int c = __ffs(~used) - 1;
@@ -353,7 +376,7 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
   }
 }
 
-__global__ void __launch_bounds__(1024) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
+__global__ void __launch_bounds__(1024, 2) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
   GridBarrier grid(&w.ctl->bar[1]);
   stamp(w.ctl, 13);
   const int nth = gridDim.x * blockDim.x;
@@ -367,9 +390,17 @@ __global__ void __launch_bounds__(1024) mpld_recover(GraphView g, Workspace w, i
       const unsigned long long kv = w.key[v];
       if (kv != ~0ull) {
         int cnt = 0;
-        for (int e = g.ce_rp[v], e1 = g.ce_rp[v + 1]; e < e1; ++e) {
-          const unsigned long long ku = w.key[g.ce_col[e]];
-          cnt += (ku > kv && ku != ~0ull) ? 1 : 0;
+        const int e1 = g.ce_rp[v + 1];
+        for (int e0 = g.ce_rp[v]; e0 < e1; e0 += kNb) {
+          int u[kNb];
+#pragma unroll
+          for (int j = 0; j < kNb; ++j) u[j] = e0 + j < e1 ? g.ce_col[e0 + j] : -1;
+#pragma unroll
+          for (int j = 0; j < kNb; ++j) {
+            if (u[j] < 0) continue;
+            const unsigned long long ku = w.key[u[j]];
+            cnt += (ku > kv && ku != ~0ull) ? 1 : 0;
+          }
         }
         w.deg[v] = cnt;
         ready = cnt == 0;
@@ -420,9 +451,14 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += nth) {
     const int cv = colors[v];
     int nc = 0, ns = 0;
-    for (int e = g.ce_rp[v], e1 = g.ce_rp[v + 1]; e < e1; ++e) {
-      const int u = g.ce_col[e];
-      if (u > v && colors[u] == cv) ++nc;
+    const int e1 = g.ce_rp[v + 1];
+    for (int e0 = g.ce_rp[v]; e0 < e1; e0 += kNb) {
+      int u[kNb];
+#pragma unroll
+      for (int j = 0; j < kNb; ++j) u[j] = e0 + j < e1 ? g.ce_col[e0 + j] : -1;
+#pragma unroll
+      for (int j = 0; j < kNb; ++j)
+        if (u[j] > v && colors[u[j]] == cv) ++nc;
     }
     for (int e = g.se_rp[v], e1 = g.se_rp[v + 1]; e < e1; ++e) {
       const int u = g.se_col[e];
