@@ -144,6 +144,29 @@ int mpld_decompose_device(mpld_context* ctx, void* stream, int32_t n_layouts,
                           double alpha, int64_t max_steps, uint32_t flags, int32_t* d_colors,
                           int64_t* d_counts, double* d_cost, int64_t* d_stats);
 
+/* ---- one batch sharded over several processes ----------------
+ * The same hot path split in three phases so that the components of ONE
+ * layout batch can be searched by shard_count processes (one per GPU):
+ *   1. every process: mpld_prepare_device   (validate?, simplification, components)
+ *   2. every process: mpld_search_device     with its shard_index: searches the
+ *      components whose root r (smallest vertex id) has
+ *      lowbias32(r) % shard_count == shard_index, writes their colours into
+ *      d_colors and leaves -1 on every other vertex;
+ *   3. the caller combines d_colors across the processes with an element-wise
+ *      maximum (an NCCL all-reduce MAX over NVLink) — the only exchange;
+ *   4. every process: mpld_finish_device     (recovery of the hidden vertices, Eq. 1).
+ * The graph pointers and k of phase 1 are remembered by the context and must
+ * stay valid until phase 4 is enqueued.  With shard_count == 1 the phases
+ * compute exactly mpld_decompose_device.  All calls are stream-ordered. */
+int mpld_prepare_device(mpld_context* ctx, void* stream, int32_t n_layouts, const int32_t* d_layout_offsets,
+                        int32_t n, const int32_t* d_ce_rowptr, const int32_t* d_ce_col,
+                        const int32_t* d_se_rowptr, const int32_t* d_se_col, int32_t k, uint32_t flags,
+                        int32_t* d_colors, int64_t* d_counts);
+int mpld_search_device(mpld_context* ctx, void* stream, double alpha, int64_t max_steps, int32_t shard_index,
+                       int32_t shard_count, int32_t* d_colors);
+int mpld_finish_device(mpld_context* ctx, void* stream, double alpha, int32_t* d_colors, int64_t* d_counts,
+                       double* d_cost, int64_t* d_stats);
+
 /* Kernel timing inside the context (for bench.py's roofline): when enabled,
  * every launch is bracketed by CUDA events on the launch stream and its
  * duration accumulated per kernel.  mpld_kernel_count() kernels, indexed

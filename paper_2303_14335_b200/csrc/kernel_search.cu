@@ -304,7 +304,8 @@ __device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* 
 
 template <int K>
 __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
-                                                              long long max_steps, int* colors) {
+                                                              long long max_steps, int shard_index,
+                                                              int shard_count, int* colors) {
   extern __shared__ __align__(16) unsigned char lsmem[];
   Control* ctl = w.ctl;
   const int n_comp = __ldcg(&ctl->n_comp);
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
   for (int ci = blockIdx.x * blockDim.x + threadIdx.x; ci < n_comp; ci += gridDim.x * blockDim.x) {
     const long long c0 = clock64();
     const int root = w.roots[ci];
+    if (shard_count > 1 && (int)(lowbias32((uint32_t)root) % (uint32_t)shard_count) != shard_index) continue;
     const int n = bfs_build<true>(g, w, root, order, adjm, sadjm);
     if (n < 0) {
       atomicOr(&ctl->err, kErrComponent);
@@ -578,12 +580,21 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
 
 }  // namespace
 
-cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
-                          cudaStream_t s, int blocks, int threads) {
+cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
+                          int shard_index, int shard_count, int* colors, cudaStream_t s, int blocks) {
   switch (k) {
-    case 2: mpld_exact_cover_search<2><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, colors); break;
-    case 3: mpld_exact_cover_search<3><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, colors); break;
-    case 4: mpld_exact_cover_search<4><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, colors); break;
+    case 2:
+      mpld_exact_cover_search<2><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
+                                                                colors);
+      break;
+    case 3:
+      mpld_exact_cover_search<3><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
+                                                                colors);
+      break;
+    case 4:
+      mpld_exact_cover_search<4><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
+                                                                colors);
+      break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -210,7 +210,6 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nth = gridDim.x * blockDim.x;
   Control* ctl = w.ctl;
-  (void)colors;
   for (int l = tid; l < 2 * g.n_layouts; l += nth) counts[l] = 0;
 
   // rounds 0 and 1, recovery priorities, union-find init
@@ -224,6 +223,7 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
       const int lo = layout_index(g, v);
       w.prio[v] = lowbias32((uint32_t)(v - (g.n_layouts > 1 ? __ldg(&g.layout_off[lo]) : 0)));
       w.parent[v] = v;
+      colors[v] = -1;  // every vertex is coloured later by exactly one search shard or the recovery
       int hr = -1;
       if (!st && b - a < k) {
         hr = 0;

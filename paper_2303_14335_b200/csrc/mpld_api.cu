@@ -38,7 +38,6 @@ const char* kKernelNames[K_COUNT] = {"mpld_validate", "mpld_simplify_components"
                                      "mpld_exact_cover_search_heavy", "mpld_recover", "mpld_evaluate"};
 
 constexpr int kCoopThreads = 1024;
-constexpr int kSearchThreads = 128;
 
 }  // namespace
 
@@ -61,6 +60,11 @@ struct mpld_context {
   int* horder = nullptr;
   int* hn = nullptr;
   Control* ctl = nullptr;
+  // phase-split calls: the prepared graph
+  GraphView g{};
+  int k = 0;
+  bool prepared = false;
+  int call_launches = 0;
   int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0;
   // host-API staging (device copies of host inputs / outputs)
   int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
@@ -154,60 +158,91 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
   return MPLD_OK;
 }
 
-int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
-                 long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost,
-                 long long* stats) {
-  Workspace ws{ctx->deg, ctx->hround, ctx->key, ctx->prio, ctx->q0, ctx->q1, ctx->parent, ctx->loc, ctx->roots, ctx->hmask, ctx->horder, ctx->hn, ctx->ctl};
+Workspace workspace(mpld_context* ctx) {
+  return Workspace{ctx->deg,    ctx->hround, ctx->key,   ctx->prio,   ctx->q0, ctx->q1, ctx->parent,
+                   ctx->loc,    ctx->roots,  ctx->hmask, ctx->horder, ctx->hn, ctx->ctl};
+}
+
+// phase 1: validate?, simplification, components (colours initialised to -1)
+int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, uint32_t flags, int* colors,
+                  long long* counts) {
+  Workspace ws = workspace(ctx);
+  ctx->g = g;
+  ctx->k = k;
+  ctx->prepared = true;
+  ctx->call_launches = 0;
   // the control block (counters, barrier arrivals, error bits) starts every call at zero
   cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
   if (e != cudaSuccess) return cuda_fail(e, "control reset");
-  int launches = 0;
-  const bool exact = max_steps <= 0;
-  const int n_launch = 4 + ((flags & MPLD_FLAG_VALIDATE) ? 1 : 0) + (exact ? 1 : 0);
   if (flags & MPLD_FLAG_VALIDATE) {
     TimedLaunch t(ctx, K_VALIDATE, s);
     e = launch_validate(g, ws, s, ctx->blocks_stream);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_validate");
     t.done();
-    ++launches;
+    ++ctx->call_launches;
   }
-  {
-    TimedLaunch t(ctx, K_SIMPLIFY, s);
-    e = launch_simplify_components(g, ws, k, colors, counts, s, ctx->blocks_simplify, kCoopThreads);
-    if (e != cudaSuccess) return cuda_fail(e, "mpld_simplify_components");
-    t.done();
-    ++launches;
-  }
+  TimedLaunch t(ctx, K_SIMPLIFY, s);
+  e = launch_simplify_components(g, ws, k, colors, counts, s, ctx->blocks_simplify, kCoopThreads);
+  if (e != cudaSuccess) return cuda_fail(e, "mpld_simplify_components");
+  t.done();
+  ++ctx->call_launches;
+  return MPLD_OK;
+}
+
+// phase 2: the exact-cover search of this shard's components
+int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_steps, int shard_index,
+                 int shard_count, int* colors) {
+  Workspace ws = workspace(ctx);
+  const GraphView& g = ctx->g;
+  // the heavy queue belongs to this search call (several shards may share a context)
+  cudaError_t e0 = cudaMemsetAsync(&ctx->ctl->n_heavy, 0, sizeof(int), s);
+  if (e0 != cudaSuccess) return cuda_fail(e0, "heavy queue reset");
   {
     TimedLaunch t(ctx, K_SEARCH, s);
-    e = launch_search(g, ws, k, w_stitch, max_steps, colors, s, ctx->blocks_search, kSearchThreads);
+    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, shard_index, shard_count, colors, s,
+                                  ctx->blocks_search);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
     t.done();
-    ++launches;
+    ++ctx->call_launches;
   }
-  if (exact) {
+  if (max_steps <= 0) {  // exact mode: heavy components on the warp-parallel search
     TimedLaunch t(ctx, K_SEARCH_HEAVY, s);
-    e = launch_search_heavy(g, ws, k, w_stitch, colors, s, ctx->num_sms * 4);
+    cudaError_t e = launch_search_heavy(g, ws, ctx->k, w_stitch, colors, s, ctx->num_sms * 4);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_heavy");
     t.done();
-    ++launches;
+    ++ctx->call_launches;
   }
+  return MPLD_OK;
+}
+
+// phase 3: recovery of the hidden vertices and Eq. (1)
+int phase_finish(mpld_context* ctx, cudaStream_t s, double alpha, int* colors, long long* counts, double* cost,
+                 long long* stats) {
+  Workspace ws = workspace(ctx);
+  const GraphView& g = ctx->g;
   {
     TimedLaunch t(ctx, K_RECOVER, s);
-    e = launch_recover(g, ws, k, colors, s, ctx->blocks_recover, kCoopThreads);
+    cudaError_t e = launch_recover(g, ws, ctx->k, colors, s, ctx->blocks_recover, kCoopThreads);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_recover");
     t.done();
-    ++launches;
+    ++ctx->call_launches;
   }
-  {
-    TimedLaunch t(ctx, K_EVALUATE, s);
-    e = launch_evaluate(g, ws, colors, alpha, counts, cost, stats, n_launch, s, ctx->blocks_stream);
-    if (e != cudaSuccess) return cuda_fail(e, "mpld_evaluate");
-    t.done();
-    ++launches;
-  }
-  (void)launches;
+  TimedLaunch t(ctx, K_EVALUATE, s);
+  cudaError_t e = launch_evaluate(g, ws, colors, alpha, counts, cost, stats, ctx->call_launches + 1, s,
+                                  ctx->blocks_stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mpld_evaluate");
+  t.done();
+  ctx->prepared = false;
   return MPLD_OK;
+}
+
+int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
+                 long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost,
+                 long long* stats) {
+  int rc = phase_prepare(ctx, s, g, k, flags, colors, counts);
+  if (rc == MPLD_OK) rc = phase_search(ctx, s, w_stitch, max_steps, 0, 1, colors);
+  if (rc == MPLD_OK) rc = phase_finish(ctx, s, alpha, colors, counts, cost, stats);
+  return rc;
 }
 
 std::mutex g_ctx_mu;
@@ -266,7 +301,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   cudaMemset(ctx->ctl, 0, sizeof(Control));
   ctx->blocks_simplify = coop_blocks_simplify(kCoopThreads, ctx->num_sms);
   ctx->blocks_recover = coop_blocks_recover(kCoopThreads, ctx->num_sms);
-  ctx->blocks_search = resident_blocks_search(kSearchThreads, ctx->num_sms);
+  ctx->blocks_search = resident_blocks_search(32, ctx->num_sms);
   ctx->blocks_stream = ctx->num_sms * 8;
   e = configure_search_heavy();
   if (e != cudaSuccess) {
@@ -326,6 +361,51 @@ int mpld_decompose_device(mpld_context* ctx, void* stream, int32_t n_layouts, co
   GraphView g{n, n_layouts, d_layout_offsets, d_ce_rowptr, d_ce_col, d_se_rowptr, d_se_col};
   return run_pipeline(ctx, (cudaStream_t)stream, g, k, w_stitch, alpha, (long long)max_steps, flags, d_colors,
                       (long long*)d_counts, d_cost, (long long*)d_stats);
+}
+
+int mpld_prepare_device(mpld_context* ctx, void* stream, int32_t n_layouts, const int32_t* d_layout_offsets,
+                        int32_t n, const int32_t* d_ce_rowptr, const int32_t* d_ce_col,
+                        const int32_t* d_se_rowptr, const int32_t* d_se_col, int32_t k, uint32_t flags,
+                        int32_t* d_colors, int64_t* d_counts) {
+  if (!ctx) return fail(MPLD_ERR_ARG, "ctx is NULL");
+  int w_stitch = 0;
+  int rc = check_scalars(n, k, 0.0, &w_stitch);
+  if (rc != MPLD_OK) return rc;
+  if (n_layouts < 1 || !d_layout_offsets || !d_ce_rowptr || !d_se_rowptr || !d_colors || !d_counts)
+    return fail(MPLD_ERR_ARG, "bad argument (NULL device pointer or n_layouts < 1)");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  rc = ensure_workspace(ctx, n, n_layouts);
+  if (rc != MPLD_OK) return rc;
+  GraphView g{n, n_layouts, d_layout_offsets, d_ce_rowptr, d_ce_col, d_se_rowptr, d_se_col};
+  return phase_prepare(ctx, (cudaStream_t)stream, g, k, flags, d_colors, (long long*)d_counts);
+}
+
+int mpld_search_device(mpld_context* ctx, void* stream, double alpha, int64_t max_steps, int32_t shard_index,
+                       int32_t shard_count, int32_t* d_colors) {
+  if (!ctx || !d_colors) return fail(MPLD_ERR_ARG, "ctx or d_colors is NULL");
+  if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
+    return fail(MPLD_ERR_ARG, "shard_index must be in [0, shard_count)");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (!ctx->prepared) return fail(MPLD_ERR_ARG, "mpld_prepare_device must be called first");
+  int w_stitch = 0;
+  int rc = check_scalars(ctx->g.n, ctx->k, alpha, &w_stitch);
+  if (rc != MPLD_OK) return rc;
+  cudaSetDevice(ctx->device);
+  return phase_search(ctx, (cudaStream_t)stream, w_stitch, (long long)max_steps, shard_index, shard_count, d_colors);
+}
+
+int mpld_finish_device(mpld_context* ctx, void* stream, double alpha, int32_t* d_colors, int64_t* d_counts,
+                       double* d_cost, int64_t* d_stats) {
+  if (!ctx || !d_colors || !d_counts || !d_cost) return fail(MPLD_ERR_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (!ctx->prepared) return fail(MPLD_ERR_ARG, "mpld_prepare_device must be called first");
+  int w_stitch = 0;
+  int rc = check_scalars(ctx->g.n, ctx->k, alpha, &w_stitch);
+  if (rc != MPLD_OK) return rc;
+  cudaSetDevice(ctx->device);
+  return phase_finish(ctx, (cudaStream_t)stream, alpha, d_colors, (long long*)d_counts, d_cost,
+                      (long long*)d_stats);
 }
 
 int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32_t n, const int32_t* ce_rowptr,

@@ -112,7 +112,7 @@ cudaError_t launch_validate(const GraphView& g, Workspace ws, cudaStream_t s, in
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors,
                                        long long* counts, cudaStream_t s, int blocks, int threads);
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
-                          int* colors, cudaStream_t s, int blocks, int threads);
+                          int shard_index, int shard_count, int* colors, cudaStream_t s, int blocks);
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
                                 int blocks);
 cudaError_t configure_search_heavy();

@@ -31,7 +31,7 @@ MPLD_STAT_LEN = len(STAT_NAMES)
 EXPORTS = ["mpld_last_error", "mpld_version", "mpld_decompose", "mpld_decompose_batch", "mpld_context_create",
            "mpld_context_destroy", "mpld_decompose_device", "mpld_context_set_timing",
            "mpld_context_reset_timing", "mpld_kernel_count", "mpld_kernel_name", "mpld_context_kernel_time",
-           "mpld_context_debug"]
+           "mpld_context_debug", "mpld_prepare_device", "mpld_search_device", "mpld_finish_device"]
 
 
 class MPLDError(RuntimeError):
@@ -74,6 +74,10 @@ def lib():
     L.mpld_context_reset_timing.argtypes = [_vp]
     L.mpld_context_kernel_time.argtypes = [_vp, ctypes.c_int, _f64p, _i64p]
     L.mpld_context_debug.argtypes = [_vp, _vp, ctypes.c_int]
+    L.mpld_prepare_device.argtypes = [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp, _vp, _vp, _vp,
+                                      ctypes.c_int32, ctypes.c_uint32, _vp, _vp]
+    L.mpld_search_device.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp]
+    L.mpld_finish_device.argtypes = [_vp, _vp, ctypes.c_double, _vp, _vp, _vp, _vp]
     _lib = L
     return L
 
@@ -180,6 +184,32 @@ class Context:
                                            _dev_ptr(ce_rowptr), _dev_ptr(ce_col), _dev_ptr(se_rowptr),
                                            _dev_ptr(se_col), int(k), float(alpha), int(max_steps), int(flags),
                                            _dev_ptr(colors), _dev_ptr(counts), _dev_ptr(cost), _dev_ptr(stats)))
+
+    # ---- phase-split calls for a batch sharded over processes (include/mpld.h) ----
+    @staticmethod
+    def _stream(stream, like):
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(like.device)
+        return _vp(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream or 0))
+
+    def prepare_device(self, layout_offsets, n, ce_rowptr, ce_col, se_rowptr, se_col, k, colors, counts,
+                       flags: int = 0, stream=None):
+        """Phase 1 (validate?, simplification, components); colours set to -1."""
+        _check(lib().mpld_prepare_device(self._h, self._stream(stream, colors), int(layout_offsets.numel() - 1),
+                                         _dev_ptr(layout_offsets), int(n), _dev_ptr(ce_rowptr), _dev_ptr(ce_col),
+                                         _dev_ptr(se_rowptr), _dev_ptr(se_col), int(k), int(flags),
+                                         _dev_ptr(colors), _dev_ptr(counts)))
+
+    def search_device(self, alpha, max_steps, shard_index, shard_count, colors, stream=None):
+        """Phase 2: search the components of this shard, colours of the others stay -1."""
+        _check(lib().mpld_search_device(self._h, self._stream(stream, colors), float(alpha), int(max_steps),
+                                        int(shard_index), int(shard_count), _dev_ptr(colors)))
+
+    def finish_device(self, alpha, colors, counts, cost, stats=None, stream=None):
+        """Phase 3: recovery and Eq. (1) (after the colours of all shards are combined)."""
+        _check(lib().mpld_finish_device(self._h, self._stream(stream, colors), float(alpha), _dev_ptr(colors),
+                                        _dev_ptr(counts), _dev_ptr(cost), _dev_ptr(stats)))
 
     def set_timing(self, enable: bool):
         _check(lib().mpld_context_set_timing(self._h, 1 if enable else 0))

@@ -220,6 +220,44 @@ def test_device_entry_point_matches_host_entry_point():
     ctx.close()
 
 
+@pytest.mark.parametrize("shards", [1, 2, 3])
+def test_sharded_phases_equal_oracle(shards):
+    """The phase-split path of one batch sharded over `shards` processes, simulated
+    on one GPU: every shard searches its components into its own colour buffer,
+    the buffers are combined by an element-wise maximum (the NCCL all-reduce MAX
+    of the multi-GPU run), then recovery + Eq. (1) — equal to the oracle."""
+    graphs, k, alpha = synth.config_graphs(1)
+    b = synth.concat(graphs[:5])
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    ctx = mp.Context(0, b.n, b.n_layouts)
+    colors = torch.empty(b.n, dtype=torch.int32, device=dev)
+    counts = torch.empty(2 * b.n_layouts, dtype=torch.int64, device=dev)
+    cost = torch.empty(b.n_layouts, dtype=torch.float64, device=dev)
+    stats = torch.empty(len(mp.STAT_NAMES), dtype=torch.int64, device=dev)
+    graph = [T(b.layout_offsets), T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr), T(b.se_col)]  # alive until finish
+    ctx.prepare_device(graph[0], b.n, *graph[1:], k, colors, counts, flags=mp.MPLD_FLAG_VALIDATE)
+    torch.cuda.synchronize()
+    assert int(colors.max()) == -1
+    parts = []
+    for s in range(shards):
+        c = colors.clone()
+        ctx.search_device(alpha, 0, s, shards, c)
+        parts.append(c)
+    torch.cuda.synchronize()
+    owned = [(p >= 0) for p in parts]
+    assert int(sum(o.int() for o in owned).max()) <= 1  # every kept vertex searched by exactly one shard
+    combined = torch.stack(parts).amax(0).contiguous()
+    ctx.finish_device(alpha, combined, counts, cost, stats)
+    torch.cuda.synchronize()
+    ref = oracle.decompose(b, k, alpha, max_steps=0)
+    assert np.array_equal(combined.cpu().numpy(), ref["colors"])
+    c2 = counts.cpu().numpy().reshape(-1, 2)
+    for li, (c, s_, cst) in enumerate(ref["per_layout"]):
+        assert (int(c2[li, 0]), int(c2[li, 1]), float(cost[li])) == (c, s_, cst)
+    ctx.close()
+
+
 def test_full_size_qpld_sampled():
     """configs[2] at full s38584 size, in bench's launch configuration: global
     invariants at full size, and the oracle recomputes a sample of components
