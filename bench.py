@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--profile-launches", action="store_true", help="short run for ncu (no clocks / baselines)")
+    ap.add_argument("--mode", default="layouts", choices=["layouts", "shard"],
+                    help="layouts: every rank decomposes its own batch (weak scaling, default); "
+                         "shard: one batch, its components sharded over the ranks, colours combined "
+                         "by an NCCL all-reduce MAX (strong scaling)")
     return ap.parse_args()
 
 
@@ -66,6 +70,8 @@ def config_dict(b, replicas, n_gpus, extra=None):
          "ce_edges_per_step": int(b.n_ce), "se_edges_per_step": int(b.n_se),
          "max_steps": MAX_STEPS, "l2": "flushed between timed steps (256 MiB write)",
          "parallelism": "dp%d (independent layouts per rank)" % n_gpus}
+    if os.environ.get("MPLD_BENCH_MODE") == "shard":
+        d["parallelism"] = "component shards over %d ranks, NCCL all-reduce MAX of colours" % n_gpus
     if extra:
         d.update(extra)
     return d
@@ -214,7 +220,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     mp.lib()
-    b, k, alpha = workload(rank, args.replicas)
+    shard = args.mode == "shard"
+    os.environ["MPLD_BENCH_MODE"] = args.mode
+    b, k, alpha = workload(0 if shard else rank, args.replicas)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     d_lo, d_cr, d_cc, d_sr, d_sc = (T(b.layout_offsets), T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr),
                                     T(b.se_col))
@@ -229,8 +237,15 @@ def main():
     flags = mp.MPLD_FLAG_VALIDATE
 
     def step():
-        ctx.decompose_device(d_lo, b.n, d_cr, d_cc, d_sr, d_sc, k, alpha, args.max_steps, colors, counts, cost,
-                             stats, flags=flags, stream=stream)
+        if not shard:
+            ctx.decompose_device(d_lo, b.n, d_cr, d_cc, d_sr, d_sc, k, alpha, args.max_steps, colors, counts, cost,
+                                 stats, flags=flags, stream=stream)
+            return
+        ctx.prepare_device(d_lo, b.n, d_cr, d_cc, d_sr, d_sc, k, colors, counts, flags=flags, stream=stream)
+        ctx.search_device(alpha, args.max_steps, rank, world, colors, stream=stream)
+        if world > 1:  # the only exchange: per-component colourings, element-wise max over NVLink
+            dist.all_reduce(colors, op=dist.ReduceOp.MAX)
+        ctx.finish_device(alpha, colors, counts, cost, stats, stream=stream)
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -275,23 +290,35 @@ def main():
     h = [pin(x) for x in (b.layout_offsets, b.ce_rowptr, b.ce_col, b.se_rowptr, b.se_col)]
     h_colors = torch.empty(b.n, dtype=torch.int32).pin_memory()
     e2e_steps = max(3, min(args.steps, 10))
-    mp.mpld_decompose_batch(h[0], b.n, h[1], h[2], h[3], h[4], k, alpha, args.max_steps, flags, out_colors=h_colors)
+
+    def e2e_step():
+        if not shard:  # the host C-ABI call: H2D, all kernels, D2H inside
+            mp.mpld_decompose_batch(h[0], b.n, h[1], h[2], h[3], h[4], k, alpha, args.max_steps, flags,
+                                    out_colors=h_colors)
+            return
+        for dst, src in zip((d_lo, d_cr, d_cc, d_sr, d_sc), h):  # H2D from pinned memory
+            dst.copy_(src, non_blocking=True)
+        step()
+        h_colors.copy_(colors, non_blocking=True)  # D2H of the result
+        torch.cuda.synchronize()
+
+    e2e_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        res = mp.mpld_decompose_batch(h[0], b.n, h[1], h[2], h[3], h[4], k, alpha, args.max_steps, flags,
-                                      out_colors=h_colors)
+        e2e_step()
     e2e_s = time.perf_counter() - t0
     assert np.array_equal(h_colors.numpy(), colors.cpu().numpy())
     h2d = sum(x.numel() * 4 for x in h)
     d2h = b.n * 4 + L * 8 * 3 + 8 * len(mp.STAT_NAMES)
 
     # aggregate over ranks
+    work = "max" if shard else "sum"  # shard mode: every rank holds the same batch
     comps_all, ms_max, e2e_comps_all, e2e_ms_max, layouts_all = aggregate(
         [comps_per_step * args.steps, total_ms, comps_per_step * e2e_steps, e2e_s * 1e3, L],
-        ["sum", "max", "sum", "max", "sum"], world, dev)
+        [work, "max", work, "max", work], world, dev)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -329,8 +356,8 @@ def main():
     share = {name: (v[0] / total_ms if total_ms else None) for name, v in ktimes.items() if v[1]}
     out = {"metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step,
-           "ms_per_layout": ms_max / args.steps / (layouts_all / world),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+           "ms_per_layout": ms_max / args.steps / (layouts_all if shard else layouts_all / world),
+           "higher_is_better": True, "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "int32",
            "data": "synthetic (seeded, synth/layouts.py)",
            "config": config_dict(b, args.replicas, world, {"components_per_step_per_rank": comps_per_step}),
            "e2e": {"value": e2e_comps_all / (e2e_ms_max / 1e3), "unit": METRIC, "h2d_bytes_per_step": int(h2d),
