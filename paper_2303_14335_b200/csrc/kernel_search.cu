@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
                                                               int shard_count, int* colors) {
   extern __shared__ __align__(16) unsigned char lsmem[];
   Control* ctl = w.ctl;
-  const int n_comp = __ldcg(&ctl->n_comp);
+  const int n_comp = __ldcg(&ctl->err) ? 0 : __ldcg(&ctl->n_comp);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

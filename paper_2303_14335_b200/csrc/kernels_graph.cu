@@ -1,5 +1,4 @@
 // Graph-level kernels of the MPLD hot path (§2.2 / Fig. 2 flow):
-//   mpld_validate            input CSR invariants (optional)
 //   mpld_simplify_components simplification (R8) + connected components (Alg. 1 lines 1-3)
 //   mpld_recover             recovery of the hidden vertices (R9)
 //   mpld_evaluate            Eq. (1) conflict / stitch counts and cost per layout
@@ -124,33 +123,27 @@ __device__ __forceinline__ void unite(int* parent, int a, int b) {
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) mpld_validate(GraphView g, Workspace w) {
-  const int nth = gridDim.x * blockDim.x;
-  int bad = 0;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += nth) {
-    for (int pass = 0; pass < 2; ++pass) {
-      const int* rp = pass ? g.se_rp : g.ce_rp;
-      const int* col = pass ? g.se_col : g.ce_col;
-      const int* orp = pass ? g.ce_rp : g.se_rp;
-      const int* ocol = pass ? g.ce_col : g.se_col;
-      int a = rp[v], b = rp[v + 1];
-      if (a > b) { bad = 1; break; }
-      int prev = -1;
-      for (int e = a; e < b; ++e) {
-        int u = col[e];
-        if (u < 0 || u >= g.n || u == v || u <= prev) { bad = 1; break; }
-        prev = u;
-        if (!row_contains(col, rp[u], rp[u + 1], v)) bad = 1;    // symmetric
-        if (row_contains(ocol, orp[v], orp[v + 1], u)) bad = 1;  // CE ∩ SE = ∅
-      }
+// Input invariants of include/mpld.h for vertex v (MPLD_FLAG_VALIDATE): both
+// rows strictly ascending, ids in range, no self loop, symmetric (binary search
+// in the neighbour's row), CE ∩ SE = ∅.
+__device__ bool vertex_invalid(const GraphView& g, int v) {
+  for (int pass = 0; pass < 2; ++pass) {
+    const int* rp = pass ? g.se_rp : g.ce_rp;
+    const int* col = pass ? g.se_col : g.ce_col;
+    const int* orp = pass ? g.ce_rp : g.se_rp;
+    const int* ocol = pass ? g.ce_col : g.se_col;
+    const int a = rp[v], b = rp[v + 1];
+    if (a > b) return true;
+    int prev = -1;
+    for (int e = a; e < b; ++e) {
+      const int u = col[e];
+      if (u < 0 || u >= g.n || u == v || u <= prev) return true;
+      prev = u;
+      if (!row_contains(col, rp[u], rp[u + 1], v)) return true;   // symmetric
+      if (row_contains(ocol, orp[v], orp[v + 1], u)) return true;  // CE ∩ SE = ∅
     }
   }
-  if (g.n_layouts > 0 && blockIdx.x == 0 && threadIdx.x == 0) {
-    if (g.layout_off[0] != 0 || g.layout_off[g.n_layouts] != g.n) bad = 1;
-    for (int l = 0; l < g.n_layouts; ++l)
-      if (g.layout_off[l] > g.layout_off[l + 1]) bad = 1;
-  }
-  if (bad) atomicOr(&w.ctl->err, kErrGraph);
+  return false;
 }
 
 // One simplification round r >= 1: push the decrements of the frontier
@@ -203,7 +196,7 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 //     neighbours of the previous round (frontier queue).
 // Then union-find connected components over CE ∪ SE of the kept vertices.
 __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g, Workspace w, int k,
-                                                                 int* colors, long long* counts) {
+                                                                    int* colors, long long* counts, int validate) {
   GridBarrier grid(&w.ctl->bar[0]);
   stamp(w.ctl, 12);
   const int n = g.n;
@@ -212,12 +205,20 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
   Control* ctl = w.ctl;
   for (int l = tid; l < 2 * g.n_layouts; l += nth) counts[l] = 0;
 
-  // rounds 0 and 1, recovery priorities, union-find init
+  // rounds 0 and 1, recovery priorities, union-find init (and the optional
+  // validation of the input, fused into this first pass over the CSR)
   int hidden0 = 0;
+  bool bad = false;
+  if (validate && tid == 0) {
+    if (g.layout_off[0] != 0 || g.layout_off[g.n_layouts] != g.n) bad = true;
+    for (int l = 0; l < g.n_layouts; ++l)
+      if (g.layout_off[l] > g.layout_off[l + 1]) bad = true;
+  }
   for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += nth) {
     const int v = v0 + threadIdx.x;
     int take = 0;
     if (v < n) {
+      if (validate) bad |= vertex_invalid(g, v);
       const int a = g.ce_rp[v], b = g.ce_rp[v + 1];
       const bool st = g.se_rp[v + 1] > g.se_rp[v];
       const int lo = layout_index(g, v);
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
         int d0 = 0;  // live degree after round 0
         for (int e = a; e < b; ++e) {
           const int u = g.ce_col[e];
+          if ((unsigned)u >= (unsigned)n) continue;  // invalid input (flagged when validating)
           d0 += (g.se_rp[u + 1] > g.se_rp[u] || g.ce_rp[u + 1] - g.ce_rp[u] >= k) ? 1 : 0;
         }
         w.deg[v] = d0;
@@ -244,8 +246,10 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
   }
   hidden0 = __reduce_add_sync(0xffffffffu, hidden0);
   if ((threadIdx.x & 31) == 0 && hidden0) atomicAdd(&ctl->n_hidden, hidden0);
+  if (bad) atomicOr(&ctl->err, kErrGraph);
   grid.sync();
   stamp(w.ctl, 0);
+  if (__ldcg(&ctl->err)) return;  // invalid input: every later kernel exits too
 
   // rounds r >= 1: push the frontier's decrements
   int r = 1;
@@ -379,6 +383,7 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
 __global__ void __launch_bounds__(1024, 2) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
   GridBarrier grid(&w.ctl->bar[1]);
   stamp(w.ctl, 13);
+  if (__ldcg(&w.ctl->err)) return;
   const int nth = gridDim.x * blockDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Control* ctl = w.ctl;
@@ -448,7 +453,8 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
                                                      int launches) {
   const int nth = gridDim.x * blockDim.x;
   stamp(w.ctl, 15);
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += nth) {
+  const int vend = __ldcg(&w.ctl->err) ? 0 : g.n;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < vend; v += nth) {
     const int cv = colors[v];
     int nc = 0, ns = 0;
     const int e1 = g.ce_rp[v + 1];
@@ -498,15 +504,10 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
 
 }  // namespace
 
-cudaError_t launch_validate(const GraphView& g, Workspace ws, cudaStream_t s, int blocks) {
-  mpld_validate<<<blocks, 256, 0, s>>>(g, ws);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors, long long* counts,
-                                       cudaStream_t s, int blocks, int threads) {
+                                       int validate, cudaStream_t s, int blocks, int threads) {
   GraphView gg = g;
-  void* args[] = {&gg, &ws, &k, &colors, &counts};
+  void* args[] = {&gg, &ws, &k, &colors, &counts, &validate};
   return cudaLaunchCooperativeKernel((void*)mpld_simplify_components, dim3(blocks), dim3(threads), args, 0, s);
 }
 

@@ -2,7 +2,6 @@
 // the launch sequence of the hot path.
 //
 // Launch sequence of one call (all on one stream, no host synchronisation):
-//   [mpld_validate]            optional (MPLD_FLAG_VALIDATE)
 //   mpld_simplify_components   cooperative: reset, simplification rounds, union-find
 //   mpld_exact_cover_search<K> persistent: one thread per component, dynamic queue
 //   mpld_recover               cooperative: LIFO recovery of hidden vertices
@@ -33,8 +32,8 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(MPLD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-enum KernelId { K_VALIDATE = 0, K_SIMPLIFY, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_COUNT };
-const char* kKernelNames[K_COUNT] = {"mpld_validate", "mpld_simplify_components", "mpld_exact_cover_search",
+enum KernelId { K_SIMPLIFY = 0, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_COUNT };
+const char* kKernelNames[K_COUNT] = {"mpld_simplify_components", "mpld_exact_cover_search",
                                      "mpld_exact_cover_search_heavy", "mpld_recover", "mpld_evaluate"};
 
 constexpr int kCoopThreads = 1024;
@@ -174,15 +173,9 @@ int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, 
   // the control block (counters, barrier arrivals, error bits) starts every call at zero
   cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
   if (e != cudaSuccess) return cuda_fail(e, "control reset");
-  if (flags & MPLD_FLAG_VALIDATE) {
-    TimedLaunch t(ctx, K_VALIDATE, s);
-    e = launch_validate(g, ws, s, ctx->blocks_stream);
-    if (e != cudaSuccess) return cuda_fail(e, "mpld_validate");
-    t.done();
-    ++ctx->call_launches;
-  }
   TimedLaunch t(ctx, K_SIMPLIFY, s);
-  e = launch_simplify_components(g, ws, k, colors, counts, s, ctx->blocks_simplify, kCoopThreads);
+  e = launch_simplify_components(g, ws, k, colors, counts, (flags & MPLD_FLAG_VALIDATE) ? 1 : 0, s,
+                                 ctx->blocks_simplify, kCoopThreads);
   if (e != cudaSuccess) return cuda_fail(e, "mpld_simplify_components");
   t.done();
   ++ctx->call_launches;

@@ -108,9 +108,8 @@ __host__ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
 
 // launch wrappers (kernels_graph.cu, kernel_search.cu); each returns the
 // cudaError_t of its launch.
-cudaError_t launch_validate(const GraphView& g, Workspace ws, cudaStream_t s, int blocks);
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors,
-                                       long long* counts, cudaStream_t s, int blocks, int threads);
+                                       long long* counts, int validate, cudaStream_t s, int blocks, int threads);
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
                           int shard_index, int shard_count, int* colors, cudaStream_t s, int blocks);
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
