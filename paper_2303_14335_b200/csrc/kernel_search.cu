@@ -37,9 +37,11 @@ namespace mpld {
 
 namespace {
 
-constexpr unsigned kLightSteps = 96;  // exact mode: thread-level budget before a component turns heavy
-constexpr int kTarget = 96;           // heavy: frontier size that stops the level-synchronous split
-constexpr int kCap = 192;             // heavy: frontier capacity per level buffer
+#ifndef MPLD_HEAVY_TARGET
+#define MPLD_HEAVY_TARGET 96
+#endif
+constexpr int kTarget = MPLD_HEAVY_TARGET;  // heavy: frontier size that stops the level-synchronous split
+constexpr int kCap = 2 * kTarget;           // heavy: frontier capacity per level buffer
 constexpr unsigned kHeavyLaneCap = 1u << 22;  // exact mode safety cap: search nodes per lane per component
 
 template <typename W>
@@ -305,7 +307,7 @@ __device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* 
 template <int K>
 __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
                                                               long long max_steps, int shard_index,
-                                                              int shard_count, int* colors) {
+                                                              int shard_count, int* colors, unsigned light_steps) {
   extern __shared__ __align__(16) unsigned char lsmem[];
   Control* ctl = w.ctl;
   const int n_comp = __ldcg(&ctl->err) ? 0 : __ldcg(&ctl->n_comp);
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
     ctl->t[14] = t;
   }
   const bool exact = max_steps <= 0;
-  const unsigned budget = exact ? kLightSteps
+  const unsigned budget = exact ? light_steps
                                 : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
   int order[kMaxComp];
   unsigned long long adjm[kMaxComp], sadjm[kMaxComp];
@@ -469,6 +471,7 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     s_next = 0;
   }
   __syncwarp();
+  const long long hc0 = clock64();
   // level-synchronous split of the canonical tree, DFS order preserved
   int m = 1, cur = 0;
   unsigned expanded = 0;
@@ -502,6 +505,7 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     m = total;
     __syncwarp();
   }
+  const long long hc1 = clock64();
   // lanes search the subtrees in DFS order with a shared incumbent
   Frame<W>* stack = (Frame<W>*)(smem + 2 * kMaxComp * sizeof(unsigned long long) +
                                 2 * kCap * sizeof(Node<MPLD_MAX_K, unsigned long long>)) + lane;
@@ -530,6 +534,12 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     capped |= trunc;
   }
   const bool any_capped = __any_sync(0xffffffffu, capped);
+  const long long hc2 = clock64();
+  if (lane == 0 && (unsigned long long)(hc2 - hc0) > ctl->dbg[5]) {  // diagnostics (racy by design)
+    atomicMax(&ctl->dbg[5], (unsigned long long)(hc2 - hc0));
+    ctl->dbg[6] = hc1 - hc0;
+    ctl->dbg[7] = ((unsigned long long)m << 32) | (unsigned)n;
+  }
   const unsigned long long win = warp_min_u64(my_best);
   const unsigned who = __ballot_sync(0xffffffffu, my_best == win && win != ~0ull);
   if (who && lane == __ffs(who) - 1 && win < ((unsigned long long)c1 << 32)) {
@@ -581,19 +591,20 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
 }  // namespace
 
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
-                          int shard_index, int shard_count, int* colors, cudaStream_t s, int blocks) {
+                          int shard_index, int shard_count, int* colors, unsigned light_steps, cudaStream_t s,
+                          int blocks) {
   switch (k) {
     case 2:
       mpld_exact_cover_search<2><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
-                                                                colors);
+                                                                colors, light_steps);
       break;
     case 3:
       mpld_exact_cover_search<3><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
-                                                                colors);
+                                                                colors, light_steps);
       break;
     case 4:
       mpld_exact_cover_search<4><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
-                                                                colors);
+                                                                colors, light_steps);
       break;
     default: return cudaErrorInvalidValue;
   }

@@ -10,6 +10,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -64,6 +65,7 @@ struct mpld_context {
   int k = 0;
   bool prepared = false;
   int call_launches = 0;
+  unsigned light_steps = kLightStepsDefault;  // MPLD_LIGHT_STEPS overrides (tuning)
   int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0;
   // host-API staging (device copies of host inputs / outputs)
   int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
@@ -192,8 +194,8 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
   if (e0 != cudaSuccess) return cuda_fail(e0, "heavy queue reset");
   {
     TimedLaunch t(ctx, K_SEARCH, s);
-    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, shard_index, shard_count, colors, s,
-                                  ctx->blocks_search);
+    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, shard_index, shard_count, colors,
+                                  ctx->light_steps, s, ctx->blocks_search);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
     t.done();
     ++ctx->call_launches;
@@ -296,6 +298,10 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   ctx->blocks_recover = coop_blocks_recover(kCoopThreads, ctx->num_sms);
   ctx->blocks_search = resident_blocks_search(32, ctx->num_sms);
   ctx->blocks_stream = ctx->num_sms * 8;
+  if (const char* ls = std::getenv("MPLD_LIGHT_STEPS")) {
+    const long v = std::strtol(ls, nullptr, 10);
+    if (v >= 1 && v <= (1L << 24)) ctx->light_steps = (unsigned)v;
+  }
   e = configure_search_heavy();
   if (e != cudaSuccess) {
     mpld_context_destroy(ctx);

@@ -111,7 +111,9 @@ __host__ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors,
                                        long long* counts, int validate, cudaStream_t s, int blocks, int threads);
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
-                          int shard_index, int shard_count, int* colors, cudaStream_t s, int blocks);
+                          int shard_index, int shard_count, int* colors, unsigned light_steps, cudaStream_t s,
+                          int blocks);
+constexpr unsigned kLightStepsDefault = 48;  // exact mode: one-lane budget before a component turns heavy
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
                                 int blocks);
 cudaError_t configure_search_heavy();
