@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mpld", choices=["mpld", "reference"])
-    ap.add_argument("--replicas", type=int, default=16, help="ISCAS-85 suites per step per rank")
+    ap.add_argument("--replicas", type=int, default=None,
+                    help="seeds of the configuration per step per rank (default 16 for configs[1], else 1)")
+    ap.add_argument("--config", type=int, default=1, choices=[1, 2, 3], help="BASELINE.json configs[] index")
     ap.add_argument("--max-steps", type=int, default=MAX_STEPS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -55,17 +57,26 @@ def parse():
     return ap.parse_args()
 
 
+CONFIG = 1  # BASELINE.json configs[] index of the workload (set by --config)
+WORKLOADS = {
+    1: "configs[1]: ISCAS-85-shaped TPLD suite c432..c7552 (Table 1 |V|,|E|) x%d seeds per rank, k=3, "
+       "alpha=0.1, stitch candidates",
+    2: "configs[2]: QPLD k=4 on the s38584-scale (Table 1 |V|,|E|) ISCAS-89-shaped layout, components up to "
+       "~40 vertices, alpha=0.1, x%d seeds per rank",
+    3: "configs[3]: TPLD k=3 on a 10^6-polygon industrial-scale layout, alpha=0.1, x%d seeds per rank",
+}
+
+
 def workload(rank: int, replicas: int):
     graphs = []
     for r in range(replicas):
-        gs, k, alpha = synth.config_graphs(1, seed=1000 * rank + 10 * r)
+        gs, k, alpha = synth.config_graphs(CONFIG, seed=1000 * rank + 10 * r)
         graphs += gs
-    return synth.concat(graphs, name="iscas85_x%d" % replicas), k, alpha
+    return synth.concat(graphs, name="cfg%d_x%d" % (CONFIG, replicas)), k, alpha
 
 
 def config_dict(b, replicas, n_gpus, extra=None):
-    d = {"workload": "configs[1]: ISCAS-85-shaped TPLD suite c432..c7552 (Table 1 |V|,|E|) x%d seeds per rank,"
-                     " k=3, alpha=0.1, stitch candidates" % replicas,
+    d = {"workload": WORKLOADS[CONFIG] % replicas,
          "layouts_per_step": int(b.n_layouts), "vertices_per_step": int(b.n),
          "ce_edges_per_step": int(b.n_ce), "se_edges_per_step": int(b.n_se),
          "max_steps": MAX_STEPS, "l2": "flushed between timed steps (256 MiB write)",
@@ -158,6 +169,9 @@ def run_cpu_baseline(layouts, k, alpha, seconds):
     """The oracle as it stands, single-threaded, on the first layouts of the batch
     until `seconds` of CPU work (bounded sample)."""
     import oracle
+    if layouts and layouts[0].n > 300_000:  # a single layout alone exceeds the bounded CPU sample
+        return {"value": None, "unit": METRIC, "cores": 1, "kind": "oracle",
+                "sample": "skipped: one layout of %d vertices exceeds the bounded CPU sample" % layouts[0].n}
     comps = done = 0
     t0 = time.perf_counter()
     for g in layouts:
@@ -204,9 +218,15 @@ def main_reference(args):
 
 
 def main():
+    global CONFIG
     args = parse()
+    CONFIG = args.config
+    if args.replicas is None:
+        args.replicas = 16 if CONFIG == 1 else 1
     if args.impl == "reference":
         return main_reference(args)
+    if CONFIG == 3:  # the 10^6-polygon layout: a large per-vertex CPU sample is out of reach, use 5 s
+        args.cpu_seconds = min(args.cpu_seconds, 5.0)
     import torch
     import torch.distributed as dist
 

@@ -1,11 +1,13 @@
 // Internal declarations of the MPLD CUDA library (not part of the C ABI).
 //
 // Data layout in HBM:
-//   graph   : caller's CSR arrays (int32), read-only.
-//   per-vertex workspace (int32 [n] each): deg, hround, hid, parent, loc
-//   per-round : rcnt[n+2] (vertices hidden in round r), roff[n+2] (their offset in hid)
-//   per-component : roots[n]
-//   Control : one Control block (counters, error bits) per context.
+//   graph     : caller's CSR arrays (int32), read-only.
+//   per vertex: deg, hround, prio, parent, loc (int32), key (u64) — indexed by vertex id
+//   queues    : q0, q1 (int32 [n]) — simplification frontiers, recovery levels,
+//               heavy-component list (root, light-phase cost) in between
+//   per comp. : roots (int32 [n]); heavy scratch: hmask/horder/hn (kHeavyScratch slots)
+//   Control   : one control block (counters, barrier arrivals, error bits,
+//               diagnostics) per context, zeroed at the start of every call.
 #pragma once
 
 #include <cuda_runtime.h>
