@@ -36,7 +36,11 @@ Search (Alg. 1 lines 5-19, readings R4-R7):
     canonical optimum (DESIGN.md R6);
   * branch and bound on the Eq. (1a) objective in integer cost units
     (W_CONF per conflict, W_STITCH per stitch): a node is pruned when
-    cost + W_CONF * (#columns with zero live rows) >= best;
+    cost + W_CONF * (#columns with zero live rows + clique deficit) >= best,
+    the clique deficit (k >= 4 only) summing, over the greedy disjoint cliques
+    of >= k vertices of the component (clique_partition below),
+    max(0, |X| - |live masks of X|) for X = the clique's uncovered columns that
+    still have a live row;
   * the result is the first minimum-cost leaf in this search order;
   * budget: every node entry is one step; once a leaf exists and steps exceed
     max_steps (> 0), the search stops and returns the best leaf so far.
@@ -145,6 +149,32 @@ class DLXMatrix:
         return out
 
 
+def clique_partition(n: int, ce_edges, minsize: int = 2):
+    """Greedy disjoint maximal cliques of the component (bound of R7): for v in
+    index order, if v is unused, Q = {v}; add the smallest unused vertex adjacent
+    to all of Q while one exists; keep Q (and mark it used) if |Q| >= minsize."""
+    nb = [set() for _ in range(n)]
+    for u, w in ce_edges:
+        nb[u].add(w)
+        nb[w].add(u)
+    used = [False] * n
+    cliques = []
+    for v in range(n):
+        if used[v]:
+            continue
+        Q = [v]
+        cand = {u for u in nb[v] if not used[u]}
+        while cand:
+            u = min(cand)
+            Q.append(u)
+            cand &= nb[u]
+        if len(Q) >= minsize:
+            cliques.append(Q)
+            for u in Q:
+                used[u] = True
+    return cliques
+
+
 def algorithm_x(n: int, k: int, ce_edges, se_adj, w_conf: int, w_stitch: int,
                 max_steps: int = 0, matrix: DLXMatrix | None = None):
     """Relaxed Algorithm X with branch and bound (module docstring).
@@ -158,6 +188,18 @@ def algorithm_x(n: int, k: int, ce_edges, se_adj, w_conf: int, w_stitch: int,
     color = [-1] * n
     INF = float("inf")
     st = {"best": INF, "colors": None, "n_conf": 0, "n_stitch": 0, "steps": 0, "truncated": False}
+    # R7: the clique term is used for k >= 4, over cliques of >= k vertices
+    cliques = clique_partition(n, ce_edges, minsize=k) if k >= 4 else []
+
+    def clique_deficit():
+        """sum over cliques of max(0, |X| - |live masks of X|), X = uncovered
+        columns of the clique with at least one live row (R7)"""
+        total = 0
+        for Q in cliques:
+            X = [v for v in Q if not covered[1 + v] and S[1 + v] > 0]
+            masks = {r % k for v in X for r in M.live_rows(1 + v)}
+            total += max(0, len(X) - len(masks))
+        return total
 
     def search(cost, n_conf, n_stitch, maxused):
         st["steps"] += 1
@@ -180,7 +222,7 @@ def algorithm_x(n: int, k: int, ce_edges, se_adj, w_conf: int, w_stitch: int,
             elif S[col] == 1 and not one:
                 one = col
             col = R[col]
-        if cost + w_conf * n_zero >= st["best"]:  # bound: each zero-row column costs >= 1 conflict
+        if st["best"] != INF and cost + w_conf * (n_zero + clique_deficit()) >= st["best"]:  # bound (R7)
             return
         cl = zero or one or R[h]  # Alg. 1 line 8
         v = cl - 1

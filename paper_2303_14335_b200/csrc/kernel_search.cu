@@ -106,6 +106,62 @@ __device__ __forceinline__ void live_counts(const W (&B)[K], W U, W& Z, W& O) {
   O = s1 & ~s2;
 }
 
+// Greedy disjoint maximal cliques of a component (bound of R7, identical to
+// oracle.dlx.clique_partition): for v in index order, if unused, Q = {v} grown
+// by the smallest unused vertex adjacent to all of Q; kept if |Q| >= minsize.
+// cl[q * cs] receives the clique masks; returns their number (<= n / 2).
+template <typename W>
+__device__ int clique_partition(const W* adj, int as, int n, W* cl, int cs, int minsize) {
+  using O = WordOps<W>;
+  W used = 0;
+  int ncl = 0;
+  for (int v = 0; v < n; ++v) {
+    const W bv = W(1) << v;
+    if (used & bv) continue;
+    W Q = bv, cand = adj[v * as] & ~used;
+    while (cand) {
+      const int u = O::ffs(cand);
+      Q |= W(1) << u;
+      cand &= adj[u * as];
+    }
+    if (O::popc(Q) >= minsize) {
+      cl[ncl * cs] = Q;
+      ++ncl;
+      used |= Q;
+    }
+  }
+  return ncl;
+}
+
+// The clique term of the bound is used for k >= 4 only, over cliques of at
+// least k vertices (R7; measured: for k = 3 it saves ~8 % of the nodes but costs
+// more than that per node, for k = 4 it makes the hardest QPLD component of
+// configs[2] finish — 16.7 M nodes instead of > 134 M).
+template <int K>
+__host__ __device__ constexpr int clique_min() {
+  return K >= 4 ? K : 0;  // 0: no cliques
+}
+
+// Lower bound of R7 in conflicts: columns with no live row, plus, over the
+// cliques, max(0, |X| - #masks live on X) for X = the clique's uncovered
+// columns that still have a live row.
+template <int K, typename W>
+__device__ __forceinline__ int bound_conflicts(const W (&B)[K], W U, W Z, const W* cl, int cs, int ncl) {
+  using O = WordOps<W>;
+  int lb = O::popc(Z);
+  if constexpr (clique_min<K>() > 0) {
+    for (int q = 0; q < ncl; ++q) {
+      const W X = cl[q * cs] & U & ~Z;
+      if (!X) continue;
+      int live = 0;
+#pragma unroll
+      for (int c = 0; c < K; ++c) live += (X & ~B[c]) ? 1 : 0;
+      lb += max(0, O::popc(X) - live);
+    }
+  }
+  return lb;
+}
+
 // Incumbent of the sequential search: strict improvement, prune on lb >= best.
 struct SeqIncumbent {
   int best = INT_MAX;
@@ -145,7 +201,8 @@ struct ParIncumbent {
 template <int K, typename W, typename Inc>
 __device__ unsigned dfs(const W* __restrict__ am_adj, const W* __restrict__ am_sadj, int as, W (&C)[K], W (&B)[K],
                         W U, int cost, int maxused, int w_stitch, unsigned max_steps,
-                        Frame<W>* __restrict__ stack, int ss, Inc& inc, W (&bestC)[K], bool& truncated) {
+                        Frame<W>* __restrict__ stack, int ss, const W* __restrict__ cl, int cs, int ncl,
+                        Inc& inc, W (&bestC)[K], bool& truncated) {
   using O = WordOps<W>;
   int depth = 0;
   unsigned steps = 0;
@@ -167,7 +224,7 @@ __device__ unsigned dfs(const W* __restrict__ am_adj, const W* __restrict__ am_s
       } else {
         W Z, Ol;
         live_counts<K, W>(B, U, Z, Ol);
-        if (!inc.prune(cost + kCostUnits * O::popc(Z))) {  // bound (R7)
+        if (!inc.prune(cost + kCostUnits * bound_conflicts<K, W>(B, U, Z, cl, cs, ncl))) {  // bound (R7)
           const W cand = Z ? Z : (Ol ? Ol : U);  // Alg. 1 line 8 (R5)
           const int v = O::ffs(cand);
           if (depth > 0) {  // spill the parent frame
@@ -236,7 +293,7 @@ __device__ __forceinline__ int colour_of(const W (&bestC)[K], int i) {
 // Per-lane search storage of the thread-per-component kernel: one warp per
 // CTA, arrays lane-interleaved in shared memory (element i of lane l at
 // i * 32 + l) so the search never touches local memory.
-constexpr int kLightSmem = 2 * kMaxComp * 32 * 8 + kMaxComp * 32 * 16;
+constexpr int kLightSmem = 2 * kMaxComp * 32 * 8 + kMaxComp * 32 * 16 + (kMaxComp / 2) * 32 * 8;
 
 template <int K, typename W>
 __device__ unsigned run_light(const unsigned long long* adjm, const unsigned long long* sadjm, int n, int w_stitch,
@@ -245,6 +302,7 @@ __device__ unsigned run_light(const unsigned long long* adjm, const unsigned lon
   W* a = (W*)smem + lane;
   W* s = a + kMaxComp * 32;
   Frame<W>* stack = (Frame<W>*)(smem + 2 * kMaxComp * 32 * 8) + lane;
+  W* cl = (W*)(smem + 2 * kMaxComp * 32 * 8 + kMaxComp * 32 * 16) + lane;
   for (int i = 0; i < n; ++i) {
     a[i * 32] = (W)adjm[i];
     s[i * 32] = (W)sadjm[i];
@@ -253,8 +311,9 @@ __device__ unsigned run_light(const unsigned long long* adjm, const unsigned lon
 #pragma unroll
   for (int c = 0; c < K; ++c) C[c] = B[c] = bestC[c] = 0;
   SeqIncumbent inc;
+  const int ncl = clique_min<K>() ? clique_partition<W>(a, 32, n, cl, 32, clique_min<K>()) : 0;
   const unsigned steps = dfs<K, W, SeqIncumbent>(a, s, 32, C, B, WordOps<W>::full(n), 0, -1, w_stitch, budget,
-                                                 stack, 32, inc, bestC, trunc);
+                                                 stack, 32, cl, 32, ncl, inc, bestC, trunc);
   for (int i = 0; i < n; ++i) cval[i] = colour_of<K, W>(bestC, i);
   best_cost = inc.best;
   return steps;
@@ -413,7 +472,8 @@ __device__ __forceinline__ int warp_excl_scan(int x, int& total) {
 // Expand node nd: number of children (0 pruned, 1 for a leaf itself) and, if
 // out != nullptr, write them in DFS (colour) order.
 template <int K, typename W>
-__device__ int expand(const Node<K, W>& nd, const W* s_adj, const W* s_sadj, int w_stitch, int bound,
+__device__ int expand(const Node<K, W>& nd, const W* s_adj, const W* s_sadj, const W* cl, int ncl, int w_stitch,
+                      int bound,
                       Node<K, W>* out) {
   using O = WordOps<W>;
   if (nd.U == 0) {
@@ -422,7 +482,8 @@ __device__ int expand(const Node<K, W>& nd, const W* s_adj, const W* s_sadj, int
   }
   W Z, Ol;
   live_counts<K, W>(nd.B, nd.U, Z, Ol);
-  if (nd.cost + kCostUnits * O::popc(Z) >= bound) return 0;  // pruned against the light-phase incumbent
+  if (nd.cost + kCostUnits * bound_conflicts<K, W>(nd.B, nd.U, Z, cl, 1, ncl) >= bound)
+    return 0;  // pruned against the light-phase incumbent
   const W cand = Z ? Z : (Ol ? Ol : nd.U);
   const int v = O::ffs(cand);
   const W bit = W(1) << v;
@@ -454,11 +515,17 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
   Node<K, W>* lvl[2] = {(Node<K, W>*)(smem + 2 * kMaxComp * sizeof(unsigned long long)), nullptr};
   lvl[1] = lvl[0] + kCap;
   __shared__ unsigned long long s_best;
-  __shared__ int s_next;
+  __shared__ int s_next, s_ncl;
+  __shared__ unsigned long long s_cl64[kMaxComp / 2];
+  W* s_cl = (W*)s_cl64;
   for (int i = lane; i < n; i += 32) {
     s_adj[i] = (W)s_adj64[i];
     s_sadj[i] = (W)s_sadj64[i];
   }
+  __syncwarp();
+  if (lane == 0) s_ncl = clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, clique_min<K>()) : 0;
+  __syncwarp();
+  const int ncl = s_ncl;
   if (lane == 0) {
     Node<K, W> root;
 #pragma unroll
@@ -480,7 +547,7 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     bool inner = false;  // some node still has uncovered columns
     for (int i0 = 0; i0 < m; i0 += 32) {
       const int i = i0 + lane;
-      const int cnt = i < m ? expand<K, W>(lvl[cur][i], s_adj, s_sadj, w_stitch, c1, nullptr) : 0;
+      const int cnt = i < m ? expand<K, W>(lvl[cur][i], s_adj, s_sadj, s_cl, ncl, w_stitch, c1, nullptr) : 0;
       inner |= __any_sync(0xffffffffu, i < m && lvl[cur][i].U != 0 && cnt > 0);
       int t;
       warp_excl_scan(cnt, t);
@@ -494,10 +561,10 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     int base = 0;
     for (int i0 = 0; i0 < m; i0 += 32) {
       const int i = i0 + lane;
-      const int cnt = i < m ? expand<K, W>(lvl[cur][i], s_adj, s_sadj, w_stitch, c1, nullptr) : 0;
+      const int cnt = i < m ? expand<K, W>(lvl[cur][i], s_adj, s_sadj, s_cl, ncl, w_stitch, c1, nullptr) : 0;
       int t;
       const int off = warp_excl_scan(cnt, t);
-      if (cnt) expand<K, W>(lvl[cur][i], s_adj, s_sadj, w_stitch, c1, &lvl[cur ^ 1][base + off]);
+      if (cnt) expand<K, W>(lvl[cur][i], s_adj, s_sadj, s_cl, ncl, w_stitch, c1, &lvl[cur ^ 1][base + off]);
       base += t;
     }
     expanded += m;
@@ -529,7 +596,7 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     inc.lane_best = my_best;
     bool trunc;
     steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, 1, nd.C, nd.B, nd.U, nd.cost, nd.mu, w_stitch,
-                                     kHeavyLaneCap - steps, stack, 32, inc, bestC, trunc);
+                                     kHeavyLaneCap - steps, stack, 32, s_cl, 1, ncl, inc, bestC, trunc);
     my_best = inc.lane_best;
     capped |= trunc;
   }

@@ -185,6 +185,39 @@ def test_budget_semantics():
         assert again["colors"] == full["colors"] and not again["truncated"]
 
 
+def test_bound_is_a_lower_bound():
+    """R7's bound (zero-live columns + clique deficit over oracle.dlx.clique_partition)
+    never exceeds the cheapest completion of a partial colouring (brute force)."""
+    import itertools
+    from oracle.dlx import clique_partition
+    rng = random.Random(21)
+    for trial in range(300):
+        n = rng.randint(2, 7)
+        k = rng.randint(2, 4)
+        ce, _ = random_graph(rng, n, rng.choice([0.5, 0.8]))
+        adj = [set() for _ in range(n)]
+        for u, v in ce:
+            adj[u].add(v)
+            adj[v].add(u)
+        colored = {v: rng.randrange(k) for v in rng.sample(range(n), rng.randint(0, n - 1))}
+        live = {v: {c for c in range(k) if all(colored.get(u) != c for u in adj[v])}
+                for v in range(n) if v not in colored}
+        zero = sum(1 for v in live if not live[v])
+        deficit = 0
+        for Q in clique_partition(n, ce):
+            X = [v for v in Q if v in live and live[v]]
+            deficit += max(0, len(X) - len(set().union(*[live[v] for v in X])))
+        free = [v for v in range(n) if v not in colored]
+        best = None
+        for assign in itertools.product(range(k), repeat=len(free)):
+            col = dict(colored)
+            col.update(zip(free, assign))
+            # conflicts not yet paid: edges with at least one uncoloured endpoint
+            c = sum(1 for u, v in ce if col[u] == col[v] and (u in live or v in live))
+            best = c if best is None else min(best, c)
+        assert zero + deficit <= best, (n, k, ce, colored)
+
+
 # ---------------------------------------------------------------- Eq. (2) round trip
 def test_dlx_cover_uncover_round_trip():
     """PAPER.md Eq. (2): Uncover is the exact inverse of Cover under LIFO."""
