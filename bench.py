@@ -335,10 +335,12 @@ def main():
     d2h = b.n * 4 + L * 8 * 3 + 8 * len(mp.STAT_NAMES)
 
     # aggregate over ranks
-    work = "max" if shard else "sum"  # shard mode: every rank holds the same batch
+    # components: every rank counts the ones it searched (shard mode: disjoint
+    # shards of one batch) -> sum; layouts: shard mode holds the same batch on
+    # every rank -> max
     comps_all, ms_max, e2e_comps_all, e2e_ms_max, layouts_all = aggregate(
         [comps_per_step * args.steps, total_ms, comps_per_step * e2e_steps, e2e_s * 1e3, L],
-        [work, "max", work, "max", work], world, dev)
+        ["sum", "max", "sum", "max", "max" if shard else "sum"], world, dev)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

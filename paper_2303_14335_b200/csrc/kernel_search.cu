@@ -323,15 +323,17 @@ __device__ unsigned run_light(const unsigned long long* adjm, const unsigned lon
 // order of G, neighbours over CE ∪ SE in ascending id, R5).  Every head's
 // neighbours are handled in batches whose global loads (ids, rounds, local
 // indices) are independent and in flight together, so a head costs a few
-// memory round trips instead of two per neighbour.  ASSIGN: discover vertices
-// and write loc[]; otherwise loc[] already holds the BFS positions (rebuild).
-// Returns n, or -1 when the component exceeds kMaxComp.
+// memory round trips instead of two per neighbour.  ASSIGN: the BFS starts at a
+// seed (a kept vertex without smaller kept neighbour) and discovers the
+// component, looking vertices up in its own order list; it gives up (-2) as
+// soon as it meets a vertex smaller than the seed — that component belongs to
+// the seed that is its minimum.  Otherwise loc[] already holds the BFS
+// positions (rebuild).  Returns n, -1 when the component exceeds kMaxComp, or -2.
 template <bool ASSIGN>
 __device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* order, unsigned long long* adjm,
                          unsigned long long* sadjm) {
   int n = 1;
   order[0] = root;
-  if (ASSIGN) w.loc[root] = 0;
   for (int head = 0; head < n; ++head) {
     const int v = order[head];
     unsigned long long adj = 0ull, sadj = 0ull;
@@ -343,15 +345,22 @@ __device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* 
       if (b >= be || (a < ae && g.ce_col[a] < g.se_col[b])) { u = g.ce_col[a++]; is_ce = true; }
       else { u = g.se_col[b++]; is_ce = false; }
       if (w.hround[u] != -1) continue;
-      int lu = w.loc[u];
+      int lu;
       if (ASSIGN) {
+        if (u < root) return -2;  // not the component's minimum
+        lu = -1;
+        for (int j = 0; j < n; ++j)
+          if (order[j] == u) {
+            lu = j;
+            break;
+          }
         if (lu < 0) {
           if (n == kMaxComp) return -1;
           lu = n;
-          w.loc[u] = n;
           order[n++] = u;
         }
       } else {
+        lu = w.loc[u];
         order[lu] = u;  // seen before the BFS head reaches its position
         n = max(n, lu + 1);
       }
@@ -369,7 +378,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
                                                               int shard_count, int* colors, unsigned light_steps) {
   extern __shared__ __align__(16) unsigned char lsmem[];
   Control* ctl = w.ctl;
-  const int n_comp = __ldcg(&ctl->err) ? 0 : __ldcg(&ctl->n_comp);
+  const int n_seed = __ldcg(&ctl->err) ? 0 : __ldcg(&ctl->n_seed);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -383,11 +392,14 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
   unsigned long long acc_steps = 0ull;
   int acc_maxn = 0, acc_maxsteps = 0;
   unsigned acc_trunc = 0;
-  for (int ci = blockIdx.x * blockDim.x + threadIdx.x; ci < n_comp; ci += gridDim.x * blockDim.x) {
+  unsigned acc_comp = 0;
+  for (int ci = blockIdx.x * blockDim.x + threadIdx.x; ci < n_seed; ci += gridDim.x * blockDim.x) {
     const long long c0 = clock64();
     const int root = w.roots[ci];
     if (shard_count > 1 && (int)(lowbias32((uint32_t)root) % (uint32_t)shard_count) != shard_index) continue;
     const int n = bfs_build<true>(g, w, root, order, adjm, sadjm);
+    if (n == -2) continue;  // the seed is not its component's minimum
+    ++acc_comp;
     if (n < 0) {
       atomicOr(&ctl->err, kErrComponent);
       atomicMax(&ctl->max_comp, kMaxComp + 1);
@@ -410,7 +422,10 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
       ctl->dbg[3] = n;
       ctl->dbg[4] = steps;
     }
-    for (int i = 0; i < n; ++i) colors[order[i]] = cval[i];
+    for (int i = 0; i < n; ++i) {
+      colors[order[i]] = cval[i];
+      w.loc[order[i]] = i;  // BFS position (rebuild of heavy components beyond the scratch)
+    }
     acc_steps += steps;
     acc_maxn = max(acc_maxn, n);
     if (trunc && exact) {  // hand the component to the warp-parallel search
@@ -437,6 +452,8 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
   acc_maxn = __reduce_max_sync(0xffffffffu, acc_maxn);
   acc_maxsteps = __reduce_max_sync(0xffffffffu, acc_maxsteps);
   acc_trunc = __reduce_add_sync(0xffffffffu, acc_trunc);
+  acc_comp = __reduce_add_sync(0xffffffffu, acc_comp);
+  if ((threadIdx.x & 31) == 0 && acc_comp) atomicAdd(&ctl->n_comp, (int)acc_comp);
   if ((threadIdx.x & 31) == 0 && acc_maxn > 0) {
     atomicAdd(&ctl->steps, acc_steps);
     atomicMax(&ctl->max_comp, acc_maxn);

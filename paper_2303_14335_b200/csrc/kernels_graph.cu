@@ -1,5 +1,5 @@
 // Graph-level kernels of the MPLD hot path (§2.2 / Fig. 2 flow):
-//   mpld_simplify_components simplification (R8) + connected components (Alg. 1 lines 1-3)
+//   mpld_simplify_components simplification (R8) + component seeds (Alg. 1 lines 1-3)
 //   mpld_recover             recovery of the hidden vertices (R9)
 //   mpld_evaluate            Eq. (1) conflict / stitch counts and cost per layout
 //
@@ -100,28 +100,6 @@ __device__ __forceinline__ void list_push(int* items, int& cnt, int v, int* coun
   else out[atomicAdd(counter, 1)] = v;
 }
 
-__device__ __forceinline__ int find_root(int* parent, int x) {
-  int p = __ldcg(&parent[x]);
-  while (p != x) {
-    x = p;
-    p = __ldcg(&parent[x]);
-  }
-  return x;
-}
-
-// Lock-free union: the larger root is hooked under the smaller one, so every
-// final root is the minimum vertex id of its component.
-__device__ __forceinline__ void unite(int* parent, int a, int b) {
-  while (true) {
-    a = find_root(parent, a);
-    b = find_root(parent, b);
-    if (a == b) return;
-    if (a < b) { int t = a; a = b; b = t; }
-    int old = atomicCAS(&parent[a], a, b);
-    if (old == a) return;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Input invariants of include/mpld.h for vertex v (MPLD_FLAG_VALIDATE): both
 // rows strictly ascending, ids in range, no self loop, symmetric (binary search
@@ -148,11 +126,11 @@ __device__ bool vertex_invalid(const GraphView& g, int v) {
 
 // One simplification round r >= 1: push the decrements of the frontier
 // (items [first, cnt) with the given stride; every thread of the CTA calls it).
-__device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r, int cnt, int first, int stride) {
-  Control* ctl = w.ctl;
+__device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r, int cnt, int first, int stride,
+                           int* qc) {
   const int* cur = (r & 1) ? w.q1 : w.q0;
   int* nxt = (r & 1) ? w.q0 : w.q1;
-  int* ncnt = &ctl->qcnt[(r + 1) % 3];
+  int* ncnt = &qc[(r + 1) % 3];
   for (int i0 = first; i0 < cnt; i0 += stride) {
     const int i = i0 + threadIdx.x;
     int items[kAppend];
@@ -194,7 +172,7 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 //   * a vertex enters round r+1 (r >= 1) exactly when its live degree crosses
 //     k -> k-1 while round r is pushed, so each round only touches the
 //     neighbours of the previous round (frontier queue).
-// Then union-find connected components over CE ∪ SE of the kept vertices.
+// Then the seeds of the component search (see below).
 __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g, Workspace w, int k,
                                                                     int* colors, long long* counts, int validate) {
   GridBarrier grid(&w.ctl->bar[0]);
@@ -223,7 +201,6 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
       const bool st = g.se_rp[v + 1] > g.se_rp[v];
       const int lo = layout_index(g, v);
       w.prio[v] = lowbias32((uint32_t)(v - (g.n_layouts > 1 ? __ldg(&g.layout_off[lo]) : 0)));
-      w.parent[v] = v;
       colors[v] = -1;  // every vertex is coloured later by exactly one search shard or the recovery
       int hr = -1;
       if (!st && b - a < k) {
@@ -263,15 +240,17 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
       if (blockIdx.x == 0) {
         int rr = r, c = cnt;
         while (c > 0) {
+          // own counters: the other CTAs may still be reading qcnt[r % 3] to
+          // take this branch, so the tail must never reset that slot
           if (threadIdx.x == 0) {
-            ctl->qcnt[(rr + 2) % 3] = 0;
+            ctl->tcnt[(rr + 2) % 3] = 0;
             ctl->n_hidden += c;
           }
           dstamp(ctl, rr, c);
-          peel_round(g, w, k, rr, c, 0, blockDim.x);
+          peel_round(g, w, k, rr, c, 0, blockDim.x, ctl->tcnt);
           ++rr;
           __syncthreads();
-          c = __ldcg(&ctl->qcnt[rr % 3]);
+          c = __ldcg(&ctl->tcnt[rr % 3]);
         }
         if (threadIdx.x == 0) ctl->n_rounds = rr;
       }
@@ -284,7 +263,7 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
       ctl->n_hidden += cnt;
     }
     dstamp(ctl, r, cnt);
-    peel_round(g, w, k, r, cnt, blockIdx.x * blockDim.x, nth);
+    peel_round(g, w, k, r, cnt, blockIdx.x * blockDim.x, nth, ctl->qcnt);
     ++r;
     grid.sync();
     stamp(w.ctl, 2);
@@ -292,35 +271,37 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
   if (tid == 0) ctl->n_rounds = __ldcg(&ctl->n_hidden) ? r : 0;
   stamp(w.ctl, 1);
 
-  // union-find hooking over CE ∪ SE between kept vertices
-  for (int v = tid; v < n; v += nth) {
-    if (__ldcg(&w.hround[v]) != -1) continue;
-    for (int pass = 0; pass < 2; ++pass) {
-      const int* rp = pass ? g.se_rp : g.ce_rp;
-      const int* col = pass ? g.se_col : g.ce_col;
-      const int e1 = rp[v + 1];
-      for (int e = rp[v]; e < e1; ++e) {
-        const int u = col[e];
-        if (u < v && __ldcg(&w.hround[u]) == -1) unite(w.parent, u, v);
-      }
-    }
-  }
-  grid.sync();
-  stamp(w.ctl, 3);
-
-  // compress, list the roots (component order is irrelevant to the result)
+  // Pop keys, and the component search seeds: a kept vertex with no kept
+  // neighbour (CE ∪ SE) of smaller id.  Every component has at least one seed
+  // (its minimum); the search kernel's BFS from a seed keeps the component only
+  // if the seed is the component's minimum, so no union-find and no further
+  // grid barrier are needed here.
   for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += nth) {
     const int v = v0 + threadIdx.x;
-    int is_root = 0;
-    if (v < n) w.key[v] = pop_key(__ldcg(&w.hround[v]), w.prio[v]);
-    if (v < n && __ldcg(&w.hround[v]) == -1) {
-      const int root = find_root(w.parent, v);
-      w.parent[v] = root;
-      w.loc[v] = -1;  // BFS marker of the search kernel
-      is_root = root == v;
+    int seed = 0;
+    if (v < n) {
+      const int hv = __ldcg(&w.hround[v]);
+      w.key[v] = pop_key(hv, w.prio[v]);
+      if (hv == -1) {
+        seed = 1;
+        for (int pass = 0; pass < 2 && seed; ++pass) {
+          const int* rp = pass ? g.se_rp : g.ce_rp;
+          const int* col = pass ? g.se_col : g.ce_col;
+          const int e0 = rp[v];
+          // rows are ascending: only the first neighbours can be smaller than v
+          for (int e = e0, e1 = rp[v + 1]; e < e1; ++e) {
+            const int u = col[e];
+            if (u > v) break;
+            if (__ldcg(&w.hround[u]) == -1) {
+              seed = 0;
+              break;
+            }
+          }
+        }
+      }
     }
     int item = v;
-    cta_append(is_root, &item, &ctl->n_comp, w.roots);
+    cta_append(seed, &item, &ctl->n_seed, w.roots);
   }
 }
 
@@ -339,11 +320,10 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
 // One recovery level: colour the ready vertices cur[first..cnt) (stride),
 // queue the successors whose last predecessor this was.
 __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int* colors, int L, int cnt, int first,
-                              int stride) {
-  Control* ctl = w.ctl;
+                              int stride, int* qc) {
   const int* cur = (L & 1) ? w.q1 : w.q0;
   int* nxt = (L & 1) ? w.q0 : w.q1;
-  int* ncnt = &ctl->rq[(L + 1) % 3];
+  int* ncnt = &qc[(L + 1) % 3];
   for (int i0 = first; i0 < cnt; i0 += stride) {
     const int i = i0 + threadIdx.x;
     int items[kAppend];
@@ -428,18 +408,18 @@ __global__ void __launch_bounds__(1024, 2) mpld_recover(GraphView g, Workspace w
       if (blockIdx.x == 0) {
         int LL = L, c = cnt;
         while (c > 0) {
-          if (threadIdx.x == 0) ctl->rq[(LL + 2) % 3] = 0;
-          recover_level(g, w, k, colors, LL, c, 0, blockDim.x);
+          if (threadIdx.x == 0) ctl->trq[(LL + 2) % 3] = 0;  // own counters, as in the simplification tail
+          recover_level(g, w, k, colors, LL, c, 0, blockDim.x, ctl->trq);
           ++LL;
           __syncthreads();
-          c = __ldcg(&ctl->rq[LL % 3]);
+          c = __ldcg(&ctl->trq[LL % 3]);
         }
         if (threadIdx.x == 0) ctl->n_levels = LL;
       }
       break;  // no grid barrier needed: the kernel ends here
     }
     if (tid == 0) ctl->rq[(L + 2) % 3] = 0;
-    recover_level(g, w, k, colors, L, cnt, blockIdx.x * blockDim.x, nth);
+    recover_level(g, w, k, colors, L, cnt, blockIdx.x * blockDim.x, nth, ctl->rq);
     ++L;
     grid.sync();
     stamp(w.ctl, 9);

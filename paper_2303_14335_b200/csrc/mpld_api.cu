@@ -53,7 +53,6 @@ struct mpld_context {
   unsigned long long* key = nullptr;
   int* q0 = nullptr;
   int* q1 = nullptr;
-  int* parent = nullptr;
   int* loc = nullptr;
   int* roots = nullptr;
   unsigned long long* hmask = nullptr;
@@ -101,7 +100,7 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
   if (n > ctx->cap_n) {
     int64_t cap = std::max<int64_t>(n, ctx->cap_n * 3 / 2);
     cudaError_t e = cudaSuccess;
-    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->parent, &ctx->loc, &ctx->roots}) {
+    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->loc, &ctx->roots}) {
       e = grow(p, cap);
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
@@ -160,7 +159,7 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 }
 
 Workspace workspace(mpld_context* ctx) {
-  return Workspace{ctx->deg,    ctx->hround, ctx->key,   ctx->prio,   ctx->q0, ctx->q1, ctx->parent,
+  return Workspace{ctx->deg,    ctx->hround, ctx->key,   ctx->prio,   ctx->q0, ctx->q1,
                    ctx->loc,    ctx->roots,  ctx->hmask, ctx->horder, ctx->hn, ctx->ctl};
 }
 
@@ -328,7 +327,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
 void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->key, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
-                  (void*)ctx->parent, (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->hmask, (void*)ctx->horder, (void*)ctx->hn, (void*)ctx->ctl, (void*)ctx->h_lo,
+                  (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->hmask, (void*)ctx->horder, (void*)ctx->hn, (void*)ctx->ctl, (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
                   (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})
     if (p) cudaFree(p);

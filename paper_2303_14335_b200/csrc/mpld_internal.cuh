@@ -2,7 +2,7 @@
 //
 // Data layout in HBM:
 //   graph     : caller's CSR arrays (int32), read-only.
-//   per vertex: deg, hround, prio, parent, loc (int32), key (u64) — indexed by vertex id
+//   per vertex: deg, hround, prio, loc (int32), key (u64) — indexed by vertex id
 //   queues    : q0, q1 (int32 [n]) — simplification frontiers, recovery levels,
 //               heavy-component list (root, light-phase cost) in between
 //   per comp. : roots (int32 [n]); heavy scratch: hmask/horder/hn (kHeavyScratch slots)
@@ -28,7 +28,8 @@ enum ErrBits : int { kErrGraph = 1, kErrComponent = 2 };
 struct Control {
   int n_rounds;     // simplification rounds R (R8)
   int n_hidden;     // |hidden vertices|
-  int n_comp;       // components found
+  int n_comp;       // components found (counted by the search kernel)
+  int n_seed;       // component-search seeds listed in roots[]
   int max_comp;     // largest component
   int truncated;    // components whose search hit max_steps
   int err;          // ErrBits
@@ -36,6 +37,8 @@ struct Control {
   int max_steps_comp;        // largest per-component step count
   int qcnt[3];               // simplification frontier sizes (rotating by round)
   int rq[3];                 // recovery level sizes (rotating by level)
+  int tcnt[3];               // ... the same, for the single-CTA tails (never read by other CTAs)
+  int trq[3];
   int n_levels;              // recovery levels (DAG depth + 1)
   int n_heavy;               // exact mode: components handed to the warp-parallel search
   unsigned long long steps;  // search nodes entered
@@ -89,9 +92,8 @@ struct Workspace {
   unsigned* prio;  // lowbias32(layout-local id), recovery priority (R9)
   int* q0;         // frontier queues (double-buffered)
   int* q1;
-  int* parent;     // union-find
   int* loc;        // local index of a kept vertex inside its component
-  int* roots;      // component roots (min vertex id of the component)
+  int* roots;      // component-search seeds (kept vertices without a smaller kept neighbour)
   unsigned long long* hmask;  // heavy components kept by the light search: adj/sadj masks
   int* horder;                // ... their BFS orders
   int* hn;                    // ... their sizes
