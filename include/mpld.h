@@ -183,7 +183,10 @@ int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* laun
  * (depth of the pop-order DAG + 1), out[17] hidden vertices, out[18] rounds,
  * out[19] largest per-component step count, out[20..51] per round (0..15) / recovery
  * level (16..31) start stamps, out[52..83] their frontier sizes, out[84..91]
- * slowest search thread (cycles total, build, search; n; steps).  Copies min(n, 92). */
+ * slowest search warp (cycles total, build, search; n; steps) and slowest heavy
+ * warp (cycles total, split; subtrees << 32 | n), out[92] component-search seeds,
+ * out[93] heavy components, out[94] components, out[95] truncated searches.
+ * Copies min(n, 96). */
 int mpld_context_debug(mpld_context* ctx, int64_t* out, int n);
 
 #ifdef __cplusplus

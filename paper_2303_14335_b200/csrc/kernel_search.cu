@@ -18,8 +18,11 @@
 // Components of <= 32 vertices run on 32-bit words, larger ones on 64-bit.
 //
 // Two kernels:
-//   mpld_exact_cover_search<K>        one thread per component (sequential DFS,
-//                                     the oracle's exact node order and budget, R7);
+//   mpld_exact_cover_search<K>        one warp per component seed: warp-parallel
+//                                     discovery of the component, relabelling to
+//                                     the R5 column order, then the sequential DFS
+//                                     on lane 0 (the oracle's exact node order and
+//                                     budget, R7);
 //   mpld_exact_cover_search_heavy<K>  exact mode (max_steps <= 0) only: one warp
 //                                     per component whose thread-level search
 //                                     needed more than kLightSteps nodes.  The
@@ -290,46 +293,200 @@ __device__ __forceinline__ int colour_of(const W (&bestC)[K], int i) {
   return c;
 }
 
-// Per-lane search storage of the thread-per-component kernel: one warp per
-// CTA, arrays lane-interleaved in shared memory (element i of lane l at
-// i * 32 + l) so the search never touches local memory.
-constexpr int kLightSmem = 2 * kMaxComp * 32 * 8 + kMaxComp * 32 * 16 + (kMaxComp / 2) * 32 * 8;
+constexpr int kCompWarps = 4;  // warps per CTA of the component kernel (one component per warp)
 
-template <int K, typename W>
-__device__ unsigned run_light(const unsigned long long* adjm, const unsigned long long* sadjm, int n, int w_stitch,
-                              unsigned budget, unsigned char* smem, int* cval, int& best_cost, bool& trunc) {
+// Per-warp shared storage of the component kernel.
+struct __align__(16) WarpComp {
+  unsigned long long dadj[kMaxComp];   // CE masks in discovery labels; then the DFS stack (with dsadj)
+  unsigned long long dsadj[kMaxComp];  // SE masks in discovery labels
+  unsigned long long adj[kMaxComp];    // CE masks in BFS labels (R5); CE ∪ SE in rank labels while relabelling
+  unsigned long long sadj[kMaxComp];   // SE masks in BFS labels
+  unsigned long long cl[kMaxComp / 2];  // clique masks (R7); then the best leaf's C[c]
+  int verts[kMaxComp];                 // discovery index -> vertex id
+  int order[kMaxComp];                 // BFS position -> vertex id (the rank queue while relabelling)
+  int rank[kMaxComp];                  // discovery index -> rank of its id inside the component
+  int bpos[kMaxComp];                  // rank -> BFS position
+};
+static_assert(sizeof(Frame<unsigned long long>) * kMaxComp <= 2 * kMaxComp * sizeof(unsigned long long),
+              "the DFS stack lives in dadj/dsadj");
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ int warp_excl_scan(int x, int& total) {
   const int lane = threadIdx.x & 31;
-  W* a = (W*)smem + lane;
-  W* s = a + kMaxComp * 32;
-  Frame<W>* stack = (Frame<W>*)(smem + 2 * kMaxComp * 32 * 8) + lane;
-  W* cl = (W*)(smem + 2 * kMaxComp * 32 * 8 + kMaxComp * 32 * 16) + lane;
-  for (int i = 0; i < n; ++i) {
-    a[i * 32] = (W)adjm[i];
-    s[i * 32] = (W)sadjm[i];
+  int y = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int z = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) y += z;
   }
+  total = __shfl_sync(0xffffffffu, y, 31);
+  return y - x;
+}
+
+// Discovers the component of a seed (a kept vertex without a smaller kept
+// neighbour) with the whole warp: the CE and SE rows of up to 32 discovered
+// vertices are concatenated and read 32 entries at a time, so one group costs
+// three dependent memory round trips (row pointers, column ids, rounds)
+// whatever its degree.  The masks come out in discovery labels (dadj/dsadj,
+// verts).  Returns n, -1 when the component exceeds kMaxComp, or -2 as soon
+// as it meets a kept vertex smaller than the seed: that component belongs to
+// the seed that is its minimum.
+__device__ int warp_discover(const GraphView& g, const Workspace& w, int seed, WarpComp& s) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < kMaxComp; i += 32) s.dadj[i] = s.dsadj[i] = 0ull;
+  if (lane == 0) s.verts[0] = seed;
+  __syncwarp();
+  int n = 1;
+  for (int head = 0; head < n;) {
+    const int gsz = min(32, n - head);
+    int ca = 0, cn = 0, sa = 0, sn = 0;
+    if (lane < gsz) {
+      const int v = s.verts[head + lane];
+      ca = __ldg(&g.ce_rp[v]);
+      cn = __ldg(&g.ce_rp[v + 1]) - ca;
+      sa = __ldg(&g.se_rp[v]);
+      sn = __ldg(&g.se_rp[v + 1]) - sa;
+    }
+    int total;
+    const int excl = warp_excl_scan(cn + sn, total);
+    for (int b = 0; b < total; b += 32) {
+      const int item = b + lane;
+      int o = 0;  // owner: the last group lane whose row range starts at or before item
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1) {
+        const int e = __shfl_sync(0xffffffffu, excl, o + st);
+        if (e <= item) o += st;
+      }
+      const int off = item - __shfl_sync(0xffffffffu, excl, o);
+      const int ocn = __shfl_sync(0xffffffffu, cn, o);
+      const int oca = __shfl_sync(0xffffffffu, ca, o);
+      const int osa = __shfl_sync(0xffffffffu, sa, o);
+      int u = -1;
+      const bool ce = off < ocn;
+      if (item < total) u = ce ? __ldg(&g.ce_col[oca + off]) : __ldg(&g.se_col[osa + off - ocn]);
+      const bool kept = u >= 0 && __ldg(&w.hround[u]) == -1;
+      if (__any_sync(0xffffffffu, kept && u < seed)) return -2;
+      int lu = -1;
+      if (kept)
+        for (int j = 0; j < n; ++j)
+          if (s.verts[j] == u) {
+            lu = j;
+            break;
+          }
+      const bool fresh = kept && lu < 0;
+      const unsigned grp = __match_any_sync(0xffffffffu, fresh ? u : -2 - lane);
+      const int leader = __ffs(grp) - 1;
+      const unsigned lead = __ballot_sync(0xffffffffu, fresh && leader == lane);
+      if (n + __popc(lead) > kMaxComp) return -1;
+      if (fresh && leader == lane) {
+        lu = n + __popc(lead & lanemask_lt());
+        s.verts[lu] = u;
+      }
+      const int lu_leader = __shfl_sync(0xffffffffu, lu, leader);
+      if (fresh) lu = lu_leader;
+      n += __popc(lead);
+      if (kept) atomicOr(ce ? &s.dadj[head + o] : &s.dsadj[head + o], 1ull << lu);
+      __syncwarp();
+    }
+    head += gsz;
+  }
+  return n;
+}
+
+// Relabels the discovered component to the column order of R5 (BFS from the
+// minimum vertex, neighbours over CE ∪ SE in ascending id): ranks of the ids,
+// the BFS on rank-labelled masks (lane 0), then the final masks and order.
+__device__ void warp_relabel(WarpComp& s, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < n; i += 32) {
+    const int vi = s.verts[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) r += s.verts[j] < vi ? 1 : 0;
+    s.rank[i] = r;
+  }
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {
+    unsigned long long m = s.dadj[i] | s.dsadj[i], x = 0ull;
+    while (m) {
+      x |= 1ull << s.rank[__ffsll((long long)m) - 1];
+      m &= m - 1;
+    }
+    s.adj[s.rank[i]] = x;
+  }
+  __syncwarp();
+  if (lane == 0) {  // BFS over ranks; rank 0 is the seed (the minimum)
+    unsigned long long seen = 1ull;
+    int tail = 1;
+    s.order[0] = 0;
+    s.bpos[0] = 0;
+    for (int h = 0; h < tail; ++h) {
+      unsigned long long m = s.adj[s.order[h]] & ~seen;
+      seen |= m;
+      while (m) {
+        const int j = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        s.bpos[j] = tail;
+        s.order[tail++] = j;
+      }
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {
+    unsigned long long a = 0ull, b = 0ull, m = s.dadj[i];
+    while (m) {
+      a |= 1ull << s.bpos[s.rank[__ffsll((long long)m) - 1]];
+      m &= m - 1;
+    }
+    m = s.dsadj[i];
+    while (m) {
+      b |= 1ull << s.bpos[s.rank[__ffsll((long long)m) - 1]];
+      m &= m - 1;
+    }
+    const int p = s.bpos[s.rank[i]];
+    s.adj[p] = a;  // every lane has read the rank-labelled masks before the barrier above
+    s.sadj[p] = b;
+    s.order[p] = s.verts[i];
+  }
+  __syncwarp();
+}
+
+// The sequential DFS of R4-R7 on lane 0 (the oracle's node order and budget).
+// W = 32-bit words read the low halves of the 64-bit masks (stride 2).
+template <int K, typename W>
+__device__ unsigned comp_dfs(WarpComp& s, int n, int w_stitch, unsigned budget, int& best_cost, bool& trunc) {
+  constexpr int as = sizeof(unsigned long long) / sizeof(W);
+  const W* a = (const W*)s.adj;
+  const W* sa = (const W*)s.sadj;
+  W* cl = (W*)s.cl;
   W C[K], B[K], bestC[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) C[c] = B[c] = bestC[c] = 0;
   SeqIncumbent inc;
-  const int ncl = clique_min<K>() ? clique_partition<W>(a, 32, n, cl, 32, clique_min<K>()) : 0;
-  const unsigned steps = dfs<K, W, SeqIncumbent>(a, s, 32, C, B, WordOps<W>::full(n), 0, -1, w_stitch, budget,
-                                                 stack, 32, cl, 32, ncl, inc, bestC, trunc);
-  for (int i = 0; i < n; ++i) cval[i] = colour_of<K, W>(bestC, i);
+  const int ncl = clique_min<K>() ? clique_partition<W>(a, as, n, cl, 1, clique_min<K>()) : 0;
+  const unsigned steps = dfs<K, W, SeqIncumbent>(a, sa, as, C, B, WordOps<W>::full(n), 0, -1, w_stitch, budget,
+                                                 (Frame<W>*)s.dadj, 1, cl, 1, ncl, inc, bestC, trunc);
+#pragma unroll
+  for (int c = 0; c < K; ++c) s.cl[c] = (unsigned long long)bestC[c];
   best_cost = inc.best;
   return steps;
 }
 
-// The component's bit-packed matrix: BFS from the root (column order = BFS
-// order of G, neighbours over CE ∪ SE in ascending id, R5).  Every head's
-// neighbours are handled in batches whose global loads (ids, rounds, local
-// indices) are independent and in flight together, so a head costs a few
-// memory round trips instead of two per neighbour.  ASSIGN: the BFS starts at a
-// seed (a kept vertex without smaller kept neighbour) and discovers the
-// component, looking vertices up in its own order list; it gives up (-2) as
-// soon as it meets a vertex smaller than the seed — that component belongs to
-// the seed that is its minimum.  Otherwise loc[] already holds the BFS
-// positions (rebuild).  Returns n, -1 when the component exceeds kMaxComp, or -2.
-template <bool ASSIGN>
+template <int K>
+__device__ __forceinline__ int colour_of_mask(const unsigned long long* bestC, int i) {
+  int c = 0;
+#pragma unroll
+  for (int cc = 1; cc < K; ++cc)
+    if ((bestC[cc] >> i) & 1ull) c = cc;
+  return c;
+}
+
+// Rebuild of a heavy component's matrix beyond the heavy scratch: loc[]
+// already holds every vertex's BFS position, so one thread reads the rows.
 __device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* order, unsigned long long* adjm,
                          unsigned long long* sadjm) {
   int n = 1;
@@ -337,34 +494,17 @@ __device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* 
   for (int head = 0; head < n; ++head) {
     const int v = order[head];
     unsigned long long adj = 0ull, sadj = 0ull;
-    int a = g.ce_rp[v], b = g.se_rp[v];
-    const int ae = g.ce_rp[v + 1], be = g.se_rp[v + 1];
-    while (a < ae || b < be) {  // merge the two ascending rows
-      int u;
-      bool is_ce;
-      if (b >= be || (a < ae && g.ce_col[a] < g.se_col[b])) { u = g.ce_col[a++]; is_ce = true; }
-      else { u = g.se_col[b++]; is_ce = false; }
-      if (w.hround[u] != -1) continue;
-      int lu;
-      if (ASSIGN) {
-        if (u < root) return -2;  // not the component's minimum
-        lu = -1;
-        for (int j = 0; j < n; ++j)
-          if (order[j] == u) {
-            lu = j;
-            break;
-          }
-        if (lu < 0) {
-          if (n == kMaxComp) return -1;
-          lu = n;
-          order[n++] = u;
-        }
-      } else {
-        lu = w.loc[u];
-        order[lu] = u;  // seen before the BFS head reaches its position
+    for (int pass = 0; pass < 2; ++pass) {
+      const int* rp = pass ? g.se_rp : g.ce_rp;
+      const int* col = pass ? g.se_col : g.ce_col;
+      for (int e = rp[v], e1 = rp[v + 1]; e < e1; ++e) {
+        const int u = col[e];
+        if (w.hround[u] != -1) continue;
+        const int lu = w.loc[u];
+        order[lu] = u;
         n = max(n, lu + 1);
+        (pass ? sadj : adj) |= 1ull << lu;
       }
-      if (is_ce) adj |= 1ull << lu; else sadj |= 1ull << lu;
     }
     adjm[head] = adj;
     sadjm[head] = sadj;
@@ -372,11 +512,17 @@ __device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* 
   return n;
 }
 
+// One warp per component seed: discovery, relabelling, the budgeted
+// sequential search on lane 0, the colours.  Exact mode hands components whose
+// search exceeds the light budget to the warp-parallel kernel below.
 template <int K>
-__global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
-                                                              long long max_steps, int shard_index,
-                                                              int shard_count, int* colors, unsigned light_steps) {
-  extern __shared__ __align__(16) unsigned char lsmem[];
+__global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
+                                                                              long long max_steps, int shard_index,
+                                                                              int shard_count, int* colors,
+                                                                              unsigned light_steps) {
+  __shared__ WarpComp s_comp[kCompWarps];
+  WarpComp& s = s_comp[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
   Control* ctl = w.ctl;
   const int n_seed = __ldcg(&ctl->err) ? 0 : __ldcg(&ctl->n_seed);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -387,74 +533,79 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search(GraphView g, Works
   const bool exact = max_steps <= 0;
   const unsigned budget = exact ? light_steps
                                 : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
-  int order[kMaxComp];
-  unsigned long long adjm[kMaxComp], sadjm[kMaxComp];
-  unsigned long long acc_steps = 0ull;
+  unsigned long long acc_steps = 0ull;  // statistics, accumulated on lane 0
   int acc_maxn = 0, acc_maxsteps = 0;
-  unsigned acc_trunc = 0;
-  unsigned acc_comp = 0;
-  for (int ci = blockIdx.x * blockDim.x + threadIdx.x; ci < n_seed; ci += gridDim.x * blockDim.x) {
+  unsigned acc_trunc = 0, acc_comp = 0;
+  const int nw = gridDim.x * kCompWarps;
+  for (int ci = blockIdx.x * kCompWarps + (threadIdx.x >> 5); ci < n_seed; ci += nw) {
     const long long c0 = clock64();
-    const int root = w.roots[ci];
+    const int root = __ldg(&w.roots[ci]);
     if (shard_count > 1 && (int)(lowbias32((uint32_t)root) % (uint32_t)shard_count) != shard_index) continue;
-    const int n = bfs_build<true>(g, w, root, order, adjm, sadjm);
+    const int n = warp_discover(g, w, root, s);
     if (n == -2) continue;  // the seed is not its component's minimum
     ++acc_comp;
     if (n < 0) {
-      atomicOr(&ctl->err, kErrComponent);
-      atomicMax(&ctl->max_comp, kMaxComp + 1);
+      if (lane == 0) {
+        atomicOr(&ctl->err, kErrComponent);
+        atomicMax(&ctl->max_comp, kMaxComp + 1);
+      }
       continue;
     }
-    unsigned steps;
-    bool trunc;
-    int best_cost;
-    int cval[kMaxComp];
+    warp_relabel(s, n);
     const long long c1 = clock64();
-    if (n <= 32)
-      steps = run_light<K, unsigned>(adjm, sadjm, n, w_stitch, budget, lsmem, cval, best_cost, trunc);
-    else
-      steps = run_light<K, unsigned long long>(adjm, sadjm, n, w_stitch, budget, lsmem, cval, best_cost, trunc);
-    const long long c2 = clock64();
-    if ((unsigned long long)(c2 - c0) > ctl->dbg[0]) {  // diagnostics (racy by design)
-      atomicMax(&ctl->dbg[0], (unsigned long long)(c2 - c0));
-      ctl->dbg[1] = c1 - c0;
-      ctl->dbg[2] = c2 - c1;
-      ctl->dbg[3] = n;
-      ctl->dbg[4] = steps;
+    unsigned steps = 0;
+    bool trunc = false;
+    int best_cost = 0;
+    if (lane == 0) {
+      if (n <= 32)
+        steps = comp_dfs<K, unsigned>(s, n, w_stitch, budget, best_cost, trunc);
+      else
+        steps = comp_dfs<K, unsigned long long>(s, n, w_stitch, budget, best_cost, trunc);
     }
-    for (int i = 0; i < n; ++i) {
-      colors[order[i]] = cval[i];
-      w.loc[order[i]] = i;  // BFS position (rebuild of heavy components beyond the scratch)
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const int v = s.order[i];
+      colors[v] = colour_of_mask<K>(s.cl, i);
+      w.loc[v] = i;  // BFS position (rebuild of heavy components beyond the scratch)
     }
-    acc_steps += steps;
-    acc_maxn = max(acc_maxn, n);
+    trunc = __shfl_sync(0xffffffffu, trunc, 0);
     if (trunc && exact) {  // hand the component to the warp-parallel search
-      const int h = atomicAdd(&ctl->n_heavy, 1);
-      w.q0[h] = root;
-      w.q1[h] = best_cost;
-      if (h < kHeavyScratch) {  // keep the matrix so the warp need not rebuild it
-        for (int i = 0; i < n; ++i) {
-          w.hmask[(size_t)h * 2 * kMaxComp + i] = adjm[i];
-          w.hmask[(size_t)h * 2 * kMaxComp + kMaxComp + i] = sadjm[i];
-          w.horder[(size_t)h * kMaxComp + i] = order[i];
-        }
-        w.hn[h] = n;
+      int h = 0;
+      if (lane == 0) {
+        h = atomicAdd(&ctl->n_heavy, 1);
+        w.q0[h] = root;
+        w.q1[h] = best_cost;
       }
-    } else {
-      acc_maxsteps = max(acc_maxsteps, (int)min(steps, (unsigned)INT_MAX));
-      acc_trunc += trunc ? 1 : 0;
+      h = __shfl_sync(0xffffffffu, h, 0);
+      if (h < kHeavyScratch) {  // keep the matrix so the warp need not rebuild it
+        for (int i = lane; i < n; i += 32) {
+          w.hmask[(size_t)h * 2 * kMaxComp + i] = s.adj[i];
+          w.hmask[(size_t)h * 2 * kMaxComp + kMaxComp + i] = s.sadj[i];
+          w.horder[(size_t)h * kMaxComp + i] = s.order[i];
+        }
+        if (lane == 0) w.hn[h] = n;
+      }
     }
+    if (lane == 0) {
+      acc_steps += steps;
+      acc_maxn = max(acc_maxn, n);
+      if (!(trunc && exact)) {
+        acc_maxsteps = max(acc_maxsteps, (int)min(steps, (unsigned)INT_MAX));
+        acc_trunc += trunc ? 1 : 0;
+      }
+      const long long c2 = clock64();
+      if ((unsigned long long)(c2 - c0) > ctl->dbg[0]) {  // diagnostics (racy by design)
+        atomicMax(&ctl->dbg[0], (unsigned long long)(c2 - c0));
+        ctl->dbg[1] = c1 - c0;
+        ctl->dbg[2] = c2 - c1;
+        ctl->dbg[3] = n;
+        ctl->dbg[4] = steps;
+      }
+    }
+    __syncwarp();
   }
-  // statistics: one atomic per warp (thousands of threads hitting one address
-  // serialise at the L2)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc_steps += __shfl_xor_sync(0xffffffffu, acc_steps, o);
-  acc_maxn = __reduce_max_sync(0xffffffffu, acc_maxn);
-  acc_maxsteps = __reduce_max_sync(0xffffffffu, acc_maxsteps);
-  acc_trunc = __reduce_add_sync(0xffffffffu, acc_trunc);
-  acc_comp = __reduce_add_sync(0xffffffffu, acc_comp);
-  if ((threadIdx.x & 31) == 0 && acc_comp) atomicAdd(&ctl->n_comp, (int)acc_comp);
-  if ((threadIdx.x & 31) == 0 && acc_maxn > 0) {
+  if (lane == 0 && acc_comp) atomicAdd(&ctl->n_comp, (int)acc_comp);
+  if (lane == 0 && acc_maxn > 0) {
     atomicAdd(&ctl->steps, acc_steps);
     atomicMax(&ctl->max_comp, acc_maxn);
     atomicMax(&ctl->max_steps_comp, acc_maxsteps);
@@ -474,17 +625,6 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x)
   return x;
 }
 
-__device__ __forceinline__ int warp_excl_scan(int x, int& total) {
-  const int lane = threadIdx.x & 31;
-  int y = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int z = __shfl_up_sync(0xffffffffu, y, o);
-    if (lane >= o) y += z;
-  }
-  total = __shfl_sync(0xffffffffu, y, 31);
-  return y - x;
-}
 
 // Expand node nd: number of children (0 pruned, 1 for a leaf itself) and, if
 // out != nullptr, write them in DFS (colour) order.
@@ -660,7 +800,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
       }
       if (threadIdx.x == 0) s_n = n;
     } else if (threadIdx.x == 0) {  // rebuild: loc[] already holds every vertex's BFS position
-      s_n = bfs_build<false>(g, w, root, s_order, s_adj64, s_sadj64);
+      s_n = bfs_build(g, w, root, s_order, s_adj64, s_sadj64);
     }
     __syncwarp();
     const int n = s_n;
@@ -679,16 +819,16 @@ cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch,
                           int blocks) {
   switch (k) {
     case 2:
-      mpld_exact_cover_search<2><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
-                                                                colors, light_steps);
+      mpld_exact_cover_search<2><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, shard_index,
+                                                                      shard_count, colors, light_steps);
       break;
     case 3:
-      mpld_exact_cover_search<3><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
-                                                                colors, light_steps);
+      mpld_exact_cover_search<3><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, shard_index,
+                                                                      shard_count, colors, light_steps);
       break;
     case 4:
-      mpld_exact_cover_search<4><<<blocks, 32, kLightSmem, s>>>(g, ws, w_stitch, max_steps, shard_index, shard_count,
-                                                                colors, light_steps);
+      mpld_exact_cover_search<4><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, shard_index,
+                                                                      shard_count, colors, light_steps);
       break;
     default: return cudaErrorInvalidValue;
   }
@@ -720,20 +860,13 @@ cudaError_t configure_search_heavy() {
     e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(mpld_exact_cover_search<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLightSmem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(mpld_exact_cover_search<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLightSmem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(mpld_exact_cover_search<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLightSmem);
   return e;
 }
 
 int resident_blocks_search(int threads, int num_sms) {
   (void)threads;
-  cudaFuncSetAttribute(mpld_exact_cover_search<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLightSmem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4>, 32, kLightSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4>, kCompWarps * 32, 0);
   return per_sm * num_sms;
 }
 

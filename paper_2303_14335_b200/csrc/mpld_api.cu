@@ -530,7 +530,7 @@ int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
   Control c;
   cudaError_t e = cudaMemcpy(&c, ctx->ctl, sizeof(Control), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "debug copy");
-  int64_t v[92];
+  int64_t v[96];
   for (int i = 0; i < 16; ++i) v[i] = (int64_t)c.t[i];
   for (int i = 0; i < 32; ++i) {
     v[20 + i] = (int64_t)c.tr[i];
@@ -541,7 +541,11 @@ int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
   v[18] = c.n_rounds;
   v[19] = c.max_steps_comp;
   for (int i = 0; i < 8; ++i) v[84 + i] = (int64_t)c.dbg[i];
-  for (int i = 0; i < n && i < 92; ++i) out[i] = v[i];
+  v[92] = c.n_seed;
+  v[93] = c.n_heavy;
+  v[94] = c.n_comp;
+  v[95] = c.truncated;
+  for (int i = 0; i < n && i < 96; ++i) out[i] = v[i];
   return MPLD_OK;
 }
 

@@ -219,8 +219,8 @@ class Context:
 
     def debug(self):
         """Diagnostics of the last call (include/mpld.h mpld_context_debug)."""
-        out = np.zeros(92, dtype=np.int64)
-        _check(lib().mpld_context_debug(self._h, out.ctypes.data, 92))
+        out = np.zeros(96, dtype=np.int64)
+        _check(lib().mpld_context_debug(self._h, out.ctypes.data, 96))
         return out
 
     def kernel_times(self):

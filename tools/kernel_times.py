@@ -54,6 +54,7 @@ def run(b, k, alpha, iters=10, flush=None, max_steps=1 << 20):
     print("  slowest light search thread: cycles total/build/search, n, steps:", d[84:89].tolist())
     print("  slowest heavy warp: cycles total/split, subtrees, n:", int(d[89]), int(d[90]), int(d[91]) >> 32,
           int(d[91]) & 0xffffffff)
+    print("  seeds, heavy components, components:", int(d[92]), int(d[93]), int(d[94]))
     st = dict(zip(mp.STAT_NAMES, stats.cpu().tolist()))
     ctx.close()
     return {name: round(1e3 * ms / max(n, 1), 1) for name, (ms, n) in t.items()}, st
