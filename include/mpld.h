@@ -40,7 +40,7 @@
  *                found so far (counted in MPLD_STAT_TRUNCATED); the node order is
  *                the sequential one of R5-R7, so truncated results are still
  *                reproducible.  <= 0: exact mode — no budget; components whose
- *                thread-level search needs more than 96 nodes are finished by a
+ *                sequential search needs more than 48 nodes are finished by a
  *                warp-parallel search that returns the same first optimal leaf
  *                (R7).  A safety cap of 2^22 nodes per lane bounds exact mode;
  *                components hitting it are counted in MPLD_STAT_TRUNCATED.
@@ -88,7 +88,10 @@ enum mpld_status {
 };
 
 /* flags */
-#define MPLD_FLAG_VALIDATE 1u /* check the CSR invariants on the device first (MPLD_ERR_GRAPH) */
+#define MPLD_FLAG_VALIDATE 1u /* check the CSR invariants on the device first (MPLD_ERR_GRAPH): row
+                               * pointers, ascending rows, id range, self loops and CE ∩ SE exactly;
+                               * symmetry by two 64-bit multiset hashes (sum H(v,u) == sum H(u,v);
+                               * an asymmetric graph passes with probability ~2^-64) */
 
 /* stats[] layout */
 enum mpld_stat {

@@ -573,8 +573,8 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
       int h = 0;
       if (lane == 0) {
         h = atomicAdd(&ctl->n_heavy, 1);
-        w.q0[h] = root;
-        w.q1[h] = best_cost;
+        w.hroot[h] = root;
+        w.hcost[h] = best_cost;
       }
       h = __shfl_sync(0xffffffffu, h, 0);
       if (h < kHeavyScratch) {  // keep the matrix so the warp need not rebuild it
@@ -789,8 +789,8 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
   Control* ctl = w.ctl;
   const int n_heavy = __ldcg(&ctl->n_heavy);
   for (int h = blockIdx.x; h < n_heavy; h += gridDim.x) {
-    const int root = __ldcg(&w.q0[h]);
-    const int c1 = __ldcg(&w.q1[h]);
+    const int root = __ldcg(&w.hroot[h]);
+    const int c1 = __ldcg(&w.hcost[h]);
     if (h < kHeavyScratch) {  // the light kernel kept the matrix
       const int n = __ldcg(&w.hn[h]);
       for (int i = threadIdx.x; i < n; i += 32) {

@@ -1,5 +1,6 @@
 // Graph-level kernels of the MPLD hot path (§2.2 / Fig. 2 flow):
-//   mpld_simplify_components simplification (R8) + component seeds (Alg. 1 lines 1-3)
+//   mpld_simplify_components simplification (R8), component seeds (Alg. 1
+//                            lines 1-3), recovery pop keys and its level 0
 //   mpld_recover             recovery of the hidden vertices (R9)
 //   mpld_evaluate            Eq. (1) conflict / stitch counts and cost per layout
 //
@@ -7,36 +8,35 @@
 // CTAs, grid-wide barriers between rounds) so that the whole path is enqueued
 // without a host synchronisation.  Queue appends reserve space with one atomic
 // per CTA (a single hot counter serialises at the L2).
+//
+// Every pass is bound by chains of dependent loads (row pointer -> column ids
+// -> the neighbours' data), not by bandwidth: the neighbours of an item are
+// read in batches of kNb independent loads, items are tiled kP per thread
+// (measured on B200: kP = 1, kNb = 4 and one 1024-thread CTA per SM are the
+// fastest; lockstep tiles of 2-3 items per thread lengthen every level).
 #include "mpld_internal.cuh"
 
 namespace mpld {
 
 namespace {
 
-constexpr int kAppend = 8;   // items one thread may append per call before spilling to direct atomics
-constexpr int kNb = 4;       // neighbours processed per batch of independent memory operations
-constexpr int kTail = 1024;  // frontiers up to one item per thread of a CTA are finished by that CTA alone
-
-__device__ __forceinline__ bool row_contains(const int* __restrict__ col, int a, int b, int x) {
-  // binary search in the strictly ascending row col[a..b)
-  while (a < b) {
-    int m = (a + b) >> 1;
-    int y = col[m];
-    if (y == x) return true;
-    if (y < x) a = m + 1; else b = m;
-  }
-  return false;
-}
-
-__device__ __forceinline__ int layout_index(const GraphView& g, int v) {
-  if (g.n_layouts <= 1) return 0;
-  int lo = 0, hi = g.n_layouts;  // off[lo] <= v < off[lo+1]
-  while (hi - lo > 1) {
-    int m = (lo + hi) >> 1;
-    if (__ldg(&g.layout_off[m]) <= v) lo = m; else hi = m;
-  }
-  return lo;
-}
+#ifndef MPLD_GRAPH_P
+#define MPLD_GRAPH_P 1
+#endif
+#ifndef MPLD_GRAPH_NB
+#define MPLD_GRAPH_NB 4
+#endif
+#ifndef MPLD_EVAL_P
+#define MPLD_EVAL_P 1
+#endif
+#ifndef MPLD_GRAPH_MINB
+#define MPLD_GRAPH_MINB 1
+#endif
+constexpr int kP = MPLD_GRAPH_P;    // items per thread and tile
+constexpr int kNb = MPLD_GRAPH_NB;  // neighbours per item and batch of independent memory operations
+constexpr int kAppend = 8;   // items one thread may append per tile before spilling to direct atomics
+constexpr int kTail = 1024;  // frontiers up to this size are finished by CTA 0 alone
+constexpr int kStitchDeg = 1 << 29;  // live degree of stitch vertices: never reaches k (never hidden, R8)
 
 __device__ __forceinline__ void stamp(Control* ctl, int i) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -61,6 +61,31 @@ __device__ __forceinline__ void dstamp(Control* ctl, int i, int cnt) {
 __device__ __forceinline__ unsigned long long pop_key(int h, uint32_t p) {
   return h < 0 ? ~0ull : (((unsigned long long)(h + 1) << 32) | p);
 }
+
+// Layout of a vertex (binary search in layout_off), cached per thread: the
+// tiles of a thread are consecutive ids, so the search rarely runs.
+struct LayoutCache {
+  int lo = 0, begin = 0, end = -1;  // layout lo covers [begin, end)
+  __device__ __forceinline__ int get(const GraphView& g, int v) {
+    if (g.n_layouts <= 1) return 0;
+    if (v < begin || v >= end) {
+      int a = 0, b = g.n_layouts;  // off[a] <= v < off[a+1]
+      while (b - a > 1) {
+        const int m = (a + b) >> 1;
+        if (__ldg(&g.layout_off[m]) <= v) a = m; else b = m;
+      }
+      lo = a;
+      begin = __ldg(&g.layout_off[a]);
+      end = __ldg(&g.layout_off[a + 1]);
+    }
+    return lo;
+  }
+  __device__ __forceinline__ int local(const GraphView& g, int v) {  // layout-local id (R10)
+    if (g.n_layouts <= 1) return v;
+    get(g, v);
+    return v - begin;
+  }
+};
 
 // Block-wide append: thread i contributes cnt_i items; the CTA reserves its
 // range with one atomicAdd.  Every thread of the CTA must call it (uniform
@@ -101,62 +126,72 @@ __device__ __forceinline__ void list_push(int* items, int& cnt, int v, int* coun
 }
 
 // ---------------------------------------------------------------------------
-// Input invariants of include/mpld.h for vertex v (MPLD_FLAG_VALIDATE): both
-// rows strictly ascending, ids in range, no self loop, symmetric (binary search
-// in the neighbour's row), CE ∩ SE = ∅.
-__device__ bool vertex_invalid(const GraphView& g, int v) {
-  for (int pass = 0; pass < 2; ++pass) {
-    const int* rp = pass ? g.se_rp : g.ce_rp;
-    const int* col = pass ? g.se_col : g.ce_col;
-    const int* orp = pass ? g.ce_rp : g.se_rp;
-    const int* ocol = pass ? g.ce_col : g.se_col;
-    const int a = rp[v], b = rp[v + 1];
-    if (a > b) return true;
-    int prev = -1;
-    for (int e = a; e < b; ++e) {
-      const int u = col[e];
-      if (u < 0 || u >= g.n || u == v || u <= prev) return true;
-      prev = u;
-      if (!row_contains(col, rp[u], rp[u + 1], v)) return true;   // symmetric
-      if (row_contains(ocol, orp[v], orp[v + 1], u)) return true;  // CE ∩ SE = ∅
-    }
-  }
-  return false;
+// Input validation (MPLD_FLAG_VALIDATE, include/mpld.h invariants), fused into
+// the first pass over the CSR: row pointers inside [0, nnz], rows strictly
+// ascending, ids in range, no self loop, CE ∩ SE = ∅ are checked exactly per
+// row.  Symmetry — every entry (v, u) has its transpose (u, v) — is checked as
+// the multiset identity sum H(v, u) == sum H(u, v) over all entries (rows are
+// strictly ascending, so entries are distinct): one 64-bit sum per direction,
+// no lookups; an asymmetric graph passes with probability ~2^-64.
+__device__ __forceinline__ unsigned long long pair_hash(int x, int y) {
+  unsigned long long z = ((unsigned long long)(unsigned)x << 32) | (unsigned)y;  // splitmix64 finaliser
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
 }
 
 // One simplification round r >= 1: push the decrements of the frontier
-// (items [first, cnt) with the given stride; every thread of the CTA calls it).
+// cur[0..cnt), tiles of kP * blockDim items starting at first, step stride.
+// A neighbour enters round r+1 exactly when its live degree crosses k -> k-1
+// (stitch vertices start at kStitchDeg and never do).
 __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r, int cnt, int first, int stride,
                            int* qc) {
   const int* cur = (r & 1) ? w.q1 : w.q0;
   int* nxt = (r & 1) ? w.q0 : w.q1;
   int* ncnt = &qc[(r + 1) % 3];
-  for (int i0 = first; i0 < cnt; i0 += stride) {
-    const int i = i0 + threadIdx.x;
+  for (int t0 = first; t0 < cnt; t0 += stride) {
     int items[kAppend];
     int m = 0;
-    if (i < cnt) {
-      const int v = __ldcg(&cur[i]);
-      const int e1 = g.ce_rp[v + 1];
-      // neighbours in batches of kNb: ids, rounds and decrements of a batch are
-      // independent and in flight together (a few memory round trips per batch
-      // instead of three per neighbour)
-      for (int e0 = g.ce_rp[v]; e0 < e1; e0 += kNb) {
-        int u[kNb], hu[kNb], old[kNb];
+    int e[kP], e1[kP];
 #pragma unroll
-        for (int j = 0; j < kNb; ++j) u[j] = e0 + j < e1 ? g.ce_col[e0 + j] : -1;
+    for (int j = 0; j < kP; ++j) {
+      const int i = t0 + j * blockDim.x + threadIdx.x;
+      const int v = i < cnt ? __ldcg(&cur[i]) : -1;
+      e[j] = v >= 0 ? __ldg(&g.ce_rp[v]) : 0;
+      e1[j] = v >= 0 ? __ldg(&g.ce_rp[v + 1]) : 0;
+    }
+    while (true) {
+      bool open = false;
 #pragma unroll
-        for (int j = 0; j < kNb; ++j) hu[j] = u[j] >= 0 ? __ldcg(&w.hround[u[j]]) : 0;
+      for (int j = 0; j < kP; ++j) open |= e[j] < e1[j];
+      if (!open) break;
+      int u[kP][kNb], hu[kP][kNb], old[kP][kNb];
 #pragma unroll
-        for (int j = 0; j < kNb; ++j)  // already-hidden neighbours' degrees no longer matter
-          old[j] = hu[j] == -1 ? atomicSub(&w.deg[u[j]], 1) : 0;
+      for (int j = 0; j < kP; ++j)
 #pragma unroll
-        for (int j = 0; j < kNb; ++j) {
-          if (old[j] == k && g.se_rp[u[j] + 1] == g.se_rp[u[j]]) {
-            w.hround[u[j]] = r + 1;
-            list_push(items, m, u[j], ncnt, nxt);
+        for (int t = 0; t < kNb; ++t) u[j][t] = e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) hu[j][t] = u[j][t] >= 0 ? __ldcg(&w.hround[u[j][t]]) : 0;
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t)  // already-hidden neighbours' degrees no longer matter
+          old[j][t] = hu[j][t] == -1 ? atomicSub(&w.deg[u[j][t]], 1) : 0;
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) {
+          if (old[j][t] == k) {
+            w.hround[u[j][t]] = r + 1;
+            list_push(items, m, u[j][t], ncnt, nxt);
           }
         }
+        e[j] += kNb;
       }
     }
     cta_append(m, items, ncnt, nxt);
@@ -172,60 +207,165 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 //   * a vertex enters round r+1 (r >= 1) exactly when its live degree crosses
 //     k -> k-1 while round r is pushed, so each round only touches the
 //     neighbours of the previous round (frontier queue).
-// Then the seeds of the component search (see below).
-__global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g, Workspace w, int k,
+// Then one pass over all vertices writes the recovery pop keys, the search
+// seeds and the recovery's predecessor counts and level 0.
+__global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_components(GraphView g, Workspace w, int k,
                                                                     int* colors, long long* counts, int validate) {
   GridBarrier grid(&w.ctl->bar[0]);
   stamp(w.ctl, 12);
   const int n = g.n;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nth = gridDim.x * blockDim.x;
+  const int tile0 = blockIdx.x * blockDim.x * kP, tstride = nth * kP;
   Control* ctl = w.ctl;
-  for (int l = tid; l < 2 * g.n_layouts; l += nth) counts[l] = 0;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < 2 * g.n_layouts; l += nth) counts[l] = 0;
 
-  // rounds 0 and 1, recovery priorities, union-find init (and the optional
+  // rounds 0 and 1, recovery priorities, colours = -1 (and the optional
   // validation of the input, fused into this first pass over the CSR)
+  const int nnz_ce = __ldg(&g.ce_rp[n]), nnz_se = __ldg(&g.se_rp[n]);
   int hidden0 = 0;
   bool bad = false;
-  if (validate && tid == 0) {
-    if (g.layout_off[0] != 0 || g.layout_off[g.n_layouts] != g.n) bad = true;
+  unsigned long long hs[4] = {0ull, 0ull, 0ull, 0ull};  // sum H(v,u), H(u,v) over CE, then over SE
+  if (validate && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (g.layout_off[0] != 0 || g.layout_off[g.n_layouts] != g.n || g.ce_rp[0] != 0 || g.se_rp[0] != 0) bad = true;
     for (int l = 0; l < g.n_layouts; ++l)
       if (g.layout_off[l] > g.layout_off[l + 1]) bad = true;
   }
-  for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += nth) {
-    const int v = v0 + threadIdx.x;
-    int take = 0;
-    if (v < n) {
-      if (validate) bad |= vertex_invalid(g, v);
-      const int a = g.ce_rp[v], b = g.ce_rp[v + 1];
-      const bool st = g.se_rp[v + 1] > g.se_rp[v];
-      const int lo = layout_index(g, v);
-      w.prio[v] = lowbias32((uint32_t)(v - (g.n_layouts > 1 ? __ldg(&g.layout_off[lo]) : 0)));
-      colors[v] = -1;  // every vertex is coloured later by exactly one search shard or the recovery
-      int hr = -1;
-      if (!st && b - a < k) {
-        hr = 0;
-        ++hidden0;
-      } else {
-        int d0 = 0;  // live degree after round 0
-        for (int e = a; e < b; ++e) {
-          const int u = g.ce_col[e];
-          if ((unsigned)u >= (unsigned)n) continue;  // invalid input (flagged when validating)
-          d0 += (g.se_rp[u + 1] > g.se_rp[u] || g.ce_rp[u + 1] - g.ce_rp[u] >= k) ? 1 : 0;
-        }
-        w.deg[v] = d0;
-        if (!st && d0 < k) { hr = 1; take = 1; }
+  LayoutCache lc;
+  for (int t0 = tile0; t0 < n; t0 += tstride) {
+    int v[kP], e[kP], e1[kP], d[kP], hr[kP], prev[kP];
+    bool need[kP], scan[kP];
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      v[j] = t0 + j * blockDim.x + threadIdx.x;
+      int a = 0, b = 0, sa = 0, sb = 0;
+      if (v[j] < n) {
+        a = __ldg(&g.ce_rp[v[j]]);
+        b = __ldg(&g.ce_rp[v[j] + 1]);
+        sa = __ldg(&g.se_rp[v[j]]);
+        sb = __ldg(&g.se_rp[v[j] + 1]);
       }
-      w.hround[v] = hr;
+      if (validate && v[j] < n) {
+        if (a < 0 || a > b || b > nnz_ce) {  // never read outside the column arrays
+          bad = true;
+          b = a = 0;
+        }
+        if (sa < 0 || sa > sb || sb > nnz_se) {
+          bad = true;
+          sb = sa = 0;
+        }
+        // stitch rows (rare): exact per-entry checks, CE ∩ SE by binary search in the CE row
+        for (int x = sa, pu = -1; x < sb; ++x) {
+          const int u = __ldg(&g.se_col[x]);
+          if (u < 0 || u >= n || u == v[j] || u <= pu) bad = true;
+          pu = u;
+          hs[2] += pair_hash(v[j], u);
+          hs[3] += pair_hash(u, v[j]);
+          int lo = a, hi = b;
+          while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            const int y = __ldg(&g.ce_col[m]);
+            if (y == u) bad = true;
+            if (y < u) lo = m + 1; else hi = m;
+          }
+        }
+      }
+      e[j] = a;
+      e1[j] = b;
+      d[j] = 0;
+      hr[j] = -1;
+      prev[j] = -1;
+      need[j] = false;
+      if (v[j] < n) {
+        w.prio[v[j]] = lowbias32((uint32_t)lc.local(g, v[j]));
+        colors[v[j]] = -1;  // every vertex is coloured later by exactly one search shard or the recovery
+        if (sb > sa) {
+          w.deg[v[j]] = kStitchDeg;
+        } else if (b - a < k) {
+          hr[j] = 0;
+          ++hidden0;
+        } else {
+          need[j] = true;
+        }
+      }
+      scan[j] = need[j] || (validate && v[j] < n);
     }
-    int item = v;
-    cta_append(take, &item, &ctl->qcnt[1], w.q1);
+    // the CE rows: live degree after round 0 of the vertices that survive it
+    // (pulled from the neighbours' row pointers), validation of every row
+    while (true) {
+      bool open = false;
+#pragma unroll
+      for (int j = 0; j < kP; ++j) open |= scan[j] && e[j] < e1[j];
+      if (!open) break;
+      int u[kP][kNb], r0[kP][kNb], r1[kP][kNb], s0[kP][kNb], s1[kP][kNb];
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) u[j][t] = scan[j] && e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) {
+          const bool ok = need[j] && (unsigned)u[j][t] < (unsigned)n;  // invalid ids are flagged by the validation
+          r0[j][t] = ok ? __ldg(&g.ce_rp[u[j][t]]) : 0;
+          r1[j][t] = ok ? __ldg(&g.ce_rp[u[j][t] + 1]) : 0;
+          s0[j][t] = ok ? __ldg(&g.se_rp[u[j][t]]) : 0;
+          s1[j][t] = ok ? __ldg(&g.se_rp[u[j][t] + 1]) : 0;
+        }
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) {
+          if (e[j] + t >= e1[j]) continue;
+          if (need[j]) d[j] += (s1[j][t] > s0[j][t] || r1[j][t] - r0[j][t] >= k) ? 1 : 0;
+          if (validate) {
+            if (u[j][t] < 0 || u[j][t] >= n || u[j][t] == v[j] || u[j][t] <= prev[j]) bad = true;
+            prev[j] = u[j][t];
+            hs[0] += pair_hash(v[j], u[j][t]);
+            hs[1] += pair_hash(u[j][t], v[j]);
+          }
+        }
+        e[j] += kNb;
+      }
+    }
+    int items[kP];
+    int m = 0;
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      if (need[j]) {
+        w.deg[v[j]] = d[j];
+        if (d[j] < k) {
+          hr[j] = 1;
+          items[m++] = v[j];
+        }
+      }
+      if (v[j] < n) w.hround[v[j]] = hr[j];
+    }
+    cta_append(m, items, &ctl->qcnt[1], w.q1);
   }
   hidden0 = __reduce_add_sync(0xffffffffu, hidden0);
   if ((threadIdx.x & 31) == 0 && hidden0) atomicAdd(&ctl->n_hidden, hidden0);
   if (bad) atomicOr(&ctl->err, kErrGraph);
+  if (validate) {  // CTA sums of the symmetry hashes, one atomic per CTA and direction
+    __shared__ unsigned long long s_h[32][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) hs[q] += __shfl_xor_sync(0xffffffffu, hs[q], o);
+      if ((threadIdx.x & 31) == 0) s_h[threadIdx.x >> 5][q] = hs[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      unsigned long long x = 0ull;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) x += s_h[i][threadIdx.x];
+      atomicAdd(&ctl->vh[threadIdx.x], x);
+    }
+  }
   grid.sync();
   stamp(w.ctl, 0);
+  if (validate && (__ldcg(&ctl->vh[0]) != __ldcg(&ctl->vh[1]) || __ldcg(&ctl->vh[2]) != __ldcg(&ctl->vh[3]))) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctl->err, kErrGraph);  // not symmetric
+    return;  // every CTA sees the same sums
+  }
   if (__ldcg(&ctl->err)) return;  // invalid input: every later kernel exits too
 
   // rounds r >= 1: push the frontier's decrements
@@ -247,7 +387,7 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
             ctl->n_hidden += c;
           }
           dstamp(ctl, rr, c);
-          peel_round(g, w, k, rr, c, 0, blockDim.x, ctl->tcnt);
+          peel_round(g, w, k, rr, c, 0, blockDim.x * kP, ctl->tcnt);
           ++rr;
           __syncthreads();
           c = __ldcg(&ctl->tcnt[rr % 3]);
@@ -258,51 +398,96 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
       r = __ldcg(&ctl->n_rounds);
       break;
     }
-    if (tid == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctl->qcnt[(r + 2) % 3] = 0;
       ctl->n_hidden += cnt;
     }
     dstamp(ctl, r, cnt);
-    peel_round(g, w, k, r, cnt, blockIdx.x * blockDim.x, nth, ctl->qcnt);
+    peel_round(g, w, k, r, cnt, tile0, tstride, ctl->qcnt);
     ++r;
     grid.sync();
     stamp(w.ctl, 2);
   }
-  if (tid == 0) ctl->n_rounds = __ldcg(&ctl->n_hidden) ? r : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_rounds = __ldcg(&ctl->n_hidden) ? r : 0;
   stamp(w.ctl, 1);
 
-  // Pop keys, and the component search seeds: a kept vertex with no kept
-  // neighbour (CE ∪ SE) of smaller id.  Every component has at least one seed
-  // (its minimum); the search kernel's BFS from a seed keeps the component only
-  // if the seed is the component's minimum, so no union-find and no further
-  // grid barrier are needed here.
-  for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += nth) {
-    const int v = v0 + threadIdx.x;
-    int seed = 0;
-    if (v < n) {
-      const int hv = __ldcg(&w.hround[v]);
-      w.key[v] = pop_key(hv, w.prio[v]);
-      if (hv == -1) {
-        seed = 1;
+  // Final pass (rounds are final now):
+  //  * pop keys (R9);
+  //  * component-search seeds: a kept vertex with no kept neighbour (CE ∪ SE)
+  //    of smaller id.  Every component has at least one seed (its minimum);
+  //    the search kernel keeps a seed only if it is its component's minimum,
+  //    so no union-find and no further grid barrier are needed here;
+  //  * recovery: hidden predecessors of every hidden vertex (conflict
+  //    neighbours popped before it) and level 0 = the vertices without one.
+  for (int t0 = tile0; t0 < n; t0 += tstride) {
+    int v[kP], e[kP], e1[kP], cnt[kP];
+    unsigned long long kv[kP];
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      v[j] = t0 + j * blockDim.x + threadIdx.x;
+      const int hv = v[j] < n ? __ldcg(&w.hround[v[j]]) : -1;
+      kv[j] = v[j] < n ? pop_key(hv, __ldcg(&w.prio[v[j]])) : ~0ull;
+      e[j] = kv[j] != ~0ull ? __ldg(&g.ce_rp[v[j]]) : 0;
+      e1[j] = kv[j] != ~0ull ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
+      cnt[j] = 0;
+      if (v[j] < n) w.key[v[j]] = kv[j];
+    }
+    while (true) {
+      bool open = false;
+#pragma unroll
+      for (int j = 0; j < kP; ++j) open |= e[j] < e1[j];
+      if (!open) break;
+      int u[kP][kNb], hu[kP][kNb];
+      unsigned pu[kP][kNb];
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) u[j][t] = e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) {
+          hu[j][t] = u[j][t] >= 0 ? __ldcg(&w.hround[u[j][t]]) : -1;
+          pu[j][t] = u[j][t] >= 0 ? __ldcg(&w.prio[u[j][t]]) : 0u;
+        }
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+#pragma unroll
+        for (int t = 0; t < kNb; ++t)
+          cnt[j] += (hu[j][t] >= 0 && pop_key(hu[j][t], pu[j][t]) > kv[j]) ? 1 : 0;
+        e[j] += kNb;
+      }
+    }
+    int ready[kP], seeds[kP];
+    int mr = 0, ms = 0;
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      if (v[j] >= n) continue;
+      if (kv[j] != ~0ull) {
+        w.deg[v[j]] = cnt[j];
+        if (cnt[j] == 0) ready[mr++] = v[j];
+      } else {
+        bool seed = true;
         for (int pass = 0; pass < 2 && seed; ++pass) {
           const int* rp = pass ? g.se_rp : g.ce_rp;
           const int* col = pass ? g.se_col : g.ce_col;
-          const int e0 = rp[v];
           // rows are ascending: only the first neighbours can be smaller than v
-          for (int e = e0, e1 = rp[v + 1]; e < e1; ++e) {
-            const int u = col[e];
-            if (u > v) break;
+          for (int x = rp[v[j]], x1 = rp[v[j] + 1]; x < x1; ++x) {
+            const int u = col[x];
+            if (u > v[j]) break;
             if (__ldcg(&w.hround[u]) == -1) {
-              seed = 0;
+              seed = false;
               break;
             }
           }
         }
+        if (seed) seeds[ms++] = v[j];
       }
     }
-    int item = v;
-    cta_append(seed, &item, &ctl->n_seed, w.roots);
+    cta_append(ms, seeds, &ctl->n_seed, w.roots);
+    cta_append(mr, ready, &ctl->rq[0], w.q0);
   }
+  stamp(w.ctl, 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -314,94 +499,90 @@ __global__ void __launch_bounds__(1024, 2) mpld_simplify_components(GraphView g,
 // Only the relative order of conflict-adjacent hidden vertices matters, so the
 // LIFO order is realised level-synchronously over the DAG "u before v" (u, v
 // adjacent, u popped first): level 0 = hidden vertices without a hidden
-// predecessor; a vertex joins the next level when its last predecessor is
-// coloured.  Every level is coloured in parallel, one grid barrier per level
-// (DAG depth ~ 10-20 on layout graphs); the result equals the sequential pop.
-// One recovery level: colour the ready vertices cur[first..cnt) (stride),
-// queue the successors whose last predecessor this was.
+// predecessor (listed by the simplification kernel); a vertex joins the next
+// level when its last predecessor is coloured.  Every level is coloured in
+// parallel, one grid barrier per level (DAG depth ~ 10-20 on layout graphs);
+// the result equals the sequential pop.
+// One recovery level: colour the ready vertices cur[0..cnt) (tiles as in
+// peel_round), queue the successors whose last predecessor this was.
 __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int* colors, int L, int cnt, int first,
                               int stride, int* qc) {
   const int* cur = (L & 1) ? w.q1 : w.q0;
   int* nxt = (L & 1) ? w.q0 : w.q1;
   int* ncnt = &qc[(L + 1) % 3];
-  for (int i0 = first; i0 < cnt; i0 += stride) {
-    const int i = i0 + threadIdx.x;
+  for (int t0 = first; t0 < cnt; t0 += stride) {
     int items[kAppend];
     int m = 0;
-    if (i < cnt) {
-      const int v = __ldcg(&cur[i]);
-      const unsigned long long kv = w.key[v];
-      unsigned used = 0;
-      const int e1 = g.ce_rp[v + 1];
-      for (int e0 = g.ce_rp[v]; e0 < e1; e0 += kNb) {  // batches with independent loads / atomics
-        int u[kNb], x[kNb];
-        bool before[kNb];
+    int v[kP], e[kP], e1[kP];
+    unsigned long long kv[kP];
+    unsigned used[kP];
 #pragma unroll
-        for (int j = 0; j < kNb; ++j) u[j] = e0 + j < e1 ? g.ce_col[e0 + j] : -1;
+    for (int j = 0; j < kP; ++j) {
+      const int i = t0 + j * blockDim.x + threadIdx.x;
+      v[j] = i < cnt ? __ldcg(&cur[i]) : -1;
+      kv[j] = v[j] >= 0 ? __ldcg(&w.key[v[j]]) : 0ull;
+      e[j] = v[j] >= 0 ? __ldg(&g.ce_rp[v[j]]) : 0;
+      e1[j] = v[j] >= 0 ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
+      used[j] = 0u;
+    }
+    while (true) {
+      bool open = false;
 #pragma unroll
-        for (int j = 0; j < kNb; ++j) before[j] = u[j] >= 0 && w.key[u[j]] > kv;  // popped before v (or kept)
+      for (int j = 0; j < kP; ++j) open |= e[j] < e1[j];
+      if (!open) break;
+      int u[kP][kNb], x[kP][kNb];
+      bool before[kP][kNb];
 #pragma unroll
-        for (int j = 0; j < kNb; ++j)
-          x[j] = u[j] < 0 ? -1 : (before[j] ? __ldcg(&colors[u[j]]) : atomicSub(&w.deg[u[j]], 1));
+      for (int j = 0; j < kP; ++j)
 #pragma unroll
-        for (int j = 0; j < kNb; ++j) {
-          if (u[j] < 0) continue;
-          if (before[j]) {
-            if (x[j] >= 0) used |= 1u << x[j];
-          } else if (x[j] == 1) {  // v was u's last predecessor
-            list_push(items, m, u[j], ncnt, nxt);
+        for (int t = 0; t < kNb; ++t) u[j][t] = e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t)  // popped before v (or kept)
+          before[j][t] = u[j][t] >= 0 && __ldcg(&w.key[u[j][t]]) > kv[j];
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t)
+          x[j][t] = u[j][t] < 0 ? -1 : (before[j][t] ? __ldcg(&colors[u[j][t]]) : atomicSub(&w.deg[u[j][t]], 1));
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) {
+          if (u[j][t] < 0) continue;
+          if (before[j][t]) {
+            if (x[j][t] >= 0) used[j] |= 1u << x[j][t];
+          } else if (x[j][t] == 1) {  // v was u's last predecessor
+            list_push(items, m, u[j][t], ncnt, nxt);
           }
         }
+        e[j] += kNb;
       }
-      const int c = __ffs(~used) - 1;
-      colors[v] = c < k ? c : 0;  // c < k by the simplification invariant
+    }
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      if (v[j] < 0) continue;
+      const int c = __ffs(~used[j]) - 1;
+      colors[v[j]] = c < k ? c : 0;  // c < k by the simplification invariant
     }
     cta_append(m, items, ncnt, nxt);
   }
 }
 
-__global__ void __launch_bounds__(1024, 2) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
+__global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
   GridBarrier grid(&w.ctl->bar[1]);
   stamp(w.ctl, 13);
   if (__ldcg(&w.ctl->err)) return;
   const int nth = gridDim.x * blockDim.x;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Control* ctl = w.ctl;
-  // level 0 and predecessor counts
-  for (int v0 = blockIdx.x * blockDim.x; v0 < g.n; v0 += nth) {
-    const int v = v0 + threadIdx.x;
-    int ready = 0;
-    if (v < g.n) {
-      const unsigned long long kv = w.key[v];
-      if (kv != ~0ull) {
-        int cnt = 0;
-        const int e1 = g.ce_rp[v + 1];
-        for (int e0 = g.ce_rp[v]; e0 < e1; e0 += kNb) {
-          int u[kNb];
-#pragma unroll
-          for (int j = 0; j < kNb; ++j) u[j] = e0 + j < e1 ? g.ce_col[e0 + j] : -1;
-#pragma unroll
-          for (int j = 0; j < kNb; ++j) {
-            if (u[j] < 0) continue;
-            const unsigned long long ku = w.key[u[j]];
-            cnt += (ku > kv && ku != ~0ull) ? 1 : 0;
-          }
-        }
-        w.deg[v] = cnt;
-        ready = cnt == 0;
-      }
-    }
-    int item = v;
-    cta_append(ready, &item, &ctl->rq[0], w.q0);
-  }
-  grid.sync();
-  stamp(w.ctl, 8);
+  const int tile0 = blockIdx.x * blockDim.x * kP, tstride = nth * kP;
   int L = 0;
   while (true) {
     const int cnt = __ldcg(&ctl->rq[L % 3]);
     dstamp(ctl, 16 + L, cnt);
     if (cnt == 0) {
-      if (tid == 0) ctl->n_levels = L;
+      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_levels = L;
       break;
     }
     if (cnt <= kTail) {  // small level: CTA 0 finishes the remaining levels with block barriers
@@ -409,7 +590,7 @@ __global__ void __launch_bounds__(1024, 2) mpld_recover(GraphView g, Workspace w
         int LL = L, c = cnt;
         while (c > 0) {
           if (threadIdx.x == 0) ctl->trq[(LL + 2) % 3] = 0;  // own counters, as in the simplification tail
-          recover_level(g, w, k, colors, LL, c, 0, blockDim.x, ctl->trq);
+          recover_level(g, w, k, colors, LL, c, 0, blockDim.x * kP, ctl->trq);
           ++LL;
           __syncthreads();
           c = __ldcg(&ctl->trq[LL % 3]);
@@ -418,8 +599,8 @@ __global__ void __launch_bounds__(1024, 2) mpld_recover(GraphView g, Workspace w
       }
       break;  // no grid barrier needed: the kernel ends here
     }
-    if (tid == 0) ctl->rq[(L + 2) % 3] = 0;
-    recover_level(g, w, k, colors, L, cnt, blockIdx.x * blockDim.x, nth, ctl->rq);
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->rq[(L + 2) % 3] = 0;
+    recover_level(g, w, k, colors, L, cnt, tile0, tstride, ctl->rq);
     ++L;
     grid.sync();
     stamp(w.ctl, 9);
@@ -431,29 +612,52 @@ __global__ void __launch_bounds__(1024, 2) mpld_recover(GraphView g, Workspace w
 __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, const int* colors, double alpha,
                                                      long long* counts, double* cost, long long* stats,
                                                      int launches) {
+  constexpr int P = MPLD_EVAL_P;
   const int nth = gridDim.x * blockDim.x;
   stamp(w.ctl, 15);
   const int vend = __ldcg(&w.ctl->err) ? 0 : g.n;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < vend; v += nth) {
-    const int cv = colors[v];
-    int nc = 0, ns = 0;
-    const int e1 = g.ce_rp[v + 1];
-    for (int e0 = g.ce_rp[v]; e0 < e1; e0 += kNb) {
-      int u[kNb];
+  LayoutCache lc;
+  for (int t0 = blockIdx.x * blockDim.x * P; t0 < vend; t0 += nth * P) {
+    int v[P], e[P], e1[P], cv[P], nc[P], ns[P];
 #pragma unroll
-      for (int j = 0; j < kNb; ++j) u[j] = e0 + j < e1 ? g.ce_col[e0 + j] : -1;
+    for (int j = 0; j < P; ++j) {
+      v[j] = t0 + j * blockDim.x + threadIdx.x;
+      const bool ok = v[j] < vend;
+      e[j] = ok ? __ldg(&g.ce_rp[v[j]]) : 0;
+      e1[j] = ok ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
+      cv[j] = ok ? __ldcg(&colors[v[j]]) : 0;
+      nc[j] = ns[j] = 0;
+    }
+    while (true) {
+      bool open = false;
 #pragma unroll
-      for (int j = 0; j < kNb; ++j)
-        if (u[j] > v && colors[u[j]] == cv) ++nc;
+      for (int j = 0; j < P; ++j) open |= e[j] < e1[j];
+      if (!open) break;
+      int u[P][kNb];
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) u[j][t] = e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+#pragma unroll
+        for (int t = 0; t < kNb; ++t)  // each conflict edge counted once, from its smaller end
+          if (u[j][t] > v[j] && __ldcg(&colors[u[j][t]]) == cv[j]) ++nc[j];
+        e[j] += kNb;
+      }
     }
-    for (int e = g.se_rp[v], e1 = g.se_rp[v + 1]; e < e1; ++e) {
-      const int u = g.se_col[e];
-      if (u > v && colors[u] != cv) ++ns;
-    }
-    if (nc | ns) {
-      const int l = layout_index(g, v);
-      if (nc) atomicAdd((unsigned long long*)&counts[2 * l], (unsigned long long)nc);
-      if (ns) atomicAdd((unsigned long long*)&counts[2 * l + 1], (unsigned long long)ns);
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      if (v[j] >= vend) continue;
+      for (int x = __ldg(&g.se_rp[v[j]]), x1 = __ldg(&g.se_rp[v[j] + 1]); x < x1; ++x) {
+        const int u = __ldg(&g.se_col[x]);
+        if (u > v[j] && __ldcg(&colors[u]) != cv[j]) ++ns[j];
+      }
+      if (nc[j] | ns[j]) {
+        const int l = lc.get(g, v[j]);
+        if (nc[j]) atomicAdd((unsigned long long*)&counts[2 * l], (unsigned long long)nc[j]);
+        if (ns[j]) atomicAdd((unsigned long long*)&counts[2 * l + 1], (unsigned long long)ns[j]);
+      }
     }
   }
   __shared__ int s_last;
@@ -513,6 +717,12 @@ int coop_blocks_simplify(int threads, int num_sms) {
 int coop_blocks_recover(int threads, int num_sms) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_recover, threads, 0);
+  return per_sm * num_sms;
+}
+
+int resident_blocks_evaluate(int num_sms) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_evaluate, 256, 0);
   return per_sm * num_sms;
 }
 

@@ -2,8 +2,10 @@
 // the launch sequence of the hot path.
 //
 // Launch sequence of one call (all on one stream, no host synchronisation):
-//   mpld_simplify_components   cooperative: reset, simplification rounds, union-find
-//   mpld_exact_cover_search<K> persistent: one thread per component, dynamic queue
+//   mpld_simplify_components   cooperative: validation, simplification rounds, seeds,
+//                              recovery pop keys and level 0
+//   mpld_exact_cover_search<K> one warp per component seed
+//   mpld_exact_cover_search_heavy<K> (exact mode) one warp per heavy component
 //   mpld_recover               cooperative: LIFO recovery of hidden vertices
 //   mpld_evaluate              Eq. (1) per layout + stats
 #include <cuda_runtime.h>
@@ -55,6 +57,8 @@ struct mpld_context {
   int* q1 = nullptr;
   int* loc = nullptr;
   int* roots = nullptr;
+  int* hroot = nullptr;
+  int* hcost = nullptr;
   unsigned long long* hmask = nullptr;
   int* horder = nullptr;
   int* hn = nullptr;
@@ -100,7 +104,7 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
   if (n > ctx->cap_n) {
     int64_t cap = std::max<int64_t>(n, ctx->cap_n * 3 / 2);
     cudaError_t e = cudaSuccess;
-    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->loc, &ctx->roots}) {
+    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->loc, &ctx->roots, &ctx->hroot, &ctx->hcost}) {
       e = grow(p, cap);
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
@@ -159,8 +163,8 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 }
 
 Workspace workspace(mpld_context* ctx) {
-  return Workspace{ctx->deg,    ctx->hround, ctx->key,   ctx->prio,   ctx->q0, ctx->q1,
-                   ctx->loc,    ctx->roots,  ctx->hmask, ctx->horder, ctx->hn, ctx->ctl};
+  return Workspace{ctx->deg,   ctx->hround, ctx->key,   ctx->prio,   ctx->q0, ctx->q1,     ctx->loc,
+                   ctx->roots, ctx->hroot,  ctx->hcost, ctx->hmask, ctx->horder, ctx->hn, ctx->ctl};
 }
 
 // phase 1: validate?, simplification, components (colours initialised to -1)
@@ -296,7 +300,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   ctx->blocks_simplify = coop_blocks_simplify(kCoopThreads, ctx->num_sms);
   ctx->blocks_recover = coop_blocks_recover(kCoopThreads, ctx->num_sms);
   ctx->blocks_search = resident_blocks_search(32, ctx->num_sms);
-  ctx->blocks_stream = ctx->num_sms * 8;
+  ctx->blocks_stream = resident_blocks_evaluate(ctx->num_sms);
   if (const char* ls = std::getenv("MPLD_LIGHT_STEPS")) {
     const long v = std::strtol(ls, nullptr, 10);
     if (v >= 1 && v <= (1L << 24)) ctx->light_steps = (unsigned)v;
@@ -327,7 +331,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
 void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->key, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
-                  (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->hmask, (void*)ctx->horder, (void*)ctx->hn, (void*)ctx->ctl, (void*)ctx->h_lo,
+                  (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->hroot, (void*)ctx->hcost, (void*)ctx->hmask, (void*)ctx->horder, (void*)ctx->hn, (void*)ctx->ctl, (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
                   (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})
     if (p) cudaFree(p);

@@ -3,8 +3,8 @@
 // Data layout in HBM:
 //   graph     : caller's CSR arrays (int32), read-only.
 //   per vertex: deg, hround, prio, loc (int32), key (u64) — indexed by vertex id
-//   queues    : q0, q1 (int32 [n]) — simplification frontiers, recovery levels,
-//               heavy-component list (root, light-phase cost) in between
+//   queues    : q0, q1 (int32 [n]) — simplification frontiers, then recovery levels
+//   heavy list: hroot, hcost (int32 [n]) — exact mode's warp-parallel components
 //   per comp. : roots (int32 [n]); heavy scratch: hmask/horder/hn (kHeavyScratch slots)
 //   Control   : one control block (counters, barrier arrivals, error bits,
 //               diagnostics) per context, zeroed at the start of every call.
@@ -42,6 +42,7 @@ struct Control {
   int n_levels;              // recovery levels (DAG depth + 1)
   int n_heavy;               // exact mode: components handed to the warp-parallel search
   unsigned long long steps;  // search nodes entered
+  unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)
   unsigned bar[2];           // grid-barrier arrival counters of the two cooperative kernels
   unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
   unsigned long long tr[32];  // diagnostics: per round / level start time (ns)
@@ -94,6 +95,8 @@ struct Workspace {
   int* q1;
   int* loc;        // local index of a kept vertex inside its component
   int* roots;      // component-search seeds (kept vertices without a smaller kept neighbour)
+  int* hroot;      // heavy components (exact mode): seed ...
+  int* hcost;      // ... and the light phase's best cost
   unsigned long long* hmask;  // heavy components kept by the light search: adj/sadj masks
   int* horder;                // ... their BFS orders
   int* hn;                    // ... their sizes
@@ -131,5 +134,6 @@ cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors,
 int coop_blocks_simplify(int threads, int num_sms);
 int coop_blocks_recover(int threads, int num_sms);
 int resident_blocks_search(int threads, int num_sms);
+int resident_blocks_evaluate(int num_sms);
 
 }  // namespace mpld

@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libmpld.so")
+LIB_PATH = os.environ.get("MPLD_LIB") or os.path.join(HERE, "lib", "libmpld.so")  # MPLD_LIB: tuning builds
 
 MPLD_OK = 0
 MPLD_ERR_ARG, MPLD_ERR_GRAPH, MPLD_ERR_COMPONENT, MPLD_ERR_CUDA, MPLD_ERR_NOMEM = 1, 2, 3, 4, 5

@@ -11,6 +11,7 @@ import pytest
 import oracle
 import synth
 from synth import from_edges
+from synth.graph import DecompGraph
 
 mp = pytest.importorskip("paper_2303_14335_b200")
 torch = pytest.importorskip("torch")
@@ -182,6 +183,58 @@ def test_validation_rejects_bad_graphs():
         mp.decompose_graph(bad, 3, 0.1, flags=mp.MPLD_FLAG_VALIDATE)
     assert ei.value.code == 2
     _assert_same(g, 3, 0.1)  # the context recovers after an error
+
+
+def _raw(n, ce_rows, se_rows, layout_offsets=None):
+    """A DecompGraph from explicit rows (may violate the CSR invariants on purpose)."""
+    def csr(rows):
+        rp = np.zeros(n + 1, dtype=np.int32)
+        rp[1:] = np.cumsum([len(r) for r in rows])
+        col = np.array([u for r in rows for u in r], dtype=np.int32)
+        return rp, col
+    crp, ccol = csr(ce_rows)
+    srp, scol = csr(se_rows)
+    g = DecompGraph(n, crp, ccol, srp, scol)
+    if layout_offsets is not None:
+        g.layout_offsets = np.array(layout_offsets, dtype=np.int32)
+    return g
+
+
+# valid reference: path 0-1-2-3 in CE, stitch 3-4; then one violation per case
+_GOOD_CE = [[1], [0, 2], [1, 3], [2], []]
+_GOOD_SE = [[], [], [], [4], [3]]
+_BAD_GRAPHS = {
+    "asymmetric_ce": ([[1], [0, 2], [1, 3], [], []], _GOOD_SE, None),
+    "asymmetric_se": (_GOOD_CE, [[], [], [], [4], []], None),
+    "unsorted_row": ([[1], [2, 0], [1, 3], [2], []], _GOOD_SE, None),
+    "duplicate_entry": ([[1, 1], [0, 0, 2], [1, 3], [2], []], _GOOD_SE, None),
+    "self_loop": ([[1], [0, 2], [1, 2, 3], [2], []], _GOOD_SE, None),
+    "id_out_of_range": ([[1, 5], [0, 2], [1, 3], [2], []], _GOOD_SE, None),
+    "negative_id": ([[-1, 1], [0, 2], [1, 3], [2], []], _GOOD_SE, None),
+    "ce_and_se_overlap": (_GOOD_CE, [[], [], [3], [2, 4], [3]], None),
+    "layout_offsets_unsorted": (_GOOD_CE, _GOOD_SE, [0, 4, 2, 5]),
+    "layout_offsets_short": (_GOOD_CE, _GOOD_SE, [0, 4]),  # rejected by the host entry point (MPLD_ERR_ARG)
+}
+
+
+def test_validation_accepts_valid_graphs():
+    good = _raw(5, _GOOD_CE, _GOOD_SE)
+    r = mp.decompose_graph(good, 2, 0.1, flags=mp.MPLD_FLAG_VALIDATE)
+    assert r["stats"]["error"] == 0
+    graphs, k, alpha = synth.config_graphs(1)
+    b = synth.concat(graphs)
+    rv = mp.decompose_graph(b, k, alpha, flags=mp.MPLD_FLAG_VALIDATE)
+    rn = mp.decompose_graph(b, k, alpha, flags=0)
+    assert np.array_equal(rv["colors"], rn["colors"]) and np.array_equal(rv["cost"], rn["cost"])
+
+
+@pytest.mark.parametrize("case", sorted(_BAD_GRAPHS))
+def test_validation_rejects_each_invariant(case):
+    ce, se, lo = _BAD_GRAPHS[case]
+    with pytest.raises(mp.MPLDError) as ei:
+        mp.decompose_graph(_raw(5, ce, se, lo), 2, 0.1, flags=mp.MPLD_FLAG_VALIDATE)
+    assert ei.value.code == (1 if case == "layout_offsets_short" else 2), case
+    _assert_same(from_edges(4, [(0, 1), (1, 2)]), 3, 0.1)  # the context recovers
 
 
 def test_batch_equals_individual_calls():

@@ -19,7 +19,7 @@ import paper_2303_14335_b200 as mp  # noqa: E402
 import synth  # noqa: E402
 
 
-def run(b, k, alpha, iters=10, flush=None, max_steps=1 << 20):
+def run(b, k, alpha, iters=10, flush=None, max_steps=1 << 20, flags=1):
     dev = torch.device("cuda:0")
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     args = [T(b.layout_offsets), b.n, T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr), T(b.se_col)]
@@ -30,18 +30,18 @@ def run(b, k, alpha, iters=10, flush=None, max_steps=1 << 20):
     stats = torch.empty(len(mp.STAT_NAMES), dtype=torch.int64, device=dev)
     ctx = mp.Context(0, b.n, L)
     for _ in range(3):
-        ctx.decompose_device(*args, k, alpha, max_steps, colors, counts, cost, stats, flags=1)
+        ctx.decompose_device(*args, k, alpha, max_steps, colors, counts, cost, stats, flags=flags)
     torch.cuda.synchronize()
     ctx.reset_timing()
     ctx.set_timing(True)
     for _ in range(iters):
         if flush is not None:
             flush.zero_()
-        ctx.decompose_device(*args, k, alpha, max_steps, colors, counts, cost, stats, flags=1)
+        ctx.decompose_device(*args, k, alpha, max_steps, colors, counts, cost, stats, flags=flags)
     torch.cuda.synchronize()
     t = ctx.kernel_times()
     ctx.set_timing(False)
-    ctx.decompose_device(*args, k, alpha, max_steps, colors, counts, cost, stats, flags=1)
+    ctx.decompose_device(*args, k, alpha, max_steps, colors, counts, cost, stats, flags=flags)
     torch.cuda.synchronize()
     d = ctx.debug()
     t0 = d[12]
@@ -65,6 +65,8 @@ def main():
     ap.add_argument("--replicas", type=int, nargs="+", default=[1, 4, 16])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--max-steps", type=int, default=0)
+    ap.add_argument("--flags", type=int, default=1, help="1 = validate the CSR (bench default)")
+    ap.add_argument("--single", action="store_true", help="skip the one-layout variant")
     a = ap.parse_args()
     flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda:0")
     for R in a.replicas:
@@ -73,11 +75,13 @@ def main():
             gs, k, alpha = synth.config_graphs(a.config, seed=10 * r)
             graphs += gs
         b = synth.concat(graphs)
-        us, st = run(b, k, alpha, flush=flush, max_steps=a.max_steps)
+        us, st = run(b, k, alpha, flush=flush, max_steps=a.max_steps, flags=a.flags)
         print(json.dumps({"replicas": R, "layouts": b.n_layouts, "n": b.n, "us_per_launch": us, "stats": st}))
+        if a.single:
+            continue
         one = synth.concat(graphs)
         one.layout_offsets = np.array([0, one.n], dtype=np.int32)
-        us, st = run(one, k, alpha, flush=flush, max_steps=a.max_steps)
+        us, st = run(one, k, alpha, flush=flush, max_steps=a.max_steps, flags=a.flags)
         print(json.dumps({"replicas": R, "layouts": 1, "n": one.n, "us_per_launch": us}))
 
 
