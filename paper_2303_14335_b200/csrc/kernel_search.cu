@@ -23,15 +23,16 @@
 //                                     the R5 column order, then the sequential DFS
 //                                     on lane 0 (the oracle's exact node order and
 //                                     budget, R7);
-//   mpld_exact_cover_search_heavy<K>  exact mode (max_steps <= 0) only: one warp
-//                                     per component whose thread-level search
-//                                     needed more than kLightSteps nodes.  The
-//                                     canonical tree is split level-synchronously
-//                                     into >= kTarget subtrees (DFS order kept),
+//   mpld_exact_cover_search_heavy<K>  exact mode (max_steps <= 0) only: one
+//                                     128-thread CTA per component whose
+//                                     sequential search needed more than the
+//                                     light budget.  The canonical tree is split
+//                                     level-synchronously into >= 384 subtrees
+//                                     (DFS order kept, nodes stored as paths),
 //                                     lanes search subtrees with a shared
 //                                     incumbent keyed (cost, subtree index); the
 //                                     first optimal leaf of R7 is recovered
-//                                     exactly (DESIGN.md §5).
+//                                     exactly (DESIGN.md §1).
 #include <climits>
 
 #include "mpld_internal.cuh"
@@ -40,11 +41,6 @@ namespace mpld {
 
 namespace {
 
-#ifndef MPLD_HEAVY_TARGET
-#define MPLD_HEAVY_TARGET 96
-#endif
-constexpr int kTarget = MPLD_HEAVY_TARGET;  // heavy: frontier size that stops the level-synchronous split
-constexpr int kCap = 2 * kTarget;           // heavy: frontier capacity per level buffer
 constexpr unsigned kHeavyLaneCap = 1u << 22;  // exact mode safety cap: search nodes per lane per component
 
 template <typename W>
@@ -68,16 +64,6 @@ struct __align__(16) Frame {
   W saved;     // B[c] before r(v,c) was selected
   int cost;    // cost when the node was entered
   int packed;  // v | (c+1) << 8 | (maxused+1) << 16
-};
-
-// A search-tree node (heavy split).
-template <int K, typename W>
-struct __align__(16) Node {
-  W C[K];
-  W B[K];
-  W U;
-  int cost;
-  int mu;
 };
 
 template <int K, typename W>
@@ -614,174 +600,246 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
 }
 
 // ----------------------------------------------------------------------------
-// warp-parallel exact search of one heavy component (block = one warp)
+// Exact mode: CTA-parallel search of one heavy component (kHeavyThreads lanes,
+// one warp per SM sub-partition, one shared incumbent).
+//
+// Split nodes are stored as their path from the root — the colour chosen at
+// each level, 2 bits per level, depth in the top bits of a 64-bit word — and
+// a lane rebuilds a node's state by replaying the path with the column rule
+// of R5 (a few mask operations per level), so the level buffers cost 8 bytes
+// per node.
 
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
-    x = y < x ? y : x;
-  }
-  return x;
+constexpr int kHeavyThreads = 128;
+constexpr int kHeavyTargetNodes = 3 * kHeavyThreads;  // subtrees wanted
+constexpr int kHeavyCapNodes = 2 * kHeavyTargetNodes;  // level buffer capacity
+constexpr int kHeavyStackBytes = 32 * 1024;            // DFS stacks of the lanes (n frames each)
+constexpr int kPathDepthShift = 58;
+constexpr int kPathMaxDepth = 29;                      // 2 bits per level below the depth field
+
+template <int K, typename W>
+struct State {
+  W C[K], B[K], U;
+  int cost, mu;
+};
+
+template <int K, typename W>
+__device__ __forceinline__ int select_column(const State<K, W>& s) {  // Alg. 1 line 8 (R5)
+  W Z, Ol;
+  live_counts<K, W>(s.B, s.U, Z, Ol);
+  return WordOps<W>::ffs(Z ? Z : (Ol ? Ol : s.U));
 }
 
-
-// Expand node nd: number of children (0 pruned, 1 for a leaf itself) and, if
-// out != nullptr, write them in DFS (colour) order.
+// select row r(v, c): cover column v and the row's secondary columns (Alg. 1
+// lines 9, 14-15), conflict and stitch cost as in dfs()
 template <int K, typename W>
-__device__ int expand(const Node<K, W>& nd, const W* s_adj, const W* s_sadj, const W* cl, int ncl, int w_stitch,
-                      int bound,
-                      Node<K, W>* out) {
+__device__ __forceinline__ void apply_row(State<K, W>& s, int v, int c, const W* adj, const W* sadj, int w_stitch) {
   using O = WordOps<W>;
-  if (nd.U == 0) {
-    if (out) *out = nd;
-    return 1;
-  }
-  W Z, Ol;
-  live_counts<K, W>(nd.B, nd.U, Z, Ol);
-  if (nd.cost + kCostUnits * bound_conflicts<K, W>(nd.B, nd.U, Z, cl, 1, ncl) >= bound)
-    return 0;  // pruned against the light-phase incumbent
-  const W cand = Z ? Z : (Ol ? Ol : nd.U);
-  const int v = O::ffs(cand);
   const W bit = W(1) << v;
-  const int lim = min(K - 1, nd.mu + 1);
-  if (out) {
-    const W a = s_adj[v], s = s_sadj[v];
-    const W U = nd.U & ~bit;
-    for (int c = 0; c <= lim; ++c) {
-      Node<K, W> ch = nd;
-      const W Cc = pick<K, W>(nd.C, c);
-      ch.U = U;
-      ch.cost = nd.cost + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(s & ~U & ~Cc);
-      put<K, W>(ch.C, c, Cc | bit);
-      put<K, W>(ch.B, c, pick<K, W>(nd.B, c) | a);
-      ch.mu = max(nd.mu, c);
-      out[c] = ch;
-    }
+  const W a = adj[v], sa = sadj[v];
+  s.U &= ~bit;
+  const W Cc = pick<K, W>(s.C, c);
+  s.cost += kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~s.U & ~Cc);
+  put<K, W>(s.C, c, Cc | bit);
+  put<K, W>(s.B, c, pick<K, W>(s.B, c) | a);
+  s.mu = max(s.mu, c);
+}
+
+template <int K, typename W>
+__device__ __forceinline__ State<K, W> replay(unsigned long long path, int n, const W* adj, const W* sadj,
+                                              int w_stitch) {
+  State<K, W> s;
+#pragma unroll
+  for (int c = 0; c < K; ++c) s.C[c] = s.B[c] = 0;
+  s.U = WordOps<W>::full(n);
+  s.cost = 0;
+  s.mu = -1;
+  const int depth = (int)(path >> kPathDepthShift);
+  for (int d = 0; d < depth; ++d) apply_row<K, W>(s, select_column<K, W>(s), (int)((path >> (2 * d)) & 3ull), adj, sadj, w_stitch);
+  return s;
+}
+
+// children of a split node: 0 = pruned against the light-phase incumbent c1
+// (its leaf precedes every subtree), 1 for a leaf (carried as itself), else
+// min(K, mu + 2) (R4 with the colour-symmetry limit R6)
+template <int K, typename W>
+__device__ __forceinline__ int split_children(const State<K, W>& s, const W* cl, int ncl, int c1) {
+  if (s.U == 0) return 1;
+  W Z, Ol;
+  live_counts<K, W>(s.B, s.U, Z, Ol);
+  if (s.cost + kCostUnits * bound_conflicts<K, W>(s.B, s.U, Z, cl, 1, ncl) >= c1) return 0;
+  return min(K - 1, s.mu + 1) + 1;
+}
+
+__device__ __forceinline__ int block_excl_scan(int x, int& total, int* s_tmp) {  // s_tmp: 32 ints
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int y = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int z = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) y += z;
   }
-  return lim + 1;
+  if (lane == 31) s_tmp[wid] = y;
+  __syncthreads();
+  int base = 0;
+  total = 0;
+  for (int i = 0; i < nw; ++i) {
+    const int t = s_tmp[i];
+    if (i < wid) base += t;
+    total += t;
+  }
+  __syncthreads();
+  return base + y - x;
 }
 
 template <int K, typename W>
 __device__ void heavy_component(int n, const int* s_order, const unsigned long long* s_adj64,
                                 const unsigned long long* s_sadj64, unsigned char* smem, int w_stitch, int c1,
                                 int* colors, Control* ctl) {
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x;
   W* s_adj = (W*)smem;
   W* s_sadj = s_adj + kMaxComp;
-  Node<K, W>* lvl[2] = {(Node<K, W>*)(smem + 2 * kMaxComp * sizeof(unsigned long long)), nullptr};
-  lvl[1] = lvl[0] + kCap;
+  W* s_cl = s_sadj + kMaxComp;
+  unsigned long long* lvl[2];
+  lvl[0] = (unsigned long long*)(smem + 3 * kMaxComp * sizeof(unsigned long long));
+  lvl[1] = lvl[0] + kHeavyCapNodes;
+  Frame<W>* stack_base = (Frame<W>*)(lvl[1] + kHeavyCapNodes);
   __shared__ unsigned long long s_best;
-  __shared__ int s_next, s_ncl;
-  __shared__ unsigned long long s_cl64[kMaxComp / 2];
-  W* s_cl = (W*)s_cl64;
-  for (int i = lane; i < n; i += 32) {
+  __shared__ unsigned long long s_win;
+  __shared__ int s_next, s_ncl, s_flag, s_tmp[32];
+  __shared__ unsigned long long s_red[32];
+  for (int i = tid; i < n; i += blockDim.x) {
     s_adj[i] = (W)s_adj64[i];
     s_sadj[i] = (W)s_sadj64[i];
   }
-  __syncwarp();
-  if (lane == 0) s_ncl = clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, clique_min<K>()) : 0;
-  __syncwarp();
-  const int ncl = s_ncl;
-  if (lane == 0) {
-    Node<K, W> root;
-#pragma unroll
-    for (int c = 0; c < K; ++c) root.C[c] = root.B[c] = 0;
-    root.U = WordOps<W>::full(n);
-    root.cost = 0;
-    root.mu = -1;
-    lvl[0][0] = root;
+  __syncthreads();
+  if (tid == 0) {
+    s_ncl = clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, clique_min<K>()) : 0;
+    lvl[0][0] = 0ull;  // the root: depth 0
     s_best = (unsigned long long)c1 << 32;  // the light-phase leaf precedes every subtree (key f+1 = 0)
     s_next = 0;
   }
-  __syncwarp();
+  __syncthreads();
+  const int ncl = s_ncl;
   const long long hc0 = clock64();
   // level-synchronous split of the canonical tree, DFS order preserved
   int m = 1, cur = 0;
   unsigned expanded = 0;
-  while (m < kTarget) {
+  while (m < kHeavyTargetNodes) {
     int total = 0;
-    bool inner = false;  // some node still has uncovered columns
-    for (int i0 = 0; i0 < m; i0 += 32) {
-      const int i = i0 + lane;
-      const int cnt = i < m ? expand<K, W>(lvl[cur][i], s_adj, s_sadj, s_cl, ncl, w_stitch, c1, nullptr) : 0;
-      inner |= __any_sync(0xffffffffu, i < m && lvl[cur][i].U != 0 && cnt > 0);
+    if (tid == 0) s_flag = 0;  // bit 0: some node still has uncovered columns; bit 1: depth limit reached
+    __syncthreads();
+    for (int i0 = 0; i0 < m; i0 += blockDim.x) {
+      const int i = i0 + tid;
+      unsigned long long path = 0ull;
+      int cnt = 0, depth = 0;
+      State<K, W> st;
+      if (i < m) {
+        path = lvl[cur][i];
+        depth = (int)(path >> kPathDepthShift);
+        st = replay<K, W>(path, n, s_adj, s_sadj, w_stitch);
+        cnt = split_children<K, W>(st, s_cl, ncl, c1);
+        if (st.U != 0 && cnt > 0) atomicOr(&s_flag, depth + 1 >= kPathMaxDepth ? 3 : 1);
+      }
       int t;
-      warp_excl_scan(cnt, t);
+      const int off = block_excl_scan(cnt, t, s_tmp);
+      if (total + t <= kHeavyCapNodes && cnt > 0) {
+        unsigned long long* out = &lvl[cur ^ 1][total + off];
+        if (st.U == 0) {
+          out[0] = path;
+        } else {
+          const unsigned long long base = (path & ((1ull << kPathDepthShift) - 1)) |
+                                          ((unsigned long long)(depth + 1) << kPathDepthShift);
+          for (int c = 0; c < cnt; ++c) out[c] = base | ((unsigned long long)c << (2 * depth));
+        }
+      }
       total += t;
     }
+    __syncthreads();
+    const int flag = s_flag;
     if (total == 0) {
       m = 0;
       break;
     }
-    if (total > kCap || !inner) break;
-    int base = 0;
-    for (int i0 = 0; i0 < m; i0 += 32) {
-      const int i = i0 + lane;
-      const int cnt = i < m ? expand<K, W>(lvl[cur][i], s_adj, s_sadj, s_cl, ncl, w_stitch, c1, nullptr) : 0;
-      int t;
-      const int off = warp_excl_scan(cnt, t);
-      if (cnt) expand<K, W>(lvl[cur][i], s_adj, s_sadj, s_cl, ncl, w_stitch, c1, &lvl[cur ^ 1][base + off]);
-      base += t;
-    }
+    if (total > kHeavyCapNodes || !(flag & 1) || (flag & 2)) break;
     expanded += m;
     cur ^= 1;
     m = total;
-    __syncwarp();
   }
   const long long hc1 = clock64();
-  // lanes search the subtrees in DFS order with a shared incumbent
-  Frame<W>* stack = (Frame<W>*)(smem + 2 * kMaxComp * sizeof(unsigned long long) +
-                                2 * kCap * sizeof(Node<MPLD_MAX_K, unsigned long long>)) + lane;
+  // lanes search the subtrees in DFS order with a shared incumbent; the stack
+  // region holds n frames per active lane
+  const int lanes = min((int)blockDim.x, (int)(kHeavyStackBytes / (n * (int)sizeof(Frame<W>))));
   W bestC[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) bestC[c] = 0;
   unsigned long long my_best = ~0ull;
   unsigned steps = 0;
   bool capped = false;
-  while (true) {
-    const int f = atomicAdd(&s_next, 1);
-    if (f >= m) break;
-    if (steps >= kHeavyLaneCap) {  // safety cap of exact mode: skip, flag as truncated
-      capped = true;
-      continue;
+  if (tid < lanes) {
+    while (true) {
+      const int f = atomicAdd(&s_next, 1);
+      if (f >= m) break;
+      if (steps >= kHeavyLaneCap) {  // safety cap of exact mode: skip, flag as truncated
+        capped = true;
+        continue;
+      }
+      State<K, W> st = replay<K, W>(lvl[cur][f], n, s_adj, s_sadj, w_stitch);
+      ParIncumbent inc;
+      inc.shared_best = &s_best;
+      inc.fkey = (unsigned long long)(f + 1);
+      inc.lane_best = my_best;
+      bool trunc;
+      steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, 1, st.C, st.B, st.U, st.cost, st.mu, w_stitch,
+                                       kHeavyLaneCap - steps, stack_base + tid, lanes, s_cl, 1, ncl, inc, bestC,
+                                       trunc);
+      my_best = inc.lane_best;
+      capped |= trunc;
     }
-    Node<K, W> nd = lvl[cur][f];
-    ParIncumbent inc;
-    inc.shared_best = &s_best;
-    inc.fkey = (unsigned long long)(f + 1);
-    inc.lane_best = my_best;
-    bool trunc;
-    steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, 1, nd.C, nd.B, nd.U, nd.cost, nd.mu, w_stitch,
-                                     kHeavyLaneCap - steps, stack, 32, s_cl, 1, ncl, inc, bestC, trunc);
-    my_best = inc.lane_best;
-    capped |= trunc;
   }
-  const bool any_capped = __any_sync(0xffffffffu, capped);
-  const long long hc2 = clock64();
-  if (lane == 0 && (unsigned long long)(hc2 - hc0) > ctl->dbg[5]) {  // diagnostics (racy by design)
-    atomicMax(&ctl->dbg[5], (unsigned long long)(hc2 - hc0));
-    ctl->dbg[6] = hc1 - hc0;
-    ctl->dbg[7] = ((unsigned long long)m << 32) | (unsigned)n;
-  }
-  const unsigned long long win = warp_min_u64(my_best);
-  const unsigned who = __ballot_sync(0xffffffffu, my_best == win && win != ~0ull);
-  if (who && lane == __ffs(who) - 1 && win < ((unsigned long long)c1 << 32)) {
-    for (int i = 0; i < n; ++i) colors[s_order[i]] = colour_of<K, W>(bestC, i);
-  }
+  // the minimum key over lanes is the canonical leaf
+  const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  unsigned long long wmin = my_best;
   unsigned total_steps = steps;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) total_steps += __shfl_xor_sync(0xffffffffu, total_steps, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, wmin, o);
+    wmin = y < wmin ? y : wmin;
+    total_steps += __shfl_xor_sync(0xffffffffu, total_steps, o);
+  }
+  const int any_capped = __syncthreads_or(capped);
   if (lane == 0) {
+    s_red[wid] = wmin;
+    s_tmp[wid] = (int)total_steps;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long w = ~0ull;
+    unsigned ts = 0;
+    for (int i = 0; i < nw; ++i) {
+      w = s_red[i] < w ? s_red[i] : w;
+      ts += (unsigned)s_tmp[i];
+    }
+    s_win = w;
     if (any_capped) atomicAdd(&ctl->truncated, 1);
-    atomicAdd(&ctl->steps, (unsigned long long)(total_steps + expanded));
-    atomicMax(&ctl->max_steps_comp, (int)min(total_steps + expanded, (unsigned)INT_MAX));
+    atomicAdd(&ctl->steps, (unsigned long long)(ts + expanded));
+    atomicMax(&ctl->max_steps_comp, (int)min(ts + expanded, (unsigned)INT_MAX));
+    const long long hc2 = clock64();
+    if ((unsigned long long)(hc2 - hc0) > ctl->dbg[5]) {  // diagnostics (racy by design)
+      atomicMax(&ctl->dbg[5], (unsigned long long)(hc2 - hc0));
+      ctl->dbg[6] = hc1 - hc0;
+      ctl->dbg[7] = ((unsigned long long)m << 32) | (unsigned)n;
+    }
+  }
+  __syncthreads();
+  const unsigned long long win = s_win;
+  if (win != ~0ull && my_best == win && win < ((unsigned long long)c1 << 32)) {  // keys are unique per subtree
+    for (int i = 0; i < n; ++i) colors[s_order[i]] = colour_of<K, W>(bestC, i);
   }
 }
 
 template <int K>
-__global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
-                                                                    int* colors) {
+__global__ void __launch_bounds__(kHeavyThreads) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
+                                                                               int* colors) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_order[kMaxComp];
   __shared__ unsigned long long s_adj64[kMaxComp], s_sadj64[kMaxComp];
@@ -791,9 +849,9 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
   for (int h = blockIdx.x; h < n_heavy; h += gridDim.x) {
     const int root = __ldcg(&w.hroot[h]);
     const int c1 = __ldcg(&w.hcost[h]);
-    if (h < kHeavyScratch) {  // the light kernel kept the matrix
+    if (h < kHeavyScratch) {  // the component kernel kept the matrix
       const int n = __ldcg(&w.hn[h]);
-      for (int i = threadIdx.x; i < n; i += 32) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
         s_order[i] = __ldcg(&w.horder[(size_t)h * kMaxComp + i]);
         s_adj64[i] = __ldcg(&w.hmask[(size_t)h * 2 * kMaxComp + i]);
         s_sadj64[i] = __ldcg(&w.hmask[(size_t)h * 2 * kMaxComp + kMaxComp + i]);
@@ -802,13 +860,13 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
     } else if (threadIdx.x == 0) {  // rebuild: loc[] already holds every vertex's BFS position
       s_n = bfs_build(g, w, root, s_order, s_adj64, s_sadj64);
     }
-    __syncwarp();
+    __syncthreads();
     const int n = s_n;
     if (n <= 32)
       heavy_component<K, unsigned>(n, s_order, s_adj64, s_sadj64, smem, w_stitch, c1, colors, ctl);
     else
       heavy_component<K, unsigned long long>(n, s_order, s_adj64, s_sadj64, smem, w_stitch, c1, colors, ctl);
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -836,20 +894,27 @@ cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch,
 }
 
 size_t heavy_smem_bytes() {
-  return 2 * kMaxComp * sizeof(unsigned long long) + 2 * kCap * sizeof(Node<MPLD_MAX_K, unsigned long long>) +
-         kMaxComp * 32 * sizeof(Frame<unsigned long long>);
+  return 3 * kMaxComp * sizeof(unsigned long long) + 2 * kHeavyCapNodes * sizeof(unsigned long long) +
+         kHeavyStackBytes;
 }
 
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
                                 int blocks) {
   const size_t smem = heavy_smem_bytes();
   switch (k) {
-    case 2: mpld_exact_cover_search_heavy<2><<<blocks, 32, smem, s>>>(g, ws, w_stitch, colors); break;
-    case 3: mpld_exact_cover_search_heavy<3><<<blocks, 32, smem, s>>>(g, ws, w_stitch, colors); break;
-    case 4: mpld_exact_cover_search_heavy<4><<<blocks, 32, smem, s>>>(g, ws, w_stitch, colors); break;
+    case 2: mpld_exact_cover_search_heavy<2><<<blocks, kHeavyThreads, smem, s>>>(g, ws, w_stitch, colors); break;
+    case 3: mpld_exact_cover_search_heavy<3><<<blocks, kHeavyThreads, smem, s>>>(g, ws, w_stitch, colors); break;
+    case 4: mpld_exact_cover_search_heavy<4><<<blocks, kHeavyThreads, smem, s>>>(g, ws, w_stitch, colors); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+int resident_blocks_heavy(int num_sms) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search_heavy<4>, kHeavyThreads,
+                                                heavy_smem_bytes());
+  return per_sm * num_sms;
 }
 
 cudaError_t configure_search_heavy() {

@@ -69,7 +69,7 @@ struct mpld_context {
   bool prepared = false;
   int call_launches = 0;
   unsigned light_steps = kLightStepsDefault;  // MPLD_LIGHT_STEPS overrides (tuning)
-  int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0;
+  int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0, blocks_heavy = 0;
   // host-API staging (device copies of host inputs / outputs)
   int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
   int* h_lo = nullptr;
@@ -205,7 +205,7 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
   }
   if (max_steps <= 0) {  // exact mode: heavy components on the warp-parallel search
     TimedLaunch t(ctx, K_SEARCH_HEAVY, s);
-    cudaError_t e = launch_search_heavy(g, ws, ctx->k, w_stitch, colors, s, ctx->num_sms * 4);
+    cudaError_t e = launch_search_heavy(g, ws, ctx->k, w_stitch, colors, s, ctx->blocks_heavy);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_heavy");
     t.done();
     ++ctx->call_launches;
@@ -310,7 +310,8 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     mpld_context_destroy(ctx);
     return cuda_fail(e, "configure heavy search");
   }
-  if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0) {
+  ctx->blocks_heavy = resident_blocks_heavy(ctx->num_sms);
+  if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0 || ctx->blocks_heavy <= 0) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_CUDA, "occupancy query failed (kernel image missing for this device?)");
   }

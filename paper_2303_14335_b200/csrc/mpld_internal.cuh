@@ -135,5 +135,6 @@ int coop_blocks_simplify(int threads, int num_sms);
 int coop_blocks_recover(int threads, int num_sms);
 int resident_blocks_search(int threads, int num_sms);
 int resident_blocks_evaluate(int num_sms);
+int resident_blocks_heavy(int num_sms);  // after configure_search_heavy()
 
 }  // namespace mpld
