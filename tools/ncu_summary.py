@@ -1,0 +1,59 @@
+"""Summarise an `ncu --set full` report into profiles/<round>_kernels.json (dev tool).
+
+python tools/ncu_summary.py REPORT.ncu-rep OUT.json "source description"
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+
+def main():
+    rep, out, src = sys.argv[1], sys.argv[2], sys.argv[3]
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    col = {h: i for i, h in enumerate(hdr)}
+    def f(d, name):
+        try:
+            return float(d[col[name]].replace(",", ""))
+        except (KeyError, ValueError):
+            return None
+
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def nbytes(d, name):
+        v = f(d, name)
+        return 0.0 if v is None else v * scale.get(units[col[name]], 1.0)
+
+    kernels = {}
+    for d in data:
+        name = d[col["Kernel Name"]].split("(")[0].split("::")[-1].split("<")[0].strip()
+        stalls = {}
+        for h, i in col.items():
+            if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
+                try:
+                    stalls[h[len("smsp__pcsamp_warps_issue_stalled_"):]] = float(d[i])
+                except ValueError:
+                    pass
+        tot = sum(stalls.values()) or 1.0
+        top = sorted(stalls.items(), key=lambda x: -x[1])[:4]
+        kernels[name] = {
+            "duration_us": f(d, "gpu__time_duration.sum"),
+            "dram_bytes": nbytes(d, "dram__bytes_read.sum") + nbytes(d, "dram__bytes_write.sum"),
+            "warps_active_pct": f(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "l2_hit_pct": f(d, "lts__t_sector_hit_rate.pct"),
+            "inst_executed": f(d, "smsp__inst_executed.sum"),
+            "grid": int(f(d, "launch__grid_size") or 0),
+            "block": int(f(d, "launch__block_size") or 0),
+            "regs": int(f(d, "launch__registers_per_thread") or 0),
+            "stall_top_pct": {k: round(100 * v / tot, 1) for k, v in top},
+        }
+    json.dump({"source": src, "kernels": kernels}, open(out, "w"), indent=1)
+    for k, v in kernels.items():
+        print(k, round(v["duration_us"], 1), "us", round(v["dram_bytes"] / 1e6, 2), "MB", v["stall_top_pct"])
+
+
+if __name__ == "__main__":
+    main()
