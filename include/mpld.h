@@ -185,8 +185,9 @@ int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* laun
  * %globaltimer stamps (ns) at phase boundaries, out[16] recovery levels
  * (depth of the pop-order DAG + 1), out[17] hidden vertices, out[18] rounds,
  * out[19] largest per-component step count, out[20..51] per round (0..15) / recovery
- * level (16..31) start stamps, out[52..83] their frontier sizes, out[84..91]
- * slowest search warp (cycles total, build, search; n; steps) and slowest heavy
+ * level (16..31) start stamps, out[52..83] their frontier sizes,
+ * out[84] slowest discovery (cycles << 16 | n), out[86] slowest light search
+ * (cycles << 24 | steps << 8 | n), out[85,87,88] unused, and the slowest heavy
  * warp (cycles total, split; subtrees << 32 | n), out[92] component-search seeds,
  * out[93] heavy components, out[94] components, out[95] truncated searches.
  * Copies min(n, 96). */

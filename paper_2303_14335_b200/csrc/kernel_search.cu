@@ -27,7 +27,7 @@
 //                                     128-thread CTA per component whose
 //                                     sequential search needed more than the
 //                                     light budget.  The canonical tree is split
-//                                     level-synchronously into >= 384 subtrees
+//                                     level-synchronously into >= 128 subtrees
 //                                     (DFS order kept, nodes stored as paths),
 //                                     lanes search subtrees with a shared
 //                                     incumbent keyed (cost, subtree index); the
@@ -279,22 +279,30 @@ __device__ __forceinline__ int colour_of(const W (&bestC)[K], int i) {
   return c;
 }
 
+#ifndef MPLD_LDD
+#define MPLD_LDD __ldg
+#endif
 constexpr int kCompWarps = 4;  // warps per CTA of the component kernel (one component per warp)
 
-// Per-warp shared storage of the component kernel.
-struct __align__(16) WarpComp {
-  unsigned long long dadj[kMaxComp];   // CE masks in discovery labels; then the DFS stack (with dsadj)
+// Per-warp shared storage of the discovery kernel.
+struct __align__(16) WarpDisc {
+  unsigned long long dadj[kMaxComp];   // CE masks in discovery labels
   unsigned long long dsadj[kMaxComp];  // SE masks in discovery labels
   unsigned long long adj[kMaxComp];    // CE masks in BFS labels (R5); CE ∪ SE in rank labels while relabelling
   unsigned long long sadj[kMaxComp];   // SE masks in BFS labels
-  unsigned long long cl[kMaxComp / 2];  // clique masks (R7); then the best leaf's C[c]
   int verts[kMaxComp];                 // discovery index -> vertex id
   int order[kMaxComp];                 // BFS position -> vertex id (the rank queue while relabelling)
   int rank[kMaxComp];                  // discovery index -> rank of its id inside the component
   int bpos[kMaxComp];                  // rank -> BFS position
 };
-static_assert(sizeof(Frame<unsigned long long>) * kMaxComp <= 2 * kMaxComp * sizeof(unsigned long long),
-              "the DFS stack lives in dadj/dsadj");
+
+// Per-warp shared storage of the search kernel.
+struct __align__(16) WarpSearch {
+  unsigned long long adj[kMaxComp];   // CE masks (BFS labels)
+  unsigned long long sadj[kMaxComp];  // SE masks
+  Frame<unsigned long long> stack[kMaxComp];
+  unsigned long long cl[kMaxComp / 2];  // clique masks (R7); then the best leaf's C[c]
+};
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -322,8 +330,9 @@ __device__ __forceinline__ int warp_excl_scan(int x, int& total) {
 // verts).  Returns n, -1 when the component exceeds kMaxComp, or -2 as soon
 // as it meets a kept vertex smaller than the seed: that component belongs to
 // the seed that is its minimum.
-__device__ int warp_discover(const GraphView& g, const Workspace& w, int seed, WarpComp& s) {
+__device__ int warp_discover(const GraphView& g, const Workspace& w, int seed, WarpDisc& s, int* diag = nullptr) {
   const int lane = threadIdx.x & 31;
+  int n_groups = 0, n_chunks = 0;
   for (int i = lane; i < kMaxComp; i += 32) s.dadj[i] = s.dsadj[i] = 0ull;
   if (lane == 0) s.verts[0] = seed;
   __syncwarp();
@@ -333,14 +342,16 @@ __device__ int warp_discover(const GraphView& g, const Workspace& w, int seed, W
     int ca = 0, cn = 0, sa = 0, sn = 0;
     if (lane < gsz) {
       const int v = s.verts[head + lane];
-      ca = __ldg(&g.ce_rp[v]);
-      cn = __ldg(&g.ce_rp[v + 1]) - ca;
-      sa = __ldg(&g.se_rp[v]);
-      sn = __ldg(&g.se_rp[v + 1]) - sa;
+      ca = MPLD_LDD(&g.ce_rp[v]);
+      cn = MPLD_LDD(&g.ce_rp[v + 1]) - ca;
+      sa = MPLD_LDD(&g.se_rp[v]);
+      sn = MPLD_LDD(&g.se_rp[v + 1]) - sa;
     }
     int total;
     const int excl = warp_excl_scan(cn + sn, total);
+    ++n_groups;
     for (int b = 0; b < total; b += 32) {
+      ++n_chunks;
       const int item = b + lane;
       int o = 0;  // owner: the last group lane whose row range starts at or before item
 #pragma unroll
@@ -354,8 +365,8 @@ __device__ int warp_discover(const GraphView& g, const Workspace& w, int seed, W
       const int osa = __shfl_sync(0xffffffffu, sa, o);
       int u = -1;
       const bool ce = off < ocn;
-      if (item < total) u = ce ? __ldg(&g.ce_col[oca + off]) : __ldg(&g.se_col[osa + off - ocn]);
-      const bool kept = u >= 0 && __ldg(&w.hround[u]) == -1;
+      if (item < total) u = ce ? MPLD_LDD(&g.ce_col[oca + off]) : MPLD_LDD(&g.se_col[osa + off - ocn]);
+      const bool kept = u >= 0 && MPLD_LDD(&w.hround[u]) == -1;
       if (__any_sync(0xffffffffu, kept && u < seed)) return -2;
       int lu = -1;
       if (kept)
@@ -376,18 +387,22 @@ __device__ int warp_discover(const GraphView& g, const Workspace& w, int seed, W
       const int lu_leader = __shfl_sync(0xffffffffu, lu, leader);
       if (fresh) lu = lu_leader;
       n += __popc(lead);
-      if (kept) atomicOr(ce ? &s.dadj[head + o] : &s.dsadj[head + o], 1ull << lu);
+      if (kept) {  // one bit: a native 32-bit shared atomic on its half (the 64-bit one is a CAS loop)
+        unsigned* word = (unsigned*)(ce ? &s.dadj[head + o] : &s.dsadj[head + o]) + (lu >> 5);
+        atomicOr(word, 1u << (lu & 31));
+      }
       __syncwarp();
     }
     head += gsz;
   }
+  if (diag) *diag = n_groups | (n_chunks << 8);
   return n;
 }
 
 // Relabels the discovered component to the column order of R5 (BFS from the
 // minimum vertex, neighbours over CE ∪ SE in ascending id): ranks of the ids,
 // the BFS on rank-labelled masks (lane 0), then the final masks and order.
-__device__ void warp_relabel(WarpComp& s, int n) {
+__device__ void warp_relabel(WarpDisc& s, int n) {
   const int lane = threadIdx.x & 31;
   for (int i = lane; i < n; i += 32) {
     const int vi = s.verts[i];
@@ -444,7 +459,7 @@ __device__ void warp_relabel(WarpComp& s, int n) {
 // The sequential DFS of R4-R7 on lane 0 (the oracle's node order and budget).
 // W = 32-bit words read the low halves of the 64-bit masks (stride 2).
 template <int K, typename W>
-__device__ unsigned comp_dfs(WarpComp& s, int n, int w_stitch, unsigned budget, int& best_cost, bool& trunc) {
+__device__ unsigned comp_dfs(WarpSearch& s, int n, int w_stitch, unsigned budget, int& best_cost, bool& trunc) {
   constexpr int as = sizeof(unsigned long long) / sizeof(W);
   const W* a = (const W*)s.adj;
   const W* sa = (const W*)s.sadj;
@@ -455,7 +470,7 @@ __device__ unsigned comp_dfs(WarpComp& s, int n, int w_stitch, unsigned budget, 
   SeqIncumbent inc;
   const int ncl = clique_min<K>() ? clique_partition<W>(a, as, n, cl, 1, clique_min<K>()) : 0;
   const unsigned steps = dfs<K, W, SeqIncumbent>(a, sa, as, C, B, WordOps<W>::full(n), 0, -1, w_stitch, budget,
-                                                 (Frame<W>*)s.dadj, 1, cl, 1, ncl, inc, bestC, trunc);
+                                                 (Frame<W>*)s.stack, 1, cl, 1, ncl, inc, bestC, trunc);
 #pragma unroll
   for (int c = 0; c < K; ++c) s.cl[c] = (unsigned long long)bestC[c];
   best_cost = inc.best;
@@ -471,43 +486,13 @@ __device__ __forceinline__ int colour_of_mask(const unsigned long long* bestC, i
   return c;
 }
 
-// Rebuild of a heavy component's matrix beyond the heavy scratch: loc[]
-// already holds every vertex's BFS position, so one thread reads the rows.
-__device__ int bfs_build(const GraphView& g, const Workspace& w, int root, int* order, unsigned long long* adjm,
-                         unsigned long long* sadjm) {
-  int n = 1;
-  order[0] = root;
-  for (int head = 0; head < n; ++head) {
-    const int v = order[head];
-    unsigned long long adj = 0ull, sadj = 0ull;
-    for (int pass = 0; pass < 2; ++pass) {
-      const int* rp = pass ? g.se_rp : g.ce_rp;
-      const int* col = pass ? g.se_col : g.ce_col;
-      for (int e = rp[v], e1 = rp[v + 1]; e < e1; ++e) {
-        const int u = col[e];
-        if (w.hround[u] != -1) continue;
-        const int lu = w.loc[u];
-        order[lu] = u;
-        n = max(n, lu + 1);
-        (pass ? sadj : adj) |= 1ull << lu;
-      }
-    }
-    adjm[head] = adj;
-    sadjm[head] = sadj;
-  }
-  return n;
-}
-
-// One warp per component seed: discovery, relabelling, the budgeted
-// sequential search on lane 0, the colours.  Exact mode hands components whose
-// search exceeds the light budget to the warp-parallel kernel below.
-template <int K>
-__global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
-                                                                              long long max_steps, int shard_index,
-                                                                              int shard_count, int* colors,
-                                                                              unsigned light_steps) {
-  __shared__ WarpComp s_comp[kCompWarps];
-  WarpComp& s = s_comp[threadIdx.x >> 5];
+// One warp per component seed: discovery, relabelling to the R5 column order
+// and the component's record in the pool (exactly one per component: the seed
+// that is its minimum).  Low register use, so 64 warps per SM discover at once.
+__global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(GraphView g, Workspace w,
+                                                                              int shard_index, int shard_count) {
+  __shared__ WarpDisc s_disc[kCompWarps];
+  WarpDisc& s = s_disc[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   Control* ctl = w.ctl;
   const int n_seed = __ldcg(&ctl->err) ? 0 : __ldcg(&ctl->n_seed);
@@ -516,18 +501,20 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     ctl->t[14] = t;
   }
-  const bool exact = max_steps <= 0;
-  const unsigned budget = exact ? light_steps
-                                : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
-  unsigned long long acc_steps = 0ull;  // statistics, accumulated on lane 0
-  int acc_maxn = 0, acc_maxsteps = 0;
-  unsigned acc_trunc = 0, acc_comp = 0;
+  unsigned acc_comp = 0;  // statistics, accumulated on lane 0
+  int acc_maxn = 0;
+  unsigned long long d_cyc = 0ull, d_n = 0ull;  // diagnostics: slowest seed of this warp
   const int nw = gridDim.x * kCompWarps;
   for (int ci = blockIdx.x * kCompWarps + (threadIdx.x >> 5); ci < n_seed; ci += nw) {
     const long long c0 = clock64();
     const int root = __ldg(&w.roots[ci]);
     if (shard_count > 1 && (int)(lowbias32((uint32_t)root) % (uint32_t)shard_count) != shard_index) continue;
+#ifdef MPLD_DIAG_DISCOVER
+    int dg = 0;
+    const int n = warp_discover(g, w, root, s, &dg);
+#else
     const int n = warp_discover(g, w, root, s);
+#endif
     if (n == -2) continue;  // the seed is not its component's minimum
     ++acc_comp;
     if (n < 0) {
@@ -537,8 +524,72 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
       }
       continue;
     }
+    // pool slot: the returning atomic is issued first, its latency hidden behind the relabelling
+    unsigned long long old = 0ull;
+    if (lane == 0) old = atomicAdd(&ctl->comp_pool, (1ull << 32) | (unsigned long long)n);
     warp_relabel(s, n);
-    const long long c1 = clock64();
+    old = __shfl_sync(0xffffffffu, old, 0);
+    const unsigned off = (unsigned)old;
+    const unsigned c = (unsigned)(old >> 32);
+    for (int i = lane; i < n; i += 32) {
+      w.pmask[2 * ((size_t)off + i)] = s.adj[i];
+      w.pmask[2 * ((size_t)off + i) + 1] = s.sadj[i];
+      w.porder[off + i] = s.order[i];
+    }
+    if (lane == 0) {
+      w.crec[c] = ((unsigned long long)off << 8) | (unsigned long long)n;
+      acc_maxn = max(acc_maxn, n);
+      const unsigned long long cyc = (unsigned long long)(clock64() - c0);
+      if (cyc > d_cyc) {
+        d_cyc = cyc;
+#ifdef MPLD_DIAG_DISCOVER
+        d_n = n | (dg << 8);
+#else
+        d_n = n;
+#endif
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && acc_comp) atomicAdd(&ctl->n_comp, (int)acc_comp);
+  if (lane == 0 && acc_maxn > 0) atomicMax(&ctl->max_comp, acc_maxn);
+  if (lane == 0 && d_cyc > 0) atomicMax(&ctl->dbg[0], (d_cyc << 16) | (d_n & 0xffffull));  // diagnostics (no return)
+}
+
+// One warp per component of the pool: the budgeted sequential search on lane
+// 0 (the oracle's node order and budget, R7), then the colours.  Exact mode
+// hands components whose search exceeds the light budget to the CTA-parallel
+// kernel below.
+template <int K>
+__global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_cover_search(GraphView g, Workspace w,
+                                                                                           int w_stitch,
+                                                                                           long long max_steps,
+                                                                                           int* colors,
+                                                                                           unsigned light_steps) {
+  __shared__ WarpSearch s_search[kCompWarps];
+  WarpSearch& s = s_search[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  Control* ctl = w.ctl;
+  const int n_comp = __ldcg(&ctl->err) ? 0 : (int)(__ldcg(&ctl->comp_pool) >> 32);
+  const bool exact = max_steps <= 0;
+  const unsigned budget = exact ? light_steps
+                                : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
+  unsigned long long acc_steps = 0ull;  // statistics, accumulated on lane 0
+  int acc_maxsteps = 0;
+  unsigned acc_trunc = 0;
+  unsigned long long d_cyc = 0ull, d_n = 0ull, d_steps = 0ull;  // diagnostics: slowest component of this warp
+  const int nw = gridDim.x * kCompWarps;
+  for (int ci = blockIdx.x * kCompWarps + (threadIdx.x >> 5); ci < n_comp; ci += nw) {
+    const long long c0 = clock64();
+    const unsigned long long rec = __ldcg(&w.crec[ci]);
+    const size_t off = (size_t)(rec >> 8);
+    const int n = (int)(rec & 0xffull);
+    for (int i = lane; i < n; i += 32) {
+      const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
+      s.adj[i] = m.x;
+      s.sadj[i] = m.y;
+    }
+    __syncwarp();
     unsigned steps = 0;
     bool trunc = false;
     int best_cost = 0;
@@ -549,51 +600,31 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
         steps = comp_dfs<K, unsigned long long>(s, n, w_stitch, budget, best_cost, trunc);
     }
     __syncwarp();
-    for (int i = lane; i < n; i += 32) {
-      const int v = s.order[i];
-      colors[v] = colour_of_mask<K>(s.cl, i);
-      w.loc[v] = i;  // BFS position (rebuild of heavy components beyond the scratch)
-    }
+    for (int i = lane; i < n; i += 32) colors[__ldcg(&w.porder[off + i])] = colour_of_mask<K>(s.cl, i);
     trunc = __shfl_sync(0xffffffffu, trunc, 0);
-    if (trunc && exact) {  // hand the component to the warp-parallel search
-      int h = 0;
-      if (lane == 0) {
-        h = atomicAdd(&ctl->n_heavy, 1);
-        w.hroot[h] = root;
-        w.hcost[h] = best_cost;
-      }
-      h = __shfl_sync(0xffffffffu, h, 0);
-      if (h < kHeavyScratch) {  // keep the matrix so the warp need not rebuild it
-        for (int i = lane; i < n; i += 32) {
-          w.hmask[(size_t)h * 2 * kMaxComp + i] = s.adj[i];
-          w.hmask[(size_t)h * 2 * kMaxComp + kMaxComp + i] = s.sadj[i];
-          w.horder[(size_t)h * kMaxComp + i] = s.order[i];
-        }
-        if (lane == 0) w.hn[h] = n;
-      }
-    }
     if (lane == 0) {
-      acc_steps += steps;
-      acc_maxn = max(acc_maxn, n);
-      if (!(trunc && exact)) {
+      if (trunc && exact) {  // hand the component to the CTA-parallel search
+        const int h = atomicAdd(&ctl->n_heavy, 1);
+        w.hcomp[h] = ci;
+        w.hcost[h] = best_cost;
+      } else {
         acc_maxsteps = max(acc_maxsteps, (int)min(steps, (unsigned)INT_MAX));
         acc_trunc += trunc ? 1 : 0;
       }
-      const long long c2 = clock64();
-      if ((unsigned long long)(c2 - c0) > ctl->dbg[0]) {  // diagnostics (racy by design)
-        atomicMax(&ctl->dbg[0], (unsigned long long)(c2 - c0));
-        ctl->dbg[1] = c1 - c0;
-        ctl->dbg[2] = c2 - c1;
-        ctl->dbg[3] = n;
-        ctl->dbg[4] = steps;
+      acc_steps += steps;
+      const unsigned long long cyc = (unsigned long long)(clock64() - c0);
+      if (cyc > d_cyc) {
+        d_cyc = cyc;
+        d_n = n;
+        d_steps = steps;
       }
     }
     __syncwarp();
   }
-  if (lane == 0 && acc_comp) atomicAdd(&ctl->n_comp, (int)acc_comp);
-  if (lane == 0 && acc_maxn > 0) {
+  if (lane == 0 && d_cyc > 0)  // diagnostics (no return): cycles << 24 | steps << 8 | n
+    atomicMax(&ctl->dbg[2], (d_cyc << 24) | (min(d_steps, 0xffffull) << 8) | (d_n & 0xffull));
+  if (lane == 0 && acc_steps) {
     atomicAdd(&ctl->steps, acc_steps);
-    atomicMax(&ctl->max_comp, acc_maxn);
     atomicMax(&ctl->max_steps_comp, acc_maxsteps);
     if (acc_trunc) atomicAdd(&ctl->truncated, (int)acc_trunc);
   }
@@ -609,10 +640,19 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
 // of R5 (a few mask operations per level), so the level buffers cost 8 bytes
 // per node.
 
-constexpr int kHeavyThreads = 128;
-constexpr int kHeavyTargetNodes = 3 * kHeavyThreads;  // subtrees wanted
+#ifndef MPLD_HEAVY_THREADS
+#define MPLD_HEAVY_THREADS 128
+#endif
+#ifndef MPLD_HEAVY_MULT
+#define MPLD_HEAVY_MULT 1
+#endif
+constexpr int kHeavyThreads = MPLD_HEAVY_THREADS;
+constexpr int kHeavyTargetNodes = MPLD_HEAVY_MULT * kHeavyThreads;  // subtrees wanted
 constexpr int kHeavyCapNodes = 2 * kHeavyTargetNodes;  // level buffer capacity
-constexpr int kHeavyStackBytes = 32 * 1024;            // DFS stacks of the lanes (n frames each)
+#ifndef MPLD_HEAVY_STACK_KB
+#define MPLD_HEAVY_STACK_KB 32
+#endif
+constexpr int kHeavyStackBytes = MPLD_HEAVY_STACK_KB * 1024;  // DFS stacks of the lanes (n frames each)
 constexpr int kPathDepthShift = 58;
 constexpr int kPathMaxDepth = 29;                      // 2 bits per level below the depth field
 
@@ -724,7 +764,11 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
   // level-synchronous split of the canonical tree, DFS order preserved
   int m = 1, cur = 0;
   unsigned expanded = 0;
+#ifdef MPLD_HEAVY_DIAG_SEQ
+  while (false) {
+#else
   while (m < kHeavyTargetNodes) {
+#endif
     int total = 0;
     if (tid == 0) s_flag = 0;  // bit 0: some node still has uncovered columns; bit 1: depth limit reached
     __syncthreads();
@@ -768,7 +812,11 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
   const long long hc1 = clock64();
   // lanes search the subtrees in DFS order with a shared incumbent; the stack
   // region holds n frames per active lane
+#ifdef MPLD_HEAVY_DIAG_SEQ
+  const int lanes = 1;
+#else
   const int lanes = min((int)blockDim.x, (int)(kHeavyStackBytes / (n * (int)sizeof(Frame<W>))));
+#endif
   W bestC[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) bestC[c] = 0;
@@ -807,6 +855,13 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     total_steps += __shfl_xor_sync(0xffffffffu, total_steps, o);
   }
   const int any_capped = __syncthreads_or(capped);
+#ifdef MPLD_DIAG_LANESTEPS
+  __shared__ unsigned s_maxsteps;
+  if (tid == 0) s_maxsteps = 0;
+  __syncthreads();
+  atomicMax(&s_maxsteps, steps);
+  __syncthreads();
+#endif
   if (lane == 0) {
     s_red[wid] = wmin;
     s_tmp[wid] = (int)total_steps;
@@ -826,7 +881,11 @@ __device__ void heavy_component(int n, const int* s_order, const unsigned long l
     const long long hc2 = clock64();
     if ((unsigned long long)(hc2 - hc0) > ctl->dbg[5]) {  // diagnostics (racy by design)
       atomicMax(&ctl->dbg[5], (unsigned long long)(hc2 - hc0));
+#ifdef MPLD_DIAG_LANESTEPS
+      ctl->dbg[6] = ((unsigned long long)s_maxsteps << 32) | (unsigned)(ts + expanded);
+#else
       ctl->dbg[6] = hc1 - hc0;
+#endif
       ctl->dbg[7] = ((unsigned long long)m << 32) | (unsigned)n;
     }
   }
@@ -843,25 +902,19 @@ __global__ void __launch_bounds__(kHeavyThreads) mpld_exact_cover_search_heavy(G
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_order[kMaxComp];
   __shared__ unsigned long long s_adj64[kMaxComp], s_sadj64[kMaxComp];
-  __shared__ int s_n;
   Control* ctl = w.ctl;
   const int n_heavy = __ldcg(&ctl->n_heavy);
   for (int h = blockIdx.x; h < n_heavy; h += gridDim.x) {
-    const int root = __ldcg(&w.hroot[h]);
     const int c1 = __ldcg(&w.hcost[h]);
-    if (h < kHeavyScratch) {  // the component kernel kept the matrix
-      const int n = __ldcg(&w.hn[h]);
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        s_order[i] = __ldcg(&w.horder[(size_t)h * kMaxComp + i]);
-        s_adj64[i] = __ldcg(&w.hmask[(size_t)h * 2 * kMaxComp + i]);
-        s_sadj64[i] = __ldcg(&w.hmask[(size_t)h * 2 * kMaxComp + kMaxComp + i]);
-      }
-      if (threadIdx.x == 0) s_n = n;
-    } else if (threadIdx.x == 0) {  // rebuild: loc[] already holds every vertex's BFS position
-      s_n = bfs_build(g, w, root, s_order, s_adj64, s_sadj64);
+    const unsigned long long rec = __ldcg(&w.crec[__ldcg(&w.hcomp[h])]);
+    const size_t off = (size_t)(rec >> 8);
+    const int n = (int)(rec & 0xffull);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      s_order[i] = __ldcg(&w.porder[off + i]);
+      s_adj64[i] = __ldcg(&w.pmask[2 * (off + i)]);
+      s_sadj64[i] = __ldcg(&w.pmask[2 * (off + i) + 1]);
     }
     __syncthreads();
-    const int n = s_n;
     if (n <= 32)
       heavy_component<K, unsigned>(n, s_order, s_adj64, s_sadj64, smem, w_stitch, c1, colors, ctl);
     else
@@ -872,21 +925,23 @@ __global__ void __launch_bounds__(kHeavyThreads) mpld_exact_cover_search_heavy(G
 
 }  // namespace
 
-cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
-                          int shard_index, int shard_count, int* colors, unsigned light_steps, cudaStream_t s,
-                          int blocks) {
+cudaError_t launch_discover(const GraphView& g, Workspace ws, int shard_index, int shard_count, cudaStream_t s,
+                            int blocks) {
+  mpld_component_discover<<<blocks, kCompWarps * 32, 0, s>>>(g, ws, shard_index, shard_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
+                          unsigned light_steps, cudaStream_t s, int blocks) {
   switch (k) {
     case 2:
-      mpld_exact_cover_search<2><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, shard_index,
-                                                                      shard_count, colors, light_steps);
+      mpld_exact_cover_search<2><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps);
       break;
     case 3:
-      mpld_exact_cover_search<3><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, shard_index,
-                                                                      shard_count, colors, light_steps);
+      mpld_exact_cover_search<3><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps);
       break;
     case 4:
-      mpld_exact_cover_search<4><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, shard_index,
-                                                                      shard_count, colors, light_steps);
+      mpld_exact_cover_search<4><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps);
       break;
     default: return cudaErrorInvalidValue;
   }
@@ -926,6 +981,12 @@ cudaError_t configure_search_heavy() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   return e;
+}
+
+int resident_blocks_discover(int num_sms) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_component_discover, kCompWarps * 32, 0);
+  return per_sm * num_sms;
 }
 
 int resident_blocks_search(int threads, int num_sms) {

@@ -4,13 +4,15 @@
 // Launch sequence of one call (all on one stream, no host synchronisation):
 //   mpld_simplify_components   cooperative: validation, simplification rounds, seeds,
 //                              recovery pop keys and level 0
-//   mpld_exact_cover_search<K> one warp per component seed
+//   mpld_component_discover    one warp per seed: components -> pool of bit-packed matrices
+//   mpld_exact_cover_search<K> one warp per component of the pool
 //   mpld_exact_cover_search_heavy<K> (exact mode) one warp per heavy component
 //   mpld_recover               cooperative: LIFO recovery of hidden vertices
 //   mpld_evaluate              Eq. (1) per layout + stats
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -35,9 +37,10 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(MPLD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-enum KernelId { K_SIMPLIFY = 0, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_COUNT };
-const char* kKernelNames[K_COUNT] = {"mpld_simplify_components", "mpld_exact_cover_search",
-                                     "mpld_exact_cover_search_heavy", "mpld_recover", "mpld_evaluate"};
+enum KernelId { K_SIMPLIFY = 0, K_DISCOVER, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_COUNT };
+const char* kKernelNames[K_COUNT] = {"mpld_simplify_components", "mpld_component_discover",
+                                     "mpld_exact_cover_search", "mpld_exact_cover_search_heavy", "mpld_recover",
+                                     "mpld_evaluate"};
 
 constexpr int kCoopThreads = 1024;
 
@@ -55,13 +58,12 @@ struct mpld_context {
   unsigned long long* key = nullptr;
   int* q0 = nullptr;
   int* q1 = nullptr;
-  int* loc = nullptr;
   int* roots = nullptr;
-  int* hroot = nullptr;
+  unsigned long long* crec = nullptr;
+  unsigned long long* pmask = nullptr;
+  int* porder = nullptr;
+  int* hcomp = nullptr;
   int* hcost = nullptr;
-  unsigned long long* hmask = nullptr;
-  int* horder = nullptr;
-  int* hn = nullptr;
   Control* ctl = nullptr;
   // phase-split calls: the prepared graph
   GraphView g{};
@@ -69,7 +71,8 @@ struct mpld_context {
   bool prepared = false;
   int call_launches = 0;
   unsigned light_steps = kLightStepsDefault;  // MPLD_LIGHT_STEPS overrides (tuning)
-  int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0, blocks_heavy = 0;
+  int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0, blocks_heavy = 0,
+      blocks_discover = 0;
   // host-API staging (device copies of host inputs / outputs)
   int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
   int* h_lo = nullptr;
@@ -104,11 +107,12 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
   if (n > ctx->cap_n) {
     int64_t cap = std::max<int64_t>(n, ctx->cap_n * 3 / 2);
     cudaError_t e = cudaSuccess;
-    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->loc, &ctx->roots, &ctx->hroot, &ctx->hcost}) {
+    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->roots, &ctx->porder, &ctx->hcomp, &ctx->hcost}) {
       e = grow(p, cap);
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
-    if (grow(&ctx->prio, cap) != cudaSuccess || grow(&ctx->key, cap) != cudaSuccess)
+    if (grow(&ctx->prio, cap) != cudaSuccess || grow(&ctx->key, cap) != cudaSuccess ||
+        grow(&ctx->crec, cap) != cudaSuccess || grow(&ctx->pmask, 2 * cap) != cudaSuccess)
       return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     ctx->cap_n = cap;
   }
@@ -163,8 +167,8 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 }
 
 Workspace workspace(mpld_context* ctx) {
-  return Workspace{ctx->deg,   ctx->hround, ctx->key,   ctx->prio,   ctx->q0, ctx->q1,     ctx->loc,
-                   ctx->roots, ctx->hroot,  ctx->hcost, ctx->hmask, ctx->horder, ctx->hn, ctx->ctl};
+  return Workspace{ctx->deg,   ctx->hround, ctx->key,    ctx->prio,  ctx->q0,    ctx->q1,
+                   ctx->roots, ctx->crec,   ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->ctl};
 }
 
 // phase 1: validate?, simplification, components (colours initialised to -1)
@@ -192,13 +196,22 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
                  int shard_count, int* colors) {
   Workspace ws = workspace(ctx);
   const GraphView& g = ctx->g;
-  // the heavy queue belongs to this search call (several shards may share a context)
-  cudaError_t e0 = cudaMemsetAsync(&ctx->ctl->n_heavy, 0, sizeof(int), s);
-  if (e0 != cudaSuccess) return cuda_fail(e0, "heavy queue reset");
+  // the component pool and the heavy queue belong to this search call (several shards may share a context)
+  cudaError_t e0 = cudaMemsetAsync(&ctx->ctl->n_heavy, 0,
+                                   offsetof(Control, comp_pool) + sizeof(unsigned long long) -
+                                       offsetof(Control, n_heavy), s);
+  if (e0 != cudaSuccess) return cuda_fail(e0, "search counters reset");
+  {
+    TimedLaunch t(ctx, K_DISCOVER, s);
+    cudaError_t e = launch_discover(g, ws, shard_index, shard_count, s, ctx->blocks_discover);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_component_discover");
+    t.done();
+    ++ctx->call_launches;
+  }
   {
     TimedLaunch t(ctx, K_SEARCH, s);
-    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, shard_index, shard_count, colors,
-                                  ctx->light_steps, s, ctx->blocks_search);
+    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, s,
+                                  ctx->blocks_search);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
     t.done();
     ++ctx->call_launches;
@@ -289,10 +302,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     delete ctx;
     return fail(MPLD_ERR_CUDA, "device does not support cooperative launch");
   }
-  if (cudaMalloc((void**)&ctx->hmask, sizeof(unsigned long long) * 2 * kMaxComp * kHeavyScratch) != cudaSuccess ||
-      cudaMalloc((void**)&ctx->horder, sizeof(int) * kMaxComp * kHeavyScratch) != cudaSuccess ||
-      cudaMalloc((void**)&ctx->hn, sizeof(int) * kHeavyScratch) != cudaSuccess ||
-      cudaMalloc((void**)&ctx->ctl, sizeof(Control)) != cudaSuccess) {
+  if (cudaMalloc((void**)&ctx->ctl, sizeof(Control)) != cudaSuccess) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_NOMEM, "control block allocation failed");
   }
@@ -300,6 +310,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   ctx->blocks_simplify = coop_blocks_simplify(kCoopThreads, ctx->num_sms);
   ctx->blocks_recover = coop_blocks_recover(kCoopThreads, ctx->num_sms);
   ctx->blocks_search = resident_blocks_search(32, ctx->num_sms);
+  ctx->blocks_discover = resident_blocks_discover(ctx->num_sms);
   ctx->blocks_stream = resident_blocks_evaluate(ctx->num_sms);
   if (const char* ls = std::getenv("MPLD_LIGHT_STEPS")) {
     const long v = std::strtol(ls, nullptr, 10);
@@ -311,7 +322,8 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     return cuda_fail(e, "configure heavy search");
   }
   ctx->blocks_heavy = resident_blocks_heavy(ctx->num_sms);
-  if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0 || ctx->blocks_heavy <= 0) {
+  if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0 || ctx->blocks_heavy <= 0 ||
+      ctx->blocks_discover <= 0) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_CUDA, "occupancy query failed (kernel image missing for this device?)");
   }
@@ -332,7 +344,8 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
 void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->key, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
-                  (void*)ctx->loc, (void*)ctx->roots, (void*)ctx->hroot, (void*)ctx->hcost, (void*)ctx->hmask, (void*)ctx->horder, (void*)ctx->hn, (void*)ctx->ctl, (void*)ctx->h_lo,
+                  (void*)ctx->roots, (void*)ctx->crec, (void*)ctx->pmask, (void*)ctx->porder, (void*)ctx->hcomp,
+                  (void*)ctx->hcost, (void*)ctx->ctl, (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
                   (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})
     if (p) cudaFree(p);

@@ -2,10 +2,14 @@
 //
 // Data layout in HBM:
 //   graph     : caller's CSR arrays (int32), read-only.
-//   per vertex: deg, hround, prio, loc (int32), key (u64) — indexed by vertex id
+//   per vertex: deg, hround, prio (int32), key (u64) — indexed by vertex id
 //   queues    : q0, q1 (int32 [n]) — simplification frontiers, then recovery levels
-//   heavy list: hroot, hcost (int32 [n]) — exact mode's warp-parallel components
-//   per comp. : roots (int32 [n]); heavy scratch: hmask/horder/hn (kHeavyScratch slots)
+//   seeds     : roots (int32 [n])
+//   component pool (filled by the discovery kernel, one record per component):
+//               crec (u64 [n]) = pool offset << 8 | size; pmask (u64 [2n]) = adj/sadj
+//               words of every component vertex in BFS column order (R5),
+//               interleaved; porder (int32 [n]) = their vertex ids
+//   heavy list: hcomp, hcost (int32 [n]) — exact mode's CTA-parallel components
 //   Control   : one control block (counters, barrier arrivals, error bits,
 //               diagnostics) per context, zeroed at the start of every call.
 #pragma once
@@ -19,7 +23,6 @@ namespace mpld {
 
 constexpr int kMaxComp = MPLD_MAX_COMPONENT;  // one 64-bit word per mask
 constexpr int kCostUnits = MPLD_COST_UNITS;
-constexpr int kHeavyScratch = 4096;  // heavy components whose matrices are kept for the warp kernel
 
 enum ErrBits : int { kErrGraph = 1, kErrComponent = 2 };
 
@@ -40,7 +43,9 @@ struct Control {
   int tcnt[3];               // ... the same, for the single-CTA tails (never read by other CTAs)
   int trq[3];
   int n_levels;              // recovery levels (DAG depth + 1)
-  int n_heavy;               // exact mode: components handed to the warp-parallel search
+  int n_heavy;               // exact mode: components handed to the CTA-parallel search (reset per search call)
+  int pad_;
+  unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
   unsigned long long steps;  // search nodes entered
   unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)
   unsigned bar[2];           // grid-barrier arrival counters of the two cooperative kernels
@@ -93,13 +98,12 @@ struct Workspace {
   unsigned* prio;  // lowbias32(layout-local id), recovery priority (R9)
   int* q0;         // frontier queues (double-buffered)
   int* q1;
-  int* loc;        // local index of a kept vertex inside its component
   int* roots;      // component-search seeds (kept vertices without a smaller kept neighbour)
-  int* hroot;      // heavy components (exact mode): seed ...
+  unsigned long long* crec;   // component records: pool offset << 8 | size
+  unsigned long long* pmask;  // component pool: adj, sadj word pairs in BFS column order
+  int* porder;                // component pool: vertex ids in BFS column order
+  int* hcomp;      // heavy components (exact mode): component index ...
   int* hcost;      // ... and the light phase's best cost
-  unsigned long long* hmask;  // heavy components kept by the light search: adj/sadj masks
-  int* horder;                // ... their BFS orders
-  int* hn;                    // ... their sizes
   Control* ctl;
 };
 
@@ -117,9 +121,10 @@ __host__ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
 // cudaError_t of its launch.
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors,
                                        long long* counts, int validate, cudaStream_t s, int blocks, int threads);
-cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
-                          int shard_index, int shard_count, int* colors, unsigned light_steps, cudaStream_t s,
-                          int blocks);
+cudaError_t launch_discover(const GraphView& g, Workspace ws, int shard_index, int shard_count, cudaStream_t s,
+                            int blocks);
+cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
+                          unsigned light_steps, cudaStream_t s, int blocks);
 constexpr unsigned kLightStepsDefault = 48;  // exact mode: one-lane budget before a component turns heavy
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
                                 int blocks);
@@ -134,6 +139,7 @@ cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors,
 int coop_blocks_simplify(int threads, int num_sms);
 int coop_blocks_recover(int threads, int num_sms);
 int resident_blocks_search(int threads, int num_sms);
+int resident_blocks_discover(int num_sms);
 int resident_blocks_evaluate(int num_sms);
 int resident_blocks_heavy(int num_sms);  // after configure_search_heavy()
 

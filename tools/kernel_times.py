@@ -51,7 +51,9 @@ def run(b, k, alpha, iters=10, flush=None, max_steps=1 << 20, flags=1):
           "evaluate start", rel(15), "levels", int(d[16]), "rounds", int(d[18]))
     rr = [(i, rel(20 + i), int(d[52 + i])) for i in range(32) if d[20 + i]]
     print("  rounds/levels (index, us, frontier):", rr)
-    print("  slowest light search thread: cycles total/build/search, n, steps:", d[84:89].tolist())
+    dd, ds = int(d[84]), int(d[86])
+    print("  slowest discovery: cycles, n(|groups<<8|chunks<<16 in diag builds):", dd >> 16, dd & 0xffff,
+          "| slowest light search: cycles, steps, n:", ds >> 24, (ds >> 8) & 0xffff, ds & 0xff)
     print("  slowest heavy warp: cycles total/split, subtrees, n:", int(d[89]), int(d[90]), int(d[91]) >> 32,
           int(d[91]) & 0xffffffff)
     print("  seeds, heavy components, components:", int(d[92]), int(d[93]), int(d[94]))

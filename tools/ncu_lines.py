@@ -30,7 +30,11 @@ def main():
         if hdr is None or len(r) < len(hdr):
             continue
         key = (fname, int(r[0]) if r[0].isdigit() else -1)
-        num = lambda x: float(x) if x not in ("", "-") else 0.0  # noqa: E731
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return 0.0
         s = num(r[4])
         by_line[key] += s
         text.setdefault(key, r[1].strip()[:90])
