@@ -46,6 +46,34 @@ constexpr int kCoopThreads = 1024;
 
 }  // namespace
 
+// One staging slot of the asynchronous host entry point: device copies of a
+// batch's inputs and outputs, pinned host copies of the outputs that need
+// post-processing, and the events that order upload -> compute -> download.
+struct AsyncSlot {
+  int* lo = nullptr;
+  int* ce_rp = nullptr;
+  int* ce_col = nullptr;
+  int* se_rp = nullptr;
+  int* se_col = nullptr;
+  int* colors = nullptr;
+  long long* counts = nullptr;
+  double* cost = nullptr;
+  long long* stats = nullptr;
+  int64_t cap_n = -1, cap_ce = -1, cap_se = -1;
+  int32_t cap_l = -1;
+  long long* h_counts = nullptr;  // pinned
+  long long* h_stats = nullptr;   // pinned [MPLD_STAT_LEN]
+  cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr, ev_d2h = nullptr;
+  int64_t ticket = -1;      // submit in flight (or last submitted)
+  bool pending = false;     // its results still need post-processing
+  int64_t fin_ticket = -1;  // last post-processed submit and its return code
+  int fin_rc = MPLD_OK;
+  int32_t n_layouts = 0;    // user outputs of the submit in flight
+  int64_t* u_nc = nullptr;
+  int64_t* u_ns = nullptr;
+  int64_t* u_stats = nullptr;
+};
+
 struct mpld_context {
   int device = 0;
   int num_sms = 0;
@@ -84,7 +112,11 @@ struct mpld_context {
   long long* h_counts = nullptr;
   double* h_cost = nullptr;
   long long* h_stats = nullptr;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // compute stream of the host entry points
+  // asynchronous host entry point: two staging slots, upload / download streams
+  AsyncSlot slot[2];
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  int64_t next_ticket = 0;
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -281,6 +313,61 @@ mpld_context* host_context(int* err) {
   return g_host_ctx[dev];
 }
 
+
+// ---- asynchronous host entry point -------------------------------------------
+
+int slot_reserve(AsyncSlot& a, int64_t n, int64_t m_ce, int64_t m_se, int32_t L) {
+  if (!a.ev_h2d) {
+    if (cudaEventCreateWithFlags(&a.ev_h2d, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.ev_comp, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.ev_d2h, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMallocHost((void**)&a.h_stats, sizeof(long long) * MPLD_STAT_LEN) != cudaSuccess)
+      return fail(MPLD_ERR_NOMEM, "async slot allocation failed");
+  }
+  if (n > a.cap_n) {
+    a.cap_n = std::max<int64_t>(n, a.cap_n * 3 / 2);
+    if (grow(&a.ce_rp, a.cap_n + 1) != cudaSuccess || grow(&a.se_rp, a.cap_n + 1) != cudaSuccess ||
+        grow(&a.colors, a.cap_n) != cudaSuccess)
+      return fail(MPLD_ERR_NOMEM, "async staging allocation failed");
+  }
+  if (m_ce > a.cap_ce) {
+    a.cap_ce = std::max<int64_t>(m_ce, a.cap_ce * 3 / 2);
+    if (grow(&a.ce_col, a.cap_ce) != cudaSuccess) return fail(MPLD_ERR_NOMEM, "async staging allocation failed");
+  }
+  if (m_se > a.cap_se) {
+    a.cap_se = std::max<int64_t>(m_se, a.cap_se * 3 / 2);
+    if (grow(&a.se_col, a.cap_se) != cudaSuccess) return fail(MPLD_ERR_NOMEM, "async staging allocation failed");
+  }
+  if (L > a.cap_l) {
+    a.cap_l = std::max<int32_t>(L, 16);
+    if (a.h_counts) cudaFreeHost(a.h_counts);
+    a.h_counts = nullptr;
+    if (grow(&a.lo, a.cap_l + 1) != cudaSuccess || grow(&a.counts, 2 * (int64_t)a.cap_l) != cudaSuccess ||
+        grow(&a.cost, a.cap_l) != cudaSuccess || grow(&a.stats, MPLD_STAT_LEN) != cudaSuccess ||
+        cudaMallocHost((void**)&a.h_counts, sizeof(long long) * 2 * a.cap_l) != cudaSuccess)
+      return fail(MPLD_ERR_NOMEM, "async staging allocation failed");
+  }
+  return MPLD_OK;
+}
+
+// wait for the slot's submit, then split the counts and check the error bits
+int slot_finish(AsyncSlot& a) {
+  if (!a.pending) return a.fin_rc;
+  a.pending = false;
+  a.fin_ticket = a.ticket;
+  cudaError_t e = cudaEventSynchronize(a.ev_d2h);
+  if (e != cudaSuccess) return a.fin_rc = cuda_fail(e, "async pipeline / D2H copy");
+  for (int l = 0; l < a.n_layouts; ++l) {
+    a.u_nc[l] = a.h_counts[2 * l];
+    a.u_ns[l] = a.h_counts[2 * l + 1];
+  }
+  if (a.u_stats) std::memcpy(a.u_stats, a.h_stats, sizeof(long long) * MPLD_STAT_LEN);
+  const long long err = a.h_stats[MPLD_STAT_ERROR];
+  if (err & kErrGraph) return a.fin_rc = fail(MPLD_ERR_GRAPH, "graph violates the CSR invariants of mpld.h");
+  if (err & kErrComponent) return a.fin_rc = fail(MPLD_ERR_COMPONENT, "a component exceeds MPLD_MAX_COMPONENT vertices");
+  return a.fin_rc = MPLD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -355,6 +442,17 @@ void mpld_context_destroy(mpld_context* ctx) {
     cudaEventDestroy(p.second.second);
   }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  for (AsyncSlot& a : ctx->slot) {
+    for (void* p : {(void*)a.lo, (void*)a.ce_rp, (void*)a.ce_col, (void*)a.se_rp, (void*)a.se_col, (void*)a.colors,
+                    (void*)a.counts, (void*)a.cost, (void*)a.stats})
+      if (p) cudaFree(p);
+    if (a.h_counts) cudaFreeHost(a.h_counts);
+    if (a.h_stats) cudaFreeHost(a.h_stats);
+    for (cudaEvent_t e : {a.ev_h2d, a.ev_comp, a.ev_d2h})
+      if (e) cudaEventDestroy(e);
+  }
+  if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+  if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
   delete ctx;
 }
 
@@ -502,6 +600,82 @@ int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32
     return fail(MPLD_ERR_COMPONENT, "a component exceeds MPLD_MAX_COMPONENT vertices");
   g_last_error.clear();
   return MPLD_OK;
+}
+
+int mpld_decompose_batch_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
+                               const int32_t* ce_rowptr, const int32_t* ce_col, const int32_t* se_rowptr,
+                               const int32_t* se_col, int32_t k, double alpha, int64_t max_steps, uint32_t flags,
+                               int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches, double* cost,
+                               int64_t* stats, int64_t* ticket) {
+  if (!ctx || !ticket) return fail(MPLD_ERR_ARG, "bad context / ticket pointer");
+  int w_stitch = 0;
+  int rc = check_scalars(n, k, alpha, &w_stitch);
+  if (rc != MPLD_OK) return rc;
+  if (n_layouts < 1 || !layout_offsets || !ce_rowptr || !se_rowptr || (n > 0 && !colors) || !n_conflicts ||
+      !n_stitches || !cost)
+    return fail(MPLD_ERR_ARG, "bad argument (NULL pointer or n_layouts < 1)");
+  if (layout_offsets[0] != 0 || layout_offsets[n_layouts] != n)
+    return fail(MPLD_ERR_ARG, "layout_offsets must start at 0 and end at n");
+  const int64_t m_ce = ce_rowptr[n], m_se = se_rowptr[n];
+  if (m_ce < 0 || m_se < 0 || (m_ce > 0 && !ce_col) || (m_se > 0 && !se_col))
+    return fail(MPLD_ERR_ARG, "bad CSR row pointer / column array");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaSetDevice(ctx->device);
+  if (!ctx->s_h2d) {
+    if (cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(MPLD_ERR_CUDA, "async stream creation failed");
+  }
+  const int64_t t = ctx->next_ticket;
+  AsyncSlot& a = ctx->slot[t & 1];
+  slot_finish(a);  // the slot's previous submit (t - 2) is complete and post-processed before reuse
+  if (n > ctx->cap_n) cudaStreamSynchronize(ctx->stream);  // the workspace grows: the other slot's compute must end
+  rc = ensure_workspace(ctx, n, n_layouts);
+  if (rc == MPLD_OK) rc = slot_reserve(a, n, m_ce, m_se, n_layouts);
+  if (rc != MPLD_OK) return rc;
+  cudaStream_t up = ctx->s_h2d, ks = ctx->stream, down = ctx->s_d2h;
+  cudaError_t e = cudaMemcpyAsync(a.lo, layout_offsets, sizeof(int) * (n_layouts + 1), cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(a.ce_rp, ce_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(a.se_rp, se_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && m_ce) e = cudaMemcpyAsync(a.ce_col, ce_col, sizeof(int) * m_ce, cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && m_se) e = cudaMemcpyAsync(a.se_col, se_col, sizeof(int) * m_se, cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess) e = cudaEventRecord(a.ev_h2d, up);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, a.ev_h2d, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "async H2D copy");
+  GraphView g{n, n_layouts, a.lo, a.ce_rp, a.ce_col, a.se_rp, a.se_col};
+  rc = run_pipeline(ctx, ks, g, k, w_stitch, alpha, (long long)max_steps, flags, a.colors, a.counts, a.cost,
+                    a.stats);
+  if (rc != MPLD_OK) return rc;
+  e = cudaEventRecord(a.ev_comp, ks);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(down, a.ev_comp, 0);
+  if (e == cudaSuccess && n > 0) e = cudaMemcpyAsync(colors, a.colors, sizeof(int) * n, cudaMemcpyDeviceToHost, down);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(a.h_counts, a.counts, sizeof(long long) * 2 * n_layouts, cudaMemcpyDeviceToHost, down);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(cost, a.cost, sizeof(double) * n_layouts, cudaMemcpyDeviceToHost, down);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(a.h_stats, a.stats, sizeof(long long) * MPLD_STAT_LEN, cudaMemcpyDeviceToHost, down);
+  if (e == cudaSuccess) e = cudaEventRecord(a.ev_d2h, down);
+  // the next upload into this slot must not overwrite inputs the compute still reads
+  if (e != cudaSuccess) return cuda_fail(e, "async D2H copy");
+  a.ticket = t;
+  a.pending = true;
+  a.n_layouts = n_layouts;
+  a.u_nc = n_conflicts;
+  a.u_ns = n_stitches;
+  a.u_stats = stats;
+  ctx->next_ticket = t + 1;
+  *ticket = t;
+  g_last_error.clear();
+  return MPLD_OK;
+}
+
+int mpld_wait(mpld_context* ctx, int64_t ticket) {
+  if (!ctx || ticket < 0 || ticket >= ctx->next_ticket) return fail(MPLD_ERR_ARG, "bad context / unknown ticket");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  AsyncSlot& a = ctx->slot[ticket & 1];
+  if (a.pending && a.ticket == ticket) return slot_finish(a);
+  if (a.fin_ticket == ticket) return a.fin_rc;
+  return MPLD_OK;  // an older submit of this slot: completed before the slot was reused
 }
 
 int mpld_decompose(int32_t n, const int32_t* ce_rowptr, const int32_t* ce_col, const int32_t* se_rowptr,

@@ -31,7 +31,8 @@ MPLD_STAT_LEN = len(STAT_NAMES)
 EXPORTS = ["mpld_last_error", "mpld_version", "mpld_decompose", "mpld_decompose_batch", "mpld_context_create",
            "mpld_context_destroy", "mpld_decompose_device", "mpld_context_set_timing",
            "mpld_context_reset_timing", "mpld_kernel_count", "mpld_kernel_name", "mpld_context_kernel_time",
-           "mpld_context_debug", "mpld_prepare_device", "mpld_search_device", "mpld_finish_device"]
+           "mpld_context_debug", "mpld_prepare_device", "mpld_search_device", "mpld_finish_device",
+           "mpld_decompose_batch_async", "mpld_wait"]
 
 
 class MPLDError(RuntimeError):
@@ -78,6 +79,10 @@ def lib():
                                       ctypes.c_int32, ctypes.c_uint32, _vp, _vp]
     L.mpld_search_device.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp]
     L.mpld_finish_device.argtypes = [_vp, _vp, ctypes.c_double, _vp, _vp, _vp, _vp]
+    L.mpld_decompose_batch_async.argtypes = [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp, _vp, _vp, _vp,
+                                             ctypes.c_int32, ctypes.c_double, ctypes.c_int64, ctypes.c_uint32, _vp,
+                                             _vp, _vp, _vp, _vp, _i64p]
+    L.mpld_wait.argtypes = [_vp, ctypes.c_int64]
     _lib = L
     return L
 
@@ -95,6 +100,17 @@ def _host_ptr(x, dtype=np.int32):
         return x.data_ptr(), x
     a = np.ascontiguousarray(x, dtype=dtype)
     return a.ctypes.data, a
+
+
+def _out_ptr(x):
+    """Address of a host output buffer (written in place: must be contiguous)."""
+    if hasattr(x, "data_ptr"):
+        if x.is_cuda or not x.is_contiguous():
+            raise ValueError("host outputs must be contiguous CPU tensors / arrays")
+        return x.data_ptr()
+    if not x.flags["C_CONTIGUOUS"]:
+        raise ValueError("host outputs must be contiguous CPU tensors / arrays")
+    return x.ctypes.data
 
 
 def _dev_ptr(t):
@@ -170,6 +186,42 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def submit(self, layout_offsets, n, ce_rowptr, ce_col, se_rowptr, se_col, k, alpha, max_steps=0, flags=0,
+               out=None):
+        """C ABI `mpld_decompose_batch_async`: host buffers (numpy arrays or CPU
+        tensors; pinned memory for asynchronous copies), returns a ticket.  The
+        result dict (colors, n_conflicts, n_stitches, cost, stats) is complete
+        after `wait(ticket)`; `out` may supply preallocated output arrays."""
+        L = lib()
+        lo_p, lo = _host_ptr(layout_offsets)
+        n_layouts = int(len(lo) - 1) if not hasattr(lo, "numel") else int(lo.numel() - 1)
+        if out is None:
+            out = {"colors": np.empty(max(int(n), 0), dtype=np.int32),
+                   "n_conflicts": np.zeros(n_layouts, dtype=np.int64),
+                   "n_stitches": np.zeros(n_layouts, dtype=np.int64),
+                   "cost": np.zeros(n_layouts, dtype=np.float64),
+                   "stats": np.zeros(MPLD_STAT_LEN, dtype=np.int64)}
+        keep = [lo] + [_host_ptr(a) for a in (ce_rowptr, ce_col, se_rowptr, se_col)]
+        ptr = {key: _out_ptr(v) for key, v in out.items()}
+        t = ctypes.c_int64()
+        _check(L.mpld_decompose_batch_async(self._h, n_layouts, lo_p, int(n), *[p for p, _ in keep[1:]], int(k),
+                                            float(alpha), int(max_steps), int(flags), ptr["colors"],
+                                            ptr["n_conflicts"], ptr["n_stitches"], ptr["cost"], ptr["stats"],
+                                            ctypes.byref(t)))
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[t.value] = (keep, out)
+        return t.value
+
+    def wait(self, ticket: int):
+        """C ABI `mpld_wait`: block until `ticket` completed; returns its result dict."""
+        keep, out = self._inflight.pop(ticket)
+        _check(lib().mpld_wait(self._h, int(ticket)))
+        res = dict(out)
+        st = res["stats"]
+        res["stats"] = dict(zip(STAT_NAMES, (st.tolist() if hasattr(st, "tolist") else list(st))))
+        return res
 
     def decompose_device(self, layout_offsets, n, ce_rowptr, ce_col, se_rowptr, se_col, k, alpha, max_steps,
                          colors, counts, cost, stats=None, flags: int = 0, stream=None):
