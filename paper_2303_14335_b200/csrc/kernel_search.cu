@@ -131,14 +131,25 @@ __host__ __device__ constexpr int clique_min() {
   return K >= 4 ? K : 0;  // 0: no cliques
 }
 
+// Exact mode's warp-parallel search may use any valid bound (its result is
+// the canonical leaf whatever it prunes); the clique term pays off there for
+// k = 3 as well (cliques of >= MPLD_HEAVY_CLIQUE vertices, 0 = as the light search).
+#ifndef MPLD_HEAVY_CLIQUE
+#define MPLD_HEAVY_CLIQUE 0
+#endif
+template <int K>
+__host__ __device__ constexpr int heavy_clique_min() {
+  return MPLD_HEAVY_CLIQUE > 0 ? MPLD_HEAVY_CLIQUE : clique_min<K>();
+}
+
 // Lower bound of R7 in conflicts: columns with no live row, plus, over the
 // cliques, max(0, |X| - #masks live on X) for X = the clique's uncovered
 // columns that still have a live row.
-template <int K, typename W>
+template <int K, typename W, bool kCliques = (clique_min<K>() > 0)>
 __device__ __forceinline__ int bound_conflicts(const W (&B)[K], W U, W Z, const W* cl, int cs, int ncl) {
   using O = WordOps<W>;
   int lb = O::popc(Z);
-  if constexpr (clique_min<K>() > 0) {
+  if constexpr (kCliques) {
     for (int q = 0; q < ncl; ++q) {
       const W X = cl[q * cs] & U & ~Z;
       if (!X) continue;
@@ -158,28 +169,6 @@ struct SeqIncumbent {
   __device__ __forceinline__ bool prune(int lb) const { return lb >= best; }
   __device__ __forceinline__ bool improves(int cost) const { return cost < best; }
   __device__ __forceinline__ void take(int cost) { best = cost; }
-};
-
-// Incumbent of the warp-parallel search: keys (cost << 32 | subtree + 1),
-// shared through a shared-memory atomicMin; a node of subtree f is pruned when
-// (lb, f+1) >= the best key, so equal-cost leaves of earlier
-// subtrees always win.
-struct ParIncumbent {
-  unsigned long long* shared_best;
-  unsigned long long fkey;  // f + 1
-  unsigned long long lane_best = ~0ull;
-  __device__ __forceinline__ bool has() const { return true; }
-  __device__ __forceinline__ bool prune(int lb) const {
-    const unsigned long long g = *((volatile unsigned long long*)shared_best);
-    return (((unsigned long long)lb << 32) | fkey) >= g;
-  }
-  __device__ __forceinline__ bool improves(int cost) const {
-    return (((unsigned long long)cost << 32) | fkey) < lane_best;
-  }
-  __device__ __forceinline__ void take(int cost) {
-    lane_best = ((unsigned long long)cost << 32) | fkey;
-    atomicMin(shared_best, lane_best);
-  }
 };
 
 // Relaxed Algorithm X with branch and bound (R4-R7) from the node
@@ -486,6 +475,20 @@ __device__ __forceinline__ int colour_of_mask(const unsigned long long* bestC, i
   return c;
 }
 
+// Adds a component's Eq. (1b)/(1c) counts to its layout (the whole warp calls;
+// nc, ns = per-lane sums over the vertices, each edge seen from both ends).
+// The recovery never adds a conflict (R9) and stitch vertices are
+// never hidden (R8), so these are the layout's final counts.
+__device__ __forceinline__ void add_counts(const GraphView& g, int v0, int nc, int ns, long long* counts) {
+  nc = __reduce_add_sync(0xffffffffu, nc) >> 1;
+  ns = __reduce_add_sync(0xffffffffu, ns) >> 1;
+  if ((threadIdx.x & 31) == 0 && (nc | ns)) {
+    const int l = layout_of(g, v0);
+    if (nc) atomicAdd((unsigned long long*)&counts[2 * l], (unsigned long long)nc);
+    if (ns) atomicAdd((unsigned long long*)&counts[2 * l + 1], (unsigned long long)ns);
+  }
+}
+
 // One warp per component seed: discovery, relabelling to the R5 column order
 // and the component's record in the pool (exactly one per component: the seed
 // that is its minimum).  Low register use, so 64 warps per SM discover at once.
@@ -565,7 +568,8 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
                                                                                            int w_stitch,
                                                                                            long long max_steps,
                                                                                            int* colors,
-                                                                                           unsigned light_steps) {
+                                                                                           unsigned light_steps,
+                                                                                           long long* counts) {
   __shared__ WarpSearch s_search[kCompWarps];
   WarpSearch& s = s_search[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -602,6 +606,15 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
     __syncwarp();
     for (int i = lane; i < n; i += 32) colors[__ldcg(&w.porder[off + i])] = colour_of_mask<K>(s.cl, i);
     trunc = __shfl_sync(0xffffffffu, trunc, 0);
+    if (counts && !(trunc && exact)) {  // final colouring: Eq. (1b)/(1c) counts of the component
+      int nc = 0, ns = 0;
+      for (int i = lane; i < n; i += 32) {
+        const unsigned long long Ci = s.cl[colour_of_mask<K>(s.cl, i)];
+        nc += __popcll(s.adj[i] & Ci);
+        ns += __popcll(s.sadj[i] & ~Ci);
+      }
+      add_counts(g, __ldcg(&w.porder[off]), nc, ns, counts);
+    }
     if (lane == 0) {
       if (trunc && exact) {  // hand the component to the CTA-parallel search
         const int h = atomicAdd(&ctl->n_heavy, 1);
@@ -631,30 +644,63 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
 }
 
 // ----------------------------------------------------------------------------
-// Exact mode: CTA-parallel search of one heavy component (kHeavyThreads lanes,
-// one warp per SM sub-partition, one shared incumbent).
+// Exact mode: warp-parallel search of one heavy component with work donation.
 //
-// Split nodes are stored as their path from the root — the colour chosen at
-// each level, 2 bits per level, depth in the top bits of a 64-bit word — and
-// a lane rebuilds a node's state by replaying the path with the column rule
-// of R5 (a few mask operations per level), so the level buffers cost 8 bytes
-// per node.
+// The result of R7 is the first minimum-cost leaf in the canonical (DFS) order.
+// Every leaf sits at depth n and the DFS visits leaves in lexicographic order
+// of their colour-choice sequences, so the result is the leaf with the minimum
+// key (cost, path), path = the choices, 2 bits per level, level 0 most
+// significant — whatever order the tree is explored in.  A node with lower
+// bound lb and path prefix p can only hold leaves with keys >= (lb, p·00…0),
+// so it is pruned iff that key >= the best key found: a leaf that beats the
+// incumbent is never cut.
+//
+// The 32 lanes of a warp run independent DFSs over disjoint parts of the tree.
+// Lane 0 starts at the root; at the top of every iteration each idle lane takes
+// one node from a busy lane: the donor gives away the LAST untried child of its
+// shallowest frame that still has one (shrinking that frame's child limit), as
+// a path, and the thief rebuilds the node's state by replaying the path with
+// the column rule of R5.  The best key is shared through warp shuffles whenever
+// a lane finds a better leaf.  The light phase's best leaf (cost c1, found in
+// the first light_steps nodes) is the starting incumbent: its path is rebuilt
+// from the colours the light kernel wrote.
+#ifndef MPLD_DONATE_MIN_LEVELS
+#define MPLD_DONATE_MIN_LEVELS 0
+#endif
+constexpr int kDonateMinLevels = MPLD_DONATE_MIN_LEVELS;  // a frame is donated from only if n - depth >= this
+#ifndef MPLD_STEAL_MIN_IDLE
+#define MPLD_STEAL_MIN_IDLE 1
+#endif
+constexpr int kStealMinIdle = MPLD_STEAL_MIN_IDLE;  // donation rounds only when at least this many lanes are idle
 
-#ifndef MPLD_HEAVY_THREADS
-#define MPLD_HEAVY_THREADS 128
-#endif
-#ifndef MPLD_HEAVY_MULT
-#define MPLD_HEAVY_MULT 1
-#endif
-constexpr int kHeavyThreads = MPLD_HEAVY_THREADS;
-constexpr int kHeavyTargetNodes = MPLD_HEAVY_MULT * kHeavyThreads;  // subtrees wanted
-constexpr int kHeavyCapNodes = 2 * kHeavyTargetNodes;  // level buffer capacity
-#ifndef MPLD_HEAVY_STACK_KB
-#define MPLD_HEAVY_STACK_KB 32
-#endif
-constexpr int kHeavyStackBytes = MPLD_HEAVY_STACK_KB * 1024;  // DFS stacks of the lanes (n frames each)
-constexpr int kPathDepthShift = 58;
-constexpr int kPathMaxDepth = 29;                      // 2 bits per level below the depth field
+struct Path {  // levels 0..31 in a, 32..63 in b; 2 bits per level, level 0 most significant
+  unsigned long long a, b;
+};
+
+// kTwo: 64-level paths (components of more than 32 vertices); else only word a is used
+template <bool kTwo = true>
+__device__ __forceinline__ void path_put(Path& P, int d, int c) {
+  const int sh = 62 - 2 * (d & 31);
+  if (!kTwo || d < 32)
+    P.a = (P.a & ~(3ull << sh)) | ((unsigned long long)c << sh);
+  else
+    P.b = (P.b & ~(3ull << sh)) | ((unsigned long long)c << sh);
+}
+
+template <bool kTwo = true>
+__device__ __forceinline__ Path path_prefix(const Path& P, int j) {  // levels < j kept, the rest zero
+  Path r;
+  r.a = j <= 0 ? 0ull : (j >= 32 ? P.a : (P.a & (~0ull << (64 - 2 * j))));
+  r.b = !kTwo || j <= 32 ? 0ull : (j >= 64 ? P.b : (P.b & (~0ull << (64 - 2 * (j - 32)))));
+  return r;
+}
+
+template <bool kTwo = true>
+__device__ __forceinline__ bool key_less(int c1, const Path& p1, int c2, const Path& p2) {
+  if (c1 != c2) return c1 < c2;
+  if (!kTwo || p1.a != p2.a) return p1.a < p2.a;
+  return p1.b < p2.b;
+}
 
 template <int K, typename W>
 struct State {
@@ -684,243 +730,405 @@ __device__ __forceinline__ void apply_row(State<K, W>& s, int v, int c, const W*
   s.mu = max(s.mu, c);
 }
 
+// warp-wide minimum of the lanes' keys (cost, path); returns the lane holding it
+template <bool kTwo>
+__device__ __forceinline__ int warp_min_key(int& c, Path& p) {
+  const int lane = threadIdx.x & 31;
+  int src = lane;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+    Path op;
+    op.a = __shfl_xor_sync(0xffffffffu, p.a, o);
+    op.b = kTwo ? __shfl_xor_sync(0xffffffffu, p.b, o) : 0ull;
+    const int os = __shfl_xor_sync(0xffffffffu, src, o);
+    if (key_less<kTwo>(oc, op, c, p) || (!key_less<kTwo>(c, p, oc, op) && os < src)) {
+      c = oc;
+      p = op;
+      src = os;
+    }
+  }
+  return src;
+}
+
+// Frames of the lanes in shared memory, [field][depth][lane] (a lane only
+// touches its own column: conflict-free).  A frame is the node N_d at which
+// column v_d was selected: its masks B and U (so a frame can be handed to
+// another lane without replaying its path), its cost, and v | (c+1) << 8 |
+// (maxused+1) << 16 | lim << 24 (current child c, child limit lim of R6).
+template <int K, typename W, int D>
+struct LaneFrames {
+  W B[K][D][32];
+  W U[D][32];
+  int cost[D][32];
+  int pk[D][32];
+};
+
 template <int K, typename W>
-__device__ __forceinline__ State<K, W> replay(unsigned long long path, int n, const W* adj, const W* sadj,
-                                              int w_stitch) {
+__host__ __device__ constexpr int heavy_depth() {
+  return sizeof(W) == 4 ? 32 : 64;
+}
+
+template <int K, typename W>
+__host__ __device__ constexpr size_t heavy_smem() {
+  return 3 * kMaxComp * sizeof(W) + sizeof(LaneFrames<K, W, heavy_depth<K, W>()>);
+}
+
+template <int K, typename W>
+__device__ void warp_heavy_search(int n, const W* __restrict__ adj, const W* __restrict__ sadj, const W* cl,
+                                  int ncl, LaneFrames<K, W, heavy_depth<K, W>()>& F, int w_stitch, int c1,
+                                  const Path& p1, const int* porder, int* colors, Control* ctl, W (&fin)[K],
+                                  unsigned& iters, unsigned& steal_rounds) {
+  using O = WordOps<W>;
+  constexpr bool kTwo = sizeof(W) == 8;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long donatable = (n - kDonateMinLevels) >= 64 ? ~0ull
+                                       : (n - kDonateMinLevels <= 0 ? 0ull : ((1ull << (n - kDonateMinLevels)) - 1ull));
+  iters = steal_rounds = 0;
+  // lane DFS state: the node (C, B, U, cost, maxused) and its path P; frames
+  // d0..depth-1, the deepest in registers; open bit d = frame d has an untried
+  // child beyond its current one
+  W C[K], B[K], U = O::full(n);
+#pragma unroll
+  for (int c = 0; c < K; ++c) C[c] = B[c] = 0;
+  int cost = 0, maxused = -1, depth = 0, d0 = 0;
+  bool active = lane == 0, enter = lane == 0;
+  W fB[K], fU = 0, f_adj = 0, f_sadj = 0;
+#pragma unroll
+  for (int c = 0; c < K; ++c) fB[c] = 0;
+  int f_cost = 0, f_v = 0, f_c = -1, f_mu = -1, f_lim = 0;
+  Path P = {0ull, 0ull};
+  unsigned long long open = 0ull;
+  // incumbent: the warp's best key (identical in every lane); a lane records a
+  // leaf only if it beats it, so only the lane that found the current best
+  // holds colours for it
+  int gcost = c1;
+  Path gP = p1;
+  bool mine = false;
+  W bestC[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) bestC[c] = 0;
+  unsigned steps = 0;
+  bool capped = false;
+  while (true) {
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (act == 0u) break;
+    ++iters;
+    if (__popc(~act) >= kStealMinIdle) {  // work donation: the i-th idle lane takes a node from the i-th donor
+      const unsigned don = __ballot_sync(0xffffffffu, active && (open & donatable) != 0ull);
+      if (don) {
+        ++steal_rounds;
+        const unsigned idle = ~act;
+        const int np = min(__popc(don), __popc(idle));
+        const unsigned lt = lanemask_lt();
+        // donor: the last untried child of its shallowest open frame j, built
+        // from the frame's masks (C at N_j = C & ~U_j)
+        W xC[K], xB[K], xU = 0;
+        int xcost = 0, xmu = 0, xd = 0;
+        Path xP = {0ull, 0ull};
+        if (((don >> lane) & 1u) && __popc(don & lt) < np) {
+          const int j = __ffsll((long long)(open & donatable)) - 1;
+          int pk, jc;
+          W jU;
+          if (j == depth - 1) {
+#pragma unroll
+            for (int c = 0; c < K; ++c) xB[c] = fB[c];
+            jU = fU;
+            jc = f_cost;
+            pk = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
+            f_lim -= 1;
+          } else {
+#pragma unroll
+            for (int c = 0; c < K; ++c) xB[c] = F.B[c][j][lane];
+            jU = F.U[j][lane];
+            jc = F.cost[j][lane];
+            pk = F.pk[j][lane];
+            F.pk[j][lane] = pk - (1 << 24);
+          }
+          const int v = pk & 0xff, cj = ((pk >> 8) & 0xff) - 1, mu = ((pk >> 16) & 0xff) - 1, lim = pk >> 24;
+          if (cj >= lim - 1) open &= ~(1ull << j);
+          const W bit = W(1) << v;
+          const W a = adj[v], sa = sadj[v];
+          xU = jU & ~bit;
+#pragma unroll
+          for (int c = 0; c < K; ++c) xC[c] = C[c] & ~jU;
+          const W Cc = pick<K, W>(xC, lim);
+          xcost = jc + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~xU & ~Cc);
+          put<K, W>(xC, lim, Cc | bit);
+          put<K, W>(xB, lim, pick<K, W>(xB, lim) | a);
+          xmu = max(mu, lim);
+          xP = path_prefix<kTwo>(P, j);
+          path_put<kTwo>(xP, j, lim);
+          xd = j + 1;
+        }
+        const bool take = !active && __popc(idle & lt) < np;
+        int src = lane;
+        if (take) {  // the donor of the same rank
+          unsigned m = don;
+          for (int r = __popc(idle & lt); r > 0; --r) m &= m - 1;
+          src = __ffs(m) - 1;
+        }
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          xC[c] = __shfl_sync(0xffffffffu, xC[c], src);
+          xB[c] = __shfl_sync(0xffffffffu, xB[c], src);
+        }
+        xU = __shfl_sync(0xffffffffu, xU, src);
+        xcost = __shfl_sync(0xffffffffu, xcost, src);
+        xmu = __shfl_sync(0xffffffffu, xmu, src);
+        xd = __shfl_sync(0xffffffffu, xd, src);
+        xP.a = __shfl_sync(0xffffffffu, xP.a, src);
+        if (kTwo) xP.b = __shfl_sync(0xffffffffu, xP.b, src);
+        if (take) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            C[c] = xC[c];
+            B[c] = xB[c];
+          }
+          U = xU;
+          cost = xcost;
+          maxused = xmu;
+          P = xP;
+          depth = d0 = xd;
+          open = 0ull;
+          active = enter = true;
+        }
+      }
+    }
+    // One DFS event per lane, written branch-free (both outcomes computed,
+    // committed with selects) so that lanes in different states do not
+    // serialise: enter the pending node (leaf / prune / expand), then advance
+    // the deepest frame (next child / exhausted: pop).
+    bool found = false;
+    const bool en = active && enter;
+    if (en && ++steps > kHeavyLaneCap) {  // exact-mode safety cap: drop this lane's work, flag the component
+      capped = true;
+      active = false;
+    }
+    {
+      W Z, Ol;
+      live_counts<K, W>(B, U, Z, Ol);
+      const int lb = cost + kCostUnits * bound_conflicts<K, W, (heavy_clique_min<K>() > 0)>(B, U, Z, cl, 1, ncl);
+      const bool leaf = U == 0;
+      const bool better = active && en && leaf && key_less<kTwo>(cost, P, gcost, gP);  // Alg. 1 line 5
+      const bool ex = active && en && !leaf && key_less<kTwo>(lb, P, gcost, gP);      // bound (R7)
+      if (better) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) bestC[c] = C[c];
+        gcost = cost;  // provisional; the warp minimum below settles it
+        gP = P;
+        found = true;
+      }
+      const int v = ex ? O::ffs(Z ? Z : (Ol ? Ol : U)) : 0;  // Alg. 1 line 8 (R5)
+      if (ex && depth > d0) {  // spill the parent frame
+        const int d = depth - 1;
+#pragma unroll
+        for (int c = 0; c < K; ++c) F.B[c][d][lane] = fB[c];
+        F.U[d][lane] = fU;
+        F.cost[d][lane] = f_cost;
+        F.pk[d][lane] = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
+      }
+      const W av = adj[v], sav = sadj[v];
+#pragma unroll
+      for (int c = 0; c < K; ++c) fB[c] = ex ? B[c] : fB[c];
+      fU = ex ? U : fU;
+      f_cost = ex ? cost : f_cost;
+      f_v = ex ? v : f_v;
+      f_c = ex ? -1 : f_c;
+      f_mu = ex ? maxused : f_mu;
+      f_lim = ex ? min(K - 1, maxused + 1) : f_lim;  // colour-symmetry limit (R6)
+      f_adj = ex ? av : f_adj;
+      f_sadj = ex ? sav : f_sadj;
+      U = ex ? (U & ~(W(1) << v)) : U;  // cover column v (line 9)
+      depth += ex ? 1 : 0;
+    }
+    {
+      const bool adv = active && depth > d0;
+      if (active && depth == d0) active = false;
+      const W bit = W(1) << f_v;
+      const bool unc = adv && f_c >= 0;  // uncover the previous row (line 17)
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        const bool mine_c = unc && c == f_c;
+        C[c] = mine_c ? (C[c] & ~bit) : C[c];
+        B[c] = mine_c ? fB[c] : B[c];
+      }
+      const int c = f_c + 1;
+      const int fd = depth - 1;
+      const bool exh = adv && c > f_lim;  // rows exhausted (R6 limit)
+      const bool nxt = adv && !exh;
+      // next child: select r(v,c) (line 14), cover its secondary columns (line 15)
+      const int cc = min(c, K - 1);
+      const W Cc = pick<K, W>(C, cc);
+      const int ncost = f_cost + kCostUnits * O::popc(f_adj & Cc) + w_stitch * O::popc(f_sadj & ~U & ~Cc);
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const bool sel = nxt && q == cc;
+        C[q] = sel ? (C[q] | bit) : C[q];
+        B[q] = sel ? (B[q] | f_adj) : B[q];
+      }
+      cost = nxt ? ncost : cost;
+      maxused = nxt ? max(f_mu, c) : maxused;
+      if (adv) path_put<kTwo>(P, max(fd, 0), nxt ? c : 0);
+      const unsigned long long fbit = 1ull << max(fd, 0);
+      open = (nxt && c < f_lim) ? (open | fbit) : (adv ? (open & ~fbit) : open);
+      // exhausted: uncover the column (line 20) and pop the parent frame
+      U = exh ? (U | bit) : U;
+      const bool pop = exh && fd > d0;
+      const int pd = max(fd - 1, 0);
+      W pB[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) pB[q] = F.B[q][pd][lane];
+      const W pU = F.U[pd][lane];
+      const int pc = F.cost[pd][lane], ppk = F.pk[pd][lane];
+      const int pv = pop ? (ppk & 0xff) : f_v;
+      const W pa = adj[pv], psa = sadj[pv];
+#pragma unroll
+      for (int q = 0; q < K; ++q) fB[q] = pop ? pB[q] : fB[q];
+      fU = pop ? pU : fU;
+      f_cost = pop ? pc : f_cost;
+      f_v = pv;
+      f_c = pop ? ((ppk >> 8) & 0xff) - 1 : (nxt ? c : f_c);
+      f_mu = pop ? ((ppk >> 16) & 0xff) - 1 : f_mu;
+      f_lim = pop ? (ppk >> 24) : f_lim;
+      f_adj = pop ? pa : f_adj;
+      f_sadj = pop ? psa : f_sadj;
+      depth = exh ? fd : depth;
+      if (exh && fd <= d0) active = false;
+      enter = nxt;
+    }
+    if (__ballot_sync(0xffffffffu, found)) {  // settle the best key: the minimum over the lanes
+      // the non-finding lanes hold the previous best, so a finding lane wins
+      mine = warp_min_key<kTwo>(gcost, gP) == lane;
+    }
+  }
+  unsigned tot = steps;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  const bool any_capped = __any_sync(0xffffffffu, capped);
+  // the best key beats the light phase's leaf iff some lane recorded a leaf;
+  // the lane that recorded the final best writes the colours
+  const unsigned owner = __ballot_sync(0xffffffffu, mine);
+  if (owner && key_less<kTwo>(gcost, gP, c1, p1)) {
+    const int win = __ffs(owner) - 1;
+#pragma unroll
+    for (int c = 0; c < K; ++c) fin[c] = __shfl_sync(0xffffffffu, bestC[c], win);
+    for (int i = lane; i < n; i += 32) colors[__ldcg(&porder[i])] = colour_of<K, W>(fin, i);
+  }
+  if (lane == 0) {
+    if (any_capped) atomicAdd(&ctl->truncated, 1);
+    atomicAdd(&ctl->steps, (unsigned long long)tot);
+    atomicMax(&ctl->max_steps_comp, (int)min(tot, (unsigned)INT_MAX));
+  }
+}
+
+// the path of the leaf whose colours are col (a leaf of the canonical tree:
+// follow the column rule and take each selected column's colour)
+template <int K, typename W>
+__device__ __forceinline__ Path leaf_path(const W (&col)[K], int n, const W* adj, const W* sadj, int w_stitch,
+                                          int& cost) {
   State<K, W> s;
 #pragma unroll
   for (int c = 0; c < K; ++c) s.C[c] = s.B[c] = 0;
   s.U = WordOps<W>::full(n);
   s.cost = 0;
   s.mu = -1;
-  const int depth = (int)(path >> kPathDepthShift);
-  for (int d = 0; d < depth; ++d) apply_row<K, W>(s, select_column<K, W>(s), (int)((path >> (2 * d)) & 3ull), adj, sadj, w_stitch);
-  return s;
-}
-
-// children of a split node: 0 = pruned against the light-phase incumbent c1
-// (its leaf precedes every subtree), 1 for a leaf (carried as itself), else
-// min(K, mu + 2) (R4 with the colour-symmetry limit R6)
-template <int K, typename W>
-__device__ __forceinline__ int split_children(const State<K, W>& s, const W* cl, int ncl, int c1) {
-  if (s.U == 0) return 1;
-  W Z, Ol;
-  live_counts<K, W>(s.B, s.U, Z, Ol);
-  if (s.cost + kCostUnits * bound_conflicts<K, W>(s.B, s.U, Z, cl, 1, ncl) >= c1) return 0;
-  return min(K - 1, s.mu + 1) + 1;
-}
-
-__device__ __forceinline__ int block_excl_scan(int x, int& total, int* s_tmp) {  // s_tmp: 32 ints
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int y = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int z = __shfl_up_sync(0xffffffffu, y, o);
-    if (lane >= o) y += z;
+  Path P = {0ull, 0ull};
+  for (int d = 0; d < n; ++d) {
+    const int v = select_column<K, W>(s);
+    const int c = colour_of<K, W>(col, v);
+    apply_row<K, W>(s, v, c, adj, sadj, w_stitch);
+    path_put(P, d, c);
   }
-  if (lane == 31) s_tmp[wid] = y;
-  __syncthreads();
-  int base = 0;
-  total = 0;
-  for (int i = 0; i < nw; ++i) {
-    const int t = s_tmp[i];
-    if (i < wid) base += t;
-    total += t;
-  }
-  __syncthreads();
-  return base + y - x;
+  cost = s.cost;
+  return P;
 }
 
 template <int K, typename W>
-__device__ void heavy_component(int n, const int* s_order, const unsigned long long* s_adj64,
-                                const unsigned long long* s_sadj64, unsigned char* smem, int w_stitch, int c1,
-                                int* colors, Control* ctl) {
-  const int tid = threadIdx.x;
+__device__ unsigned long long heavy_component(const GraphView& g, int n, size_t off, const Workspace& w,
+                                              unsigned char* smem, int w_stitch, int c1, int* colors,
+                                              long long* counts) {
+  const int lane = threadIdx.x & 31;
   W* s_adj = (W*)smem;
   W* s_sadj = s_adj + kMaxComp;
   W* s_cl = s_sadj + kMaxComp;
-  unsigned long long* lvl[2];
-  lvl[0] = (unsigned long long*)(smem + 3 * kMaxComp * sizeof(unsigned long long));
-  lvl[1] = lvl[0] + kHeavyCapNodes;
-  Frame<W>* stack_base = (Frame<W>*)(lvl[1] + kHeavyCapNodes);
-  __shared__ unsigned long long s_best;
-  __shared__ unsigned long long s_win;
-  __shared__ int s_next, s_ncl, s_flag, s_tmp[32];
-  __shared__ unsigned long long s_red[32];
-  for (int i = tid; i < n; i += blockDim.x) {
-    s_adj[i] = (W)s_adj64[i];
-    s_sadj[i] = (W)s_sadj64[i];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    s_ncl = clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, clique_min<K>()) : 0;
-    lvl[0][0] = 0ull;  // the root: depth 0
-    s_best = (unsigned long long)c1 << 32;  // the light-phase leaf precedes every subtree (key f+1 = 0)
-    s_next = 0;
-  }
-  __syncthreads();
-  const int ncl = s_ncl;
-  const long long hc0 = clock64();
-  // level-synchronous split of the canonical tree, DFS order preserved
-  int m = 1, cur = 0;
-  unsigned expanded = 0;
-#ifdef MPLD_HEAVY_DIAG_SEQ
-  while (false) {
-#else
-  while (m < kHeavyTargetNodes) {
-#endif
-    int total = 0;
-    if (tid == 0) s_flag = 0;  // bit 0: some node still has uncovered columns; bit 1: depth limit reached
-    __syncthreads();
-    for (int i0 = 0; i0 < m; i0 += blockDim.x) {
-      const int i = i0 + tid;
-      unsigned long long path = 0ull;
-      int cnt = 0, depth = 0;
-      State<K, W> st;
-      if (i < m) {
-        path = lvl[cur][i];
-        depth = (int)(path >> kPathDepthShift);
-        st = replay<K, W>(path, n, s_adj, s_sadj, w_stitch);
-        cnt = split_children<K, W>(st, s_cl, ncl, c1);
-        if (st.U != 0 && cnt > 0) atomicOr(&s_flag, depth + 1 >= kPathMaxDepth ? 3 : 1);
-      }
-      int t;
-      const int off = block_excl_scan(cnt, t, s_tmp);
-      if (total + t <= kHeavyCapNodes && cnt > 0) {
-        unsigned long long* out = &lvl[cur ^ 1][total + off];
-        if (st.U == 0) {
-          out[0] = path;
-        } else {
-          const unsigned long long base = (path & ((1ull << kPathDepthShift) - 1)) |
-                                          ((unsigned long long)(depth + 1) << kPathDepthShift);
-          for (int c = 0; c < cnt; ++c) out[c] = base | ((unsigned long long)c << (2 * depth));
-        }
-      }
-      total += t;
-    }
-    __syncthreads();
-    const int flag = s_flag;
-    if (total == 0) {
-      m = 0;
-      break;
-    }
-    if (total > kHeavyCapNodes || !(flag & 1) || (flag & 2)) break;
-    expanded += m;
-    cur ^= 1;
-    m = total;
-  }
-  const long long hc1 = clock64();
-  // lanes search the subtrees in DFS order with a shared incumbent; the stack
-  // region holds n frames per active lane
-#ifdef MPLD_HEAVY_DIAG_SEQ
-  const int lanes = 1;
-#else
-  const int lanes = min((int)blockDim.x, (int)(kHeavyStackBytes / (n * (int)sizeof(Frame<W>))));
-#endif
-  W bestC[K];
+  auto& F = *(LaneFrames<K, W, heavy_depth<K, W>()>*)(smem + 3 * kMaxComp * sizeof(W));
+  const int* porder = w.porder + off;
+  W col[K];
 #pragma unroll
-  for (int c = 0; c < K; ++c) bestC[c] = 0;
-  unsigned long long my_best = ~0ull;
-  unsigned steps = 0;
-  bool capped = false;
-  if (tid < lanes) {
-    while (true) {
-      const int f = atomicAdd(&s_next, 1);
-      if (f >= m) break;
-      if (steps >= kHeavyLaneCap) {  // safety cap of exact mode: skip, flag as truncated
-        capped = true;
-        continue;
-      }
-      State<K, W> st = replay<K, W>(lvl[cur][f], n, s_adj, s_sadj, w_stitch);
-      ParIncumbent inc;
-      inc.shared_best = &s_best;
-      inc.fkey = (unsigned long long)(f + 1);
-      inc.lane_best = my_best;
-      bool trunc;
-      steps += dfs<K, W, ParIncumbent>(s_adj, s_sadj, 1, st.C, st.B, st.U, st.cost, st.mu, w_stitch,
-                                       kHeavyLaneCap - steps, stack_base + tid, lanes, s_cl, 1, ncl, inc, bestC,
-                                       trunc);
-      my_best = inc.lane_best;
-      capped |= trunc;
+  for (int c = 0; c < K; ++c) col[c] = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    int ci = -1;
+    if (i < n) {
+      const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
+      s_adj[i] = (W)m.x;
+      s_sadj[i] = (W)m.y;
+      ci = __ldcg(&colors[__ldcg(&porder[i])]);  // the light phase's best leaf
     }
-  }
-  // the minimum key over lanes is the canonical leaf
-  const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  unsigned long long wmin = my_best;
-  unsigned total_steps = steps;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long y = __shfl_xor_sync(0xffffffffu, wmin, o);
-    wmin = y < wmin ? y : wmin;
-    total_steps += __shfl_xor_sync(0xffffffffu, total_steps, o);
-  }
-  const int any_capped = __syncthreads_or(capped);
-#ifdef MPLD_DIAG_LANESTEPS
-  __shared__ unsigned s_maxsteps;
-  if (tid == 0) s_maxsteps = 0;
-  __syncthreads();
-  atomicMax(&s_maxsteps, steps);
-  __syncthreads();
-#endif
-  if (lane == 0) {
-    s_red[wid] = wmin;
-    s_tmp[wid] = (int)total_steps;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long w = ~0ull;
-    unsigned ts = 0;
-    for (int i = 0; i < nw; ++i) {
-      w = s_red[i] < w ? s_red[i] : w;
-      ts += (unsigned)s_tmp[i];
-    }
-    s_win = w;
-    if (any_capped) atomicAdd(&ctl->truncated, 1);
-    atomicAdd(&ctl->steps, (unsigned long long)(ts + expanded));
-    atomicMax(&ctl->max_steps_comp, (int)min(ts + expanded, (unsigned)INT_MAX));
-    const long long hc2 = clock64();
-    if ((unsigned long long)(hc2 - hc0) > ctl->dbg[5]) {  // diagnostics (racy by design)
-      atomicMax(&ctl->dbg[5], (unsigned long long)(hc2 - hc0));
-#ifdef MPLD_DIAG_LANESTEPS
-      ctl->dbg[6] = ((unsigned long long)s_maxsteps << 32) | (unsigned)(ts + expanded);
-#else
-      ctl->dbg[6] = hc1 - hc0;
-#endif
-      ctl->dbg[7] = ((unsigned long long)m << 32) | (unsigned)n;
+    for (int c = 0; c < K; ++c) {
+      const unsigned b = __ballot_sync(0xffffffffu, ci == c);
+      col[c] |= (W)b << i0;
     }
   }
-  __syncthreads();
-  const unsigned long long win = s_win;
-  if (win != ~0ull && my_best == win && win < ((unsigned long long)c1 << 32)) {  // keys are unique per subtree
-    for (int i = 0; i < n; ++i) colors[s_order[i]] = colour_of<K, W>(bestC, i);
+  __syncwarp();
+  const int ncl = heavy_clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, heavy_clique_min<K>()) : 0;
+  __syncwarp();
+  int lc = 0;  // == c1 (the light phase's best cost)
+  const Path p1 = leaf_path<K, W>(col, n, s_adj, s_sadj, w_stitch, lc);
+  unsigned iters, steals;
+  W fin[K];  // the final colouring: the light leaf unless the search beats it
+#pragma unroll
+  for (int c = 0; c < K; ++c) fin[c] = col[c];
+  warp_heavy_search<K, W>(n, s_adj, s_sadj, s_cl, ncl, F, w_stitch, c1, p1, porder, colors, w.ctl, fin, iters,
+                          steals);
+  if (counts) {
+    int nc = 0, ns = 0;
+    for (int i = lane; i < n; i += 32) {
+      const W Ci = pick<K, W>(fin, colour_of<K, W>(fin, i));
+      nc += WordOps<W>::popc(s_adj[i] & Ci);
+      ns += WordOps<W>::popc(s_sadj[i] & ~Ci);
+    }
+    add_counts(g, __ldcg(&porder[0]), nc, ns, counts);
   }
+  __syncwarp();
+  return (unsigned long long)iters << 32 | steals;
 }
 
-template <int K>
-__global__ void __launch_bounds__(kHeavyThreads) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
-                                                                               int* colors) {
+// One warp per heavy component of one word class: W = 32-bit words for
+// components of <= 32 vertices, 64-bit words for larger ones (the frames of
+// the 64-bit class are twice as deep and wide, so each class gets its own
+// launch with its own shared-memory size).
+template <int K, typename W>
+__global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
+                                                                    int* colors, long long* counts) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int s_order[kMaxComp];
-  __shared__ unsigned long long s_adj64[kMaxComp], s_sadj64[kMaxComp];
+  constexpr int cls = sizeof(W) == 4 ? 0 : 1;
   Control* ctl = w.ctl;
   const int n_heavy = __ldcg(&ctl->n_heavy);
-  for (int h = blockIdx.x; h < n_heavy; h += gridDim.x) {
-    const int c1 = __ldcg(&w.hcost[h]);
+  const long long t0 = clock64();
+  while (true) {
+    int h = 0;
+    if (threadIdx.x == 0) h = atomicAdd(&ctl->heavy_next[cls], 1);  // dynamic schedule over the heavy list
+    h = __shfl_sync(0xffffffffu, h, 0);
+    if (h >= n_heavy) break;
     const unsigned long long rec = __ldcg(&w.crec[__ldcg(&w.hcomp[h])]);
-    const size_t off = (size_t)(rec >> 8);
     const int n = (int)(rec & 0xffull);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      s_order[i] = __ldcg(&w.porder[off + i]);
-      s_adj64[i] = __ldcg(&w.pmask[2 * (off + i)]);
-      s_sadj64[i] = __ldcg(&w.pmask[2 * (off + i) + 1]);
+    if ((n > 32) != (cls == 1)) continue;  // the other class's launch takes it
+    const int c1 = __ldcg(&w.hcost[h]);
+    const size_t off = (size_t)(rec >> 8);
+    const long long c0 = clock64();
+    const unsigned long long is = heavy_component<K, W>(g, n, off, w, smem, w_stitch, c1, colors, counts);
+    if (threadIdx.x == 0) {  // diagnostics (racy by design): slowest component, its size, iterations, steal rounds
+      const unsigned long long cyc = (unsigned long long)(clock64() - c0);
+      if (cyc > ctl->dbg[5]) {
+        atomicMax(&ctl->dbg[5], cyc);
+        ctl->dbg[7] = (unsigned long long)n | ((is >> 32) << 8) | ((is & 0xffffffull) << 40);
+      }
     }
-    __syncthreads();
-    if (n <= 32)
-      heavy_component<K, unsigned>(n, s_order, s_adj64, s_sadj64, smem, w_stitch, c1, colors, ctl);
-    else
-      heavy_component<K, unsigned long long>(n, s_order, s_adj64, s_sadj64, smem, w_stitch, c1, colors, ctl);
-    __syncthreads();
   }
+  if (threadIdx.x == 0) atomicMax(&ctl->dbg[6], (unsigned long long)(clock64() - t0));  // slowest warp overall
 }
 
 }  // namespace
@@ -932,54 +1140,67 @@ cudaError_t launch_discover(const GraphView& g, Workspace ws, int shard_index, i
 }
 
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
-                          unsigned light_steps, cudaStream_t s, int blocks) {
+                          unsigned light_steps, long long* counts, cudaStream_t s, int blocks) {
   switch (k) {
     case 2:
-      mpld_exact_cover_search<2><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps);
+      mpld_exact_cover_search<2><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
+                                                                     counts);
       break;
     case 3:
-      mpld_exact_cover_search<3><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps);
+      mpld_exact_cover_search<3><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
+                                                                     counts);
       break;
     case 4:
-      mpld_exact_cover_search<4><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps);
+      mpld_exact_cover_search<4><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
+                                                                     counts);
       break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
-size_t heavy_smem_bytes() {
-  return 3 * kMaxComp * sizeof(unsigned long long) + 2 * kHeavyCapNodes * sizeof(unsigned long long) +
-         kHeavyStackBytes;
-}
-
-cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
-                                int blocks) {
-  const size_t smem = heavy_smem_bytes();
-  switch (k) {
-    case 2: mpld_exact_cover_search_heavy<2><<<blocks, kHeavyThreads, smem, s>>>(g, ws, w_stitch, colors); break;
-    case 3: mpld_exact_cover_search_heavy<3><<<blocks, kHeavyThreads, smem, s>>>(g, ws, w_stitch, colors); break;
-    case 4: mpld_exact_cover_search_heavy<4><<<blocks, kHeavyThreads, smem, s>>>(g, ws, w_stitch, colors); break;
-    default: return cudaErrorInvalidValue;
-  }
+template <int K>
+cudaError_t launch_heavy_k(const GraphView& g, Workspace ws, int w_stitch, int* colors, long long* counts,
+                           cudaStream_t s, const int* blocks) {
+  mpld_exact_cover_search_heavy<K, unsigned>
+      <<<blocks[0], 32, heavy_smem<K, unsigned>(), s>>>(g, ws, w_stitch, colors, counts);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  mpld_exact_cover_search_heavy<K, unsigned long long>
+      <<<blocks[1], 32, heavy_smem<K, unsigned long long>(), s>>>(g, ws, w_stitch, colors, counts);
   return cudaGetLastError();
 }
 
-int resident_blocks_heavy(int num_sms) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search_heavy<4>, kHeavyThreads,
-                                                heavy_smem_bytes());
-  return per_sm * num_sms;
+cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, long long* counts,
+                                cudaStream_t s, const int* blocks) {
+  switch (k) {
+    case 2: return launch_heavy_k<2>(g, ws, w_stitch, colors, counts, s, blocks + 0);
+    case 3: return launch_heavy_k<3>(g, ws, w_stitch, colors, counts, s, blocks + 2);
+    case 4: return launch_heavy_k<4>(g, ws, w_stitch, colors, counts, s, blocks + 4);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
-cudaError_t configure_search_heavy() {
-  const int smem = (int)heavy_smem_bytes();
-  cudaError_t e = cudaSuccess;
-  e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+template <int K, typename W>
+cudaError_t configure_heavy_kw(int num_sms, int* blocks) {
+  const cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<K, W>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem<K, W>());
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search_heavy<K, W>, 32, heavy_smem<K, W>());
+  *blocks = per_sm * num_sms;
+  return cudaSuccess;
+}
+
+// sets the shared-memory limits of the six heavy kernels and their resident grid sizes
+// blocks[2 * (k - 2) + cls]
+cudaError_t configure_search_heavy(int num_sms, int* blocks) {
+  cudaError_t e = configure_heavy_kw<2, unsigned>(num_sms, blocks + 0);
+  if (e == cudaSuccess) e = configure_heavy_kw<2, unsigned long long>(num_sms, blocks + 1);
+  if (e == cudaSuccess) e = configure_heavy_kw<3, unsigned>(num_sms, blocks + 2);
+  if (e == cudaSuccess) e = configure_heavy_kw<3, unsigned long long>(num_sms, blocks + 3);
+  if (e == cudaSuccess) e = configure_heavy_kw<4, unsigned>(num_sms, blocks + 4);
+  if (e == cudaSuccess) e = configure_heavy_kw<4, unsigned long long>(num_sms, blocks + 5);
   return e;
 }
 

@@ -14,7 +14,11 @@
 // read in batches of kNb independent loads, items are tiled kP per thread
 // (measured on B200: kP = 1, kNb = 4 and one 1024-thread CTA per SM are the
 // fastest; lockstep tiles of 2-3 items per thread lengthen every level).
+#include <cooperative_groups.h>
+
 #include "mpld_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mpld {
 
@@ -32,10 +36,16 @@ namespace {
 #ifndef MPLD_GRAPH_MINB
 #define MPLD_GRAPH_MINB 1
 #endif
-constexpr int kP = MPLD_GRAPH_P;    // items per thread and tile
+#ifndef MPLD_GRAPH_PF
+#define MPLD_GRAPH_PF 1
+#endif
+constexpr int kP = MPLD_GRAPH_P;    // items per thread and tile (frontier rounds, recovery levels)
+constexpr int kPF = MPLD_GRAPH_PF;  // items per thread and tile of the full passes over all vertices
 constexpr int kNb = MPLD_GRAPH_NB;  // neighbours per item and batch of independent memory operations
-constexpr int kAppend = 8;   // items one thread may append per tile before spilling to direct atomics
-constexpr int kTail = 1024;  // frontiers up to this size are finished by CTA 0 alone
+#ifndef MPLD_TAIL
+#define MPLD_TAIL 1024
+#endif
+constexpr int kTail = MPLD_TAIL;  // frontiers up to this size are finished by CTA 0 alone
 constexpr int kStitchDeg = 1 << 29;  // live degree of stitch vertices: never reaches k (never hidden, R8)
 
 __device__ __forceinline__ void stamp(Control* ctl, int i) {
@@ -87,43 +97,90 @@ struct LayoutCache {
   }
 };
 
-// Block-wide append: thread i contributes cnt_i items; the CTA reserves its
-// range with one atomicAdd.  Every thread of the CTA must call it (uniform
-// control flow); blockDim.x must be a multiple of 32.
-__device__ __forceinline__ void cta_append(int cnt, const int* items, int* counter, int* out) {
-  __shared__ int s_warp[32];
-  __shared__ int s_base;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int x = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_warp[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    const int t = lane < nw ? s_warp[lane] : 0;
-    int y = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int z = __shfl_up_sync(0xffffffffu, y, o);
-      if (lane >= o) y += z;
-    }
-    if (lane < nw) s_warp[lane] = y - t;  // exclusive prefix of the warp totals
-    if (lane == 31) s_base = y ? atomicAdd(counter, y) : 0;
-  }
-  __syncthreads();
-  const int pos = s_base + s_warp[wid] + x - cnt;
-  for (int i = 0; i < cnt; ++i) out[pos + i] = items[i];
+// CTA queues in shared memory: items are pushed with one shared atomic per
+// coalesced group of lanes (no CTA barrier inside a pass, so the warps of a CTA
+// progress independently through their tiles) and flushed once at the end of
+// the pass with one global atomic per CTA.  Items beyond kQCap go straight to
+// the global queue (warp-aggregated atomics).
+#ifndef MPLD_QCAP
+#define MPLD_QCAP 4096
+#endif
+constexpr int kQCap = MPLD_QCAP;
+struct CtaQueues {
+  int n[2], m[2], base[2];
+  int item[2][kQCap];
+};
+
+__device__ __forceinline__ void cq_init(CtaQueues& Q) {
+  if (threadIdx.x < 2) Q.n[threadIdx.x] = 0;
   __syncthreads();
 }
 
-// push into a per-thread append list, spilling to a direct atomic when full
-__device__ __forceinline__ void list_push(int* items, int& cnt, int v, int* counter, int* out) {
-  if (cnt < kAppend) items[cnt++] = v;
-  else out[atomicAdd(counter, 1)] = v;
+__device__ __forceinline__ void cq_push(CtaQueues& Q, int q, int v, int* gcnt, int* gout) {
+  const cg::coalesced_group grp = cg::coalesced_threads();
+  int base = 0;
+  if (grp.thread_rank() == 0) base = atomicAdd(&Q.n[q], (int)grp.size());
+  const int i = grp.shfl(base, 0) + (int)grp.thread_rank();
+  if (i < kQCap) {
+    Q.item[q][i] = v;
+  } else {  // overflow: direct global append
+    const cg::coalesced_group ov = cg::coalesced_threads();
+    int gb = 0;
+    if (ov.thread_rank() == 0) gb = atomicAdd(gcnt, (int)ov.size());
+    gout[ov.shfl(gb, 0) + (int)ov.thread_rank()] = v;
+  }
 }
+
+// Every thread of the CTA must call it (uniform control flow).
+__device__ __forceinline__ void cq_flush(CtaQueues& Q, int q, int* gcnt, int* gout) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int m = min(Q.n[q], kQCap);
+    Q.m[q] = m;
+    Q.base[q] = m ? atomicAdd(gcnt, m) : 0;
+    Q.n[q] = 0;
+  }
+  __syncthreads();
+  const int m = Q.m[q], b = Q.base[q];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) gout[b + i] = Q.item[q][i];
+  __syncthreads();
+}
+
+// Item i of a frontier whose first s_cnt items sit in shared memory (a CTA
+// queue of the single-CTA tail) and the rest in global memory.
+__device__ __forceinline__ int frontier_item(const int* s_in, int s_cnt, const int* g_in, int i) {
+  return i < s_cnt ? s_in[i] : __ldcg(&g_in[i - s_cnt]);
+}
+
+// The single-CTA tail of a level-synchronous loop (simplification rounds,
+// recovery levels): the frontier stays in the CTA's two shared queues (items
+// beyond kQCap spill to the global queue that is not being read), so a level
+// costs its dependent loads plus two block barriers.
+struct TailFrontier {
+  int in_slot = -1;  // shared slot holding the input's first items (-1: input all global)
+  int s_cnt = 0;
+  const int* g_in;
+  int out_slot = 0;
+  __device__ __forceinline__ const int* s_in(const CtaQueues& Q) const { return in_slot >= 0 ? Q.item[in_slot] : nullptr; }
+  __device__ __forceinline__ int* g_out(const Workspace& w) const { return g_in == w.q0 ? w.q1 : w.q0; }
+  // after the level: the output becomes the input; returns its size
+  __device__ __forceinline__ int advance(CtaQueues& Q, const Workspace& w) {
+    __syncthreads();
+    const int c = Q.n[out_slot];
+    __syncthreads();
+    if (threadIdx.x == 0 && in_slot >= 0) Q.n[in_slot] = 0;
+    g_in = g_out(w);
+    in_slot = out_slot;
+    s_cnt = min(c, kQCap);
+    out_slot ^= 1;
+    __syncthreads();
+    return c;
+  }
+  __device__ __forceinline__ void finish(CtaQueues& Q) {
+    if (threadIdx.x < 2) Q.n[threadIdx.x] = 0;
+    __syncthreads();
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Input validation (MPLD_FLAG_VALIDATE, include/mpld.h invariants), fused into
@@ -145,21 +202,21 @@ __device__ __forceinline__ unsigned long long pair_hash(int x, int y) {
 
 // One simplification round r >= 1: push the decrements of the frontier
 // cur[0..cnt), tiles of kP * blockDim items starting at first, step stride.
-// A neighbour enters round r+1 exactly when its live degree crosses k -> k-1
-// (stitch vertices start at kStitchDeg and never do).
+// A neighbour enters round r+1 exactly when its live degree crosses k -> k-1.
+// The decrement is unconditional (no load of the neighbour's round first):
+// hidden vertices already sit below k (round-0 vertices at 0, later rounds at
+// their degree when hidden) and stitch vertices at kStitchDeg, so only a live
+// vertex can cross k -> k-1.
+// The frontier is item i = frontier_item(s_in, s_cnt, g_in, i); hidden
+// neighbours are pushed into CTA queue slot qo (overflow: ocnt / oarr).
 __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r, int cnt, int first, int stride,
-                           int* qc) {
-  const int* cur = (r & 1) ? w.q1 : w.q0;
-  int* nxt = (r & 1) ? w.q0 : w.q1;
-  int* ncnt = &qc[(r + 1) % 3];
+                           const int* s_in, int s_cnt, const int* g_in, CtaQueues& Q, int qo, int* ocnt, int* oarr) {
   for (int t0 = first; t0 < cnt; t0 += stride) {
-    int items[kAppend];
-    int m = 0;
     int e[kP], e1[kP];
 #pragma unroll
     for (int j = 0; j < kP; ++j) {
       const int i = t0 + j * blockDim.x + threadIdx.x;
-      const int v = i < cnt ? __ldcg(&cur[i]) : -1;
+      const int v = i < cnt ? frontier_item(s_in, s_cnt, g_in, i) : -1;
       e[j] = v >= 0 ? __ldg(&g.ce_rp[v]) : 0;
       e1[j] = v >= 0 ? __ldg(&g.ce_rp[v + 1]) : 0;
     }
@@ -168,7 +225,7 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 #pragma unroll
       for (int j = 0; j < kP; ++j) open |= e[j] < e1[j];
       if (!open) break;
-      int u[kP][kNb], hu[kP][kNb], old[kP][kNb];
+      int u[kP][kNb], old[kP][kNb];
 #pragma unroll
       for (int j = 0; j < kP; ++j)
 #pragma unroll
@@ -176,25 +233,19 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 #pragma unroll
       for (int j = 0; j < kP; ++j)
 #pragma unroll
-        for (int t = 0; t < kNb; ++t) hu[j][t] = u[j][t] >= 0 ? __ldcg(&w.hround[u[j][t]]) : 0;
-#pragma unroll
-      for (int j = 0; j < kP; ++j)
-#pragma unroll
-        for (int t = 0; t < kNb; ++t)  // already-hidden neighbours' degrees no longer matter
-          old[j][t] = hu[j][t] == -1 ? atomicSub(&w.deg[u[j][t]], 1) : 0;
+        for (int t = 0; t < kNb; ++t) old[j][t] = u[j][t] >= 0 ? atomicSub(&w.deg[u[j][t]], 1) : 0;
 #pragma unroll
       for (int j = 0; j < kP; ++j) {
 #pragma unroll
         for (int t = 0; t < kNb; ++t) {
           if (old[j][t] == k) {
             w.hround[u[j][t]] = r + 1;
-            list_push(items, m, u[j][t], ncnt, nxt);
+            cq_push(Q, qo, u[j][t], ocnt, oarr);
           }
         }
         e[j] += kNb;
       }
     }
-    cta_append(m, items, ncnt, nxt);
   }
 }
 
@@ -212,10 +263,13 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_components(GraphView g, Workspace w, int k,
                                                                     int* colors, long long* counts, int validate) {
   GridBarrier grid(&w.ctl->bar[0]);
+  __shared__ CtaQueues Q;
+  cq_init(Q);
   stamp(w.ctl, 12);
   const int n = g.n;
   const int nth = gridDim.x * blockDim.x;
   const int tile0 = blockIdx.x * blockDim.x * kP, tstride = nth * kP;
+  const int tile0f = blockIdx.x * blockDim.x * kPF, tstridef = nth * kPF;
   Control* ctl = w.ctl;
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < 2 * g.n_layouts; l += nth) counts[l] = 0;
 
@@ -231,11 +285,11 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
       if (g.layout_off[l] > g.layout_off[l + 1]) bad = true;
   }
   LayoutCache lc;
-  for (int t0 = tile0; t0 < n; t0 += tstride) {
-    int v[kP], e[kP], e1[kP], d[kP], hr[kP], prev[kP];
-    bool need[kP], scan[kP];
+  for (int t0 = tile0f; t0 < n; t0 += tstridef) {
+    int v[kPF], e[kPF], e1[kPF], d[kPF], hr[kPF], prev[kPF];
+    bool need[kPF], scan[kPF];
 #pragma unroll
-    for (int j = 0; j < kP; ++j) {
+    for (int j = 0; j < kPF; ++j) {
       v[j] = t0 + j * blockDim.x + threadIdx.x;
       int a = 0, b = 0, sa = 0, sb = 0;
       if (v[j] < n) {
@@ -294,15 +348,15 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
     while (true) {
       bool open = false;
 #pragma unroll
-      for (int j = 0; j < kP; ++j) open |= scan[j] && e[j] < e1[j];
+      for (int j = 0; j < kPF; ++j) open |= scan[j] && e[j] < e1[j];
       if (!open) break;
-      int u[kP][kNb], r0[kP][kNb], r1[kP][kNb], s0[kP][kNb], s1[kP][kNb];
+      int u[kPF][kNb], r0[kPF][kNb], r1[kPF][kNb], s0[kPF][kNb], s1[kPF][kNb];
 #pragma unroll
-      for (int j = 0; j < kP; ++j)
+      for (int j = 0; j < kPF; ++j)
 #pragma unroll
         for (int t = 0; t < kNb; ++t) u[j][t] = scan[j] && e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
 #pragma unroll
-      for (int j = 0; j < kP; ++j)
+      for (int j = 0; j < kPF; ++j)
 #pragma unroll
         for (int t = 0; t < kNb; ++t) {
           const bool ok = need[j] && (unsigned)u[j][t] < (unsigned)n;  // invalid ids are flagged by the validation
@@ -312,7 +366,7 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
           s1[j][t] = ok ? __ldg(&g.se_rp[u[j][t] + 1]) : 0;
         }
 #pragma unroll
-      for (int j = 0; j < kP; ++j) {
+      for (int j = 0; j < kPF; ++j) {
 #pragma unroll
         for (int t = 0; t < kNb; ++t) {
           if (e[j] + t >= e1[j]) continue;
@@ -327,21 +381,21 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
         e[j] += kNb;
       }
     }
-    int items[kP];
-    int m = 0;
 #pragma unroll
-    for (int j = 0; j < kP; ++j) {
+    for (int j = 0; j < kPF; ++j) {
       if (need[j]) {
         w.deg[v[j]] = d[j];
         if (d[j] < k) {
           hr[j] = 1;
-          items[m++] = v[j];
+          cq_push(Q, 0, v[j], &ctl->qcnt[1], w.q1);
         }
+      } else if (hr[j] == 0) {
+        w.deg[v[j]] = 0;  // below k for good: later rounds decrement without checking (peel_round)
       }
       if (v[j] < n) w.hround[v[j]] = hr[j];
     }
-    cta_append(m, items, &ctl->qcnt[1], w.q1);
   }
+  cq_flush(Q, 0, &ctl->qcnt[1], w.q1);
   hidden0 = __reduce_add_sync(0xffffffffu, hidden0);
   if ((threadIdx.x & 31) == 0 && hidden0) atomicAdd(&ctl->n_hidden, hidden0);
   if (bad) atomicOr(&ctl->err, kErrGraph);
@@ -379,19 +433,22 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
       // dependent-load latency)
       if (blockIdx.x == 0) {
         int rr = r, c = cnt;
+        TailFrontier tf;
+        tf.g_in = (r & 1) ? w.q1 : w.q0;
         while (c > 0) {
-          // own counters: the other CTAs may still be reading qcnt[r % 3] to
-          // take this branch, so the tail must never reset that slot
+          // own overflow counter: the other CTAs may still be reading qcnt[r % 3] to take this branch
           if (threadIdx.x == 0) {
-            ctl->tcnt[(rr + 2) % 3] = 0;
+            ctl->tcnt[0] = 0;
             ctl->n_hidden += c;
           }
           dstamp(ctl, rr, c);
-          peel_round(g, w, k, rr, c, 0, blockDim.x * kP, ctl->tcnt);
-          ++rr;
           __syncthreads();
-          c = __ldcg(&ctl->tcnt[rr % 3]);
+          peel_round(g, w, k, rr, c, 0, blockDim.x * kP, tf.s_in(Q), tf.s_cnt, tf.g_in, Q, tf.out_slot,
+                     &ctl->tcnt[0], tf.g_out(w));
+          ++rr;
+          c = tf.advance(Q, w);
         }
+        tf.finish(Q);
         if (threadIdx.x == 0) ctl->n_rounds = rr;
       }
       grid.sync();
@@ -403,7 +460,13 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
       ctl->n_hidden += cnt;
     }
     dstamp(ctl, r, cnt);
-    peel_round(g, w, k, r, cnt, tile0, tstride, ctl->qcnt);
+    {
+      const int* cur = (r & 1) ? w.q1 : w.q0;
+      int* nxt = (r & 1) ? w.q0 : w.q1;
+      int* ncnt = &ctl->qcnt[(r + 1) % 3];
+      peel_round(g, w, k, r, cnt, tile0, tstride, nullptr, 0, cur, Q, 0, ncnt, nxt);
+      cq_flush(Q, 0, ncnt, nxt);
+    }
     ++r;
     grid.sync();
     stamp(w.ctl, 2);
@@ -419,53 +482,56 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
   //    so no union-find and no further grid barrier are needed here;
   //  * recovery: hidden predecessors of every hidden vertex (conflict
   //    neighbours popped before it) and level 0 = the vertices without one.
-  for (int t0 = tile0; t0 < n; t0 += tstride) {
-    int v[kP], e[kP], e1[kP], cnt[kP];
-    unsigned long long kv[kP];
+  for (int t0 = tile0f; t0 < n; t0 += tstridef) {
+    int v[kPF], e0[kPF], e[kPF], e1[kPF], cnt[kPF];
+    unsigned long long kv[kPF], bm[kPF];
 #pragma unroll
-    for (int j = 0; j < kP; ++j) {
+    for (int j = 0; j < kPF; ++j) {
       v[j] = t0 + j * blockDim.x + threadIdx.x;
       const int hv = v[j] < n ? __ldcg(&w.hround[v[j]]) : -1;
       kv[j] = v[j] < n ? pop_key(hv, __ldcg(&w.prio[v[j]])) : ~0ull;
-      e[j] = kv[j] != ~0ull ? __ldg(&g.ce_rp[v[j]]) : 0;
+      e[j] = e0[j] = kv[j] != ~0ull ? __ldg(&g.ce_rp[v[j]]) : 0;
       e1[j] = kv[j] != ~0ull ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
       cnt[j] = 0;
-      if (v[j] < n) w.key[v[j]] = kv[j];
+      bm[j] = 0ull;
     }
     while (true) {
       bool open = false;
 #pragma unroll
-      for (int j = 0; j < kP; ++j) open |= e[j] < e1[j];
+      for (int j = 0; j < kPF; ++j) open |= e[j] < e1[j];
       if (!open) break;
-      int u[kP][kNb], hu[kP][kNb];
-      unsigned pu[kP][kNb];
+      int u[kPF][kNb], hu[kPF][kNb];
+      unsigned pu[kPF][kNb];
 #pragma unroll
-      for (int j = 0; j < kP; ++j)
+      for (int j = 0; j < kPF; ++j)
 #pragma unroll
         for (int t = 0; t < kNb; ++t) u[j][t] = e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
 #pragma unroll
-      for (int j = 0; j < kP; ++j)
+      for (int j = 0; j < kPF; ++j)
 #pragma unroll
         for (int t = 0; t < kNb; ++t) {
           hu[j][t] = u[j][t] >= 0 ? __ldcg(&w.hround[u[j][t]]) : -1;
           pu[j][t] = u[j][t] >= 0 ? __ldcg(&w.prio[u[j][t]]) : 0u;
         }
 #pragma unroll
-      for (int j = 0; j < kP; ++j) {
+      for (int j = 0; j < kPF; ++j) {
 #pragma unroll
-        for (int t = 0; t < kNb; ++t)
+        for (int t = 0; t < kNb; ++t) {
+          if (u[j][t] < 0) continue;
           cnt[j] += (hu[j][t] >= 0 && pop_key(hu[j][t], pu[j][t]) > kv[j]) ? 1 : 0;
+          const int rel = e[j] + t - e0[j];  // popped before v, or kept
+          if (rel < 64 && pop_key(hu[j][t], pu[j][t]) > kv[j]) bm[j] |= 1ull << rel;
+        }
         e[j] += kNb;
       }
     }
-    int ready[kP], seeds[kP];
-    int mr = 0, ms = 0;
 #pragma unroll
-    for (int j = 0; j < kP; ++j) {
+    for (int j = 0; j < kPF; ++j) {
       if (v[j] >= n) continue;
       if (kv[j] != ~0ull) {
         w.deg[v[j]] = cnt[j];
-        if (cnt[j] == 0) ready[mr++] = v[j];
+        w.bmask[v[j]] = bm[j];
+        if (cnt[j] == 0) cq_push(Q, 1, v[j], &ctl->rq[0], w.q0);
       } else {
         bool seed = true;
         for (int pass = 0; pass < 2 && seed; ++pass) {
@@ -481,12 +547,12 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
             }
           }
         }
-        if (seed) seeds[ms++] = v[j];
+        if (seed) cq_push(Q, 0, v[j], &ctl->n_seed, w.roots);
       }
     }
-    cta_append(ms, seeds, &ctl->n_seed, w.roots);
-    cta_append(mr, ready, &ctl->rq[0], w.q0);
   }
+  cq_flush(Q, 0, &ctl->n_seed, w.roots);
+  cq_flush(Q, 1, &ctl->rq[0], w.q0);
   stamp(w.ctl, 3);
 }
 
@@ -505,24 +571,21 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
 // the result equals the sequential pop.
 // One recovery level: colour the ready vertices cur[0..cnt) (tiles as in
 // peel_round), queue the successors whose last predecessor this was.
-__device__ void recover_level(const GraphView& g, const Workspace& w, int k, int* colors, int L, int cnt, int first,
-                              int stride, int* qc) {
-  const int* cur = (L & 1) ? w.q1 : w.q0;
-  int* nxt = (L & 1) ? w.q0 : w.q1;
-  int* ncnt = &qc[(L + 1) % 3];
+__device__ void recover_level(const GraphView& g, const Workspace& w, int k, int* colors, int cnt, int first,
+                              int stride, const int* s_in, int s_cnt, const int* g_in, CtaQueues& Q, int qo,
+                              int* ocnt, int* oarr) {
   for (int t0 = first; t0 < cnt; t0 += stride) {
-    int items[kAppend];
-    int m = 0;
-    int v[kP], e[kP], e1[kP];
-    unsigned long long kv[kP];
+    int v[kP], e0[kP], e[kP], e1[kP];
+    unsigned long long bm[kP], kv[kP];
     unsigned used[kP];
 #pragma unroll
     for (int j = 0; j < kP; ++j) {
       const int i = t0 + j * blockDim.x + threadIdx.x;
-      v[j] = i < cnt ? __ldcg(&cur[i]) : -1;
-      kv[j] = v[j] >= 0 ? __ldcg(&w.key[v[j]]) : 0ull;
-      e[j] = v[j] >= 0 ? __ldg(&g.ce_rp[v[j]]) : 0;
+      v[j] = i < cnt ? frontier_item(s_in, s_cnt, g_in, i) : -1;
+      bm[j] = v[j] >= 0 ? __ldcg(&w.bmask[v[j]]) : 0ull;
+      e[j] = e0[j] = v[j] >= 0 ? __ldg(&g.ce_rp[v[j]]) : 0;
       e1[j] = v[j] >= 0 ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
+      kv[j] = e1[j] - e0[j] > 64 ? pop_key(__ldcg(&w.hround[v[j]]), __ldcg(&w.prio[v[j]])) : 0ull;  // long rows only
       used[j] = 0u;
     }
     while (true) {
@@ -539,8 +602,11 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
 #pragma unroll
       for (int j = 0; j < kP; ++j)
 #pragma unroll
-        for (int t = 0; t < kNb; ++t)  // popped before v (or kept)
-          before[j][t] = u[j][t] >= 0 && __ldcg(&w.key[u[j][t]]) > kv[j];
+        for (int t = 0; t < kNb; ++t) {  // popped before v (or kept): the final pass's bit, past 64 the keys
+          const int rel = e[j] + t - e0[j];
+          before[j][t] = u[j][t] >= 0 && (rel < 64 ? ((bm[j] >> rel) & 1ull) != 0ull
+                                                   : pop_key(__ldcg(&w.hround[u[j][t]]), __ldcg(&w.prio[u[j][t]])) > kv[j]);
+        }
 #pragma unroll
       for (int j = 0; j < kP; ++j)
 #pragma unroll
@@ -554,7 +620,7 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
           if (before[j][t]) {
             if (x[j][t] >= 0) used[j] |= 1u << x[j][t];
           } else if (x[j][t] == 1) {  // v was u's last predecessor
-            list_push(items, m, u[j][t], ncnt, nxt);
+            cq_push(Q, qo, u[j][t], ocnt, oarr);
           }
         }
         e[j] += kNb;
@@ -566,14 +632,55 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
       const int c = __ffs(~used[j]) - 1;
       colors[v[j]] = c < k ? c : 0;  // c < k by the simplification invariant
     }
-    cta_append(m, items, ncnt, nxt);
   }
 }
 
-__global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover(GraphView g, Workspace w, int k, int* colors) {
+// Eq. (1a) cost per layout and the statistics, by the last CTA of a kernel
+// to finish (counter `done`; the caller's threads have all finished their part).
+__device__ void finalize_outputs(const GraphView& g, const Workspace& w, const Outputs& out, int* done) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(done, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int l = threadIdx.x; l < g.n_layouts; l += blockDim.x) {
+    const long long nc = __ldcg(&out.counts[2 * l]);
+    const long long ns = __ldcg(&out.counts[2 * l + 1]);
+    out.cost[l] = __dadd_rn(__dmul_rn(out.alpha, (double)ns), (double)nc);
+  }
+  if (threadIdx.x == 0 && out.stats) {
+    Control* ctl = w.ctl;
+    out.stats[MPLD_STAT_COMPONENTS] = __ldcg(&ctl->n_comp);
+    out.stats[MPLD_STAT_HIDDEN] = __ldcg(&ctl->n_hidden);
+    out.stats[MPLD_STAT_ROUNDS] = __ldcg(&ctl->n_rounds);
+    out.stats[MPLD_STAT_MAX_COMP] = __ldcg(&ctl->max_comp);
+    out.stats[MPLD_STAT_STEPS] = (long long)__ldcg(&ctl->steps);
+    out.stats[MPLD_STAT_TRUNCATED] = __ldcg(&ctl->truncated);
+    out.stats[MPLD_STAT_ERROR] = __ldcg(&ctl->err);
+    out.stats[MPLD_STAT_LAUNCHES] = out.launches;
+    out.stats[MPLD_STAT_MAX_STEPS] = __ldcg(&ctl->max_steps_comp);
+  }
+}
+
+__device__ void recover_levels(const GraphView& g, const Workspace& w, int k, int* colors, GridBarrier& grid,
+                               CtaQueues& Q);
+
+// With out.enabled the search kernels have accumulated the counts (one shard)
+// and the last CTA of the recovery writes the costs and statistics.
+__global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover(GraphView g, Workspace w, int k, int* colors,
+                                                                    Outputs out) {
   GridBarrier grid(&w.ctl->bar[1]);
+  __shared__ CtaQueues Q;
+  cq_init(Q);
   stamp(w.ctl, 13);
-  if (__ldcg(&w.ctl->err)) return;
+  if (!__ldcg(&w.ctl->err)) recover_levels(g, w, k, colors, grid, Q);
+  if (out.enabled) finalize_outputs(g, w, out, &w.ctl->done_recover);
+}
+
+__device__ void recover_levels(const GraphView& g, const Workspace& w, int k, int* colors, GridBarrier& grid,
+                               CtaQueues& Q) {
   const int nth = gridDim.x * blockDim.x;
   Control* ctl = w.ctl;
   const int tile0 = blockIdx.x * blockDim.x * kP, tstride = nth * kP;
@@ -588,19 +695,28 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover(GraphView 
     if (cnt <= kTail) {  // small level: CTA 0 finishes the remaining levels with block barriers
       if (blockIdx.x == 0) {
         int LL = L, c = cnt;
+        TailFrontier tf;
+        tf.g_in = (L & 1) ? w.q1 : w.q0;
         while (c > 0) {
-          if (threadIdx.x == 0) ctl->trq[(LL + 2) % 3] = 0;  // own counters, as in the simplification tail
-          recover_level(g, w, k, colors, LL, c, 0, blockDim.x * kP, ctl->trq);
-          ++LL;
+          if (threadIdx.x == 0) ctl->trq[0] = 0;  // own overflow counter, as in the simplification tail
           __syncthreads();
-          c = __ldcg(&ctl->trq[LL % 3]);
+          recover_level(g, w, k, colors, c, 0, blockDim.x * kP, tf.s_in(Q), tf.s_cnt, tf.g_in, Q, tf.out_slot,
+                        &ctl->trq[0], tf.g_out(w));
+          ++LL;
+          c = tf.advance(Q, w);
         }
         if (threadIdx.x == 0) ctl->n_levels = LL;
       }
       break;  // no grid barrier needed: the kernel ends here
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->rq[(L + 2) % 3] = 0;
-    recover_level(g, w, k, colors, L, cnt, tile0, tstride, ctl->rq);
+    {
+      const int* cur = (L & 1) ? w.q1 : w.q0;
+      int* nxt = (L & 1) ? w.q0 : w.q1;
+      int* ncnt = &ctl->rq[(L + 1) % 3];
+      recover_level(g, w, k, colors, cnt, tile0, tstride, nullptr, 0, cur, Q, 0, ncnt, nxt);
+      cq_flush(Q, 0, ncnt, nxt);
+    }
     ++L;
     grid.sync();
     stamp(w.ctl, 9);
@@ -660,30 +776,14 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
       }
     }
   }
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&w.ctl->done_blocks, 1) == (int)gridDim.x - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int l = threadIdx.x; l < g.n_layouts; l += blockDim.x) {
-    const long long nc = __ldcg(&counts[2 * l]);
-    const long long ns = __ldcg(&counts[2 * l + 1]);
-    cost[l] = __dadd_rn(__dmul_rn(alpha, (double)ns), (double)nc);
-  }
-  if (threadIdx.x == 0 && stats) {
-    Control* ctl = w.ctl;
-    stats[MPLD_STAT_COMPONENTS] = __ldcg(&ctl->n_comp);
-    stats[MPLD_STAT_HIDDEN] = __ldcg(&ctl->n_hidden);
-    stats[MPLD_STAT_ROUNDS] = __ldcg(&ctl->n_rounds);
-    stats[MPLD_STAT_MAX_COMP] = __ldcg(&ctl->max_comp);
-    stats[MPLD_STAT_STEPS] = (long long)__ldcg(&ctl->steps);
-    stats[MPLD_STAT_TRUNCATED] = __ldcg(&ctl->truncated);
-    stats[MPLD_STAT_ERROR] = __ldcg(&ctl->err);
-    stats[MPLD_STAT_LAUNCHES] = launches;
-    stats[MPLD_STAT_MAX_STEPS] = __ldcg(&ctl->max_steps_comp);
-  }
+  Outputs out;
+  out.counts = counts;
+  out.cost = cost;
+  out.stats = stats;
+  out.alpha = alpha;
+  out.launches = launches;
+  out.enabled = 1;
+  finalize_outputs(g, w, out, &w.ctl->done_blocks);
 }
 
 }  // namespace
@@ -695,10 +795,10 @@ cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, 
   return cudaLaunchCooperativeKernel((void*)mpld_simplify_components, dim3(blocks), dim3(threads), args, 0, s);
 }
 
-cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, cudaStream_t s, int blocks,
-                           int threads) {
+cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
+                           int blocks, int threads) {
   GraphView gg = g;
-  void* args[] = {&gg, &ws, &k, &colors};
+  void* args[] = {&gg, &ws, &k, &colors, &out};
   return cudaLaunchCooperativeKernel((void*)mpld_recover, dim3(blocks), dim3(threads), args, 0, s);
 }
 

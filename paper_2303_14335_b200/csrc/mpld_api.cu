@@ -6,11 +6,13 @@
 //                              recovery pop keys and level 0
 //   mpld_component_discover    one warp per seed: components -> pool of bit-packed matrices
 //   mpld_exact_cover_search<K> one warp per component of the pool
-//   mpld_exact_cover_search_heavy<K> (exact mode) one warp per heavy component
+//   mpld_exact_cover_search_heavy<K,W> (exact mode) one warp per heavy component, one launch
+//                              per word class (32-bit: n <= 32, 64-bit: n > 32)
 //   mpld_recover               cooperative: LIFO recovery of hidden vertices
 //   mpld_evaluate              Eq. (1) per layout + stats
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstddef>
 #include <cstdio>
@@ -83,7 +85,7 @@ struct mpld_context {
   int* deg = nullptr;
   int* hround = nullptr;
   unsigned* prio = nullptr;
-  unsigned long long* key = nullptr;
+  unsigned long long* bmask = nullptr;
   int* q0 = nullptr;
   int* q1 = nullptr;
   int* roots = nullptr;
@@ -99,8 +101,10 @@ struct mpld_context {
   bool prepared = false;
   int call_launches = 0;
   unsigned light_steps = kLightStepsDefault;  // MPLD_LIGHT_STEPS overrides (tuning)
-  int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0, blocks_heavy = 0,
-      blocks_discover = 0;
+  int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0, blocks_discover = 0;
+  int blocks_heavy[6] = {0, 0, 0, 0, 0, 0};  // per k = 2..4 and word class (32-bit, 64-bit)
+  long long* counts = nullptr;  // the prepare phase's d_counts (zeroed by the simplification kernel)
+  bool search_counted = false;  // the search accumulated the counts (one shard)
   // host-API staging (device copies of host inputs / outputs)
   int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
   int* h_lo = nullptr;
@@ -143,7 +147,7 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
       e = grow(p, cap);
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
-    if (grow(&ctx->prio, cap) != cudaSuccess || grow(&ctx->key, cap) != cudaSuccess ||
+    if (grow(&ctx->prio, cap) != cudaSuccess || grow(&ctx->bmask, cap) != cudaSuccess ||
         grow(&ctx->crec, cap) != cudaSuccess || grow(&ctx->pmask, 2 * cap) != cudaSuccess)
       return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     ctx->cap_n = cap;
@@ -199,7 +203,7 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 }
 
 Workspace workspace(mpld_context* ctx) {
-  return Workspace{ctx->deg,   ctx->hround, ctx->key,    ctx->prio,  ctx->q0,    ctx->q1,
+  return Workspace{ctx->deg,   ctx->hround, ctx->bmask,    ctx->prio,  ctx->q0,    ctx->q1,
                    ctx->roots, ctx->crec,   ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->ctl};
 }
 
@@ -209,6 +213,8 @@ int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, 
   Workspace ws = workspace(ctx);
   ctx->g = g;
   ctx->k = k;
+  ctx->counts = counts;
+  ctx->search_counted = false;
   ctx->prepared = true;
   ctx->call_launches = 0;
   // the control block (counters, barrier arrivals, error bits) starts every call at zero
@@ -233,6 +239,11 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
                                    offsetof(Control, comp_pool) + sizeof(unsigned long long) -
                                        offsetof(Control, n_heavy), s);
   if (e0 != cudaSuccess) return cuda_fail(e0, "search counters reset");
+  // one shard: the search kernels accumulate the Eq. (1) counts of the final
+  // colourings (the recovery adds no conflict, R9), so the finish
+  // phase needs no evaluation pass
+  ctx->search_counted = shard_count == 1;
+  long long* count = ctx->search_counted ? ctx->counts : nullptr;
   {
     TimedLaunch t(ctx, K_DISCOVER, s);
     cudaError_t e = launch_discover(g, ws, shard_index, shard_count, s, ctx->blocks_discover);
@@ -242,7 +253,7 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
   }
   {
     TimedLaunch t(ctx, K_SEARCH, s);
-    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, s,
+    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, count, s,
                                   ctx->blocks_search);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
     t.done();
@@ -250,10 +261,10 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
   }
   if (max_steps <= 0) {  // exact mode: heavy components on the warp-parallel search
     TimedLaunch t(ctx, K_SEARCH_HEAVY, s);
-    cudaError_t e = launch_search_heavy(g, ws, ctx->k, w_stitch, colors, s, ctx->blocks_heavy);
+    cudaError_t e = launch_search_heavy(g, ws, ctx->k, w_stitch, colors, count, s, ctx->blocks_heavy);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_heavy");
     t.done();
-    ++ctx->call_launches;
+    ctx->call_launches += 2;  // one launch per word class
   }
   return MPLD_OK;
 }
@@ -263,18 +274,26 @@ int phase_finish(mpld_context* ctx, cudaStream_t s, double alpha, int* colors, l
                  long long* stats) {
   Workspace ws = workspace(ctx);
   const GraphView& g = ctx->g;
+  Outputs out;
+  out.counts = counts;
+  out.cost = cost;
+  out.stats = stats;
+  out.alpha = alpha;
+  out.enabled = ctx->search_counted && counts == ctx->counts;
   {
     TimedLaunch t(ctx, K_RECOVER, s);
-    cudaError_t e = launch_recover(g, ws, ctx->k, colors, s, ctx->blocks_recover, kCoopThreads);
+    out.launches = ++ctx->call_launches;
+    cudaError_t e = launch_recover(g, ws, ctx->k, colors, out, s, ctx->blocks_recover, kCoopThreads);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_recover");
     t.done();
-    ++ctx->call_launches;
   }
-  TimedLaunch t(ctx, K_EVALUATE, s);
-  cudaError_t e = launch_evaluate(g, ws, colors, alpha, counts, cost, stats, ctx->call_launches + 1, s,
-                                  ctx->blocks_stream);
-  if (e != cudaSuccess) return cuda_fail(e, "mpld_evaluate");
-  t.done();
+  if (!out.enabled) {  // sharded search: the counts come from one pass over the combined colours
+    TimedLaunch t(ctx, K_EVALUATE, s);
+    cudaError_t e = launch_evaluate(g, ws, colors, alpha, counts, cost, stats, ctx->call_launches + 1, s,
+                                    ctx->blocks_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_evaluate");
+    t.done();
+  }
   ctx->prepared = false;
   return MPLD_OK;
 }
@@ -403,13 +422,14 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     const long v = std::strtol(ls, nullptr, 10);
     if (v >= 1 && v <= (1L << 24)) ctx->light_steps = (unsigned)v;
   }
-  e = configure_search_heavy();
+  e = configure_search_heavy(ctx->num_sms, ctx->blocks_heavy);
   if (e != cudaSuccess) {
     mpld_context_destroy(ctx);
     return cuda_fail(e, "configure heavy search");
   }
-  ctx->blocks_heavy = resident_blocks_heavy(ctx->num_sms);
-  if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0 || ctx->blocks_heavy <= 0 ||
+  int min_heavy = ctx->blocks_heavy[0];
+  for (int b : ctx->blocks_heavy) min_heavy = std::min(min_heavy, b);
+  if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0 || min_heavy <= 0 ||
       ctx->blocks_discover <= 0) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_CUDA, "occupancy query failed (kernel image missing for this device?)");
@@ -430,7 +450,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
 
 void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
-  for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->key, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
+  for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->bmask, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->roots, (void*)ctx->crec, (void*)ctx->pmask, (void*)ctx->porder, (void*)ctx->hcomp,
                   (void*)ctx->hcost, (void*)ctx->ctl, (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,

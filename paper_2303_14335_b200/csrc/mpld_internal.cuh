@@ -2,14 +2,14 @@
 //
 // Data layout in HBM:
 //   graph     : caller's CSR arrays (int32), read-only.
-//   per vertex: deg, hround, prio (int32), key (u64) — indexed by vertex id
+//   per vertex: deg, hround, prio (int32), bmask (u64) — indexed by vertex id
 //   queues    : q0, q1 (int32 [n]) — simplification frontiers, then recovery levels
 //   seeds     : roots (int32 [n])
 //   component pool (filled by the discovery kernel, one record per component):
 //               crec (u64 [n]) = pool offset << 8 | size; pmask (u64 [2n]) = adj/sadj
 //               words of every component vertex in BFS column order (R5),
 //               interleaved; porder (int32 [n]) = their vertex ids
-//   heavy list: hcomp, hcost (int32 [n]) — exact mode's CTA-parallel components
+//   heavy list: hcomp, hcost (int32 [n]) — exact mode's warp-parallel components
 //   Control   : one control block (counters, barrier arrivals, error bits,
 //               diagnostics) per context, zeroed at the start of every call.
 #pragma once
@@ -37,13 +37,15 @@ struct Control {
   int truncated;    // components whose search hit max_steps
   int err;          // ErrBits
   int done_blocks;  // last-block detection of the evaluation kernel
+  int done_recover; // last-block detection of the recovery kernel (finalisation)
   int max_steps_comp;        // largest per-component step count
   int qcnt[3];               // simplification frontier sizes (rotating by round)
   int rq[3];                 // recovery level sizes (rotating by level)
   int tcnt[3];               // ... the same, for the single-CTA tails (never read by other CTAs)
   int trq[3];
   int n_levels;              // recovery levels (DAG depth + 1)
-  int n_heavy;               // exact mode: components handed to the CTA-parallel search (reset per search call)
+  int n_heavy;               // exact mode: components handed to the warp-parallel search (reset per search call)
+  int heavy_next[2];         // exact mode: next heavy component to take per word class (reset with n_heavy)
   int pad_;
   unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
   unsigned long long steps;  // search nodes entered
@@ -94,7 +96,7 @@ struct GraphView {
 struct Workspace {
   int* deg;        // live conflict degree (simplification), then hidden-predecessor count (recovery)
   int* hround;     // -1 kept, else the round the vertex was hidden in
-  unsigned long long* key;  // recovery pop-order key (round, priority); ~0 for kept vertices
+  unsigned long long* bmask;  // recovery: bit t = CE entry t of the row pops before the vertex (or is kept)
   unsigned* prio;  // lowbias32(layout-local id), recovery priority (R9)
   int* q0;         // frontier queues (double-buffered)
   int* q1;
@@ -105,6 +107,29 @@ struct Workspace {
   int* hcomp;      // heavy components (exact mode): component index ...
   int* hcost;      // ... and the light phase's best cost
   Control* ctl;
+};
+
+// Layout of vertex v: the l with layout_off[l] <= v < layout_off[l+1] (binary
+// search; the offsets are tiny and stay in L1).
+__device__ __forceinline__ int layout_of(const GraphView& g, int v) {
+  int a = 0, b = g.n_layouts;
+  while (b - a > 1) {
+    const int m = (a + b) >> 1;
+    if (__ldg(&g.layout_off[m]) <= v) a = m; else b = m;
+  }
+  return a;
+}
+
+// Eq. (1) outputs: per-layout (n_conflicts, n_stitches) accumulated by the
+// search kernels (counts), the cost and the statistics written at the end of
+// the recovery (enabled) or by the evaluation kernel.
+struct Outputs {
+  long long* counts;  // [2 * n_layouts]
+  double* cost;       // [n_layouts]
+  long long* stats;   // [MPLD_STAT_LEN] or null
+  double alpha;
+  int launches;
+  int enabled;
 };
 
 // 32-bit counter-based mix (a bijection), recovery priority of DESIGN.md R9.
@@ -124,12 +149,12 @@ cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, 
 cudaError_t launch_discover(const GraphView& g, Workspace ws, int shard_index, int shard_count, cudaStream_t s,
                             int blocks);
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
-                          unsigned light_steps, cudaStream_t s, int blocks);
+                          unsigned light_steps, long long* counts, cudaStream_t s, int blocks);
 constexpr unsigned kLightStepsDefault = 48;  // exact mode: one-lane budget before a component turns heavy
-cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, cudaStream_t s,
-                                int blocks);
-cudaError_t configure_search_heavy();
-cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, cudaStream_t s,
+cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, long long* counts,
+                                cudaStream_t s, const int* blocks);
+cudaError_t configure_search_heavy(int num_sms, int* blocks);  // blocks[6]: resident grids of the heavy kernels
+cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
                            int blocks, int threads);
 cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors, double alpha,
                             long long* counts, double* cost, long long* stats, int launches,
@@ -141,6 +166,5 @@ int coop_blocks_recover(int threads, int num_sms);
 int resident_blocks_search(int threads, int num_sms);
 int resident_blocks_discover(int num_sms);
 int resident_blocks_evaluate(int num_sms);
-int resident_blocks_heavy(int num_sms);  // after configure_search_heavy()
 
 }  // namespace mpld

@@ -54,8 +54,9 @@ def run(b, k, alpha, iters=10, flush=None, max_steps=1 << 20, flags=1):
     dd, ds = int(d[84]), int(d[86])
     print("  slowest discovery: cycles, n(|groups<<8|chunks<<16 in diag builds):", dd >> 16, dd & 0xffff,
           "| slowest light search: cycles, steps, n:", ds >> 24, (ds >> 8) & 0xffff, ds & 0xff)
-    print("  slowest heavy warp: cycles total/split, subtrees, n:", int(d[89]), int(d[90]), int(d[91]) >> 32,
-          int(d[91]) & 0xffffffff)
+    h = int(d[91])
+    print("  heavy search: slowest component cycles, its n, iterations, steal rounds; slowest warp cycles:", int(d[89]),
+          h & 0xff, (h >> 8) & 0xffffffff, h >> 40, int(d[90]))
     print("  seeds, heavy components, components:", int(d[92]), int(d[93]), int(d[94]))
     st = dict(zip(mp.STAT_NAMES, stats.cpu().tolist()))
     ctx.close()
