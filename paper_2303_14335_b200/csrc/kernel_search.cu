@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
 #endif
 constexpr int kDonateMinLevels = MPLD_DONATE_MIN_LEVELS;  // a frame is donated from only if n - depth >= this
 #ifndef MPLD_STEAL_MIN_IDLE
-#define MPLD_STEAL_MIN_IDLE 1
+#define MPLD_STEAL_MIN_IDLE 8
 #endif
 constexpr int kStealMinIdle = MPLD_STEAL_MIN_IDLE;  // donation rounds only when at least this many lanes are idle
 
@@ -730,25 +730,24 @@ __device__ __forceinline__ void apply_row(State<K, W>& s, int v, int c, const W*
   s.mu = max(s.mu, c);
 }
 
-// warp-wide minimum of the lanes' keys (cost, path); returns the lane holding it
+// warp-wide minimum of the lanes' keys (cost, path), by 32-bit warp reductions
+// (REDUX): the cost first, then each path word among the lanes still tied.
+// Every lane receives the minimum; returns the lowest lane holding it.
 template <bool kTwo>
 __device__ __forceinline__ int warp_min_key(int& c, Path& p) {
-  const int lane = threadIdx.x & 31;
-  int src = lane;
+  const int mc = (int)(__reduce_min_sync(0xffffffffu, (unsigned)c ^ 0x80000000u) ^ 0x80000000u);  // signed order
+  bool tie = c == mc;
+  unsigned words[4] = {(unsigned)(p.a >> 32), (unsigned)p.a, (unsigned)(p.b >> 32), (unsigned)p.b};
+  unsigned best[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const int oc = __shfl_xor_sync(0xffffffffu, c, o);
-    Path op;
-    op.a = __shfl_xor_sync(0xffffffffu, p.a, o);
-    op.b = kTwo ? __shfl_xor_sync(0xffffffffu, p.b, o) : 0ull;
-    const int os = __shfl_xor_sync(0xffffffffu, src, o);
-    if (key_less<kTwo>(oc, op, c, p) || (!key_less<kTwo>(c, p, oc, op) && os < src)) {
-      c = oc;
-      p = op;
-      src = os;
-    }
+  for (int i = 0; i < (kTwo ? 4 : 2); ++i) {
+    best[i] = __reduce_min_sync(0xffffffffu, tie ? words[i] : 0xffffffffu);
+    tie = tie && words[i] == best[i];
   }
-  return src;
+  c = mc;
+  p.a = ((unsigned long long)best[0] << 32) | best[1];
+  p.b = kTwo ? (((unsigned long long)best[2] << 32) | best[3]) : 0ull;
+  return __ffs(__ballot_sync(0xffffffffu, tie)) - 1;
 }
 
 // Frames of the lanes in shared memory, [field][depth][lane] (a lane only
@@ -778,7 +777,7 @@ template <int K, typename W>
 __device__ void warp_heavy_search(int n, const W* __restrict__ adj, const W* __restrict__ sadj, const W* cl,
                                   int ncl, LaneFrames<K, W, heavy_depth<K, W>()>& F, int w_stitch, int c1,
                                   const Path& p1, const int* porder, int* colors, Control* ctl, W (&fin)[K],
-                                  unsigned& iters, unsigned& steal_rounds) {
+                                  int* slot, unsigned& iters, unsigned& steal_rounds) {
   using O = WordOps<W>;
   constexpr bool kTwo = sizeof(W) == 8;
   const int lane = threadIdx.x & 31;
@@ -862,12 +861,11 @@ __device__ void warp_heavy_search(int n, const W* __restrict__ adj, const W* __r
           xd = j + 1;
         }
         const bool take = !active && __popc(idle & lt) < np;
-        int src = lane;
-        if (take) {  // the donor of the same rank
-          unsigned m = don;
-          for (int r = __popc(idle & lt); r > 0; --r) m &= m - 1;
-          src = __ffs(m) - 1;
-        }
+        // pair the i-th idle lane with the i-th donor through the warp's slot table
+        if (((don >> lane) & 1u) && __popc(don & lt) < np) slot[__popc(don & lt)] = lane;
+        __syncwarp();
+        const int src = take ? slot[__popc(idle & lt)] : lane;
+        __syncwarp();
 #pragma unroll
         for (int c = 0; c < K; ++c) {
           xC[c] = __shfl_sync(0xffffffffu, xC[c], src);
@@ -1081,8 +1079,9 @@ __device__ unsigned long long heavy_component(const GraphView& g, int n, size_t 
   W fin[K];  // the final colouring: the light leaf unless the search beats it
 #pragma unroll
   for (int c = 0; c < K; ++c) fin[c] = col[c];
-  warp_heavy_search<K, W>(n, s_adj, s_sadj, s_cl, ncl, F, w_stitch, c1, p1, porder, colors, w.ctl, fin, iters,
-                          steals);
+  __shared__ int s_slot[32];  // donor lanes by rank (work donation)
+  warp_heavy_search<K, W>(n, s_adj, s_sadj, s_cl, ncl, F, w_stitch, c1, p1, porder, colors, w.ctl, fin, s_slot,
+                          iters, steals);
   if (counts) {
     int nc = 0, ns = 0;
     for (int i = lane; i < n; i += 32) {
