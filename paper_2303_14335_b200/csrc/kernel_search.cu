@@ -616,10 +616,12 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
       add_counts(g, __ldcg(&w.porder[off]), nc, ns, counts);
     }
     if (lane == 0) {
-      if (trunc && exact) {  // hand the component to the CTA-parallel search
-        const int h = atomicAdd(&ctl->n_heavy, 1);
-        w.hcomp[h] = ci;
-        w.hcost[h] = best_cost;
+      if (trunc && exact) {  // hand the component to the warp-parallel search of its word class
+        const int cls = n > 32 ? 1 : 0;
+        const int h = atomicAdd(&ctl->n_heavy[cls], 1);
+        const int idx = cls ? g.n - 1 - h : h;
+        w.hcomp[idx] = ci;
+        w.hcost[idx] = best_cost;
       } else {
         acc_maxsteps = max(acc_maxsteps, (int)min(steps, (unsigned)INT_MAX));
         acc_trunc += trunc ? 1 : 0;
@@ -1105,17 +1107,17 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int cls = sizeof(W) == 4 ? 0 : 1;
   Control* ctl = w.ctl;
-  const int n_heavy = __ldcg(&ctl->n_heavy);
+  const int n_heavy = __ldcg(&ctl->n_heavy[cls]);
   const long long t0 = clock64();
   while (true) {
     int h = 0;
-    if (threadIdx.x == 0) h = atomicAdd(&ctl->heavy_next[cls], 1);  // dynamic schedule over the heavy list
+    if (threadIdx.x == 0 && n_heavy) h = atomicAdd(&ctl->heavy_next[cls], 1);  // dynamic schedule over the list
     h = __shfl_sync(0xffffffffu, h, 0);
     if (h >= n_heavy) break;
-    const unsigned long long rec = __ldcg(&w.crec[__ldcg(&w.hcomp[h])]);
+    const int idx = cls ? g.n - 1 - h : h;
+    const unsigned long long rec = __ldcg(&w.crec[__ldcg(&w.hcomp[idx])]);
     const int n = (int)(rec & 0xffull);
-    if ((n > 32) != (cls == 1)) continue;  // the other class's launch takes it
-    const int c1 = __ldcg(&w.hcost[h]);
+    const int c1 = __ldcg(&w.hcost[idx]);
     const size_t off = (size_t)(rec >> 8);
     const long long c0 = clock64();
     const unsigned long long is = heavy_component<K, W>(g, n, off, w, smem, w_stitch, c1, colors, counts);

@@ -475,25 +475,30 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
   stamp(w.ctl, 1);
 
   // Final pass (rounds are final now):
-  //  * pop keys (R9);
+  //  * the "popped before" bitmask of every hidden vertex (pop keys, R9);
   //  * component-search seeds: a kept vertex with no kept neighbour (CE ∪ SE)
   //    of smaller id.  Every component has at least one seed (its minimum);
   //    the search kernel keeps a seed only if it is its component's minimum,
   //    so no union-find and no further grid barrier are needed here;
   //  * recovery: hidden predecessors of every hidden vertex (conflict
   //    neighbours popped before it) and level 0 = the vertices without one.
+  // One batched walk over the CE row of every vertex: a hidden vertex counts
+  // its predecessors, a kept one looks for a kept neighbour of smaller id
+  // (rows ascending: the walk stops at the first larger id).
   for (int t0 = tile0f; t0 < n; t0 += tstridef) {
     int v[kPF], e0[kPF], e[kPF], e1[kPF], cnt[kPF];
     unsigned long long kv[kPF], bm[kPF];
+    bool seed[kPF];
 #pragma unroll
     for (int j = 0; j < kPF; ++j) {
       v[j] = t0 + j * blockDim.x + threadIdx.x;
       const int hv = v[j] < n ? __ldcg(&w.hround[v[j]]) : -1;
       kv[j] = v[j] < n ? pop_key(hv, __ldcg(&w.prio[v[j]])) : ~0ull;
-      e[j] = e0[j] = kv[j] != ~0ull ? __ldg(&g.ce_rp[v[j]]) : 0;
-      e1[j] = kv[j] != ~0ull ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
+      e[j] = e0[j] = v[j] < n ? __ldg(&g.ce_rp[v[j]]) : 0;
+      e1[j] = v[j] < n ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
       cnt[j] = 0;
       bm[j] = 0ull;
+      seed[j] = true;
     }
     while (true) {
       bool open = false;
@@ -511,18 +516,25 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
 #pragma unroll
         for (int t = 0; t < kNb; ++t) {
           hu[j][t] = u[j][t] >= 0 ? __ldcg(&w.hround[u[j][t]]) : -1;
-          pu[j][t] = u[j][t] >= 0 ? __ldcg(&w.prio[u[j][t]]) : 0u;
+          pu[j][t] = u[j][t] >= 0 && kv[j] != ~0ull ? __ldcg(&w.prio[u[j][t]]) : 0u;
         }
 #pragma unroll
       for (int j = 0; j < kPF; ++j) {
+        bool past = false;  // kept v: a neighbour above v was seen
 #pragma unroll
         for (int t = 0; t < kNb; ++t) {
           if (u[j][t] < 0) continue;
-          cnt[j] += (hu[j][t] >= 0 && pop_key(hu[j][t], pu[j][t]) > kv[j]) ? 1 : 0;
-          const int rel = e[j] + t - e0[j];  // popped before v, or kept
-          if (rel < 64 && pop_key(hu[j][t], pu[j][t]) > kv[j]) bm[j] |= 1ull << rel;
+          if (kv[j] != ~0ull) {
+            const bool before = pop_key(hu[j][t], pu[j][t]) > kv[j];  // popped before v, or kept
+            cnt[j] += (hu[j][t] >= 0 && before) ? 1 : 0;
+            const int rel = e[j] + t - e0[j];
+            if (rel < 64 && before) bm[j] |= 1ull << rel;
+          } else {
+            if (u[j][t] < v[j] && hu[j][t] == -1) seed[j] = false;
+            past |= u[j][t] > v[j];
+          }
         }
-        e[j] += kNb;
+        e[j] = (kv[j] == ~0ull && (past || !seed[j])) ? e1[j] : e[j] + kNb;
       }
     }
 #pragma unroll
@@ -533,21 +545,17 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
         w.bmask[v[j]] = bm[j];
         if (cnt[j] == 0) cq_push(Q, 1, v[j], &ctl->rq[0], w.q0);
       } else {
-        bool seed = true;
-        for (int pass = 0; pass < 2 && seed; ++pass) {
-          const int* rp = pass ? g.se_rp : g.ce_rp;
-          const int* col = pass ? g.se_col : g.ce_col;
-          // rows are ascending: only the first neighbours can be smaller than v
-          for (int x = rp[v[j]], x1 = rp[v[j] + 1]; x < x1; ++x) {
-            const int u = col[x];
+        // stitch neighbours (stitch vertices only; rows ascending)
+        if (seed[j])
+          for (int x = __ldg(&g.se_rp[v[j]]), x1 = __ldg(&g.se_rp[v[j] + 1]); x < x1; ++x) {
+            const int u = __ldg(&g.se_col[x]);
             if (u > v[j]) break;
             if (__ldcg(&w.hround[u]) == -1) {
-              seed = false;
+              seed[j] = false;
               break;
             }
           }
-        }
-        if (seed) cq_push(Q, 0, v[j], &ctl->n_seed, w.roots);
+        if (seed[j]) cq_push(Q, 0, v[j], &ctl->n_seed, w.roots);
       }
     }
   }

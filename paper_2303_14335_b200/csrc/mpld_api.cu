@@ -754,7 +754,7 @@ int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
   v[19] = c.max_steps_comp;
   for (int i = 0; i < 8; ++i) v[84 + i] = (int64_t)c.dbg[i];
   v[92] = c.n_seed;
-  v[93] = c.n_heavy;
+  v[93] = c.n_heavy[0] + c.n_heavy[1];
   v[94] = c.n_comp;
   v[95] = c.truncated;
   for (int i = 0; i < n && i < 96; ++i) out[i] = v[i];

@@ -44,9 +44,9 @@ struct Control {
   int tcnt[3];               // ... the same, for the single-CTA tails (never read by other CTAs)
   int trq[3];
   int n_levels;              // recovery levels (DAG depth + 1)
-  int n_heavy;               // exact mode: components handed to the warp-parallel search (reset per search call)
+  int n_heavy[2];            // exact mode: components handed to the warp-parallel search, per word class
+                             // (32-bit: hcomp[0..), 64-bit: hcomp[n-1], hcomp[n-2], ...; reset per search call)
   int heavy_next[2];         // exact mode: next heavy component to take per word class (reset with n_heavy)
-  int pad_;
   unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
   unsigned long long steps;  // search nodes entered
   unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)

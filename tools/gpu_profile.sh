@@ -1,0 +1,5 @@
+# round profile set: bench line, ncu launch list, ncu --set full of every kernel of one step (dev tool)
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 300 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err; cat gpurun_out/bench.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --profile-launches --steps 2 --warmup 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:mpld_ -c 7 -o gpurun_out/full -f python bench.py --profile-launches --steps 1 --warmup 1 > gpurun_out/ncu_full.log 2>&1; tail -2 gpurun_out/ncu_full.log

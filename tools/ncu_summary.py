@@ -29,7 +29,12 @@ def main():
 
     kernels = {}
     for d in data:
-        name = d[col["Kernel Name"]].split("(")[0].split("::")[-1].split("<")[0].strip()
+        full = d[col["Kernel Name"]].split("(")[0]
+        name = full.split("::")[-1].split("<")[0].strip()
+        if "<" in full and ("unsigned long long" in full or full.rstrip().endswith("unsigned int>")):
+            name += "<64>" if "unsigned long long" in full else "<32>"  # word class of the heavy search
+        if name in kernels:  # a later launch of the same kernel (the next step): keep the first
+            continue
         stalls = {}
         for h, i in col.items():
             if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
