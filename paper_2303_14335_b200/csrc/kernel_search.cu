@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
   }
   if (lane == 0 && acc_comp) atomicAdd(&ctl->n_comp, (int)acc_comp);
   if (lane == 0 && acc_maxn > 0) atomicMax(&ctl->max_comp, acc_maxn);
-  if (lane == 0 && d_cyc > 0) atomicMax(&ctl->dbg[0], (d_cyc << 16) | (d_n & 0xffffull));  // diagnostics (no return)
+  if (MPLD_DIAG && lane == 0 && d_cyc > 0) atomicMax(&ctl->dbg[0], (d_cyc << 16) | (d_n & 0xffffull));
 }
 
 // One warp per component of the pool: the budgeted sequential search on lane
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_co
     }
     __syncwarp();
   }
-  if (lane == 0 && d_cyc > 0)  // diagnostics (no return): cycles << 24 | steps << 8 | n
+  if (MPLD_DIAG && lane == 0 && d_cyc > 0)  // diagnostics: cycles << 24 | steps << 8 | n
     atomicMax(&ctl->dbg[2], (d_cyc << 24) | (min(d_steps, 0xffffull) << 8) | (d_n & 0xffull));
   if (lane == 0 && acc_steps) {
     atomicAdd(&ctl->steps, acc_steps);
@@ -1121,7 +1121,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
     const size_t off = (size_t)(rec >> 8);
     const long long c0 = clock64();
     const unsigned long long is = heavy_component<K, W>(g, n, off, w, smem, w_stitch, c1, colors, counts);
-    if (threadIdx.x == 0) {  // diagnostics (racy by design): slowest component, its size, iterations, steal rounds
+    if (MPLD_DIAG && threadIdx.x == 0) {  // diagnostics (racy by design): slowest component, size, iterations, steals
       const unsigned long long cyc = (unsigned long long)(clock64() - c0);
       if (cyc > ctl->dbg[5]) {
         atomicMax(&ctl->dbg[5], cyc);
@@ -1129,7 +1129,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
       }
     }
   }
-  if (threadIdx.x == 0) atomicMax(&ctl->dbg[6], (unsigned long long)(clock64() - t0));  // slowest warp overall
+  if (MPLD_DIAG && threadIdx.x == 0) atomicMax(&ctl->dbg[6], (unsigned long long)(clock64() - t0));
 }
 
 }  // namespace

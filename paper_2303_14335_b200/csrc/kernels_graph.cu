@@ -262,7 +262,7 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 // seeds and the recovery's predecessor counts and level 0.
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_components(GraphView g, Workspace w, int k,
                                                                     int* colors, long long* counts, int validate) {
-  GridBarrier grid(&w.ctl->bar[0]);
+  GridBarrier grid(&w.ctl->bar0);
   __shared__ CtaQueues Q;
   cq_init(Q);
   stamp(w.ctl, 12);
@@ -679,7 +679,7 @@ __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, in
 // and the last CTA of the recovery writes the costs and statistics.
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover(GraphView g, Workspace w, int k, int* colors,
                                                                     Outputs out) {
-  GridBarrier grid(&w.ctl->bar[1]);
+  GridBarrier grid(&w.ctl->bar1);
   __shared__ CtaQueues Q;
   cq_init(Q);
   stamp(w.ctl, 13);

@@ -28,34 +28,42 @@ enum ErrBits : int { kErrGraph = 1, kErrComponent = 2 };
 
 // Device-resident control block, zeroed by one memset node at the start of
 // every call (before the optional validation kernel).
+// Counters that are hit by atomics from many warps in the same kernel sit on
+// their own 128-byte lines (one L2 slice each), away from the polled barrier
+// counters and from each other.
 struct Control {
   int n_rounds;     // simplification rounds R (R8)
   int n_hidden;     // |hidden vertices|
-  int n_comp;       // components found (counted by the search kernel)
   int n_seed;       // component-search seeds listed in roots[]
-  int max_comp;     // largest component
-  int truncated;    // components whose search hit max_steps
   int err;          // ErrBits
   int done_blocks;  // last-block detection of the evaluation kernel
   int done_recover; // last-block detection of the recovery kernel (finalisation)
-  int max_steps_comp;        // largest per-component step count
-  int qcnt[3];               // simplification frontier sizes (rotating by round)
+  int n_levels;     // recovery levels (DAG depth + 1)
+  alignas(128) int qcnt[3];  // simplification frontier sizes (rotating by round)
   int rq[3];                 // recovery level sizes (rotating by level)
   int tcnt[3];               // ... the same, for the single-CTA tails (never read by other CTAs)
   int trq[3];
-  int n_levels;              // recovery levels (DAG depth + 1)
-  int n_heavy[2];            // exact mode: components handed to the warp-parallel search, per word class
-                             // (32-bit: hcomp[0..), 64-bit: hcomp[n-1], hcomp[n-2], ...; reset per search call)
-  int heavy_next[2];         // exact mode: next heavy component to take per word class (reset with n_heavy)
-  unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
-  unsigned long long steps;  // search nodes entered
-  unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)
-  unsigned bar[2];           // grid-barrier arrival counters of the two cooperative kernels
+  alignas(128) unsigned bar0;  // grid-barrier arrival counter of mpld_simplify_components
+  alignas(128) unsigned bar1;  // ... of mpld_recover
+  alignas(128) int n_comp;     // components found (counted by the discovery kernel)
+  int max_comp;                // largest component
+  alignas(128) int truncated;  // components whose search hit max_steps
+  int max_steps_comp;          // largest per-component step count
+  unsigned long long steps;    // search nodes entered
+  alignas(128) int n_heavy[2]; // exact mode: components handed to the warp-parallel search, per word class
+                               // (32-bit: hcomp[0..), 64-bit: hcomp[n-1], hcomp[n-2], ...; reset per search call)
+  int heavy_next[2];           // exact mode: next heavy component to take per word class (reset with n_heavy)
+  alignas(128) unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
+  alignas(128) unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)
   unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
   unsigned long long tr[32];  // diagnostics: per round / level start time (ns)
   int nr[32];                // diagnostics: per round / level frontier size
-  unsigned long long dbg[8];  // diagnostics: slowest search thread (cycles total/build/search, n, steps)
+  alignas(128) unsigned long long dbg[8];  // diagnostics (MPLD_DIAG builds): slowest discovery / search / heavy search
 };
+
+#ifndef MPLD_DIAG
+#define MPLD_DIAG 0  // per-warp diagnostics atomics (tools/kernel_times.py); off in production builds
+#endif
 
 // Grid-wide barrier for the cooperatively launched persistent kernels.  Each
 // CTA arrives once per barrier on a monotonically increasing counter and polls
