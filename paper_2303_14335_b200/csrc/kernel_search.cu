@@ -559,89 +559,270 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
   if (MPLD_DIAG && lane == 0 && d_cyc > 0) atomicMax(&ctl->dbg[0], (d_cyc << 16) | (d_n & 0xffffull));
 }
 
-// One warp per component of the pool: the budgeted sequential search on lane
-// 0 (the oracle's node order and budget, R7), then the colours.  Exact mode
-// hands components whose search exceeds the light budget to the CTA-parallel
+// The budgeted sequential search (the oracle's node order and budget, R7) of
+// one component per LANE: a warp takes 32 consecutive components of the pool
+// and every lane runs the DFS of dfs() on its own component (32-bit words,
+// components of <= 32 vertices), written branch-free so that the lanes issue
+// one instruction stream.  Masks and frames are [index][lane] in shared memory
+// (a lane only touches its own column).  Components of more than 32 vertices
+// are searched afterwards one at a time on lane 0 (64-bit words).  Exact mode
+// hands components whose search exceeds the light budget to the warp-parallel
 // kernel below.
+constexpr int kLaneWarps = 2;  // warps per CTA of the light search
+
+struct __align__(16) LaneLight {
+  unsigned A[32][32];       // adj[v][lane]
+  unsigned S[32][32];       // sadj[v][lane]
+  unsigned saved[32][32];   // frame d: B[c] before r(v,c) was selected
+  int cost[32][32];         // frame d: cost when the node was entered
+  int pk[32][32];           // frame d: v | (c+1) << 8 | (maxused+1) << 16
+  unsigned cl[16][32];      // clique masks (R7, k >= 4)
+};
+static_assert(sizeof(LaneLight) >= sizeof(WarpSearch), "the single-lane path reuses the lane storage");
+
+// the DFS of dfs() with a SeqIncumbent, one component per lane; returns the nodes entered
 template <int K>
-__global__ void __launch_bounds__(kCompWarps * 32, K >= 4 ? 6 : 8) mpld_exact_cover_search(GraphView g, Workspace w,
-                                                                                           int w_stitch,
-                                                                                           long long max_steps,
-                                                                                           int* colors,
-                                                                                           unsigned light_steps,
-                                                                                           long long* counts) {
-  __shared__ WarpSearch s_search[kCompWarps];
-  WarpSearch& s = s_search[threadIdx.x >> 5];
+__device__ unsigned lane_dfs(LaneLight& L, int lane, bool valid, int n, int w_stitch, unsigned budget, int ncl,
+                             unsigned (&bestC)[K], int& best, bool& trunc) {
+  using W = unsigned;
+  using O = WordOps<W>;
+  W C[K], B[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) C[c] = B[c] = bestC[c] = 0;
+  W U = valid ? O::full(n) : 0;
+  int cost = 0, maxused = -1, depth = 0;
+  best = INT_MAX;
+  trunc = false;
+  unsigned steps = 0;
+  bool active = valid, enter = valid;
+  W f_saved = 0, f_adj = 0, f_sadj = 0;
+  int f_cost = 0, f_v = 0, f_c = -1, f_mu = -1;
+  const W* cl = &L.cl[0][lane];
+  while (__any_sync(0xffffffffu, active)) {
+    const bool en = active && enter;
+    if (en && ++steps > budget && best != INT_MAX) {  // budget (R7): stop at exactly the oracle's node
+      trunc = true;
+      active = false;
+    }
+    {  // enter the pending node: leaf / prune / expand
+      W Z, Ol;
+      live_counts<K, W>(B, U, Z, Ol);
+      const int lb = cost + kCostUnits * bound_conflicts<K, W>(B, U, Z, cl, 32, ncl);
+      const bool leaf = U == 0;
+      const bool better = active && en && leaf && cost < best;  // Alg. 1 line 5, strict improvement
+      const bool ex = active && en && !leaf && lb < best;       // bound (R7)
+      if (better) {
+        best = cost;
+#pragma unroll
+        for (int c = 0; c < K; ++c) bestC[c] = C[c];
+      }
+      const int v = ex ? O::ffs(Z ? Z : (Ol ? Ol : U)) : 0;  // Alg. 1 line 8 (R5)
+      if (ex && depth > 0) {  // spill the parent frame
+        const int d = depth - 1;
+        L.saved[d][lane] = f_saved;
+        L.cost[d][lane] = f_cost;
+        L.pk[d][lane] = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16);
+      }
+      const W av = L.A[v][lane], sav = L.S[v][lane];
+      f_v = ex ? v : f_v;
+      f_c = ex ? -1 : f_c;
+      f_mu = ex ? maxused : f_mu;
+      f_cost = ex ? cost : f_cost;
+      f_adj = ex ? av : f_adj;
+      f_sadj = ex ? sav : f_sadj;
+      U = ex ? (U & ~(W(1) << v)) : U;  // cover column v (line 9)
+      depth += ex ? 1 : 0;
+    }
+    {  // advance the deepest frame: next row, or exhausted -> pop
+      const bool adv = active && depth > 0;
+      if (active && depth == 0) active = false;
+      const W bit = W(1) << f_v;
+      const bool unc = adv && f_c >= 0;  // uncover the previous row (line 17)
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        const bool mc = unc && c == f_c;
+        C[c] = mc ? (C[c] & ~bit) : C[c];
+        B[c] = mc ? f_saved : B[c];
+      }
+      const int c = f_c + 1;
+      const int fd = depth - 1;
+      const bool exh = adv && c > min(K - 1, f_mu + 1);  // rows exhausted (colour-symmetry limit R6)
+      const bool nxt = adv && !exh;
+      const int cc = min(c, K - 1);
+      const W Cc = pick<K, W>(C, cc), Bc = pick<K, W>(B, cc);
+      const int ncost = f_cost + kCostUnits * O::popc(f_adj & Cc) + w_stitch * O::popc(f_sadj & ~U & ~Cc);
+#pragma unroll
+      for (int q = 0; q < K; ++q) {  // select r(v,c) (line 14), cover its secondary columns (line 15)
+        const bool sel = nxt && q == cc;
+        C[q] = sel ? (C[q] | bit) : C[q];
+        B[q] = sel ? (B[q] | f_adj) : B[q];
+      }
+      f_saved = nxt ? Bc : f_saved;
+      cost = nxt ? ncost : cost;
+      maxused = nxt ? max(f_mu, c) : maxused;
+      U = exh ? (U | bit) : U;  // exhausted: uncover the column (line 20)
+      const bool pop = exh && fd > 0;
+      const int pd = max(fd - 1, 0);
+      const W ps = L.saved[pd][lane];
+      const int pc = L.cost[pd][lane], ppk = L.pk[pd][lane];
+      const int pv = pop ? (ppk & 0xff) : f_v;
+      const W pa = L.A[pv][lane], psa = L.S[pv][lane];
+      f_saved = pop ? ps : f_saved;
+      f_cost = pop ? pc : f_cost;
+      f_v = pv;
+      f_c = pop ? ((ppk >> 8) & 0xff) - 1 : (nxt ? c : f_c);
+      f_mu = pop ? ((ppk >> 16) & 0xff) - 1 : f_mu;
+      f_adj = pop ? pa : f_adj;
+      f_sadj = pop ? psa : f_sadj;
+      depth = exh ? fd : depth;
+      if (exh && fd == 0) active = false;
+      enter = nxt;
+    }
+  }
+  return steps;
+}
+
+// The component's epilogue: colours, Eq. (1b)/(1c) counts, statistics, hand-off.
+struct LightAcc {
+  unsigned long long steps = 0ull;
+  int maxsteps = 0;
+  unsigned trunc = 0;
+};
+
+__device__ __forceinline__ void light_handoff(const GraphView& g, const Workspace& w, int ci, int n, int best_cost) {
+  const int cls = n > 32 ? 1 : 0;
+  const int h = atomicAdd(&w.ctl->n_heavy[cls], 1);
+  const int idx = cls ? g.n - 1 - h : h;
+  w.hcomp[idx] = ci;
+  w.hcost[idx] = best_cost;
+}
+
+// One component of more than 32 vertices on lane 0 of the warp (64-bit words).
+template <int K>
+__device__ void light_single(const GraphView& g, const Workspace& w, WarpSearch& s, int ci, int w_stitch,
+                             unsigned budget, bool exact, int* colors, long long* counts, LightAcc& acc) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long rec = __ldcg(&w.crec[ci]);
+  const size_t off = (size_t)(rec >> 8);
+  const int n = (int)(rec & 0xffull);
+  for (int i = lane; i < n; i += 32) {
+    const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
+    s.adj[i] = m.x;
+    s.sadj[i] = m.y;
+  }
+  __syncwarp();
+  unsigned steps = 0;
+  bool trunc = false;
+  int best_cost = 0;
+  if (lane == 0) steps = comp_dfs<K, unsigned long long>(s, n, w_stitch, budget, best_cost, trunc);
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) colors[__ldcg(&w.porder[off + i])] = colour_of_mask<K>(s.cl, i);
+  trunc = __shfl_sync(0xffffffffu, trunc, 0);
+  if (counts && !(trunc && exact)) {
+    int nc = 0, ns = 0;
+    for (int i = lane; i < n; i += 32) {
+      const unsigned long long Ci = s.cl[colour_of_mask<K>(s.cl, i)];
+      nc += __popcll(s.adj[i] & Ci);
+      ns += __popcll(s.sadj[i] & ~Ci);
+    }
+    add_counts(g, __ldcg(&w.porder[off]), nc, ns, counts);
+  }
+  if (lane == 0) {
+    if (trunc && exact) {
+      light_handoff(g, w, ci, n, best_cost);
+    } else {
+      acc.maxsteps = max(acc.maxsteps, (int)min(steps, (unsigned)INT_MAX));
+      acc.trunc += trunc ? 1 : 0;
+    }
+    acc.steps += steps;
+  }
+  __syncwarp();
+}
+
+template <int K>
+__global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
+                                                                           long long max_steps, int* colors,
+                                                                           unsigned light_steps, long long* counts) {
+  __shared__ LaneLight s_lane[kLaneWarps];
+  LaneLight& L = s_lane[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   Control* ctl = w.ctl;
   const int n_comp = __ldcg(&ctl->err) ? 0 : (int)(__ldcg(&ctl->comp_pool) >> 32);
   const bool exact = max_steps <= 0;
   const unsigned budget = exact ? light_steps
                                 : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
-  unsigned long long acc_steps = 0ull;  // statistics, accumulated on lane 0
-  int acc_maxsteps = 0;
-  unsigned acc_trunc = 0;
-  unsigned long long d_cyc = 0ull, d_n = 0ull, d_steps = 0ull;  // diagnostics: slowest component of this warp
-  const int nw = gridDim.x * kCompWarps;
-  for (int ci = blockIdx.x * kCompWarps + (threadIdx.x >> 5); ci < n_comp; ci += nw) {
-    const long long c0 = clock64();
-    const unsigned long long rec = __ldcg(&w.crec[ci]);
+  LightAcc acc;  // this lane's statistics
+  const int nb = gridDim.x * kLaneWarps;
+  for (int b = blockIdx.x * kLaneWarps + (threadIdx.x >> 5); b * 32 < n_comp; b += nb) {
+    const int ci = b * 32 + lane;
+    unsigned long long rec = 0ull;
+    if (ci < n_comp) rec = __ldcg(&w.crec[ci]);
     const size_t off = (size_t)(rec >> 8);
     const int n = (int)(rec & 0xffull);
-    for (int i = lane; i < n; i += 32) {
-      const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
-      s.adj[i] = m.x;
-      s.sadj[i] = m.y;
-    }
-    __syncwarp();
-    unsigned steps = 0;
-    bool trunc = false;
+    const bool valid = ci < n_comp && n <= 32;
+    if (valid)
+      for (int i = 0; i < n; ++i) {
+        const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
+        L.A[i][lane] = (unsigned)m.x;
+        L.S[i][lane] = (unsigned)m.y;
+      }
+    const int ncl = valid && clique_min<K>() ? clique_partition<unsigned>(&L.A[0][lane], 32, n, &L.cl[0][lane], 32,
+                                                                           clique_min<K>())
+                                             : 0;
+    unsigned bestC[K];
     int best_cost = 0;
-    if (lane == 0) {
-      if (n <= 32)
-        steps = comp_dfs<K, unsigned>(s, n, w_stitch, budget, best_cost, trunc);
-      else
-        steps = comp_dfs<K, unsigned long long>(s, n, w_stitch, budget, best_cost, trunc);
-    }
-    __syncwarp();
-    for (int i = lane; i < n; i += 32) colors[__ldcg(&w.porder[off + i])] = colour_of_mask<K>(s.cl, i);
-    trunc = __shfl_sync(0xffffffffu, trunc, 0);
-    if (counts && !(trunc && exact)) {  // final colouring: Eq. (1b)/(1c) counts of the component
-      int nc = 0, ns = 0;
-      for (int i = lane; i < n; i += 32) {
-        const unsigned long long Ci = s.cl[colour_of_mask<K>(s.cl, i)];
-        nc += __popcll(s.adj[i] & Ci);
-        ns += __popcll(s.sadj[i] & ~Ci);
-      }
-      add_counts(g, __ldcg(&w.porder[off]), nc, ns, counts);
-    }
-    if (lane == 0) {
-      if (trunc && exact) {  // hand the component to the warp-parallel search of its word class
-        const int cls = n > 32 ? 1 : 0;
-        const int h = atomicAdd(&ctl->n_heavy[cls], 1);
-        const int idx = cls ? g.n - 1 - h : h;
-        w.hcomp[idx] = ci;
-        w.hcost[idx] = best_cost;
+    bool trunc = false;
+    const unsigned steps = lane_dfs<K>(L, lane, valid, n, w_stitch, budget, ncl, bestC, best_cost, trunc);
+    if (valid) {
+      for (int i = 0; i < n; ++i) colors[__ldcg(&w.porder[off + i])] = colour_of<K, unsigned>(bestC, i);
+      if (trunc && exact) {
+        light_handoff(g, w, ci, n, best_cost);
       } else {
-        acc_maxsteps = max(acc_maxsteps, (int)min(steps, (unsigned)INT_MAX));
-        acc_trunc += trunc ? 1 : 0;
+        if (counts) {  // final colouring: Eq. (1b)/(1c) counts of the component
+          int nc = 0, ns = 0;
+          for (int i = 0; i < n; ++i) {
+            const unsigned Ci = pick<K, unsigned>(bestC, colour_of<K, unsigned>(bestC, i));
+            nc += __popc(L.A[i][lane] & Ci);
+            ns += __popc(L.S[i][lane] & ~Ci);
+          }
+          nc >>= 1;
+          ns >>= 1;
+          if (nc | ns) {
+            const int l = layout_of(g, __ldcg(&w.porder[off]));
+            if (nc) atomicAdd((unsigned long long*)&counts[2 * l], (unsigned long long)nc);
+            if (ns) atomicAdd((unsigned long long*)&counts[2 * l + 1], (unsigned long long)ns);
+          }
+        }
+        acc.maxsteps = max(acc.maxsteps, (int)min(steps, (unsigned)INT_MAX));
+        acc.trunc += trunc ? 1 : 0;
       }
-      acc_steps += steps;
-      const unsigned long long cyc = (unsigned long long)(clock64() - c0);
-      if (cyc > d_cyc) {
-        d_cyc = cyc;
-        d_n = n;
-        d_steps = steps;
-      }
+      acc.steps += steps;
+    }
+    // components of more than 32 vertices: one at a time on lane 0
+    unsigned big = __ballot_sync(0xffffffffu, ci < n_comp && n > 32);
+    __syncwarp();
+    while (big) {
+      const int l = __ffs(big) - 1;
+      big &= big - 1;
+      light_single<K>(g, w, *reinterpret_cast<WarpSearch*>(&L), b * 32 + l, w_stitch, budget, exact, colors, counts,
+                      acc);
     }
     __syncwarp();
   }
-  if (MPLD_DIAG && lane == 0 && d_cyc > 0)  // diagnostics: cycles << 24 | steps << 8 | n
-    atomicMax(&ctl->dbg[2], (d_cyc << 24) | (min(d_steps, 0xffffull) << 8) | (d_n & 0xffull));
-  if (lane == 0 && acc_steps) {
-    atomicAdd(&ctl->steps, acc_steps);
-    atomicMax(&ctl->max_steps_comp, acc_maxsteps);
-    if (acc_trunc) atomicAdd(&ctl->truncated, (int)acc_trunc);
+  // statistics: one atomic per warp
+  unsigned long long st = acc.steps;
+  int mx = acc.maxsteps;
+  unsigned tr = acc.trunc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    st += __shfl_xor_sync(0xffffffffu, st, o);
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  }
+  if (lane == 0 && st) {
+    atomicAdd(&ctl->steps, st);
+    atomicMax(&ctl->max_steps_comp, mx);
+    if (tr) atomicAdd(&ctl->truncated, (int)tr);
   }
 }
 
@@ -1144,15 +1325,15 @@ cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch,
                           unsigned light_steps, long long* counts, cudaStream_t s, int blocks) {
   switch (k) {
     case 2:
-      mpld_exact_cover_search<2><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
+      mpld_exact_cover_search<2><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
                                                                      counts);
       break;
     case 3:
-      mpld_exact_cover_search<3><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
+      mpld_exact_cover_search<3><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
                                                                      counts);
       break;
     case 4:
-      mpld_exact_cover_search<4><<<blocks, kCompWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
+      mpld_exact_cover_search<4><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
                                                                      counts);
       break;
     default: return cudaErrorInvalidValue;
@@ -1214,7 +1395,7 @@ int resident_blocks_discover(int num_sms) {
 int resident_blocks_search(int threads, int num_sms) {
   (void)threads;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4>, kCompWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4>, kLaneWarps * 32, 0);
   return per_sm * num_sms;
 }
 
