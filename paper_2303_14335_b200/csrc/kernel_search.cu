@@ -855,6 +855,15 @@ constexpr int kDonateMinLevels = MPLD_DONATE_MIN_LEVELS;  // a frame is donated 
 #define MPLD_STEAL_MIN_IDLE 8
 #endif
 constexpr int kStealMinIdle = MPLD_STEAL_MIN_IDLE;  // donation rounds only when at least this many lanes are idle
+#ifndef MPLD_SPILL
+#define MPLD_SPILL 1
+#endif
+#ifndef MPLD_QUEUE_LOW
+#define MPLD_QUEUE_LOW 64
+#endif
+constexpr int kQueueLow = MPLD_QUEUE_LOW;  // the work queue is fed while it holds fewer items than this
+constexpr unsigned kSpillCheck = 64;  // spill / slot-sync checks every this many iterations (power of two),
+                                      // from Workspace::spill_iters on
 
 struct Path {  // levels 0..31 in a, 32..63 in b; 2 bits per level, level 0 most significant
   unsigned long long a, b;
@@ -956,38 +965,73 @@ __host__ __device__ constexpr size_t heavy_smem() {
   return 3 * kMaxComp * sizeof(W) + sizeof(LaneFrames<K, W, heavy_depth<K, W>()>);
 }
 
+// One work unit of the warp-parallel search: the subtree of one node (the root
+// of a heavy component, or a spilled work item) searched by the warp's 32
+// lanes with work donation.  The incumbent key (gcost, gP) is in/out; on
+// return `mine` marks the lane that recorded the best leaf (bestC).  A unit
+// that runs past kSpillIters iterations hands its open work to the work queue
+// (`spilled`).
 template <int K, typename W>
-__device__ void warp_heavy_search(int n, const W* __restrict__ adj, const W* __restrict__ sadj, const W* cl,
-                                  int ncl, LaneFrames<K, W, heavy_depth<K, W>()>& F, int w_stitch, int c1,
-                                  const Path& p1, const int* porder, int* colors, Control* ctl, W (&fin)[K],
-                                  int* slot, unsigned& iters, unsigned& steal_rounds) {
+struct HeavyUnit {
+  int n, ncl, w_stitch, cls, ci;
+  int slot;  // spilled component's slot, -1 before the first spill
+  const W* adj;
+  const W* sadj;
+  const W* cl;
+  LaneFrames<K, W, heavy_depth<K, W>()>* F;
+  int* pair;  // 32 ints: donor pairing table
+  int c1;     // the light phase's leaf: key and colour masks (component units; slot initialisation)
+  Path p1;
+  W col[K];
+};
+
+__device__ __forceinline__ void slot_lock(HeavySlot* s) {
+  while (atomicCAS(&s->lock, 0, 1) != 0) __nanosleep(32);
+  __threadfence();
+}
+__device__ __forceinline__ void slot_unlock(HeavySlot* s) {
+  __threadfence();
+  atomicExch(&s->lock, 0);
+}
+
+template <int K, typename W>
+__device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const W (&sC)[K], const W (&sB)[K], W sU,
+                                  int scost, int smu, Path sP, int sdepth, int& gcost, Path& gP, bool& mine,
+                                  W (&bestC)[K], unsigned& steps_out, bool& capped_out, bool& spilled) {
   using O = WordOps<W>;
   constexpr bool kTwo = sizeof(W) == 8;
   const int lane = threadIdx.x & 31;
+  const int n = u.n, ncl = u.ncl, w_stitch = u.w_stitch;
+  const W* __restrict__ adj = u.adj;
+  const W* __restrict__ sadj = u.sadj;
+  const W* cl = u.cl;
+  auto& F = *u.F;
+  int* slot = u.pair;
   const unsigned long long donatable = (n - kDonateMinLevels) >= 64 ? ~0ull
                                        : (n - kDonateMinLevels <= 0 ? 0ull : ((1ull << (n - kDonateMinLevels)) - 1ull));
-  iters = steal_rounds = 0;
+  unsigned iters = 0;
+  spilled = false;
   // lane DFS state: the node (C, B, U, cost, maxused) and its path P; frames
   // d0..depth-1, the deepest in registers; open bit d = frame d has an untried
-  // child beyond its current one
-  W C[K], B[K], U = O::full(n);
+  // child beyond its current one.  Lane 0 starts at the unit's node.
+  W C[K], B[K], U = lane == 0 ? sU : W(0);
 #pragma unroll
-  for (int c = 0; c < K; ++c) C[c] = B[c] = 0;
-  int cost = 0, maxused = -1, depth = 0, d0 = 0;
+  for (int c = 0; c < K; ++c) {
+    C[c] = lane == 0 ? sC[c] : W(0);
+    B[c] = lane == 0 ? sB[c] : W(0);
+  }
+  int cost = scost, maxused = smu, depth = sdepth, d0 = sdepth;
   bool active = lane == 0, enter = lane == 0;
   W fB[K], fU = 0, f_adj = 0, f_sadj = 0;
 #pragma unroll
   for (int c = 0; c < K; ++c) fB[c] = 0;
   int f_cost = 0, f_v = 0, f_c = -1, f_mu = -1, f_lim = 0;
-  Path P = {0ull, 0ull};
+  Path P = sP;
   unsigned long long open = 0ull;
   // incumbent: the warp's best key (identical in every lane); a lane records a
   // leaf only if it beats it, so only the lane that found the current best
   // holds colours for it
-  int gcost = c1;
-  Path gP = p1;
-  bool mine = false;
-  W bestC[K];
+  mine = false;
 #pragma unroll
   for (int c = 0; c < K; ++c) bestC[c] = 0;
   unsigned steps = 0;
@@ -996,10 +1040,154 @@ __device__ void warp_heavy_search(int n, const W* __restrict__ adj, const W* __r
     const unsigned act = __ballot_sync(0xffffffffu, active);
     if (act == 0u) break;
     ++iters;
+    if (MPLD_SPILL && iters >= w.spill_iters && (iters & (kSpillCheck - 1)) == 0) {
+      // share the best key with the other units of a spilled component
+      if (u.slot >= 0) {
+        const unsigned owner = __ballot_sync(0xffffffffu, mine);
+        const int src = owner ? __ffs(owner) - 1 : 0;
+        W oc[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) oc[c] = __shfl_sync(0xffffffffu, bestC[c], src);
+        int adopt = 0;
+        Path sp = gP;
+        int sc = gcost;
+        if (lane == 0) {
+          HeavySlot* hs = &w.hslot[u.slot];
+          slot_lock(hs);
+          const Path cur = {__ldcg(&hs->pa), __ldcg(&hs->pb)};
+          const int cc = __ldcg(&hs->cost);
+          if (owner && key_less<kTwo>(gcost, gP, cc, cur)) {
+            hs->cost = gcost;
+            hs->pa = gP.a;
+            hs->pb = gP.b;
+#pragma unroll
+            for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)oc[c];
+          } else if (key_less<kTwo>(cc, cur, gcost, gP)) {
+            adopt = 1;
+            sc = cc;
+            sp = cur;
+          }
+          slot_unlock(hs);
+        }
+        adopt = __shfl_sync(0xffffffffu, adopt, 0);
+        if (owner) mine = false;  // the slot holds this unit's best (or a better one) now
+        if (adopt) {
+          gcost = __shfl_sync(0xffffffffu, sc, 0);
+          gP.a = __shfl_sync(0xffffffffu, sp.a, 0);
+          gP.b = __shfl_sync(0xffffffffu, sp.b, 0);
+        }
+      }
+      // feed the work queue when it runs low: every lane gives away the untried
+      // children of its shallowest open frame (the largest subtrees it holds)
+      int hungry = 0;
+      if (lane == 0)
+        hungry = *(volatile int*)&w.ctl->wq_tail[u.cls] - *(volatile int*)&w.ctl->wq_head[u.cls] < kQueueLow;
+      if (__shfl_sync(0xffffffffu, hungry, 0)) {
+        int cnt = 0, j = -1;
+        if (active && (open & donatable)) {
+          j = __ffsll((long long)(open & donatable)) - 1;
+          const int pk = j == depth - 1 ? (f_c + 1) << 8 | (f_lim << 24) : F.pk[j][lane];
+          cnt = (pk >> 24) - (((pk >> 8) & 0xff) - 1);
+        }
+        int tot = 0;
+        const int excl = warp_excl_scan(cnt, tot);
+        int base = -1;
+        if (lane == 0 && tot > 0) {
+          if (u.slot < 0) {  // the component's first spill: a slot holding the light leaf, one unit pending (this)
+            const int sl = atomicAdd(&w.ctl->slot_next, 1);
+            if (sl < kSlots) {
+              HeavySlot* hs = &w.hslot[sl];
+              hs->lock = 0;
+              hs->pend = 1;
+              hs->cost = hs->lcost = u.c1;
+              hs->pa = hs->lpa = u.p1.a;
+              hs->pb = hs->lpb = u.p1.b;
+#pragma unroll
+              for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)u.col[c];
+              hs->ci = u.ci;
+              __threadfence();
+              u.slot = sl;
+            }
+          }
+          if (u.slot >= 0) {
+            int t = *(volatile int*)&w.ctl->wq_tail[u.cls];
+            while (t + tot <= kWQCap) {
+              const int o = atomicCAS(&w.ctl->wq_tail[u.cls], t, t + tot);
+              if (o == t) {
+                base = t;
+                break;
+              }
+              t = o;
+            }
+            if (base >= 0) atomicAdd(&w.hslot[u.slot].pend, tot);  // before any item is published
+          }
+        }
+        u.slot = __shfl_sync(0xffffffffu, u.slot, 0);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= 0 && cnt > 0) {
+          WorkItem* q = w.wq + (size_t)u.cls * kWQCap;
+          unsigned* qf = w.wq_flag + (size_t)u.cls * kWQCap;
+          int at = base + excl;
+          W jB[K], jU;
+          int pk, jc;
+          if (j == depth - 1) {
+#pragma unroll
+            for (int c = 0; c < K; ++c) jB[c] = fB[c];
+            jU = fU;
+            jc = f_cost;
+            pk = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
+            f_lim = f_c;  // its children are in the queue now
+          } else {
+#pragma unroll
+            for (int c = 0; c < K; ++c) jB[c] = F.B[c][j][lane];
+            jU = F.U[j][lane];
+            jc = F.cost[j][lane];
+            pk = F.pk[j][lane];
+            F.pk[j][lane] = (pk & 0x00ffffff) | ((((pk >> 8) & 0xff) - 1) << 24);
+          }
+          open &= ~(1ull << j);
+          const int v = pk & 0xff, cj = ((pk >> 8) & 0xff) - 1, mu = ((pk >> 16) & 0xff) - 1, lim = pk >> 24;
+          const W bit = W(1) << v;
+          const W a = adj[v], sa = sadj[v];
+          for (int ch = cj + 1; ch <= lim; ++ch) {  // the untried children of frame j (C at N_j = C & ~U_j)
+            W xC[K], xB[K];
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+              xC[c] = C[c] & ~jU;
+              xB[c] = jB[c];
+            }
+            const W xU = jU & ~bit;
+            const W Cc = pick<K, W>(xC, ch);
+            const int xcost = jc + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~xU & ~Cc);
+            put<K, W>(xC, ch, Cc | bit);
+            put<K, W>(xB, ch, pick<K, W>(xB, ch) | a);
+            Path xP = path_prefix<kTwo>(P, j);
+            path_put<kTwo>(xP, j, ch);
+            WorkItem& it = q[at];
+            it.slot = u.slot;
+            it.depth = j + 1;
+            it.cost = xcost;
+            it.mu = max(mu, ch);
+            it.pa = xP.a;
+            it.pb = xP.b;
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+              it.C[c] = (unsigned long long)xC[c];
+              it.B[c] = (unsigned long long)xB[c];
+            }
+            it.U = (unsigned long long)xU;
+            __threadfence();
+            *(volatile unsigned*)&qf[at] = w.epoch;
+            ++at;
+          }
+        }
+        if (base >= 0) spilled = true;
+      }
+    }
     if (__popc(~act) >= kStealMinIdle) {  // work donation: the i-th idle lane takes a node from the i-th donor
       const unsigned don = __ballot_sync(0xffffffffu, active && (open & donatable) != 0ull);
       if (don) {
-        ++steal_rounds;
+
         const unsigned idle = ~act;
         const int np = min(__popc(don), __popc(idle));
         const unsigned lt = lanemask_lt();
@@ -1186,21 +1374,8 @@ __device__ void warp_heavy_search(int n, const W* __restrict__ adj, const W* __r
   unsigned tot = steps;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-  const bool any_capped = __any_sync(0xffffffffu, capped);
-  // the best key beats the light phase's leaf iff some lane recorded a leaf;
-  // the lane that recorded the final best writes the colours
-  const unsigned owner = __ballot_sync(0xffffffffu, mine);
-  if (owner && key_less<kTwo>(gcost, gP, c1, p1)) {
-    const int win = __ffs(owner) - 1;
-#pragma unroll
-    for (int c = 0; c < K; ++c) fin[c] = __shfl_sync(0xffffffffu, bestC[c], win);
-    for (int i = lane; i < n; i += 32) colors[__ldcg(&porder[i])] = colour_of<K, W>(fin, i);
-  }
-  if (lane == 0) {
-    if (any_capped) atomicAdd(&ctl->truncated, 1);
-    atomicAdd(&ctl->steps, (unsigned long long)tot);
-    atomicMax(&ctl->max_steps_comp, (int)min(tot, (unsigned)INT_MAX));
-  }
+  steps_out = tot;
+  capped_out = __any_sync(0xffffffffu, capped);
 }
 
 // the path of the leaf whose colours are col (a leaf of the canonical tree:
@@ -1225,17 +1400,62 @@ __device__ __forceinline__ Path leaf_path(const W (&col)[K], int n, const W* adj
   return P;
 }
 
+// Eq. (1b)/(1c) counts of a component's final colouring (whole warp)
 template <int K, typename W>
-__device__ unsigned long long heavy_component(const GraphView& g, int n, size_t off, const Workspace& w,
-                                              unsigned char* smem, int w_stitch, int c1, int* colors,
-                                              long long* counts) {
+__device__ __forceinline__ void heavy_counts(const GraphView& g, const W* adj, const W* sadj, int n, const W (&fin)[K],
+                                             int v0, long long* counts) {
+  if (!counts) return;
+  int nc = 0, ns = 0;
+  for (int i = threadIdx.x & 31; i < n; i += 32) {
+    const W Ci = pick<K, W>(fin, colour_of<K, W>(fin, i));
+    nc += WordOps<W>::popc(adj[i] & Ci);
+    ns += WordOps<W>::popc(sadj[i] & ~Ci);
+  }
+  add_counts(g, v0, nc, ns, counts);
+}
+
+// The end of a unit of a spilled component: merge the unit's best leaf into
+// the slot; the last unit of the component writes its colours and counts.
+template <int K, typename W>
+__device__ void heavy_unit_done(const GraphView& g, const Workspace& w, const HeavyUnit<K, W>& u, int gcost,
+                                const Path& gP, bool mine, const W (&bestC)[K], const int* porder, int* colors,
+                                long long* counts) {
+  constexpr bool kTwo = sizeof(W) == 8;
   const int lane = threadIdx.x & 31;
-  W* s_adj = (W*)smem;
-  W* s_sadj = s_adj + kMaxComp;
-  W* s_cl = s_sadj + kMaxComp;
-  auto& F = *(LaneFrames<K, W, heavy_depth<K, W>()>*)(smem + 3 * kMaxComp * sizeof(W));
-  const int* porder = w.porder + off;
-  W col[K];
+  const unsigned owner = __ballot_sync(0xffffffffu, mine);
+  const int src = owner ? __ffs(owner) - 1 : 0;
+  W oc[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) oc[c] = __shfl_sync(0xffffffffu, bestC[c], src);
+  HeavySlot* hs = &w.hslot[u.slot];
+  int last = 0;
+  if (lane == 0) {
+    slot_lock(hs);
+    const Path cur = {__ldcg(&hs->pa), __ldcg(&hs->pb)};
+    if (owner && key_less<kTwo>(gcost, gP, __ldcg(&hs->cost), cur)) {
+      hs->cost = gcost;
+      hs->pa = gP.a;
+      hs->pb = gP.b;
+#pragma unroll
+      for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)oc[c];
+    }
+    slot_unlock(hs);
+    last = atomicSub(&hs->pend, 1) == 1;
+    __threadfence();
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  W fin[K];  // the component's final colouring
+#pragma unroll
+  for (int c = 0; c < K; ++c) fin[c] = (W)__ldcg(&hs->C[c]);
+  for (int i = lane; i < u.n; i += 32) colors[__ldcg(&porder[i])] = colour_of<K, W>(fin, i);
+  heavy_counts<K, W>(g, u.adj, u.sadj, u.n, fin, __ldcg(&porder[0]), counts);
+}
+
+// A heavy component's pool record -> shared memory (masks, clique partition).
+template <int K, typename W>
+__device__ void heavy_load(const Workspace& w, size_t off, int n, W* s_adj, W* s_sadj, W* s_cl, int& ncl,
+                           const int* colors, W (&col)[K]) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int c = 0; c < K; ++c) col[c] = 0;
   for (int i0 = 0; i0 < n; i0 += 32) {
@@ -1245,7 +1465,7 @@ __device__ unsigned long long heavy_component(const GraphView& g, int n, size_t 
       const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
       s_adj[i] = (W)m.x;
       s_sadj[i] = (W)m.y;
-      ci = __ldcg(&colors[__ldcg(&porder[i])]);  // the light phase's best leaf
+      if (colors) ci = __ldcg(&colors[__ldcg(&w.porder[off + i])]);  // the light phase's best leaf
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) {
@@ -1254,63 +1474,167 @@ __device__ unsigned long long heavy_component(const GraphView& g, int n, size_t 
     }
   }
   __syncwarp();
-  const int ncl = heavy_clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, heavy_clique_min<K>()) : 0;
+  ncl = heavy_clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, heavy_clique_min<K>()) : 0;
   __syncwarp();
-  int lc = 0;  // == c1 (the light phase's best cost)
-  const Path p1 = leaf_path<K, W>(col, n, s_adj, s_sadj, w_stitch, lc);
-  unsigned iters, steals;
-  W fin[K];  // the final colouring: the light leaf unless the search beats it
-#pragma unroll
-  for (int c = 0; c < K; ++c) fin[c] = col[c];
-  __shared__ int s_slot[32];  // donor lanes by rank (work donation)
-  warp_heavy_search<K, W>(n, s_adj, s_sadj, s_cl, ncl, F, w_stitch, c1, p1, porder, colors, w.ctl, fin, s_slot,
-                          iters, steals);
-  if (counts) {
-    int nc = 0, ns = 0;
-    for (int i = lane; i < n; i += 32) {
-      const W Ci = pick<K, W>(fin, colour_of<K, W>(fin, i));
-      nc += WordOps<W>::popc(s_adj[i] & Ci);
-      ns += WordOps<W>::popc(s_sadj[i] & ~Ci);
-    }
-    add_counts(g, __ldcg(&porder[0]), nc, ns, counts);
-  }
-  __syncwarp();
-  return (unsigned long long)iters << 32 | steals;
 }
 
 // One warp per heavy component of one word class: W = 32-bit words for
-// components of <= 32 vertices, 64-bit words for larger ones (the frames of
-// the 64-bit class are twice as deep and wide, so each class gets its own
-// launch with its own shared-memory size).
+// components of <= 32 vertices, 64-bit words for larger ones (each class gets
+// its own launch with its own shared-memory size).  Warps take heavy
+// components first, then spilled work items, until every unit is done.
 template <int K, typename W>
 __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
                                                                     int* colors, long long* counts) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int cls = sizeof(W) == 4 ? 0 : 1;
+  constexpr bool kTwo = sizeof(W) == 8;
+  __shared__ int s_pair[32];
+  const int lane = threadIdx.x & 31;
   Control* ctl = w.ctl;
   const int n_heavy = __ldcg(&ctl->n_heavy[cls]);
-  const long long t0 = clock64();
+  W* s_adj = (W*)smem;
+  W* s_sadj = s_adj + kMaxComp;
+  W* s_cl = s_sadj + kMaxComp;
+  auto* F = (LaneFrames<K, W, heavy_depth<K, W>()>*)(smem + 3 * kMaxComp * sizeof(W));
+  unsigned long long acc_steps = 0ull;
+  int acc_max = 0, acc_capped = 0;
+  bool comps_left = n_heavy > 0;
+  unsigned backoff = 64;
   while (true) {
-    int h = 0;
-    if (threadIdx.x == 0 && n_heavy) h = atomicAdd(&ctl->heavy_next[cls], 1);  // dynamic schedule over the list
-    h = __shfl_sync(0xffffffffu, h, 0);
-    if (h >= n_heavy) break;
-    const int idx = cls ? g.n - 1 - h : h;
-    const unsigned long long rec = __ldcg(&w.crec[__ldcg(&w.hcomp[idx])]);
-    const int n = (int)(rec & 0xffull);
-    const int c1 = __ldcg(&w.hcost[idx]);
-    const size_t off = (size_t)(rec >> 8);
-    const long long c0 = clock64();
-    const unsigned long long is = heavy_component<K, W>(g, n, off, w, smem, w_stitch, c1, colors, counts);
-    if (MPLD_DIAG && threadIdx.x == 0) {  // diagnostics (racy by design): slowest component, size, iterations, steals
-      const unsigned long long cyc = (unsigned long long)(clock64() - c0);
-      if (cyc > ctl->dbg[5]) {
-        atomicMax(&ctl->dbg[5], cyc);
-        ctl->dbg[7] = (unsigned long long)n | ((is >> 32) << 8) | ((is & 0xffffffull) << 40);
+    HeavyUnit<K, W> u;
+    u.w_stitch = w_stitch;
+    u.cls = cls;
+    u.adj = s_adj;
+    u.sadj = s_sadj;
+    u.cl = s_cl;
+    u.F = F;
+    u.pair = s_pair;
+    int gcost;
+    Path gP;
+    bool mine, capped, spilled;
+    unsigned steps;
+    W bestC[K];
+    if (comps_left) {  // a heavy component: the light leaf is the starting incumbent
+      int h = 0;
+      if (lane == 0) h = atomicAdd(&ctl->heavy_next[cls], 1);
+      h = __shfl_sync(0xffffffffu, h, 0);
+      if (h < n_heavy) {
+        const int idx = cls ? g.n - 1 - h : h;
+        u.ci = __ldcg(&w.hcomp[idx]);
+        const unsigned long long rec = __ldcg(&w.crec[u.ci]);
+        const size_t off = (size_t)(rec >> 8);
+        u.n = (int)(rec & 0xffull);
+        u.c1 = __ldcg(&w.hcost[idx]);
+        u.slot = -1;
+        heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, colors, u.col);
+        int lc = 0;  // == c1
+        u.p1 = leaf_path<K, W>(u.col, u.n, s_adj, s_sadj, w_stitch, lc);
+        gcost = u.c1;
+        gP = u.p1;
+        W zero[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) zero[c] = 0;
+        warp_heavy_search<K, W>(u, w, zero, zero, WordOps<W>::full(u.n), 0, -1, Path{0ull, 0ull}, 0, gcost, gP,
+                                mine, bestC, steps, capped, spilled);
+        const int* porder = w.porder + off;
+        if (u.slot < 0) {  // searched whole: the final colouring is the warp's best (or the light leaf)
+          W fin[K];
+#pragma unroll
+          for (int c = 0; c < K; ++c) fin[c] = u.col[c];
+          const unsigned owner = __ballot_sync(0xffffffffu, mine);
+          if (owner && key_less<kTwo>(gcost, gP, u.c1, u.p1)) {
+#pragma unroll
+            for (int c = 0; c < K; ++c) fin[c] = __shfl_sync(0xffffffffu, bestC[c], __ffs(owner) - 1);
+            for (int i = lane; i < u.n; i += 32) colors[__ldcg(&porder[i])] = colour_of<K, W>(fin, i);
+          }
+          heavy_counts<K, W>(g, s_adj, s_sadj, u.n, fin, __ldcg(&porder[0]), counts);
+        } else {
+          heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, porder, colors, counts);
+        }
+        acc_steps += steps;
+        acc_max = max(acc_max, (int)min(steps, (unsigned)INT_MAX));
+        acc_capped += capped ? 1 : 0;  // per unit (a spilled component may count more than once)
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(&ctl->wq_done[cls], 1);
+        }
+        continue;
       }
+      comps_left = false;
     }
+    // a spilled work item
+    int it = -1;
+    if (lane == 0) {
+      const int hd = *(volatile int*)&ctl->wq_head[cls];
+      if (hd < *(volatile int*)&ctl->wq_tail[cls] && atomicCAS(&ctl->wq_head[cls], hd, hd + 1) == hd) it = hd;
+    }
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= 0) {
+      backoff = 64;
+      if (lane == 0)
+        while (*(volatile unsigned*)&w.wq_flag[(size_t)cls * kWQCap + it] != w.epoch) {
+        }
+      __syncwarp();
+      __threadfence();
+      const WorkItem* q = w.wq + (size_t)cls * kWQCap + it;
+      u.slot = __ldcg(&q->slot);
+      HeavySlot* hs = &w.hslot[u.slot];
+      u.ci = __ldcg(&hs->ci);
+      const unsigned long long rec = __ldcg(&w.crec[u.ci]);
+      const size_t off = (size_t)(rec >> 8);
+      u.n = (int)(rec & 0xffull);
+      heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, nullptr, u.col);
+      W sC[K], sB[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        sC[c] = (W)__ldcg(&q->C[c]);
+        sB[c] = (W)__ldcg(&q->B[c]);
+      }
+      const Path sP = {__ldcg(&q->pa), __ldcg(&q->pb)};
+      int sc = 0;  // the slot's key as the starting incumbent
+      Path sk = {0ull, 0ull};
+      if (lane == 0) {
+        slot_lock(hs);
+        sc = __ldcg(&hs->cost);
+        sk.a = __ldcg(&hs->pa);
+        sk.b = __ldcg(&hs->pb);
+        slot_unlock(hs);
+      }
+      gcost = __shfl_sync(0xffffffffu, sc, 0);
+      gP.a = __shfl_sync(0xffffffffu, sk.a, 0);
+      gP.b = __shfl_sync(0xffffffffu, sk.b, 0);
+      warp_heavy_search<K, W>(u, w, sC, sB, (W)__ldcg(&q->U), __ldcg(&q->cost), __ldcg(&q->mu), sP,
+                              __ldcg(&q->depth), gcost, gP, mine, bestC, steps, capped, spilled);
+      heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, w.porder + off, colors, counts);
+      acc_steps += steps;
+      acc_capped += capped ? 1 : 0;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(&ctl->wq_done[cls], 1);
+      }
+      continue;
+    }
+    // done when every unit (heavy components + items) has finished: no unit
+    // is running, so no item can be added
+    // (plain polling: the kernel cannot end before its slowest unit anyway)
+    int fin = 0;
+    if (lane == 0) {
+      const int d = *(volatile int*)&ctl->wq_done[cls];
+      __threadfence();
+      const int t = *(volatile int*)&ctl->wq_tail[cls];
+      fin = d >= n_heavy + t;
+    }
+    if (__shfl_sync(0xffffffffu, fin, 0)) break;
+    __nanosleep(backoff);
+    backoff = min(backoff * 2u, 512u);
   }
-  if (MPLD_DIAG && threadIdx.x == 0) atomicMax(&ctl->dbg[6], (unsigned long long)(clock64() - t0));
+  if (lane == 0 && acc_steps) {
+    atomicAdd(&ctl->steps, acc_steps);
+    atomicMax(&ctl->max_steps_comp, acc_max);
+  }
+  if (lane == 0 && acc_capped) atomicAdd(&ctl->truncated, acc_capped);
 }
 
 }  // namespace

@@ -94,6 +94,11 @@ struct mpld_context {
   int* porder = nullptr;
   int* hcomp = nullptr;
   int* hcost = nullptr;
+  WorkItem* wq = nullptr;     // spilled heavy-search work (fixed size)
+  unsigned* wq_flag = nullptr;
+  HeavySlot* hslot = nullptr;
+  unsigned epoch = 0;         // search calls so far (tags wq_flag)
+  unsigned spill_iters = 256; // heavy-search spill threshold; MPLD_HEAVY_SPILL overrides (tests of the spill path)
   Control* ctl = nullptr;
   // phase-split calls: the prepared graph
   GraphView g{};
@@ -203,8 +208,9 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 }
 
 Workspace workspace(mpld_context* ctx) {
-  return Workspace{ctx->deg,   ctx->hround, ctx->bmask,    ctx->prio,  ctx->q0,    ctx->q1,
-                   ctx->roots, ctx->crec,   ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->ctl};
+  return Workspace{ctx->deg,   ctx->hround, ctx->bmask,  ctx->prio,  ctx->q0,    ctx->q1,    ctx->roots,
+                   ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->ctl,   ctx->wq,
+                   ctx->wq_flag, ctx->hslot, ctx->epoch, ctx->spill_iters};
 }
 
 // phase 1: validate?, simplification, components (colours initialised to -1)
@@ -242,6 +248,8 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
   // one shard: the search kernels accumulate the Eq. (1) counts of the final
   // colourings (the recovery adds no conflict, R9), so the finish
   // phase needs no evaluation pass
+  ++ctx->epoch;  // fresh tag for the spilled-work flags of this call
+  ws.epoch = ctx->epoch;
   ctx->search_counted = shard_count == 1;
   long long* count = ctx->search_counted ? ctx->counts : nullptr;
   {
@@ -413,11 +421,22 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     return fail(MPLD_ERR_NOMEM, "control block allocation failed");
   }
   cudaMemset(ctx->ctl, 0, sizeof(Control));
+  if (cudaMalloc((void**)&ctx->wq, sizeof(WorkItem) * 2 * kWQCap) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->wq_flag, sizeof(unsigned) * 2 * kWQCap) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->hslot, sizeof(HeavySlot) * kSlots) != cudaSuccess) {
+    mpld_context_destroy(ctx);
+    return fail(MPLD_ERR_NOMEM, "heavy-search work queue allocation failed");
+  }
+  cudaMemset(ctx->wq_flag, 0, sizeof(unsigned) * 2 * kWQCap);  // epochs start at 1
   ctx->blocks_simplify = coop_blocks_simplify(kCoopThreads, ctx->num_sms);
   ctx->blocks_recover = coop_blocks_recover(kCoopThreads, ctx->num_sms);
   ctx->blocks_search = resident_blocks_search(32, ctx->num_sms);
   ctx->blocks_discover = resident_blocks_discover(ctx->num_sms);
   ctx->blocks_stream = resident_blocks_evaluate(ctx->num_sms);
+  if (const char* hs = std::getenv("MPLD_HEAVY_SPILL")) {
+    const long v = std::strtol(hs, nullptr, 10);
+    if (v >= 64) ctx->spill_iters = (unsigned)std::min<long>(v & ~63L, 1L << 30);
+  }
   if (const char* ls = std::getenv("MPLD_LIGHT_STEPS")) {
     const long v = std::strtol(ls, nullptr, 10);
     if (v >= 1 && v <= (1L << 24)) ctx->light_steps = (unsigned)v;
@@ -452,7 +471,8 @@ void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->bmask, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->roots, (void*)ctx->crec, (void*)ctx->pmask, (void*)ctx->porder, (void*)ctx->hcomp,
-                  (void*)ctx->hcost, (void*)ctx->ctl, (void*)ctx->h_lo,
+                  (void*)ctx->hcost, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
+                  (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
                   (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})
     if (p) cudaFree(p);

@@ -53,6 +53,10 @@ struct Control {
   alignas(128) int n_heavy[2]; // exact mode: components handed to the warp-parallel search, per word class
                                // (32-bit: hcomp[0..), 64-bit: hcomp[n-1], hcomp[n-2], ...; reset per search call)
   int heavy_next[2];           // exact mode: next heavy component to take per word class (reset with n_heavy)
+  int wq_tail[2];              // spilled work items reserved per word class (reset with n_heavy)
+  int wq_head[2];              // ... claimed
+  int wq_done[2];              // work units (heavy components + items) finished per word class
+  int slot_next;               // spilled-component slots handed out
   alignas(128) unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
   alignas(128) unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)
   unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
@@ -101,6 +105,25 @@ struct GraphView {
   const int* se_col;
 };
 
+// Exact mode, spilled heavy searches (kernel_search.cu): a warp whose search
+// of one component runs long hands its open work to all heavy warps as work
+// items (node states); a slot per spilled component gathers the best key.
+constexpr int kWQCap = 1 << 16;  // work items per word class and call
+constexpr int kSlots = 1024;     // spilled components per call
+struct WorkItem {
+  int slot, depth, cost, mu;
+  unsigned long long pa, pb;  // path (2 bits per level, level 0 most significant)
+  unsigned long long C[4], B[4], U;
+  unsigned long long pad;
+};
+struct HeavySlot {
+  int lock, pend;             // spin lock of the key; work units of the component not finished
+  int cost, lcost;            // best key found, the light phase's key (their costs)
+  unsigned long long pa, pb, lpa, lpb;
+  unsigned long long C[4];    // colour masks of the best leaf
+  int ci, pad[3];             // component (pool record)
+};
+
 struct Workspace {
   int* deg;        // live conflict degree (simplification), then hidden-predecessor count (recovery)
   int* hround;     // -1 kept, else the round the vertex was hidden in
@@ -115,6 +138,11 @@ struct Workspace {
   int* hcomp;      // heavy components (exact mode): component index ...
   int* hcost;      // ... and the light phase's best cost
   Control* ctl;
+  WorkItem* wq;    // [2][kWQCap] spilled work items per word class
+  unsigned* wq_flag;  // [2][kWQCap] == epoch once the item is written
+  HeavySlot* hslot;   // [kSlots]
+  unsigned epoch;     // this search call's tag for wq_flag
+  unsigned spill_iters;  // a heavy unit's iterations before it may spill (multiple of 64; MPLD_HEAVY_SPILL)
 };
 
 // Layout of vertex v: the l with layout_off[l] <= v < layout_off[l+1] (binary

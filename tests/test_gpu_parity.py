@@ -382,3 +382,40 @@ def test_async_pipeline_matches_sync_calls():
     t = ctx.submit(b.layout_offsets, b.n, b.ce_rowptr, b.ce_col, b.se_rowptr, b.se_col, k, alpha)
     assert np.array_equal(ctx.wait(t)["colors"], mp.decompose_graph(b, k, alpha)["colors"])
     ctx.close()
+
+
+@pytest.mark.parametrize("case", ["stress20", "k4", "cfg1"])
+def test_heavy_search_spill(monkeypatch, case):
+    """Exact mode with the heavy-search spill threshold at its minimum (64 warp
+    iterations): long searches hand their open work to the work queue, other
+    warps take it, slots merge the best keys — the result must still be the
+    oracle's first optimal leaf (R7) for every component."""
+    monkeypatch.setenv("MPLD_HEAVY_SPILL", "64")
+    if case == "stress20":
+        k, alpha = 3, 0.1
+        g = synth.stress_components(20, 40, 3, seed=11)
+    elif case == "k4":
+        graphs, k, alpha = synth.config_graphs(2, scale=0.05)
+        g = graphs[0]
+    else:
+        graphs, k, alpha = synth.config_graphs(1)
+        g = synth.concat(graphs[:6])
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    L = int(g.layout_offsets.size - 1)
+    lo = g.layout_offsets
+    ctx = mp.Context(0, g.n, L)  # reads MPLD_HEAVY_SPILL
+    colors = torch.empty(g.n, dtype=torch.int32, device=dev)
+    counts = torch.empty(2 * L, dtype=torch.int64, device=dev)
+    cost = torch.empty(L, dtype=torch.float64, device=dev)
+    stats = torch.empty(len(mp.STAT_NAMES), dtype=torch.int64, device=dev)
+    ctx.decompose_device(T(lo), g.n, T(g.ce_rowptr), T(g.ce_col), T(g.se_rowptr), T(g.se_col),
+                         k, alpha, 0, colors, counts, cost, stats, flags=mp.MPLD_FLAG_VALIDATE)
+    torch.cuda.synchronize()
+    ref = oracle.decompose(g, k, alpha, max_steps=0)
+    assert np.array_equal(colors.cpu().numpy(), ref["colors"])
+    c2 = counts.cpu().numpy().reshape(-1, 2)
+    for li, (c, s_, cst) in enumerate(ref["per_layout"]):
+        assert (int(c2[li, 0]), int(c2[li, 1]), float(cost[li])) == (c, s_, cst)
+    assert int(stats.cpu().numpy()[mp.STAT_NAMES.index("truncated")]) == 0
+    ctx.close()
