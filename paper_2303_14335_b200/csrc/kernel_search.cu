@@ -858,6 +858,10 @@ constexpr int kStealMinIdle = MPLD_STEAL_MIN_IDLE;  // donation rounds only when
 #ifndef MPLD_SPILL
 #define MPLD_SPILL 1
 #endif
+#ifndef MPLD_POLL_CAP
+#define MPLD_POLL_CAP 512
+#endif
+
 #ifndef MPLD_QUEUE_LOW
 #define MPLD_QUEUE_LOW 64
 #endif
@@ -1036,154 +1040,16 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
   for (int c = 0; c < K; ++c) bestC[c] = 0;
   unsigned steps = 0;
   bool capped = false;
-  while (true) {
+  bool all_idle = false;
+  while (!all_idle) {
+   // a compact inner loop of kSpillCheck iterations; the work-queue check between
+   for (unsigned inner = 0; inner < kSpillCheck; ++inner) {
     const unsigned act = __ballot_sync(0xffffffffu, active);
-    if (act == 0u) break;
-    ++iters;
-    if (MPLD_SPILL && iters >= w.spill_iters && (iters & (kSpillCheck - 1)) == 0) {
-      // share the best key with the other units of a spilled component
-      if (u.slot >= 0) {
-        const unsigned owner = __ballot_sync(0xffffffffu, mine);
-        const int src = owner ? __ffs(owner) - 1 : 0;
-        W oc[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) oc[c] = __shfl_sync(0xffffffffu, bestC[c], src);
-        int adopt = 0;
-        Path sp = gP;
-        int sc = gcost;
-        if (lane == 0) {
-          HeavySlot* hs = &w.hslot[u.slot];
-          slot_lock(hs);
-          const Path cur = {__ldcg(&hs->pa), __ldcg(&hs->pb)};
-          const int cc = __ldcg(&hs->cost);
-          if (owner && key_less<kTwo>(gcost, gP, cc, cur)) {
-            hs->cost = gcost;
-            hs->pa = gP.a;
-            hs->pb = gP.b;
-#pragma unroll
-            for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)oc[c];
-          } else if (key_less<kTwo>(cc, cur, gcost, gP)) {
-            adopt = 1;
-            sc = cc;
-            sp = cur;
-          }
-          slot_unlock(hs);
-        }
-        adopt = __shfl_sync(0xffffffffu, adopt, 0);
-        if (owner) mine = false;  // the slot holds this unit's best (or a better one) now
-        if (adopt) {
-          gcost = __shfl_sync(0xffffffffu, sc, 0);
-          gP.a = __shfl_sync(0xffffffffu, sp.a, 0);
-          gP.b = __shfl_sync(0xffffffffu, sp.b, 0);
-        }
-      }
-      // feed the work queue when it runs low: every lane gives away the untried
-      // children of its shallowest open frame (the largest subtrees it holds)
-      int hungry = 0;
-      if (lane == 0)
-        hungry = *(volatile int*)&w.ctl->wq_tail[u.cls] - *(volatile int*)&w.ctl->wq_head[u.cls] < kQueueLow;
-      if (__shfl_sync(0xffffffffu, hungry, 0)) {
-        int cnt = 0, j = -1;
-        if (active && (open & donatable)) {
-          j = __ffsll((long long)(open & donatable)) - 1;
-          const int pk = j == depth - 1 ? (f_c + 1) << 8 | (f_lim << 24) : F.pk[j][lane];
-          cnt = (pk >> 24) - (((pk >> 8) & 0xff) - 1);
-        }
-        int tot = 0;
-        const int excl = warp_excl_scan(cnt, tot);
-        int base = -1;
-        if (lane == 0 && tot > 0) {
-          if (u.slot < 0) {  // the component's first spill: a slot holding the light leaf, one unit pending (this)
-            const int sl = atomicAdd(&w.ctl->slot_next, 1);
-            if (sl < kSlots) {
-              HeavySlot* hs = &w.hslot[sl];
-              hs->lock = 0;
-              hs->pend = 1;
-              hs->cost = hs->lcost = u.c1;
-              hs->pa = hs->lpa = u.p1.a;
-              hs->pb = hs->lpb = u.p1.b;
-#pragma unroll
-              for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)u.col[c];
-              hs->ci = u.ci;
-              __threadfence();
-              u.slot = sl;
-            }
-          }
-          if (u.slot >= 0) {
-            int t = *(volatile int*)&w.ctl->wq_tail[u.cls];
-            while (t + tot <= kWQCap) {
-              const int o = atomicCAS(&w.ctl->wq_tail[u.cls], t, t + tot);
-              if (o == t) {
-                base = t;
-                break;
-              }
-              t = o;
-            }
-            if (base >= 0) atomicAdd(&w.hslot[u.slot].pend, tot);  // before any item is published
-          }
-        }
-        u.slot = __shfl_sync(0xffffffffu, u.slot, 0);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= 0 && cnt > 0) {
-          WorkItem* q = w.wq + (size_t)u.cls * kWQCap;
-          unsigned* qf = w.wq_flag + (size_t)u.cls * kWQCap;
-          int at = base + excl;
-          W jB[K], jU;
-          int pk, jc;
-          if (j == depth - 1) {
-#pragma unroll
-            for (int c = 0; c < K; ++c) jB[c] = fB[c];
-            jU = fU;
-            jc = f_cost;
-            pk = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
-            f_lim = f_c;  // its children are in the queue now
-          } else {
-#pragma unroll
-            for (int c = 0; c < K; ++c) jB[c] = F.B[c][j][lane];
-            jU = F.U[j][lane];
-            jc = F.cost[j][lane];
-            pk = F.pk[j][lane];
-            F.pk[j][lane] = (pk & 0x00ffffff) | ((((pk >> 8) & 0xff) - 1) << 24);
-          }
-          open &= ~(1ull << j);
-          const int v = pk & 0xff, cj = ((pk >> 8) & 0xff) - 1, mu = ((pk >> 16) & 0xff) - 1, lim = pk >> 24;
-          const W bit = W(1) << v;
-          const W a = adj[v], sa = sadj[v];
-          for (int ch = cj + 1; ch <= lim; ++ch) {  // the untried children of frame j (C at N_j = C & ~U_j)
-            W xC[K], xB[K];
-#pragma unroll
-            for (int c = 0; c < K; ++c) {
-              xC[c] = C[c] & ~jU;
-              xB[c] = jB[c];
-            }
-            const W xU = jU & ~bit;
-            const W Cc = pick<K, W>(xC, ch);
-            const int xcost = jc + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~xU & ~Cc);
-            put<K, W>(xC, ch, Cc | bit);
-            put<K, W>(xB, ch, pick<K, W>(xB, ch) | a);
-            Path xP = path_prefix<kTwo>(P, j);
-            path_put<kTwo>(xP, j, ch);
-            WorkItem& it = q[at];
-            it.slot = u.slot;
-            it.depth = j + 1;
-            it.cost = xcost;
-            it.mu = max(mu, ch);
-            it.pa = xP.a;
-            it.pb = xP.b;
-#pragma unroll
-            for (int c = 0; c < K; ++c) {
-              it.C[c] = (unsigned long long)xC[c];
-              it.B[c] = (unsigned long long)xB[c];
-            }
-            it.U = (unsigned long long)xU;
-            __threadfence();
-            *(volatile unsigned*)&qf[at] = w.epoch;
-            ++at;
-          }
-        }
-        if (base >= 0) spilled = true;
-      }
+    if (act == 0u) {
+      all_idle = true;
+      break;
     }
+    ++iters;
     if (__popc(~act) >= kStealMinIdle) {  // work donation: the i-th idle lane takes a node from the i-th donor
       const unsigned don = __ballot_sync(0xffffffffu, active && (open & donatable) != 0ull);
       if (don) {
@@ -1370,6 +1236,128 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       // the non-finding lanes hold the previous best, so a finding lane wins
       mine = warp_min_key<kTwo>(gcost, gP) == lane;
     }
+   }
+    if (MPLD_SPILL && !all_idle && iters >= w.spill_iters) {
+      // share the best cost with the other units of a spilled component (no
+      // lock: their keys are merged when the units end)
+      if (u.slot >= 0) {
+        HeavySlot* hs = &w.hslot[u.slot];
+        const int bc = *(volatile int*)&hs->bcost;
+        if (bc < gcost) {  // a cheaper leaf exists: (bc, max path) is a valid, weaker incumbent
+          gcost = bc;
+          gP = Path{~0ull, ~0ull};
+          mine = false;
+        } else if (gcost < bc && __any_sync(0xffffffffu, mine)) {
+          if (lane == 0) atomicMin(&hs->bcost, gcost);
+        }
+      }
+      // feed the work queue when it runs low: every lane gives away the untried
+      // children of its shallowest open frame (the largest subtrees it holds)
+      int hungry = 0;
+      if (lane == 0)
+        hungry = *(volatile int*)&w.ctl->wq_tail[u.cls] - *(volatile int*)&w.ctl->wq_head[u.cls] < kQueueLow;  // < 0: warps wait
+      if (__shfl_sync(0xffffffffu, hungry, 0)) {
+        int cnt = 0, j = -1;
+        if (active && (open & donatable)) {
+          j = __ffsll((long long)(open & donatable)) - 1;
+          const int pk = j == depth - 1 ? (f_c + 1) << 8 | (f_lim << 24) : F.pk[j][lane];
+          cnt = (pk >> 24) - (((pk >> 8) & 0xff) - 1);
+        }
+        int tot = 0;
+        const int excl = warp_excl_scan(cnt, tot);
+        int base = -1;
+        if (lane == 0 && tot > 0) {
+          if (u.slot < 0) {  // the component's first spill: a slot holding the light leaf, one unit pending (this)
+            const int sl = atomicAdd(&w.ctl->slot_next, 1);
+            if (sl < kSlots) {
+              HeavySlot* hs = &w.hslot[sl];
+              hs->lock = 0;
+              hs->pend = 1;
+              hs->cost = hs->lcost = hs->bcost = u.c1;
+              hs->pa = hs->lpa = u.p1.a;
+              hs->pb = hs->lpb = u.p1.b;
+#pragma unroll
+              for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)u.col[c];
+              hs->ci = u.ci;
+              __threadfence();
+              u.slot = sl;
+            }
+          }
+          if (u.slot >= 0) {
+            int t = *(volatile int*)&w.ctl->wq_tail[u.cls];
+            while (t + tot <= kWQCap) {
+              const int o = atomicCAS(&w.ctl->wq_tail[u.cls], t, t + tot);
+              if (o == t) {
+                base = t;
+                break;
+              }
+              t = o;
+            }
+            if (base >= 0) atomicAdd(&w.hslot[u.slot].pend, tot);  // before any item is published
+          }
+        }
+        u.slot = __shfl_sync(0xffffffffu, u.slot, 0);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= 0 && cnt > 0) {
+          WorkItem* q = w.wq + (size_t)u.cls * kWQCap;
+          unsigned* qf = w.wq_flag + (size_t)u.cls * kWQCap;
+          int at = base + excl;
+          W jB[K], jU;
+          int pk, jc;
+          if (j == depth - 1) {
+#pragma unroll
+            for (int c = 0; c < K; ++c) jB[c] = fB[c];
+            jU = fU;
+            jc = f_cost;
+            pk = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
+            f_lim = f_c;  // its children are in the queue now
+          } else {
+#pragma unroll
+            for (int c = 0; c < K; ++c) jB[c] = F.B[c][j][lane];
+            jU = F.U[j][lane];
+            jc = F.cost[j][lane];
+            pk = F.pk[j][lane];
+            F.pk[j][lane] = (pk & 0x00ffffff) | ((((pk >> 8) & 0xff) - 1) << 24);
+          }
+          open &= ~(1ull << j);
+          const int v = pk & 0xff, cj = ((pk >> 8) & 0xff) - 1, mu = ((pk >> 16) & 0xff) - 1, lim = pk >> 24;
+          const W bit = W(1) << v;
+          const W a = adj[v], sa = sadj[v];
+          for (int ch = cj + 1; ch <= lim; ++ch) {  // the untried children of frame j (C at N_j = C & ~U_j)
+            W xC[K], xB[K];
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+              xC[c] = C[c] & ~jU;
+              xB[c] = jB[c];
+            }
+            const W xU = jU & ~bit;
+            const W Cc = pick<K, W>(xC, ch);
+            const int xcost = jc + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~xU & ~Cc);
+            put<K, W>(xC, ch, Cc | bit);
+            put<K, W>(xB, ch, pick<K, W>(xB, ch) | a);
+            Path xP = path_prefix<kTwo>(P, j);
+            path_put<kTwo>(xP, j, ch);
+            WorkItem& it = q[at];
+            it.slot = u.slot;
+            it.depth = j + 1;
+            it.cost = xcost;
+            it.mu = max(mu, ch);
+            it.pa = xP.a;
+            it.pb = xP.b;
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+              it.C[c] = (unsigned long long)xC[c];
+              it.B[c] = (unsigned long long)xB[c];
+            }
+            it.U = (unsigned long long)xU;
+            __threadfence();
+            *(volatile unsigned*)&qf[at] = w.epoch;
+            ++at;
+          }
+        }
+        if (base >= 0) spilled = true;
+      }
+    }
   }
   unsigned tot = steps;
 #pragma unroll
@@ -1430,16 +1418,20 @@ __device__ void heavy_unit_done(const GraphView& g, const Workspace& w, const He
   HeavySlot* hs = &w.hslot[u.slot];
   int last = 0;
   if (lane == 0) {
-    slot_lock(hs);
-    const Path cur = {__ldcg(&hs->pa), __ldcg(&hs->pb)};
-    if (owner && key_less<kTwo>(gcost, gP, __ldcg(&hs->cost), cur)) {
-      hs->cost = gcost;
-      hs->pa = gP.a;
-      hs->pb = gP.b;
+    if (owner && gcost <= *(volatile int*)&hs->bcost) {  // a leaf that may beat the slot's key
+      atomicMin(&hs->bcost, gcost);
+      slot_lock(hs);
+      const Path cur = {__ldcg(&hs->pa), __ldcg(&hs->pb)};
+      if (key_less<kTwo>(gcost, gP, __ldcg(&hs->cost), cur)) {
+        hs->cost = gcost;
+        hs->pa = gP.a;
+        hs->pb = gP.b;
 #pragma unroll
-      for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)oc[c];
+        for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)oc[c];
+      }
+      slot_unlock(hs);
     }
-    slot_unlock(hs);
+    __threadfence();
     last = atomicSub(&hs->pend, 1) == 1;
     __threadfence();
   }
@@ -1500,6 +1492,8 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
   int acc_max = 0, acc_capped = 0;
   bool comps_left = n_heavy > 0;
   unsigned backoff = 64;
+  int cur_ci = -1, cur_ncl = 0;  // the component whose masks are in shared memory
+  int ticket = -1;               // this warp's queue position (-1: none taken)
   while (true) {
     HeavyUnit<K, W> u;
     u.w_stitch = w_stitch;
@@ -1527,6 +1521,8 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
         u.c1 = __ldcg(&w.hcost[idx]);
         u.slot = -1;
         heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, colors, u.col);
+        cur_ci = u.ci;
+        cur_ncl = u.ncl;
         int lc = 0;  // == c1
         u.p1 = leaf_path<K, W>(u.col, u.n, s_adj, s_sadj, w_stitch, lc);
         gcost = u.c1;
@@ -1563,18 +1559,20 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
       }
       comps_left = false;
     }
-    // a spilled work item
+    // a spilled work item: take a ticket (one position of the queue) and wait
+    // for its item, or for the end of all work if it never comes
+    if (ticket < 0) {
+      if (lane == 0) ticket = atomicAdd(&ctl->wq_head[cls], 1);
+      ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    }
     int it = -1;
     if (lane == 0) {
-      const int hd = *(volatile int*)&ctl->wq_head[cls];
-      if (hd < *(volatile int*)&ctl->wq_tail[cls] && atomicCAS(&ctl->wq_head[cls], hd, hd + 1) == hd) it = hd;
+      if (ticket < kWQCap && *(volatile unsigned*)&w.wq_flag[(size_t)cls * kWQCap + ticket] == w.epoch) it = ticket;
     }
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= 0) {
       backoff = 64;
-      if (lane == 0)
-        while (*(volatile unsigned*)&w.wq_flag[(size_t)cls * kWQCap + it] != w.epoch) {
-        }
+      ticket = -1;
       __syncwarp();
       __threadfence();
       const WorkItem* q = w.wq + (size_t)cls * kWQCap + it;
@@ -1584,7 +1582,12 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
       const unsigned long long rec = __ldcg(&w.crec[u.ci]);
       const size_t off = (size_t)(rec >> 8);
       u.n = (int)(rec & 0xffull);
-      heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, nullptr, u.col);
+      if (u.ci != cur_ci) {  // items of one component mostly follow each other: keep its masks
+        heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, nullptr, u.col);
+        cur_ci = u.ci;
+        cur_ncl = u.ncl;
+      }
+      u.ncl = cur_ncl;
       W sC[K], sB[K];
 #pragma unroll
       for (int c = 0; c < K; ++c) {
@@ -1592,18 +1595,12 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
         sB[c] = (W)__ldcg(&q->B[c]);
       }
       const Path sP = {__ldcg(&q->pa), __ldcg(&q->pb)};
-      int sc = 0;  // the slot's key as the starting incumbent
-      Path sk = {0ull, 0ull};
-      if (lane == 0) {
-        slot_lock(hs);
-        sc = __ldcg(&hs->cost);
-        sk.a = __ldcg(&hs->pa);
-        sk.b = __ldcg(&hs->pb);
-        slot_unlock(hs);
-      }
+      // the best cost known as the starting incumbent, (bcost, max path): a
+      // valid key no smaller than the slot's
+      int sc = 0;
+      if (lane == 0) sc = *(volatile int*)&hs->bcost;
       gcost = __shfl_sync(0xffffffffu, sc, 0);
-      gP.a = __shfl_sync(0xffffffffu, sk.a, 0);
-      gP.b = __shfl_sync(0xffffffffu, sk.b, 0);
+      gP = Path{~0ull, ~0ull};
       warp_heavy_search<K, W>(u, w, sC, sB, (W)__ldcg(&q->U), __ldcg(&q->cost), __ldcg(&q->mu), sP,
                               __ldcg(&q->depth), gcost, gP, mine, bestC, steps, capped, spilled);
       heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, w.porder + off, colors, counts);
@@ -1617,18 +1614,17 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
       continue;
     }
     // done when every unit (heavy components + items) has finished: no unit
-    // is running, so no item can be added
-    // (plain polling: the kernel cannot end before its slowest unit anyway)
+    // is running, so no item can be added and this ticket stays empty
     int fin = 0;
     if (lane == 0) {
       const int d = *(volatile int*)&ctl->wq_done[cls];
       __threadfence();
       const int t = *(volatile int*)&ctl->wq_tail[cls];
-      fin = d >= n_heavy + t;
+      fin = d >= n_heavy + t && ticket >= t;
     }
     if (__shfl_sync(0xffffffffu, fin, 0)) break;
     __nanosleep(backoff);
-    backoff = min(backoff * 2u, 512u);
+    backoff = min(backoff * 2u, (unsigned)MPLD_POLL_CAP);
   }
   if (lane == 0 && acc_steps) {
     atomicAdd(&ctl->steps, acc_steps);

@@ -119,9 +119,10 @@ struct WorkItem {
 struct HeavySlot {
   int lock, pend;             // spin lock of the key; work units of the component not finished
   int cost, lcost;            // best key found, the light phase's key (their costs)
+  int bcost, pad0;            // the best cost known (atomicMin, read without the lock: pruning)
   unsigned long long pa, pb, lpa, lpb;
   unsigned long long C[4];    // colour masks of the best leaf
-  int ci, pad[3];             // component (pool record)
+  int ci, pad[1];             // component (pool record)
 };
 
 struct Workspace {
