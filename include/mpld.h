@@ -180,10 +180,14 @@ int mpld_wait(mpld_context* ctx, int64_t ticket);
  * The same hot path split in three phases so that the components of ONE
  * layout batch can be searched by shard_count processes (one per GPU):
  *   1. every process: mpld_prepare_device   (validate?, simplification, components)
- *   2. every process: mpld_search_device     with its shard_index: searches the
- *      components whose root r (smallest vertex id) has
- *      lowbias32(r) % shard_count == shard_index, writes their colours into
- *      d_colors and leaves -1 on every other vertex;
+ *   2. every process: mpld_search_device     with its shard_index: discovers every
+ *      component, estimates its search cost as n * k^n (capped at 2^40; the
+ *      north_star's "size x k^n"), takes the inclusive prefix sum of the
+ *      estimates in order of the components' roots (smallest vertex ids), and
+ *      searches the components whose cost interval starts in the shard_index-th
+ *      of shard_count equal parts of the total (contiguous root ranges of
+ *      equal estimated cost, computed identically by every process); writes
+ *      their colours into d_colors and leaves -1 on every other vertex;
  *   3. the caller combines d_colors across the processes with an element-wise
  *      maximum (an NCCL all-reduce MAX over NVLink) — the only exchange;
  *   4. every process: mpld_finish_device     (recovery of the hidden vertices, Eq. 1).

@@ -492,8 +492,8 @@ __device__ __forceinline__ void add_counts(const GraphView& g, int v0, int nc, i
 // One warp per component seed: discovery, relabelling to the R5 column order
 // and the component's record in the pool (exactly one per component: the seed
 // that is its minimum).  Low register use, so 64 warps per SM discover at once.
-__global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(GraphView g, Workspace w,
-                                                                              int shard_index, int shard_count) {
+__global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(GraphView g, Workspace w, int k,
+                                                                              int sharded) {
   __shared__ WarpDisc s_disc[kCompWarps];
   WarpDisc& s = s_disc[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -504,14 +504,13 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     ctl->t[14] = t;
   }
-  unsigned acc_comp = 0;  // statistics, accumulated on lane 0
+
   int acc_maxn = 0;
   unsigned long long d_cyc = 0ull, d_n = 0ull;  // diagnostics: slowest seed of this warp
   const int nw = gridDim.x * kCompWarps;
   for (int ci = blockIdx.x * kCompWarps + (threadIdx.x >> 5); ci < n_seed; ci += nw) {
     const long long c0 = clock64();
     const int root = __ldg(&w.roots[ci]);
-    if (shard_count > 1 && (int)(lowbias32((uint32_t)root) % (uint32_t)shard_count) != shard_index) continue;
 #ifdef MPLD_DIAG_DISCOVER
     int dg = 0;
     const int n = warp_discover(g, w, root, s, &dg);
@@ -519,7 +518,7 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
     const int n = warp_discover(g, w, root, s);
 #endif
     if (n == -2) continue;  // the seed is not its component's minimum
-    ++acc_comp;
+
     if (n < 0) {
       if (lane == 0) {
         atomicOr(&ctl->err, kErrComponent);
@@ -541,6 +540,7 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
     }
     if (lane == 0) {
       w.crec[c] = ((unsigned long long)off << 8) | (unsigned long long)n;
+      if (sharded) w.est[root] = partition_estimate(n, k);  // the balanced partition (scan, then light search)
       acc_maxn = max(acc_maxn, n);
       const unsigned long long cyc = (unsigned long long)(clock64() - c0);
       if (cyc > d_cyc) {
@@ -554,7 +554,6 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
     }
     __syncwarp();
   }
-  if (lane == 0 && acc_comp) atomicAdd(&ctl->n_comp, (int)acc_comp);
   if (lane == 0 && acc_maxn > 0) atomicMax(&ctl->max_comp, acc_maxn);
   if (MPLD_DIAG && lane == 0 && d_cyc > 0) atomicMax(&ctl->dbg[0], (d_cyc << 16) | (d_n & 0xffffull));
 }
@@ -687,6 +686,7 @@ struct LightAcc {
   unsigned long long steps = 0ull;
   int maxsteps = 0;
   unsigned trunc = 0;
+  unsigned comps = 0;  // components searched (this shard's)
 };
 
 __device__ __forceinline__ void light_handoff(const GraphView& g, const Workspace& w, int ci, int n, int best_cost) {
@@ -739,10 +739,24 @@ __device__ void light_single(const GraphView& g, const Workspace& w, WarpSearch&
   __syncwarp();
 }
 
+// Sharded search: the component rooted at `root` belongs to the
+// shard in which its cost interval [prefix - est, prefix) starts (contiguous
+// root-id ranges of equal estimated cost; the same on every rank).
+__device__ __forceinline__ bool in_shard(const GraphView& g, const Workspace& w, int root, int n, int k,
+                                         int shard_index, int shard_count) {
+  if (shard_count <= 1) return true;
+  const unsigned long long total = __ldcg(&w.est[g.n - 1]);
+  const unsigned long long start = __ldcg(&w.est[root]) - partition_estimate(n, k);
+  int s = (int)((double)start / (double)total * (double)shard_count);
+  s = min(max(s, 0), shard_count - 1);
+  return s == shard_index;
+}
+
 template <int K>
 __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
                                                                            long long max_steps, int* colors,
-                                                                           unsigned light_steps, long long* counts) {
+                                                                           unsigned light_steps, long long* counts,
+                                                                           int shard_index, int shard_count) {
   __shared__ LaneLight s_lane[kLaneWarps];
   LaneLight& L = s_lane[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -759,7 +773,9 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
     if (ci < n_comp) rec = __ldcg(&w.crec[ci]);
     const size_t off = (size_t)(rec >> 8);
     const int n = (int)(rec & 0xffull);
-    const bool valid = ci < n_comp && n <= 32;
+    const bool mine_c = ci < n_comp && in_shard(g, w, __ldcg(&w.porder[off]), n, K, shard_index, shard_count);
+    const bool valid = mine_c && n <= 32;
+    acc.comps += mine_c ? 1 : 0;
     if (valid)
       for (int i = 0; i < n; ++i) {
         const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
@@ -799,7 +815,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
       acc.steps += steps;
     }
     // components of more than 32 vertices: one at a time on lane 0
-    unsigned big = __ballot_sync(0xffffffffu, ci < n_comp && n > 32);
+    unsigned big = __ballot_sync(0xffffffffu, mine_c && n > 32);
     __syncwarp();
     while (big) {
       const int l = __ffs(big) - 1;
@@ -812,13 +828,15 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
   // statistics: one atomic per warp
   unsigned long long st = acc.steps;
   int mx = acc.maxsteps;
-  unsigned tr = acc.trunc;
+  unsigned tr = acc.trunc, nc = acc.comps;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     st += __shfl_xor_sync(0xffffffffu, st, o);
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    nc += __shfl_xor_sync(0xffffffffu, nc, o);
   }
+  if (lane == 0 && nc) atomicAdd(&ctl->n_comp, (int)nc);
   if (lane == 0 && st) {
     atomicAdd(&ctl->steps, st);
     atomicMax(&ctl->max_steps_comp, mx);
@@ -1494,6 +1512,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
   unsigned backoff = 64;
   int cur_ci = -1, cur_ncl = 0;  // the component whose masks are in shared memory
   int ticket = -1;               // this warp's queue position (-1: none taken)
+  unsigned polls = 0;
   while (true) {
     HeavyUnit<K, W> u;
     u.w_stitch = w_stitch;
@@ -1616,7 +1635,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
     // done when every unit (heavy components + items) has finished: no unit
     // is running, so no item can be added and this ticket stays empty
     int fin = 0;
-    if (lane == 0) {
+    if (lane == 0 && (++polls & 3) == 0) {  // the ticket's flag every poll, the end of all work every 4th
       const int d = *(volatile int*)&ctl->wq_done[cls];
       __threadfence();
       const int t = *(volatile int*)&ctl->wq_tail[cls];
@@ -1635,26 +1654,106 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
 
 }  // namespace
 
-cudaError_t launch_discover(const GraphView& g, Workspace ws, int shard_index, int shard_count, cudaStream_t s,
-                            int blocks) {
-  mpld_component_discover<<<blocks, kCompWarps * 32, 0, s>>>(g, ws, shard_index, shard_count);
+cudaError_t launch_discover(const GraphView& g, Workspace ws, int k, int sharded, cudaStream_t s, int blocks) {
+  mpld_component_discover<<<blocks, kCompWarps * 32, 0, s>>>(g, ws, k, sharded);
+  return cudaGetLastError();
+}
+
+// Inclusive prefix sum of ws.est[0..n) (the balanced shard partition): block
+// sums, one block scanning them, every block rescanning its tile.
+__device__ __forceinline__ unsigned long long block_scan_u64(unsigned long long x, unsigned long long* s_w,
+                                                             unsigned long long& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned long long y = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long z = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) y += z;
+  }
+  if (lane == 31) s_w[wid] = y;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long t = lane < nw ? s_w[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long z = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += z;
+    }
+    if (lane < nw) s_w[lane] = t;
+  }
+  __syncthreads();
+  total = s_w[nw - 1];
+  const unsigned long long r = y + (wid ? s_w[wid - 1] : 0ull);  // inclusive
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) mpld_partition_sums(int n, const unsigned long long* est,
+                                                            unsigned long long* bsum) {
+  __shared__ unsigned long long s_w[32];
+  const size_t base = (size_t)blockIdx.x * kScanTile;
+  unsigned long long x = 0ull;
+  for (int j = 0; j < kScanTile / 1024; ++j) {
+    const size_t i = base + (size_t)j * 1024 + threadIdx.x;
+    if (i < (size_t)n) x += __ldcg(&est[i]);
+  }
+  unsigned long long total;
+  block_scan_u64(x, s_w, total);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) mpld_partition_offsets(int nb, unsigned long long* bsum) {
+  __shared__ unsigned long long s_w[32];
+  unsigned long long carry = 0ull;
+  for (int b0 = 0; b0 < nb; b0 += 1024) {  // exclusive scan of the block sums, in place
+    const int i = b0 + threadIdx.x;
+    const unsigned long long x = i < nb ? bsum[i] : 0ull;
+    unsigned long long total;
+    const unsigned long long inc = block_scan_u64(x, s_w, total);
+    if (i < nb) bsum[i] = carry + inc - x;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(1024) mpld_partition_apply(int n, unsigned long long* est,
+                                                             const unsigned long long* bsum) {
+  __shared__ unsigned long long s_w[32];
+  const size_t base = (size_t)blockIdx.x * kScanTile;
+  unsigned long long carry = bsum[blockIdx.x];
+  for (int j = 0; j < kScanTile / 1024; ++j) {
+    const size_t i = base + (size_t)j * 1024 + threadIdx.x;
+    const unsigned long long x = i < (size_t)n ? est[i] : 0ull;
+    unsigned long long total;
+    const unsigned long long inc = block_scan_u64(x, s_w, total);
+    if (i < (size_t)n) est[i] = carry + inc;
+    carry += total;
+  }
+}
+
+cudaError_t launch_partition_scan(const GraphView& g, Workspace ws, cudaStream_t s) {
+  if (g.n <= 0) return cudaSuccess;
+  const int nb = (g.n + kScanTile - 1) / kScanTile;
+  mpld_partition_sums<<<nb, 1024, 0, s>>>(g.n, ws.est, ws.bsum);
+  mpld_partition_offsets<<<1, 1024, 0, s>>>(nb, ws.bsum);
+  mpld_partition_apply<<<nb, 1024, 0, s>>>(g.n, ws.est, ws.bsum);
   return cudaGetLastError();
 }
 
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
-                          unsigned light_steps, long long* counts, cudaStream_t s, int blocks) {
+                          unsigned light_steps, long long* counts, int shard_index, int shard_count, cudaStream_t s,
+                          int blocks) {
   switch (k) {
     case 2:
       mpld_exact_cover_search<2><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
-                                                                     counts);
+                                                                     counts, shard_index, shard_count);
       break;
     case 3:
       mpld_exact_cover_search<3><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
-                                                                     counts);
+                                                                     counts, shard_index, shard_count);
       break;
     case 4:
       mpld_exact_cover_search<4><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
-                                                                     counts);
+                                                                     counts, shard_index, shard_count);
       break;
     default: return cudaErrorInvalidValue;
   }

@@ -97,6 +97,8 @@ struct mpld_context {
   WorkItem* wq = nullptr;     // spilled heavy-search work (fixed size)
   unsigned* wq_flag = nullptr;
   HeavySlot* hslot = nullptr;
+  unsigned long long* est = nullptr;   // sharded search: cost-balanced partition (cap_n)
+  unsigned long long* bsum = nullptr;
   unsigned epoch = 0;         // search calls so far (tags wq_flag)
   unsigned spill_iters = 256; // heavy-search spill threshold; MPLD_HEAVY_SPILL overrides (tests of the spill path)
   Control* ctl = nullptr;
@@ -152,6 +154,8 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
       e = grow(p, cap);
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
+    if (grow(&ctx->est, cap) != cudaSuccess || grow(&ctx->bsum, cap / kScanTile + 2) != cudaSuccess)
+      return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     if (grow(&ctx->prio, cap) != cudaSuccess || grow(&ctx->bmask, cap) != cudaSuccess ||
         grow(&ctx->crec, cap) != cudaSuccess || grow(&ctx->pmask, 2 * cap) != cudaSuccess)
       return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
@@ -210,7 +214,7 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 Workspace workspace(mpld_context* ctx) {
   return Workspace{ctx->deg,   ctx->hround, ctx->bmask,  ctx->prio,  ctx->q0,    ctx->q1,    ctx->roots,
                    ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->ctl,   ctx->wq,
-                   ctx->wq_flag, ctx->hslot, ctx->epoch, ctx->spill_iters};
+                   ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters};
 }
 
 // phase 1: validate?, simplification, components (colours initialised to -1)
@@ -252,17 +256,29 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
   ws.epoch = ctx->epoch;
   ctx->search_counted = shard_count == 1;
   long long* count = ctx->search_counted ? ctx->counts : nullptr;
+  // sharded: every shard discovers all components; a scan of their estimated
+  // costs in vertex-id order gives the cost-balanced partition
+  const int sharded = shard_count > 1 ? 1 : 0;
+  if (sharded) {
+    cudaError_t e = cudaMemsetAsync(ws.est, 0, sizeof(unsigned long long) * (size_t)g.n, s);
+    if (e != cudaSuccess) return cuda_fail(e, "partition reset");
+  }
   {
     TimedLaunch t(ctx, K_DISCOVER, s);
-    cudaError_t e = launch_discover(g, ws, shard_index, shard_count, s, ctx->blocks_discover);
+    cudaError_t e = launch_discover(g, ws, ctx->k, sharded, s, ctx->blocks_discover);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_component_discover");
     t.done();
     ++ctx->call_launches;
   }
+  if (sharded) {
+    cudaError_t e = launch_partition_scan(g, ws, s);
+    if (e != cudaSuccess) return cuda_fail(e, "partition scan");
+    ctx->call_launches += 3;
+  }
   {
     TimedLaunch t(ctx, K_SEARCH, s);
-    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, count, s,
-                                  ctx->blocks_search);
+    cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, count, shard_index,
+                                  shard_count, s, ctx->blocks_search);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
     t.done();
     ++ctx->call_launches;
@@ -472,6 +488,7 @@ void mpld_context_destroy(mpld_context* ctx) {
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->bmask, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->roots, (void*)ctx->crec, (void*)ctx->pmask, (void*)ctx->porder, (void*)ctx->hcomp,
                   (void*)ctx->hcost, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
+                  (void*)ctx->est, (void*)ctx->bsum,
                   (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
                   (void*)ctx->h_colors, (void*)ctx->h_counts, (void*)ctx->h_cost, (void*)ctx->h_stats})

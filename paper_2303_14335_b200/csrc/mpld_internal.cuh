@@ -52,11 +52,11 @@ struct Control {
   unsigned long long steps;    // search nodes entered
   alignas(128) int n_heavy[2]; // exact mode: components handed to the warp-parallel search, per word class
                                // (32-bit: hcomp[0..), 64-bit: hcomp[n-1], hcomp[n-2], ...; reset per search call)
-  int heavy_next[2];           // exact mode: next heavy component to take per word class (reset with n_heavy)
-  int wq_tail[2];              // spilled work items reserved per word class (reset with n_heavy)
-  int wq_head[2];              // ... claimed
-  int wq_done[2];              // work units (heavy components + items) finished per word class
-  int slot_next;               // spilled-component slots handed out
+  int slot_next;               // spilled-component slots handed out (reset with n_heavy)
+  alignas(128) int heavy_next[2];  // exact mode: next heavy component to take per word class (reset with n_heavy)
+  alignas(128) int wq_head[2];     // spilled work items: tickets handed out per word class (reset with n_heavy)
+  alignas(128) int wq_tail[2];     // ... positions reserved (polled)
+  int wq_done[2];                  // work units (heavy components + items) finished per word class (polled)
   alignas(128) unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
   alignas(128) unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)
   unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
@@ -105,6 +105,16 @@ struct GraphView {
   const int* se_col;
 };
 
+constexpr int kScanTile = 8192;  // elements per block of the partition scan (1024 threads x 8)
+
+// Estimated search cost of a component of n vertices for the cost-balanced
+// shard partition (north_star: size x k^n), capped at 2^40.
+__host__ __device__ __forceinline__ unsigned long long partition_estimate(int n, int k) {
+  unsigned long long e = (unsigned long long)n;
+  for (int i = 0; i < n && e < (1ull << 40); ++i) e *= (unsigned long long)k;
+  return e < (1ull << 40) ? e : (1ull << 40);
+}
+
 // Exact mode, spilled heavy searches (kernel_search.cu): a warp whose search
 // of one component runs long hands its open work to all heavy warps as work
 // items (node states); a slot per spilled component gathers the best key.
@@ -142,6 +152,9 @@ struct Workspace {
   WorkItem* wq;    // [2][kWQCap] spilled work items per word class
   unsigned* wq_flag;  // [2][kWQCap] == epoch once the item is written
   HeavySlot* hslot;   // [kSlots]
+  unsigned long long* est;   // [n] sharded search: estimated search cost of the component rooted at v, then
+                             // its inclusive prefix sum over vertex ids (the balanced partition)
+  unsigned long long* bsum;  // [n / kScanTile + 2] block sums of that scan
   unsigned epoch;     // this search call's tag for wq_flag
   unsigned spill_iters;  // a heavy unit's iterations before it may spill (multiple of 64; MPLD_HEAVY_SPILL)
 };
@@ -183,10 +196,11 @@ __host__ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
 // cudaError_t of its launch.
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors,
                                        long long* counts, int validate, cudaStream_t s, int blocks, int threads);
-cudaError_t launch_discover(const GraphView& g, Workspace ws, int shard_index, int shard_count, cudaStream_t s,
-                            int blocks);
+cudaError_t launch_discover(const GraphView& g, Workspace ws, int k, int sharded, cudaStream_t s, int blocks);
+cudaError_t launch_partition_scan(const GraphView& g, Workspace ws, cudaStream_t s);  // inclusive scan of ws.est
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
-                          unsigned light_steps, long long* counts, cudaStream_t s, int blocks);
+                          unsigned light_steps, long long* counts, int shard_index, int shard_count, cudaStream_t s,
+                          int blocks);
 constexpr unsigned kLightStepsDefault = 48;  // exact mode: one-lane budget before a component turns heavy
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, long long* counts,
                                 cudaStream_t s, const int* blocks);

@@ -300,6 +300,27 @@ def test_sharded_phases_equal_oracle(shards):
     torch.cuda.synchronize()
     owned = [(p >= 0) for p in parts]
     assert int(sum(o.int() for o in owned).max()) <= 1  # every kept vertex searched by exactly one shard
+    # the cost-balanced partition (include/mpld.h phase 2), recomputed from the
+    # oracle's components: estimate n * k^n capped at 2^40, inclusive prefix in
+    # root order, shard of the interval's start
+    ref_comps = sorted(oracle.decompose(b, k, alpha, max_steps=0)["components"], key=lambda c: c["root"])
+
+    def estimate(n):
+        e = n
+        for _ in range(n):
+            if e >= 1 << 40:
+                break
+            e *= k
+        return min(e, 1 << 40)
+
+    ests = [estimate(c["size"]) for c in ref_comps]
+    total, acc = float(sum(ests)), 0
+    host_owned = [o.cpu().numpy() for o in owned]
+    for c, e in zip(ref_comps, ests):
+        acc += e
+        want = min(max(int(float(acc - e) / total * float(shards)), 0), shards - 1)
+        got = [s for s in range(shards) if host_owned[s][c["root"]]]
+        assert got == [want], (c, got, want)
     combined = torch.stack(parts).amax(0).contiguous()
     ctx.finish_device(alpha, combined, counts, cost, stats)
     torch.cuda.synchronize()
