@@ -691,6 +691,7 @@ struct LightAcc {
 
 __device__ __forceinline__ void light_handoff(const GraphView& g, const Workspace& w, int ci, int n, int best_cost) {
   const int cls = n > 32 ? 1 : 0;
+  if (n >= kHelpersMinN) atomicOr(&w.ctl->may_spill, 1);
   const int h = atomicAdd(&w.ctl->n_heavy[cls], 1);
   const int idx = cls ? g.n - 1 - h : h;
   w.hcomp[idx] = ci;
@@ -1581,6 +1582,13 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
     // a spilled work item: take a ticket (one position of the queue) and wait
     // for its item, or for the end of all work if it never comes
     if (ticket < 0) {
+      // no component left: stay for spilled work only if some may come (small
+      // components never run long; a spill without helpers is still drained
+      // by the warps that are running, the spilling one included)
+      int leave = 0;
+      if (lane == 0)
+        leave = *(volatile int*)&ctl->may_spill == 0 && *(volatile int*)&ctl->wq_tail[cls] == 0;
+      if (__shfl_sync(0xffffffffu, leave, 0)) break;
       if (lane == 0) ticket = atomicAdd(&ctl->wq_head[cls], 1);
       ticket = __shfl_sync(0xffffffffu, ticket, 0);
     }

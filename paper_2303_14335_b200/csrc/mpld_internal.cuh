@@ -53,6 +53,8 @@ struct Control {
   alignas(128) int n_heavy[2]; // exact mode: components handed to the warp-parallel search, per word class
                                // (32-bit: hcomp[0..), 64-bit: hcomp[n-1], hcomp[n-2], ...; reset per search call)
   int slot_next;               // spilled-component slots handed out (reset with n_heavy)
+  int may_spill;               // a heavy component of >= kHelpersMinN vertices was handed off: idle heavy
+                               // warps stay for spilled work instead of leaving (reset with n_heavy)
   alignas(128) int heavy_next[2];  // exact mode: next heavy component to take per word class (reset with n_heavy)
   alignas(128) int wq_head[2];     // spilled work items: tickets handed out per word class (reset with n_heavy)
   alignas(128) int wq_tail[2];     // ... positions reserved (polled)
@@ -119,6 +121,7 @@ __host__ __device__ __forceinline__ unsigned long long partition_estimate(int n,
 // of one component runs long hands its open work to all heavy warps as work
 // items (node states); a slot per spilled component gathers the best key.
 constexpr int kWQCap = 1 << 16;  // work items per word class and call
+constexpr int kHelpersMinN = 16;  // heavy components this large may run long enough to spill
 constexpr int kSlots = 1024;     // spilled components per call
 struct WorkItem {
   int slot, depth, cost, mu;
