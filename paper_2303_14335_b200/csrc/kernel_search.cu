@@ -494,6 +494,7 @@ __device__ __forceinline__ void add_counts(const GraphView& g, int v0, int nc, i
 // that is its minimum).  Low register use, so 64 warps per SM discover at once.
 __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(GraphView g, Workspace w, int k,
                                                                               int sharded) {
+  pdl_begin();
   __shared__ WarpDisc s_disc[kCompWarps];
   WarpDisc& s = s_disc[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -758,6 +759,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
                                                                            long long max_steps, int* colors,
                                                                            unsigned light_steps, long long* counts,
                                                                            int shard_index, int shard_count) {
+  pdl_begin();
   __shared__ LaneLight s_lane[kLaneWarps];
   LaneLight& L = s_lane[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1496,6 +1498,7 @@ __device__ void heavy_load(const Workspace& w, size_t off, int n, W* s_adj, W* s
 template <int K, typename W>
 __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
                                                                     int* colors, long long* counts) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int cls = sizeof(W) == 4 ? 0 : 1;
   constexpr bool kTwo = sizeof(W) == 8;
@@ -1662,9 +1665,8 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
 
 }  // namespace
 
-cudaError_t launch_discover(const GraphView& g, Workspace ws, int k, int sharded, cudaStream_t s, int blocks) {
-  mpld_component_discover<<<blocks, kCompWarps * 32, 0, s>>>(g, ws, k, sharded);
-  return cudaGetLastError();
+cudaError_t launch_discover(const GraphView& g, Workspace ws, int k, int sharded, cudaStream_t s, int blocks, bool pdl) {
+  return launch_ex(mpld_component_discover, dim3(blocks), dim3(kCompWarps * 32), 0, s, pdl, false, g, ws, k, sharded);
 }
 
 // Inclusive prefix sum of ws.est[0..n) (the balanced shard partition): block
@@ -1749,20 +1751,17 @@ cudaError_t launch_partition_scan(const GraphView& g, Workspace ws, cudaStream_t
 
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
                           unsigned light_steps, long long* counts, int shard_index, int shard_count, cudaStream_t s,
-                          int blocks) {
+                          int blocks, bool pdl) {
   switch (k) {
     case 2:
-      mpld_exact_cover_search<2><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
-                                                                     counts, shard_index, shard_count);
-      break;
+      return launch_ex(mpld_exact_cover_search<2>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws, w_stitch,
+                       max_steps, colors, light_steps, counts, shard_index, shard_count);
     case 3:
-      mpld_exact_cover_search<3><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
-                                                                     counts, shard_index, shard_count);
-      break;
+      return launch_ex(mpld_exact_cover_search<3>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws, w_stitch,
+                       max_steps, colors, light_steps, counts, shard_index, shard_count);
     case 4:
-      mpld_exact_cover_search<4><<<blocks, kLaneWarps * 32, 0, s>>>(g, ws, w_stitch, max_steps, colors, light_steps,
-                                                                     counts, shard_index, shard_count);
-      break;
+      return launch_ex(mpld_exact_cover_search<4>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws, w_stitch,
+                       max_steps, colors, light_steps, counts, shard_index, shard_count);
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -1770,22 +1769,20 @@ cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch,
 
 template <int K>
 cudaError_t launch_heavy_k(const GraphView& g, Workspace ws, int w_stitch, int* colors, long long* counts,
-                           cudaStream_t s, const int* blocks) {
-  mpld_exact_cover_search_heavy<K, unsigned>
-      <<<blocks[0], 32, heavy_smem<K, unsigned>(), s>>>(g, ws, w_stitch, colors, counts);
-  cudaError_t e = cudaGetLastError();
+                           cudaStream_t s, const int* blocks, bool pdl) {
+  cudaError_t e = launch_ex(mpld_exact_cover_search_heavy<K, unsigned>, dim3(blocks[0]), dim3(32),
+                            heavy_smem<K, unsigned>(), s, pdl, false, g, ws, w_stitch, colors, counts);
   if (e != cudaSuccess) return e;
-  mpld_exact_cover_search_heavy<K, unsigned long long>
-      <<<blocks[1], 32, heavy_smem<K, unsigned long long>(), s>>>(g, ws, w_stitch, colors, counts);
-  return cudaGetLastError();
+  return launch_ex(mpld_exact_cover_search_heavy<K, unsigned long long>, dim3(blocks[1]), dim3(32),
+                   heavy_smem<K, unsigned long long>(), s, true, false, g, ws, w_stitch, colors, counts);
 }
 
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, long long* counts,
-                                cudaStream_t s, const int* blocks) {
+                                cudaStream_t s, const int* blocks, bool pdl) {
   switch (k) {
-    case 2: return launch_heavy_k<2>(g, ws, w_stitch, colors, counts, s, blocks + 0);
-    case 3: return launch_heavy_k<3>(g, ws, w_stitch, colors, counts, s, blocks + 2);
-    case 4: return launch_heavy_k<4>(g, ws, w_stitch, colors, counts, s, blocks + 4);
+    case 2: return launch_heavy_k<2>(g, ws, w_stitch, colors, counts, s, blocks + 0, pdl);
+    case 3: return launch_heavy_k<3>(g, ws, w_stitch, colors, counts, s, blocks + 2, pdl);
+    case 4: return launch_heavy_k<4>(g, ws, w_stitch, colors, counts, s, blocks + 4, pdl);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -24,6 +24,8 @@ namespace mpld {
 
 namespace {
 
+bool g_pdl = true;
+
 #ifndef MPLD_GRAPH_P
 #define MPLD_GRAPH_P 1
 #endif
@@ -679,6 +681,7 @@ __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, in
 // and the last CTA of the recovery writes the costs and statistics.
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover(GraphView g, Workspace w, int k, int* colors,
                                                                     Outputs out) {
+  pdl_begin();
   GridBarrier grid(&w.ctl->bar1);
   __shared__ CtaQueues Q;
   cq_init(Q);
@@ -796,6 +799,9 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
 
 }  // namespace
 
+bool pdl_enabled() { return g_pdl; }
+void set_pdl(bool enable) { g_pdl = enable; }
+
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors, long long* counts,
                                        int validate, cudaStream_t s, int blocks, int threads) {
   GraphView gg = g;
@@ -804,10 +810,8 @@ cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, 
 }
 
 cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
-                           int blocks, int threads) {
-  GraphView gg = g;
-  void* args[] = {&gg, &ws, &k, &colors, &out};
-  return cudaLaunchCooperativeKernel((void*)mpld_recover, dim3(blocks), dim3(threads), args, 0, s);
+                           int blocks, int threads, bool pdl) {
+  return launch_ex(mpld_recover, dim3(blocks), dim3(threads), 0, s, pdl, true, g, ws, k, colors, out);
 }
 
 cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors, double alpha, long long* counts,

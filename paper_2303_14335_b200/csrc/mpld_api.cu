@@ -112,6 +112,7 @@ struct mpld_context {
   int blocks_heavy[6] = {0, 0, 0, 0, 0, 0};  // per k = 2..4 and word class (32-bit, 64-bit)
   long long* counts = nullptr;  // the prepare phase's d_counts (zeroed by the simplification kernel)
   bool search_counted = false;  // the search accumulated the counts (one shard)
+  int searches_since_prepare = 0;
   // host-API staging (device copies of host inputs / outputs)
   int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
   int* h_lo = nullptr;
@@ -225,6 +226,7 @@ int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, 
   ctx->k = k;
   ctx->counts = counts;
   ctx->search_counted = false;
+  ctx->searches_since_prepare = 0;
   ctx->prepared = true;
   ctx->call_launches = 0;
   // the control block (counters, barrier arrivals, error bits) starts every call at zero
@@ -244,11 +246,16 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
                  int shard_count, int* colors) {
   Workspace ws = workspace(ctx);
   const GraphView& g = ctx->g;
-  // the component pool and the heavy queue belong to this search call (several shards may share a context)
-  cudaError_t e0 = cudaMemsetAsync(&ctx->ctl->n_heavy, 0,
-                                   offsetof(Control, comp_pool) + sizeof(unsigned long long) -
-                                       offsetof(Control, n_heavy), s);
-  if (e0 != cudaSuccess) return cuda_fail(e0, "search counters reset");
+  // the component pool and the heavy queue belong to this search call (several
+  // shards may share a context); the first search after prepare finds them zeroed
+  // by the call's control reset, so the kernels follow each other directly (PDL)
+  const bool pdl = ctx->searches_since_prepare++ == 0;
+  if (!pdl) {
+    cudaError_t e0 = cudaMemsetAsync(&ctx->ctl->n_heavy, 0,
+                                     offsetof(Control, comp_pool) + sizeof(unsigned long long) -
+                                         offsetof(Control, n_heavy), s);
+    if (e0 != cudaSuccess) return cuda_fail(e0, "search counters reset");
+  }
   // one shard: the search kernels accumulate the Eq. (1) counts of the final
   // colourings (the recovery adds no conflict, R9), so the finish
   // phase needs no evaluation pass
@@ -265,7 +272,7 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
   }
   {
     TimedLaunch t(ctx, K_DISCOVER, s);
-    cudaError_t e = launch_discover(g, ws, ctx->k, sharded, s, ctx->blocks_discover);
+    cudaError_t e = launch_discover(g, ws, ctx->k, sharded, s, ctx->blocks_discover, pdl && !sharded);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_component_discover");
     t.done();
     ++ctx->call_launches;
@@ -278,14 +285,14 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
   {
     TimedLaunch t(ctx, K_SEARCH, s);
     cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, count, shard_index,
-                                  shard_count, s, ctx->blocks_search);
+                                  shard_count, s, ctx->blocks_search, !sharded);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
     t.done();
     ++ctx->call_launches;
   }
   if (max_steps <= 0) {  // exact mode: heavy components on the warp-parallel search
     TimedLaunch t(ctx, K_SEARCH_HEAVY, s);
-    cudaError_t e = launch_search_heavy(g, ws, ctx->k, w_stitch, colors, count, s, ctx->blocks_heavy);
+    cudaError_t e = launch_search_heavy(g, ws, ctx->k, w_stitch, colors, count, s, ctx->blocks_heavy, true);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_heavy");
     t.done();
     ctx->call_launches += 2;  // one launch per word class
@@ -307,7 +314,10 @@ int phase_finish(mpld_context* ctx, cudaStream_t s, double alpha, int* colors, l
   {
     TimedLaunch t(ctx, K_RECOVER, s);
     out.launches = ++ctx->call_launches;
-    cudaError_t e = launch_recover(g, ws, ctx->k, colors, out, s, ctx->blocks_recover, kCoopThreads);
+    // PDL after the search kernels of the same thread of calls (a sharded run
+    // puts an all-reduce between the search and this call)
+    cudaError_t e = launch_recover(g, ws, ctx->k, colors, out, s, ctx->blocks_recover, kCoopThreads,
+                                   ctx->search_counted);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_recover");
     t.done();
   }
@@ -449,6 +459,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   ctx->blocks_search = resident_blocks_search(32, ctx->num_sms);
   ctx->blocks_discover = resident_blocks_discover(ctx->num_sms);
   ctx->blocks_stream = resident_blocks_evaluate(ctx->num_sms);
+  if (const char* pd = std::getenv("MPLD_PDL")) set_pdl(std::strtol(pd, nullptr, 10) != 0);
   if (const char* hs = std::getenv("MPLD_HEAVY_SPILL")) {
     const long v = std::strtol(hs, nullptr, 10);
     if (v >= 64) ctx->spill_iters = (unsigned)std::min<long>(v & ~63L, 1L << 30);

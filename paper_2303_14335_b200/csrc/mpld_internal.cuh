@@ -195,21 +195,59 @@ __host__ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
   return x;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with the attribute
+// may be scheduled while its predecessor in the stream drains; it triggers
+// its own dependents and waits for its predecessor's memory at its first
+// statement (both no-ops without the attribute).
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+bool pdl_enabled();         // MPLD_PDL=0 disables it (A/B measurements)
+void set_pdl(bool enable);
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                      bool coop, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  unsigned na = 0;
+  if (pdl && pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // launch wrappers (kernels_graph.cu, kernel_search.cu); each returns the
-// cudaError_t of its launch.
+// cudaError_t of its launch.  `pdl`: the stream's previous operation is one
+// of these kernels.
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors,
                                        long long* counts, int validate, cudaStream_t s, int blocks, int threads);
-cudaError_t launch_discover(const GraphView& g, Workspace ws, int k, int sharded, cudaStream_t s, int blocks);
+cudaError_t launch_discover(const GraphView& g, Workspace ws, int k, int sharded, cudaStream_t s, int blocks, bool pdl);
 cudaError_t launch_partition_scan(const GraphView& g, Workspace ws, cudaStream_t s);  // inclusive scan of ws.est
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
                           unsigned light_steps, long long* counts, int shard_index, int shard_count, cudaStream_t s,
-                          int blocks);
+                          int blocks, bool pdl);
 constexpr unsigned kLightStepsDefault = 48;  // exact mode: one-lane budget before a component turns heavy
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, long long* counts,
-                                cudaStream_t s, const int* blocks);
+                                cudaStream_t s, const int* blocks, bool pdl);
 cudaError_t configure_search_heavy(int num_sms, int* blocks);  // blocks[6]: resident grids of the heavy kernels
 cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
-                           int blocks, int threads);
+                           int blocks, int threads, bool pdl);
 cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors, double alpha,
                             long long* counts, double* cost, long long* stats, int launches,
                             cudaStream_t s, int blocks);
