@@ -48,6 +48,10 @@ constexpr int kNb = MPLD_GRAPH_NB;  // neighbours per item and batch of independ
 #define MPLD_TAIL 1024
 #endif
 constexpr int kTail = MPLD_TAIL;  // frontiers up to this size are finished by CTA 0 alone
+#ifndef MPLD_GROUP
+#define MPLD_GROUP 16
+#endif
+constexpr int kGroup = MPLD_GROUP;  // frontiers up to kGroup * blockDim items: the first kGroup CTAs, group barriers
 constexpr int kStitchDeg = 1 << 29;  // live degree of stitch vertices: never reaches k (never hidden, R8)
 
 __device__ __forceinline__ void stamp(Control* ctl, int i) {
@@ -424,39 +428,14 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
   }
   if (__ldcg(&ctl->err)) return;  // invalid input: every later kernel exits too
 
-  // rounds r >= 1: push the frontier's decrements
+  // rounds r >= 1: push the frontier's decrements.  Large frontiers: every
+  // CTA, one grid barrier per round; up to kGroup * blockDim items: the first
+  // kGroup CTAs with their own barrier; up to kTail items: CTA 0 alone with
+  // block barriers (a barrier over fewer CTAs is cheaper; the rounds only need
+  // the dependent-load latency).  Everyone meets at one grid barrier after.
   int r = 1;
-  while (true) {
-    const int cnt = __ldcg(&ctl->qcnt[r % 3]);
-    if (cnt == 0) break;
-    if (cnt <= kTail) {
-      // small frontier: CTA 0 runs the remaining rounds alone with block
-      // barriers (a grid barrier costs ~1.5 µs; the rounds only need the
-      // dependent-load latency)
-      if (blockIdx.x == 0) {
-        int rr = r, c = cnt;
-        TailFrontier tf;
-        tf.g_in = (r & 1) ? w.q1 : w.q0;
-        while (c > 0) {
-          // own overflow counter: the other CTAs may still be reading qcnt[r % 3] to take this branch
-          if (threadIdx.x == 0) {
-            ctl->tcnt[0] = 0;
-            ctl->n_hidden += c;
-          }
-          dstamp(ctl, rr, c);
-          __syncthreads();
-          peel_round(g, w, k, rr, c, 0, blockDim.x * kP, tf.s_in(Q), tf.s_cnt, tf.g_in, Q, tf.out_slot,
-                     &ctl->tcnt[0], tf.g_out(w));
-          ++rr;
-          c = tf.advance(Q, w);
-        }
-        tf.finish(Q);
-        if (threadIdx.x == 0) ctl->n_rounds = rr;
-      }
-      grid.sync();
-      r = __ldcg(&ctl->n_rounds);
-      break;
-    }
+  int cnt = __ldcg(&ctl->qcnt[1]);
+  while (cnt > kGroup * (int)blockDim.x) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctl->qcnt[(r + 2) % 3] = 0;
       ctl->n_hidden += cnt;
@@ -472,7 +451,50 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
     ++r;
     grid.sync();
     stamp(w.ctl, 2);
+    cnt = __ldcg(&ctl->qcnt[r % 3]);
   }
+  if (cnt > kTail && (int)blockIdx.x < kGroup) {  // group rounds (every CTA read the same cnt)
+    GridBarrier grp(&ctl->bar0g, kGroup);
+    while (cnt > kTail) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->qcnt[(r + 2) % 3] = 0;
+        ctl->n_hidden += cnt;
+      }
+      dstamp(ctl, r, cnt);
+      const int* cur = (r & 1) ? w.q1 : w.q0;
+      int* nxt = (r & 1) ? w.q0 : w.q1;
+      int* ncnt = &ctl->qcnt[(r + 1) % 3];
+      peel_round(g, w, k, r, cnt, blockIdx.x * blockDim.x * kP, kGroup * blockDim.x * kP, nullptr, 0, cur, Q, 0,
+                 ncnt, nxt);
+      cq_flush(Q, 0, ncnt, nxt);
+      ++r;
+      grp.sync();
+      cnt = __ldcg(&ctl->qcnt[r % 3]);
+    }
+  }
+  if (blockIdx.x == 0) {
+    if (cnt > 0) {  // the single-CTA tail, frontier in shared memory
+      int c = cnt;
+      TailFrontier tf;
+      tf.g_in = (r & 1) ? w.q1 : w.q0;
+      while (c > 0) {
+        if (threadIdx.x == 0) {
+          ctl->tcnt[0] = 0;  // own overflow counter
+          ctl->n_hidden += c;
+        }
+        dstamp(ctl, r, c);
+        __syncthreads();
+        peel_round(g, w, k, r, c, 0, blockDim.x * kP, tf.s_in(Q), tf.s_cnt, tf.g_in, Q, tf.out_slot,
+                   &ctl->tcnt[0], tf.g_out(w));
+        ++r;
+        c = tf.advance(Q, w);
+      }
+      tf.finish(Q);
+    }
+    if (threadIdx.x == 0) ctl->n_rounds = r;
+  }
+  grid.sync();
+  r = __ldcg(&ctl->n_rounds);
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_rounds = __ldcg(&ctl->n_hidden) ? r : 0;
   stamp(w.ctl, 1);
 
@@ -695,31 +717,13 @@ __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, in
   const int nth = gridDim.x * blockDim.x;
   Control* ctl = w.ctl;
   const int tile0 = blockIdx.x * blockDim.x * kP, tstride = nth * kP;
+  // as the simplification rounds: every CTA for large levels, the first
+  // kGroup CTAs with their own barrier for levels up to kGroup * blockDim
+  // items, CTA 0 alone (frontier in shared memory) for the last small levels
   int L = 0;
-  while (true) {
-    const int cnt = __ldcg(&ctl->rq[L % 3]);
+  int cnt = __ldcg(&ctl->rq[0]);
+  while (cnt > kGroup * (int)blockDim.x) {
     dstamp(ctl, 16 + L, cnt);
-    if (cnt == 0) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_levels = L;
-      break;
-    }
-    if (cnt <= kTail) {  // small level: CTA 0 finishes the remaining levels with block barriers
-      if (blockIdx.x == 0) {
-        int LL = L, c = cnt;
-        TailFrontier tf;
-        tf.g_in = (L & 1) ? w.q1 : w.q0;
-        while (c > 0) {
-          if (threadIdx.x == 0) ctl->trq[0] = 0;  // own overflow counter, as in the simplification tail
-          __syncthreads();
-          recover_level(g, w, k, colors, c, 0, blockDim.x * kP, tf.s_in(Q), tf.s_cnt, tf.g_in, Q, tf.out_slot,
-                        &ctl->trq[0], tf.g_out(w));
-          ++LL;
-          c = tf.advance(Q, w);
-        }
-        if (threadIdx.x == 0) ctl->n_levels = LL;
-      }
-      break;  // no grid barrier needed: the kernel ends here
-    }
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->rq[(L + 2) % 3] = 0;
     {
       const int* cur = (L & 1) ? w.q1 : w.q0;
@@ -731,6 +735,39 @@ __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, in
     ++L;
     grid.sync();
     stamp(w.ctl, 9);
+    cnt = __ldcg(&ctl->rq[L % 3]);
+  }
+  if (cnt > kTail && (int)blockIdx.x < kGroup) {  // group levels (every CTA read the same cnt)
+    GridBarrier grp(&ctl->bar1g, kGroup);
+    while (cnt > kTail) {
+      dstamp(ctl, 16 + L, cnt);
+      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->rq[(L + 2) % 3] = 0;
+      const int* cur = (L & 1) ? w.q1 : w.q0;
+      int* nxt = (L & 1) ? w.q0 : w.q1;
+      int* ncnt = &ctl->rq[(L + 1) % 3];
+      recover_level(g, w, k, colors, cnt, blockIdx.x * blockDim.x * kP, kGroup * blockDim.x * kP, nullptr, 0, cur,
+                    Q, 0, ncnt, nxt);
+      cq_flush(Q, 0, ncnt, nxt);
+      ++L;
+      grp.sync();
+      cnt = __ldcg(&ctl->rq[L % 3]);
+    }
+  }
+  if (blockIdx.x == 0) {
+    if (cnt > 0) {  // the single-CTA tail
+      int c = cnt;
+      TailFrontier tf;
+      tf.g_in = (L & 1) ? w.q1 : w.q0;
+      while (c > 0) {
+        if (threadIdx.x == 0) ctl->trq[0] = 0;  // own overflow counter, as in the simplification tail
+        __syncthreads();
+        recover_level(g, w, k, colors, c, 0, blockDim.x * kP, tf.s_in(Q), tf.s_cnt, tf.g_in, Q, tf.out_slot,
+                      &ctl->trq[0], tf.g_out(w));
+        ++L;
+        c = tf.advance(Q, w);
+      }
+    }
+    if (threadIdx.x == 0) ctl->n_levels = L;
   }
 }
 

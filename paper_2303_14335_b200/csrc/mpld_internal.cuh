@@ -45,6 +45,8 @@ struct Control {
   int trq[3];
   alignas(128) unsigned bar0;  // grid-barrier arrival counter of mpld_simplify_components
   alignas(128) unsigned bar1;  // ... of mpld_recover
+  alignas(128) unsigned bar0g; // group barriers (the first kGroup CTAs) of the two kernels
+  alignas(128) unsigned bar1g;
   alignas(128) int n_comp;     // components found (counted by the discovery kernel)
   int max_comp;                // largest component
   alignas(128) int truncated;  // components whose search hit max_steps
@@ -80,6 +82,7 @@ struct GridBarrier {
   unsigned nblocks;
   unsigned epoch;
   __device__ __forceinline__ GridBarrier(unsigned* c) : count(c), nblocks(gridDim.x), epoch(0) {}
+  __device__ __forceinline__ GridBarrier(unsigned* c, unsigned nb) : count(c), nblocks(nb), epoch(0) {}
   __device__ __forceinline__ void sync() {
     __syncthreads();
     if (threadIdx.x == 0) {
