@@ -51,6 +51,20 @@ constexpr int kTail = MPLD_TAIL;  // frontiers up to this size are finished by C
 #ifndef MPLD_GROUP
 #define MPLD_GROUP 16
 #endif
+#ifndef MPLD_CLUSTER_TAIL
+#define MPLD_CLUSTER_TAIL 1
+#endif
+#ifndef MPLD_CLUSTER
+#define MPLD_CLUSTER 16
+#endif
+#ifndef MPLD_TAIL_LOCAL
+#define MPLD_TAIL_LOCAL 1
+#endif
+#ifndef MPLD_CLUSTER_ROUNDS
+#define MPLD_CLUSTER_ROUNDS 0  // measured slower in the PDL chain: off
+#endif
+constexpr int kTC = MPLD_CLUSTER;                // CTAs of the recovery's cluster tail
+constexpr int kClusterTailMax = kTC * 1024;      // levels up to this size go to the cluster tail
 constexpr int kGroup = MPLD_GROUP;  // frontiers up to kGroup * blockDim items: the first kGroup CTAs, group barriers
 constexpr int kStitchDeg = 1 << 29;  // live degree of stitch vertices: never reaches k (never hidden, R8)
 
@@ -255,6 +269,95 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
   }
 }
 
+// The final pass of the simplification (the rounds are final): see the
+// comment at its call in mpld_simplify_components.
+__device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q) {
+  const int n = g.n;
+  const int nth = gridDim.x * blockDim.x;
+  const int tile0f = blockIdx.x * blockDim.x * kPF, tstridef = nth * kPF;
+  Control* ctl = w.ctl;
+  // One batched walk over the CE row of every vertex: a hidden vertex counts
+  // its predecessors, a kept one looks for a kept neighbour of smaller id
+  // (rows ascending: the walk stops at the first larger id).
+  for (int t0 = tile0f; t0 < n; t0 += tstridef) {
+    int v[kPF], e0[kPF], e[kPF], e1[kPF], cnt[kPF];
+    unsigned long long kv[kPF], bm[kPF];
+    bool seed[kPF];
+#pragma unroll
+    for (int j = 0; j < kPF; ++j) {
+      v[j] = t0 + j * blockDim.x + threadIdx.x;
+      const int hv = v[j] < n ? __ldcg(&w.hround[v[j]]) : -1;
+      kv[j] = v[j] < n ? pop_key(hv, __ldcg(&w.prio[v[j]])) : ~0ull;
+      e[j] = e0[j] = v[j] < n ? __ldg(&g.ce_rp[v[j]]) : 0;
+      e1[j] = v[j] < n ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
+      cnt[j] = 0;
+      bm[j] = 0ull;
+      seed[j] = true;
+    }
+    while (true) {
+      bool open = false;
+#pragma unroll
+      for (int j = 0; j < kPF; ++j) open |= e[j] < e1[j];
+      if (!open) break;
+      int u[kPF][kNb], hu[kPF][kNb];
+      unsigned pu[kPF][kNb];
+#pragma unroll
+      for (int j = 0; j < kPF; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) u[j][t] = e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
+#pragma unroll
+      for (int j = 0; j < kPF; ++j)
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) {
+          hu[j][t] = u[j][t] >= 0 ? __ldcg(&w.hround[u[j][t]]) : -1;
+          pu[j][t] = u[j][t] >= 0 && kv[j] != ~0ull ? __ldcg(&w.prio[u[j][t]]) : 0u;
+        }
+#pragma unroll
+      for (int j = 0; j < kPF; ++j) {
+        bool past = false;  // kept v: a neighbour above v was seen
+#pragma unroll
+        for (int t = 0; t < kNb; ++t) {
+          if (u[j][t] < 0) continue;
+          if (kv[j] != ~0ull) {
+            const bool before = pop_key(hu[j][t], pu[j][t]) > kv[j];  // popped before v, or kept
+            cnt[j] += (hu[j][t] >= 0 && before) ? 1 : 0;
+            const int rel = e[j] + t - e0[j];
+            if (rel < 64 && before) bm[j] |= 1ull << rel;
+          } else {
+            if (u[j][t] < v[j] && hu[j][t] == -1) seed[j] = false;
+            past |= u[j][t] > v[j];
+          }
+        }
+        e[j] = (kv[j] == ~0ull && (past || !seed[j])) ? e1[j] : e[j] + kNb;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kPF; ++j) {
+      if (v[j] >= n) continue;
+      if (kv[j] != ~0ull) {
+        w.deg[v[j]] = cnt[j];
+        w.bmask[v[j]] = bm[j];
+        if (cnt[j] == 0) cq_push(Q, 1, v[j], &ctl->rq[0], w.q0);
+      } else {
+        // stitch neighbours (stitch vertices only; rows ascending)
+        if (seed[j])
+          for (int x = __ldg(&g.se_rp[v[j]]), x1 = __ldg(&g.se_rp[v[j] + 1]); x < x1; ++x) {
+            const int u = __ldg(&g.se_col[x]);
+            if (u > v[j]) break;
+            if (__ldcg(&w.hround[u]) == -1) {
+              seed[j] = false;
+              break;
+            }
+          }
+        if (seed[j]) cq_push(Q, 0, v[j], &ctl->n_seed, w.roots);
+      }
+    }
+  }
+  cq_flush(Q, 0, &ctl->n_seed, w.roots);
+  cq_flush(Q, 1, &ctl->rq[0], w.q0);
+  stamp(w.ctl, 3);
+}
+
 // ---------------------------------------------------------------------------
 // Simplification (R8, §2.2 "simplify the layout graph"):
 // round r hides every not-yet-hidden vertex without stitch edges whose
@@ -267,7 +370,8 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 // Then one pass over all vertices writes the recovery pop keys, the search
 // seeds and the recovery's predecessor counts and level 0.
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_components(GraphView g, Workspace w, int k,
-                                                                    int* colors, long long* counts, int validate) {
+                                                                    int* colors, long long* counts, int validate,
+                                                                    int cluster_rounds) {
   GridBarrier grid(&w.ctl->bar0);
   __shared__ CtaQueues Q;
   cq_init(Q);
@@ -435,7 +539,8 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
   // the dependent-load latency).  Everyone meets at one grid barrier after.
   int r = 1;
   int cnt = __ldcg(&ctl->qcnt[1]);
-  while (cnt > kGroup * (int)blockDim.x) {
+  const int grid_min = cluster_rounds ? kClusterTailMax : kGroup * (int)blockDim.x;
+  while (cnt > grid_min) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctl->qcnt[(r + 2) % 3] = 0;
       ctl->n_hidden += cnt;
@@ -452,6 +557,10 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
     grid.sync();
     stamp(w.ctl, 2);
     cnt = __ldcg(&ctl->qcnt[r % 3]);
+  }
+  if (cluster_rounds) {  // the remaining rounds: mpld_simplify_tail, then mpld_final_pass
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_rounds = r;
+    return;
   }
   if (cnt > kTail && (int)blockIdx.x < kGroup) {  // group rounds (every CTA read the same cnt)
     GridBarrier grp(&ctl->bar0g, kGroup);
@@ -506,86 +615,94 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
   //    so no union-find and no further grid barrier are needed here;
   //  * recovery: hidden predecessors of every hidden vertex (conflict
   //    neighbours popped before it) and level 0 = the vertices without one.
-  // One batched walk over the CE row of every vertex: a hidden vertex counts
-  // its predecessors, a kept one looks for a kept neighbour of smaller id
-  // (rows ascending: the walk stops at the first larger id).
-  for (int t0 = tile0f; t0 < n; t0 += tstridef) {
-    int v[kPF], e0[kPF], e[kPF], e1[kPF], cnt[kPF];
-    unsigned long long kv[kPF], bm[kPF];
-    bool seed[kPF];
+  final_pass(g, w, Q);
+}
+
+// ---------------------------------------------------------------------------
+// The last simplification rounds (<= kClusterTailMax hidden vertices) on ONE
+// thread-block cluster: every CTA pushes the decrements of the vertices its
+// own threads hid (frontier slots in its shared memory, no global queue), the
+// rounds are separated by the hardware cluster barrier.  Then
+// mpld_final_pass runs the final pass on the whole GPU.
+template <typename Push>
+__device__ __forceinline__ void peel_vertex(const GraphView& g, const Workspace& w, int k, int r, int v, Push push) {
+  const int e1 = __ldg(&g.ce_rp[v + 1]);
+  for (int e = __ldg(&g.ce_rp[v]); e < e1; e += kNb) {
+    int u[kNb], old[kNb];
 #pragma unroll
-    for (int j = 0; j < kPF; ++j) {
-      v[j] = t0 + j * blockDim.x + threadIdx.x;
-      const int hv = v[j] < n ? __ldcg(&w.hround[v[j]]) : -1;
-      kv[j] = v[j] < n ? pop_key(hv, __ldcg(&w.prio[v[j]])) : ~0ull;
-      e[j] = e0[j] = v[j] < n ? __ldg(&g.ce_rp[v[j]]) : 0;
-      e1[j] = v[j] < n ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
-      cnt[j] = 0;
-      bm[j] = 0ull;
-      seed[j] = true;
-    }
-    while (true) {
-      bool open = false;
+    for (int t = 0; t < kNb; ++t) u[t] = e + t < e1 ? __ldg(&g.ce_col[e + t]) : -1;
 #pragma unroll
-      for (int j = 0; j < kPF; ++j) open |= e[j] < e1[j];
-      if (!open) break;
-      int u[kPF][kNb], hu[kPF][kNb];
-      unsigned pu[kPF][kNb];
+    for (int t = 0; t < kNb; ++t) old[t] = u[t] >= 0 ? atomicSub(&w.deg[u[t]], 1) : 0;
 #pragma unroll
-      for (int j = 0; j < kPF; ++j)
-#pragma unroll
-        for (int t = 0; t < kNb; ++t) u[j][t] = e[j] + t < e1[j] ? __ldg(&g.ce_col[e[j] + t]) : -1;
-#pragma unroll
-      for (int j = 0; j < kPF; ++j)
-#pragma unroll
-        for (int t = 0; t < kNb; ++t) {
-          hu[j][t] = u[j][t] >= 0 ? __ldcg(&w.hround[u[j][t]]) : -1;
-          pu[j][t] = u[j][t] >= 0 && kv[j] != ~0ull ? __ldcg(&w.prio[u[j][t]]) : 0u;
-        }
-#pragma unroll
-      for (int j = 0; j < kPF; ++j) {
-        bool past = false;  // kept v: a neighbour above v was seen
-#pragma unroll
-        for (int t = 0; t < kNb; ++t) {
-          if (u[j][t] < 0) continue;
-          if (kv[j] != ~0ull) {
-            const bool before = pop_key(hu[j][t], pu[j][t]) > kv[j];  // popped before v, or kept
-            cnt[j] += (hu[j][t] >= 0 && before) ? 1 : 0;
-            const int rel = e[j] + t - e0[j];
-            if (rel < 64 && before) bm[j] |= 1ull << rel;
-          } else {
-            if (u[j][t] < v[j] && hu[j][t] == -1) seed[j] = false;
-            past |= u[j][t] > v[j];
-          }
-        }
-        e[j] = (kv[j] == ~0ull && (past || !seed[j])) ? e1[j] : e[j] + kNb;
+    for (int t = 0; t < kNb; ++t)
+      if (old[t] == k) {  // live degree k -> k-1: hidden in round r + 1 (see peel_round)
+        w.hround[u[t]] = r + 1;
+        push(u[t]);
       }
-    }
-#pragma unroll
-    for (int j = 0; j < kPF; ++j) {
-      if (v[j] >= n) continue;
-      if (kv[j] != ~0ull) {
-        w.deg[v[j]] = cnt[j];
-        w.bmask[v[j]] = bm[j];
-        if (cnt[j] == 0) cq_push(Q, 1, v[j], &ctl->rq[0], w.q0);
-      } else {
-        // stitch neighbours (stitch vertices only; rows ascending)
-        if (seed[j])
-          for (int x = __ldg(&g.se_rp[v[j]]), x1 = __ldg(&g.se_rp[v[j] + 1]); x < x1; ++x) {
-            const int u = __ldg(&g.se_col[x]);
-            if (u > v[j]) break;
-            if (__ldcg(&w.hround[u]) == -1) {
-              seed[j] = false;
-              break;
-            }
-          }
-        if (seed[j]) cq_push(Q, 0, v[j], &ctl->n_seed, w.roots);
-      }
-    }
   }
-  cq_flush(Q, 0, &ctl->n_seed, w.roots);
-  cq_flush(Q, 1, &ctl->rq[0], w.q0);
-  stamp(w.ctl, 3);
+}
+
+constexpr int kTQ = 4096;  // frontier slots per CTA and parity of the cluster tails
+
+__global__ void __launch_bounds__(1024) mpld_simplify_tail(GraphView g, Workspace w, int k) {
+  pdl_begin();
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ int s_item[2][kTQ];
+  __shared__ int s_n[2];
+  __shared__ int s_tot;
+  const int rank = (int)cl.block_rank(), nc = (int)cl.num_blocks();
+  Control* ctl = w.ctl;
+  if (threadIdx.x < 2) s_n[threadIdx.x] = 0;
+  cl.sync();
+  const bool ok = !__ldcg(&ctl->err);
+  int r = ok ? __ldcg(&ctl->n_rounds) : 0;  // the first round the grid kernel left
+  int total = ok ? __ldcg(&ctl->qcnt[r % 3]) : 0;
+  const int* g_first = (r & 1) ? w.q1 : w.q0;
+  int* const ovf[2] = {w.q0 == g_first ? w.q1 : w.q0, w.roots};  // spill lists (not the first frontier)
+  int n_ovf = 0;
+  for (int t = 0; total > 0; ++t) {
+    const int in = t & 1, outs = in ^ 1;
+    if (threadIdx.x == 0) s_n[outs] = 0;
+    if (rank == 0 && threadIdx.x == 0) {
+      ctl->tovf[outs] = 0;
+      ctl->n_hidden += total;
+    }
+    __syncthreads();
+    auto push = [&](int u) {
+      const int i = atomicAdd(&s_n[outs], 1);
+      if (i < kTQ) s_item[outs][i] = u;
+      else ovf[outs][atomicAdd(&ctl->tovf[outs], 1)] = u;
+    };
+    if (t == 0) {
+      for (int i = rank * (int)blockDim.x + threadIdx.x; i < total; i += nc * (int)blockDim.x)
+        peel_vertex(g, w, k, r, __ldcg(&g_first[i]), push);
+    } else {
+      const int mine = min(s_n[in], kTQ);
+      for (int i = threadIdx.x; i < mine; i += blockDim.x) peel_vertex(g, w, k, r, s_item[in][i], push);
+      for (int i = rank * (int)blockDim.x + threadIdx.x; i < n_ovf; i += nc * (int)blockDim.x)
+        peel_vertex(g, w, k, r, __ldcg(&ovf[in][i]), push);
+    }
+    cl.sync();  // the round's decrements are done; every CTA's output slot is complete
+    if (threadIdx.x < 32) {
+      const int x = (int)threadIdx.x < nc ? min(*cl.map_shared_rank(&s_n[outs], (int)threadIdx.x), kTQ) : 0;
+      const int sum = __reduce_add_sync(0xffffffffu, x);
+      if (threadIdx.x == 0) s_tot = sum;
+    }
+    __syncthreads();
+    n_ovf = __ldcg(&ctl->tovf[outs]);
+    total = s_tot + n_ovf;
+    ++r;
+  }
+  cl.sync();  // no CTA leaves while others may still read its shared memory
+  if (rank == 0 && threadIdx.x == 0) ctl->n_rounds = __ldcg(&ctl->n_hidden) ? r : 0;
+}
+
+__global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_final_pass(GraphView g, Workspace w) {
+  pdl_begin();
+  __shared__ CtaQueues Q;
+  cq_init(Q);
+  if (__ldcg(&w.ctl->err)) return;
+  final_pass(g, w, Q);
 }
 
 // ---------------------------------------------------------------------------
@@ -697,7 +814,7 @@ __device__ void finalize_outputs(const GraphView& g, const Workspace& w, const O
 }
 
 __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, int* colors, GridBarrier& grid,
-                               CtaQueues& Q);
+                               CtaQueues& Q, int cluster_tail);
 
 // With out.enabled the search kernels have accumulated the counts (one shard)
 // and the last CTA of the recovery writes the costs and statistics.
@@ -708,12 +825,12 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover(GraphView 
   __shared__ CtaQueues Q;
   cq_init(Q);
   stamp(w.ctl, 13);
-  if (!__ldcg(&w.ctl->err)) recover_levels(g, w, k, colors, grid, Q);
-  if (out.enabled) finalize_outputs(g, w, out, &w.ctl->done_recover);
+  if (!__ldcg(&w.ctl->err)) recover_levels(g, w, k, colors, grid, Q, out.cluster_tail);
+  if (out.enabled && !out.cluster_tail) finalize_outputs(g, w, out, &w.ctl->done_recover);
 }
 
 __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, int* colors, GridBarrier& grid,
-                               CtaQueues& Q) {
+                               CtaQueues& Q, int cluster_tail) {
   const int nth = gridDim.x * blockDim.x;
   Control* ctl = w.ctl;
   const int tile0 = blockIdx.x * blockDim.x * kP, tstride = nth * kP;
@@ -722,7 +839,8 @@ __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, in
   // items, CTA 0 alone (frontier in shared memory) for the last small levels
   int L = 0;
   int cnt = __ldcg(&ctl->rq[0]);
-  while (cnt > kGroup * (int)blockDim.x) {
+  const int grid_min = cluster_tail ? kClusterTailMax : kGroup * (int)blockDim.x;
+  while (cnt > grid_min) {
     dstamp(ctl, 16 + L, cnt);
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->rq[(L + 2) % 3] = 0;
     {
@@ -736,6 +854,10 @@ __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, in
     grid.sync();
     stamp(w.ctl, 9);
     cnt = __ldcg(&ctl->rq[L % 3]);
+  }
+  if (cluster_tail) {  // the remaining levels: mpld_recover_tail (one thread-block cluster)
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_levels = L;
+    return;
   }
   if (cnt > kTail && (int)blockIdx.x < kGroup) {  // group levels (every CTA read the same cnt)
     GridBarrier grp(&ctl->bar1g, kGroup);
@@ -769,6 +891,127 @@ __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, in
     }
     if (threadIdx.x == 0) ctl->n_levels = L;
   }
+}
+
+// ---------------------------------------------------------------------------
+// The last recovery levels (<= kClusterTailMax ready vertices) on ONE
+// thread-block cluster of kTC CTAs: the frontier lives in the CTAs' shared
+// memory (read across the cluster through distributed shared memory) and the
+// levels are separated by the hardware cluster barrier — no global counter,
+// flush or grid barrier per level.  Ready vertices beyond a CTA's kTQ slots
+// spill to a global list per level parity (roots / hcomp, free after the
+// search).  The last CTA writes the Eq. (1a) costs and the statistics.
+template <typename Push>
+__device__ __forceinline__ void recover_vertex(const GraphView& g, const Workspace& w, int k, int* colors, int v,
+                                               Push push) {
+  const int e0 = __ldg(&g.ce_rp[v]), e1 = __ldg(&g.ce_rp[v + 1]);
+  const unsigned long long bm = __ldcg(&w.bmask[v]);
+  const unsigned long long kv = e1 - e0 > 64 ? pop_key(__ldcg(&w.hround[v]), __ldcg(&w.prio[v])) : 0ull;
+  unsigned used = 0u;
+  for (int e = e0; e < e1; e += kNb) {
+    int u[kNb], x[kNb];
+    bool before[kNb];
+#pragma unroll
+    for (int t = 0; t < kNb; ++t) u[t] = e + t < e1 ? __ldg(&g.ce_col[e + t]) : -1;
+#pragma unroll
+    for (int t = 0; t < kNb; ++t) {  // popped before v (or kept): the final pass's bit, past 64 the keys
+      const int rel = e + t - e0;
+      before[t] = u[t] >= 0 && (rel < 64 ? ((bm >> rel) & 1ull) != 0ull
+                                         : pop_key(__ldcg(&w.hround[u[t]]), __ldcg(&w.prio[u[t]])) > kv);
+    }
+#pragma unroll
+    for (int t = 0; t < kNb; ++t) x[t] = u[t] < 0 ? -1 : (before[t] ? __ldcg(&colors[u[t]]) : atomicSub(&w.deg[u[t]], 1));
+#pragma unroll
+    for (int t = 0; t < kNb; ++t) {
+      if (u[t] < 0) continue;
+      if (before[t]) {
+        if (x[t] >= 0) used |= 1u << x[t];
+      } else if (x[t] == 1) {  // v was u's last predecessor
+        push(u[t]);
+      }
+    }
+  }
+  const int c = __ffs(~used) - 1;
+  colors[v] = c < k ? c : 0;  // c < k by the simplification invariant
+}
+
+__global__ void __launch_bounds__(1024) mpld_recover_tail(GraphView g, Workspace w, int k, int* colors, Outputs out) {
+  pdl_begin();
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ int s_item[2][kTQ];
+  __shared__ int s_n[2];
+  __shared__ int s_pref[kTC + 1];
+  const int rank = (int)cl.block_rank(), nc = (int)cl.num_blocks();
+  Control* ctl = w.ctl;
+  if (threadIdx.x < 2) s_n[threadIdx.x] = 0;
+  cl.sync();
+  int L = __ldcg(&ctl->n_levels);  // the first level the grid kernel left
+  int total = __ldcg(&ctl->err) ? 0 : __ldcg(&ctl->rq[L % 3]);
+  const int* g_first = (L & 1) ? w.q1 : w.q0;
+  int* const ovf[2] = {w.roots, w.hcomp};
+  int n_local = 0, n_ovf = 0;  // input level: items in the CTAs' slots, then in the global spill list
+  for (int t = 0; total > 0; ++t) {
+    const int in = t & 1, outs = in ^ 1;
+    if (threadIdx.x == 0) s_n[outs] = 0;  // read by the other CTAs two levels ago
+    if (rank == 0 && threadIdx.x == 0) ctl->tovf[outs] = 0;  // read two levels ago, written from the next level on
+    __syncthreads();
+    auto push = [&](int u) {
+      const int i = atomicAdd(&s_n[outs], 1);
+      if (i < kTQ) s_item[outs][i] = u;
+      else ovf[outs][atomicAdd(&ctl->tovf[outs], 1)] = u;
+    };
+#if MPLD_TAIL_LOCAL
+    // every CTA colours the vertices its own threads made ready (no remote
+    // reads), plus a strided share of the first level and of the spill list
+    if (t == 0) {
+      for (int i = rank * (int)blockDim.x + threadIdx.x; i < total; i += nc * (int)blockDim.x)
+        recover_vertex(g, w, k, colors, __ldcg(&g_first[i]), push);
+    } else {
+      const int mine = min(s_n[in], kTQ);
+      for (int i = threadIdx.x; i < mine; i += blockDim.x) recover_vertex(g, w, k, colors, s_item[in][i], push);
+      for (int i = rank * (int)blockDim.x + threadIdx.x; i < n_ovf; i += nc * (int)blockDim.x)
+        recover_vertex(g, w, k, colors, __ldcg(&ovf[in][i]), push);
+    }
+#else
+    for (int i = rank * (int)blockDim.x + threadIdx.x; i < total; i += nc * (int)blockDim.x) {
+      int v;
+      if (t == 0) {
+        v = __ldcg(&g_first[i]);
+      } else if (i < n_local) {
+        int lo = 0, hi = nc - 1;  // the CTA holding item i: s_pref[lo] <= i < s_pref[lo + 1]
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_pref[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        v = *cl.map_shared_rank(&s_item[in][i - s_pref[lo]], lo);
+      } else {
+        v = __ldcg(&ovf[in][i - n_local]);
+      }
+      recover_vertex(g, w, k, colors, v, push);
+    }
+#endif
+    cl.sync();  // the level is coloured; every CTA's output slot is complete
+    if (threadIdx.x < 32) {  // one remote count per lane, a warp scan
+      const int lane = threadIdx.x;
+      const int x = lane < nc ? min(*cl.map_shared_rank(&s_n[outs], lane), kTQ) : 0;
+      int y = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      if (lane < nc) s_pref[lane] = y - x;
+      if (lane == nc - 1) s_pref[nc] = y;
+    }
+    __syncthreads();
+    n_local = s_pref[nc];
+    n_ovf = __ldcg(&ctl->tovf[outs]);
+    total = n_local + n_ovf;
+    ++L;
+  }
+  if (rank == 0 && threadIdx.x == 0) ctl->n_levels = L;
+  cl.sync();  // no CTA leaves while others may still read its shared memory
+  if (out.enabled) finalize_outputs(g, w, out, &ctl->done_recover);
 }
 
 // ---------------------------------------------------------------------------
@@ -839,16 +1082,76 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
 bool pdl_enabled() { return g_pdl; }
 void set_pdl(bool enable) { g_pdl = enable; }
 
+bool g_tail_ok = false;
+
+// one thread-block cluster of kTC CTAs (the cluster tails), after the previous kernel (PDL)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_cluster(void (*kern)(KArgs...), cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kTC);
+  cfg.blockDim = dim3(1024);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kTC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  unsigned na = 1;
+  if (pdl_enabled()) {
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    na = 2;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors, long long* counts,
                                        int validate, cudaStream_t s, int blocks, int threads) {
-  GraphView gg = g;
-  void* args[] = {&gg, &ws, &k, &colors, &counts, &validate};
-  return cudaLaunchCooperativeKernel((void*)mpld_simplify_components, dim3(blocks), dim3(threads), args, 0, s);
+  const int cluster = g_tail_ok && MPLD_CLUSTER_ROUNDS ? 1 : 0;
+  cudaError_t e = launch_ex(mpld_simplify_components, dim3(blocks), dim3(threads), 0, s, false, true, g, ws, k, colors,
+                            counts, validate, cluster);
+  if (e != cudaSuccess || !cluster) return e;
+  e = launch_cluster(mpld_simplify_tail, s, g, ws, k);
+  if (e != cudaSuccess) return e;
+  return launch_ex(mpld_final_pass, dim3(blocks), dim3(threads), 0, s, true, false, g, ws);
 }
+int simplify_launches() { return g_tail_ok && MPLD_CLUSTER_ROUNDS ? 3 : 1; }
+cudaError_t configure_recover_tail() {
+  g_tail_ok = false;
+  if (!MPLD_CLUSTER_TAIL) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(mpld_recover_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(mpld_simplify_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cudaSuccess;  // no cluster tail: the grid kernel finishes every level
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kTC);
+  cfg.blockDim = dim3(1024);
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = kTC;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&nclusters, mpld_recover_tail, &cfg);
+  if (e != cudaSuccess) cudaGetLastError();
+  g_tail_ok = e == cudaSuccess && nclusters >= 1;
+  return cudaSuccess;
+}
+bool recover_tail_available() { return g_tail_ok; }
 
 cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
                            int blocks, int threads, bool pdl) {
-  return launch_ex(mpld_recover, dim3(blocks), dim3(threads), 0, s, pdl, true, g, ws, k, colors, out);
+  out.cluster_tail = g_tail_ok ? 1 : 0;
+  cudaError_t e = launch_ex(mpld_recover, dim3(blocks), dim3(threads), 0, s, pdl, true, g, ws, k, colors, out);
+  if (e != cudaSuccess || !out.cluster_tail) return e;
+  return launch_cluster(mpld_recover_tail, s, g, ws, k, colors, out);
 }
 
 cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors, double alpha, long long* counts,

@@ -237,7 +237,7 @@ int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, 
                                  ctx->blocks_simplify, kCoopThreads);
   if (e != cudaSuccess) return cuda_fail(e, "mpld_simplify_components");
   t.done();
-  ++ctx->call_launches;
+  ctx->call_launches += simplify_launches();
   return MPLD_OK;
 }
 
@@ -311,9 +311,11 @@ int phase_finish(mpld_context* ctx, cudaStream_t s, double alpha, int* colors, l
   out.stats = stats;
   out.alpha = alpha;
   out.enabled = ctx->search_counted && counts == ctx->counts;
+  out.cluster_tail = 0;  // set by launch_recover
   {
     TimedLaunch t(ctx, K_RECOVER, s);
-    out.launches = ++ctx->call_launches;
+    ctx->call_launches += recover_tail_available() ? 2 : 1;  // + the cluster tail of the last levels
+    out.launches = ctx->call_launches;
     // PDL after the search kernels of the same thread of calls (a sharded run
     // puts an all-reduce between the search and this call)
     cudaError_t e = launch_recover(g, ws, ctx->k, colors, out, s, ctx->blocks_recover, kCoopThreads,
@@ -467,6 +469,11 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   if (const char* ls = std::getenv("MPLD_LIGHT_STEPS")) {
     const long v = std::strtol(ls, nullptr, 10);
     if (v >= 1 && v <= (1L << 24)) ctx->light_steps = (unsigned)v;
+  }
+  e = configure_recover_tail();
+  if (e != cudaSuccess) {
+    mpld_context_destroy(ctx);
+    return cuda_fail(e, "configure recovery tail");
   }
   e = configure_search_heavy(ctx->num_sms, ctx->blocks_heavy);
   if (e != cudaSuccess) {

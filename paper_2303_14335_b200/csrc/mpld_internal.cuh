@@ -47,6 +47,7 @@ struct Control {
   alignas(128) unsigned bar1;  // ... of mpld_recover
   alignas(128) unsigned bar0g; // group barriers (the first kGroup CTAs) of the two kernels
   alignas(128) unsigned bar1g;
+  alignas(128) int tovf[2];    // recovery cluster tail: ready vertices spilled to global memory per level parity
   alignas(128) int n_comp;     // components found (counted by the discovery kernel)
   int max_comp;                // largest component
   alignas(128) int truncated;  // components whose search hit max_steps
@@ -186,6 +187,7 @@ struct Outputs {
   double alpha;
   int launches;
   int enabled;
+  int cluster_tail;  // the last levels run on mpld_recover_tail (set by launch_recover)
 };
 
 // 32-bit counter-based mix (a bijection), recovery priority of DESIGN.md R9.
@@ -251,6 +253,9 @@ cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_s
 cudaError_t configure_search_heavy(int num_sms, int* blocks);  // blocks[6]: resident grids of the heavy kernels
 cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
                            int blocks, int threads, bool pdl);
+bool recover_tail_available();  // the cluster tail kernel can be launched (cluster size support)
+int simplify_launches();        // kernels launch_simplify_components enqueues (1, or 3 with the cluster tail)
+cudaError_t configure_recover_tail();
 cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors, double alpha,
                             long long* counts, double* cost, long long* stats, int launches,
                             cudaStream_t s, int blocks);
