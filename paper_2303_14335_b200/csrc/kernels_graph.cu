@@ -271,7 +271,9 @@ __device__ void peel_round(const GraphView& g, const Workspace& w, int k, int r,
 
 // The final pass of the simplification (the rounds are final): see the
 // comment at its call in mpld_simplify_components.
-__device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q) {
+// mode bit 1: the component seeds (kept vertices); bit 2: the recovery's
+// predecessor counts, "popped before" bitmasks and level 0 (hidden vertices).
+__device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q, int mode) {
   const int n = g.n;
   const int nth = gridDim.x * blockDim.x;
   const int tile0f = blockIdx.x * blockDim.x * kPF, tstridef = nth * kPF;
@@ -288,8 +290,9 @@ __device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q)
       v[j] = t0 + j * blockDim.x + threadIdx.x;
       const int hv = v[j] < n ? __ldcg(&w.hround[v[j]]) : -1;
       kv[j] = v[j] < n ? pop_key(hv, __ldcg(&w.prio[v[j]])) : ~0ull;
-      e[j] = e0[j] = v[j] < n ? __ldg(&g.ce_rp[v[j]]) : 0;
-      e1[j] = v[j] < n ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
+      const bool walk = v[j] < n && (mode & (kv[j] == ~0ull ? 1 : 2));
+      e[j] = e0[j] = walk ? __ldg(&g.ce_rp[v[j]]) : 0;
+      e1[j] = walk ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
       cnt[j] = 0;
       bm[j] = 0ull;
       seed[j] = true;
@@ -333,7 +336,7 @@ __device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q)
     }
 #pragma unroll
     for (int j = 0; j < kPF; ++j) {
-      if (v[j] >= n) continue;
+      if (v[j] >= n || !(mode & (kv[j] == ~0ull ? 1 : 2))) continue;
       if (kv[j] != ~0ull) {
         w.deg[v[j]] = cnt[j];
         w.bmask[v[j]] = bm[j];
@@ -353,9 +356,9 @@ __device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q)
       }
     }
   }
-  cq_flush(Q, 0, &ctl->n_seed, w.roots);
-  cq_flush(Q, 1, &ctl->rq[0], w.q0);
-  stamp(w.ctl, 3);
+  if (mode & 1) cq_flush(Q, 0, &ctl->n_seed, w.roots);
+  if (mode & 2) cq_flush(Q, 1, &ctl->rq[0], w.q0);
+  if (mode & 1) stamp(w.ctl, 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -371,7 +374,7 @@ __device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q)
 // seeds and the recovery's predecessor counts and level 0.
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_components(GraphView g, Workspace w, int k,
                                                                     int* colors, long long* counts, int validate,
-                                                                    int cluster_rounds) {
+                                                                    int cluster_rounds, int separate_prep) {
   GridBarrier grid(&w.ctl->bar0);
   __shared__ CtaQueues Q;
   cq_init(Q);
@@ -615,7 +618,7 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
   //    so no union-find and no further grid barrier are needed here;
   //  * recovery: hidden predecessors of every hidden vertex (conflict
   //    neighbours popped before it) and level 0 = the vertices without one.
-  final_pass(g, w, Q);
+  final_pass(g, w, Q, separate_prep ? 1 : 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -702,7 +705,16 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_final_pass(GraphVi
   __shared__ CtaQueues Q;
   cq_init(Q);
   if (__ldcg(&w.ctl->err)) return;
-  final_pass(g, w, Q);
+  final_pass(g, w, Q, 3);
+}
+
+// The recovery's share of the final pass (predecessor counts, bitmasks, level
+// 0) as its own kernel, on a second stream while the search runs.
+__global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover_prep(GraphView g, Workspace w) {
+  __shared__ CtaQueues Q;
+  cq_init(Q);
+  if (__ldcg(&w.ctl->err)) return;
+  final_pass(g, w, Q, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -1108,16 +1120,20 @@ cudaError_t launch_cluster(void (*kern)(KArgs...), cudaStream_t s, Args&&... arg
 }
 
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors, long long* counts,
-                                       int validate, cudaStream_t s, int blocks, int threads) {
+                                       int validate, cudaStream_t s, int blocks, int threads, int separate_prep) {
   const int cluster = g_tail_ok && MPLD_CLUSTER_ROUNDS ? 1 : 0;
   cudaError_t e = launch_ex(mpld_simplify_components, dim3(blocks), dim3(threads), 0, s, false, true, g, ws, k, colors,
-                            counts, validate, cluster);
+                            counts, validate, cluster, cluster ? 0 : separate_prep);
   if (e != cudaSuccess || !cluster) return e;
   e = launch_cluster(mpld_simplify_tail, s, g, ws, k);
   if (e != cudaSuccess) return e;
   return launch_ex(mpld_final_pass, dim3(blocks), dim3(threads), 0, s, true, false, g, ws);
 }
 int simplify_launches() { return g_tail_ok && MPLD_CLUSTER_ROUNDS ? 3 : 1; }
+
+cudaError_t launch_recover_prep(const GraphView& g, Workspace ws, cudaStream_t s, int blocks, int threads) {
+  return launch_ex(mpld_recover_prep, dim3(blocks), dim3(threads), 0, s, false, false, g, ws);
+}
 cudaError_t configure_recover_tail() {
   g_tail_ok = false;
   if (!MPLD_CLUSTER_TAIL) return cudaSuccess;

@@ -39,12 +39,15 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(MPLD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-enum KernelId { K_SIMPLIFY = 0, K_DISCOVER, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_COUNT };
+enum KernelId { K_SIMPLIFY = 0, K_DISCOVER, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_PREP, K_COUNT };
 const char* kKernelNames[K_COUNT] = {"mpld_simplify_components", "mpld_component_discover",
                                      "mpld_exact_cover_search", "mpld_exact_cover_search_heavy", "mpld_recover",
-                                     "mpld_evaluate"};
+                                     "mpld_evaluate", "mpld_recover_prep"};
 
 constexpr int kCoopThreads = 1024;
+#ifndef MPLD_SEPARATE_PREP
+#define MPLD_SEPARATE_PREP 1
+#endif
 
 }  // namespace
 
@@ -113,6 +116,12 @@ struct mpld_context {
   long long* counts = nullptr;  // the prepare phase's d_counts (zeroed by the simplification kernel)
   bool search_counted = false;  // the search accumulated the counts (one shard)
   int searches_since_prepare = 0;
+  // the recovery's share of the final pass runs on `aux` beside the search
+  // (forked after the simplification, joined before the recovery)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int blocks_prep = 0;
+  bool prep_forked = false;
   // host-API staging (device copies of host inputs / outputs)
   int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
   int* h_lo = nullptr;
@@ -233,11 +242,26 @@ int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, 
   cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
   if (e != cudaSuccess) return cuda_fail(e, "control reset");
   TimedLaunch t(ctx, K_SIMPLIFY, s);
+  const int separate_prep = simplify_launches() == 1 && MPLD_SEPARATE_PREP ? 1 : 0;
   e = launch_simplify_components(g, ws, k, colors, counts, (flags & MPLD_FLAG_VALIDATE) ? 1 : 0, s,
-                                 ctx->blocks_simplify, kCoopThreads);
+                                 ctx->blocks_simplify, kCoopThreads, separate_prep);
   if (e != cudaSuccess) return cuda_fail(e, "mpld_simplify_components");
   t.done();
   ctx->call_launches += simplify_launches();
+  ctx->prep_forked = false;
+  if (separate_prep) {  // the recovery's prep beside the search: fork onto the second stream
+    e = cudaEventRecord(ctx->ev_fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "prep fork");
+    TimedLaunch tp(ctx, K_PREP, ctx->aux);
+    e = launch_recover_prep(g, ws, ctx->aux, ctx->blocks_prep, kCoopThreads);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_recover_prep");
+    tp.done();
+    e = cudaEventRecord(ctx->ev_join, ctx->aux);
+    if (e != cudaSuccess) return cuda_fail(e, "prep join");
+    ++ctx->call_launches;
+    ctx->prep_forked = true;
+  }
   return MPLD_OK;
 }
 
@@ -312,6 +336,10 @@ int phase_finish(mpld_context* ctx, cudaStream_t s, double alpha, int* colors, l
   out.alpha = alpha;
   out.enabled = ctx->search_counted && counts == ctx->counts;
   out.cluster_tail = 0;  // set by launch_recover
+  if (ctx->prep_forked) {  // join the recovery's prep (second stream)
+    cudaError_t e = cudaStreamWaitEvent(s, ctx->ev_join, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "prep join");
+  }
   {
     TimedLaunch t(ctx, K_RECOVER, s);
     ctx->call_launches += recover_tail_available() ? 2 : 1;  // + the cluster tail of the last levels
@@ -319,7 +347,7 @@ int phase_finish(mpld_context* ctx, cudaStream_t s, double alpha, int* colors, l
     // PDL after the search kernels of the same thread of calls (a sharded run
     // puts an all-reduce between the search and this call)
     cudaError_t e = launch_recover(g, ws, ctx->k, colors, out, s, ctx->blocks_recover, kCoopThreads,
-                                   ctx->search_counted);
+                                   ctx->search_counted && !ctx->prep_forked);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_recover");
     t.done();
   }
@@ -493,10 +521,14 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     return rc;
   }
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     mpld_context_destroy(ctx);
     return cuda_fail(e, "cudaStreamCreate");
   }
+  ctx->blocks_prep = ctx->num_sms;  // one CTA per SM on the second stream, beside the search kernels
   *out = ctx;
   return MPLD_OK;
 }
@@ -517,6 +549,9 @@ void mpld_context_destroy(mpld_context* ctx) {
     cudaEventDestroy(p.second.second);
   }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   for (AsyncSlot& a : ctx->slot) {
     for (void* p : {(void*)a.lo, (void*)a.ce_rp, (void*)a.ce_col, (void*)a.se_rp, (void*)a.se_col, (void*)a.colors,
                     (void*)a.counts, (void*)a.cost, (void*)a.stats})

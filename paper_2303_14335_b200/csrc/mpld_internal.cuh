@@ -241,7 +241,10 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 // cudaError_t of its launch.  `pdl`: the stream's previous operation is one
 // of these kernels.
 cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, int* colors,
-                                       long long* counts, int validate, cudaStream_t s, int blocks, int threads);
+                                       long long* counts, int validate, cudaStream_t s, int blocks, int threads,
+                                       int separate_prep);
+// the recovery's share of the final pass (separate_prep above), on a second stream
+cudaError_t launch_recover_prep(const GraphView& g, Workspace ws, cudaStream_t s, int blocks, int threads);
 cudaError_t launch_discover(const GraphView& g, Workspace ws, int k, int sharded, cudaStream_t s, int blocks, bool pdl);
 cudaError_t launch_partition_scan(const GraphView& g, Workspace ws, cudaStream_t s);  // inclusive scan of ws.est
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
