@@ -312,8 +312,10 @@ def main():
     kernel_pass_ms = sum(v[0] for v in ktimes.values())
     st = dict(zip(mp.STAT_NAMES, stats.cpu().tolist()))
     assert st["error"] == 0, st
-    # kernels launched per step; the heavy search is one launch per word class (two per call)
-    launches = sum(v[1] for v in ktimes.values()) + ktimes.get("mpld_exact_cover_search_heavy", (0, 0))[1]
+    # kernels launched in the timed steps: the library's own count per call
+    # (simplify, discover, light search, heavy x2 word classes, recovery prep,
+    # recovery + its cluster tail)
+    launches = int(st["launches"]) * args.steps
 
     # e2e: the host C-ABI call on pinned host buffers (H2D + kernels + D2H inside)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
