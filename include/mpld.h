@@ -135,6 +135,9 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
 void mpld_context_destroy(mpld_context* ctx);
 
 /* Enqueue the whole hot path on `stream` (a cudaStream_t; NULL = legacy default).
+ * The recovery's preparation runs on the context's own second stream, forked
+ * from `stream` by an event after the simplification and joined back before
+ * the recovery, so all work stays ordered with respect to `stream`.
  * All pointers are device pointers.  d_counts [2*n_layouts] int64 receives
  * (n_conflicts, n_stitches) per layout, d_cost [n_layouts] the Eq. (1a) cost,
  * d_stats [MPLD_STAT_LEN] the statistics (MPLD_STAT_ERROR != 0 means the
