@@ -700,12 +700,12 @@ __global__ void __launch_bounds__(1024) mpld_simplify_tail(GraphView g, Workspac
   if (rank == 0 && threadIdx.x == 0) ctl->n_rounds = __ldcg(&ctl->n_hidden) ? r : 0;
 }
 
-__global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_final_pass(GraphView g, Workspace w) {
+__global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_final_pass(GraphView g, Workspace w, int separate_prep) {
   pdl_begin();
   __shared__ CtaQueues Q;
   cq_init(Q);
   if (__ldcg(&w.ctl->err)) return;
-  final_pass(g, w, Q, 3);
+  final_pass(g, w, Q, separate_prep ? 1 : 3);
 }
 
 // The recovery's share of the final pass (predecessor counts, bitmasks, level
@@ -1123,11 +1123,11 @@ cudaError_t launch_simplify_components(const GraphView& g, Workspace ws, int k, 
                                        int validate, cudaStream_t s, int blocks, int threads, int separate_prep) {
   const int cluster = g_tail_ok && MPLD_CLUSTER_ROUNDS ? 1 : 0;
   cudaError_t e = launch_ex(mpld_simplify_components, dim3(blocks), dim3(threads), 0, s, false, true, g, ws, k, colors,
-                            counts, validate, cluster, cluster ? 0 : separate_prep);
+                            counts, validate, cluster, separate_prep);
   if (e != cudaSuccess || !cluster) return e;
   e = launch_cluster(mpld_simplify_tail, s, g, ws, k);
   if (e != cudaSuccess) return e;
-  return launch_ex(mpld_final_pass, dim3(blocks), dim3(threads), 0, s, true, false, g, ws);
+  return launch_ex(mpld_final_pass, dim3(blocks), dim3(threads), 0, s, true, false, g, ws, separate_prep);
 }
 int simplify_launches() { return g_tail_ok && MPLD_CLUSTER_ROUNDS ? 3 : 1; }
 

@@ -242,7 +242,7 @@ int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, 
   cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
   if (e != cudaSuccess) return cuda_fail(e, "control reset");
   TimedLaunch t(ctx, K_SIMPLIFY, s);
-  const int separate_prep = simplify_launches() == 1 && MPLD_SEPARATE_PREP ? 1 : 0;
+  const int separate_prep = MPLD_SEPARATE_PREP ? 1 : 0;
   e = launch_simplify_components(g, ws, k, colors, counts, (flags & MPLD_FLAG_VALIDATE) ? 1 : 0, s,
                                  ctx->blocks_simplify, kCoopThreads, separate_prep);
   if (e != cudaSuccess) return cuda_fail(e, "mpld_simplify_components");
