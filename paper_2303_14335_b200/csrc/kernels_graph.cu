@@ -64,7 +64,10 @@ constexpr int kTail = MPLD_TAIL;  // frontiers up to this size are finished by C
 #define MPLD_CLUSTER_ROUNDS 0  // measured slower in the PDL chain: off
 #endif
 constexpr int kTC = MPLD_CLUSTER;                // CTAs of the recovery's cluster tail
-constexpr int kClusterTailMax = kTC * 1024;      // levels up to this size go to the cluster tail
+#ifndef MPLD_CLUSTER_TAIL_ITEMS
+#define MPLD_CLUSTER_TAIL_ITEMS 1
+#endif
+constexpr int kClusterTailMax = MPLD_CLUSTER_TAIL_ITEMS * kTC * 1024;  // levels up to this size go to the cluster tail
 constexpr int kGroup = MPLD_GROUP;  // frontiers up to kGroup * blockDim items: the first kGroup CTAs, group barriers
 constexpr int kStitchDeg = 1 << 29;  // live degree of stitch vertices: never reaches k (never hidden, R8)
 
