@@ -355,33 +355,38 @@ def main():
                     "n_stitches": torch.zeros(L, dtype=torch.int64).pin_memory(),
                     "cost": torch.zeros(L, dtype=torch.float64).pin_memory(),
                     "stats": torch.zeros(len(mp.STAT_NAMES), dtype=torch.int64).pin_memory()}
-        outs = [pinned_out(), pinned_out()]
+        outs = [pinned_out(), pinned_out(), pinned_out()]  # one per staging slot of the context
         actx = mp.Context(local, b.n, L)
+        # the stitch candidates as (u, v) pairs, the input of the pairs entry point
+        # (prepared once, outside the timed region, like every other input array)
+        se = b.se_edges()
+        se = se[se[:, 0] < se[:, 1]] if se.size else np.zeros((0, 2), np.int32)
+        h_pairs = pin(np.ascontiguousarray(se, dtype=np.int32))
 
         def submit(i):
-            return actx.submit(h[0], b.n, h[1], h[2], h[3], h[4], k, alpha, args.max_steps, flags,
-                               out=outs[i & 1])
+            return actx.submit_pairs(h[0], b.n, h[1], h[2], h_pairs, k, alpha, args.max_steps, flags,
+                                     out=outs[i % 3])
 
-        actx.wait(submit(0))  # warm-up allocates both staging slots outside the timed region
-        actx.wait(submit(1))
+        for i in range(3):  # warm-up allocates the three staging slots outside the timed region
+            actx.wait(submit(i))
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        prev = None
-        for i in range(e2e_steps):
-            t = submit(i)
-            if prev is not None:
-                r = actx.wait(prev)
-            prev = t
-        r = actx.wait(prev)
+        pend = []
+        for i in range(e2e_steps):  # up to three submits in flight; every result is waited for
+            pend.append(submit(i))
+            if len(pend) > 2:
+                r = actx.wait(pend.pop(0))
+        for t in pend:
+            r = actx.wait(t)
         e2e_s = time.perf_counter() - t0
         assert np.array_equal(r["colors"].numpy(), colors.cpu().numpy()) and r["stats"]["error"] == 0
         actx.close()
         e2e_how = ("wall clock around %d pipelined submits of the asynchronous host C-ABI call "
-                   "mpld_decompose_batch_async + mpld_wait (pinned buffers, two staging slots: step i+1's "
-                   "upload overlaps step i's compute); blocking mpld_decompose_batch: %.3f ms/step"
-                   % (e2e_steps, blocking_ms))
-    h2d = sum(x.numel() * 4 for x in h)
+                   "mpld_decompose_batch_pairs_async + mpld_wait (CE as CSR, stitch candidates as pairs; pinned "
+                   "buffers, three staging slots: step i+1's upload overlaps step i's compute); blocking "
+                   "mpld_decompose_batch: %.3f ms/step" % (e2e_steps, blocking_ms))
+    h2d = (sum(x.numel() * 4 for x in h[:3]) + h_pairs.numel() * 4) if not shard else sum(x.numel() * 4 for x in h)
     d2h = b.n * 4 + L * 8 * 3 + 8 * len(mp.STAT_NAMES)
 
     # aggregate over ranks

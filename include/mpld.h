@@ -154,17 +154,17 @@ int mpld_decompose_device(mpld_context* ctx, void* stream, int32_t n_layouts,
  * mpld_decompose_batch_async: the host batch call of mpld_decompose_batch
  * (same arguments and outputs, same results) on an explicit context, returning
  * before the result is ready.  It enqueues the upload of the inputs into one of
- * the context's two device staging slots (its own copy stream), the hot path
+ * the context's three device staging slots (its own copy stream), the hot path
  * after the upload (the context's compute stream) and the download of colors /
  * counts / cost / stats after the compute (a third stream), then writes a
- * ticket.  Consecutive submits alternate slots, so submit t+1's upload overlaps
- * submit t's compute and t's download overlaps t+1's compute.
+ * ticket.  Consecutive submits rotate through the slots, so submit t+1's upload
+ * overlaps submit t's compute and t's download overlaps t+1's compute.
  * Ownership: the host buffers of a submit must stay valid and unmodified until
  * mpld_wait(ctx, ticket) returns; the outputs are complete only then (counts
  * are split into n_conflicts / n_stitches by mpld_wait).  Page-locked
  * (pinned) host memory makes the copies asynchronous; pageable memory is
  * correct but serialises them.  A submit reusing a slot first waits for and
- * finishes the submit that used it two calls before.
+ * finishes the submit that used it three calls before.
  * Errors: argument errors are returned by the submit; device-side results
  * (MPLD_ERR_GRAPH / MPLD_ERR_COMPONENT from the error bits, CUDA errors) by
  * mpld_wait.  The context must not be used from several threads at once. */
@@ -173,6 +173,20 @@ int mpld_decompose_batch_async(mpld_context* ctx, int32_t n_layouts, const int32
                                const int32_t* se_col, int32_t k, double alpha, int64_t max_steps,
                                uint32_t flags, int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches,
                                double* cost, int64_t* stats, int64_t* ticket);
+
+/* The same submit with the stitch edges given as n_stitch_pairs (u, v) pairs
+ * (stitch_pairs [2 * n_stitch_pairs], each SE edge once, in either direction)
+ * instead of CSR: the H2D copy carries 8 B per stitch edge instead of the
+ * (n+1)-entry SE row-pointer array, and the SE CSR is built on the device
+ * (degrees, scan, scatter, rows sorted) before the hot path.  Pairs with an id
+ * outside [0, n) or u == v are rejected on the host (MPLD_ERR_GRAPH); duplicate
+ * pairs and CE ∩ SE are caught by MPLD_FLAG_VALIDATE on the built CSR.  Results
+ * are identical to mpld_decompose_batch_async on the same graph. */
+int mpld_decompose_batch_pairs_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
+                                     const int32_t* ce_rowptr, const int32_t* ce_col, int64_t n_stitch_pairs,
+                                     const int32_t* stitch_pairs, int32_t k, double alpha, int64_t max_steps,
+                                     uint32_t flags, int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches,
+                                     double* cost, int64_t* stats, int64_t* ticket);
 
 /* Block until submit `ticket` of ctx has completed; returns its result code
  * (MPLD_OK or the error of that submit).  Waiting on an older ticket whose slot

@@ -1092,9 +1092,135 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
   finalize_outputs(g, w, out, &w.ctl->done_blocks);
 }
 
+// ---------------------------------------------------------------------------
+// Stitch edges given as pairs (mpld_decompose_batch_pairs_async): the SE CSR
+// is built on the device — degrees, an exclusive scan, a scatter, each row
+// sorted (rows hold one or two segments' worth of entries).
+__global__ void __launch_bounds__(256) mpld_se_degrees(int m, const int* __restrict__ pairs, int* deg) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    atomicAdd(&deg[pairs[2 * i]], 1);
+    atomicAdd(&deg[pairs[2 * i + 1]], 1);
+  }
+}
+
+constexpr int kScanTileI = 8192;  // elements per block of the int scan (1024 threads x 8)
+
+__device__ __forceinline__ int block_scan_int(int x, int* s_w, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int y = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int z = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) y += z;
+  }
+  if (lane == 31) s_w[wid] = y;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < nw ? s_w[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int z = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += z;
+    }
+    if (lane < nw) s_w[lane] = t;
+  }
+  __syncthreads();
+  total = s_w[nw - 1];
+  const int r = y + (wid ? s_w[wid - 1] : 0);  // inclusive
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) mpld_scan_sums(int n, const int* in, int* bsum) {
+  __shared__ int s_w[32];
+  const size_t base = (size_t)blockIdx.x * kScanTileI;
+  int x = 0;
+  for (int j = 0; j < kScanTileI / 1024; ++j) {
+    const size_t i = base + (size_t)j * 1024 + threadIdx.x;
+    if (i < (size_t)n) x += in[i];
+  }
+  int total;
+  block_scan_int(x, s_w, total);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) mpld_scan_offsets(int nb, int* bsum) {
+  __shared__ int s_w[32];
+  int carry = 0;
+  for (int b0 = 0; b0 < nb; b0 += 1024) {  // exclusive scan of the block sums, in place
+    const int i = b0 + threadIdx.x;
+    const int x = i < nb ? bsum[i] : 0;
+    int total;
+    const int inc = block_scan_int(x, s_w, total);
+    if (i < nb) bsum[i] = carry + inc - x;
+    carry += total;
+  }
+}
+
+// out[i] = sum of in[0..i) for i in [0, n]; in and out may not alias
+__global__ void __launch_bounds__(1024) mpld_scan_apply(int n, const int* in, const int* bsum, int* out) {
+  __shared__ int s_w[32];
+  const size_t base = (size_t)blockIdx.x * kScanTileI;
+  int carry = bsum[blockIdx.x];
+  for (int j = 0; j < kScanTileI / 1024; ++j) {
+    const size_t i = base + (size_t)j * 1024 + threadIdx.x;
+    const int x = i < (size_t)n ? in[i] : 0;
+    int total;
+    const int inc = block_scan_int(x, s_w, total);
+    if (i < (size_t)n) out[i] = carry + inc - x;
+    if (i == (size_t)n - 1) out[n] = carry + inc;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(256) mpld_se_scatter(int m, const int* __restrict__ pairs,
+                                                       const int* __restrict__ rp, int* fill, int* col) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int u = pairs[2 * i], v = pairs[2 * i + 1];
+    col[rp[u] + atomicAdd(&fill[u], 1)] = v;
+    col[rp[v] + atomicAdd(&fill[v], 1)] = u;
+  }
+}
+
+__global__ void __launch_bounds__(256) mpld_se_sort_rows(int n, const int* __restrict__ rp, int* col) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int a = rp[v], b = rp[v + 1];
+    for (int i = a + 1; i < b; ++i) {  // insertion sort (rows are short)
+      const int x = col[i];
+      int j = i - 1;
+      while (j >= a && col[j] > x) {
+        col[j + 1] = col[j];
+        --j;
+      }
+      col[j + 1] = x;
+    }
+  }
+}
+
 }  // namespace
 
 bool pdl_enabled() { return g_pdl; }
+
+// SE CSR from m pairs (ids already checked on the host): deg / fill are [n]
+// scratch arrays, bsum [n / kScanTileI + 2]
+cudaError_t launch_se_from_pairs(int n, int m, const int* pairs, int* rp, int* col, int* deg, int* fill, int* bsum,
+                                 cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(deg, 0, sizeof(int) * (size_t)(n > 0 ? n : 1), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(fill, 0, sizeof(int) * (size_t)(n > 0 ? n : 1), s);
+  if (e != cudaSuccess) return e;
+  if (n <= 0) return cudaMemsetAsync(rp, 0, sizeof(int), s);
+  const int gb = 1184;
+  if (m > 0) mpld_se_degrees<<<gb, 256, 0, s>>>(m, pairs, deg);
+  const int nb = (n + kScanTileI - 1) / kScanTileI;
+  mpld_scan_sums<<<nb, 1024, 0, s>>>(n, deg, bsum);
+  mpld_scan_offsets<<<1, 1024, 0, s>>>(nb, bsum);
+  mpld_scan_apply<<<nb, 1024, 0, s>>>(n, deg, bsum, rp);
+  if (m > 0) {
+    mpld_se_scatter<<<gb, 256, 0, s>>>(m, pairs, rp, fill, col);
+    mpld_se_sort_rows<<<gb, 256, 0, s>>>(n, rp, col);
+  }
+  return cudaGetLastError();
+}
 void set_pdl(bool enable) { g_pdl = enable; }
 
 bool g_tail_ok = false;

@@ -54,17 +54,23 @@ constexpr int kCoopThreads = 1024;
 // One staging slot of the asynchronous host entry point: device copies of a
 // batch's inputs and outputs, pinned host copies of the outputs that need
 // post-processing, and the events that order upload -> compute -> download.
+// Three staging slots: the upload of submit t+1 never waits for the download
+// of submit t-1 (with two, the slot reuse chained upload, compute and download
+// of consecutive submits).
+constexpr int kAsyncSlots = 3;
+
 struct AsyncSlot {
   int* lo = nullptr;
   int* ce_rp = nullptr;
   int* ce_col = nullptr;
   int* se_rp = nullptr;
   int* se_col = nullptr;
+  int* se_pairs = nullptr;  // stitch edges as pairs (the pairs entry point)
   int* colors = nullptr;
   long long* counts = nullptr;
   double* cost = nullptr;
   long long* stats = nullptr;
-  int64_t cap_n = -1, cap_ce = -1, cap_se = -1;
+  int64_t cap_n = -1, cap_ce = -1, cap_se = -1, cap_pairs = -1;
   int32_t cap_l = -1;
   long long* h_counts = nullptr;  // pinned
   long long* h_stats = nullptr;   // pinned [MPLD_STAT_LEN]
@@ -134,8 +140,8 @@ struct mpld_context {
   double* h_cost = nullptr;
   long long* h_stats = nullptr;
   cudaStream_t stream = nullptr;  // compute stream of the host entry points
-  // asynchronous host entry point: two staging slots, upload / download streams
-  AsyncSlot slot[2];
+  // asynchronous host entry points: kAsyncSlots staging slots, upload / download streams
+  AsyncSlot slot[kAsyncSlots];
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   int64_t next_ticket = 0;
   // timing
@@ -553,7 +559,7 @@ void mpld_context_destroy(mpld_context* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   for (AsyncSlot& a : ctx->slot) {
-    for (void* p : {(void*)a.lo, (void*)a.ce_rp, (void*)a.ce_col, (void*)a.se_rp, (void*)a.se_col, (void*)a.colors,
+    for (void* p : {(void*)a.lo, (void*)a.ce_rp, (void*)a.ce_col, (void*)a.se_rp, (void*)a.se_col, (void*)a.se_pairs, (void*)a.colors,
                     (void*)a.counts, (void*)a.cost, (void*)a.stats})
       if (p) cudaFree(p);
     if (a.h_counts) cudaFreeHost(a.h_counts);
@@ -712,22 +718,34 @@ int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32
   return MPLD_OK;
 }
 
-int mpld_decompose_batch_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
-                               const int32_t* ce_rowptr, const int32_t* ce_col, const int32_t* se_rowptr,
-                               const int32_t* se_col, int32_t k, double alpha, int64_t max_steps, uint32_t flags,
-                               int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches, double* cost,
-                               int64_t* stats, int64_t* ticket) {
+namespace {
+// The pipelined host submit; stitch edges either as CSR (se_rowptr, se_col) or
+// as n_pairs (u, v) pairs (se_pairs, se_rowptr == NULL), built into CSR on the device.
+int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
+                 const int32_t* ce_rowptr, const int32_t* ce_col, const int32_t* se_rowptr, const int32_t* se_col,
+                 const int32_t* se_pairs, int64_t n_pairs, int32_t k, double alpha, int64_t max_steps,
+                 uint32_t flags, int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches, double* cost,
+                 int64_t* stats, int64_t* ticket) {
   if (!ctx || !ticket) return fail(MPLD_ERR_ARG, "bad context / ticket pointer");
   int w_stitch = 0;
   int rc = check_scalars(n, k, alpha, &w_stitch);
   if (rc != MPLD_OK) return rc;
-  if (n_layouts < 1 || !layout_offsets || !ce_rowptr || !se_rowptr || (n > 0 && !colors) || !n_conflicts ||
-      !n_stitches || !cost)
+  const bool pairs = se_rowptr == nullptr;
+  if (n_layouts < 1 || !layout_offsets || !ce_rowptr || (n > 0 && !colors) || !n_conflicts || !n_stitches || !cost)
     return fail(MPLD_ERR_ARG, "bad argument (NULL pointer or n_layouts < 1)");
   if (layout_offsets[0] != 0 || layout_offsets[n_layouts] != n)
     return fail(MPLD_ERR_ARG, "layout_offsets must start at 0 and end at n");
-  const int64_t m_ce = ce_rowptr[n], m_se = se_rowptr[n];
-  if (m_ce < 0 || m_se < 0 || (m_ce > 0 && !ce_col) || (m_se > 0 && !se_col))
+  if (pairs) {
+    if (n_pairs < 0 || (n_pairs > 0 && !se_pairs) || 2 * n_pairs > (int64_t)INT32_MAX)
+      return fail(MPLD_ERR_ARG, "bad stitch pairs");
+    for (int64_t i = 0; i < 2 * n_pairs; i += 2) {  // ids and self loops; the rest is the device validation's
+      const int32_t u = se_pairs[i], v = se_pairs[i + 1];
+      if (u < 0 || u >= n || v < 0 || v >= n || u == v)
+        return fail(MPLD_ERR_GRAPH, "stitch pair " + std::to_string(i / 2) + " out of range or a self loop");
+    }
+  }
+  const int64_t m_ce = ce_rowptr[n], m_se = pairs ? 2 * n_pairs : se_rowptr[n];
+  if (m_ce < 0 || m_se < 0 || (m_ce > 0 && !ce_col) || (!pairs && m_se > 0 && !se_col))
     return fail(MPLD_ERR_ARG, "bad CSR row pointer / column array");
   std::lock_guard<std::mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
@@ -737,21 +755,32 @@ int mpld_decompose_batch_async(mpld_context* ctx, int32_t n_layouts, const int32
       return fail(MPLD_ERR_CUDA, "async stream creation failed");
   }
   const int64_t t = ctx->next_ticket;
-  AsyncSlot& a = ctx->slot[t & 1];
+  AsyncSlot& a = ctx->slot[t % kAsyncSlots];
   slot_finish(a);  // the slot's previous submit (t - 2) is complete and post-processed before reuse
   if (n > ctx->cap_n) cudaStreamSynchronize(ctx->stream);  // the workspace grows: the other slot's compute must end
   rc = ensure_workspace(ctx, n, n_layouts);
   if (rc == MPLD_OK) rc = slot_reserve(a, n, m_ce, m_se, n_layouts);
+  if (rc == MPLD_OK && pairs && m_se > a.cap_pairs) {
+    a.cap_pairs = std::max<int64_t>(m_se, a.cap_pairs * 3 / 2);
+    if (grow(&a.se_pairs, a.cap_pairs) != cudaSuccess) rc = fail(MPLD_ERR_NOMEM, "async staging allocation failed");
+  }
   if (rc != MPLD_OK) return rc;
   cudaStream_t up = ctx->s_h2d, ks = ctx->stream, down = ctx->s_d2h;
   cudaError_t e = cudaMemcpyAsync(a.lo, layout_offsets, sizeof(int) * (n_layouts + 1), cudaMemcpyHostToDevice, up);
   if (e == cudaSuccess) e = cudaMemcpyAsync(a.ce_rp, ce_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, up);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(a.se_rp, se_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && !pairs)
+    e = cudaMemcpyAsync(a.se_rp, se_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, up);
   if (e == cudaSuccess && m_ce) e = cudaMemcpyAsync(a.ce_col, ce_col, sizeof(int) * m_ce, cudaMemcpyHostToDevice, up);
-  if (e == cudaSuccess && m_se) e = cudaMemcpyAsync(a.se_col, se_col, sizeof(int) * m_se, cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && m_se)
+    e = pairs ? cudaMemcpyAsync(a.se_pairs, se_pairs, sizeof(int) * m_se, cudaMemcpyHostToDevice, up)
+              : cudaMemcpyAsync(a.se_col, se_col, sizeof(int) * m_se, cudaMemcpyHostToDevice, up);
   if (e == cudaSuccess) e = cudaEventRecord(a.ev_h2d, up);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, a.ev_h2d, 0);
   if (e != cudaSuccess) return cuda_fail(e, "async H2D copy");
+  if (pairs) {  // the SE CSR on the device (scratch: the workspace's deg / q0 / bsum, rewritten later)
+    e = launch_se_from_pairs(n, (int)n_pairs, a.se_pairs, a.se_rp, a.se_col, ctx->deg, ctx->q0, (int*)ctx->bsum, ks);
+    if (e != cudaSuccess) return cuda_fail(e, "stitch CSR build");
+  }
   GraphView g{n, n_layouts, a.lo, a.ce_rp, a.ce_col, a.se_rp, a.se_col};
   rc = run_pipeline(ctx, ks, g, k, w_stitch, alpha, (long long)max_steps, flags, a.colors, a.counts, a.cost,
                     a.stats);
@@ -778,11 +807,32 @@ int mpld_decompose_batch_async(mpld_context* ctx, int32_t n_layouts, const int32
   g_last_error.clear();
   return MPLD_OK;
 }
+}  // namespace
+
+int mpld_decompose_batch_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
+                               const int32_t* ce_rowptr, const int32_t* ce_col, const int32_t* se_rowptr,
+                               const int32_t* se_col, int32_t k, double alpha, int64_t max_steps, uint32_t flags,
+                               int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches, double* cost,
+                               int64_t* stats, int64_t* ticket) {
+  if (!se_rowptr) return fail(MPLD_ERR_ARG, "bad argument (NULL se_rowptr)");
+  return submit_async(ctx, n_layouts, layout_offsets, n, ce_rowptr, ce_col, se_rowptr, se_col, nullptr, 0, k, alpha,
+                      max_steps, flags, colors, n_conflicts, n_stitches, cost, stats, ticket);
+}
+
+int mpld_decompose_batch_pairs_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
+                                     const int32_t* ce_rowptr, const int32_t* ce_col, int64_t n_stitch_pairs,
+                                     const int32_t* stitch_pairs, int32_t k, double alpha, int64_t max_steps,
+                                     uint32_t flags, int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches,
+                                     double* cost, int64_t* stats, int64_t* ticket) {
+  return submit_async(ctx, n_layouts, layout_offsets, n, ce_rowptr, ce_col, nullptr, nullptr, stitch_pairs,
+                      n_stitch_pairs, k, alpha, max_steps, flags, colors, n_conflicts, n_stitches, cost, stats,
+                      ticket);
+}
 
 int mpld_wait(mpld_context* ctx, int64_t ticket) {
   if (!ctx || ticket < 0 || ticket >= ctx->next_ticket) return fail(MPLD_ERR_ARG, "bad context / unknown ticket");
   std::lock_guard<std::mutex> lk(ctx->mu);
-  AsyncSlot& a = ctx->slot[ticket & 1];
+  AsyncSlot& a = ctx->slot[ticket % kAsyncSlots];
   if (a.pending && a.ticket == ticket) return slot_finish(a);
   if (a.fin_ticket == ticket) return a.fin_rc;
   return MPLD_OK;  // an older submit of this slot: completed before the slot was reused

@@ -256,6 +256,8 @@ cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_s
 cudaError_t configure_search_heavy(int num_sms, int* blocks);  // blocks[6]: resident grids of the heavy kernels
 cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
                            int blocks, int threads, bool pdl);
+cudaError_t launch_se_from_pairs(int n, int m, const int* pairs, int* rp, int* col, int* deg, int* fill, int* bsum,
+                                 cudaStream_t s);
 bool recover_tail_available();  // the cluster tail kernel can be launched (cluster size support)
 int simplify_launches();        // kernels launch_simplify_components enqueues (1, or 3 with the cluster tail)
 cudaError_t configure_recover_tail();

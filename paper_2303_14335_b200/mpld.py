@@ -32,7 +32,7 @@ EXPORTS = ["mpld_last_error", "mpld_version", "mpld_decompose", "mpld_decompose_
            "mpld_context_destroy", "mpld_decompose_device", "mpld_context_set_timing",
            "mpld_context_reset_timing", "mpld_kernel_count", "mpld_kernel_name", "mpld_context_kernel_time",
            "mpld_context_debug", "mpld_prepare_device", "mpld_search_device", "mpld_finish_device",
-           "mpld_decompose_batch_async", "mpld_wait"]
+           "mpld_decompose_batch_async", "mpld_decompose_batch_pairs_async", "mpld_wait"]
 
 
 class MPLDError(RuntimeError):
@@ -82,6 +82,9 @@ def lib():
     L.mpld_decompose_batch_async.argtypes = [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp, _vp, _vp, _vp,
                                              ctypes.c_int32, ctypes.c_double, ctypes.c_int64, ctypes.c_uint32, _vp,
                                              _vp, _vp, _vp, _vp, _i64p]
+    L.mpld_decompose_batch_pairs_async.argtypes = [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp, _vp, ctypes.c_int64,
+                                                   _vp, ctypes.c_int32, ctypes.c_double, ctypes.c_int64,
+                                                   ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _i64p]
     L.mpld_wait.argtypes = [_vp, ctypes.c_int64]
     _lib = L
     return L
@@ -209,6 +212,34 @@ class Context:
                                             float(alpha), int(max_steps), int(flags), ptr["colors"],
                                             ptr["n_conflicts"], ptr["n_stitches"], ptr["cost"], ptr["stats"],
                                             ctypes.byref(t)))
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[t.value] = (keep, out)
+        return t.value
+
+    def submit_pairs(self, layout_offsets, n, ce_rowptr, ce_col, stitch_pairs, k, alpha, max_steps=0, flags=0,
+                     out=None):
+        """C ABI `mpld_decompose_batch_pairs_async`: as `submit`, with the stitch
+        edges as an int32 array of (u, v) pairs (shape [m, 2] or flat [2m]),
+        each edge once; the SE CSR is built on the device."""
+        L = lib()
+        lo_p, lo = _host_ptr(layout_offsets)
+        n_layouts = int(len(lo) - 1) if not hasattr(lo, "numel") else int(lo.numel() - 1)
+        if out is None:
+            out = {"colors": np.empty(max(int(n), 0), dtype=np.int32),
+                   "n_conflicts": np.zeros(n_layouts, dtype=np.int64),
+                   "n_stitches": np.zeros(n_layouts, dtype=np.int64),
+                   "cost": np.zeros(n_layouts, dtype=np.float64),
+                   "stats": np.zeros(MPLD_STAT_LEN, dtype=np.int64)}
+        sp = _host_ptr(stitch_pairs)
+        m = int(sp[1].numel() if hasattr(sp[1], "numel") else np.asarray(sp[1]).size) // 2
+        keep = [lo] + [_host_ptr(a) for a in (ce_rowptr, ce_col)] + [sp]
+        ptr = {key: _out_ptr(v) for key, v in out.items()}
+        t = ctypes.c_int64()
+        _check(L.mpld_decompose_batch_pairs_async(self._h, n_layouts, lo_p, int(n), keep[1][0], keep[2][0], m, sp[0],
+                                                  int(k), float(alpha), int(max_steps), int(flags), ptr["colors"],
+                                                  ptr["n_conflicts"], ptr["n_stitches"], ptr["cost"], ptr["stats"],
+                                                  ctypes.byref(t)))
         if not hasattr(self, "_inflight"):
             self._inflight = {}
         self._inflight[t.value] = (keep, out)

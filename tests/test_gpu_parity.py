@@ -440,3 +440,40 @@ def test_heavy_search_spill(monkeypatch, case):
         assert (int(c2[li, 0]), int(c2[li, 1]), float(cost[li])) == (c, s_, cst)
     assert int(stats.cpu().numpy()[mp.STAT_NAMES.index("truncated")]) == 0
     ctx.close()
+
+
+def _se_pairs(g):
+    """Each stitch edge once, (u, v) with u < v, int32 [m, 2]."""
+    e = g.se_edges()
+    return np.ascontiguousarray(e[e[:, 0] < e[:, 1]], dtype=np.int32) if e.size else np.zeros((0, 2), np.int32)
+
+
+def test_stitch_pairs_entry_point():
+    """mpld_decompose_batch_pairs_async (stitch edges as pairs, SE CSR built on
+    the device) gives the oracle's colours and per-layout counts, pair order
+    and direction notwithstanding; bad pairs are rejected."""
+    graphs, k, alpha = synth.config_graphs(1)
+    b = synth.concat(graphs[:6])
+    pairs = _se_pairs(b)
+    assert pairs.shape[0] > 0
+    rng = np.random.default_rng(0)
+    shuffled = pairs[rng.permutation(pairs.shape[0])].copy()
+    flip = rng.random(shuffled.shape[0]) < 0.5
+    shuffled[flip] = shuffled[flip][:, ::-1]
+    ref = oracle.decompose(b, k, alpha, max_steps=0)
+    ctx = mp.Context(0, b.n, b.n_layouts)
+    for pp in (pairs, shuffled):
+        t = ctx.submit_pairs(b.layout_offsets, b.n, b.ce_rowptr, b.ce_col, pp, k, alpha, 0, mp.MPLD_FLAG_VALIDATE)
+        r = ctx.wait(t)
+        assert np.array_equal(r["colors"], ref["colors"])
+        for li, (c, s_, cst) in enumerate(ref["per_layout"]):
+            assert (int(r["n_conflicts"][li]), int(r["n_stitches"][li]), float(r["cost"][li])) == (c, s_, cst)
+    bad = pairs.copy()
+    bad[0, 1] = b.n  # out of range
+    with pytest.raises(mp.MPLDError):
+        ctx.submit_pairs(b.layout_offsets, b.n, b.ce_rowptr, b.ce_col, bad, k, alpha, 0, mp.MPLD_FLAG_VALIDATE)
+    dup = np.concatenate([pairs, pairs[:1]])  # a duplicate stitch edge: caught by the device validation
+    with pytest.raises(mp.MPLDError):
+        ctx.wait(ctx.submit_pairs(b.layout_offsets, b.n, b.ce_rowptr, b.ce_col, dup, k, alpha, 0,
+                                  mp.MPLD_FLAG_VALIDATE))
+    ctx.close()
