@@ -29,10 +29,13 @@ def out():
             "stats": torch.zeros(len(mp.STAT_NAMES), dtype=torch.int64).pin_memory()}
 
 
-outs = [out(), out()]
+outs = [out(), out(), out()]
 ctx = mp.Context(0, b.n, L)
-sub = lambda i: ctx.submit(h[0], b.n, h[1], h[2], h[3], h[4], k, alpha, 0, 1, out=outs[i & 1])  # noqa: E731
-ctx.wait(sub(0))
+se = b.se_edges()
+pairs = pin(np.ascontiguousarray(se[se[:, 0] < se[:, 1]], dtype=np.int32))
+sub = lambda i: ctx.submit_pairs(h[0], b.n, h[1], h[2], pairs, k, alpha, 0, 1, out=outs[i % 3])  # noqa: E731
+for i in range(3):
+    ctx.wait(sub(i))
 N = 10
 t0 = time.perf_counter()
 for i in range(N):
@@ -44,19 +47,28 @@ for i in range(N):
     a = time.perf_counter()
     t = sub(i)
     ts.append(time.perf_counter() - a)
-    if i:
-        ctx.wait(t - 1)
+    if i >= 2:
+        ctx.wait(t - 2)
+ctx.wait(t - 1)
 ctx.wait(t)
 print("pipelined ms/step", (time.perf_counter() - t0) * 1e3 / N, "submit call ms", [round(x * 1e3, 3) for x in ts])
-# H2D alone
-d = [torch.empty_like(x, device="cuda") for x in h]
+# H2D alone (the pairs entry point's inputs), D2H alone (its outputs)
+hin = h[:3] + [pairs]
+d = [torch.empty_like(x, device="cuda") for x in hin]
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 for i in range(N):
-    for dd, x in zip(d, h):
+    for dd, x in zip(d, hin):
         dd.copy_(x, non_blocking=True)
 torch.cuda.synchronize()
-print("H2D only ms/step", (time.perf_counter() - t0) * 1e3 / N, "bytes", sum(x.numel() * 4 for x in h))
+print("H2D only ms/step", (time.perf_counter() - t0) * 1e3 / N, "bytes", sum(x.numel() * 4 for x in hin))
+dc = torch.empty(b.n, dtype=torch.int32, device="cuda")
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for i in range(N):
+    outs[0]["colors"].copy_(dc, non_blocking=True)
+torch.cuda.synchronize()
+print("D2H colours only ms/step", (time.perf_counter() - t0) * 1e3 / N)
 # blocking host call
 t0 = time.perf_counter()
 for i in range(N):
