@@ -654,6 +654,7 @@ __global__ void __launch_bounds__(1024) mpld_simplify_tail(GraphView g, Workspac
   pdl_begin();
   cg::cluster_group cl = cg::this_cluster();
   __shared__ int s_item[2][kTQ];
+  const int tq = min(max(w.tail_slots, 0), kTQ);  // slots in use (MPLD_TAIL_SLOTS lowers it: tests)
   __shared__ int s_n[2];
   __shared__ int s_tot;
   const int rank = (int)cl.block_rank(), nc = (int)cl.num_blocks();
@@ -676,21 +677,21 @@ __global__ void __launch_bounds__(1024) mpld_simplify_tail(GraphView g, Workspac
     __syncthreads();
     auto push = [&](int u) {
       const int i = atomicAdd(&s_n[outs], 1);
-      if (i < kTQ) s_item[outs][i] = u;
+      if (i < tq) s_item[outs][i] = u;
       else ovf[outs][atomicAdd(&ctl->tovf[outs], 1)] = u;
     };
     if (t == 0) {
       for (int i = rank * (int)blockDim.x + threadIdx.x; i < total; i += nc * (int)blockDim.x)
         peel_vertex(g, w, k, r, __ldcg(&g_first[i]), push);
     } else {
-      const int mine = min(s_n[in], kTQ);
+      const int mine = min(s_n[in], tq);
       for (int i = threadIdx.x; i < mine; i += blockDim.x) peel_vertex(g, w, k, r, s_item[in][i], push);
       for (int i = rank * (int)blockDim.x + threadIdx.x; i < n_ovf; i += nc * (int)blockDim.x)
         peel_vertex(g, w, k, r, __ldcg(&ovf[in][i]), push);
     }
     cl.sync();  // the round's decrements are done; every CTA's output slot is complete
     if (threadIdx.x < 32) {
-      const int x = (int)threadIdx.x < nc ? min(*cl.map_shared_rank(&s_n[outs], (int)threadIdx.x), kTQ) : 0;
+      const int x = (int)threadIdx.x < nc ? min(*cl.map_shared_rank(&s_n[outs], (int)threadIdx.x), tq) : 0;
       const int sum = __reduce_add_sync(0xffffffffu, x);
       if (threadIdx.x == 0) s_tot = sum;
     }
@@ -954,6 +955,7 @@ __global__ void __launch_bounds__(1024) mpld_recover_tail(GraphView g, Workspace
   pdl_begin();
   cg::cluster_group cl = cg::this_cluster();
   __shared__ int s_item[2][kTQ];
+  const int tq = min(max(w.tail_slots, 0), kTQ);  // slots in use (MPLD_TAIL_SLOTS lowers it: tests)
   __shared__ int s_n[2];
   __shared__ int s_pref[kTC + 1];
   const int rank = (int)cl.block_rank(), nc = (int)cl.num_blocks();
@@ -972,7 +974,7 @@ __global__ void __launch_bounds__(1024) mpld_recover_tail(GraphView g, Workspace
     __syncthreads();
     auto push = [&](int u) {
       const int i = atomicAdd(&s_n[outs], 1);
-      if (i < kTQ) s_item[outs][i] = u;
+      if (i < tq) s_item[outs][i] = u;
       else ovf[outs][atomicAdd(&ctl->tovf[outs], 1)] = u;
     };
 #if MPLD_TAIL_LOCAL
@@ -982,7 +984,7 @@ __global__ void __launch_bounds__(1024) mpld_recover_tail(GraphView g, Workspace
       for (int i = rank * (int)blockDim.x + threadIdx.x; i < total; i += nc * (int)blockDim.x)
         recover_vertex(g, w, k, colors, __ldcg(&g_first[i]), push);
     } else {
-      const int mine = min(s_n[in], kTQ);
+      const int mine = min(s_n[in], tq);
       for (int i = threadIdx.x; i < mine; i += blockDim.x) recover_vertex(g, w, k, colors, s_item[in][i], push);
       for (int i = rank * (int)blockDim.x + threadIdx.x; i < n_ovf; i += nc * (int)blockDim.x)
         recover_vertex(g, w, k, colors, __ldcg(&ovf[in][i]), push);
@@ -1008,7 +1010,7 @@ __global__ void __launch_bounds__(1024) mpld_recover_tail(GraphView g, Workspace
     cl.sync();  // the level is coloured; every CTA's output slot is complete
     if (threadIdx.x < 32) {  // one remote count per lane, a warp scan
       const int lane = threadIdx.x;
-      const int x = lane < nc ? min(*cl.map_shared_rank(&s_n[outs], lane), kTQ) : 0;
+      const int x = lane < nc ? min(*cl.map_shared_rank(&s_n[outs], lane), tq) : 0;
       int y = x;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {

@@ -110,6 +110,7 @@ struct mpld_context {
   unsigned long long* bsum = nullptr;
   unsigned epoch = 0;         // search calls so far (tags wq_flag)
   unsigned spill_iters = 256; // heavy-search spill threshold; MPLD_HEAVY_SPILL overrides (tests of the spill path)
+  int tail_slots = 1 << 30;   // cluster-tail frontier slots per CTA (capped at the kernel's); MPLD_TAIL_SLOTS lowers it
   Control* ctl = nullptr;
   // phase-split calls: the prepared graph
   GraphView g{};
@@ -230,7 +231,7 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
 Workspace workspace(mpld_context* ctx) {
   return Workspace{ctx->deg,   ctx->hround, ctx->bmask,  ctx->prio,  ctx->q0,    ctx->q1,    ctx->roots,
                    ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->ctl,   ctx->wq,
-                   ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters};
+                   ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters, ctx->tail_slots};
 }
 
 // phase 1: validate?, simplification, components (colours initialised to -1)
@@ -496,6 +497,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   ctx->blocks_discover = resident_blocks_discover(ctx->num_sms);
   ctx->blocks_stream = resident_blocks_evaluate(ctx->num_sms);
   if (const char* pd = std::getenv("MPLD_PDL")) set_pdl(std::strtol(pd, nullptr, 10) != 0);
+  if (const char* ts = std::getenv("MPLD_TAIL_SLOTS")) ctx->tail_slots = (int)std::strtol(ts, nullptr, 10);
   if (const char* hs = std::getenv("MPLD_HEAVY_SPILL")) {
     const long v = std::strtol(hs, nullptr, 10);
     if (v >= 64) ctx->spill_iters = (unsigned)std::min<long>(v & ~63L, 1L << 30);

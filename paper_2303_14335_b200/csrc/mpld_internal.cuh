@@ -164,6 +164,7 @@ struct Workspace {
   unsigned long long* bsum;  // [n / kScanTile + 2] block sums of that scan
   unsigned epoch;     // this search call's tag for wq_flag
   unsigned spill_iters;  // a heavy unit's iterations before it may spill (multiple of 64; MPLD_HEAVY_SPILL)
+  int tail_slots;        // cluster tails: frontier slots per CTA in use (MPLD_TAIL_SLOTS lowers it: tests)
 };
 
 // Layout of vertex v: the l with layout_off[l] <= v < layout_off[l+1] (binary

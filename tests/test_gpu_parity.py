@@ -477,3 +477,30 @@ def test_stitch_pairs_entry_point():
         ctx.wait(ctx.submit_pairs(b.layout_offsets, b.n, b.ce_rowptr, b.ce_col, dup, k, alpha, 0,
                                   mp.MPLD_FLAG_VALIDATE))
     ctx.close()
+
+
+@pytest.mark.parametrize("slots", ["0", "4", "64"])
+def test_recovery_cluster_tail_spill(monkeypatch, slots):
+    """The recovery's cluster tail keeps each CTA's ready vertices in its shared
+    memory and spills the rest to a global list processed cluster-wide; with the
+    slots capped (0: every vertex after the tail's first level spills) the
+    colours must not change (R9)."""
+    monkeypatch.setenv("MPLD_TAIL_SLOTS", slots)
+    graphs, k, alpha = synth.config_graphs(1)
+    b = synth.concat(graphs[:8])
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    ctx = mp.Context(0, b.n, b.n_layouts)  # reads MPLD_TAIL_SLOTS
+    colors = torch.empty(b.n, dtype=torch.int32, device=dev)
+    counts = torch.empty(2 * b.n_layouts, dtype=torch.int64, device=dev)
+    cost = torch.empty(b.n_layouts, dtype=torch.float64, device=dev)
+    stats = torch.empty(len(mp.STAT_NAMES), dtype=torch.int64, device=dev)
+    ctx.decompose_device(T(b.layout_offsets), b.n, T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr), T(b.se_col),
+                         k, alpha, 0, colors, counts, cost, stats, flags=mp.MPLD_FLAG_VALIDATE)
+    torch.cuda.synchronize()
+    ref = oracle.decompose(b, k, alpha, max_steps=0)
+    assert np.array_equal(colors.cpu().numpy(), ref["colors"])
+    c2 = counts.cpu().numpy().reshape(-1, 2)
+    for li, (c, s_, cst) in enumerate(ref["per_layout"]):
+        assert (int(c2[li, 0]), int(c2[li, 1]), float(cost[li])) == (c, s_, cst)
+    ctx.close()
