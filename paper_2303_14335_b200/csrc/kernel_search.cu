@@ -17,22 +17,24 @@
 // Cover/uncover (Eq. 2) become mask AND/OR; backtracking pops a 32-byte frame.
 // Components of <= 32 vertices run on 32-bit words, larger ones on 64-bit.
 //
-// Two kernels:
-//   mpld_exact_cover_search<K>        one warp per component seed: warp-parallel
-//                                     discovery of the component, relabelling to
-//                                     the R5 column order, then the sequential DFS
-//                                     on lane 0 (the oracle's exact node order and
-//                                     budget, R7);
-//   mpld_exact_cover_search_heavy<K>  exact mode (max_steps <= 0) only: one
-//                                     128-thread CTA per component whose
-//                                     sequential search needed more than the
-//                                     light budget.  The canonical tree is split
-//                                     level-synchronously into >= 128 subtrees
-//                                     (DFS order kept, nodes stored as paths),
-//                                     lanes search subtrees with a shared
-//                                     incumbent keyed (cost, subtree index); the
-//                                     first optimal leaf of R7 is recovered
-//                                     exactly.
+// Kernels:
+//   mpld_component_discover           one warp per component seed: warp-parallel
+//                                     discovery of the component and relabelling
+//                                     to the R5 column order into the pool;
+//   mpld_exact_cover_search<K>        the sequential DFS of R4-R7 (the oracle's
+//                                     node order and budget), one component per
+//                                     lane, 32 per warp (larger than 32 vertices:
+//                                     lane 0 alone);
+//   mpld_exact_cover_search_heavy<K,W> exact mode (max_steps <= 0) only: one warp
+//                                     per component whose sequential search
+//                                     needed more than the light budget; lanes
+//                                     search disjoint parts of the canonical tree
+//                                     with work donation and a (cost, leaf path)
+//                                     incumbent, very large searches spill their
+//                                     open work to a GPU-wide queue; the first
+//                                     optimal leaf of R7 is recovered exactly
+//                                     (DESIGN.md §1);
+//   mpld_partition_*                  the cost-balanced shard partition (scan).
 #include <climits>
 
 #include "mpld_internal.cuh"
@@ -1036,6 +1038,8 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
                                        : (n - kDonateMinLevels <= 0 ? 0ull : ((1ull << (n - kDonateMinLevels)) - 1ull));
   unsigned iters = 0;
   spilled = false;
+  // large components (the ones idle warps stay for) feed the queue early
+  const unsigned spill_at = n >= kHelpersMinN ? min(w.spill_iters, 64u) : w.spill_iters;
   // lane DFS state: the node (C, B, U, cost, maxused) and its path P; frames
   // d0..depth-1, the deepest in registers; open bit d = frame d has an untried
   // child beyond its current one.  Lane 0 starts at the unit's node.
@@ -1258,7 +1262,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       mine = warp_min_key<kTwo>(gcost, gP) == lane;
     }
    }
-    if (MPLD_SPILL && !all_idle && iters >= w.spill_iters) {
+    if (MPLD_SPILL && !all_idle && iters >= spill_at) {
       // share the best cost with the other units of a spilled component (no
       // lock: their keys are merged when the units end)
       if (u.slot >= 0) {
