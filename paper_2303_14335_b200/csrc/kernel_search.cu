@@ -881,6 +881,9 @@ constexpr int kStealMinIdle = MPLD_STEAL_MIN_IDLE;  // donation rounds only when
 #ifndef MPLD_SPILL
 #define MPLD_SPILL 1
 #endif
+#ifndef MPLD_SPILL_LARGE
+#define MPLD_SPILL_LARGE 64  // spill threshold of components of >= kHelpersMinN vertices
+#endif
 #ifndef MPLD_POLL_CAP
 #define MPLD_POLL_CAP 512
 #endif
@@ -1039,7 +1042,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
   unsigned iters = 0;
   spilled = false;
   // large components (the ones idle warps stay for) feed the queue early
-  const unsigned spill_at = n >= kHelpersMinN ? min(w.spill_iters, 64u) : w.spill_iters;
+  const unsigned spill_at = n >= kHelpersMinN ? min(w.spill_iters, (unsigned)MPLD_SPILL_LARGE) : w.spill_iters;
   // lane DFS state: the node (C, B, U, cost, maxused) and its path P; frames
   // d0..depth-1, the deepest in registers; open bit d = frame d has an untried
   // child beyond its current one.  Lane 0 starts at the unit's node.
