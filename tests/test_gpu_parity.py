@@ -504,3 +504,43 @@ def test_recovery_cluster_tail_spill(monkeypatch, slots):
     for li, (c, s_, cst) in enumerate(ref["per_layout"]):
         assert (int(c2[li, 0]), int(c2[li, 1]), float(cost[li])) == (c, s_, cst)
     ctx.close()
+
+
+def test_bench_launch_config1_sampled():
+    """configs[1] exactly as bench.py times it (bench.workload(0, 16): the ten
+    ISCAS-85-shaped layouts x16 seeds in one batch, exact mode, validation on):
+    Eq. (1) counts recomputed from the colours of every layout, and the oracle
+    decomposes every layout on its own (layouts are independent, so each slice
+    of the batch must equal its own oracle result element by element)."""
+    graphs = []
+    for r in range(16):
+        gs, k, alpha = synth.config_graphs(1, seed=10 * r)
+        graphs += gs
+    b = synth.concat(graphs)
+    got = mp.decompose_graph(b, k, alpha, max_steps=0, flags=mp.MPLD_FLAG_VALIDATE)
+    colors = got["colors"]
+    assert got["stats"]["error"] == 0 and got["stats"]["truncated"] == 0
+    assert ((colors >= 0) & (colors < k)).all()
+    offs = b.layout_offsets
+    ce, se = b.ce_edges(), b.se_edges()
+    lay_ce = np.searchsorted(offs, ce[:, 0], side="right") - 1
+    lay_se = np.searchsorted(offs, se[:, 0], side="right") - 1
+    nc = np.bincount(lay_ce, weights=(colors[ce[:, 0]] == colors[ce[:, 1]]), minlength=b.n_layouts)
+    ns = np.bincount(lay_se, weights=(colors[se[:, 0]] != colors[se[:, 1]]), minlength=b.n_layouts)
+    assert np.array_equal(nc.astype(np.int64), np.asarray(got["n_conflicts"], dtype=np.int64))
+    assert np.array_equal(ns.astype(np.int64), np.asarray(got["n_stitches"], dtype=np.int64))
+    parts = synth.split(b)
+    for li in range(b.n_layouts):  # every layout (~0.2 s of oracle each)
+        ref = oracle.decompose(parts[li], k, alpha, max_steps=0)
+        a, e = int(offs[li]), int(offs[li + 1])
+        assert np.array_equal(colors[a:e], ref["colors"]), li
+        c, s_, cst = ref["per_layout"][0]
+        assert (int(got["n_conflicts"][li]), int(got["n_stitches"][li]), float(got["cost"][li])) == (c, s_, cst)
+
+
+def test_full_size_config3_element_by_element():
+    """configs[3] at full size (10^6 polygons, one layout, k = 3) in exact mode,
+    as bench.py --config 3 times it: full element-by-element parity (~20 s of
+    oracle)."""
+    graphs, k, alpha = synth.config_graphs(3)
+    _assert_same(graphs[0], k, alpha, max_steps=0)
