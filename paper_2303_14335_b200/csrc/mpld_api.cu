@@ -131,6 +131,7 @@ struct mpld_context {
   bool prep_forked = false;
   // host-API staging (device copies of host inputs / outputs)
   int64_t cap_ce = 0, cap_se = 0, cap_stage_n = 0;
+  int32_t cap_stage_layouts = 0;  // own capacity: ensure_workspace() grows cap_layouts first
   int* h_lo = nullptr;
   int* h_ce_rp = nullptr;
   int* h_ce_col = nullptr;
@@ -663,7 +664,7 @@ int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32
   if (rc != MPLD_OK) return rc;
   // staging buffers
   if (n > ctx->cap_stage_n || !ctx->h_ce_rp) {
-    ctx->cap_stage_n = ctx->cap_n;
+    ctx->cap_stage_n = std::max<int64_t>(n, ctx->cap_n);
     if (grow(&ctx->h_ce_rp, ctx->cap_stage_n + 1) != cudaSuccess ||
         grow(&ctx->h_se_rp, ctx->cap_stage_n + 1) != cudaSuccess || grow(&ctx->h_colors, ctx->cap_stage_n) != cudaSuccess)
       return fail(MPLD_ERR_NOMEM, "staging allocation failed");
@@ -676,11 +677,11 @@ int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32
     ctx->cap_se = std::max<int64_t>(m_se, ctx->cap_se * 3 / 2);
     if (grow(&ctx->h_se_col, ctx->cap_se) != cudaSuccess) return fail(MPLD_ERR_NOMEM, "staging allocation failed");
   }
-  if (!ctx->h_lo || n_layouts > ctx->cap_layouts || !ctx->h_counts) {
-    ctx->cap_layouts = std::max<int32_t>(n_layouts, ctx->cap_layouts);
-    if (grow(&ctx->h_lo, ctx->cap_layouts + 1) != cudaSuccess ||
-        grow(&ctx->h_counts, 2 * (int64_t)ctx->cap_layouts) != cudaSuccess ||
-        grow(&ctx->h_cost, ctx->cap_layouts) != cudaSuccess || grow(&ctx->h_stats, MPLD_STAT_LEN) != cudaSuccess)
+  if (!ctx->h_lo || n_layouts > ctx->cap_stage_layouts || !ctx->h_counts) {
+    ctx->cap_stage_layouts = std::max<int32_t>(n_layouts, ctx->cap_layouts);
+    if (grow(&ctx->h_lo, ctx->cap_stage_layouts + 1) != cudaSuccess ||
+        grow(&ctx->h_counts, 2 * (int64_t)ctx->cap_stage_layouts) != cudaSuccess ||
+        grow(&ctx->h_cost, ctx->cap_stage_layouts) != cudaSuccess || grow(&ctx->h_stats, MPLD_STAT_LEN) != cudaSuccess)
       return fail(MPLD_ERR_NOMEM, "staging allocation failed");
   }
   cudaStream_t s = ctx->stream;

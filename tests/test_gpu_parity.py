@@ -544,3 +544,59 @@ def test_full_size_config3_element_by_element():
     oracle)."""
     graphs, k, alpha = synth.config_graphs(3)
     _assert_same(graphs[0], k, alpha, max_steps=0)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("size", [4, 8, 16, 32, 64])
+def test_full_size_stress_sweep(size, k):
+    """configs[4] at full size: 10^5 components of `size` vertices in one launch
+    (500 distinct components, each repeated in 200 layouts).  Every copy of a
+    component must get the same colours wherever it lands (light lanes, heavy
+    warps, work queue), the counts must be recomputable from the colours, and
+    the oracle recomputes a sample of the distinct components one by one."""
+    tmpl = synth.stress_components(size, 500, k, seed=7000 + 10 * size + k)
+    g = synth.concat([tmpl] * 200, name=f"stress{size}_k{k}_1e5")
+    budget = 0 if size <= 16 else 20000  # exact mode where the oracle can follow
+    got = mp.decompose_graph(g, k, 0.1, max_steps=budget, flags=mp.MPLD_FLAG_VALIDATE)
+    colors = got["colors"]
+    ce_adj, se_adj = tmpl.ce_adj(), tmpl.se_adj()
+    hround, _ = oracle.simplify(tmpl.n, ce_adj, se_adj, k)
+    comps = oracle.components(tmpl.n, ce_adj, se_adj, hround)
+    # a component of <= k vertices has every degree < k: the simplification hides it whole
+    assert len(comps) == (500 if size > k else 0)
+    assert got["stats"]["components"] == 200 * len(comps)
+    assert ((colors >= 0) & (colors < k)).all()
+    per = colors.reshape(200, tmpl.n)
+    assert (per == per[0]).all()
+    ce = g.ce_edges()
+    assert int((colors[ce[:, 0]] == colors[ce[:, 1]]).sum()) == int(got["n_conflicts"].sum())
+    assert (got["n_conflicts"] == got["n_conflicts"][0]).all()
+    assert (got["n_stitches"] == 0).all()
+    assert np.allclose(got["cost"], got["n_conflicts"].astype(np.float64))
+    if budget == 0:
+        assert got["stats"]["truncated"] == 0
+    w = oracle.alpha_units(0.1)
+    for order in random.Random(size * 10 + k).sample(comps, min(len(comps), 6 if size >= 32 else 20)):
+        r = oracle.solve_component(order, ce_adj, se_adj, k, w, budget)
+        for v, c in r["global_colors"].items():
+            assert per[0, v] == c
+    if not comps:  # everything recovered: the whole template equals the oracle's run
+        assert np.array_equal(per[0], oracle.decompose(tmpl, k, 0.1, max_steps=0)["colors"])
+
+
+def test_host_staging_grows_with_layout_count():
+    """Regression: a host call with more layouts than any earlier call must grow
+    the device staging of layout offsets / counts / costs (it once sized them
+    from the workspace capacity, already grown by then, and overflowed)."""
+    small = synth.concat([synth.stress_components(6, 4, 3, seed=s) for s in range(2)])
+    ref_s = oracle.decompose(small, 3, 0.1, max_steps=0)
+    got = mp.decompose_graph(small, 3, 0.1, max_steps=0)
+    assert np.array_equal(got["colors"], ref_s["colors"])
+    tmpl = synth.stress_components(6, 4, 3, seed=9)
+    ref_t = oracle.decompose(tmpl, 3, 0.1, max_steps=0)
+    for n_lay in (300, 1000):
+        big = synth.concat([tmpl] * n_lay)
+        got = mp.decompose_graph(big, 3, 0.1, max_steps=0)
+        assert np.array_equal(got["colors"].reshape(n_lay, tmpl.n), np.tile(ref_t["colors"], (n_lay, 1)))
+        c, s_, cst = ref_t["per_layout"][0]
+        assert (got["n_conflicts"] == c).all() and (got["n_stitches"] == s_).all() and (got["cost"] == cst).all()
