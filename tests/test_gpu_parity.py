@@ -600,3 +600,43 @@ def test_host_staging_grows_with_layout_count():
         assert np.array_equal(got["colors"].reshape(n_lay, tmpl.n), np.tile(ref_t["colors"], (n_lay, 1)))
         c, s_, cst = ref_t["per_layout"][0]
         assert (got["n_conflicts"] == c).all() and (got["n_stitches"] == s_).all() and (got["cost"] == cst).all()
+
+
+def test_capacity_sequence_all_entry_points():
+    """Batches that grow and shrink in vertices, edges and layout count, sent
+    in turn through every entry point of ONE context that starts small (and the
+    process-wide host call): each result must be the oracle's, so no staging
+    or workspace buffer may be sized from a capacity another buffer grew."""
+    shapes = [(1, 150), (40, 50), (2, 1500), (1, 30), (150, 12), (3, 400), (300, 10), (1, 2500)]
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    ctx = mp.Context(0, 1 << 6, 1)
+    for i, (n_lay, nv) in enumerate(shapes):
+        b = synth.concat([synth.make_layout(nv, int(1.2 * nv), k=3, stitch_prob=0.5, comp_max=8, seed=50 * i + j)
+                          for j in range(n_lay)])
+        k, alpha = 3, 0.1
+        ref = oracle.decompose(b, k, alpha, max_steps=0)
+        want_c = np.array([p[0] for p in ref["per_layout"]], dtype=np.int64)
+        want_s = np.array([p[1] for p in ref["per_layout"]], dtype=np.int64)
+        want_cost = np.array([p[2] for p in ref["per_layout"]], dtype=np.float64)
+        results = [mp.decompose_graph(b, k, alpha, max_steps=0, flags=mp.MPLD_FLAG_VALIDATE)]
+        t1 = ctx.submit(b.layout_offsets, b.n, b.ce_rowptr, b.ce_col, b.se_rowptr, b.se_col, k, alpha, 0,
+                        mp.MPLD_FLAG_VALIDATE)
+        t2 = ctx.submit_pairs(b.layout_offsets, b.n, b.ce_rowptr, b.ce_col, _se_pairs(b), k, alpha, 0,
+                              mp.MPLD_FLAG_VALIDATE)
+        results += [ctx.wait(t1), ctx.wait(t2)]
+        colors = torch.empty(b.n, dtype=torch.int32, device=dev)
+        counts = torch.empty(2 * b.n_layouts, dtype=torch.int64, device=dev)
+        cost = torch.empty(b.n_layouts, dtype=torch.float64, device=dev)
+        ctx.decompose_device(T(b.layout_offsets), b.n, T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr), T(b.se_col),
+                             k, alpha, 0, colors, counts, cost, flags=mp.MPLD_FLAG_VALIDATE)
+        torch.cuda.synchronize()
+        c2 = counts.cpu().numpy().reshape(-1, 2)
+        results.append({"colors": colors.cpu().numpy(), "n_conflicts": c2[:, 0], "n_stitches": c2[:, 1],
+                        "cost": cost.cpu().numpy()})
+        for path, r in zip(("host", "async", "pairs", "device"), results):
+            assert np.array_equal(r["colors"], ref["colors"]), (i, path)
+            assert np.array_equal(np.asarray(r["n_conflicts"], np.int64), want_c), (i, path)
+            assert np.array_equal(np.asarray(r["n_stitches"], np.int64), want_s), (i, path)
+            assert np.array_equal(np.asarray(r["cost"], np.float64), want_cost), (i, path)
+    ctx.close()
