@@ -604,8 +604,8 @@ def test_host_staging_grows_with_layout_count():
 
 def test_capacity_sequence_all_entry_points():
     """Batches that grow and shrink in vertices, edges and layout count, sent
-    in turn through every entry point of ONE context that starts small (and the
-    process-wide host call): each result must be the oracle's, so no staging
+    in turn through every entry point of ONE context that starts small (async,
+    pairs, device, the sharded phases; and the process-wide host call): each result must be the oracle's, so no staging
     or workspace buffer may be sized from a capacity another buffer grew."""
     shapes = [(1, 150), (40, 50), (2, 1500), (1, 30), (150, 12), (3, 400), (300, 10), (1, 2500)]
     dev = torch.device("cuda:0")
@@ -634,7 +634,21 @@ def test_capacity_sequence_all_entry_points():
         c2 = counts.cpu().numpy().reshape(-1, 2)
         results.append({"colors": colors.cpu().numpy(), "n_conflicts": c2[:, 0], "n_stitches": c2[:, 1],
                         "cost": cost.cpu().numpy()})
-        for path, r in zip(("host", "async", "pairs", "device"), results):
+        # the phase-split path, two shards simulated on this GPU (combined by max)
+        graph = [T(b.layout_offsets), T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr), T(b.se_col)]
+        ctx.prepare_device(graph[0], b.n, *graph[1:], k, colors, counts, flags=mp.MPLD_FLAG_VALIDATE)
+        parts = []
+        for sh in range(2):
+            c = colors.clone()
+            ctx.search_device(alpha, 0, sh, 2, c)
+            parts.append(c)
+        combined = torch.stack(parts).amax(0).contiguous()
+        ctx.finish_device(alpha, combined, counts, cost)
+        torch.cuda.synchronize()
+        c2 = counts.cpu().numpy().reshape(-1, 2)
+        results.append({"colors": combined.cpu().numpy(), "n_conflicts": c2[:, 0], "n_stitches": c2[:, 1],
+                        "cost": cost.cpu().numpy()})
+        for path, r in zip(("host", "async", "pairs", "device", "sharded"), results):
             assert np.array_equal(r["colors"], ref["colors"]), (i, path)
             assert np.array_equal(np.asarray(r["n_conflicts"], np.int64), want_c), (i, path)
             assert np.array_equal(np.asarray(r["n_stitches"], np.int64), want_s), (i, path)
