@@ -111,14 +111,23 @@ enum mpld_stat {
 const char* mpld_last_error(void);
 const char* mpld_version(void);
 
-/* One layout, host buffers (end-to-end call: H2D copy, all kernels, D2H copy). */
+/* One layout, host buffers (end-to-end call: H2D copy, all kernels, D2H copy).
+ * The north_star signature: PAPER.md §2.1 Eq. (1) is the objective, §2.2 /
+ * Fig. 2 the flow (simplify -> colouring solver -> recover), §2.3 / Alg. 1 the
+ * solver; colors [n], *n_conflicts (Eq. 1b), *n_stitches (Eq. 1c), *cost
+ * (Eq. 1a) are written on MPLD_OK.  No validation (see mpld_decompose_batch). */
 int mpld_decompose(int32_t n, const int32_t* ce_rowptr, const int32_t* ce_col,
                    const int32_t* se_rowptr, const int32_t* se_col, int32_t k,
                    double alpha, int64_t max_steps, int32_t* colors,
                    int64_t* n_conflicts, int64_t* n_stitches, double* cost);
 
 /* A batch of n_layouts layouts (disjoint union), host buffers.
- * layout_offsets [n_layouts+1]; n_conflicts, n_stitches, cost: [n_layouts]. */
+ * layout_offsets [n_layouts+1]; n_conflicts, n_stitches, cost: [n_layouts].
+ * Alg. 1 lines 1-4 ("the original DG will be decomposed into sub-graphs ...
+ * parallelly executed on different blocks"): every component of every layout
+ * of the batch is searched in the same launches; a batched layout decomposes
+ * exactly as alone (R10).  flags: MPLD_FLAG_VALIDATE.  Blocks until
+ * the results are on the host. */
 int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
                          const int32_t* ce_rowptr, const int32_t* ce_col,
                          const int32_t* se_rowptr, const int32_t* se_col, int32_t k,
@@ -130,11 +139,17 @@ int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32
 typedef struct mpld_context mpld_context;
 
 /* Create a context on `device` with workspace for up to max_vertices vertices
- * and max_layouts layouts (grown on demand by later calls). */
+ * and max_layouts layouts (grown on demand by later calls).  A context owns
+ * its device workspace and control block; calls of one context may be
+ * enqueued on different streams (a call on a stream other than the previous
+ * call's waits for that call's last operation through an event), but the
+ * context must not be used from several host threads at once. */
 int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, mpld_context** out);
 void mpld_context_destroy(mpld_context* ctx);
 
-/* Enqueue the whole hot path on `stream` (a cudaStream_t; NULL = legacy default).
+/* Enqueue the whole hot path on `stream` (a cudaStream_t; NULL = legacy default):
+ * the same computation as mpld_decompose_batch (§2.2 flow, §2.3
+ * Alg. 1 solver, Eq. (1) outputs) on inputs already resident in HBM.
  * The recovery's preparation runs on the context's own second stream, forked
  * from `stream` by an event after the simplification and joined back before
  * the recovery, so all work stays ordered with respect to `stream`.
@@ -198,25 +213,49 @@ int mpld_wait(mpld_context* ctx, int64_t ticket);
  * layout batch can be searched by shard_count processes (one per GPU):
  *   1. every process: mpld_prepare_device   (validate?, simplification, components)
  *   2. every process: mpld_search_device     with its shard_index: discovers every
- *      component, estimates its search cost as n * k^n (capped at 2^40; the
+ *      component, estimates its search cost as n * k^n (capped at 2^32; the
  *      north_star's "size x k^n"), takes the inclusive prefix sum of the
  *      estimates in order of the components' roots (smallest vertex ids), and
  *      searches the components whose cost interval starts in the shard_index-th
  *      of shard_count equal parts of the total (contiguous root ranges of
  *      equal estimated cost, computed identically by every process); writes
  *      their colours into d_colors and leaves -1 on every other vertex;
- *   3. the caller combines d_colors across the processes with an element-wise
- *      maximum (an NCCL all-reduce MAX over NVLink) — the only exchange;
+ *   3. the caller combines d_colors across the processes — the only exchange:
+ *      an element-wise maximum (an NCCL all-reduce MAX of n int32), or the
+ *      compact lists of mpld_shard_export / mpld_shard_import (all-gather);
  *   4. every process: mpld_finish_device     (recovery of the hidden vertices, Eq. 1).
  * The graph pointers and k of phase 1 are remembered by the context and must
  * stay valid until phase 4 is enqueued.  With shard_count == 1 the phases
  * compute exactly mpld_decompose_device.  All calls are stream-ordered. */
+/* Phase 1 — PAPER.md §2.2 "simplify the layout graph" and Alg. 1 lines 1-3
+ * (components).  d_counts is zeroed here. */
 int mpld_prepare_device(mpld_context* ctx, void* stream, int32_t n_layouts, const int32_t* d_layout_offsets,
                         int32_t n, const int32_t* d_ce_rowptr, const int32_t* d_ce_col,
                         const int32_t* d_se_rowptr, const int32_t* d_se_col, int32_t k, uint32_t flags,
                         int32_t* d_colors, int64_t* d_counts);
+/* Phase 2 — Alg. 1 lines 4-19 (the exact-cover search) over this shard's
+ * components; d_colors of the other kept vertices stay -1. */
 int mpld_search_device(mpld_context* ctx, void* stream, double alpha, int64_t max_steps, int32_t shard_index,
                        int32_t shard_count, int32_t* d_colors);
+/* Phase 3, compact form — instead of combining the full d_colors
+ * arrays, each process exports the colours its search wrote as a compact list
+ * and scatters the lists of all processes (after an all-gather):
+ *   mpld_shard_export: d_pairs [2 * n] int32 receives (vertex, colour) pairs,
+ *     one per vertex with d_colors >= 0 (the vertices of this shard's
+ *     components; order unspecified); *d_count (device int64) their number.
+ *   mpld_shard_import: for each of n_pairs pairs with vertex in [0, n),
+ *     d_colors[vertex] = colour (pairs with vertex < 0 are padding, skipped).
+ * Both are stream-ordered device calls between phases 2 and 4 (the colours of
+ * §2.2's coloring solver, Fig. 2, gathered before the recovery). */
+int mpld_shard_export(mpld_context* ctx, void* stream, const int32_t* d_colors, int32_t* d_pairs,
+                      int64_t* d_count);
+int mpld_shard_import(mpld_context* ctx, void* stream, const int32_t* d_pairs, int64_t n_pairs,
+                      int32_t* d_colors);
+
+/* Phase 4 — §2.2 "recover the nodes removed in simplification step" and
+ * Eq. (1).  d_counts may be any [2*n_layouts] int64 buffer: when it is not
+ * the one of phase 1, or the search was sharded, it is reset and recomputed
+ * from the combined colours (mpld_evaluate). */
 int mpld_finish_device(mpld_context* ctx, void* stream, double alpha, int32_t* d_colors, int64_t* d_counts,
                        double* d_cost, int64_t* d_stats);
 

@@ -14,6 +14,7 @@
 // read in batches of kNb independent loads, items are tiled kP per thread
 // (measured on B200: kP = 1, kNb = 4 and one 1024-thread CTA per SM are the
 // fastest; lockstep tiles of 2-3 items per thread lengthen every level).
+#include <algorithm>
 #include <cooperative_groups.h>
 
 #include "mpld_internal.cuh"
@@ -1095,6 +1096,39 @@ __global__ void __launch_bounds__(256) mpld_evaluate(GraphView g, Workspace w, c
 }
 
 // ---------------------------------------------------------------------------
+// Sharded runs: the colours one shard's search wrote, as a
+// compact list of (vertex, colour) pairs (every vertex a search coloured; -1
+// everywhere else), and the scatter of the lists of all shards.  Appends are
+// warp-aggregated: one atomic per warp and chunk.
+__global__ void __launch_bounds__(256) mpld_shard_export(int n, const int* __restrict__ colors, int* pairs,
+                                                         unsigned long long* count) {
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * blockDim.x;
+  for (int v0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); v0 < n; v0 += stride) {
+    const int v = v0 + lane;
+    const int c = v < n ? __ldg(&colors[v]) : -1;
+    const unsigned m = __ballot_sync(0xffffffffu, c >= 0);
+    if (!m) continue;
+    unsigned long long base = 0ull;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (c >= 0) {
+      const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
+      pairs[2 * at] = v;
+      pairs[2 * at + 1] = c;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) mpld_shard_import(long long m, const int* __restrict__ pairs, int n,
+                                                         int* colors) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+    const int v = __ldg(&pairs[2 * i]);
+    if (v >= 0 && v < n) colors[v] = __ldg(&pairs[2 * i + 1]);  // v < 0: padding of a shorter list
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Stitch edges given as pairs (mpld_decompose_batch_pairs_async): the SE CSR
 // is built on the device — degrees, an exclusive scan, a scatter, each row
 // sorted (rows hold one or two segments' worth of entries).
@@ -1304,6 +1338,20 @@ cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors,
 cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors, double alpha, long long* counts,
                             double* cost, long long* stats, int launches, cudaStream_t s, int blocks) {
   mpld_evaluate<<<blocks, 256, 0, s>>>(g, ws, colors, alpha, counts, cost, stats, launches);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_export(int n, const int* colors, int* pairs, unsigned long long* count, cudaStream_t s,
+                                int blocks) {
+  cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess || n <= 0) return e;
+  mpld_shard_export<<<std::min(blocks, (n + 255) / 256), 256, 0, s>>>(n, colors, pairs, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_import(long long m, const int* pairs, int n, int* colors, cudaStream_t s, int blocks) {
+  if (m <= 0) return cudaSuccess;
+  mpld_shard_import<<<(int)std::min<long long>(blocks, (m + 255) / 256), 256, 0, s>>>(m, pairs, n, colors);
   return cudaGetLastError();
 }
 

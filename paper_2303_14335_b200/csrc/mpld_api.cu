@@ -8,8 +8,11 @@
 //   mpld_exact_cover_search<K> one warp per component of the pool
 //   mpld_exact_cover_search_heavy<K,W> (exact mode) one warp per heavy component, one launch
 //                              per word class (32-bit: n <= 32, 64-bit: n > 32)
-//   mpld_recover               cooperative: LIFO recovery of hidden vertices
-//   mpld_evaluate              Eq. (1) per layout + stats
+//   mpld_recover_prep          (second stream, beside discovery and search) recovery
+//                              predecessor counts and level 0
+//   mpld_recover               cooperative: LIFO recovery of hidden vertices (large levels)
+//   mpld_recover_tail          one thread-block cluster: the last levels, Eq. (1a) costs, stats
+//   mpld_evaluate              only after a sharded search: Eq. (1) per layout + stats
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -123,6 +126,12 @@ struct mpld_context {
   long long* counts = nullptr;  // the prepare phase's d_counts (zeroed by the simplification kernel)
   bool search_counted = false;  // the search accumulated the counts (one shard)
   int searches_since_prepare = 0;
+  // cross-stream ordering: calls share the workspace and control block, so a
+  // call enqueued on a stream other than the previous call's waits for that
+  // call's last operation (ev_last, recorded at the end of every entry point)
+  cudaEvent_t ev_last = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
   // the recovery's share of the final pass runs on `aux` beside the search
   // (forked after the simplification, joined before the recovery)
   cudaStream_t aux = nullptr;
@@ -226,6 +235,23 @@ int check_scalars(int32_t n, int32_t k, double alpha, int* w_stitch) {
   double r = std::nearbyint(a);
   if (std::fabs(a - r) > 1e-6) return fail(MPLD_ERR_ARG, "alpha must be a multiple of 0.001");
   *w_stitch = (int)r;
+  return MPLD_OK;
+}
+
+// A call on a stream other than the previous call's waits for the previous
+// call's last operation (same stream: stream order suffices, and programmatic
+// dependent launch between the call's kernels is kept).
+int order_after_last(mpld_context* ctx, cudaStream_t s) {
+  if (!ctx->has_last || s == ctx->last_stream) return MPLD_OK;
+  const cudaError_t e = cudaStreamWaitEvent(s, ctx->ev_last, 0);
+  return e == cudaSuccess ? MPLD_OK : cuda_fail(e, "cross-stream ordering");
+}
+
+int mark_last(mpld_context* ctx, cudaStream_t s) {
+  const cudaError_t e = cudaEventRecord(ctx->ev_last, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cross-stream ordering");
+  ctx->last_stream = s;
+  ctx->has_last = true;
   return MPLD_OK;
 }
 
@@ -348,6 +374,10 @@ int phase_finish(mpld_context* ctx, cudaStream_t s, double alpha, int* colors, l
     cudaError_t e = cudaStreamWaitEvent(s, ctx->ev_join, 0);
     if (e != cudaSuccess) return cuda_fail(e, "prep join");
   }
+  if (!out.enabled) {  // the evaluation pass accumulates into counts: start it at zero
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(long long) * 2 * (size_t)g.n_layouts, s);
+    if (e != cudaSuccess) return cuda_fail(e, "counts reset");
+  }
   {
     TimedLaunch t(ctx, K_RECOVER, s);
     ctx->call_launches += recover_tail_available() ? 2 : 1;  // + the cluster tail of the last levels
@@ -376,6 +406,7 @@ int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, i
   int rc = phase_prepare(ctx, s, g, k, flags, colors, counts);
   if (rc == MPLD_OK) rc = phase_search(ctx, s, w_stitch, max_steps, 0, 1, colors);
   if (rc == MPLD_OK) rc = phase_finish(ctx, s, alpha, colors, counts, cost, stats);
+  if (rc == MPLD_OK) rc = mark_last(ctx, s);
   return rc;
 }
 
@@ -533,6 +564,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_last, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     mpld_context_destroy(ctx);
     return cuda_fail(e, "cudaStreamCreate");
@@ -561,6 +593,7 @@ void mpld_context_destroy(mpld_context* ctx) {
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_last) cudaEventDestroy(ctx->ev_last);
   for (AsyncSlot& a : ctx->slot) {
     for (void* p : {(void*)a.lo, (void*)a.ce_rp, (void*)a.ce_col, (void*)a.se_rp, (void*)a.se_col, (void*)a.se_pairs, (void*)a.colors,
                     (void*)a.counts, (void*)a.cost, (void*)a.stats})
@@ -592,6 +625,8 @@ int mpld_decompose_device(mpld_context* ctx, void* stream, int32_t n_layouts, co
   rc = ensure_workspace(ctx, n, n_layouts);
   if (rc != MPLD_OK) return rc;
   GraphView g{n, n_layouts, d_layout_offsets, d_ce_rowptr, d_ce_col, d_se_rowptr, d_se_col};
+  rc = order_after_last(ctx, (cudaStream_t)stream);
+  if (rc != MPLD_OK) return rc;
   return run_pipeline(ctx, (cudaStream_t)stream, g, k, w_stitch, alpha, (long long)max_steps, flags, d_colors,
                       (long long*)d_counts, d_cost, (long long*)d_stats);
 }
@@ -611,7 +646,10 @@ int mpld_prepare_device(mpld_context* ctx, void* stream, int32_t n_layouts, cons
   rc = ensure_workspace(ctx, n, n_layouts);
   if (rc != MPLD_OK) return rc;
   GraphView g{n, n_layouts, d_layout_offsets, d_ce_rowptr, d_ce_col, d_se_rowptr, d_se_col};
-  return phase_prepare(ctx, (cudaStream_t)stream, g, k, flags, d_colors, (long long*)d_counts);
+  rc = order_after_last(ctx, (cudaStream_t)stream);
+  if (rc == MPLD_OK) rc = phase_prepare(ctx, (cudaStream_t)stream, g, k, flags, d_colors, (long long*)d_counts);
+  if (rc == MPLD_OK) rc = mark_last(ctx, (cudaStream_t)stream);
+  return rc;
 }
 
 int mpld_search_device(mpld_context* ctx, void* stream, double alpha, int64_t max_steps, int32_t shard_index,
@@ -625,7 +663,11 @@ int mpld_search_device(mpld_context* ctx, void* stream, double alpha, int64_t ma
   int rc = check_scalars(ctx->g.n, ctx->k, alpha, &w_stitch);
   if (rc != MPLD_OK) return rc;
   cudaSetDevice(ctx->device);
-  return phase_search(ctx, (cudaStream_t)stream, w_stitch, (long long)max_steps, shard_index, shard_count, d_colors);
+  rc = order_after_last(ctx, (cudaStream_t)stream);
+  if (rc == MPLD_OK)
+    rc = phase_search(ctx, (cudaStream_t)stream, w_stitch, (long long)max_steps, shard_index, shard_count, d_colors);
+  if (rc == MPLD_OK) rc = mark_last(ctx, (cudaStream_t)stream);
+  return rc;
 }
 
 int mpld_finish_device(mpld_context* ctx, void* stream, double alpha, int32_t* d_colors, int64_t* d_counts,
@@ -637,8 +679,38 @@ int mpld_finish_device(mpld_context* ctx, void* stream, double alpha, int32_t* d
   int rc = check_scalars(ctx->g.n, ctx->k, alpha, &w_stitch);
   if (rc != MPLD_OK) return rc;
   cudaSetDevice(ctx->device);
-  return phase_finish(ctx, (cudaStream_t)stream, alpha, d_colors, (long long*)d_counts, d_cost,
-                      (long long*)d_stats);
+  rc = order_after_last(ctx, (cudaStream_t)stream);
+  if (rc == MPLD_OK)
+    rc = phase_finish(ctx, (cudaStream_t)stream, alpha, d_colors, (long long*)d_counts, d_cost, (long long*)d_stats);
+  if (rc == MPLD_OK) rc = mark_last(ctx, (cudaStream_t)stream);
+  return rc;
+}
+
+int mpld_shard_export(mpld_context* ctx, void* stream, const int32_t* d_colors, int32_t* d_pairs, int64_t* d_count) {
+  if (!ctx || !d_colors || !d_pairs || !d_count) return fail(MPLD_ERR_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (!ctx->prepared) return fail(MPLD_ERR_ARG, "mpld_prepare_device must be called first");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = order_after_last(ctx, s);
+  if (rc != MPLD_OK) return rc;
+  const cudaError_t e = launch_shard_export(ctx->g.n, d_colors, d_pairs, (unsigned long long*)d_count, s,
+                                            ctx->blocks_stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mpld_shard_export");
+  return mark_last(ctx, s);
+}
+
+int mpld_shard_import(mpld_context* ctx, void* stream, const int32_t* d_pairs, int64_t n_pairs, int32_t* d_colors) {
+  if (!ctx || !d_colors || (n_pairs > 0 && !d_pairs) || n_pairs < 0) return fail(MPLD_ERR_ARG, "bad argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (!ctx->prepared) return fail(MPLD_ERR_ARG, "mpld_prepare_device must be called first");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = order_after_last(ctx, s);
+  if (rc != MPLD_OK) return rc;
+  const cudaError_t e = launch_shard_import((long long)n_pairs, d_pairs, ctx->g.n, d_colors, s, ctx->blocks_stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mpld_shard_import");
+  return mark_last(ctx, s);
 }
 
 int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32_t n, const int32_t* ce_rowptr,
@@ -685,6 +757,8 @@ int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32
       return fail(MPLD_ERR_NOMEM, "staging allocation failed");
   }
   cudaStream_t s = ctx->stream;
+  rc = order_after_last(ctx, s);
+  if (rc != MPLD_OK) return rc;
   cudaError_t e;
   e = cudaMemcpyAsync(ctx->h_lo, layout_offsets, sizeof(int) * (n_layouts + 1), cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
@@ -759,7 +833,7 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
   }
   const int64_t t = ctx->next_ticket;
   AsyncSlot& a = ctx->slot[t % kAsyncSlots];
-  slot_finish(a);  // the slot's previous submit (t - 2) is complete and post-processed before reuse
+  slot_finish(a);  // the slot's previous submit (t - 3) is complete and post-processed before reuse
   if (n > ctx->cap_n) cudaStreamSynchronize(ctx->stream);  // the workspace grows: the other slot's compute must end
   rc = ensure_workspace(ctx, n, n_layouts);
   if (rc == MPLD_OK) rc = slot_reserve(a, n, m_ce, m_se, n_layouts);
@@ -780,6 +854,8 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
   if (e == cudaSuccess) e = cudaEventRecord(a.ev_h2d, up);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, a.ev_h2d, 0);
   if (e != cudaSuccess) return cuda_fail(e, "async H2D copy");
+  rc = order_after_last(ctx, ks);
+  if (rc != MPLD_OK) return rc;
   if (pairs) {  // the SE CSR on the device (scratch: the workspace's deg / q0 / bsum, rewritten later)
     e = launch_se_from_pairs(n, (int)n_pairs, a.se_pairs, a.se_rp, a.se_col, ctx->deg, ctx->q0, (int*)ctx->bsum, ks);
     if (e != cudaSuccess) return cuda_fail(e, "stitch CSR build");

@@ -114,11 +114,13 @@ struct GraphView {
 constexpr int kScanTile = 8192;  // elements per block of the partition scan (1024 threads x 8)
 
 // Estimated search cost of a component of n vertices for the cost-balanced
-// shard partition (north_star: size x k^n), capped at 2^40.
+// shard partition (north_star: size x k^n), capped at 2^32 so that the prefix
+// sum over any n < 2^31 vertices stays below 2^63 (no wrap-around).
+constexpr unsigned long long kEstimateCap = 1ull << 32;
 __host__ __device__ __forceinline__ unsigned long long partition_estimate(int n, int k) {
   unsigned long long e = (unsigned long long)n;
-  for (int i = 0; i < n && e < (1ull << 40); ++i) e *= (unsigned long long)k;
-  return e < (1ull << 40) ? e : (1ull << 40);
+  for (int i = 0; i < n && e < kEstimateCap; ++i) e *= (unsigned long long)k;
+  return e < kEstimateCap ? e : kEstimateCap;
 }
 
 // Exact mode, spilled heavy searches (kernel_search.cu): a warp whose search
@@ -265,6 +267,11 @@ cudaError_t configure_recover_tail();
 cudaError_t launch_evaluate(const GraphView& g, Workspace ws, const int* colors, double alpha,
                             long long* counts, double* cost, long long* stats, int launches,
                             cudaStream_t s, int blocks);
+
+// sharded runs: compact (vertex, colour) list of the colours a shard's search wrote, and its scatter
+cudaError_t launch_shard_export(int n, const int* colors, int* pairs, unsigned long long* count, cudaStream_t s,
+                                int blocks);
+cudaError_t launch_shard_import(long long m, const int* pairs, int n, int* colors, cudaStream_t s, int blocks);
 
 // occupancy helpers for the cooperative (persistent) kernels
 int coop_blocks_simplify(int threads, int num_sms);

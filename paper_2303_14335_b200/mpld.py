@@ -5,7 +5,10 @@ module never computes any part of the result.  There is no CPU fallback: if the
 library is missing or no CUDA device is present the calls raise.
 
 Array arguments may be numpy arrays / torch CPU tensors (host entry points) or
-torch CUDA tensors (device entry points); they must be contiguous int32.
+torch CUDA tensors (device entry points).  Graph arrays and colours are int32,
+counts and stats int64, costs float64 (include/mpld.h); torch tensors and
+output buffers of another element type or not contiguous are rejected
+(TypeError / ValueError), numpy inputs are converted.
 """
 from __future__ import annotations
 
@@ -32,7 +35,8 @@ EXPORTS = ["mpld_last_error", "mpld_version", "mpld_decompose", "mpld_decompose_
            "mpld_context_destroy", "mpld_decompose_device", "mpld_context_set_timing",
            "mpld_context_reset_timing", "mpld_kernel_count", "mpld_kernel_name", "mpld_context_kernel_time",
            "mpld_context_debug", "mpld_prepare_device", "mpld_search_device", "mpld_finish_device",
-           "mpld_decompose_batch_async", "mpld_decompose_batch_pairs_async", "mpld_wait"]
+           "mpld_decompose_batch_async", "mpld_decompose_batch_pairs_async", "mpld_wait",
+           "mpld_shard_export", "mpld_shard_import"]
 
 
 class MPLDError(RuntimeError):
@@ -86,6 +90,8 @@ def lib():
                                                    _vp, ctypes.c_int32, ctypes.c_double, ctypes.c_int64,
                                                    ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _i64p]
     L.mpld_wait.argtypes = [_vp, ctypes.c_int64]
+    L.mpld_shard_export.argtypes = [_vp, _vp, _vp, _vp, _vp]
+    L.mpld_shard_import.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp]
     _lib = L
     return L
 
@@ -95,35 +101,57 @@ def _check(rc: int):
         raise MPLDError(rc, lib().mpld_last_error().decode())
 
 
-def _host_ptr(x, dtype=np.int32):
-    """Address of a host buffer (numpy array or torch CPU tensor) plus a keep-alive."""
+_TORCH_DTYPE = {np.dtype(np.int32): "torch.int32", np.dtype(np.int64): "torch.int64",
+                np.dtype(np.float64): "torch.float64"}
+
+
+def _check_tensor(t, dtype, what):
+    """A torch tensor argument must have the element type the C ABI reads and be contiguous."""
+    want = _TORCH_DTYPE[np.dtype(dtype)]
+    if str(t.dtype) != want:
+        raise TypeError(f"{what}: expected {want}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: tensor must be contiguous")
+
+
+def _host_ptr(x, dtype=np.int32, what="host array"):
+    """Address of a host input buffer (numpy array or torch CPU tensor) plus a
+    keep-alive.  numpy inputs are converted to `dtype`; torch tensors must
+    already have it (no silent reinterpretation of e.g. int64 indices)."""
     if hasattr(x, "data_ptr"):
         if x.is_cuda:
-            raise ValueError("host entry point given a CUDA tensor")
+            raise ValueError(f"{what}: host entry point given a CUDA tensor")
+        _check_tensor(x, dtype, what)
         return x.data_ptr(), x
     a = np.ascontiguousarray(x, dtype=dtype)
     return a.ctypes.data, a
 
 
-def _out_ptr(x):
-    """Address of a host output buffer (written in place: must be contiguous)."""
+def _out_ptr(x, dtype, what="host output"):
+    """Address of a host output buffer (written in place: must be contiguous and
+    of exactly the element type the C ABI writes)."""
     if hasattr(x, "data_ptr"):
-        if x.is_cuda or not x.is_contiguous():
-            raise ValueError("host outputs must be contiguous CPU tensors / arrays")
+        if x.is_cuda:
+            raise ValueError(f"{what}: host outputs must be CPU tensors / arrays")
+        _check_tensor(x, dtype, what)
         return x.data_ptr()
-    if not x.flags["C_CONTIGUOUS"]:
-        raise ValueError("host outputs must be contiguous CPU tensors / arrays")
+    if not isinstance(x, np.ndarray) or x.dtype != np.dtype(dtype) or not x.flags["C_CONTIGUOUS"]:
+        raise TypeError(f"{what}: host outputs must be contiguous {np.dtype(dtype)} arrays")
     return x.ctypes.data
 
 
-def _dev_ptr(t):
+def _dev_ptr(t, dtype=np.int32, what="device tensor"):
     if t is None:
         return None
     if not (hasattr(t, "is_cuda") and t.is_cuda):
-        raise ValueError("device entry point needs CUDA tensors")
-    if not t.is_contiguous():
-        raise ValueError("tensors must be contiguous")
+        raise ValueError(f"{what}: device entry point needs CUDA tensors")
+    _check_tensor(t, dtype, what)
     return t.data_ptr()
+
+
+# element types of the result buffers (include/mpld.h)
+_OUT_DTYPES = {"colors": np.int32, "n_conflicts": np.int64, "n_stitches": np.int64, "cost": np.float64,
+               "stats": np.int64}
 
 
 def version() -> str:
@@ -149,7 +177,7 @@ def mpld_decompose_batch(layout_offsets, n, ce_rowptr, ce_col, se_rowptr, se_col
     lo_p, lo = _host_ptr(layout_offsets)
     n_layouts = int(len(lo) - 1) if not hasattr(lo, "numel") else int(lo.numel() - 1)
     colors = out_colors if out_colors is not None else np.empty(max(int(n), 0), dtype=np.int32)
-    col_p, _ = _host_ptr(colors)
+    col_p = _out_ptr(colors, np.int32, "out_colors")
     nc = np.zeros(n_layouts, dtype=np.int64)
     ns = np.zeros(n_layouts, dtype=np.int64)
     cost = np.zeros(n_layouts, dtype=np.float64)
@@ -206,7 +234,7 @@ class Context:
                    "cost": np.zeros(n_layouts, dtype=np.float64),
                    "stats": np.zeros(MPLD_STAT_LEN, dtype=np.int64)}
         keep = [lo] + [_host_ptr(a) for a in (ce_rowptr, ce_col, se_rowptr, se_col)]
-        ptr = {key: _out_ptr(v) for key, v in out.items()}
+        ptr = {key: _out_ptr(v, _OUT_DTYPES[key], key) for key, v in out.items()}
         t = ctypes.c_int64()
         _check(L.mpld_decompose_batch_async(self._h, n_layouts, lo_p, int(n), *[p for p, _ in keep[1:]], int(k),
                                             float(alpha), int(max_steps), int(flags), ptr["colors"],
@@ -234,7 +262,7 @@ class Context:
         sp = _host_ptr(stitch_pairs)
         m = int(sp[1].numel() if hasattr(sp[1], "numel") else np.asarray(sp[1]).size) // 2
         keep = [lo] + [_host_ptr(a) for a in (ce_rowptr, ce_col)] + [sp]
-        ptr = {key: _out_ptr(v) for key, v in out.items()}
+        ptr = {key: _out_ptr(v, _OUT_DTYPES[key], key) for key, v in out.items()}
         t = ctypes.c_int64()
         _check(L.mpld_decompose_batch_pairs_async(self._h, n_layouts, lo_p, int(n), keep[1][0], keep[2][0], m, sp[0],
                                                   int(k), float(alpha), int(max_steps), int(flags), ptr["colors"],
@@ -266,7 +294,8 @@ class Context:
         _check(lib().mpld_decompose_device(self._h, _vp(sh), n_layouts, _dev_ptr(layout_offsets), int(n),
                                            _dev_ptr(ce_rowptr), _dev_ptr(ce_col), _dev_ptr(se_rowptr),
                                            _dev_ptr(se_col), int(k), float(alpha), int(max_steps), int(flags),
-                                           _dev_ptr(colors), _dev_ptr(counts), _dev_ptr(cost), _dev_ptr(stats)))
+                                           _dev_ptr(colors), _dev_ptr(counts, np.int64, "counts"),
+                                           _dev_ptr(cost, np.float64, "cost"), _dev_ptr(stats, np.int64, "stats")))
 
     # ---- phase-split calls for a batch sharded over processes (include/mpld.h) ----
     @staticmethod
@@ -282,17 +311,31 @@ class Context:
         _check(lib().mpld_prepare_device(self._h, self._stream(stream, colors), int(layout_offsets.numel() - 1),
                                          _dev_ptr(layout_offsets), int(n), _dev_ptr(ce_rowptr), _dev_ptr(ce_col),
                                          _dev_ptr(se_rowptr), _dev_ptr(se_col), int(k), int(flags),
-                                         _dev_ptr(colors), _dev_ptr(counts)))
+                                         _dev_ptr(colors), _dev_ptr(counts, np.int64, "counts")))
 
     def search_device(self, alpha, max_steps, shard_index, shard_count, colors, stream=None):
         """Phase 2: search the components of this shard, colours of the others stay -1."""
         _check(lib().mpld_search_device(self._h, self._stream(stream, colors), float(alpha), int(max_steps),
                                         int(shard_index), int(shard_count), _dev_ptr(colors)))
 
+    def shard_export(self, colors, pairs, count, stream=None):
+        """Phase 3 (compact): the (vertex, colour) pairs of this shard's search into
+        pairs (int32 [>= 2n]), their number into count (int64 [1]), on the device."""
+        if pairs.numel() < 2 * int(colors.numel()):
+            raise ValueError("pairs must hold 2 * n int32")
+        _check(lib().mpld_shard_export(self._h, self._stream(stream, colors), _dev_ptr(colors), _dev_ptr(pairs),
+                                       _dev_ptr(count, np.int64, "count")))
+
+    def shard_import(self, pairs, colors, stream=None):
+        """Phase 3 (compact): scatter (vertex, colour) pairs (int32, flat; vertex < 0 = padding) into colors."""
+        _check(lib().mpld_shard_import(self._h, self._stream(stream, colors), _dev_ptr(pairs),
+                                       int(pairs.numel() // 2), _dev_ptr(colors)))
+
     def finish_device(self, alpha, colors, counts, cost, stats=None, stream=None):
         """Phase 3: recovery and Eq. (1) (after the colours of all shards are combined)."""
         _check(lib().mpld_finish_device(self._h, self._stream(stream, colors), float(alpha), _dev_ptr(colors),
-                                        _dev_ptr(counts), _dev_ptr(cost), _dev_ptr(stats)))
+                                        _dev_ptr(counts, np.int64, "counts"), _dev_ptr(cost, np.float64, "cost"),
+                                        _dev_ptr(stats, np.int64, "stats")))
 
     def set_timing(self, enable: bool):
         _check(lib().mpld_context_set_timing(self._h, 1 if enable else 0))

@@ -12,6 +12,11 @@ Recipe (restated in DESIGN.md §3 "Input recipe"):
     - *clusters* (dense regions: contact arrays, cell rows) — s points uniform in
       a square of side sqrt(s/density), a CE edge whenever two points are closer
       than 1 (the spacing).  Only these survive the low-degree simplification.
+      configs[2] (QPLD, k = 4) draws 3/4 of its clusters as *lattice clusters*
+      instead: track-aligned features on a jittered square lattice of pitch
+      0.68 (jitter +-0.15), near-planar graphs whose k = 4 cores reach ~40
+      vertices; its random clusters use density 1.0 (at 1.2, about one cluster
+      in 500 has a sequential search of > 10^8 nodes at k = 4).
       Stitch candidates (Fig. 1(c)): a cluster vertex of conflict degree >= k is,
       with probability `stitch_prob`, split into two segments joined by an SE
       edge; neighbours left of its x-coordinate stay on segment 0, the rest move
@@ -43,17 +48,24 @@ TABLE1 = {
 ISCAS85 = ["c432", "c499", "c880", "c1355", "c1908", "c2670", "c3540", "c5315", "c6288", "c7552"]
 
 
-def _cluster(rng, s, k, density, stitch_prob, comp_max):
-    """One dense cluster: returns (n_vertices, ce_edges, se_edges) in local ids."""
-    side = np.sqrt(s / density)
-    pts = rng.random((s, 2)) * side
+def _points_graph(pts):
+    """CE adjacency of features closer than the colouring spacing 1 (unit disk)."""
+    s = len(pts)
     d2 = ((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)
     iu, ju = np.nonzero(np.triu(d2 < 1.0, 1))
     adj = [set() for _ in range(s)]
     for a, b in zip(iu.tolist(), ju.tolist()):
         adj[a].add(b)
         adj[b].add(a)
-    xs = pts[:, 0].tolist()
+    return adj
+
+
+def _split_stitches(rng, adj, xs, k, stitch_prob, comp_max):
+    """Stitch candidates (Fig. 1(c)): a vertex of conflict degree >= k is, with
+    probability stitch_prob, split into two segments joined by an SE edge;
+    neighbours left of its x-coordinate stay on segment 0, the rest move to
+    segment 1 (no split if either side would be empty, none past comp_max)."""
+    s = len(adj)
     se = []
     n = s
     if stitch_prob > 0:
@@ -81,11 +93,37 @@ def _cluster(rng, s, k, density, stitch_prob, comp_max):
     return n, ce, se
 
 
+def _cluster(rng, s, k, density, stitch_prob, comp_max):
+    """One dense random cluster: s points uniform in a square of side
+    sqrt(s/density); returns (n_vertices, ce_edges, se_edges) in local ids."""
+    side = np.sqrt(s / density)
+    pts = rng.random((s, 2)) * side
+    adj = _points_graph(pts)
+    return _split_stitches(rng, adj, pts[:, 0].tolist(), k, stitch_prob, comp_max)
+
+
+def _lattice_cluster(rng, s, k, pitch, jitter, stitch_prob, comp_max):
+    """One track-aligned cluster (a cell row / contact array on routing tracks):
+    s features on a jittered square lattice of the given pitch (in units of the
+    colouring spacing), row by row, ceil(sqrt(1.5 s)) per row, each coordinate
+    offset uniformly in [-jitter, jitter].  At pitch 0.7 the orthogonal
+    neighbours always conflict and about half the diagonals do: a near-planar
+    graph of degree ~6 whose k = 4 core keeps most of the cluster."""
+    cols = int(np.ceil(np.sqrt(1.5 * s)))
+    pts = np.array([((i % cols) * pitch, (i // cols) * pitch) for i in range(s)], dtype=np.float64)
+    pts += rng.uniform(-jitter, jitter, size=(s, 2))
+    adj = _points_graph(pts)
+    return _split_stitches(rng, adj, pts[:, 0].tolist(), k, stitch_prob, comp_max)
+
+
 def make_layout(n_target: int, e_target: int, k: int = 3, stitch_prob: float = 0.0,
                 comp_max: int = 8, comp_min: int = 4, cluster_frac: float = 0.1,
                 density: float = 1.3, ladder_frac: float = 0.02, seed: int = 0,
-                name: str = "layout") -> DecompGraph:
-    """One synthetic layout with exactly n_target vertices and about e_target edges."""
+                name: str = "layout", lattice_frac: float = 0.0, pitch: float = 0.7,
+                jitter: float = 0.15) -> DecompGraph:
+    """One synthetic layout with exactly n_target vertices and about e_target edges.
+    A fraction lattice_frac of the clusters are track-aligned lattice clusters
+    (_lattice_cluster), the rest random unit-disk clusters (_cluster)."""
     rng = np.random.default_rng(seed)
     pieces = []  # (size, ce, se, kind)
     nv = 0
@@ -93,7 +131,10 @@ def make_layout(n_target: int, e_target: int, k: int = 3, stitch_prob: float = 0
     while nv < n_cluster:
         s = int(rng.integers(comp_min, comp_max + 1))
         s = min(s, comp_max)
-        sz, ce, se = _cluster(rng, s, k, density, stitch_prob, comp_max)
+        if lattice_frac > 0 and rng.random() < lattice_frac:
+            sz, ce, se = _lattice_cluster(rng, s, k, pitch, jitter, stitch_prob, comp_max)
+        else:
+            sz, ce, se = _cluster(rng, s, k, density, stitch_prob, comp_max)
         if nv + sz > n_target:
             break
         pieces.append((sz, ce, se, "cluster"))
@@ -217,8 +258,9 @@ def config_graphs(config: int, seed: int = 0, scale: float = 1.0):
     if config == 2:
         nv, ne = TABLE1["s38584"]
         nv, ne = int(nv * scale), int(ne * scale)
-        return [make_layout(nv, ne, k=4, stitch_prob=0.2, comp_max=48, comp_min=24,
-                            cluster_frac=0.08, density=1.2, seed=seed, name="s38584")], 4, 0.1
+        return [make_layout(nv, ne, k=4, stitch_prob=0.2, comp_max=48, comp_min=24, cluster_frac=0.1,
+                            density=1.0, lattice_frac=0.75, pitch=0.68, jitter=0.15, seed=seed,
+                            name="s38584")], 4, 0.1
     if config == 3:
         nv = int(1_000_000 * scale)
         return [make_layout(nv, int(nv * 1.17), k=3, stitch_prob=0.5, comp_max=16,

@@ -63,3 +63,16 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_host_binding_rejects_wrong_element_types():
+    """Host entry points: torch tensors of another element type and output
+    arrays of another element type are rejected before the C ABI is called."""
+    import torch
+    z = np.zeros(4, np.int32)
+    with pytest.raises(TypeError):
+        mp.mpld_decompose_batch(np.array([0, 3], np.int32), 3, torch.zeros(4, dtype=torch.int64),
+                                np.zeros(0, np.int32), z, np.zeros(0, np.int32), 3, 0.1)
+    with pytest.raises(TypeError):
+        mp.mpld_decompose_batch(np.array([0, 3], np.int32), 3, z, np.zeros(0, np.int32), z, np.zeros(0, np.int32),
+                                3, 0.1, out_colors=np.zeros(3, np.int64))

@@ -41,6 +41,45 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
+def _worker_compact(rank, world, port, out):
+    """bench.exchange_compact on CPU tensors: each rank owns a different part
+    of one colouring (different list lengths); the gathered lists, applied to
+    an all -1 array the way mpld_shard_import does, give the whole colouring."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    import bench
+    n = 1000
+    rng = np.random.default_rng(5)
+    full = rng.integers(0, 4, n).astype(np.int32)
+    owner = rng.choice(world + 1, n, p=[0.5, 0.2, 0.3])  # owner == world: a hidden vertex nobody searched
+    mine = np.nonzero(owner == rank)[0]
+    pairs = np.full(2 * n, 12345, dtype=np.int32)  # capacity 2n, garbage past the list (the export buffer)
+    pairs[0:2 * mine.size:2] = mine
+    pairs[1:2 * mine.size:2] = full[mine]
+    got = bench.exchange_compact(torch.from_numpy(pairs), torch.tensor([mine.size], dtype=torch.int64), world)
+    colors = np.full(n, -1, dtype=np.int32)
+    g = got.numpy().reshape(-1, 2)
+    for v, c in g:  # mpld_shard_import's rule
+        if 0 <= v < n:
+            colors[v] = c
+    want = np.where(owner < world, full, -1)
+    out.put((rank, bool(np.array_equal(colors, want)), int(g.shape[0]), int((g[:, 0] < 0).sum())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_compact_colour_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    mp.start_processes(_worker_compact, args=(2, port, q), nprocs=2, join=True, start_method="spawn")
+    res = sorted(q.get(timeout=60) for _ in range(2))
+    assert all(ok for _, ok, _, _ in res)
+    assert res[0][2] == res[1][2] and res[0][3] > 0  # equal gathered lengths; the shorter list was padded
+
+
 def test_gloo_world2_partition_and_aggregation():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -3,6 +3,7 @@ element: colours, conflict and stitch counts and cost are compared bit-exactly
 (integer / index results; the cost is the same IEEE expression on both sides)."""
 from __future__ import annotations
 
+import functools
 import random
 
 import numpy as np
@@ -301,17 +302,17 @@ def test_sharded_phases_equal_oracle(shards):
     owned = [(p >= 0) for p in parts]
     assert int(sum(o.int() for o in owned).max()) <= 1  # every kept vertex searched by exactly one shard
     # the cost-balanced partition (include/mpld.h phase 2), recomputed from the
-    # oracle's components: estimate n * k^n capped at 2^40, inclusive prefix in
+    # oracle's components: estimate n * k^n capped at 2^32, inclusive prefix in
     # root order, shard of the interval's start
     ref_comps = sorted(oracle.decompose(b, k, alpha, max_steps=0)["components"], key=lambda c: c["root"])
 
     def estimate(n):
         e = n
         for _ in range(n):
-            if e >= 1 << 40:
+            if e >= 1 << 32:
                 break
             e *= k
-        return min(e, 1 << 40)
+        return min(e, 1 << 32)
 
     ests = [estimate(c["size"]) for c in ref_comps]
     total, acc = float(sum(ests)), 0
@@ -322,6 +323,25 @@ def test_sharded_phases_equal_oracle(shards):
         got = [s for s in range(shards) if host_owned[s][c["root"]]]
         assert got == [want], (c, got, want)
     combined = torch.stack(parts).amax(0).contiguous()
+    # the compact exchange (mpld_shard_export / mpld_shard_import): each shard's
+    # (vertex, colour) list, concatenated with padding, scattered into the
+    # all -1 colours of phase 1 gives the same combined colouring
+    lists = []
+    for p in parts:
+        pr = torch.empty(2 * b.n, dtype=torch.int32, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        ctx.shard_export(p, pr, cnt)
+        torch.cuda.synchronize()
+        m = int(cnt.item())
+        assert m == int((p >= 0).sum())
+        exp = pr[: 2 * m].view(-1, 2).cpu().numpy()
+        assert sorted(exp[:, 0].tolist()) == torch.nonzero(p >= 0).flatten().cpu().tolist()
+        assert (p.cpu().numpy()[exp[:, 0]] == exp[:, 1]).all()
+        lists += [pr[: 2 * m], torch.full((6,), -1, dtype=torch.int32, device=dev)]
+    imported = colors.clone()
+    ctx.shard_import(torch.cat(lists), imported)
+    torch.cuda.synchronize()
+    assert torch.equal(imported, combined)
     ctx.finish_device(alpha, combined, counts, cost, stats)
     torch.cuda.synchronize()
     ref = oracle.decompose(b, k, alpha, max_steps=0)
@@ -332,34 +352,20 @@ def test_sharded_phases_equal_oracle(shards):
     ctx.close()
 
 
-def test_full_size_qpld_sampled():
-    """configs[2] at full s38584 size, in bench's launch configuration: global
-    invariants at full size, and the oracle recomputes a sample of components
-    one by one (their colours must match element by element)."""
-    graphs, k, alpha = synth.config_graphs(2)
-    g = graphs[0]
-    got = mp.decompose_graph(g, k, alpha, max_steps=BUDGET, flags=mp.MPLD_FLAG_VALIDATE)
-    colors = got["colors"]
-    assert ((colors >= 0) & (colors < k)).all()
-    ce, se = g.ce_edges(), g.se_edges()
-    assert int((colors[ce[:, 0]] == colors[ce[:, 1]]).sum()) == int(got["n_conflicts"][0])
-    assert int((colors[se[:, 0]] != colors[se[:, 1]]).sum()) == int(got["n_stitches"][0])
-    ce_adj, se_adj = g.ce_adj(), g.se_adj()
-    hround, rounds = oracle.simplify(g.n, ce_adj, se_adj, k)
-    assert got["stats"]["rounds"] == len(rounds)
-    comps = oracle.components(g.n, ce_adj, se_adj, hround)
-    assert got["stats"]["components"] == len(comps)
-    rng = random.Random(0)
-    sample = rng.sample(comps, min(60, len(comps))) + sorted(comps, key=len)[-5:]
-    w = oracle.alpha_units(alpha)
-    for order in sample:
-        r = oracle.solve_component(order, ce_adj, se_adj, k, w, BUDGET)
-        for v, c in r["global_colors"].items():
-            assert colors[v] == c
-    # recovery adds no conflict: every conflict lies inside a component
-    kept = np.array(hround) == -1
-    conf_edges = ce[colors[ce[:, 0]] == colors[ce[:, 1]]]
-    assert kept[conf_edges[:, 0]].all() and kept[conf_edges[:, 1]].all()
+def test_full_size_config2_exact_element_by_element():
+    """configs[2] at full s38584 size exactly as bench.py times it
+    (bench.workload_items(2, 0, 1): one QPLD layout, k = 4, components up to
+    ~40 vertices, exact mode, validation on): full element-by-element parity
+    with the oracle (~15 s of oracle): light lanes, the 32- and 64-bit heavy
+    searches and their work-queue spill all take part."""
+    import bench
+    it = bench.workload_items(2, 0, 1)[0]
+    assert it.max_steps == 0 and it.k == 4
+    got, ref = _assert_same(it.g, it.k, it.alpha, max_steps=it.max_steps)
+    sizes = [c["size"] for c in ref["components"]]
+    assert 36 <= max(sizes) <= 48 and sum(1 for n in sizes if n > 32) >= 5  # the shape configs[2] names
+    assert got["stats"]["max_component"] == max(sizes)
+    assert got["stats"]["truncated"] == 0
 
 
 def test_async_pipeline_matches_sync_calls():
@@ -547,26 +553,30 @@ def test_full_size_config3_element_by_element():
 
 
 @pytest.mark.parametrize("k", [3, 4])
-@pytest.mark.parametrize("size", [4, 8, 16, 32, 64])
+@pytest.mark.parametrize("size", [4, 8, 16, 24, 32, 48, 64])
 def test_full_size_stress_sweep(size, k):
-    """configs[4] at full size: 10^5 components of `size` vertices in one launch
-    (500 distinct components, each repeated in 200 layouts).  Every copy of a
-    component must get the same colours wherever it lands (light lanes, heavy
-    warps, work queue), the counts must be recomputable from the colours, and
-    the oracle recomputes a sample of the distinct components one by one."""
-    tmpl = synth.stress_components(size, 500, k, seed=7000 + 10 * size + k)
-    g = synth.concat([tmpl] * 200, name=f"stress{size}_k{k}_1e5")
-    budget = 0 if size <= 16 else 20000  # exact mode where the oracle can follow
+    """configs[4] at full size exactly as bench.py times it (bench.workload_items(4, 0, 1):
+    10^5 components of `size` vertices in one launch, 500 distinct components
+    repeated in 200 layouts; exact up to 16 vertices, the bench's budget above,
+    DESIGN.md R13).  Every copy of a component must get the same colours
+    wherever it lands (light lanes, heavy warps, work queue), the counts must be
+    recomputable from the colours, and the oracle recomputes a sample of the
+    distinct components one by one at the same budget."""
+    import bench
+    it = [i for i in bench.workload_items(4, 0, 1) if i.label == f"n{size}_k{k}"][0]
+    g, budget = it.g, it.max_steps
+    tmpl = bench.stress_template(size, k)
+    assert g.n == bench.STRESS_COPIES * tmpl.n and np.array_equal(g.ce_col[: tmpl.ce_col.size], tmpl.ce_col)
     got = mp.decompose_graph(g, k, 0.1, max_steps=budget, flags=mp.MPLD_FLAG_VALIDATE)
     colors = got["colors"]
     ce_adj, se_adj = tmpl.ce_adj(), tmpl.se_adj()
     hround, _ = oracle.simplify(tmpl.n, ce_adj, se_adj, k)
     comps = oracle.components(tmpl.n, ce_adj, se_adj, hround)
     # a component of <= k vertices has every degree < k: the simplification hides it whole
-    assert len(comps) == (500 if size > k else 0)
-    assert got["stats"]["components"] == 200 * len(comps)
+    assert len(comps) == (bench.STRESS_TEMPLATES if size > k else 0)
+    assert got["stats"]["components"] == bench.STRESS_COPIES * len(comps)
     assert ((colors >= 0) & (colors < k)).all()
-    per = colors.reshape(200, tmpl.n)
+    per = colors.reshape(bench.STRESS_COPIES, tmpl.n)
     assert (per == per[0]).all()
     ce = g.ce_edges()
     assert int((colors[ce[:, 0]] == colors[ce[:, 1]]).sum()) == int(got["n_conflicts"].sum())
@@ -575,13 +585,81 @@ def test_full_size_stress_sweep(size, k):
     assert np.allclose(got["cost"], got["n_conflicts"].astype(np.float64))
     if budget == 0:
         assert got["stats"]["truncated"] == 0
+    else:  # the budget is per component and deterministic: every copy truncates alike
+        assert got["stats"]["truncated"] % bench.STRESS_COPIES == 0
     w = oracle.alpha_units(0.1)
+    trunc = 0
     for order in random.Random(size * 10 + k).sample(comps, min(len(comps), 6 if size >= 32 else 20)):
         r = oracle.solve_component(order, ce_adj, se_adj, k, w, budget)
+        trunc += r["truncated"]
         for v, c in r["global_colors"].items():
             assert per[0, v] == c
     if not comps:  # everything recovered: the whole template equals the oracle's run
         assert np.array_equal(per[0], oracle.decompose(tmpl, k, 0.1, max_steps=0)["colors"])
+
+
+@functools.lru_cache(maxsize=None)
+def _solvable_stress_components(size, k):
+    """Up to 4 components of the configs[4] template whose exact search the
+    oracle finishes within 200,000 nodes, with the oracle's results."""
+    import bench
+    tmpl = bench.stress_template(size, k)
+    ce_adj, se_adj = tmpl.ce_adj(), tmpl.se_adj()
+    hround, _ = oracle.simplify(tmpl.n, ce_adj, se_adj, k)
+    comps = oracle.components(tmpl.n, ce_adj, se_adj, hround)
+    w = oracle.alpha_units(0.1)
+    solved = []
+    for order in comps[:40]:
+        r = oracle.solve_component(order, ce_adj, se_adj, k, w, 200_000)
+        if not r["truncated"]:
+            solved.append((order, r))
+        if len(solved) == 4:
+            break
+    return solved, ce_adj
+
+
+@pytest.mark.parametrize("spill", [None, "64"])
+@pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("size", [32, 48, 64])
+def test_exact_mode_large_stress_components(monkeypatch, size, k, spill):
+    """Exact mode (max_steps = 0) on 32-64-vertex components (the 64-bit light
+    lane, the 64-bit heavy search, its work queue and slots): the configs[4]
+    components whose exact search the oracle finishes within 200,000 nodes,
+    each repeated, must get the oracle's first optimal leaf, untruncated."""
+    if spill:
+        monkeypatch.setenv("MPLD_HEAVY_SPILL", spill)
+    solved, ce_adj = _solvable_stress_components(size, k)
+    assert len(solved) >= 2, "too few oracle-solvable components"
+    parts = []
+    for order, _ in solved:  # each solved component as its own layout (local ids in the template's order)
+        loc = {v: i for i, v in enumerate(sorted(order))}
+        es = {(min(loc[v], loc[u]), max(loc[v], loc[u])) for v in order for u in ce_adj[v] if u in loc}
+        parts.append(from_edges(len(order), sorted(es)))
+    b = synth.concat(parts * 16)
+    ctx = mp.Context(0, b.n, b.n_layouts)  # reads MPLD_HEAVY_SPILL
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    colors = torch.empty(b.n, dtype=torch.int32, device=dev)
+    counts = torch.empty(2 * b.n_layouts, dtype=torch.int64, device=dev)
+    cost = torch.empty(b.n_layouts, dtype=torch.float64, device=dev)
+    stats = torch.empty(len(mp.STAT_NAMES), dtype=torch.int64, device=dev)
+    ctx.decompose_device(T(b.layout_offsets), b.n, T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr), T(b.se_col),
+                         k, 0.1, 0, colors, counts, cost, stats, flags=mp.MPLD_FLAG_VALIDATE)
+    torch.cuda.synchronize()
+    st = dict(zip(mp.STAT_NAMES, stats.cpu().tolist()))
+    assert st["error"] == 0 and st["truncated"] == 0
+    got = colors.cpu().numpy()
+    c2 = counts.cpu().numpy().reshape(-1, 2)
+    offs = b.layout_offsets
+    for li in range(b.n_layouts):
+        order, r = solved[li % len(solved)]
+        loc = {v: i for i, v in enumerate(sorted(order))}
+        want = np.zeros(len(order), np.int32)
+        for v, c in r["global_colors"].items():
+            want[loc[v]] = c
+        assert np.array_equal(got[offs[li]:offs[li + 1]], want), li
+        assert int(c2[li, 0]) == r["n_conf"] and float(cost[li]) == r["n_conf"] + 0.1 * r["n_stitch"]
+    ctx.close()
 
 
 def test_host_staging_grows_with_layout_count():
@@ -653,4 +731,83 @@ def test_capacity_sequence_all_entry_points():
             assert np.array_equal(np.asarray(r["n_conflicts"], np.int64), want_c), (i, path)
             assert np.array_equal(np.asarray(r["n_stitches"], np.int64), want_s), (i, path)
             assert np.array_equal(np.asarray(r["cost"], np.float64), want_cost), (i, path)
+    ctx.close()
+
+
+def test_phases_on_different_streams_and_a_fresh_counts_buffer():
+    """A context's calls may be enqueued on different streams (each waits for
+    the previous call's last operation), and mpld_finish_device may be given a
+    counts buffer other than the one of mpld_prepare_device (it is reset and
+    recomputed): results equal the oracle's."""
+    graphs, k, alpha = synth.config_graphs(1)
+    b = synth.concat(graphs[:5])
+    b2 = synth.concat(graphs[5:])
+    ref = oracle.decompose(b, k, alpha, max_steps=0)
+    ref2 = oracle.decompose(b2, k, alpha, max_steps=0)
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    ctx = mp.Context(0, 1 << 10, 1)
+    sa, sb, sc, sd = (torch.cuda.Stream(dev) for _ in range(4))
+    graph = [T(b.layout_offsets), T(b.ce_rowptr), T(b.ce_col), T(b.se_rowptr), T(b.se_col)]
+    torch.cuda.synchronize()
+    colors = torch.empty(b.n, dtype=torch.int32, device=dev)
+    counts1 = torch.empty(2 * b.n_layouts, dtype=torch.int64, device=dev)
+    counts2 = torch.full((2 * b.n_layouts,), 987654321, dtype=torch.int64, device=dev)
+    cost = torch.empty(b.n_layouts, dtype=torch.float64, device=dev)
+    for one_shard_counts_buffer in (counts2, counts1):
+        if one_shard_counts_buffer is counts2:
+            counts2.fill_(987654321)
+            torch.cuda.synchronize()
+        ctx.prepare_device(graph[0], b.n, *graph[1:], k, colors, counts1, flags=mp.MPLD_FLAG_VALIDATE, stream=sa)
+        ctx.search_device(alpha, 0, 0, 1, colors, stream=sb)
+        ctx.finish_device(alpha, colors, one_shard_counts_buffer, cost, stream=sc)
+        sc.synchronize()
+        assert np.array_equal(colors.cpu().numpy(), ref["colors"])
+        c2 = one_shard_counts_buffer.cpu().numpy().reshape(-1, 2)
+        for li, (c, s_, cst) in enumerate(ref["per_layout"]):
+            assert (int(c2[li, 0]), int(c2[li, 1]), float(cost[li])) == (c, s_, cst)
+    # an asynchronous host submit (the context's own stream) followed at once by a
+    # device call of another batch on another stream: both results intact
+    t = ctx.submit(b.layout_offsets, b.n, b.ce_rowptr, b.ce_col, b.se_rowptr, b.se_col, k, alpha, 0,
+                   mp.MPLD_FLAG_VALIDATE)
+    g2 = [T(b2.layout_offsets), T(b2.ce_rowptr), T(b2.ce_col), T(b2.se_rowptr), T(b2.se_col)]
+    col2 = torch.empty(b2.n, dtype=torch.int32, device=dev)
+    cnt2 = torch.empty(2 * b2.n_layouts, dtype=torch.int64, device=dev)
+    cost2 = torch.empty(b2.n_layouts, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    ctx.decompose_device(g2[0], b2.n, *g2[1:], k, alpha, 0, col2, cnt2, cost2, flags=mp.MPLD_FLAG_VALIDATE,
+                         stream=sd)
+    r = ctx.wait(t)
+    sd.synchronize()
+    assert np.array_equal(r["colors"], ref["colors"])
+    assert np.array_equal(col2.cpu().numpy(), ref2["colors"])
+    assert np.array_equal(cost2.cpu().numpy(), np.array([p[2] for p in ref2["per_layout"]]))
+    ctx.close()
+
+
+def test_binding_rejects_wrong_element_types():
+    """The binding checks element types and contiguity (an int64 index tensor or
+    a float32 cost buffer would otherwise be reinterpreted by the C ABI)."""
+    g = synth.fixtures()["K4"]
+    dev = torch.device("cuda:0")
+    ctx = mp.Context(0, 16, 1)
+    lo = torch.tensor(g.layout_offsets, dtype=torch.int32, device=dev)
+    cr64 = torch.tensor(g.ce_rowptr, dtype=torch.int64, device=dev)
+    args = [torch.tensor(a, dtype=torch.int32, device=dev) for a in (g.ce_rowptr, g.ce_col, g.se_rowptr, g.se_col)]
+    colors = torch.empty(g.n, dtype=torch.int32, device=dev)
+    counts = torch.empty(2, dtype=torch.int64, device=dev)
+    cost = torch.empty(1, dtype=torch.float64, device=dev)
+    with pytest.raises(TypeError):
+        ctx.decompose_device(lo, g.n, cr64, *args[1:], 3, 0.1, 0, colors, counts, cost)
+    with pytest.raises(TypeError):
+        ctx.decompose_device(lo, g.n, *args, 3, 0.1, 0, colors, counts, cost.float())
+    with pytest.raises(TypeError):
+        mp.mpld_decompose_batch(g.layout_offsets, g.n, torch.tensor(g.ce_rowptr, dtype=torch.int64), g.ce_col,
+                                g.se_rowptr, g.se_col, 3, 0.1)
+    with pytest.raises(TypeError):
+        mp.mpld_decompose_batch(g.layout_offsets, g.n, g.ce_rowptr, g.ce_col, g.se_rowptr, g.se_col, 3, 0.1,
+                                out_colors=np.empty(g.n, dtype=np.int64))
+    ctx.decompose_device(lo, g.n, *args, 3, 0.1, 0, colors, counts, cost)
+    torch.cuda.synchronize()
+    assert int(counts[0]) == 1
     ctx.close()
