@@ -33,7 +33,7 @@ def validate(g) -> None:
     symmetric, rows strictly ascending, no self loops, ids in range, CE ∩ SE = ∅."""
     n = g.n
     for name, rp, col in (("CE", g.ce_rowptr, g.ce_col), ("SE", g.se_rowptr, g.se_col)):
-        if len(rp) != n + 1 or rp[0] != 0 or rp[-1] != len(col):
+        if len(rp) != n + 1 or rp[0] != 0 or rp[-1] != len(col) or np.any(np.diff(rp) < 0):
             raise ValueError(f"{name}: bad row pointer")
         adj = [col[rp[v]:rp[v + 1]].tolist() for v in range(n)]
         for v in range(n):

@@ -3,6 +3,9 @@
 * `eq1` evaluates PAPER.md Eq. (1) from a colouring with exact rationals.
 * `brute_force` enumerates all k^n colourings (the plain definition of the
   optimum of Eq. 1).
+* `bfs_components` lists the components of a graph in the column order of
+  DESIGN.md R5 with its own queue (collections.deque), for the pins that need
+  the order without trusting oracle.components.
 * `canonical_leaves` enumerates, WITHOUT any pruning, budget or dancing links,
   the leaves of the search tree DESIGN.md R4-R6 define (column rule of Alg. 1
   line 8, rows in index order), so the first minimum-cost leaf can be compared
@@ -10,6 +13,7 @@
 """
 from __future__ import annotations
 
+import collections
 import itertools
 import random
 from fractions import Fraction
@@ -76,3 +80,65 @@ def random_graph(rng: random.Random, n, p_ce, p_se=0.0):
             elif r < p_se + p_ce:
                 ce.append((u, v))
     return ce, se
+
+
+def bfs_components(n, ce, se):
+    """Components over CE ∪ SE, each in BFS order from its smallest vertex with
+    neighbours in ascending id (R5), listed by ascending root."""
+    nb = [set() for _ in range(n)]
+    for u, v in list(ce) + list(se):
+        nb[u].add(v)
+        nb[v].add(u)
+    seen = [False] * n
+    out = []
+    for r in range(n):
+        if seen[r]:
+            continue
+        seen[r] = True
+        q, order = collections.deque([r]), []
+        while q:
+            v = q.popleft()
+            order.append(v)
+            for u in sorted(nb[v]):
+                if not seen[u]:
+                    seen[u] = True
+                    q.append(u)
+        out.append(order)
+    return out
+
+
+def raw_graph(n, ce_rows, se_rows, layout_offsets=None):
+    """A DecompGraph from explicit rows (may violate the CSR invariants on purpose)."""
+    import numpy as np
+    from synth.graph import DecompGraph
+
+    def csr(rows):
+        rp = np.zeros(n + 1, dtype=np.int32)
+        rp[1:] = np.cumsum([len(r) for r in rows])
+        col = np.array([u for r in rows for u in r], dtype=np.int32)
+        return rp, col
+
+    crp, ccol = csr(ce_rows)
+    srp, scol = csr(se_rows)
+    g = DecompGraph(n, crp, ccol, srp, scol)
+    if layout_offsets is not None:
+        g.layout_offsets = np.array(layout_offsets, dtype=np.int32)
+    return g
+
+
+# valid reference: path 0-1-2-3 in CE, stitch 3-4; then one violation of the
+# CSR invariants of include/mpld.h per case (rows, symmetry, ids, CE ∩ SE)
+GOOD_CE = [[1], [0, 2], [1, 3], [2], []]
+GOOD_SE = [[], [], [], [4], [3]]
+BAD_GRAPHS = {
+    "asymmetric_ce": ([[1], [0, 2], [1, 3], [], []], GOOD_SE, None),
+    "asymmetric_se": (GOOD_CE, [[], [], [], [4], []], None),
+    "unsorted_row": ([[1], [2, 0], [1, 3], [2], []], GOOD_SE, None),
+    "duplicate_entry": ([[1, 1], [0, 0, 2], [1, 3], [2], []], GOOD_SE, None),
+    "self_loop": ([[1], [0, 2], [1, 2, 3], [2], []], GOOD_SE, None),
+    "id_out_of_range": ([[1, 5], [0, 2], [1, 3], [2], []], GOOD_SE, None),
+    "negative_id": ([[-1, 1], [0, 2], [1, 3], [2], []], GOOD_SE, None),
+    "ce_and_se_overlap": (GOOD_CE, [[], [], [3], [2, 4], [3]], None),
+    "layout_offsets_unsorted": (GOOD_CE, GOOD_SE, [0, 4, 2, 5]),
+    "layout_offsets_short": (GOOD_CE, GOOD_SE, [0, 4]),  # rejected by the host entry point (MPLD_ERR_ARG)
+}

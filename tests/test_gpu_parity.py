@@ -12,7 +12,7 @@ import pytest
 import oracle
 import synth
 from synth import from_edges
-from synth.graph import DecompGraph
+from tests._pins import BAD_GRAPHS, GOOD_CE, GOOD_SE, raw_graph
 
 mp = pytest.importorskip("paper_2303_14335_b200")
 torch = pytest.importorskip("torch")
@@ -186,36 +186,8 @@ def test_validation_rejects_bad_graphs():
     _assert_same(g, 3, 0.1)  # the context recovers after an error
 
 
-def _raw(n, ce_rows, se_rows, layout_offsets=None):
-    """A DecompGraph from explicit rows (may violate the CSR invariants on purpose)."""
-    def csr(rows):
-        rp = np.zeros(n + 1, dtype=np.int32)
-        rp[1:] = np.cumsum([len(r) for r in rows])
-        col = np.array([u for r in rows for u in r], dtype=np.int32)
-        return rp, col
-    crp, ccol = csr(ce_rows)
-    srp, scol = csr(se_rows)
-    g = DecompGraph(n, crp, ccol, srp, scol)
-    if layout_offsets is not None:
-        g.layout_offsets = np.array(layout_offsets, dtype=np.int32)
-    return g
-
-
-# valid reference: path 0-1-2-3 in CE, stitch 3-4; then one violation per case
-_GOOD_CE = [[1], [0, 2], [1, 3], [2], []]
-_GOOD_SE = [[], [], [], [4], [3]]
-_BAD_GRAPHS = {
-    "asymmetric_ce": ([[1], [0, 2], [1, 3], [], []], _GOOD_SE, None),
-    "asymmetric_se": (_GOOD_CE, [[], [], [], [4], []], None),
-    "unsorted_row": ([[1], [2, 0], [1, 3], [2], []], _GOOD_SE, None),
-    "duplicate_entry": ([[1, 1], [0, 0, 2], [1, 3], [2], []], _GOOD_SE, None),
-    "self_loop": ([[1], [0, 2], [1, 2, 3], [2], []], _GOOD_SE, None),
-    "id_out_of_range": ([[1, 5], [0, 2], [1, 3], [2], []], _GOOD_SE, None),
-    "negative_id": ([[-1, 1], [0, 2], [1, 3], [2], []], _GOOD_SE, None),
-    "ce_and_se_overlap": (_GOOD_CE, [[], [], [3], [2, 4], [3]], None),
-    "layout_offsets_unsorted": (_GOOD_CE, _GOOD_SE, [0, 4, 2, 5]),
-    "layout_offsets_short": (_GOOD_CE, _GOOD_SE, [0, 4]),  # rejected by the host entry point (MPLD_ERR_ARG)
-}
+_raw = raw_graph
+_GOOD_CE, _GOOD_SE, _BAD_GRAPHS = GOOD_CE, GOOD_SE, BAD_GRAPHS
 
 
 def test_validation_accepts_valid_graphs():
@@ -811,3 +783,23 @@ def test_binding_rejects_wrong_element_types():
     torch.cuda.synchronize()
     assert int(counts[0]) == 1
     ctx.close()
+
+
+def _budget_trace_rows():
+    import os
+    rows = []
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "k4_budget_trace.txt")):
+        if line.startswith("budget"):
+            _, b, steps, tr, cost, *col = line.split()
+            rows.append((int(b), int(steps), int(tr), int(cost), [int(c) for c in col]))
+    return rows
+
+
+@pytest.mark.parametrize("budget,steps,truncated,cost,colors", _budget_trace_rows())
+def test_k4_budget_hand_trace_through_the_c_abi(budget, steps, truncated, cost, colors):
+    """The hand-traced node counts of tests/golden/k4_budget_trace.txt (K4,
+    k = 3) at every budget: the GPU stops at exactly the traced node."""
+    got = mp.decompose_graph(synth.fixtures()["K4"], 3, 0.1, max_steps=budget, flags=mp.MPLD_FLAG_VALIDATE)
+    assert got["colors"].tolist() == colors
+    assert (got["stats"]["steps"], got["stats"]["truncated"]) == (steps, truncated)
+    assert int(got["n_conflicts"][0]) * 1000 == cost

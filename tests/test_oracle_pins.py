@@ -16,7 +16,8 @@ import pytest
 import oracle
 import synth
 from synth import from_edges
-from tests._pins import brute_force, eq1, first_optimal_leaf, canonical_leaves, random_graph
+from tests._pins import (BAD_GRAPHS, GOOD_CE, GOOD_SE, bfs_components, brute_force, canonical_leaves, eq1,
+                         first_optimal_leaf, random_graph, raw_graph)
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -127,10 +128,73 @@ def test_brute_force_alpha(alpha):
 
 # ---------------------------------------------------------------- canonical answer
 def _bfs_relabel(n, ce, se):
-    g = from_edges(n, ce, se)
-    hround = [-1] * n
-    comps = oracle.components(n, g.ce_adj(), g.se_adj(), hround)
-    return comps
+    """The R5 column order from the pins' own BFS (tests/_pins.py), not oracle.components."""
+    return bfs_components(n, ce, se)
+
+
+def _read_bfs_golden():
+    out, cur = [], None
+    for line in open(os.path.join(GOLDEN, "bfs_order.txt")):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        key, *rest = line.split()
+        if key == "graph":
+            cur = {"name": rest[0], "ce": [], "se": [], "hidden": [], "components": []}
+        elif key == "end":
+            out.append(cur)
+        elif key in ("ce", "se"):
+            cur[key] = [tuple(int(x) for x in e.split("-")) for e in rest]
+        elif key == "hidden":
+            cur["hidden"] = [int(x) for x in rest]
+        elif key == "component":
+            cur["components"].append([int(x) for x in rest])
+        else:
+            cur[key] = int(rest[0])
+    return out
+
+
+@pytest.mark.parametrize("gold", _read_bfs_golden(), ids=lambda g: g["name"])
+def test_components_bfs_order_golden(gold):
+    """oracle.components against a hand-derived BFS (tests/golden/bfs_order.txt):
+    a graph where CE-before-SE order, depth-first order and ascending id order
+    all differ from the R5 order."""
+    g = from_edges(gold["n"], gold["ce"], gold["se"])
+    hround = [0 if v in gold["hidden"] else -1 for v in range(gold["n"])]
+    assert oracle.components(gold["n"], g.ce_adj(), g.se_adj(), hround) == gold["components"]
+
+
+def test_components_match_independent_bfs():
+    """oracle.components equals the pins' own BFS (tests/_pins.py) on random graphs."""
+    rng = random.Random(31)
+    for trial in range(200):
+        n = rng.randint(1, 14)
+        ce, se = random_graph(rng, n, rng.choice([0.1, 0.25, 0.4]), rng.choice([0.0, 0.1]))
+        g = from_edges(n, ce, se)
+        assert oracle.components(n, g.ce_adj(), g.se_adj(), [-1] * n) == bfs_components(n, ce, se)
+
+
+def _read_budget_trace():
+    rows = []
+    for line in open(os.path.join(GOLDEN, "k4_budget_trace.txt")):
+        if line.startswith("budget"):
+            _, b, steps, tr, cost, *col = line.split()
+            rows.append((int(b), int(steps), bool(int(tr)), int(cost), tuple(int(c) for c in col)))
+    return rows
+
+
+@pytest.mark.parametrize("budget,steps,truncated,cost,colors", _read_budget_trace())
+def test_k4_budget_hand_trace(budget, steps, truncated, cost, colors):
+    """Node counts and truncated results at every budget against the hand trace
+    of tests/golden/k4_budget_trace.txt (K4, k = 3), through algorithm_x and
+    through the whole flow (K4 survives the k = 3 simplification whole)."""
+    K4 = [(i, j) for i in range(4) for j in range(i + 1, 4)]
+    r = oracle.algorithm_x(4, 3, K4, [[] for _ in range(4)], oracle.W_CONF, 100, max_steps=budget)
+    assert (r["steps"], r["truncated"], r["cost"], tuple(r["colors"])) == (steps, truncated, cost, colors)
+    d = oracle.decompose(synth.fixtures()["K4"], 3, 0.1, max_steps=budget)
+    c = d["components"][0]
+    assert (c["steps"], c["truncated"], c["cost_units"]) == (steps, truncated, cost)
+    assert tuple(int(x) for x in d["colors"]) == colors
 
 
 @pytest.mark.parametrize("k", [2, 3, 4])
@@ -191,10 +255,10 @@ def test_bound_is_a_lower_bound():
     import itertools
     from oracle.dlx import clique_partition
     rng = random.Random(21)
-    for trial in range(300):
+    for trial in range(400):
         n = rng.randint(2, 7)
-        k = rng.randint(2, 4)
-        ce, _ = random_graph(rng, n, rng.choice([0.5, 0.8]))
+        k = rng.choice([2, 3, 4, 4])
+        ce, _ = random_graph(rng, n, rng.choice([0.5, 0.8, 0.95]))
         adj = [set() for _ in range(n)]
         for u, v in ce:
             adj[u].add(v)
@@ -203,10 +267,18 @@ def test_bound_is_a_lower_bound():
         live = {v: {c for c in range(k) if all(colored.get(u) != c for u in adj[v])}
                 for v in range(n) if v not in colored}
         zero = sum(1 for v in live if not live[v])
-        deficit = 0
-        for Q in clique_partition(n, ce):
-            X = [v for v in Q if v in live and live[v]]
-            deficit += max(0, len(X) - len(set().union(*[live[v] for v in X])))
+        def deficit_over(cliques):
+            d = 0
+            for Q in cliques:
+                X = [v for v in Q if v in live and live[v]]
+                d += max(0, len(X) - len(set().union(*[live[v] for v in X])))
+            return d
+
+        # the partition the oracle uses (oracle/dlx.py: cliques of >= k vertices, k >= 4 only) and,
+        # as a stronger check of the argument, every greedy clique of >= 2 vertices
+        used = clique_partition(n, ce, minsize=k) if k >= 4 else []
+        deficit = deficit_over(used)
+        deficit2 = deficit_over(clique_partition(n, ce, minsize=2))
         free = [v for v in range(n) if v not in colored]
         best = None
         for assign in itertools.product(range(k), repeat=len(free)):
@@ -216,6 +288,7 @@ def test_bound_is_a_lower_bound():
             c = sum(1 for u, v in ce if col[u] == col[v] and (u in live or v in live))
             best = c if best is None else min(best, c)
         assert zero + deficit <= best, (n, k, ce, colored)
+        assert zero + deficit2 <= best, (n, k, ce, colored)
 
 
 # ---------------------------------------------------------------- Eq. (2) round trip
@@ -392,6 +465,34 @@ def test_alpha_units():
         oracle.alpha_units(0.0001)
     with pytest.raises(ValueError):
         oracle.alpha_units(-0.1)
+
+
+@pytest.mark.parametrize("case", sorted(c for c in BAD_GRAPHS if not c.startswith("layout_offsets")))
+def test_validate_rejects_each_invariant(case):
+    """oracle.validate against one violation of each CSR invariant of §2.1's
+    "E = {CE ∪ SE}" as include/mpld.h states it (the same table the GPU
+    validation tests use)."""
+    ce, se, _ = BAD_GRAPHS[case]
+    with pytest.raises(ValueError):
+        oracle.validate(raw_graph(5, ce, se))
+
+
+@pytest.mark.parametrize("case", ["rowptr_start", "rowptr_end", "rowptr_length", "rowptr_decreasing"])
+def test_validate_rejects_bad_row_pointers(case):
+    g = raw_graph(5, GOOD_CE, GOOD_SE)
+    oracle.validate(g)  # the reference graph is valid
+    rp = g.ce_rowptr.copy()
+    if case == "rowptr_start":
+        rp = rp + 1
+    elif case == "rowptr_end":
+        rp[-1] -= 1
+    elif case == "rowptr_length":
+        rp = rp[:-1]
+    else:
+        rp[2], rp[3] = rp[3], rp[2] - 1
+    g.ce_rowptr = rp
+    with pytest.raises(ValueError):
+        oracle.validate(g)
 
 
 def test_validate_rejects_bad_graphs():
