@@ -35,6 +35,7 @@
 //                                     optimal leaf of R7 is recovered exactly
 //                                     (DESIGN.md §1);
 //   mpld_partition_*                  the cost-balanced shard partition (scan).
+#include <algorithm>
 #include <climits>
 
 #include "mpld_internal.cuh"
@@ -58,14 +59,6 @@ struct WordOps<unsigned long long> {
   static __device__ __forceinline__ int popc(unsigned long long x) { return __popcll(x); }
   static __device__ __forceinline__ int ffs(unsigned long long x) { return __ffsll((long long)x) - 1; }
   static __device__ __forceinline__ unsigned long long full(int n) { return n == 64 ? ~0ull : ((1ull << n) - 1ull); }
-};
-
-// One level of the explicit backtrack stack (Alg. 1 recursion, lines 13-18).
-template <typename W>
-struct __align__(16) Frame {
-  W saved;     // B[c] before r(v,c) was selected
-  int cost;    // cost when the node was entered
-  int packed;  // v | (c+1) << 8 | (maxused+1) << 16
 };
 
 template <int K, typename W>
@@ -164,103 +157,6 @@ __device__ __forceinline__ int bound_conflicts(const W (&B)[K], W U, W Z, const 
   return lb;
 }
 
-// Incumbent of the sequential search: strict improvement, prune on lb >= best.
-struct SeqIncumbent {
-  int best = INT_MAX;
-  __device__ __forceinline__ bool has() const { return best != INT_MAX; }
-  __device__ __forceinline__ bool prune(int lb) const { return lb >= best; }
-  __device__ __forceinline__ bool improves(int cost) const { return cost < best; }
-  __device__ __forceinline__ void take(int cost) { best = cost; }
-};
-
-// Relaxed Algorithm X with branch and bound (R4-R7) from the node
-// (C, B, U, cost, maxused).  am_adj[i*as] / am_sadj[i*as] = masks of local
-// vertex i; stack[d*ss] = frame of depth d (strides let a warp interleave its
-// lanes' arrays in shared memory).  Returns the nodes entered; the best
-// leaf's masks in bestC.
-template <int K, typename W, typename Inc>
-__device__ unsigned dfs(const W* __restrict__ am_adj, const W* __restrict__ am_sadj, int as, W (&C)[K], W (&B)[K],
-                        W U, int cost, int maxused, int w_stitch, unsigned max_steps,
-                        Frame<W>* __restrict__ stack, int ss, const W* __restrict__ cl, int cs, int ncl,
-                        Inc& inc, W (&bestC)[K], bool& truncated) {
-  using O = WordOps<W>;
-  int depth = 0;
-  unsigned steps = 0;
-  truncated = false;
-  bool enter = true;
-  // the frame of the deepest expanded node lives in registers
-  W f_saved = 0, f_adj = 0, f_sadj = 0;
-  int f_cost = 0, f_v = 0, f_c = -1, f_mu = -1;
-  while (true) {
-    if (enter) {
-      ++steps;
-      if (inc.has() && steps > max_steps) { truncated = true; break; }
-      if (U == 0) {  // Alg. 1 line 5: every column covered -> a solution
-        if (inc.improves(cost)) {
-          inc.take(cost);
-#pragma unroll
-          for (int c = 0; c < K; ++c) bestC[c] = C[c];
-        }
-      } else {
-        W Z, Ol;
-        live_counts<K, W>(B, U, Z, Ol);
-        if (!inc.prune(cost + kCostUnits * bound_conflicts<K, W>(B, U, Z, cl, cs, ncl))) {  // bound (R7)
-          const W cand = Z ? Z : (Ol ? Ol : U);  // Alg. 1 line 8 (R5)
-          const int v = O::ffs(cand);
-          if (depth > 0) {  // spill the parent frame
-            Frame<W> f;
-            f.saved = f_saved;
-            f.cost = f_cost;
-            f.packed = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16);
-            stack[(depth - 1) * ss] = f;
-          }
-          f_v = v;
-          f_c = -1;
-          f_mu = maxused;
-          f_cost = cost;
-          f_adj = am_adj[v * as];
-          f_sadj = am_sadj[v * as];
-          U &= ~(W(1) << v);  // cover column v (line 9)
-          ++depth;
-        }
-      }
-    }
-    if (depth == 0) break;
-    const W bit = W(1) << f_v;
-    if (f_c >= 0) {  // uncover the previous row (line 17)
-      put<K, W>(C, f_c, pick<K, W>(C, f_c) & ~bit);
-      put<K, W>(B, f_c, f_saved);
-    }
-    const int c = f_c + 1;
-    if (c > min(K - 1, f_mu + 1)) {  // rows exhausted (colour-symmetry limit R6): uncover column (line 20)
-      U |= bit;
-      --depth;
-      if (depth > 0) {
-        const Frame<W> f = stack[(depth - 1) * ss];
-        f_saved = f.saved;
-        f_cost = f.cost;
-        f_v = f.packed & 0xff;
-        f_c = ((f.packed >> 8) & 0xff) - 1;
-        f_mu = ((f.packed >> 16) & 0xff) - 1;
-        f_adj = am_adj[f_v * as];
-        f_sadj = am_sadj[f_v * as];
-      }
-      enter = false;
-      continue;
-    }
-    const W Cc = pick<K, W>(C, c);
-    const W Bc = pick<K, W>(B, c);
-    cost = f_cost + kCostUnits * O::popc(f_adj & Cc) + w_stitch * O::popc(f_sadj & ~U & ~Cc);
-    f_saved = Bc;
-    f_c = c;
-    put<K, W>(C, c, Cc | bit);  // select r(v,c) (line 14) and cover its secondary columns (line 15)
-    put<K, W>(B, c, Bc | f_adj);
-    maxused = max(f_mu, c);
-    enter = true;
-  }
-  return steps;
-}
-
 template <int K, typename W>
 __device__ __forceinline__ int colour_of(const W (&bestC)[K], int i) {
   int c = 0;
@@ -285,14 +181,6 @@ struct __align__(16) WarpDisc {
   int order[kMaxComp];                 // BFS position -> vertex id (the rank queue while relabelling)
   int rank[kMaxComp];                  // discovery index -> rank of its id inside the component
   int bpos[kMaxComp];                  // rank -> BFS position
-};
-
-// Per-warp shared storage of the search kernel.
-struct __align__(16) WarpSearch {
-  unsigned long long adj[kMaxComp];   // CE masks (BFS labels)
-  unsigned long long sadj[kMaxComp];  // SE masks
-  Frame<unsigned long long> stack[kMaxComp];
-  unsigned long long cl[kMaxComp / 2];  // clique masks (R7); then the best leaf's C[c]
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -447,36 +335,6 @@ __device__ void warp_relabel(WarpDisc& s, int n) {
   __syncwarp();
 }
 
-// The sequential DFS of R4-R7 on lane 0 (the oracle's node order and budget).
-// W = 32-bit words read the low halves of the 64-bit masks (stride 2).
-template <int K, typename W>
-__device__ unsigned comp_dfs(WarpSearch& s, int n, int w_stitch, unsigned budget, int& best_cost, bool& trunc) {
-  constexpr int as = sizeof(unsigned long long) / sizeof(W);
-  const W* a = (const W*)s.adj;
-  const W* sa = (const W*)s.sadj;
-  W* cl = (W*)s.cl;
-  W C[K], B[K], bestC[K];
-#pragma unroll
-  for (int c = 0; c < K; ++c) C[c] = B[c] = bestC[c] = 0;
-  SeqIncumbent inc;
-  const int ncl = clique_min<K>() ? clique_partition<W>(a, as, n, cl, 1, clique_min<K>()) : 0;
-  const unsigned steps = dfs<K, W, SeqIncumbent>(a, sa, as, C, B, WordOps<W>::full(n), 0, -1, w_stitch, budget,
-                                                 (Frame<W>*)s.stack, 1, cl, 1, ncl, inc, bestC, trunc);
-#pragma unroll
-  for (int c = 0; c < K; ++c) s.cl[c] = (unsigned long long)bestC[c];
-  best_cost = inc.best;
-  return steps;
-}
-
-template <int K>
-__device__ __forceinline__ int colour_of_mask(const unsigned long long* bestC, int i) {
-  int c = 0;
-#pragma unroll
-  for (int cc = 1; cc < K; ++cc)
-    if ((bestC[cc] >> i) & 1ull) c = cc;
-  return c;
-}
-
 // Adds a component's Eq. (1b)/(1c) counts to its layout (the whole warp calls;
 // nc, ns = per-lane sums over the vertices, each edge seen from both ends).
 // The recovery never adds a conflict (R9) and stitch vertices are
@@ -563,30 +421,34 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
 
 // The budgeted sequential search (the oracle's node order and budget, R7) of
 // one component per LANE: a warp takes 32 consecutive components of the pool
-// and every lane runs the DFS of dfs() on its own component (32-bit words,
-// components of <= 32 vertices), written branch-free so that the lanes issue
-// one instruction stream.  Masks and frames are [index][lane] in shared memory
-// (a lane only touches its own column).  Components of more than 32 vertices
-// are searched afterwards one at a time on lane 0 (64-bit words).  Exact mode
-// hands components whose search exceeds the light budget to the warp-parallel
+// and every lane runs the DFS of lane_dfs() on its own component, written
+// branch-free so that the lanes issue one instruction stream.  Masks and
+// frames are [index][lane] in shared memory (a lane only touches its own
+// column).  mpld_exact_cover_search<K> runs the components of <= 32 vertices
+// on 32-bit words and lists the larger ones; mpld_exact_cover_search_wide<K>
+// runs those, again one per lane, on 64-bit words.  Exact mode hands
+// components whose search exceeds the light budget to the warp-parallel
 // kernel below.
-constexpr int kLaneWarps = 2;  // warps per CTA of the light search
+constexpr int kLaneWarps = 2;  // warps per CTA of the light search (32-bit words)
 
-struct __align__(16) LaneLight {
-  unsigned A[32][32];       // adj[v][lane]
-  unsigned S[32][32];       // sadj[v][lane]
-  unsigned saved[32][32];   // frame d: B[c] before r(v,c) was selected
-  int cost[32][32];         // frame d: cost when the node was entered
-  int pk[32][32];           // frame d: v | (c+1) << 8 | (maxused+1) << 16
-  unsigned cl[16][32];      // clique masks (R7, k >= 4)
+template <typename W, int N>
+struct __align__(16) LaneStore {
+  W A[N][32];        // adj[v][lane]
+  W S[N][32];        // sadj[v][lane]
+  W saved[N][32];    // frame d: B[c] before r(v,c) was selected
+  int cost[N][32];   // frame d: cost when the node was entered
+  int pk[N][32];     // frame d: v | (c+1) << 8 | (maxused+1) << 16
+  W cl[N / 2][32];   // clique masks (R7, k >= 4)
 };
-static_assert(sizeof(LaneLight) >= sizeof(WarpSearch), "the single-lane path reuses the lane storage");
+using LaneLight = LaneStore<unsigned, 32>;
+using LaneWide = LaneStore<unsigned long long, kMaxComp>;
 
-// the DFS of dfs() with a SeqIncumbent, one component per lane; returns the nodes entered
-template <int K>
-__device__ unsigned lane_dfs(LaneLight& L, int lane, bool valid, int n, int w_stitch, unsigned budget, int ncl,
-                             unsigned (&bestC)[K], int& best, bool& trunc) {
-  using W = unsigned;
+// The relaxed Algorithm X of R4-R7 with branch and bound, one component per
+// lane (the oracle's node order, incumbent rule and budget); returns the nodes
+// entered and the best leaf's colour masks in bestC.
+template <int K, typename W, int N>
+__device__ unsigned lane_dfs(LaneStore<W, N>& L, int lane, bool valid, int n, int w_stitch, unsigned budget, int ncl,
+                             W (&bestC)[K], int& best, bool& trunc) {
   using O = WordOps<W>;
   W C[K], B[K];
 #pragma unroll
@@ -701,48 +563,6 @@ __device__ __forceinline__ void light_handoff(const GraphView& g, const Workspac
   w.hcost[idx] = best_cost;
 }
 
-// One component of more than 32 vertices on lane 0 of the warp (64-bit words).
-template <int K>
-__device__ void light_single(const GraphView& g, const Workspace& w, WarpSearch& s, int ci, int w_stitch,
-                             unsigned budget, bool exact, int* colors, long long* counts, LightAcc& acc) {
-  const int lane = threadIdx.x & 31;
-  const unsigned long long rec = __ldcg(&w.crec[ci]);
-  const size_t off = (size_t)(rec >> 8);
-  const int n = (int)(rec & 0xffull);
-  for (int i = lane; i < n; i += 32) {
-    const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
-    s.adj[i] = m.x;
-    s.sadj[i] = m.y;
-  }
-  __syncwarp();
-  unsigned steps = 0;
-  bool trunc = false;
-  int best_cost = 0;
-  if (lane == 0) steps = comp_dfs<K, unsigned long long>(s, n, w_stitch, budget, best_cost, trunc);
-  __syncwarp();
-  for (int i = lane; i < n; i += 32) colors[__ldcg(&w.porder[off + i])] = colour_of_mask<K>(s.cl, i);
-  trunc = __shfl_sync(0xffffffffu, trunc, 0);
-  if (counts && !(trunc && exact)) {
-    int nc = 0, ns = 0;
-    for (int i = lane; i < n; i += 32) {
-      const unsigned long long Ci = s.cl[colour_of_mask<K>(s.cl, i)];
-      nc += __popcll(s.adj[i] & Ci);
-      ns += __popcll(s.sadj[i] & ~Ci);
-    }
-    add_counts(g, __ldcg(&w.porder[off]), nc, ns, counts);
-  }
-  if (lane == 0) {
-    if (trunc && exact) {
-      light_handoff(g, w, ci, n, best_cost);
-    } else {
-      acc.maxsteps = max(acc.maxsteps, (int)min(steps, (unsigned)INT_MAX));
-      acc.trunc += trunc ? 1 : 0;
-    }
-    acc.steps += steps;
-  }
-  __syncwarp();
-}
-
 // Sharded search: the component rooted at `root` belongs to the
 // shard in which its cost interval [prefix - est, prefix) starts (contiguous
 // root-id ranges of equal estimated cost; the same on every rank).
@@ -756,81 +576,58 @@ __device__ __forceinline__ bool in_shard(const GraphView& g, const Workspace& w,
   return s == shard_index;
 }
 
-template <int K>
-__global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
-                                                                           long long max_steps, int* colors,
-                                                                           unsigned light_steps, long long* counts,
-                                                                           int shard_index, int shard_count) {
-  pdl_begin();
-  __shared__ LaneLight s_lane[kLaneWarps];
-  LaneLight& L = s_lane[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
-  Control* ctl = w.ctl;
-  const int n_comp = __ldcg(&ctl->err) ? 0 : (int)(__ldcg(&ctl->comp_pool) >> 32);
-  const bool exact = max_steps <= 0;
-  const unsigned budget = exact ? light_steps
-                                : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
-  LightAcc acc;  // this lane's statistics
-  const int nb = gridDim.x * kLaneWarps;
-  for (int b = blockIdx.x * kLaneWarps + (threadIdx.x >> 5); b * 32 < n_comp; b += nb) {
-    const int ci = b * 32 + lane;
-    unsigned long long rec = 0ull;
-    if (ci < n_comp) rec = __ldcg(&w.crec[ci]);
-    const size_t off = (size_t)(rec >> 8);
-    const int n = (int)(rec & 0xffull);
-    const bool mine_c = ci < n_comp && in_shard(g, w, __ldcg(&w.porder[off]), n, K, shard_index, shard_count);
-    const bool valid = mine_c && n <= 32;
-    acc.comps += mine_c ? 1 : 0;
-    if (valid)
+// One component per lane (lane `valid` with pool record `rec`): staging of its
+// masks, clique partition, the DFS, then colours / counts / statistics, or the
+// hand-off to the warp-parallel search (exact mode, light budget exceeded).
+template <int K, typename W, int N>
+__device__ __forceinline__ void lane_component(const GraphView& g, const Workspace& w, LaneStore<W, N>& L, int lane,
+                                               bool valid, int ci, unsigned long long rec, int w_stitch,
+                                               unsigned budget, bool exact, int* colors, long long* counts,
+                                               LightAcc& acc) {
+  const size_t off = (size_t)(rec >> 8);
+  const int n = (int)(rec & 0xffull);
+  if (valid)
+    for (int i = 0; i < n; ++i) {
+      const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
+      L.A[i][lane] = (W)m.x;
+      L.S[i][lane] = (W)m.y;
+    }
+  const int ncl = valid && clique_min<K>() ? clique_partition<W>(&L.A[0][lane], 32, n, &L.cl[0][lane], 32,
+                                                                  clique_min<K>())
+                                           : 0;
+  W bestC[K];
+  int best_cost = 0;
+  bool trunc = false;
+  const unsigned steps = lane_dfs<K, W, N>(L, lane, valid, n, w_stitch, budget, ncl, bestC, best_cost, trunc);
+  if (!valid) return;
+  for (int i = 0; i < n; ++i) colors[__ldcg(&w.porder[off + i])] = colour_of<K, W>(bestC, i);
+  if (trunc && exact) {
+    light_handoff(g, w, ci, n, best_cost);
+  } else {
+    if (counts) {  // final colouring: Eq. (1b)/(1c) counts of the component
+      int nc = 0, ns = 0;
       for (int i = 0; i < n; ++i) {
-        const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
-        L.A[i][lane] = (unsigned)m.x;
-        L.S[i][lane] = (unsigned)m.y;
+        const W Ci = pick<K, W>(bestC, colour_of<K, W>(bestC, i));
+        nc += WordOps<W>::popc(L.A[i][lane] & Ci);
+        ns += WordOps<W>::popc(L.S[i][lane] & ~Ci);
       }
-    const int ncl = valid && clique_min<K>() ? clique_partition<unsigned>(&L.A[0][lane], 32, n, &L.cl[0][lane], 32,
-                                                                           clique_min<K>())
-                                             : 0;
-    unsigned bestC[K];
-    int best_cost = 0;
-    bool trunc = false;
-    const unsigned steps = lane_dfs<K>(L, lane, valid, n, w_stitch, budget, ncl, bestC, best_cost, trunc);
-    if (valid) {
-      for (int i = 0; i < n; ++i) colors[__ldcg(&w.porder[off + i])] = colour_of<K, unsigned>(bestC, i);
-      if (trunc && exact) {
-        light_handoff(g, w, ci, n, best_cost);
-      } else {
-        if (counts) {  // final colouring: Eq. (1b)/(1c) counts of the component
-          int nc = 0, ns = 0;
-          for (int i = 0; i < n; ++i) {
-            const unsigned Ci = pick<K, unsigned>(bestC, colour_of<K, unsigned>(bestC, i));
-            nc += __popc(L.A[i][lane] & Ci);
-            ns += __popc(L.S[i][lane] & ~Ci);
-          }
-          nc >>= 1;
-          ns >>= 1;
-          if (nc | ns) {
-            const int l = layout_of(g, __ldcg(&w.porder[off]));
-            if (nc) atomicAdd((unsigned long long*)&counts[2 * l], (unsigned long long)nc);
-            if (ns) atomicAdd((unsigned long long*)&counts[2 * l + 1], (unsigned long long)ns);
-          }
-        }
-        acc.maxsteps = max(acc.maxsteps, (int)min(steps, (unsigned)INT_MAX));
-        acc.trunc += trunc ? 1 : 0;
+      nc >>= 1;
+      ns >>= 1;
+      if (nc | ns) {
+        const int l = layout_of(g, __ldcg(&w.porder[off]));
+        if (nc) atomicAdd((unsigned long long*)&counts[2 * l], (unsigned long long)nc);
+        if (ns) atomicAdd((unsigned long long*)&counts[2 * l + 1], (unsigned long long)ns);
       }
-      acc.steps += steps;
     }
-    // components of more than 32 vertices: one at a time on lane 0
-    unsigned big = __ballot_sync(0xffffffffu, mine_c && n > 32);
-    __syncwarp();
-    while (big) {
-      const int l = __ffs(big) - 1;
-      big &= big - 1;
-      light_single<K>(g, w, *reinterpret_cast<WarpSearch*>(&L), b * 32 + l, w_stitch, budget, exact, colors, counts,
-                      acc);
-    }
-    __syncwarp();
+    acc.maxsteps = max(acc.maxsteps, (int)min(steps, (unsigned)INT_MAX));
+    acc.trunc += trunc ? 1 : 0;
   }
-  // statistics: one atomic per warp
+  acc.steps += steps;
+}
+
+// statistics of a light kernel: one atomic per warp
+__device__ __forceinline__ void light_stats(Control* ctl, const LightAcc& acc) {
+  const int lane = threadIdx.x & 31;
   unsigned long long st = acc.steps;
   int mx = acc.maxsteps;
   unsigned tr = acc.trunc, nc = acc.comps;
@@ -847,6 +644,76 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
     atomicMax(&ctl->max_steps_comp, mx);
     if (tr) atomicAdd(&ctl->truncated, (int)tr);
   }
+}
+
+__host__ __device__ constexpr unsigned light_budget(long long max_steps, unsigned light_steps) {
+  return max_steps <= 0 ? light_steps : (max_steps >= (long long)UINT_MAX ? UINT_MAX : (unsigned)max_steps);
+}
+
+template <int K>
+__global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
+                                                                           long long max_steps, int* colors,
+                                                                           unsigned light_steps, long long* counts,
+                                                                           int shard_index, int shard_count) {
+  pdl_begin();
+  __shared__ LaneLight s_lane[kLaneWarps];
+  LaneLight& L = s_lane[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  Control* ctl = w.ctl;
+  const int n_comp = __ldcg(&ctl->err) ? 0 : (int)(__ldcg(&ctl->comp_pool) >> 32);
+  const bool exact = max_steps <= 0;
+  const unsigned budget = light_budget(max_steps, light_steps);
+  LightAcc acc;  // this lane's statistics
+  const int nb = gridDim.x * kLaneWarps;
+  for (int b = blockIdx.x * kLaneWarps + (threadIdx.x >> 5); b * 32 < n_comp; b += nb) {
+    const int ci = b * 32 + lane;
+    unsigned long long rec = 0ull;
+    if (ci < n_comp) rec = __ldcg(&w.crec[ci]);
+    const size_t off = (size_t)(rec >> 8);
+    const int n = (int)(rec & 0xffull);
+    const bool mine_c = ci < n_comp && in_shard(g, w, __ldcg(&w.porder[off]), n, K, shard_index, shard_count);
+    acc.comps += mine_c ? 1 : 0;
+    // components of more than 32 vertices: listed for the 64-bit lane kernel
+    const bool wide = mine_c && n > 32;
+    const unsigned wm = __ballot_sync(0xffffffffu, wide);
+    if (wm) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&ctl->n_wide, __popc(wm));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (wide) w.wide[base + __popc(wm & lanemask_lt())] = ci;
+    }
+    lane_component<K, unsigned, 32>(g, w, L, lane, mine_c && n <= 32, ci, rec, w_stitch, budget, exact, colors,
+                                    counts, acc);
+    __syncwarp();
+  }
+  light_stats(ctl, acc);
+}
+
+// The components of more than 32 vertices (listed by the kernel above), one
+// per lane on 64-bit words; one warp per CTA (LaneWide is 72 KB of shared memory).
+template <int K>
+__global__ void __launch_bounds__(32) mpld_exact_cover_search_wide(GraphView g, Workspace w, int w_stitch,
+                                                                   long long max_steps, int* colors,
+                                                                   unsigned light_steps, long long* counts) {
+  pdl_begin();
+  extern __shared__ __align__(16) unsigned char smem[];
+  LaneWide& L = *reinterpret_cast<LaneWide*>(smem);
+  const int lane = threadIdx.x & 31;
+  Control* ctl = w.ctl;
+  const int n_wide = __ldcg(&ctl->err) ? 0 : __ldcg(&ctl->n_wide);
+  const bool exact = max_steps <= 0;
+  const unsigned budget = light_budget(max_steps, light_steps);
+  LightAcc acc;
+  for (int b = blockIdx.x; b * 32 < n_wide; b += gridDim.x) {
+    const int j = b * 32 + lane;
+    const int ci = j < n_wide ? __ldcg(&w.wide[j]) : -1;
+    const unsigned long long rec = ci >= 0 ? __ldcg(&w.crec[ci]) : 0ull;
+    lane_component<K, unsigned long long, kMaxComp>(g, w, L, lane, ci >= 0, ci, rec, w_stitch, budget, exact,
+                                                    colors, counts, acc);
+    __syncwarp();
+  }
+  acc.comps = 0;  // counted by the kernel that listed them
+  light_stats(ctl, acc);
 }
 
 // ----------------------------------------------------------------------------
@@ -1756,22 +1623,61 @@ cudaError_t launch_partition_scan(const GraphView& g, Workspace ws, cudaStream_t
   return cudaGetLastError();
 }
 
+template <int K>
+cudaError_t launch_search_k(const GraphView& g, Workspace ws, int w_stitch, long long max_steps, int* colors,
+                            unsigned light_steps, long long* counts, int shard_index, int shard_count, cudaStream_t s,
+                            int blocks, bool pdl) {
+  return launch_ex(mpld_exact_cover_search<K>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws, w_stitch,
+                   max_steps, colors, light_steps, counts, shard_index, shard_count);
+}
+
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
                           unsigned light_steps, long long* counts, int shard_index, int shard_count, cudaStream_t s,
                           int blocks, bool pdl) {
   switch (k) {
-    case 2:
-      return launch_ex(mpld_exact_cover_search<2>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws, w_stitch,
-                       max_steps, colors, light_steps, counts, shard_index, shard_count);
-    case 3:
-      return launch_ex(mpld_exact_cover_search<3>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws, w_stitch,
-                       max_steps, colors, light_steps, counts, shard_index, shard_count);
-    case 4:
-      return launch_ex(mpld_exact_cover_search<4>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws, w_stitch,
-                       max_steps, colors, light_steps, counts, shard_index, shard_count);
+    case 2: return launch_search_k<2>(g, ws, w_stitch, max_steps, colors, light_steps, counts, shard_index,
+                                      shard_count, s, blocks, pdl);
+    case 3: return launch_search_k<3>(g, ws, w_stitch, max_steps, colors, light_steps, counts, shard_index,
+                                      shard_count, s, blocks, pdl);
+    case 4: return launch_search_k<4>(g, ws, w_stitch, max_steps, colors, light_steps, counts, shard_index,
+                                      shard_count, s, blocks, pdl);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
+}
+
+cudaError_t launch_search_wide(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
+                               int* colors, unsigned light_steps, long long* counts, cudaStream_t s, int blocks) {
+  const size_t smem = sizeof(LaneWide);
+  switch (k) {
+    case 2: return launch_ex(mpld_exact_cover_search_wide<2>, dim3(blocks), dim3(32), smem, s, true, false, g, ws,
+                             w_stitch, max_steps, colors, light_steps, counts);
+    case 3: return launch_ex(mpld_exact_cover_search_wide<3>, dim3(blocks), dim3(32), smem, s, true, false, g, ws,
+                             w_stitch, max_steps, colors, light_steps, counts);
+    case 4: return launch_ex(mpld_exact_cover_search_wide<4>, dim3(blocks), dim3(32), smem, s, true, false, g, ws,
+                             w_stitch, max_steps, colors, light_steps, counts);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int K>
+cudaError_t configure_wide_k(int num_sms, int* blocks) {
+  const cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_wide<K>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaneWide));
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search_wide<K>, 32, sizeof(LaneWide));
+  *blocks = per_sm * num_sms;
+  return cudaSuccess;
+}
+
+// shared-memory limit and resident grid of the 64-bit lane kernels (the same for every k)
+cudaError_t configure_search_wide(int num_sms, int* blocks) {
+  int b2 = 0, b3 = 0, b4 = 0;
+  cudaError_t e = configure_wide_k<2>(num_sms, &b2);
+  if (e == cudaSuccess) e = configure_wide_k<3>(num_sms, &b3);
+  if (e == cudaSuccess) e = configure_wide_k<4>(num_sms, &b4);
+  *blocks = std::min(b2, std::min(b3, b4));
+  return e;
 }
 
 template <int K>

@@ -5,7 +5,8 @@
 //   mpld_simplify_components   cooperative: validation, simplification rounds, seeds,
 //                              recovery pop keys and level 0
 //   mpld_component_discover    one warp per seed: components -> pool of bit-packed matrices
-//   mpld_exact_cover_search<K> one warp per component of the pool
+//   mpld_exact_cover_search<K> one component of <= 32 vertices per lane (32-bit words)
+//   mpld_exact_cover_search_wide<K> one component of > 32 vertices per lane (64-bit words)
 //   mpld_exact_cover_search_heavy<K,W> (exact mode) one warp per heavy component, one launch
 //                              per word class (32-bit: n <= 32, 64-bit: n > 32)
 //   mpld_recover_prep          (second stream, beside discovery and search) recovery
@@ -42,10 +43,11 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(MPLD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-enum KernelId { K_SIMPLIFY = 0, K_DISCOVER, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_PREP, K_COUNT };
+enum KernelId { K_SIMPLIFY = 0, K_DISCOVER, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_PREP, K_SEARCH_WIDE,
+                K_COUNT };
 const char* kKernelNames[K_COUNT] = {"mpld_simplify_components", "mpld_component_discover",
                                      "mpld_exact_cover_search", "mpld_exact_cover_search_heavy", "mpld_recover",
-                                     "mpld_evaluate", "mpld_recover_prep"};
+                                     "mpld_evaluate", "mpld_recover_prep", "mpld_exact_cover_search_wide"};
 
 constexpr int kCoopThreads = 1024;
 #ifndef MPLD_SEPARATE_PREP
@@ -106,6 +108,7 @@ struct mpld_context {
   int* porder = nullptr;
   int* hcomp = nullptr;
   int* hcost = nullptr;
+  int* wide = nullptr;
   WorkItem* wq = nullptr;     // spilled heavy-search work (fixed size)
   unsigned* wq_flag = nullptr;
   HeavySlot* hslot = nullptr;
@@ -123,6 +126,7 @@ struct mpld_context {
   unsigned light_steps = kLightStepsDefault;  // MPLD_LIGHT_STEPS overrides (tuning)
   int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0, blocks_discover = 0;
   int blocks_heavy[6] = {0, 0, 0, 0, 0, 0};  // per k = 2..4 and word class (32-bit, 64-bit)
+  int blocks_wide = 0;                        // the 64-bit lane kernel
   long long* counts = nullptr;  // the prepare phase's d_counts (zeroed by the simplification kernel)
   bool search_counted = false;  // the search accumulated the counts (one shard)
   int searches_since_prepare = 0;
@@ -177,7 +181,8 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
   if (n > ctx->cap_n) {
     int64_t cap = std::max<int64_t>(n, ctx->cap_n * 3 / 2);
     cudaError_t e = cudaSuccess;
-    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->roots, &ctx->porder, &ctx->hcomp, &ctx->hcost}) {
+    for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->roots, &ctx->porder, &ctx->hcomp, &ctx->hcost,
+                    &ctx->wide}) {
       e = grow(p, cap);
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
@@ -257,7 +262,7 @@ int mark_last(mpld_context* ctx, cudaStream_t s) {
 
 Workspace workspace(mpld_context* ctx) {
   return Workspace{ctx->deg,   ctx->hround, ctx->bmask,  ctx->prio,  ctx->q0,    ctx->q1,    ctx->roots,
-                   ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->ctl,   ctx->wq,
+                   ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->wide,  ctx->ctl,   ctx->wq,
                    ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters, ctx->tail_slots};
 }
 
@@ -345,6 +350,14 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
     cudaError_t e = launch_search(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, count, shard_index,
                                   shard_count, s, ctx->blocks_search, !sharded);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
+    t.done();
+    ++ctx->call_launches;
+  }
+  {  // the components of > 32 vertices, one per lane on 64-bit words
+    TimedLaunch t(ctx, K_SEARCH_WIDE, s);
+    cudaError_t e = launch_search_wide(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, count, s,
+                                       ctx->blocks_wide);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_wide");
     t.done();
     ++ctx->call_launches;
   }
@@ -544,7 +557,8 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     return cuda_fail(e, "configure recovery tail");
   }
   e = configure_search_heavy(ctx->num_sms, ctx->blocks_heavy);
-  if (e != cudaSuccess) {
+  if (e == cudaSuccess) e = configure_search_wide(ctx->num_sms, &ctx->blocks_wide);
+  if (e != cudaSuccess || ctx->blocks_wide <= 0) {
     mpld_context_destroy(ctx);
     return cuda_fail(e, "configure heavy search");
   }
@@ -578,7 +592,7 @@ void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->bmask, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->roots, (void*)ctx->crec, (void*)ctx->pmask, (void*)ctx->porder, (void*)ctx->hcomp,
-                  (void*)ctx->hcost, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
+                  (void*)ctx->hcost, (void*)ctx->wide, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
                   (void*)ctx->est, (void*)ctx->bsum,
                   (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,

@@ -58,6 +58,7 @@ struct Control {
   int slot_next;               // spilled-component slots handed out (reset with n_heavy)
   int may_spill;               // a heavy component of >= kHelpersMinN vertices was handed off: idle heavy
                                // warps stay for spilled work instead of leaving (reset with n_heavy)
+  int n_wide;                  // components of > 32 vertices listed for the 64-bit lane kernel (reset with n_heavy)
   alignas(128) int heavy_next[2];  // exact mode: next heavy component to take per word class (reset with n_heavy)
   alignas(128) int wq_head[2];     // spilled work items: tickets handed out per word class (reset with n_heavy)
   alignas(128) int wq_tail[2];     // ... positions reserved (polled)
@@ -157,6 +158,7 @@ struct Workspace {
   int* porder;                // component pool: vertex ids in BFS column order
   int* hcomp;      // heavy components (exact mode): component index ...
   int* hcost;      // ... and the light phase's best cost
+  int* wide;       // components of > 32 vertices (pool index), searched by the 64-bit lane kernel
   Control* ctl;
   WorkItem* wq;    // [2][kWQCap] spilled work items per word class
   unsigned* wq_flag;  // [2][kWQCap] == epoch once the item is written
@@ -254,6 +256,10 @@ cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch,
                           unsigned light_steps, long long* counts, int shard_index, int shard_count, cudaStream_t s,
                           int blocks, bool pdl);
 constexpr unsigned kLightStepsDefault = 48;  // exact mode: one-lane budget before a component turns heavy
+// the components of > 32 vertices the light kernel listed, one per lane on 64-bit words
+cudaError_t launch_search_wide(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps,
+                               int* colors, unsigned light_steps, long long* counts, cudaStream_t s, int blocks);
+cudaError_t configure_search_wide(int num_sms, int* blocks);
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, long long* counts,
                                 cudaStream_t s, const int* blocks, bool pdl);
 cudaError_t configure_search_heavy(int num_sms, int* blocks);  // blocks[6]: resident grids of the heavy kernels
