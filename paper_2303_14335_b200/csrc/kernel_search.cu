@@ -758,7 +758,11 @@ constexpr int kStealMinIdle = MPLD_STEAL_MIN_IDLE;  // donation rounds only when
 #ifndef MPLD_QUEUE_LOW
 #define MPLD_QUEUE_LOW 64
 #endif
-constexpr int kQueueLow = MPLD_QUEUE_LOW;  // the work queue is fed while it holds fewer items than this
+constexpr int kQueueLow = MPLD_QUEUE_LOW;
+#ifndef MPLD_SEED_INCUMBENT
+#define MPLD_SEED_INCUMBENT 1
+#endif
+constexpr bool kSeedIncumbent = MPLD_SEED_INCUMBENT != 0;  // greedy starting incumbent of heavy components  // the work queue is fed while it holds fewer items than this
 constexpr unsigned kSpillCheck = 64;  // spill / slot-sync checks every this many iterations (power of two),
                                       // from Workspace::spill_iters on
 
@@ -880,6 +884,7 @@ struct HeavyUnit {
   int c1;     // the light phase's leaf: key and colour masks (component units; slot initialisation)
   Path p1;
   W col[K];
+  int hc;     // the starting incumbent's cost: min(c1, greedy seed) (a leaf of that cost exists)
 };
 
 __device__ __forceinline__ void slot_lock(HeavySlot* s) {
@@ -1168,7 +1173,8 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
               HeavySlot* hs = &w.hslot[sl];
               hs->lock = 0;
               hs->pend = 1;
-              hs->cost = hs->lcost = hs->bcost = u.c1;
+              hs->cost = hs->lcost = u.c1;
+              hs->bcost = u.hc;
               hs->pa = hs->lpa = u.p1.a;
               hs->pb = hs->lpb = u.p1.b;
 #pragma unroll
@@ -1259,6 +1265,98 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
   steps_out = tot;
   capped_out = __any_sync(0xffffffffu, capped);
+}
+
+// A starting incumbent for the exact search ("seeded
+// incumbent"): every lane builds one colouring greedily — the uncovered
+// column with the fewest live rows (a random one among ties), the row of least
+// Eq. (1) cost (random tie order) — then improves it by single-vertex moves
+// (three sweeps); the warp's minimum cost is returned.  Masks are
+// interchangeable, so a colouring of cost c is (after renaming masks into
+// first-use order along its own column sequence) a leaf of the canonical tree:
+// (c, maximal path) is a valid incumbent key that never cuts the canonical
+// optimum (its key is <= (c, path of any leaf of cost c)).
+template <int K, typename W>
+__device__ int warp_greedy_seed(const W* adj, const W* sadj, int n, int w_stitch, unsigned seed) {
+  using O = WordOps<W>;
+  const int lane = threadIdx.x & 31;
+  unsigned r = lowbias32(seed * 32u + (unsigned)lane + 0x9e3779b9u);
+  W C[K], B[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) C[c] = B[c] = 0;
+  W U = O::full(n);
+  for (int d = 0; d < n; ++d) {
+    // live-row count of every uncovered column, bit-sliced (3 bits: 0..4)
+    W b0 = 0, b1 = 0, b2 = 0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const W F = U & ~B[c];
+      const W c0 = b0 & F;
+      b0 ^= F;
+      const W c1 = b1 & c0;
+      b1 ^= c0;
+      b2 |= c1;
+    }
+    W cand = U & ~b0 & ~b1 & ~b2;                         // 0 live rows
+    if (!cand) cand = b0 & ~b1 & ~b2;                     // 1
+    if (!cand) cand = ~b0 & b1 & ~b2 & U;                 // 2
+    if (!cand) cand = b0 & b1 & ~b2;                      // 3
+    if (!cand) cand = U;                                  // 4
+    r = r * 1664525u + 1013904223u;
+    const int sh = (int)((r >> 8) % (unsigned)n);
+    const W rot = sh ? (((cand >> sh) | (cand << (n - sh))) & O::full(n)) : cand;
+    int v = O::ffs(rot) + sh;
+    v = v >= n ? v - n : v;
+    const W bit = W(1) << v;
+    const W a = adj[v], sa = sadj[v];
+    const int off = (int)((r >> 24) % (unsigned)K);
+    int bc = 0, bcost = INT_MAX;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int c = (i + off) % K;
+      const int cc = kCostUnits * O::popc(a & C[c]) + w_stitch * O::popc(sa & ~U & ~C[c]);
+      if (cc < bcost) {
+        bcost = cc;
+        bc = c;
+      }
+    }
+    U &= ~bit;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      C[c] = c == bc ? (C[c] | bit) : C[c];
+      B[c] = c == bc ? (B[c] | a) : B[c];
+    }
+  }
+  for (int sweep = 0; sweep < 3; ++sweep)
+    for (int v = 0; v < n; ++v) {
+      const W bit = W(1) << v;
+      const W a = adj[v], sa = sadj[v];
+      int cur = 0, bc = 0, bcost = INT_MAX;
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        const int cc = kCostUnits * O::popc(a & C[c]) + w_stitch * O::popc(sa & ~C[c]);
+        if (C[c] & bit) cur = cc;
+        if (cc < bcost) {
+          bcost = cc;
+          bc = c;
+        }
+      }
+      if (bcost < cur) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) C[c] = c == bc ? (C[c] | bit) : (C[c] & ~bit);
+      }
+    }
+  int nc = 0, ns = 0;
+  for (int v = 0; v < n; ++v) {
+    const W bit = W(1) << v;
+    W Cv = C[0];
+#pragma unroll
+    for (int c = 1; c < K; ++c) Cv = (C[c] & bit) ? C[c] : Cv;
+    nc += O::popc(adj[v] & Cv);
+    ns += O::popc(sadj[v] & ~Cv);
+  }
+  const int cost = kCostUnits * (nc >> 1) + w_stitch * (ns >> 1);
+  return (int)(__reduce_min_sync(0xffffffffu, (unsigned)cost));
 }
 
 // the path of the leaf whose colours are col (a leaf of the canonical tree:
@@ -1424,6 +1522,15 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g,
         u.p1 = leaf_path<K, W>(u.col, u.n, s_adj, s_sadj, w_stitch, lc);
         gcost = u.c1;
         gP = u.p1;
+        u.hc = u.c1;
+        if (kSeedIncumbent) {  // a cheaper greedy colouring: (its cost, maximal path) is a valid incumbent key
+          const int hc = warp_greedy_seed<K, W>(s_adj, s_sadj, u.n, w_stitch, (unsigned)u.ci);
+          if (hc < u.c1) {
+            u.hc = hc;
+            gcost = hc;
+            gP = Path{~0ull, ~0ull};
+          }
+        }
         W zero[K];
 #pragma unroll
         for (int c = 0; c < K; ++c) zero[c] = 0;
