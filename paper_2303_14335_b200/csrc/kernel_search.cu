@@ -430,6 +430,10 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
 // components whose search exceeds the light budget to the warp-parallel
 // kernel below.
 constexpr int kLaneWarps = 2;  // warps per CTA of the light search (32-bit words)
+#ifndef MPLD_STAGED_LIGHT
+#define MPLD_STAGED_LIGHT 1
+#endif
+constexpr bool kStagedLight = MPLD_STAGED_LIGHT != 0;  // coalesced warp staging of the light kernel's records
 
 template <typename W, int N>
 struct __align__(16) LaneStore {
@@ -576,22 +580,72 @@ __device__ __forceinline__ bool in_shard(const GraphView& g, const Workspace& w,
   return s == shard_index;
 }
 
+// Staging of the warp's 32 CONSECUTIVE pool records (the light kernel's lanes
+// take components b*32 + lane; the discovery kernel hands out component index
+// and pool offset from one atomic, so lane l's rows are pool entries
+// [off_l, off_l + n_l), contiguous and increasing with l): the warp reads the
+// whole range with coalesced loads, entry e going to the lane that owns it
+// (binary search over the lanes' start offsets by shuffles), transposed into
+// the [row][lane] layout of shared memory.  Lanes with `has` = false hold no
+// record; rows of lanes with `store` = false are read but not kept.
+__device__ __forceinline__ int warp_owner(unsigned rel, unsigned e) {
+  int o = 0;
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1) {
+    const unsigned r = __shfl_sync(0xffffffffu, rel, o + st);
+    if (r <= e) o += st;
+  }
+  return o;
+}
+
+template <typename W, int N, bool kOrder>
+__device__ __forceinline__ void warp_stage(const Workspace& w, LaneStore<W, N>& L, int lane, bool has, bool store,
+                                           size_t off, int n) {
+  const size_t base = __shfl_sync(0xffffffffu, off, 0);  // lane 0 always holds a record
+  const unsigned rel = has ? (unsigned)(off - base) : 0xffffffffu;
+  const unsigned end = __reduce_max_sync(0xffffffffu, has ? rel + (unsigned)n : 0u);
+  for (unsigned e0 = 0; e0 < end; e0 += 32) {
+    const unsigned e = e0 + lane;
+    const int o = warp_owner(rel, e);
+    const unsigned ro = __shfl_sync(0xffffffffu, rel, o);
+    const bool so = __shfl_sync(0xffffffffu, store, o);
+    if (e < end) {
+      if (kOrder) {  // vertex ids (after the search: the frames' pk rows are free)
+        const int v = __ldcg(&w.porder[base + e]);
+        if (so) L.pk[e - ro][o] = v;
+      } else {  // adj / sadj words
+        const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (base + e)]);
+        if (so) {
+          L.A[e - ro][o] = (W)m.x;
+          L.S[e - ro][o] = (W)m.y;
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
 // One component per lane (lane `valid` with pool record `rec`): staging of its
 // masks, clique partition, the DFS, then colours / counts / statistics, or the
 // hand-off to the warp-parallel search (exact mode, light budget exceeded).
-template <int K, typename W, int N>
+// kStaged: the warp's records are consecutive (warp_stage), `has` = the lane
+// holds a record; else each lane reads its own record.
+template <int K, typename W, int N, bool kStaged>
 __device__ __forceinline__ void lane_component(const GraphView& g, const Workspace& w, LaneStore<W, N>& L, int lane,
-                                               bool valid, int ci, unsigned long long rec, int w_stitch,
+                                               bool has, bool valid, int ci, unsigned long long rec, int w_stitch,
                                                unsigned budget, bool exact, int* colors, long long* counts,
                                                LightAcc& acc) {
   const size_t off = (size_t)(rec >> 8);
   const int n = (int)(rec & 0xffull);
-  if (valid)
+  if (kStaged) {
+    warp_stage<W, N, false>(w, L, lane, has, valid, off, n);
+  } else if (valid) {
     for (int i = 0; i < n; ++i) {
       const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (off + i)]);
       L.A[i][lane] = (W)m.x;
       L.S[i][lane] = (W)m.y;
     }
+  }
   const int ncl = valid && clique_min<K>() ? clique_partition<W>(&L.A[0][lane], 32, n, &L.cl[0][lane], 32,
                                                                   clique_min<K>())
                                            : 0;
@@ -599,8 +653,10 @@ __device__ __forceinline__ void lane_component(const GraphView& g, const Workspa
   int best_cost = 0;
   bool trunc = false;
   const unsigned steps = lane_dfs<K, W, N>(L, lane, valid, n, w_stitch, budget, ncl, bestC, best_cost, trunc);
+  if (kStaged) warp_stage<W, N, true>(w, L, lane, has, valid, off, n);
   if (!valid) return;
-  for (int i = 0; i < n; ++i) colors[__ldcg(&w.porder[off + i])] = colour_of<K, W>(bestC, i);
+  for (int i = 0; i < n; ++i)
+    colors[kStaged ? L.pk[i][lane] : __ldcg(&w.porder[off + i])] = colour_of<K, W>(bestC, i);
   if (trunc && exact) {
     light_handoff(g, w, ci, n, best_cost);
   } else {
@@ -614,7 +670,7 @@ __device__ __forceinline__ void lane_component(const GraphView& g, const Workspa
       nc >>= 1;
       ns >>= 1;
       if (nc | ns) {
-        const int l = layout_of(g, __ldcg(&w.porder[off]));
+        const int l = layout_of(g, kStaged ? L.pk[0][lane] : __ldcg(&w.porder[off]));
         if (nc) atomicAdd((unsigned long long*)&counts[2 * l], (unsigned long long)nc);
         if (ns) atomicAdd((unsigned long long*)&counts[2 * l + 1], (unsigned long long)ns);
       }
@@ -682,8 +738,8 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
       base = __shfl_sync(0xffffffffu, base, 0);
       if (wide) w.wide[base + __popc(wm & lanemask_lt())] = ci;
     }
-    lane_component<K, unsigned, 32>(g, w, L, lane, mine_c && n <= 32, ci, rec, w_stitch, budget, exact, colors,
-                                    counts, acc);
+    lane_component<K, unsigned, 32, kStagedLight>(g, w, L, lane, ci < n_comp, mine_c && n <= 32, ci, rec, w_stitch,
+                                                  budget, exact, colors, counts, acc);
     __syncwarp();
   }
   light_stats(ctl, acc);
@@ -708,8 +764,8 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_wide(GraphView g, 
     const int j = b * 32 + lane;
     const int ci = j < n_wide ? __ldcg(&w.wide[j]) : -1;
     const unsigned long long rec = ci >= 0 ? __ldcg(&w.crec[ci]) : 0ull;
-    lane_component<K, unsigned long long, kMaxComp>(g, w, L, lane, ci >= 0, ci, rec, w_stitch, budget, exact,
-                                                    colors, counts, acc);
+    lane_component<K, unsigned long long, kMaxComp, false>(g, w, L, lane, ci >= 0, ci >= 0, ci, rec, w_stitch,
+                                                           budget, exact, colors, counts, acc);
     __syncwarp();
   }
   acc.comps = 0;  // counted by the kernel that listed them
@@ -844,17 +900,39 @@ __device__ __forceinline__ int warp_min_key(int& c, Path& p) {
 }
 
 // Frames of the lanes in shared memory, [field][depth][lane] (a lane only
-// touches its own column: conflict-free).  A frame is the node N_d at which
-// column v_d was selected: its masks B and U (so a frame can be handed to
-// another lane without replaying its path), its cost, and v | (c+1) << 8 |
-// (maxused+1) << 16 | lim << 24 (current child c, child limit lim of R6).
+// touches its own column: conflict-free).  Frame d is the node N_d at which
+// column v_d was selected: saved = B[c] before its current child r(v_d, c)
+// was selected, the node's cost, and v | (c+1) << 8 | (maxused+1) << 16 |
+// lim << 24 (current child c, child limit lim of R6).  The masks of N_j (for
+// a donation or a spill) are rebuilt from the lane's current state by undoing
+// the frames below j (node_at); the deepest frame lives in registers.
 template <int K, typename W, int D>
 struct LaneFrames {
-  W B[K][D][32];
-  W U[D][32];
+  W saved[D][32];
   int cost[D][32];
   int pk[D][32];
 };
+
+// B, C and U at N_j from the lane's state at depth `depth` (frames j..depth-2
+// in shared memory, frame depth-1 in registers: f_saved, f_v, f_c): undo the
+// selected rows of frames depth-1 down to j, uncover their columns.
+template <int K, typename W, int D>
+__device__ __forceinline__ void node_at(int j, int depth, const W (&B)[K], const W (&C)[K], W U, W f_saved, int f_v,
+                                        int f_c, const LaneFrames<K, W, D>& F, int lane, W (&jB)[K], W (&jC)[K],
+                                        W& jU) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) jB[c] = B[c];
+  W bits = W(1) << f_v;
+  if (f_c >= 0) put<K, W>(jB, f_c, f_saved);
+  for (int d = depth - 2; d >= j; --d) {  // frames above the deepest always have a selected child
+    const int pk = F.pk[d][lane];
+    bits |= W(1) << (pk & 0xff);
+    put<K, W>(jB, ((pk >> 8) & 0xff) - 1, F.saved[d][lane]);
+  }
+  jU = U | bits;
+#pragma unroll
+  for (int c = 0; c < K; ++c) jC[c] = C[c] & ~bits;
+}
 
 template <int K, typename W>
 __host__ __device__ constexpr int heavy_depth() {
@@ -926,9 +1004,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
   }
   int cost = scost, maxused = smu, depth = sdepth, d0 = sdepth;
   bool active = lane == 0, enter = lane == 0;
-  W fB[K], fU = 0, f_adj = 0, f_sadj = 0;
-#pragma unroll
-  for (int c = 0; c < K; ++c) fB[c] = 0;
+  W f_saved = 0, f_adj = 0, f_sadj = 0;
   int f_cost = 0, f_v = 0, f_c = -1, f_mu = -1, f_lim = 0;
   Path P = sP;
   unsigned long long open = 0ull;
@@ -966,17 +1042,12 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           const int j = __ffsll((long long)(open & donatable)) - 1;
           int pk, jc;
           W jU;
+          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, F, lane, xB, xC, jU);
           if (j == depth - 1) {
-#pragma unroll
-            for (int c = 0; c < K; ++c) xB[c] = fB[c];
-            jU = fU;
             jc = f_cost;
             pk = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
             f_lim -= 1;
           } else {
-#pragma unroll
-            for (int c = 0; c < K; ++c) xB[c] = F.B[c][j][lane];
-            jU = F.U[j][lane];
             jc = F.cost[j][lane];
             pk = F.pk[j][lane];
             F.pk[j][lane] = pk - (1 << 24);
@@ -986,8 +1057,6 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           const W bit = W(1) << v;
           const W a = adj[v], sa = sadj[v];
           xU = jU & ~bit;
-#pragma unroll
-          for (int c = 0; c < K; ++c) xC[c] = C[c] & ~jU;
           const W Cc = pick<K, W>(xC, lim);
           xcost = jc + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~xU & ~Cc);
           put<K, W>(xC, lim, Cc | bit);
@@ -1057,16 +1126,11 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       const int v = ex ? O::ffs(Z ? Z : (Ol ? Ol : U)) : 0;  // Alg. 1 line 8 (R5)
       if (ex && depth > d0) {  // spill the parent frame
         const int d = depth - 1;
-#pragma unroll
-        for (int c = 0; c < K; ++c) F.B[c][d][lane] = fB[c];
-        F.U[d][lane] = fU;
+        F.saved[d][lane] = f_saved;
         F.cost[d][lane] = f_cost;
         F.pk[d][lane] = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
       }
       const W av = adj[v], sav = sadj[v];
-#pragma unroll
-      for (int c = 0; c < K; ++c) fB[c] = ex ? B[c] : fB[c];
-      fU = ex ? U : fU;
       f_cost = ex ? cost : f_cost;
       f_v = ex ? v : f_v;
       f_c = ex ? -1 : f_c;
@@ -1086,7 +1150,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       for (int c = 0; c < K; ++c) {
         const bool mine_c = unc && c == f_c;
         C[c] = mine_c ? (C[c] & ~bit) : C[c];
-        B[c] = mine_c ? fB[c] : B[c];
+        B[c] = mine_c ? f_saved : B[c];
       }
       const int c = f_c + 1;
       const int fd = depth - 1;
@@ -1095,6 +1159,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       // next child: select r(v,c) (line 14), cover its secondary columns (line 15)
       const int cc = min(c, K - 1);
       const W Cc = pick<K, W>(C, cc);
+      const W Bc = pick<K, W>(B, cc);
       const int ncost = f_cost + kCostUnits * O::popc(f_adj & Cc) + w_stitch * O::popc(f_sadj & ~U & ~Cc);
 #pragma unroll
       for (int q = 0; q < K; ++q) {
@@ -1102,6 +1167,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
         C[q] = sel ? (C[q] | bit) : C[q];
         B[q] = sel ? (B[q] | f_adj) : B[q];
       }
+      f_saved = nxt ? Bc : f_saved;
       cost = nxt ? ncost : cost;
       maxused = nxt ? max(f_mu, c) : maxused;
       if (adv) path_put<kTwo>(P, max(fd, 0), nxt ? c : 0);
@@ -1111,16 +1177,11 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       U = exh ? (U | bit) : U;
       const bool pop = exh && fd > d0;
       const int pd = max(fd - 1, 0);
-      W pB[K];
-#pragma unroll
-      for (int q = 0; q < K; ++q) pB[q] = F.B[q][pd][lane];
-      const W pU = F.U[pd][lane];
+      const W ps = F.saved[pd][lane];
       const int pc = F.cost[pd][lane], ppk = F.pk[pd][lane];
       const int pv = pop ? (ppk & 0xff) : f_v;
       const W pa = adj[pv], psa = sadj[pv];
-#pragma unroll
-      for (int q = 0; q < K; ++q) fB[q] = pop ? pB[q] : fB[q];
-      fU = pop ? pU : fU;
+      f_saved = pop ? ps : f_saved;
       f_cost = pop ? pc : f_cost;
       f_v = pv;
       f_c = pop ? ((ppk >> 8) & 0xff) - 1 : (nxt ? c : f_c);
@@ -1203,19 +1264,14 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           WorkItem* q = w.wq + (size_t)u.cls * kWQCap;
           unsigned* qf = w.wq_flag + (size_t)u.cls * kWQCap;
           int at = base + excl;
-          W jB[K], jU;
+          W jB[K], jC[K], jU;
           int pk, jc;
+          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, F, lane, jB, jC, jU);
           if (j == depth - 1) {
-#pragma unroll
-            for (int c = 0; c < K; ++c) jB[c] = fB[c];
-            jU = fU;
             jc = f_cost;
             pk = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
             f_lim = f_c;  // its children are in the queue now
           } else {
-#pragma unroll
-            for (int c = 0; c < K; ++c) jB[c] = F.B[c][j][lane];
-            jU = F.U[j][lane];
             jc = F.cost[j][lane];
             pk = F.pk[j][lane];
             F.pk[j][lane] = (pk & 0x00ffffff) | ((((pk >> 8) & 0xff) - 1) << 24);
@@ -1228,7 +1284,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
             W xC[K], xB[K];
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-              xC[c] = C[c] & ~jU;
+              xC[c] = jC[c];
               xB[c] = jB[c];
             }
             const W xU = jU & ~bit;
@@ -1314,7 +1370,8 @@ __device__ int warp_greedy_seed(const W* adj, const W* sadj, int n, int w_stitch
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       const int c = (i + off) % K;
-      const int cc = kCostUnits * O::popc(a & C[c]) + w_stitch * O::popc(sa & ~U & ~C[c]);
+      const W Cc = pick<K, W>(C, c);
+      const int cc = kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~U & ~Cc);
       if (cc < bcost) {
         bcost = cc;
         bc = c;
