@@ -104,7 +104,9 @@ enum mpld_stat {
   MPLD_STAT_ERROR = 6,      /* device-side error bits (1 = graph, 2 = component too large) */
   MPLD_STAT_LAUNCHES = 7,   /* kernels launched by the call */
   MPLD_STAT_MAX_STEPS = 8,  /* largest per-component step count */
-  MPLD_STAT_LEN = 9
+  MPLD_STAT_SPILL_REFUSED = 9, /* exact mode: spills of open search work refused (work ring full or no
+                                * component slot left; the unit went on alone — a slowdown, not an error) */
+  MPLD_STAT_LEN = 10
 };
 
 /* Last error message of the calling thread ("" if none). */

@@ -1245,9 +1245,9 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
               u.slot = sl;
             }
           }
-          if (u.slot >= 0) {
+          if (u.slot >= 0) {  // reserve tot ring positions while the ring has room (items not yet read)
             int t = *(volatile int*)&w.ctl->wq_tail[u.cls];
-            while (t + tot <= kWQCap) {
+            while (t + tot - *(volatile int*)&w.ctl->wq_read[u.cls] <= kWQCap) {
               const int o = atomicCAS(&w.ctl->wq_tail[u.cls], t, t + tot);
               if (o == t) {
                 base = t;
@@ -1257,12 +1257,13 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
             }
             if (base >= 0) atomicAdd(&w.hslot[u.slot].pend, tot);  // before any item is published
           }
+          if (base < 0) atomicAdd(&w.ctl->spill_refused, 1);  // ring full or no slot: this unit goes on alone
         }
         u.slot = __shfl_sync(0xffffffffu, u.slot, 0);
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= 0 && cnt > 0) {
           WorkItem* q = w.wq + (size_t)u.cls * kWQCap;
-          unsigned* qf = w.wq_flag + (size_t)u.cls * kWQCap;
+          unsigned long long* qf = w.wq_flag + (size_t)u.cls * kWQCap;
           int at = base + excl;
           W jB[K], jC[K], jU;
           int pk, jc;
@@ -1294,7 +1295,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
             put<K, W>(xB, ch, pick<K, W>(xB, ch) | a);
             Path xP = path_prefix<kTwo>(P, j);
             path_put<kTwo>(xP, j, ch);
-            WorkItem& it = q[at];
+            WorkItem& it = q[at & (kWQCap - 1)];
             it.slot = u.slot;
             it.depth = j + 1;
             it.cost = xcost;
@@ -1308,7 +1309,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
             }
             it.U = (unsigned long long)xU;
             __threadfence();
-            *(volatile unsigned*)&qf[at] = w.epoch;
+            *(volatile unsigned long long*)&qf[at & (kWQCap - 1)] = wq_tag(w.epoch, at);
             ++at;
           }
         }
@@ -1520,185 +1521,242 @@ __device__ void heavy_load(const Workspace& w, size_t off, int n, W* s_adj, W* s
   __syncwarp();
 }
 
-// One warp per heavy component of one word class: W = 32-bit words for
-// components of <= 32 vertices, 64-bit words for larger ones (each class gets
-// its own launch with its own shared-memory size).  Warps take heavy
-// components first, then spilled work items, until every unit is done.
+// The units of the warp-parallel search: a heavy component (its light leaf or
+// a cheaper greedy colouring as the starting incumbent), or a spilled work
+// item.  W = 32-bit words for components of <= 32 vertices, 64-bit words for
+// larger ones; both word classes share the warp's shared memory (sized for
+// the 64-bit class).
+struct HeavyAcc {
+  unsigned long long steps = 0ull;
+  int max = 0, capped = 0;
+};
+
 template <int K, typename W>
+__device__ void heavy_component(const GraphView& g, const Workspace& w, int h, int w_stitch, int* colors,
+                                long long* counts, unsigned char* smem, int* s_pair, int& cur_ci, int& cur_ncl,
+                                HeavyAcc& acc) {
+  constexpr int cls = sizeof(W) == 4 ? 0 : 1;
+  constexpr bool kTwo = sizeof(W) == 8;
+  const int lane = threadIdx.x & 31;
+  W* s_adj = (W*)smem;
+  W* s_sadj = s_adj + kMaxComp;
+  W* s_cl = s_sadj + kMaxComp;
+  HeavyUnit<K, W> u;
+  u.w_stitch = w_stitch;
+  u.cls = cls;
+  u.adj = s_adj;
+  u.sadj = s_sadj;
+  u.cl = s_cl;
+  u.F = (LaneFrames<K, W, heavy_depth<K, W>()>*)(smem + 3 * kMaxComp * sizeof(unsigned long long));
+  u.pair = s_pair;
+  const int idx = cls ? g.n - 1 - h : h;
+  u.ci = __ldcg(&w.hcomp[idx]);
+  const unsigned long long rec = __ldcg(&w.crec[u.ci]);
+  const size_t off = (size_t)(rec >> 8);
+  u.n = (int)(rec & 0xffull);
+  u.c1 = __ldcg(&w.hcost[idx]);
+  u.slot = -1;
+  heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, colors, u.col);
+  cur_ci = u.ci;
+  cur_ncl = u.ncl;
+  int lc = 0;  // == c1
+  u.p1 = leaf_path<K, W>(u.col, u.n, s_adj, s_sadj, w_stitch, lc);
+  int gcost = u.c1;
+  Path gP = u.p1;
+  u.hc = u.c1;
+  if (kSeedIncumbent) {  // a cheaper greedy colouring: (its cost, maximal path) is a valid incumbent key
+    const int hc = warp_greedy_seed<K, W>(s_adj, s_sadj, u.n, w_stitch, (unsigned)u.ci);
+    if (hc < u.c1) {
+      u.hc = hc;
+      gcost = hc;
+      gP = Path{~0ull, ~0ull};
+    }
+  }
+  W zero[K], bestC[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) zero[c] = 0;
+  bool mine, capped, spilled;
+  unsigned steps;
+  warp_heavy_search<K, W>(u, w, zero, zero, WordOps<W>::full(u.n), 0, -1, Path{0ull, 0ull}, 0, gcost, gP, mine,
+                          bestC, steps, capped, spilled);
+  const int* porder = w.porder + off;
+  if (u.slot < 0) {  // searched whole: the final colouring is the warp's best (or the light leaf)
+    W fin[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) fin[c] = u.col[c];
+    const unsigned owner = __ballot_sync(0xffffffffu, mine);
+    if (owner && key_less<kTwo>(gcost, gP, u.c1, u.p1)) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) fin[c] = __shfl_sync(0xffffffffu, bestC[c], __ffs(owner) - 1);
+      for (int i = lane; i < u.n; i += 32) colors[__ldcg(&porder[i])] = colour_of<K, W>(fin, i);
+    }
+    heavy_counts<K, W>(g, s_adj, s_sadj, u.n, fin, __ldcg(&porder[0]), counts);
+  } else {
+    heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, porder, colors, counts);
+  }
+  acc.steps += steps;
+  acc.max = max(acc.max, (int)min(steps, (unsigned)INT_MAX));
+  acc.capped += capped ? 1 : 0;  // per unit (a spilled component may count more than once)
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(&w.ctl->wq_done[cls], 1);
+  }
+}
+
+template <int K, typename W>
+__device__ void heavy_item(const GraphView& g, const Workspace& w, int pos, int w_stitch, int* colors,
+                           long long* counts, unsigned char* smem, int* s_pair, int& cur_ci, int& cur_ncl,
+                           HeavyAcc& acc) {
+  constexpr int cls = sizeof(W) == 4 ? 0 : 1;
+  const int lane = threadIdx.x & 31;
+  W* s_adj = (W*)smem;
+  W* s_sadj = s_adj + kMaxComp;
+  W* s_cl = s_sadj + kMaxComp;
+  HeavyUnit<K, W> u;
+  u.w_stitch = w_stitch;
+  u.cls = cls;
+  u.adj = s_adj;
+  u.sadj = s_sadj;
+  u.cl = s_cl;
+  u.F = (LaneFrames<K, W, heavy_depth<K, W>()>*)(smem + 3 * kMaxComp * sizeof(unsigned long long));
+  u.pair = s_pair;
+  u.hc = INT_MAX;
+  const WorkItem* q = w.wq + (size_t)cls * kWQCap + (pos & (kWQCap - 1));
+  u.slot = __ldcg(&q->slot);
+  HeavySlot* hs = &w.hslot[u.slot];
+  u.ci = __ldcg(&hs->ci);
+  const unsigned long long rec = __ldcg(&w.crec[u.ci]);
+  const size_t off = (size_t)(rec >> 8);
+  u.n = (int)(rec & 0xffull);
+  W sC[K], sB[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    sC[c] = (W)__ldcg(&q->C[c]);
+    sB[c] = (W)__ldcg(&q->B[c]);
+  }
+  const Path sP = {__ldcg(&q->pa), __ldcg(&q->pb)};
+  const W sU = (W)__ldcg(&q->U);
+  const int scost = __ldcg(&q->cost), smu = __ldcg(&q->mu), sdepth = __ldcg(&q->depth);
+  __syncwarp();
+  if (lane == 0) {  // the ring slot may be reused from now on
+    __threadfence();
+    atomicAdd(&w.ctl->wq_read[cls], 1);
+  }
+  if (u.ci != cur_ci) {  // items of one component mostly follow each other: keep its masks
+    heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, nullptr, u.col);
+    cur_ci = u.ci;
+    cur_ncl = u.ncl;
+  }
+  u.ncl = cur_ncl;
+  // the best cost known as the starting incumbent, (bcost, max path): a valid
+  // key no smaller than the slot's
+  int sc = 0;
+  if (lane == 0) sc = *(volatile int*)&hs->bcost;
+  int gcost = __shfl_sync(0xffffffffu, sc, 0);
+  Path gP = Path{~0ull, ~0ull};
+  W bestC[K];
+  bool mine, capped, spilled;
+  unsigned steps;
+  warp_heavy_search<K, W>(u, w, sC, sB, sU, scost, smu, sP, sdepth, gcost, gP, mine, bestC, steps, capped, spilled);
+  heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, w.porder + off, colors, counts);
+  acc.steps += steps;
+  acc.capped += capped ? 1 : 0;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(&w.ctl->wq_done[cls], 1);
+  }
+}
+
+// One warp per heavy component, both word classes in one launch: the 64-bit
+// class first (the longest searches), then the 32-bit class, then spilled
+// work items of either class (a warp claims a ring position only once a
+// producer has reserved it, so no warp waits on one class while the other
+// has work), until every unit of both classes is done.
+template <int K>
 __global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
                                                                     int* colors, long long* counts) {
   pdl_begin();
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int cls = sizeof(W) == 4 ? 0 : 1;
-  constexpr bool kTwo = sizeof(W) == 8;
   __shared__ int s_pair[32];
   const int lane = threadIdx.x & 31;
   Control* ctl = w.ctl;
-  const int n_heavy = __ldcg(&ctl->n_heavy[cls]);
-  W* s_adj = (W*)smem;
-  W* s_sadj = s_adj + kMaxComp;
-  W* s_cl = s_sadj + kMaxComp;
-  auto* F = (LaneFrames<K, W, heavy_depth<K, W>()>*)(smem + 3 * kMaxComp * sizeof(W));
-  unsigned long long acc_steps = 0ull;
-  int acc_max = 0, acc_capped = 0;
-  bool comps_left = n_heavy > 0;
-  unsigned backoff = 64;
+  const int n_heavy0 = __ldcg(&ctl->n_heavy[0]), n_heavy1 = __ldcg(&ctl->n_heavy[1]);
+  HeavyAcc acc;
   int cur_ci = -1, cur_ncl = 0;  // the component whose masks are in shared memory
-  int ticket = -1;               // this warp's queue position (-1: none taken)
-  unsigned polls = 0;
+  while (true) {  // the 64-bit class first (the longest searches)
+    int h = 0;
+    if (lane == 0) h = atomicAdd(&ctl->heavy_next[1], 1);
+    h = __shfl_sync(0xffffffffu, h, 0);
+    if (h >= n_heavy1) break;
+    heavy_component<K, unsigned long long>(g, w, h, w_stitch, colors, counts, smem, s_pair, cur_ci, cur_ncl, acc);
+  }
   while (true) {
-    HeavyUnit<K, W> u;
-    u.w_stitch = w_stitch;
-    u.cls = cls;
-    u.adj = s_adj;
-    u.sadj = s_sadj;
-    u.cl = s_cl;
-    u.F = F;
-    u.pair = s_pair;
-    int gcost;
-    Path gP;
-    bool mine, capped, spilled;
-    unsigned steps;
-    W bestC[K];
-    if (comps_left) {  // a heavy component: the light leaf is the starting incumbent
-      int h = 0;
-      if (lane == 0) h = atomicAdd(&ctl->heavy_next[cls], 1);
-      h = __shfl_sync(0xffffffffu, h, 0);
-      if (h < n_heavy) {
-        const int idx = cls ? g.n - 1 - h : h;
-        u.ci = __ldcg(&w.hcomp[idx]);
-        const unsigned long long rec = __ldcg(&w.crec[u.ci]);
-        const size_t off = (size_t)(rec >> 8);
-        u.n = (int)(rec & 0xffull);
-        u.c1 = __ldcg(&w.hcost[idx]);
-        u.slot = -1;
-        heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, colors, u.col);
-        cur_ci = u.ci;
-        cur_ncl = u.ncl;
-        int lc = 0;  // == c1
-        u.p1 = leaf_path<K, W>(u.col, u.n, s_adj, s_sadj, w_stitch, lc);
-        gcost = u.c1;
-        gP = u.p1;
-        u.hc = u.c1;
-        if (kSeedIncumbent) {  // a cheaper greedy colouring: (its cost, maximal path) is a valid incumbent key
-          const int hc = warp_greedy_seed<K, W>(s_adj, s_sadj, u.n, w_stitch, (unsigned)u.ci);
-          if (hc < u.c1) {
-            u.hc = hc;
-            gcost = hc;
-            gP = Path{~0ull, ~0ull};
-          }
-        }
-        W zero[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) zero[c] = 0;
-        warp_heavy_search<K, W>(u, w, zero, zero, WordOps<W>::full(u.n), 0, -1, Path{0ull, 0ull}, 0, gcost, gP,
-                                mine, bestC, steps, capped, spilled);
-        const int* porder = w.porder + off;
-        if (u.slot < 0) {  // searched whole: the final colouring is the warp's best (or the light leaf)
-          W fin[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) fin[c] = u.col[c];
-          const unsigned owner = __ballot_sync(0xffffffffu, mine);
-          if (owner && key_less<kTwo>(gcost, gP, u.c1, u.p1)) {
-#pragma unroll
-            for (int c = 0; c < K; ++c) fin[c] = __shfl_sync(0xffffffffu, bestC[c], __ffs(owner) - 1);
-            for (int i = lane; i < u.n; i += 32) colors[__ldcg(&porder[i])] = colour_of<K, W>(fin, i);
-          }
-          heavy_counts<K, W>(g, s_adj, s_sadj, u.n, fin, __ldcg(&porder[0]), counts);
-        } else {
-          heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, porder, colors, counts);
-        }
-        acc_steps += steps;
-        acc_max = max(acc_max, (int)min(steps, (unsigned)INT_MAX));
-        acc_capped += capped ? 1 : 0;  // per unit (a spilled component may count more than once)
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(&ctl->wq_done[cls], 1);
-        }
-        continue;
-      }
-      comps_left = false;
-    }
-    // a spilled work item: take a ticket (one position of the queue) and wait
-    // for its item, or for the end of all work if it never comes
-    if (ticket < 0) {
-      // no component left: stay for spilled work only if some may come (small
-      // components never run long; a spill without helpers is still drained
-      // by the warps that are running, the spilling one included)
-      int leave = 0;
-      if (lane == 0)
-        leave = *(volatile int*)&ctl->may_spill == 0 && *(volatile int*)&ctl->wq_tail[cls] == 0;
-      if (__shfl_sync(0xffffffffu, leave, 0)) break;
-      if (lane == 0) ticket = atomicAdd(&ctl->wq_head[cls], 1);
-      ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    }
-    int it = -1;
+    int h = 0;
+    if (lane == 0) h = atomicAdd(&ctl->heavy_next[0], 1);
+    h = __shfl_sync(0xffffffffu, h, 0);
+    if (h >= n_heavy0) break;
+    heavy_component<K, unsigned>(g, w, h, w_stitch, colors, counts, smem, s_pair, cur_ci, cur_ncl, acc);
+  }
+  // no component left: stay for spilled work only if some may come (small
+  // components never run long; a spill without helpers is still drained by the
+  // warps that are running, the spilling one included)
+  int leave = 0;
+  if (lane == 0)
+    leave = *(volatile int*)&ctl->may_spill == 0 && *(volatile int*)&ctl->wq_tail[0] == 0 &&
+            *(volatile int*)&ctl->wq_tail[1] == 0;
+  unsigned backoff = 32, polls = 0;
+  while (!__shfl_sync(0xffffffffu, leave, 0)) {
+    int pos = -1, pcls = 0;
     if (lane == 0) {
-      if (ticket < kWQCap && *(volatile unsigned*)&w.wq_flag[(size_t)cls * kWQCap + ticket] == w.epoch) it = ticket;
-    }
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= 0) {
-      backoff = 64;
-      ticket = -1;
-      __syncwarp();
-      __threadfence();
-      const WorkItem* q = w.wq + (size_t)cls * kWQCap + it;
-      u.slot = __ldcg(&q->slot);
-      HeavySlot* hs = &w.hslot[u.slot];
-      u.ci = __ldcg(&hs->ci);
-      const unsigned long long rec = __ldcg(&w.crec[u.ci]);
-      const size_t off = (size_t)(rec >> 8);
-      u.n = (int)(rec & 0xffull);
-      if (u.ci != cur_ci) {  // items of one component mostly follow each other: keep its masks
-        heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, nullptr, u.col);
-        cur_ci = u.ci;
-        cur_ncl = u.ncl;
+      for (int c = 1; c >= 0 && pos < 0; --c) {  // claim a reserved position (64-bit class first)
+        int hd = *(volatile int*)&ctl->wq_head[c];
+        while (hd < *(volatile int*)&ctl->wq_tail[c]) {
+          const int o = atomicCAS(&ctl->wq_head[c], hd, hd + 1);
+          if (o == hd) {
+            pos = hd;
+            pcls = c;
+            break;
+          }
+          hd = o;
+        }
       }
-      u.ncl = cur_ncl;
-      W sC[K], sB[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        sC[c] = (W)__ldcg(&q->C[c]);
-        sB[c] = (W)__ldcg(&q->B[c]);
-      }
-      const Path sP = {__ldcg(&q->pa), __ldcg(&q->pb)};
-      // the best cost known as the starting incumbent, (bcost, max path): a
-      // valid key no smaller than the slot's
-      int sc = 0;
-      if (lane == 0) sc = *(volatile int*)&hs->bcost;
-      gcost = __shfl_sync(0xffffffffu, sc, 0);
-      gP = Path{~0ull, ~0ull};
-      warp_heavy_search<K, W>(u, w, sC, sB, (W)__ldcg(&q->U), __ldcg(&q->cost), __ldcg(&q->mu), sP,
-                              __ldcg(&q->depth), gcost, gP, mine, bestC, steps, capped, spilled);
-      heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, w.porder + off, colors, counts);
-      acc_steps += steps;
-      acc_capped += capped ? 1 : 0;
-      __syncwarp();
-      if (lane == 0) {
+      if (pos >= 0) {  // its producer publishes the item right after reserving it
+        const unsigned long long tag = wq_tag(w.epoch, pos);
+        const volatile unsigned long long* f = &w.wq_flag[(size_t)pcls * kWQCap + (pos & (kWQCap - 1))];
+        while (*f != tag) __nanosleep(20);
         __threadfence();
-        atomicAdd(&ctl->wq_done[cls], 1);
       }
+    }
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    pcls = __shfl_sync(0xffffffffu, pcls, 0);
+    if (pos >= 0) {
+      backoff = 32;
+      if (pcls)
+        heavy_item<K, unsigned long long>(g, w, pos, w_stitch, colors, counts, smem, s_pair, cur_ci, cur_ncl, acc);
+      else
+        heavy_item<K, unsigned>(g, w, pos, w_stitch, colors, counts, smem, s_pair, cur_ci, cur_ncl, acc);
       continue;
     }
-    // done when every unit (heavy components + items) has finished: no unit
-    // is running, so no item can be added and this ticket stays empty
-    int fin = 0;
-    if (lane == 0 && (++polls & 3) == 0) {  // the ticket's flag every poll, the end of all work every 4th
-      const int d = *(volatile int*)&ctl->wq_done[cls];
+    // done when every unit (heavy components + items) of both classes has
+    // finished: no unit is running, so no item can be added
+    if (lane == 0 && (++polls & 3) == 0) {
+      const int d0 = *(volatile int*)&ctl->wq_done[0], d1 = *(volatile int*)&ctl->wq_done[1];
       __threadfence();
-      const int t = *(volatile int*)&ctl->wq_tail[cls];
-      fin = d >= n_heavy + t && ticket >= t;
+      const int t0 = *(volatile int*)&ctl->wq_tail[0], t1 = *(volatile int*)&ctl->wq_tail[1];
+      leave = d0 >= n_heavy0 + t0 && d1 >= n_heavy1 + t1;
     }
-    if (__shfl_sync(0xffffffffu, fin, 0)) break;
-    __nanosleep(backoff);
-    backoff = min(backoff * 2u, (unsigned)MPLD_POLL_CAP);
+    if (!__shfl_sync(0xffffffffu, leave, 0)) {
+      __nanosleep(backoff);
+      backoff = min(backoff * 2u, (unsigned)MPLD_POLL_CAP);
+    }
   }
-  if (lane == 0 && acc_steps) {
-    atomicAdd(&ctl->steps, acc_steps);
-    atomicMax(&ctl->max_steps_comp, acc_max);
+  if (lane == 0 && acc.steps) {
+    atomicAdd(&ctl->steps, acc.steps);
+    atomicMax(&ctl->max_steps_comp, acc.max);
   }
-  if (lane == 0 && acc_capped) atomicAdd(&ctl->truncated, acc_capped);
+  if (lane == 0 && acc.capped) atomicAdd(&ctl->truncated, acc.capped);
 }
 
 }  // namespace
@@ -1844,46 +1902,44 @@ cudaError_t configure_search_wide(int num_sms, int* blocks) {
   return e;
 }
 
-template <int K>
-cudaError_t launch_heavy_k(const GraphView& g, Workspace ws, int w_stitch, int* colors, long long* counts,
-                           cudaStream_t s, const int* blocks, bool pdl) {
-  cudaError_t e = launch_ex(mpld_exact_cover_search_heavy<K, unsigned>, dim3(blocks[0]), dim3(32),
-                            heavy_smem<K, unsigned>(), s, pdl, false, g, ws, w_stitch, colors, counts);
-  if (e != cudaSuccess) return e;
-  return launch_ex(mpld_exact_cover_search_heavy<K, unsigned long long>, dim3(blocks[1]), dim3(32),
-                   heavy_smem<K, unsigned long long>(), s, true, false, g, ws, w_stitch, colors, counts);
+constexpr size_t heavy_smem_all(int k) {
+  // masks + clique words (64-bit) and the frames of the 64-bit class (the 32-bit class needs less)
+  return 3 * kMaxComp * sizeof(unsigned long long) +
+         (k == 2 ? sizeof(LaneFrames<2, unsigned long long, 64>)
+                 : (k == 3 ? sizeof(LaneFrames<3, unsigned long long, 64>) : sizeof(LaneFrames<4, unsigned long long, 64>)));
 }
+static_assert(sizeof(LaneFrames<4, unsigned, 32>) <= sizeof(LaneFrames<4, unsigned long long, 64>),
+              "the 32-bit class fits the shared memory of the 64-bit class");
 
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, long long* counts,
                                 cudaStream_t s, const int* blocks, bool pdl) {
   switch (k) {
-    case 2: return launch_heavy_k<2>(g, ws, w_stitch, colors, counts, s, blocks + 0, pdl);
-    case 3: return launch_heavy_k<3>(g, ws, w_stitch, colors, counts, s, blocks + 2, pdl);
-    case 4: return launch_heavy_k<4>(g, ws, w_stitch, colors, counts, s, blocks + 4, pdl);
+    case 2: return launch_ex(mpld_exact_cover_search_heavy<2>, dim3(blocks[0]), dim3(32), heavy_smem_all(2), s, pdl,
+                             false, g, ws, w_stitch, colors, counts);
+    case 3: return launch_ex(mpld_exact_cover_search_heavy<3>, dim3(blocks[1]), dim3(32), heavy_smem_all(3), s, pdl,
+                             false, g, ws, w_stitch, colors, counts);
+    case 4: return launch_ex(mpld_exact_cover_search_heavy<4>, dim3(blocks[2]), dim3(32), heavy_smem_all(4), s, pdl,
+                             false, g, ws, w_stitch, colors, counts);
     default: return cudaErrorInvalidValue;
   }
 }
 
-template <int K, typename W>
-cudaError_t configure_heavy_kw(int num_sms, int* blocks) {
-  const cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<K, W>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem<K, W>());
+template <int K>
+cudaError_t configure_heavy_k(int num_sms, int* blocks) {
+  const cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<K>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem_all(K));
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search_heavy<K, W>, 32, heavy_smem<K, W>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search_heavy<K>, 32, heavy_smem_all(K));
   *blocks = per_sm * num_sms;
   return cudaSuccess;
 }
 
-// sets the shared-memory limits of the six heavy kernels and their resident grid sizes
-// blocks[2 * (k - 2) + cls]
+// sets the shared-memory limits of the heavy kernels and their resident grid sizes blocks[k - 2]
 cudaError_t configure_search_heavy(int num_sms, int* blocks) {
-  cudaError_t e = configure_heavy_kw<2, unsigned>(num_sms, blocks + 0);
-  if (e == cudaSuccess) e = configure_heavy_kw<2, unsigned long long>(num_sms, blocks + 1);
-  if (e == cudaSuccess) e = configure_heavy_kw<3, unsigned>(num_sms, blocks + 2);
-  if (e == cudaSuccess) e = configure_heavy_kw<3, unsigned long long>(num_sms, blocks + 3);
-  if (e == cudaSuccess) e = configure_heavy_kw<4, unsigned>(num_sms, blocks + 4);
-  if (e == cudaSuccess) e = configure_heavy_kw<4, unsigned long long>(num_sms, blocks + 5);
+  cudaError_t e = configure_heavy_k<2>(num_sms, blocks + 0);
+  if (e == cudaSuccess) e = configure_heavy_k<3>(num_sms, blocks + 1);
+  if (e == cudaSuccess) e = configure_heavy_k<4>(num_sms, blocks + 2);
   return e;
 }
 

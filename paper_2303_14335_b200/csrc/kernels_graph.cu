@@ -827,6 +827,7 @@ __device__ void finalize_outputs(const GraphView& g, const Workspace& w, const O
     out.stats[MPLD_STAT_ERROR] = __ldcg(&ctl->err);
     out.stats[MPLD_STAT_LAUNCHES] = out.launches;
     out.stats[MPLD_STAT_MAX_STEPS] = __ldcg(&ctl->max_steps_comp);
+    out.stats[MPLD_STAT_SPILL_REFUSED] = __ldcg(&ctl->spill_refused);
   }
 }
 

@@ -110,7 +110,7 @@ struct mpld_context {
   int* hcost = nullptr;
   int* wide = nullptr;
   WorkItem* wq = nullptr;     // spilled heavy-search work (fixed size)
-  unsigned* wq_flag = nullptr;
+  unsigned long long* wq_flag = nullptr;
   HeavySlot* hslot = nullptr;
   unsigned long long* est = nullptr;   // sharded search: cost-balanced partition (cap_n)
   unsigned long long* bsum = nullptr;
@@ -125,7 +125,7 @@ struct mpld_context {
   int call_launches = 0;
   unsigned light_steps = kLightStepsDefault;  // MPLD_LIGHT_STEPS overrides (tuning)
   int blocks_simplify = 0, blocks_recover = 0, blocks_search = 0, blocks_stream = 0, blocks_discover = 0;
-  int blocks_heavy[6] = {0, 0, 0, 0, 0, 0};  // per k = 2..4 and word class (32-bit, 64-bit)
+  int blocks_heavy[3] = {0, 0, 0};  // per k = 2..4
   int blocks_wide = 0;                        // the 64-bit lane kernel
   long long* counts = nullptr;  // the prepare phase's d_counts (zeroed by the simplification kernel)
   bool search_counted = false;  // the search accumulated the counts (one shard)
@@ -366,7 +366,7 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
     cudaError_t e = launch_search_heavy(g, ws, ctx->k, w_stitch, colors, count, s, ctx->blocks_heavy, true);
     if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_heavy");
     t.done();
-    ctx->call_launches += 2;  // one launch per word class
+    ++ctx->call_launches;
   }
   return MPLD_OK;
 }
@@ -530,12 +530,12 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   }
   cudaMemset(ctx->ctl, 0, sizeof(Control));
   if (cudaMalloc((void**)&ctx->wq, sizeof(WorkItem) * 2 * kWQCap) != cudaSuccess ||
-      cudaMalloc((void**)&ctx->wq_flag, sizeof(unsigned) * 2 * kWQCap) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->wq_flag, sizeof(unsigned long long) * 2 * kWQCap) != cudaSuccess ||
       cudaMalloc((void**)&ctx->hslot, sizeof(HeavySlot) * kSlots) != cudaSuccess) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_NOMEM, "heavy-search work queue allocation failed");
   }
-  cudaMemset(ctx->wq_flag, 0, sizeof(unsigned) * 2 * kWQCap);  // epochs start at 1
+  cudaMemset(ctx->wq_flag, 0, sizeof(unsigned long long) * 2 * kWQCap);  // epochs start at 1
   ctx->blocks_simplify = coop_blocks_simplify(kCoopThreads, ctx->num_sms);
   ctx->blocks_recover = coop_blocks_recover(kCoopThreads, ctx->num_sms);
   ctx->blocks_search = resident_blocks_search(32, ctx->num_sms);

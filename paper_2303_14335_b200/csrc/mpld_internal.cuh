@@ -60,9 +60,11 @@ struct Control {
                                // warps stay for spilled work instead of leaving (reset with n_heavy)
   int n_wide;                  // components of > 32 vertices listed for the 64-bit lane kernel (reset with n_heavy)
   alignas(128) int heavy_next[2];  // exact mode: next heavy component to take per word class (reset with n_heavy)
-  alignas(128) int wq_head[2];     // spilled work items: tickets handed out per word class (reset with n_heavy)
-  alignas(128) int wq_tail[2];     // ... positions reserved (polled)
+  alignas(128) int wq_head[2];     // spilled work items (a ring per word class): positions claimed by consumers
+  alignas(128) int wq_tail[2];     // ... positions reserved by producers (polled)
   int wq_done[2];                  // work units (heavy components + items) finished per word class (polled)
+  alignas(128) int wq_read[2];     // ... items copied out by their consumers (ring slots free again)
+  int spill_refused;               // spills refused (ring full or no slot left): those units ran on alone
   alignas(128) unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
   alignas(128) unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)
   unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
@@ -127,7 +129,7 @@ __host__ __device__ __forceinline__ unsigned long long partition_estimate(int n,
 // Exact mode, spilled heavy searches (kernel_search.cu): a warp whose search
 // of one component runs long hands its open work to all heavy warps as work
 // items (node states); a slot per spilled component gathers the best key.
-constexpr int kWQCap = 1 << 16;  // work items per word class and call
+constexpr int kWQCap = 1 << 16;  // ring slots of spilled work items per word class
 constexpr int kHelpersMinN = 16;  // heavy components this large may run long enough to spill
 constexpr int kSlots = 1024;     // spilled components per call
 struct WorkItem {
@@ -160,8 +162,8 @@ struct Workspace {
   int* hcost;      // ... and the light phase's best cost
   int* wide;       // components of > 32 vertices (pool index), searched by the 64-bit lane kernel
   Control* ctl;
-  WorkItem* wq;    // [2][kWQCap] spilled work items per word class
-  unsigned* wq_flag;  // [2][kWQCap] == epoch once the item is written
+  WorkItem* wq;    // [2][kWQCap] spilled work items per word class (rings)
+  unsigned long long* wq_flag;  // [2][kWQCap] == epoch << 32 | position once the item at that position is written
   HeavySlot* hslot;   // [kSlots]
   unsigned long long* est;   // [n] sharded search: estimated search cost of the component rooted at v, then
                              // its inclusive prefix sum over vertex ids (the balanced partition)
@@ -242,6 +244,10 @@ cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+__host__ __device__ __forceinline__ unsigned long long wq_tag(unsigned epoch, int pos) {
+  return ((unsigned long long)epoch << 32) | (unsigned)pos;
+}
+
 // launch wrappers (kernels_graph.cu, kernel_search.cu); each returns the
 // cudaError_t of its launch.  `pdl`: the stream's previous operation is one
 // of these kernels.
@@ -262,7 +268,7 @@ cudaError_t launch_search_wide(const GraphView& g, Workspace ws, int k, int w_st
 cudaError_t configure_search_wide(int num_sms, int* blocks);
 cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_stitch, int* colors, long long* counts,
                                 cudaStream_t s, const int* blocks, bool pdl);
-cudaError_t configure_search_heavy(int num_sms, int* blocks);  // blocks[6]: resident grids of the heavy kernels
+cudaError_t configure_search_heavy(int num_sms, int* blocks);  // blocks[3]: resident grids of the heavy kernels (k = 2..4)
 cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
                            int blocks, int threads, bool pdl);
 cudaError_t launch_se_from_pairs(int n, int m, const int* pairs, int* rp, int* col, int* deg, int* fill, int* bsum,

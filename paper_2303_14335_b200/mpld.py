@@ -27,7 +27,7 @@ MPLD_MAX_K = 4
 MPLD_MAX_COMPONENT = 64
 MPLD_COST_UNITS = 1000
 STAT_NAMES = ["components", "hidden", "rounds", "max_component", "steps", "truncated", "error", "launches",
-              "max_steps"]
+              "max_steps", "spill_refused"]
 MPLD_STAT_LEN = len(STAT_NAMES)
 
 # every symbol include/mpld.h declares

@@ -51,7 +51,8 @@ def test_stats_layout_matches_header():
     enum = re.findall(r"MPLD_STAT_([A-Z_]+)\s*=\s*(\d+)", src)
     idx = {name: int(v) for name, v in enum}
     assert idx["LEN"] == len(mp.STAT_NAMES)
-    order = ["COMPONENTS", "HIDDEN", "ROUNDS", "MAX_COMP", "STEPS", "TRUNCATED", "ERROR", "LAUNCHES", "MAX_STEPS"]
+    order = ["COMPONENTS", "HIDDEN", "ROUNDS", "MAX_COMP", "STEPS", "TRUNCATED", "ERROR", "LAUNCHES", "MAX_STEPS",
+             "SPILL_REFUSED"]
     assert [idx[o] for o in order] == list(range(len(order)))
 
 

@@ -1,0 +1,7 @@
+# round 2: unified heavy kernel (both word classes, ring queue) + batch sweep (dev tool)
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/t_r2e.log 2>&1; tail -3 gpurun_out/t_r2e.log
+for i in 1 2 3; do timeout 900 python bench.py --config 2 --steps 5 --warmup 2 --no-cpu-baseline > gpurun_out/b_r2e_c2.json 2> gpurun_out/b_r2e_c2.err; tail -3 gpurun_out/b_r2e_c2.err; python -c "
+import json; d=json.load(open('gpurun_out/b_r2e_c2.json')); print(2, d['ms_per_step'], d['value'], json.dumps(d['kernel_share']), json.dumps(d['stats']))"; done
+for i in 1 2; do timeout 300 python bench.py --steps 10 --no-cpu-baseline --no-secondary 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c1', d['ms_per_step'], d['e2e']['ms_per_step'], json.dumps(d['kernel_share']))"; done
+timeout 600 python tools/batch_sweep.py gpurun_out/batch_sweep.json

@@ -33,8 +33,10 @@ def main():
         name = full.split("::")[-1].split("<")[0].strip()
         if "<" in full and ("unsigned long long" in full or full.rstrip().endswith("unsigned int>")):
             name += "<64>" if "unsigned long long" in full else "<32>"  # word class of the heavy search
-        if name in kernels:  # a later launch of the same kernel (the next step): keep the first
+        if name in kernels and not ("--all" in sys.argv):  # a later launch of the same kernel: keep the first
             continue
+        if name in kernels:
+            name += "#%d" % sum(1 for x in kernels if x.split("#")[0] == name)
         stalls = {}
         for h, i in col.items():
             if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
@@ -54,10 +56,21 @@ def main():
             "block": int(f(d, "launch__block_size") or 0),
             "regs": int(f(d, "launch__registers_per_thread") or 0),
             "stall_top_pct": {k: round(100 * v / tot, 1) for k, v in top},
+            # the counters the north_star names: divergence (active threads per executed
+            # warp instruction, 32 = none), issue-slot use, L2 / L1+shared throughput
+            "threads_per_inst": f(d, "smsp__thread_inst_executed_per_inst_executed.ratio"),
+            "divergent_branch_targets": f(d, "smsp__sass_branch_targets_threads_divergent.sum"),
+            "issue_active_pct": f(d, "sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
+            "l2_throughput_pct": f(d, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "l1tex_throughput_pct": f(d, "l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "shared_wavefronts_pct": f(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+            "dram_throughput_pct": f(d, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
         }
     json.dump({"source": src, "kernels": kernels}, open(out, "w"), indent=1)
     for k, v in kernels.items():
-        print(k, round(v["duration_us"], 1), "us", round(v["dram_bytes"] / 1e6, 2), "MB", v["stall_top_pct"])
+        print(k, round(v["duration_us"], 1), "us", round(v["dram_bytes"] / 1e6, 2), "MB", v["stall_top_pct"],
+              "thr/inst", v["threads_per_inst"], "issue%", v["issue_active_pct"], "L2%", v["l2_throughput_pct"],
+              "L1%", v["l1tex_throughput_pct"], "shm%", v["shared_wavefronts_pct"], "warps%", v["warps_active_pct"])
 
 
 if __name__ == "__main__":
