@@ -902,36 +902,64 @@ __device__ __forceinline__ int warp_min_key(int& c, Path& p) {
 // Frames of the lanes in shared memory, [field][depth][lane] (a lane only
 // touches its own column: conflict-free).  Frame d is the node N_d at which
 // column v_d was selected: saved = B[c] before its current child r(v_d, c)
-// was selected, the node's cost, and v | (c+1) << 8 | (maxused+1) << 16 |
-// lim << 24 (current child c, child limit lim of R6).  The masks of N_j (for
-// a donation or a spill) are rebuilt from the lane's current state by undoing
-// the frames below j (node_at); the deepest frame lives in registers.
+// was selected, and the 16-bit state v | (c+1) << 6 | (maxused+1) << 9 |
+// lim << 12 (current child c, child limit lim of R6).  The node's cost is not
+// stored: popping back to N_d subtracts the cost of the row r(v_d, c) from
+// the child's cost.  The masks and cost of N_j (for a donation or a spill) are
+// rebuilt from the lane's current state by undoing the frames below j
+// (node_at); the deepest frame lives in registers.
 template <int K, typename W, int D>
 struct LaneFrames {
   W saved[D][32];
-  int cost[D][32];
-  int pk[D][32];
+  unsigned short pk[D][32];
 };
 
-// B, C and U at N_j from the lane's state at depth `depth` (frames j..depth-2
-// in shared memory, frame depth-1 in registers: f_saved, f_v, f_c): undo the
-// selected rows of frames depth-1 down to j, uncover their columns.
+__device__ __forceinline__ int pk16(int v, int c, int mu, int lim) {
+  return v | ((c + 1) << 6) | ((mu + 1) << 9) | (lim << 12);
+}
+__device__ __forceinline__ int pk_v(int p) { return p & 63; }
+__device__ __forceinline__ int pk_c(int p) { return ((p >> 6) & 7) - 1; }
+__device__ __forceinline__ int pk_mu(int p) { return ((p >> 9) & 7) - 1; }
+__device__ __forceinline__ int pk_lim(int p) { return p >> 12; }
+
+// Eq. (1) cost of selecting row r(v, c) (Alg. 1 lines 14-15) with colour
+// masks C and uncovered columns U: conflicts with neighbours coloured c,
+// stitches to neighbours coloured otherwise.
+template <typename W>
+__device__ __forceinline__ int row_cost(W a, W sa, W Cc, W U, int w_stitch) {
+  return kCostUnits * WordOps<W>::popc(a & Cc) + w_stitch * WordOps<W>::popc(sa & ~U & ~Cc);
+}
+
+// B, C, U and the cost at N_j from the lane's state at depth `depth` (frames
+// j..depth-2 in shared memory, frame depth-1 in registers: f_saved, f_v, f_c,
+// f_cost = cost of N_{depth-1}): undo the selected rows of frames depth-1 down
+// to j, uncover their columns, subtract their row costs.
 template <int K, typename W, int D>
 __device__ __forceinline__ void node_at(int j, int depth, const W (&B)[K], const W (&C)[K], W U, W f_saved, int f_v,
-                                        int f_c, const LaneFrames<K, W, D>& F, int lane, W (&jB)[K], W (&jC)[K],
-                                        W& jU) {
+                                        int f_c, int f_cost, const LaneFrames<K, W, D>& F, int lane, const W* adj,
+                                        const W* sadj, int w_stitch, W (&jB)[K], W (&jC)[K], W& jU, int& jcost) {
 #pragma unroll
-  for (int c = 0; c < K; ++c) jB[c] = B[c];
-  W bits = W(1) << f_v;
-  if (f_c >= 0) put<K, W>(jB, f_c, f_saved);
+  for (int c = 0; c < K; ++c) {
+    jB[c] = B[c];
+    jC[c] = C[c];
+  }
+  const W fbit = W(1) << f_v;
+  if (f_c >= 0) {
+    put<K, W>(jB, f_c, f_saved);
+    put<K, W>(jC, f_c, pick<K, W>(jC, f_c) & ~fbit);
+  }
+  jU = U | fbit;
+  jcost = f_cost;
   for (int d = depth - 2; d >= j; --d) {  // frames above the deepest always have a selected child
     const int pk = F.pk[d][lane];
-    bits |= W(1) << (pk & 0xff);
-    put<K, W>(jB, ((pk >> 8) & 0xff) - 1, F.saved[d][lane]);
+    const int v = pk_v(pk), c = pk_c(pk);
+    const W bit = W(1) << v;
+    put<K, W>(jB, c, F.saved[d][lane]);
+    const W Cc = pick<K, W>(jC, c) & ~bit;
+    put<K, W>(jC, c, Cc);
+    jU |= bit;
+    jcost -= row_cost<W>(adj[v], sadj[v], Cc, jU, w_stitch);  // the row that led from N_d to N_{d+1}
   }
-  jU = U | bits;
-#pragma unroll
-  for (int c = 0; c < K; ++c) jC[c] = C[c] & ~bits;
 }
 
 template <int K, typename W>
@@ -1042,23 +1070,22 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           const int j = __ffsll((long long)(open & donatable)) - 1;
           int pk, jc;
           W jU;
-          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, F, lane, xB, xC, jU);
+          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
+                                             w_stitch, xB, xC, jU, jc);
           if (j == depth - 1) {
-            jc = f_cost;
-            pk = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
+            pk = pk16(f_v, f_c, f_mu, f_lim);
             f_lim -= 1;
           } else {
-            jc = F.cost[j][lane];
             pk = F.pk[j][lane];
-            F.pk[j][lane] = pk - (1 << 24);
+            F.pk[j][lane] = (unsigned short)(pk - (1 << 12));
           }
-          const int v = pk & 0xff, cj = ((pk >> 8) & 0xff) - 1, mu = ((pk >> 16) & 0xff) - 1, lim = pk >> 24;
+          const int v = pk_v(pk), cj = pk_c(pk), mu = pk_mu(pk), lim = pk_lim(pk);
           if (cj >= lim - 1) open &= ~(1ull << j);
           const W bit = W(1) << v;
           const W a = adj[v], sa = sadj[v];
           xU = jU & ~bit;
           const W Cc = pick<K, W>(xC, lim);
-          xcost = jc + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~xU & ~Cc);
+          xcost = jc + row_cost<W>(a, sa, Cc, xU, w_stitch);
           put<K, W>(xC, lim, Cc | bit);
           put<K, W>(xB, lim, pick<K, W>(xB, lim) | a);
           xmu = max(mu, lim);
@@ -1127,8 +1154,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       if (ex && depth > d0) {  // spill the parent frame
         const int d = depth - 1;
         F.saved[d][lane] = f_saved;
-        F.cost[d][lane] = f_cost;
-        F.pk[d][lane] = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
+        F.pk[d][lane] = (unsigned short)pk16(f_v, f_c, f_mu, f_lim);
       }
       const W av = adj[v], sav = sadj[v];
       f_cost = ex ? cost : f_cost;
@@ -1160,7 +1186,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       const int cc = min(c, K - 1);
       const W Cc = pick<K, W>(C, cc);
       const W Bc = pick<K, W>(B, cc);
-      const int ncost = f_cost + kCostUnits * O::popc(f_adj & Cc) + w_stitch * O::popc(f_sadj & ~U & ~Cc);
+      const int ncost = f_cost + row_cost<W>(f_adj, f_sadj, Cc, U, w_stitch);
 #pragma unroll
       for (int q = 0; q < K; ++q) {
         const bool sel = nxt && q == cc;
@@ -1178,15 +1204,19 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       const bool pop = exh && fd > d0;
       const int pd = max(fd - 1, 0);
       const W ps = F.saved[pd][lane];
-      const int pc = F.cost[pd][lane], ppk = F.pk[pd][lane];
-      const int pv = pop ? (ppk & 0xff) : f_v;
+      const int ppk = F.pk[pd][lane];
+      const int pv = pop ? pk_v(ppk) : f_v;
       const W pa = adj[pv], psa = sadj[pv];
+      // cost of N_pd = cost of its child N_fd minus the row r(pv, pc) still applied in C
+      const int pcc = max(pk_c(ppk), 0);
+      const W pC = pick<K, W>(C, pcc) & ~(W(1) << pv);
+      const int pinc = row_cost<W>(pa, psa, pC, U, w_stitch);
       f_saved = pop ? ps : f_saved;
-      f_cost = pop ? pc : f_cost;
+      f_cost = pop ? f_cost - pinc : f_cost;
       f_v = pv;
-      f_c = pop ? ((ppk >> 8) & 0xff) - 1 : (nxt ? c : f_c);
-      f_mu = pop ? ((ppk >> 16) & 0xff) - 1 : f_mu;
-      f_lim = pop ? (ppk >> 24) : f_lim;
+      f_c = pop ? pk_c(ppk) : (nxt ? c : f_c);
+      f_mu = pop ? pk_mu(ppk) : f_mu;
+      f_lim = pop ? pk_lim(ppk) : f_lim;
       f_adj = pop ? pa : f_adj;
       f_sadj = pop ? psa : f_sadj;
       depth = exh ? fd : depth;
@@ -1221,8 +1251,8 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
         int cnt = 0, j = -1;
         if (active && (open & donatable)) {
           j = __ffsll((long long)(open & donatable)) - 1;
-          const int pk = j == depth - 1 ? (f_c + 1) << 8 | (f_lim << 24) : F.pk[j][lane];
-          cnt = (pk >> 24) - (((pk >> 8) & 0xff) - 1);
+          const int pk = j == depth - 1 ? pk16(f_v, f_c, f_mu, f_lim) : F.pk[j][lane];
+          cnt = pk_lim(pk) - pk_c(pk);
         }
         int tot = 0;
         const int excl = warp_excl_scan(cnt, tot);
@@ -1267,18 +1297,17 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           int at = base + excl;
           W jB[K], jC[K], jU;
           int pk, jc;
-          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, F, lane, jB, jC, jU);
+          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
+                                             w_stitch, jB, jC, jU, jc);
           if (j == depth - 1) {
-            jc = f_cost;
-            pk = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16) | (f_lim << 24);
+            pk = pk16(f_v, f_c, f_mu, f_lim);
             f_lim = f_c;  // its children are in the queue now
           } else {
-            jc = F.cost[j][lane];
             pk = F.pk[j][lane];
-            F.pk[j][lane] = (pk & 0x00ffffff) | ((((pk >> 8) & 0xff) - 1) << 24);
+            F.pk[j][lane] = (unsigned short)((pk & 0x0fff) | (pk_c(pk) << 12));
           }
           open &= ~(1ull << j);
-          const int v = pk & 0xff, cj = ((pk >> 8) & 0xff) - 1, mu = ((pk >> 16) & 0xff) - 1, lim = pk >> 24;
+          const int v = pk_v(pk), cj = pk_c(pk), mu = pk_mu(pk), lim = pk_lim(pk);
           const W bit = W(1) << v;
           const W a = adj[v], sa = sadj[v];
           for (int ch = cj + 1; ch <= lim; ++ch) {  // the untried children of frame j (C at N_j = C & ~U_j)
@@ -1290,7 +1319,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
             }
             const W xU = jU & ~bit;
             const W Cc = pick<K, W>(xC, ch);
-            const int xcost = jc + kCostUnits * O::popc(a & Cc) + w_stitch * O::popc(sa & ~xU & ~Cc);
+            const int xcost = jc + row_cost<W>(a, sa, Cc, xU, w_stitch);
             put<K, W>(xC, ch, Cc | bit);
             put<K, W>(xB, ch, pick<K, W>(xB, ch) | a);
             Path xP = path_prefix<kTwo>(P, j);
@@ -1675,7 +1704,7 @@ __device__ void heavy_item(const GraphView& g, const Workspace& w, int pos, int 
 // producer has reserved it, so no warp waits on one class while the other
 // has work), until every unit of both classes is done.
 template <int K>
-__global__ void __launch_bounds__(32) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
+__global__ void __launch_bounds__(32, 9) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
                                                                     int* colors, long long* counts) {
   pdl_begin();
   extern __shared__ __align__(16) unsigned char smem[];
