@@ -730,13 +730,17 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
     const bool mine_c = ci < n_comp && in_shard(g, w, __ldcg(&w.porder[off]), n, K, shard_index, shard_count);
     acc.comps += mine_c ? 1 : 0;
     // components of more than 32 vertices: listed for the 64-bit lane kernel
+    // (budgeted mode), or handed to the warp-parallel search unsearched (exact
+    // mode: the light budget would not finish them; the heavy search starts
+    // from a greedy colouring)
     const bool wide = mine_c && n > 32;
-    const unsigned wm = __ballot_sync(0xffffffffu, wide);
+    if (wide && exact) light_handoff(g, w, ci, n, INT_MAX);
+    const unsigned wm = __ballot_sync(0xffffffffu, wide && !exact);
     if (wm) {
       int base = 0;
       if (lane == 0) base = atomicAdd(&ctl->n_wide, __popc(wm));
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (wide) w.wide[base + __popc(wm & lanemask_lt())] = ci;
+      if (wide && !exact) w.wide[base + __popc(wm & lanemask_lt())] = ci;
     }
     lane_component<K, unsigned, 32, kStagedLight>(g, w, L, lane, ci < n_comp, mine_c && n <= 32, ci, rec, w_stitch,
                                                   budget, exact, colors, counts, acc);
@@ -1363,7 +1367,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
 // (c, maximal path) is a valid incumbent key that never cuts the canonical
 // optimum (its key is <= (c, path of any leaf of cost c)).
 template <int K, typename W>
-__device__ int warp_greedy_seed(const W* adj, const W* sadj, int n, int w_stitch, unsigned seed) {
+__device__ int warp_greedy_seed(const W* adj, const W* sadj, int n, int w_stitch, unsigned seed, W (&best)[K]) {
   using O = WordOps<W>;
   const int lane = threadIdx.x & 31;
   unsigned r = lowbias32(seed * 32u + (unsigned)lane + 0x9e3779b9u);
@@ -1443,14 +1447,21 @@ __device__ int warp_greedy_seed(const W* adj, const W* sadj, int n, int w_stitch
     ns += O::popc(sadj[v] & ~Cv);
   }
   const int cost = kCostUnits * (nc >> 1) + w_stitch * (ns >> 1);
-  return (int)(__reduce_min_sync(0xffffffffu, (unsigned)cost));
+  const int mc = (int)__reduce_min_sync(0xffffffffu, (unsigned)cost);
+  const int src = __ffs(__ballot_sync(0xffffffffu, cost == mc)) - 1;
+#pragma unroll
+  for (int c = 0; c < K; ++c) best[c] = __shfl_sync(0xffffffffu, C[c], src);
+  return mc;
 }
 
-// the path of the leaf whose colours are col (a leaf of the canonical tree:
-// follow the column rule and take each selected column's colour)
+// The canonical leaf of a colouring: follow the column rule of R5 and take
+// each selected column's colour, masks renamed into first-use order along
+// that column sequence (R6: masks are interchangeable and the live counts that
+// drive R5 do not depend on their names, so the renamed colouring is a leaf of
+// the canonical tree with the same cost).  col is renamed in place; returns
+// the leaf's path and its cost.
 template <int K, typename W>
-__device__ __forceinline__ Path leaf_path(const W (&col)[K], int n, const W* adj, const W* sadj, int w_stitch,
-                                          int& cost) {
+__device__ __forceinline__ Path leaf_path(W (&col)[K], int n, const W* adj, const W* sadj, int w_stitch, int& cost) {
   State<K, W> s;
 #pragma unroll
   for (int c = 0; c < K; ++c) s.C[c] = s.B[c] = 0;
@@ -1458,12 +1469,20 @@ __device__ __forceinline__ Path leaf_path(const W (&col)[K], int n, const W* adj
   s.cost = 0;
   s.mu = -1;
   Path P = {0ull, 0ull};
+  int perm = 0;  // 3 bits per original mask: 0 = not seen yet, else new name + 1
   for (int d = 0; d < n; ++d) {
     const int v = select_column<K, W>(s);
-    const int c = colour_of<K, W>(col, v);
+    const int c0 = colour_of<K, W>(col, v);
+    int c = ((perm >> (3 * c0)) & 7) - 1;
+    if (c < 0) {
+      c = s.mu + 1;
+      perm |= (c + 1) << (3 * c0);
+    }
     apply_row<K, W>(s, v, c, adj, sadj, w_stitch);
     path_put(P, d, c);
   }
+#pragma unroll
+  for (int c = 0; c < K; ++c) col[c] = s.C[c];
   cost = s.cost;
   return P;
 }
@@ -1585,21 +1604,28 @@ __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, i
   u.n = (int)(rec & 0xffull);
   u.c1 = __ldcg(&w.hcost[idx]);
   u.slot = -1;
-  heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, colors, u.col);
+  const bool light_leaf = u.c1 != INT_MAX;  // exact mode hands components of > 32 vertices over unsearched
+  heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, light_leaf ? colors : nullptr, u.col);
   cur_ci = u.ci;
   cur_ncl = u.ncl;
-  int lc = 0;  // == c1
+  W gcol[K];
+  const int hc = (kSeedIncumbent || !light_leaf) ? warp_greedy_seed<K, W>(s_adj, s_sadj, u.n, w_stitch,
+                                                                          (unsigned)u.ci, gcol)
+                                                 : INT_MAX;
+  if (!light_leaf) {  // the greedy colouring (renamed into a canonical leaf by leaf_path) is the starting leaf
+#pragma unroll
+    for (int c = 0; c < K; ++c) u.col[c] = gcol[c];
+  }
+  int lc = 0;  // the leaf's cost
   u.p1 = leaf_path<K, W>(u.col, u.n, s_adj, s_sadj, w_stitch, lc);
+  if (!light_leaf) u.c1 = lc;
   int gcost = u.c1;
   Path gP = u.p1;
   u.hc = u.c1;
-  if (kSeedIncumbent) {  // a cheaper greedy colouring: (its cost, maximal path) is a valid incumbent key
-    const int hc = warp_greedy_seed<K, W>(s_adj, s_sadj, u.n, w_stitch, (unsigned)u.ci);
-    if (hc < u.c1) {
-      u.hc = hc;
-      gcost = hc;
-      gP = Path{~0ull, ~0ull};
-    }
+  if (hc < u.c1) {  // a cheaper greedy colouring: (its cost, maximal path) is a valid incumbent key
+    u.hc = hc;
+    gcost = hc;
+    gP = Path{~0ull, ~0ull};
   }
   W zero[K], bestC[K];
 #pragma unroll
@@ -1614,11 +1640,13 @@ __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, i
 #pragma unroll
     for (int c = 0; c < K; ++c) fin[c] = u.col[c];
     const unsigned owner = __ballot_sync(0xffffffffu, mine);
-    if (owner && key_less<kTwo>(gcost, gP, u.c1, u.p1)) {
+    const bool better = owner && key_less<kTwo>(gcost, gP, u.c1, u.p1);
+    if (better) {
 #pragma unroll
       for (int c = 0; c < K; ++c) fin[c] = __shfl_sync(0xffffffffu, bestC[c], __ffs(owner) - 1);
-      for (int i = lane; i < u.n; i += 32) colors[__ldcg(&porder[i])] = colour_of<K, W>(fin, i);
     }
+    if (better || !light_leaf)
+      for (int i = lane; i < u.n; i += 32) colors[__ldcg(&porder[i])] = colour_of<K, W>(fin, i);
     heavy_counts<K, W>(g, s_adj, s_sadj, u.n, fin, __ldcg(&porder[0]), counts);
   } else {
     heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, porder, colors, counts);

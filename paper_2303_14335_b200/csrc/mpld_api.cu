@@ -353,7 +353,8 @@ int phase_search(mpld_context* ctx, cudaStream_t s, int w_stitch, long long max_
     t.done();
     ++ctx->call_launches;
   }
-  {  // the components of > 32 vertices, one per lane on 64-bit words
+  if (max_steps > 0) {  // budgeted mode: the components of > 32 vertices, one per lane on 64-bit words
+                        // (exact mode hands them to the warp-parallel search directly)
     TimedLaunch t(ctx, K_SEARCH_WIDE, s);
     cudaError_t e = launch_search_wide(g, ws, ctx->k, w_stitch, max_steps, colors, ctx->light_steps, count, s,
                                        ctx->blocks_wide);

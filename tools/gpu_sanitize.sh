@@ -1,3 +1,7 @@
-# compute-sanitizer over a subset of the GPU parity tests (dev tool)
-timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -x -q -k "edge_cases or spill or tail or pairs or sharded or single_layout or k2" > gpurun_out/memcheck.log 2>&1; echo "memcheck rc $?"; tail -15 gpurun_out/memcheck.log
-timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 20 python -m pytest tests/test_gpu_parity.py -x -q -k "edge_cases or single_layout" > gpurun_out/racecheck.log 2>&1; echo "racecheck rc $?"; grep -E "ERROR SUMMARY|hazard|passed|failed" gpurun_out/racecheck.log | tail -8
+# compute-sanitizer over the search tests (dev tool): memcheck, racecheck, synccheck
+mkdir -p gpurun_out/sanitizer
+T="tests/test_gpu_parity.py"
+SEL="edge_cases or heavy_search_spill or exact_mode_warp or stitch_pairs or sharded or recovery_cluster_tail or k4_budget"
+timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest $T -q -x -k "$SEL" > gpurun_out/sanitizer/memcheck.log 2>&1; echo "memcheck rc=$?"; tail -3 gpurun_out/sanitizer/memcheck.log
+timeout 1500 compute-sanitizer --tool racecheck --racecheck-report hazard --error-exitcode 9 python -m pytest $T -q -x -k "heavy_search_spill or exact_mode_warp" > gpurun_out/sanitizer/racecheck.log 2>&1; echo "racecheck rc=$?"; tail -3 gpurun_out/sanitizer/racecheck.log
+timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest $T -q -x -k "heavy_search_spill or exact_mode_warp" > gpurun_out/sanitizer/synccheck.log 2>&1; echo "synccheck rc=$?"; tail -3 gpurun_out/sanitizer/synccheck.log
