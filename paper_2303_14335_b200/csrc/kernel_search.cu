@@ -132,30 +132,29 @@ __host__ __device__ constexpr int clique_min() {
 #ifndef MPLD_HEAVY_CLIQUE
 #define MPLD_HEAVY_CLIQUE 0
 #endif
+// Lower bound of R7 in conflicts: columns with no live row (popc(Z), summed by
+// the callers), plus this clique term: over the cliques, max(0, |X| - #masks
+// live on X) for X = the clique's uncovered columns that still have a live row.
+template <int K, typename W>
+__device__ __forceinline__ int clique_deficit(const W (&B)[K], W U, W Z, const W* cl, int cs, int ncl) {
+  using O = WordOps<W>;
+  int d = 0;
+  for (int q = 0; q < ncl; ++q) {
+    const W X = cl[q * cs] & U & ~Z;
+    if (!X) continue;
+    int live = 0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) live += (X & ~B[c]) ? 1 : 0;
+    d += max(0, O::popc(X) - live);
+  }
+  return d;
+}
+
 template <int K>
 __host__ __device__ constexpr int heavy_clique_min() {
   return MPLD_HEAVY_CLIQUE > 0 ? MPLD_HEAVY_CLIQUE : clique_min<K>();
 }
 
-// Lower bound of R7 in conflicts: columns with no live row, plus, over the
-// cliques, max(0, |X| - #masks live on X) for X = the clique's uncovered
-// columns that still have a live row.
-template <int K, typename W, bool kCliques = (clique_min<K>() > 0)>
-__device__ __forceinline__ int bound_conflicts(const W (&B)[K], W U, W Z, const W* cl, int cs, int ncl) {
-  using O = WordOps<W>;
-  int lb = O::popc(Z);
-  if constexpr (kCliques) {
-    for (int q = 0; q < ncl; ++q) {
-      const W X = cl[q * cs] & U & ~Z;
-      if (!X) continue;
-      int live = 0;
-#pragma unroll
-      for (int c = 0; c < K; ++c) live += (X & ~B[c]) ? 1 : 0;
-      lb += max(0, O::popc(X) - live);
-    }
-  }
-  return lb;
-}
 
 template <int K, typename W>
 __device__ __forceinline__ int colour_of(const W (&bestC)[K], int i) {
@@ -452,7 +451,7 @@ using LaneWide = LaneStore<unsigned long long, kMaxComp>;
 // entered and the best leaf's colour masks in bestC.
 template <int K, typename W, int N>
 __device__ unsigned lane_dfs(LaneStore<W, N>& L, int lane, bool valid, int n, int w_stitch, unsigned budget, int ncl,
-                             W (&bestC)[K], int& best, bool& trunc) {
+                             W clu, W (&bestC)[K], int& best, bool& trunc) {
   using O = WordOps<W>;
   W C[K], B[K];
 #pragma unroll
@@ -475,7 +474,13 @@ __device__ unsigned lane_dfs(LaneStore<W, N>& L, int lane, bool valid, int n, in
     {  // enter the pending node: leaf / prune / expand
       W Z, Ol;
       live_counts<K, W>(B, U, Z, Ol);
-      const int lb = cost + kCostUnits * bound_conflicts<K, W>(B, U, Z, cl, 32, ncl);
+      // bound (R7): cost + zero-live columns + clique deficit.  The deficit is at
+      // most the number of live columns inside cliques (clu), so it is summed
+      // only when it can change the decision lb < best (same decisions, same
+      // node order as the oracle; most nodes skip the clique loop)
+      const int base = cost + kCostUnits * O::popc(Z);
+      const bool undecided = clique_min<K>() > 0 && base < best && base + kCostUnits * O::popc(U & ~Z & clu) >= best;
+      const int lb = undecided ? base + kCostUnits * clique_deficit<K, W>(B, U, Z, cl, 32, ncl) : base;
       const bool leaf = U == 0;
       const bool better = active && en && leaf && cost < best;  // Alg. 1 line 5, strict improvement
       const bool ex = active && en && !leaf && lb < best;       // bound (R7)
@@ -601,6 +606,7 @@ __device__ __forceinline__ int warp_owner(unsigned rel, unsigned e) {
 template <typename W, int N, bool kOrder>
 __device__ __forceinline__ void warp_stage(const Workspace& w, LaneStore<W, N>& L, int lane, bool has, bool store,
                                            size_t off, int n) {
+  __syncwarp();  // the lanes' earlier accesses to the rows written below (frames / masks) are complete
   const size_t base = __shfl_sync(0xffffffffu, off, 0);  // lane 0 always holds a record
   const unsigned rel = has ? (unsigned)(off - base) : 0xffffffffu;
   const unsigned end = __reduce_max_sync(0xffffffffu, has ? rel + (unsigned)n : 0u);
@@ -649,10 +655,12 @@ __device__ __forceinline__ void lane_component(const GraphView& g, const Workspa
   const int ncl = valid && clique_min<K>() ? clique_partition<W>(&L.A[0][lane], 32, n, &L.cl[0][lane], 32,
                                                                   clique_min<K>())
                                            : 0;
+  W clu = 0;  // the cliques' union
+  for (int q = 0; q < ncl; ++q) clu |= L.cl[q][lane];
   W bestC[K];
   int best_cost = 0;
   bool trunc = false;
-  const unsigned steps = lane_dfs<K, W, N>(L, lane, valid, n, w_stitch, budget, ncl, bestC, best_cost, trunc);
+  const unsigned steps = lane_dfs<K, W, N>(L, lane, valid, n, w_stitch, budget, ncl, clu, bestC, best_cost, trunc);
   if (kStaged) warp_stage<W, N, true>(w, L, lane, has, valid, off, n);
   if (!valid) return;
   for (int i = 0; i < n; ++i)
@@ -1019,6 +1027,8 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
   const W* cl = u.cl;
   auto& F = *u.F;
   int* slot = u.pair;
+  W clu = 0;  // the cliques' union (the clique term is summed only when it can change a decision)
+  for (int q = 0; q < ncl; ++q) clu |= cl[q];
   const unsigned long long donatable = (n - kDonateMinLevels) >= 64 ? ~0ull
                                        : (n - kDonateMinLevels <= 0 ? 0ull : ((1ull << (n - kDonateMinLevels)) - 1ull));
   unsigned iters = 0;
@@ -1143,7 +1153,12 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
     {
       W Z, Ol;
       live_counts<K, W>(B, U, Z, Ol);
-      const int lb = cost + kCostUnits * bound_conflicts<K, W, (heavy_clique_min<K>() > 0)>(B, U, Z, cl, 1, ncl);
+      // bound (R7): the clique deficit is at most the live columns inside
+      // cliques, so it is summed only when it can change the key comparison
+      const int base = cost + kCostUnits * O::popc(Z);
+      const bool undecided = heavy_clique_min<K>() > 0 && key_less<kTwo>(base, P, gcost, gP) &&
+                             !key_less<kTwo>(base + kCostUnits * O::popc(U & ~Z & clu), P, gcost, gP);
+      const int lb = undecided ? base + kCostUnits * clique_deficit<K, W>(B, U, Z, cl, 1, ncl) : base;
       const bool leaf = U == 0;
       const bool better = active && en && leaf && key_less<kTwo>(cost, P, gcost, gP);  // Alg. 1 line 5
       const bool ex = active && en && !leaf && key_less<kTwo>(lb, P, gcost, gP);      // bound (R7)
@@ -1732,7 +1747,7 @@ __device__ void heavy_item(const GraphView& g, const Workspace& w, int pos, int 
 // producer has reserved it, so no warp waits on one class while the other
 // has work), until every unit of both classes is done.
 template <int K>
-__global__ void __launch_bounds__(32, 9) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
+__global__ void __launch_bounds__(32, 8) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
                                                                     int* colors, long long* counts) {
   pdl_begin();
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1767,22 +1782,33 @@ __global__ void __launch_bounds__(32, 9) mpld_exact_cover_search_heavy(GraphView
   while (!__shfl_sync(0xffffffffu, leave, 0)) {
     int pos = -1, pcls = 0;
     if (lane == 0) {
-      for (int c = 1; c >= 0 && pos < 0; --c) {  // claim a reserved position (64-bit class first)
-        int hd = *(volatile int*)&ctl->wq_head[c];
-        while (hd < *(volatile int*)&ctl->wq_tail[c]) {
-          const int o = atomicCAS(&ctl->wq_head[c], hd, hd + 1);
-          if (o == hd) {
-            pos = hd;
-            pcls = c;
-            break;
-          }
-          hd = o;
+      // take a ticket (one ring position, one atomic, no retries) in a class
+      // whose ring holds unclaimed items (64-bit class first); a ticket taken
+      // past the reserved positions (a race) waits for its item, or is void
+      // once its class has finished (no producer can reserve it any more)
+      for (int c = 1; c >= 0 && pos < 0; --c) {
+        if (*(volatile int*)&ctl->wq_head[c] < *(volatile int*)&ctl->wq_tail[c]) {
+          pos = atomicAdd(&ctl->wq_head[c], 1);
+          pcls = c;
         }
       }
-      if (pos >= 0) {  // its producer publishes the item right after reserving it
+      if (pos >= 0) {
         const unsigned long long tag = wq_tag(w.epoch, pos);
         const volatile unsigned long long* f = &w.wq_flag[(size_t)pcls * kWQCap + (pos & (kWQCap - 1))];
-        while (*f != tag) __nanosleep(20);
+        const int nh = pcls ? n_heavy1 : n_heavy0;
+        unsigned wait = 20;
+        while (*f != tag) {
+          if (pos >= *(volatile int*)&ctl->wq_tail[pcls]) {  // not reserved yet: its class may have finished
+            const int d = *(volatile int*)&ctl->wq_done[pcls];
+            __threadfence();
+            if (d >= nh + *(volatile int*)&ctl->wq_tail[pcls] && pos >= *(volatile int*)&ctl->wq_tail[pcls]) {
+              pos = -1;
+              break;
+            }
+          }
+          __nanosleep(wait);
+          wait = min(wait * 2u, 256u);
+        }
         __threadfence();
       }
     }
