@@ -205,6 +205,24 @@ int mpld_decompose_batch_pairs_async(mpld_context* ctx, int32_t n_layouts, const
                                      uint32_t flags, int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches,
                                      double* cost, int64_t* stats, int64_t* ticket);
 
+/* The same submit with the conflict edges given as the upper triangle of
+ * their CSR: ce_up_deg [n] uint8 = the number of CE neighbours u > v of each
+ * vertex v (< 256 per vertex), ce_up_col [n_ce_edges] = those neighbours,
+ * rows in vertex order, each row strictly ascending (every undirected CE edge
+ * once, in the row of its smaller end); stitch candidates as pairs.  The
+ * upload carries n + 4|CE| + 8|SE| bytes instead of 4(n+1) + 8|CE| + 8|SE|
+ * and the symmetric CE CSR (rows ascending) is built on the device before the
+ * hot path (§2.1: E = {CE ∪ SE} is undirected, so the triangle holds
+ * the whole graph).  Entries outside (v, n), rows not strictly ascending or
+ * degrees not summing to n_ce_edges are reported by mpld_wait as
+ * MPLD_ERR_GRAPH (whatever the flags); results are identical to
+ * mpld_decompose_batch_pairs_async on the same graph. */
+int mpld_decompose_batch_upper_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
+                                     const uint8_t* ce_up_deg, int64_t n_ce_edges, const int32_t* ce_up_col,
+                                     int64_t n_stitch_pairs, const int32_t* stitch_pairs, int32_t k, double alpha,
+                                     int64_t max_steps, uint32_t flags, int32_t* colors, int64_t* n_conflicts,
+                                     int64_t* n_stitches, double* cost, int64_t* stats, int64_t* ticket);
+
 /* Block until submit `ticket` of ctx has completed; returns its result code
  * (MPLD_OK or the error of that submit).  Waiting on an older ticket whose slot
  * has been reused returns its stored result. */

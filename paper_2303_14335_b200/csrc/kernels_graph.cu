@@ -396,6 +396,10 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_component
   int hidden0 = 0;
   bool bad = false;
   unsigned long long hs[4] = {0ull, 0ull, 0ull, 0ull};  // sum H(v,u), H(u,v) over CE, then over SE
+  if (blockIdx.x == 0 && threadIdx.x == 0 && w.build_err && *w.build_err) {  // CSR built on the device from bad input
+    bad = true;
+    *w.build_err = 0;
+  }
   if (validate && blockIdx.x == 0 && threadIdx.x == 0) {
     if (g.layout_off[0] != 0 || g.layout_off[g.n_layouts] != g.n || g.ce_rp[0] != 0 || g.se_rp[0] != 0) bad = true;
     for (int l = 0; l < g.n_layouts; ++l)
@@ -1168,13 +1172,14 @@ __device__ __forceinline__ int block_scan_int(int x, int* s_w, int& total) {
   return r;
 }
 
-__global__ void __launch_bounds__(1024) mpld_scan_sums(int n, const int* in, int* bsum) {
+template <typename T>
+__global__ void __launch_bounds__(1024) mpld_scan_sums(int n, const T* in, int* bsum) {
   __shared__ int s_w[32];
   const size_t base = (size_t)blockIdx.x * kScanTileI;
   int x = 0;
   for (int j = 0; j < kScanTileI / 1024; ++j) {
     const size_t i = base + (size_t)j * 1024 + threadIdx.x;
-    if (i < (size_t)n) x += in[i];
+    if (i < (size_t)n) x += (int)in[i];
   }
   int total;
   block_scan_int(x, s_w, total);
@@ -1195,13 +1200,14 @@ __global__ void __launch_bounds__(1024) mpld_scan_offsets(int nb, int* bsum) {
 }
 
 // out[i] = sum of in[0..i) for i in [0, n]; in and out may not alias
-__global__ void __launch_bounds__(1024) mpld_scan_apply(int n, const int* in, const int* bsum, int* out) {
+template <typename T>
+__global__ void __launch_bounds__(1024) mpld_scan_apply(int n, const T* in, const int* bsum, int* out) {
   __shared__ int s_w[32];
   const size_t base = (size_t)blockIdx.x * kScanTileI;
   int carry = bsum[blockIdx.x];
   for (int j = 0; j < kScanTileI / 1024; ++j) {
     const size_t i = base + (size_t)j * 1024 + threadIdx.x;
-    const int x = i < (size_t)n ? in[i] : 0;
+    const int x = i < (size_t)n ? (int)in[i] : 0;
     int total;
     const int inc = block_scan_int(x, s_w, total);
     if (i < (size_t)n) out[i] = carry + inc - x;
@@ -1234,9 +1240,98 @@ __global__ void __launch_bounds__(256) mpld_se_sort_rows(int n, const int* __res
   }
 }
 
+// The conflict edges given as the upper triangle of the CSR
+// (mpld_decompose_batch_upper_async): deg_up[v] (uint8) = number of CE
+// neighbours u > v, col_up = those neighbours, rows in vertex order, each row
+// strictly ascending.  rp_up = exclusive scan of deg_up.  An entry is valid
+// iff v < u < n and it is larger than its row predecessor; invalid entries
+// (and rows running past the m copied entries) are dropped and flag *err
+// (MPLD_ERR_GRAPH through the simplification's validation).
+__device__ __forceinline__ bool up_entry_ok(const int* col_up, int a, int p, int v, int n) {
+  const int u = __ldg(&col_up[p]);
+  return u > v && u < n && (p == a || u > __ldg(&col_up[p - 1]));
+}
+
+__global__ void __launch_bounds__(256) mpld_up_degrees(int n, int m, const int* __restrict__ rp_up,
+                                                       const int* __restrict__ col_up, int* full, int* err) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int a = rp_up[v], b0 = rp_up[v + 1], b = min(b0, m);
+    int cnt = 0;
+    bool bad = b0 > m;
+    for (int p = a; p < b; ++p) {
+      if (up_entry_ok(col_up, a, p, v, n)) {
+        ++cnt;
+        atomicAdd(&full[__ldg(&col_up[p])], 1);  // the lower entry v of row u
+      } else {
+        bad = true;
+      }
+    }
+    if (cnt) atomicAdd(&full[v], cnt);
+    if (bad) atomicOr(err, 1);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && rp_up[n] != m) atomicOr(err, 1);
+}
+
+// rows of the symmetric CSR: the lower entries (u < v) of row v first, written
+// by atomics (fill), then row v's own upper entries in order
+__global__ void __launch_bounds__(256) mpld_up_scatter(int n, int m, const int* __restrict__ rp_up,
+                                                       const int* __restrict__ col_up, const int* __restrict__ rp,
+                                                       int* fill, int* col) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int a = rp_up[v], b = min(rp_up[v + 1], m);
+    int nup = 0;
+    for (int p = a; p < b; ++p) nup += up_entry_ok(col_up, a, p, v, n) ? 1 : 0;
+    int at = rp[v + 1] - nup;
+    for (int p = a; p < b; ++p) {
+      if (!up_entry_ok(col_up, a, p, v, n)) continue;
+      const int u = __ldg(&col_up[p]);
+      col[at++] = u;
+      col[rp[u] + atomicAdd(&fill[u], 1)] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) mpld_sort_prefix(int n, const int* __restrict__ rp,
+                                                        const int* __restrict__ len, int* col) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int a = rp[v], b = a + len[v];
+    for (int i = a + 1; i < b; ++i) {  // insertion sort of the lower entries (rows are short)
+      const int x = col[i];
+      int j = i - 1;
+      while (j >= a && col[j] > x) {
+        col[j + 1] = col[j];
+        --j;
+      }
+      col[j + 1] = x;
+    }
+  }
+}
+
 }  // namespace
 
 bool pdl_enabled() { return g_pdl; }
+
+// Symmetric CE CSR (rp [n+1], col [2m]) from the upper triangle (deg_up, col_up
+// [m]); rp_up [n+1], full / fill [n] and bsum are scratch, *err is set on invalid input.
+cudaError_t launch_ce_from_upper(int n, int m, const unsigned char* deg_up, const int* col_up, int* rp_up, int* rp,
+                                 int* col, int* full, int* fill, int* bsum, int* err, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(full, 0, sizeof(int) * (size_t)(n > 0 ? n : 1), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(fill, 0, sizeof(int) * (size_t)(n > 0 ? n : 1), s);
+  if (e != cudaSuccess) return e;
+  if (n <= 0) return cudaMemsetAsync(rp, 0, sizeof(int), s);
+  const int gb = 1184;
+  const int nb = (n + kScanTileI - 1) / kScanTileI;
+  mpld_scan_sums<unsigned char><<<nb, 1024, 0, s>>>(n, deg_up, bsum);
+  mpld_scan_offsets<<<1, 1024, 0, s>>>(nb, bsum);
+  mpld_scan_apply<unsigned char><<<nb, 1024, 0, s>>>(n, deg_up, bsum, rp_up);
+  mpld_up_degrees<<<gb, 256, 0, s>>>(n, m, rp_up, col_up, full, err);
+  mpld_scan_sums<int><<<nb, 1024, 0, s>>>(n, full, bsum);
+  mpld_scan_offsets<<<1, 1024, 0, s>>>(nb, bsum);
+  mpld_scan_apply<int><<<nb, 1024, 0, s>>>(n, full, bsum, rp);
+  mpld_up_scatter<<<gb, 256, 0, s>>>(n, m, rp_up, col_up, rp, fill, col);
+  mpld_sort_prefix<<<gb, 256, 0, s>>>(n, rp, fill, col);
+  return cudaGetLastError();
+}
 
 // SE CSR from m pairs (ids already checked on the host): deg / fill are [n]
 // scratch arrays, bsum [n / kScanTileI + 2]
@@ -1249,9 +1344,9 @@ cudaError_t launch_se_from_pairs(int n, int m, const int* pairs, int* rp, int* c
   const int gb = 1184;
   if (m > 0) mpld_se_degrees<<<gb, 256, 0, s>>>(m, pairs, deg);
   const int nb = (n + kScanTileI - 1) / kScanTileI;
-  mpld_scan_sums<<<nb, 1024, 0, s>>>(n, deg, bsum);
+  mpld_scan_sums<int><<<nb, 1024, 0, s>>>(n, deg, bsum);
   mpld_scan_offsets<<<1, 1024, 0, s>>>(nb, bsum);
-  mpld_scan_apply<<<nb, 1024, 0, s>>>(n, deg, bsum, rp);
+  mpld_scan_apply<int><<<nb, 1024, 0, s>>>(n, deg, bsum, rp);
   if (m > 0) {
     mpld_se_scatter<<<gb, 256, 0, s>>>(m, pairs, rp, fill, col);
     mpld_se_sort_rows<<<gb, 256, 0, s>>>(n, rp, col);

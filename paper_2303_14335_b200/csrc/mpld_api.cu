@@ -71,6 +71,9 @@ struct AsyncSlot {
   int* se_rp = nullptr;
   int* se_col = nullptr;
   int* se_pairs = nullptr;  // stitch edges as pairs (the pairs entry point)
+  unsigned char* up_deg = nullptr;  // conflict edges as the upper triangle (the upper entry point)
+  int* up_col = nullptr;
+  int64_t cap_up = -1, cap_up_n = -1;
   int* colors = nullptr;
   long long* counts = nullptr;
   double* cost = nullptr;
@@ -133,6 +136,7 @@ struct mpld_context {
   // cross-stream ordering: calls share the workspace and control block, so a
   // call enqueued on a stream other than the previous call's waits for that
   // call's last operation (ev_last, recorded at the end of every entry point)
+  int* build_err = nullptr;  // device flag of the CSR builds from uploaded triangles (Workspace::build_err)
   cudaEvent_t ev_last = nullptr;
   cudaStream_t last_stream = nullptr;
   bool has_last = false;
@@ -263,7 +267,8 @@ int mark_last(mpld_context* ctx, cudaStream_t s) {
 Workspace workspace(mpld_context* ctx) {
   return Workspace{ctx->deg,   ctx->hround, ctx->bmask,  ctx->prio,  ctx->q0,    ctx->q1,    ctx->roots,
                    ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->wide,  ctx->ctl,   ctx->wq,
-                   ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters, ctx->tail_slots};
+                   ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters, ctx->tail_slots,
+                   ctx->build_err};
 }
 
 // phase 1: validate?, simplification, components (colours initialised to -1)
@@ -530,6 +535,11 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     return fail(MPLD_ERR_NOMEM, "control block allocation failed");
   }
   cudaMemset(ctx->ctl, 0, sizeof(Control));
+  if (cudaMalloc((void**)&ctx->build_err, sizeof(int)) != cudaSuccess) {
+    mpld_context_destroy(ctx);
+    return fail(MPLD_ERR_NOMEM, "control block allocation failed");
+  }
+  cudaMemset(ctx->build_err, 0, sizeof(int));
   if (cudaMalloc((void**)&ctx->wq, sizeof(WorkItem) * 2 * kWQCap) != cudaSuccess ||
       cudaMalloc((void**)&ctx->wq_flag, sizeof(unsigned long long) * 2 * kWQCap) != cudaSuccess ||
       cudaMalloc((void**)&ctx->hslot, sizeof(HeavySlot) * kSlots) != cudaSuccess) {
@@ -593,7 +603,7 @@ void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->bmask, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->roots, (void*)ctx->crec, (void*)ctx->pmask, (void*)ctx->porder, (void*)ctx->hcomp,
-                  (void*)ctx->hcost, (void*)ctx->wide, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
+                  (void*)ctx->hcost, (void*)ctx->wide, (void*)ctx->build_err, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
                   (void*)ctx->est, (void*)ctx->bsum,
                   (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
@@ -610,7 +620,8 @@ void mpld_context_destroy(mpld_context* ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_last) cudaEventDestroy(ctx->ev_last);
   for (AsyncSlot& a : ctx->slot) {
-    for (void* p : {(void*)a.lo, (void*)a.ce_rp, (void*)a.ce_col, (void*)a.se_rp, (void*)a.se_col, (void*)a.se_pairs, (void*)a.colors,
+    for (void* p : {(void*)a.lo, (void*)a.ce_rp, (void*)a.ce_col, (void*)a.se_rp, (void*)a.se_col, (void*)a.se_pairs,
+                    (void*)a.up_deg, (void*)a.up_col, (void*)a.colors,
                     (void*)a.counts, (void*)a.cost, (void*)a.stats})
       if (p) cudaFree(p);
     if (a.h_counts) cudaFreeHost(a.h_counts);
@@ -813,17 +824,25 @@ int mpld_decompose_batch(int32_t n_layouts, const int32_t* layout_offsets, int32
 namespace {
 // The pipelined host submit; stitch edges either as CSR (se_rowptr, se_col) or
 // as n_pairs (u, v) pairs (se_pairs, se_rowptr == NULL), built into CSR on the device.
+// Conflict edges as CSR (ce_rowptr, ce_col) or as the upper triangle
+// (ce_up_deg, ce_up_col with n_ce_up entries; ce_rowptr == NULL), built into
+// the symmetric CSR on the device.
 int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
                  const int32_t* ce_rowptr, const int32_t* ce_col, const int32_t* se_rowptr, const int32_t* se_col,
                  const int32_t* se_pairs, int64_t n_pairs, int32_t k, double alpha, int64_t max_steps,
                  uint32_t flags, int32_t* colors, int64_t* n_conflicts, int64_t* n_stitches, double* cost,
-                 int64_t* stats, int64_t* ticket) {
+                 int64_t* stats, int64_t* ticket, const unsigned char* ce_up_deg = nullptr,
+                 const int32_t* ce_up_col = nullptr, int64_t n_ce_up = 0) {
   if (!ctx || !ticket) return fail(MPLD_ERR_ARG, "bad context / ticket pointer");
   int w_stitch = 0;
   int rc = check_scalars(n, k, alpha, &w_stitch);
   if (rc != MPLD_OK) return rc;
   const bool pairs = se_rowptr == nullptr;
-  if (n_layouts < 1 || !layout_offsets || !ce_rowptr || (n > 0 && !colors) || !n_conflicts || !n_stitches || !cost)
+  const bool upper = ce_rowptr == nullptr;
+  if (upper && (n_ce_up < 0 || n_ce_up > (int64_t)INT32_MAX / 2 || (n > 0 && !ce_up_deg) || (n_ce_up > 0 && !ce_up_col)))
+    return fail(MPLD_ERR_ARG, "bad upper-triangle conflict edges");
+  if (n_layouts < 1 || !layout_offsets || (!upper && !ce_rowptr) || (n > 0 && !colors) || !n_conflicts ||
+      !n_stitches || !cost)
     return fail(MPLD_ERR_ARG, "bad argument (NULL pointer or n_layouts < 1)");
   if (layout_offsets[0] != 0 || layout_offsets[n_layouts] != n)
     return fail(MPLD_ERR_ARG, "layout_offsets must start at 0 and end at n");
@@ -836,8 +855,8 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
         return fail(MPLD_ERR_GRAPH, "stitch pair " + std::to_string(i / 2) + " out of range or a self loop");
     }
   }
-  const int64_t m_ce = ce_rowptr[n], m_se = pairs ? 2 * n_pairs : se_rowptr[n];
-  if (m_ce < 0 || m_se < 0 || (m_ce > 0 && !ce_col) || (!pairs && m_se > 0 && !se_col))
+  const int64_t m_ce = upper ? 2 * n_ce_up : ce_rowptr[n], m_se = pairs ? 2 * n_pairs : se_rowptr[n];
+  if (m_ce < 0 || m_se < 0 || (!upper && m_ce > 0 && !ce_col) || (!pairs && m_se > 0 && !se_col))
     return fail(MPLD_ERR_ARG, "bad CSR row pointer / column array");
   std::lock_guard<std::mutex> lk(ctx->mu);
   cudaSetDevice(ctx->device);
@@ -856,13 +875,26 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
     a.cap_pairs = std::max<int64_t>(m_se, a.cap_pairs * 3 / 2);
     if (grow(&a.se_pairs, a.cap_pairs) != cudaSuccess) rc = fail(MPLD_ERR_NOMEM, "async staging allocation failed");
   }
+  if (rc == MPLD_OK && upper && n_ce_up > a.cap_up) {
+    a.cap_up = std::max<int64_t>(n_ce_up, a.cap_up * 3 / 2);
+    if (grow(&a.up_col, a.cap_up) != cudaSuccess) rc = fail(MPLD_ERR_NOMEM, "async staging allocation failed");
+  }
+  if (rc == MPLD_OK && upper && n > a.cap_up_n) {
+    a.cap_up_n = std::max<int64_t>(n, a.cap_up_n * 3 / 2);
+    if (grow(&a.up_deg, a.cap_up_n) != cudaSuccess) rc = fail(MPLD_ERR_NOMEM, "async staging allocation failed");
+  }
   if (rc != MPLD_OK) return rc;
   cudaStream_t up = ctx->s_h2d, ks = ctx->stream, down = ctx->s_d2h;
   cudaError_t e = cudaMemcpyAsync(a.lo, layout_offsets, sizeof(int) * (n_layouts + 1), cudaMemcpyHostToDevice, up);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(a.ce_rp, ce_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && !upper)
+    e = cudaMemcpyAsync(a.ce_rp, ce_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, up);
   if (e == cudaSuccess && !pairs)
     e = cudaMemcpyAsync(a.se_rp, se_rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, up);
-  if (e == cudaSuccess && m_ce) e = cudaMemcpyAsync(a.ce_col, ce_col, sizeof(int) * m_ce, cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && !upper && m_ce)
+    e = cudaMemcpyAsync(a.ce_col, ce_col, sizeof(int) * m_ce, cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && upper && n > 0) e = cudaMemcpyAsync(a.up_deg, ce_up_deg, n, cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && upper && n_ce_up)
+    e = cudaMemcpyAsync(a.up_col, ce_up_col, sizeof(int) * n_ce_up, cudaMemcpyHostToDevice, up);
   if (e == cudaSuccess && m_se)
     e = pairs ? cudaMemcpyAsync(a.se_pairs, se_pairs, sizeof(int) * m_se, cudaMemcpyHostToDevice, up)
               : cudaMemcpyAsync(a.se_col, se_col, sizeof(int) * m_se, cudaMemcpyHostToDevice, up);
@@ -871,6 +903,11 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
   if (e != cudaSuccess) return cuda_fail(e, "async H2D copy");
   rc = order_after_last(ctx, ks);
   if (rc != MPLD_OK) return rc;
+  if (upper) {  // the CE CSR on the device (scratch: se_rp as the upper row pointer, deg / q0 / bsum)
+    e = launch_ce_from_upper(n, (int)n_ce_up, a.up_deg, a.up_col, a.se_rp, a.ce_rp, a.ce_col, ctx->deg, ctx->q0,
+                             (int*)ctx->bsum, ctx->build_err, ks);
+    if (e != cudaSuccess) return cuda_fail(e, "conflict CSR build");
+  }
   if (pairs) {  // the SE CSR on the device (scratch: the workspace's deg / q0 / bsum, rewritten later)
     e = launch_se_from_pairs(n, (int)n_pairs, a.se_pairs, a.se_rp, a.se_col, ctx->deg, ctx->q0, (int*)ctx->bsum, ks);
     if (e != cudaSuccess) return cuda_fail(e, "stitch CSR build");
@@ -921,6 +958,16 @@ int mpld_decompose_batch_pairs_async(mpld_context* ctx, int32_t n_layouts, const
   return submit_async(ctx, n_layouts, layout_offsets, n, ce_rowptr, ce_col, nullptr, nullptr, stitch_pairs,
                       n_stitch_pairs, k, alpha, max_steps, flags, colors, n_conflicts, n_stitches, cost, stats,
                       ticket);
+}
+
+int mpld_decompose_batch_upper_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
+                                     const uint8_t* ce_up_deg, int64_t n_ce_edges, const int32_t* ce_up_col,
+                                     int64_t n_stitch_pairs, const int32_t* stitch_pairs, int32_t k, double alpha,
+                                     int64_t max_steps, uint32_t flags, int32_t* colors, int64_t* n_conflicts,
+                                     int64_t* n_stitches, double* cost, int64_t* stats, int64_t* ticket) {
+  return submit_async(ctx, n_layouts, layout_offsets, n, nullptr, nullptr, nullptr, nullptr, stitch_pairs,
+                      n_stitch_pairs, k, alpha, max_steps, flags, colors, n_conflicts, n_stitches, cost, stats,
+                      ticket, ce_up_deg, ce_up_col, n_ce_edges);
 }
 
 int mpld_wait(mpld_context* ctx, int64_t ticket) {

@@ -171,6 +171,8 @@ struct Workspace {
   unsigned epoch;     // this search call's tag for wq_flag
   unsigned spill_iters;  // a heavy unit's iterations before it may spill (multiple of 64; MPLD_HEAVY_SPILL)
   int tail_slots;        // cluster tails: frontier slots per CTA in use (MPLD_TAIL_SLOTS lowers it: tests)
+  int* build_err;        // set when a CSR built on the device (upper-triangle upload) saw bad input; the
+                         // simplification turns it into MPLD_ERR_GRAPH and clears it
 };
 
 // Layout of vertex v: the l with layout_off[l] <= v < layout_off[l+1] (binary
@@ -273,6 +275,8 @@ cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors,
                            int blocks, int threads, bool pdl);
 cudaError_t launch_se_from_pairs(int n, int m, const int* pairs, int* rp, int* col, int* deg, int* fill, int* bsum,
                                  cudaStream_t s);
+cudaError_t launch_ce_from_upper(int n, int m, const unsigned char* deg_up, const int* col_up, int* rp_up, int* rp,
+                                 int* col, int* full, int* fill, int* bsum, int* err, cudaStream_t s);
 bool recover_tail_available();  // the cluster tail kernel can be launched (cluster size support)
 int simplify_launches();        // kernels launch_simplify_components enqueues (1, or 3 with the cluster tail)
 cudaError_t configure_recover_tail();

@@ -36,7 +36,7 @@ EXPORTS = ["mpld_last_error", "mpld_version", "mpld_decompose", "mpld_decompose_
            "mpld_context_reset_timing", "mpld_kernel_count", "mpld_kernel_name", "mpld_context_kernel_time",
            "mpld_context_debug", "mpld_prepare_device", "mpld_search_device", "mpld_finish_device",
            "mpld_decompose_batch_async", "mpld_decompose_batch_pairs_async", "mpld_wait",
-           "mpld_shard_export", "mpld_shard_import"]
+           "mpld_shard_export", "mpld_shard_import", "mpld_decompose_batch_upper_async"]
 
 
 class MPLDError(RuntimeError):
@@ -91,6 +91,9 @@ def lib():
                                                    ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _i64p]
     L.mpld_wait.argtypes = [_vp, ctypes.c_int64]
     L.mpld_shard_export.argtypes = [_vp, _vp, _vp, _vp, _vp]
+    L.mpld_decompose_batch_upper_async.argtypes = [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp, ctypes.c_int64,
+                                                   _vp, ctypes.c_int64, _vp, ctypes.c_int32, ctypes.c_double,
+                                                   ctypes.c_int64, ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _i64p]
     L.mpld_shard_import.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp]
     _lib = L
     return L
@@ -102,7 +105,7 @@ def _check(rc: int):
 
 
 _TORCH_DTYPE = {np.dtype(np.int32): "torch.int32", np.dtype(np.int64): "torch.int64",
-                np.dtype(np.float64): "torch.float64"}
+                np.dtype(np.float64): "torch.float64", np.dtype(np.uint8): "torch.uint8"}
 
 
 def _check_tensor(t, dtype, what):
@@ -265,6 +268,38 @@ class Context:
         ptr = {key: _out_ptr(v, _OUT_DTYPES[key], key) for key, v in out.items()}
         t = ctypes.c_int64()
         _check(L.mpld_decompose_batch_pairs_async(self._h, n_layouts, lo_p, int(n), keep[1][0], keep[2][0], m, sp[0],
+                                                  int(k), float(alpha), int(max_steps), int(flags), ptr["colors"],
+                                                  ptr["n_conflicts"], ptr["n_stitches"], ptr["cost"], ptr["stats"],
+                                                  ctypes.byref(t)))
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[t.value] = (keep, out)
+        return t.value
+
+    def submit_upper(self, layout_offsets, n, ce_up_deg, ce_up_col, stitch_pairs, k, alpha, max_steps=0, flags=0,
+                     out=None):
+        """C ABI `mpld_decompose_batch_upper_async`: as `submit_pairs`, with the
+        conflict edges as the upper triangle of their CSR (ce_up_deg: uint8 [n]
+        counts of neighbours u > v; ce_up_col: int32 neighbours, rows ascending;
+        synth.upper_csr builds both); the symmetric CSR is built on the device."""
+        L = lib()
+        lo_p, lo = _host_ptr(layout_offsets)
+        n_layouts = int(len(lo) - 1) if not hasattr(lo, "numel") else int(lo.numel() - 1)
+        if out is None:
+            out = {"colors": np.empty(max(int(n), 0), dtype=np.int32),
+                   "n_conflicts": np.zeros(n_layouts, dtype=np.int64),
+                   "n_stitches": np.zeros(n_layouts, dtype=np.int64),
+                   "cost": np.zeros(n_layouts, dtype=np.float64),
+                   "stats": np.zeros(MPLD_STAT_LEN, dtype=np.int64)}
+        dg = _host_ptr(ce_up_deg, np.uint8, "ce_up_deg")
+        cu = _host_ptr(ce_up_col, np.int32, "ce_up_col")
+        sp = _host_ptr(stitch_pairs)
+        m_ce = int(cu[1].numel() if hasattr(cu[1], "numel") else np.asarray(cu[1]).size)
+        m_se = int(sp[1].numel() if hasattr(sp[1], "numel") else np.asarray(sp[1]).size) // 2
+        keep = [lo, dg, cu, sp]
+        ptr = {key: _out_ptr(v, _OUT_DTYPES[key], key) for key, v in out.items()}
+        t = ctypes.c_int64()
+        _check(L.mpld_decompose_batch_upper_async(self._h, n_layouts, lo_p, int(n), dg[0], m_ce, cu[0], m_se, sp[0],
                                                   int(k), float(alpha), int(max_steps), int(flags), ptr["colors"],
                                                   ptr["n_conflicts"], ptr["n_stitches"], ptr["cost"], ptr["stats"],
                                                   ctypes.byref(t)))

@@ -128,3 +128,23 @@ def concat(graphs, name: str = "batch") -> DecompGraph:
     return DecompGraph(n, cat(cr).astype(np.int32), cat(cc).astype(np.int32),
                        cat(sr).astype(np.int32), cat(sc).astype(np.int32), name=name,
                        layout_offsets=np.array(offs, dtype=np.int32))
+
+
+def upper_csr(g: DecompGraph):
+    """The upper triangle of the CE CSR (the input of
+    mpld_decompose_batch_upper_async): uint8 counts of the neighbours u > v of
+    every vertex v and those neighbours, rows ascending.  Raises if a vertex
+    has 256 or more larger neighbours."""
+    n = g.n
+    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(g.ce_rowptr.astype(np.int64)))
+    up = g.ce_col > src
+    deg = np.bincount(src[up], minlength=n) if n else np.zeros(0, np.int64)
+    if deg.size and deg.max() > 255:
+        raise ValueError("a vertex has more than 255 larger conflict neighbours")
+    return deg.astype(np.uint8), np.ascontiguousarray(g.ce_col[up], dtype=np.int32)
+
+
+def stitch_pairs(g: DecompGraph):
+    """Each stitch edge once, (u, v) with u < v, int32 [m, 2]."""
+    e = g.se_edges()
+    return np.ascontiguousarray(e, dtype=np.int32).reshape(-1, 2)

@@ -803,3 +803,51 @@ def test_k4_budget_hand_trace_through_the_c_abi(budget, steps, truncated, cost, 
     assert got["colors"].tolist() == colors
     assert (got["stats"]["steps"], got["stats"]["truncated"]) == (steps, truncated)
     assert int(got["n_conflicts"][0]) * 1000 == cost
+
+
+def test_upper_triangle_entry_point():
+    """mpld_decompose_batch_upper_async (conflict edges as the upper triangle
+    of their CSR with uint8 row lengths, stitch candidates as pairs, the
+    symmetric CSR built on the device) gives the oracle's colours and
+    per-layout counts; malformed triangles are reported as MPLD_ERR_GRAPH and
+    the context keeps working."""
+    graphs, k, alpha = synth.config_graphs(1)
+    b = synth.concat(graphs[:6])
+    ref = oracle.decompose(b, k, alpha, max_steps=0)
+    ctx = mp.Context(0, b.n, b.n_layouts)
+    deg, col = synth.upper_csr(b)
+    pairs = synth.stitch_pairs(b)
+    for flags in (mp.MPLD_FLAG_VALIDATE, 0):
+        r = ctx.wait(ctx.submit_upper(b.layout_offsets, b.n, deg, col, pairs, k, alpha, 0, flags))
+        assert np.array_equal(r["colors"], ref["colors"])
+        for li, (c, s_, cst) in enumerate(ref["per_layout"]):
+            assert (int(r["n_conflicts"][li]), int(r["n_stitches"][li]), float(r["cost"][li])) == (c, s_, cst)
+    # the device-built CSR equals the host one: a second graph with a denser triangle (k = 4 clusters)
+    g2 = synth.config_graphs(2, scale=0.05)[0][0]
+    ref2 = oracle.decompose(g2, 4, 0.1, max_steps=0)
+    d2, c2 = synth.upper_csr(g2)
+    r = ctx.wait(ctx.submit_upper(g2.layout_offsets, g2.n, d2, c2, synth.stitch_pairs(g2), 4, 0.1, 0,
+                                  mp.MPLD_FLAG_VALIDATE))
+    assert np.array_equal(r["colors"], ref2["colors"])
+    bad_cases = []
+    bc = col.copy()
+    bc[5] = b.n  # out of range
+    bad_cases.append((deg, bc))
+    bc = col.copy()
+    i = int(np.nonzero(deg > 1)[0][0])
+    a = int(deg[:i].astype(np.int64).sum())
+    bc[a], bc[a + 1] = bc[a + 1], bc[a]  # a row not ascending
+    bad_cases.append((deg, bc))
+    bd = deg.copy()
+    bd[i] -= 1  # row lengths that do not sum to the entries sent
+    bad_cases.append((bd, col))
+    bc = col.copy()
+    bc[a] = i  # a self loop / an entry below the row's vertex
+    bad_cases.append((deg, bc))
+    for dd, cc in bad_cases:
+        with pytest.raises(mp.MPLDError) as ei:
+            ctx.wait(ctx.submit_upper(b.layout_offsets, b.n, dd, cc, pairs, k, alpha, 0, 0))
+        assert ei.value.code == 2
+    r = ctx.wait(ctx.submit_upper(b.layout_offsets, b.n, deg, col, pairs, k, alpha, 0, mp.MPLD_FLAG_VALIDATE))
+    assert np.array_equal(r["colors"], ref["colors"])
+    ctx.close()
