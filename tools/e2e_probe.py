@@ -41,6 +41,24 @@ t0 = time.perf_counter()
 for i in range(N):
     ctx.wait(sub(i))
 print("serial submit+wait ms/step", (time.perf_counter() - t0) * 1e3 / N)
+# the upper-triangle upload (uint8 row lengths + upper columns; CSR built on the device)
+ud, uc = synth.upper_csr(b)
+ud, uc = pin(ud), pin(uc)
+subu = lambda i: ctx.submit_upper(h[0], b.n, ud, uc, pairs, k, alpha, 0, 1, out=outs[i % 3])  # noqa: E731
+for i in range(3):
+    ctx.wait(subu(i))
+t0 = time.perf_counter()
+for i in range(N):
+    ctx.wait(subu(i))
+print("upper: serial submit+wait ms/step", (time.perf_counter() - t0) * 1e3 / N)
+t0 = time.perf_counter()
+for i in range(N):
+    t = subu(i)
+    if i >= 2:
+        ctx.wait(t - 2)
+ctx.wait(t - 1)
+ctx.wait(t)
+print("upper: pipelined ms/step", (time.perf_counter() - t0) * 1e3 / N)
 t0 = time.perf_counter()
 ts = []
 for i in range(N):
