@@ -1134,18 +1134,8 @@ __global__ void __launch_bounds__(256) mpld_shard_import(long long m, const int*
 }
 
 // ---------------------------------------------------------------------------
-// Stitch edges given as pairs (mpld_decompose_batch_pairs_async): the SE CSR
-// is built on the device — degrees, an exclusive scan, a scatter, each row
-// sorted (rows hold one or two segments' worth of entries).
-__global__ void __launch_bounds__(256) mpld_se_degrees(int m, const int* __restrict__ pairs, int* deg) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    atomicAdd(&deg[pairs[2 * i]], 1);
-    atomicAdd(&deg[pairs[2 * i + 1]], 1);
-  }
-}
-
-constexpr int kScanTileI = 8192;  // elements per block of the int scan (1024 threads x 8)
-
+// Block-wide integer scan (the graph build below): returns the inclusive
+// prefix, `total` the block's sum.
 __device__ __forceinline__ int block_scan_int(int x, int* s_w, int& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int y = x;
@@ -1172,187 +1162,202 @@ __device__ __forceinline__ int block_scan_int(int x, int* s_w, int& total) {
   return r;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(1024) mpld_scan_sums(int n, const T* in, int* bsum) {
-  __shared__ int s_w[32];
-  const size_t base = (size_t)blockIdx.x * kScanTileI;
-  int x = 0;
-  for (int j = 0; j < kScanTileI / 1024; ++j) {
-    const size_t i = base + (size_t)j * 1024 + threadIdx.x;
-    if (i < (size_t)n) x += (int)in[i];
-  }
-  int total;
-  block_scan_int(x, s_w, total);
-  if (threadIdx.x == 0) bsum[blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(1024) mpld_scan_offsets(int nb, int* bsum) {
-  __shared__ int s_w[32];
-  int carry = 0;
-  for (int b0 = 0; b0 < nb; b0 += 1024) {  // exclusive scan of the block sums, in place
-    const int i = b0 + threadIdx.x;
-    const int x = i < nb ? bsum[i] : 0;
-    int total;
-    const int inc = block_scan_int(x, s_w, total);
-    if (i < nb) bsum[i] = carry + inc - x;
-    carry += total;
-  }
-}
-
-// out[i] = sum of in[0..i) for i in [0, n]; in and out may not alias
-template <typename T>
-__global__ void __launch_bounds__(1024) mpld_scan_apply(int n, const T* in, const int* bsum, int* out) {
-  __shared__ int s_w[32];
-  const size_t base = (size_t)blockIdx.x * kScanTileI;
-  int carry = bsum[blockIdx.x];
-  for (int j = 0; j < kScanTileI / 1024; ++j) {
-    const size_t i = base + (size_t)j * 1024 + threadIdx.x;
-    const int x = i < (size_t)n ? (int)in[i] : 0;
-    int total;
-    const int inc = block_scan_int(x, s_w, total);
-    if (i < (size_t)n) out[i] = carry + inc - x;
-    if (i == (size_t)n - 1) out[n] = carry + inc;
-    carry += total;
-  }
-}
-
-__global__ void __launch_bounds__(256) mpld_se_scatter(int m, const int* __restrict__ pairs,
-                                                       const int* __restrict__ rp, int* fill, int* col) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const int u = pairs[2 * i], v = pairs[2 * i + 1];
-    col[rp[u] + atomicAdd(&fill[u], 1)] = v;
-    col[rp[v] + atomicAdd(&fill[v], 1)] = u;
-  }
-}
-
-__global__ void __launch_bounds__(256) mpld_se_sort_rows(int n, const int* __restrict__ rp, int* col) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const int a = rp[v], b = rp[v + 1];
-    for (int i = a + 1; i < b; ++i) {  // insertion sort (rows are short)
-      const int x = col[i];
-      int j = i - 1;
-      while (j >= a && col[j] > x) {
-        col[j + 1] = col[j];
-        --j;
-      }
-      col[j + 1] = x;
-    }
-  }
-}
-
-// The conflict edges given as the upper triangle of the CSR
-// (mpld_decompose_batch_upper_async): deg_up[v] (uint8) = number of CE
-// neighbours u > v, col_up = those neighbours, rows in vertex order, each row
-// strictly ascending.  rp_up = exclusive scan of deg_up.  An entry is valid
-// iff v < u < n and it is larger than its row predecessor; invalid entries
-// (and rows running past the m copied entries) are dropped and flag *err
-// (MPLD_ERR_GRAPH through the simplification's validation).
+// An upper-triangle entry p of row v (row start a) is valid iff v < u < n and
+// it is larger than its row predecessor.
 __device__ __forceinline__ bool up_entry_ok(const int* col_up, int a, int p, int v, int n) {
   const int u = __ldg(&col_up[p]);
   return u > v && u < n && (p == a || u > __ldg(&col_up[p - 1]));
 }
 
-__global__ void __launch_bounds__(256) mpld_up_degrees(int n, int m, const int* __restrict__ rp_up,
-                                                       const int* __restrict__ col_up, int* full, int* err) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const int a = rp_up[v], b0 = rp_up[v + 1], b = min(b0, m);
-    int cnt = 0;
-    bool bad = b0 > m;
-    for (int p = a; p < b; ++p) {
-      if (up_entry_ok(col_up, a, p, v, n)) {
-        ++cnt;
-        atomicAdd(&full[__ldg(&col_up[p])], 1);  // the lower entry v of row u
-      } else {
-        bad = true;
-      }
-    }
-    if (cnt) atomicAdd(&full[v], cnt);
-    if (bad) atomicOr(err, 1);
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && rp_up[n] != m) atomicOr(err, 1);
+// ---------------------------------------------------------------------------
+// The graph build of the compact uploads in ONE cooperative launch (one
+// 1024-thread CTA per SM, five grid barriers): CTA c owns the vertex range
+// [c n / G, (c+1) n / G).
+//   P1 zero the counters of its range; its sum of deg_up
+//   P2 exclusive scan of deg_up over its range (base = the earlier CTAs'
+//      sums) -> rp_up; for every valid upper entry (v, u): cnt_ce[u]++ (the
+//      lower entry), cnt_ce[v] += its valid entries; stitch pairs (grid-stride):
+//      cnt_se[u]++, cnt_se[v]++
+//   P3 its sums of cnt_ce and cnt_se
+//   P4 scans -> ce_rp, se_rp
+//   P5 scatter: lower CE entries by atomics on fill_ce, the upper ones in
+//      order after them; SE entries by atomics on fill_se
+//   P6 sort the lower part of every CE row and every SE row (insertion sort:
+//      rows are short)
+// Validity of an upper entry and error reporting as mpld_up_degrees.
+__device__ __forceinline__ int block_scan_excl(int x, int* s_w, int& total) {
+  return block_scan_int(x, s_w, total) - x;
 }
 
-// rows of the symmetric CSR: the lower entries (u < v) of row v first, written
-// by atomics (fill), then row v's own upper entries in order
-__global__ void __launch_bounds__(256) mpld_up_scatter(int n, int m, const int* __restrict__ rp_up,
-                                                       const int* __restrict__ col_up, const int* __restrict__ rp,
-                                                       int* fill, int* col) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const int a = rp_up[v], b = min(rp_up[v + 1], m);
-    int nup = 0;
-    for (int p = a; p < b; ++p) nup += up_entry_ok(col_up, a, p, v, n) ? 1 : 0;
-    int at = rp[v + 1] - nup;
-    for (int p = a; p < b; ++p) {
-      if (!up_entry_ok(col_up, a, p, v, n)) continue;
-      const int u = __ldg(&col_up[p]);
-      col[at++] = u;
-      col[rp[u] + atomicAdd(&fill[u], 1)] = v;
+__device__ __forceinline__ void build_insertion_sort(int* col, int a, int b) {
+  for (int i = a + 1; i < b; ++i) {
+    const int x = col[i];
+    int j = i - 1;
+    while (j >= a && col[j] > x) {
+      col[j + 1] = col[j];
+      --j;
     }
+    col[j + 1] = x;
   }
 }
 
-__global__ void __launch_bounds__(256) mpld_sort_prefix(int n, const int* __restrict__ rp,
-                                                        const int* __restrict__ len, int* col) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const int a = rp[v], b = a + len[v];
-    for (int i = a + 1; i < b; ++i) {  // insertion sort of the lower entries (rows are short)
-      const int x = col[i];
-      int j = i - 1;
-      while (j >= a && col[j] > x) {
-        col[j + 1] = col[j];
-        --j;
-      }
-      col[j + 1] = x;
+__global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
+  __shared__ int s_w[32];
+  __shared__ int s_base[3];
+  GridBarrier grid(b.bar, gridDim.x, b.epoch0);
+  const int G = gridDim.x, c = blockIdx.x, n = b.n;
+  const int v0 = (int)((long long)n * c / G), v1 = (int)((long long)n * (c + 1) / G);
+  const bool ce = b.deg_up != nullptr, se = b.m_se >= 0;
+  // P1
+  int sum_up = 0;
+  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    if (ce) {
+      b.cnt_ce[v] = 0;
+      b.fill_ce[v] = 0;
+      sum_up += b.deg_up[v];
     }
+    if (se) {
+      b.cnt_se[v] = 0;
+      b.fill_se[v] = 0;
+    }
+  }
+  {
+    int total;
+    block_scan_int(sum_up, s_w, total);
+    if (threadIdx.x == 0) b.tot[c] = total;
+  }
+  grid.sync();
+  // P2
+  if (ce) {
+    if (threadIdx.x == 0) {
+      int base = 0;
+      for (int i = 0; i < c; ++i) base += __ldcg(&b.tot[i]);
+      s_base[0] = base;
+    }
+    __syncthreads();
+    int carry = s_base[0];
+    bool bad = false;
+    for (int v00 = v0; v00 < v1; v00 += blockDim.x) {
+      const int v = v00 + threadIdx.x;
+      const int d = v < v1 ? (int)b.deg_up[v] : 0;
+      int total;
+      const int a = carry + block_scan_excl(d, s_w, total);
+      carry += total;
+      if (v >= v1) continue;
+      b.rp_up[v] = a;
+      const int e1 = min(a + d, b.m_up);
+      bad |= a + d > b.m_up;
+      int cnt = 0;
+      for (int p = a; p < e1; ++p) {
+        if (up_entry_ok(b.col_up, a, p, v, n)) {
+          ++cnt;
+          atomicAdd(&b.cnt_ce[__ldg(&b.col_up[p])], 1);
+        } else {
+          bad = true;
+        }
+      }
+      if (cnt) atomicAdd(&b.cnt_ce[v], cnt);
+    }
+    if (c == G - 1 && threadIdx.x == 0) {
+      b.rp_up[n] = carry;
+      if (carry != b.m_up) bad = true;
+    }
+    if (bad) atomicOr(b.err, 1);
+  }
+  if (se)
+    for (int i = c * blockDim.x + threadIdx.x; i < b.m_se; i += G * blockDim.x) {
+      atomicAdd(&b.cnt_se[__ldg(&b.se_pairs[2 * i])], 1);
+      atomicAdd(&b.cnt_se[__ldg(&b.se_pairs[2 * i + 1])], 1);
+    }
+  grid.sync();
+  // P3
+  {
+    int sc = 0, ss = 0;
+    for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+      if (ce) sc += __ldcg(&b.cnt_ce[v]);
+      if (se) ss += __ldcg(&b.cnt_se[v]);
+    }
+    int total;
+    block_scan_int(sc, s_w, total);
+    if (threadIdx.x == 0) b.tot[G + c] = total;
+    block_scan_int(ss, s_w, total);
+    if (threadIdx.x == 0) b.tot[2 * G + c] = total;
+  }
+  grid.sync();
+  // P4
+  if (threadIdx.x < 2) {
+    int base = 0;
+    for (int i = 0; i < c; ++i) base += __ldcg(&b.tot[(1 + threadIdx.x) * G + i]);
+    s_base[1 + threadIdx.x] = base;
+  }
+  __syncthreads();
+  for (int q = 0; q < 2; ++q) {
+    if (!(q == 0 ? ce : se)) continue;
+    const int* cnt = q == 0 ? b.cnt_ce : b.cnt_se;
+    int* rp = q == 0 ? b.ce_rp : b.se_rp;
+    int carry = s_base[1 + q];
+    for (int v00 = v0; v00 < v1; v00 += blockDim.x) {
+      const int v = v00 + threadIdx.x;
+      const int d = v < v1 ? __ldcg(&cnt[v]) : 0;
+      int total;
+      const int a = carry + block_scan_excl(d, s_w, total);
+      carry += total;
+      if (v < v1) rp[v] = a;
+    }
+    if (c == G - 1 && threadIdx.x == 0) rp[n] = carry;
+  }
+  grid.sync();
+  // P5
+  if (ce)
+    for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+      const int a = __ldcg(&b.rp_up[v]), e1 = min(__ldcg(&b.rp_up[v + 1]), b.m_up);
+      int nup = 0;
+      for (int p = a; p < e1; ++p) nup += up_entry_ok(b.col_up, a, p, v, n) ? 1 : 0;
+      int at = __ldcg(&b.ce_rp[v + 1]) - nup;
+      for (int p = a; p < e1; ++p) {
+        if (!up_entry_ok(b.col_up, a, p, v, n)) continue;
+        const int u = __ldg(&b.col_up[p]);
+        b.ce_col[at++] = u;
+        b.ce_col[__ldcg(&b.ce_rp[u]) + atomicAdd(&b.fill_ce[u], 1)] = v;
+      }
+    }
+  if (se)
+    for (int i = c * blockDim.x + threadIdx.x; i < b.m_se; i += G * blockDim.x) {
+      const int u = __ldg(&b.se_pairs[2 * i]), v = __ldg(&b.se_pairs[2 * i + 1]);
+      b.se_col[__ldcg(&b.se_rp[u]) + atomicAdd(&b.fill_se[u], 1)] = v;
+      b.se_col[__ldcg(&b.se_rp[v]) + atomicAdd(&b.fill_se[v], 1)] = u;
+    }
+  grid.sync();
+  // P6
+  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    if (ce) {
+      const int a = __ldcg(&b.ce_rp[v]);
+      build_insertion_sort(b.ce_col, a, a + __ldcg(&b.fill_ce[v]));
+    }
+    if (se) build_insertion_sort(b.se_col, __ldcg(&b.se_rp[v]), __ldcg(&b.se_rp[v + 1]));
   }
 }
 
 }  // namespace
 
+cudaError_t launch_graph_build(const GraphBuild& b, cudaStream_t s, int blocks) {
+  if (b.n <= 0) {
+    cudaError_t e = cudaSuccess;
+    if (b.deg_up) e = cudaMemsetAsync(b.ce_rp, 0, sizeof(int), s);
+    if (e == cudaSuccess && b.m_se >= 0) e = cudaMemsetAsync(b.se_rp, 0, sizeof(int), s);
+    return e;
+  }
+  return launch_ex(mpld_graph_build, dim3(blocks), dim3(1024), 0, s, false, true, b);
+}
+
+int coop_blocks_build(int num_sms) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_graph_build, 1024, 0);
+  return std::min(per_sm, 1) * num_sms;
+}
+
 bool pdl_enabled() { return g_pdl; }
 
-// Symmetric CE CSR (rp [n+1], col [2m]) from the upper triangle (deg_up, col_up
-// [m]); rp_up [n+1], full / fill [n] and bsum are scratch, *err is set on invalid input.
-cudaError_t launch_ce_from_upper(int n, int m, const unsigned char* deg_up, const int* col_up, int* rp_up, int* rp,
-                                 int* col, int* full, int* fill, int* bsum, int* err, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(full, 0, sizeof(int) * (size_t)(n > 0 ? n : 1), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(fill, 0, sizeof(int) * (size_t)(n > 0 ? n : 1), s);
-  if (e != cudaSuccess) return e;
-  if (n <= 0) return cudaMemsetAsync(rp, 0, sizeof(int), s);
-  const int gb = 1184;
-  const int nb = (n + kScanTileI - 1) / kScanTileI;
-  mpld_scan_sums<unsigned char><<<nb, 1024, 0, s>>>(n, deg_up, bsum);
-  mpld_scan_offsets<<<1, 1024, 0, s>>>(nb, bsum);
-  mpld_scan_apply<unsigned char><<<nb, 1024, 0, s>>>(n, deg_up, bsum, rp_up);
-  mpld_up_degrees<<<gb, 256, 0, s>>>(n, m, rp_up, col_up, full, err);
-  mpld_scan_sums<int><<<nb, 1024, 0, s>>>(n, full, bsum);
-  mpld_scan_offsets<<<1, 1024, 0, s>>>(nb, bsum);
-  mpld_scan_apply<int><<<nb, 1024, 0, s>>>(n, full, bsum, rp);
-  mpld_up_scatter<<<gb, 256, 0, s>>>(n, m, rp_up, col_up, rp, fill, col);
-  mpld_sort_prefix<<<gb, 256, 0, s>>>(n, rp, fill, col);
-  return cudaGetLastError();
-}
-
-// SE CSR from m pairs (ids already checked on the host): deg / fill are [n]
-// scratch arrays, bsum [n / kScanTileI + 2]
-cudaError_t launch_se_from_pairs(int n, int m, const int* pairs, int* rp, int* col, int* deg, int* fill, int* bsum,
-                                 cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(deg, 0, sizeof(int) * (size_t)(n > 0 ? n : 1), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(fill, 0, sizeof(int) * (size_t)(n > 0 ? n : 1), s);
-  if (e != cudaSuccess) return e;
-  if (n <= 0) return cudaMemsetAsync(rp, 0, sizeof(int), s);
-  const int gb = 1184;
-  if (m > 0) mpld_se_degrees<<<gb, 256, 0, s>>>(m, pairs, deg);
-  const int nb = (n + kScanTileI - 1) / kScanTileI;
-  mpld_scan_sums<int><<<nb, 1024, 0, s>>>(n, deg, bsum);
-  mpld_scan_offsets<<<1, 1024, 0, s>>>(nb, bsum);
-  mpld_scan_apply<int><<<nb, 1024, 0, s>>>(n, deg, bsum, rp);
-  if (m > 0) {
-    mpld_se_scatter<<<gb, 256, 0, s>>>(m, pairs, rp, fill, col);
-    mpld_se_sort_rows<<<gb, 256, 0, s>>>(n, rp, col);
-  }
-  return cudaGetLastError();
-}
 void set_pdl(bool enable) { g_pdl = enable; }
 
 bool g_tail_ok = false;

@@ -136,7 +136,11 @@ struct mpld_context {
   // cross-stream ordering: calls share the workspace and control block, so a
   // call enqueued on a stream other than the previous call's waits for that
   // call's last operation (ev_last, recorded at the end of every entry point)
-  int* build_err = nullptr;  // device flag of the CSR builds from uploaded triangles (Workspace::build_err)
+  int* build_err = nullptr;  // device flag of the CSR builds from compact uploads (Workspace::build_err)
+  unsigned* build_bar = nullptr;  // grid-barrier counter of mpld_graph_build (never reset)
+  int* build_tot = nullptr;       // [3 * blocks_build] per-CTA sums
+  unsigned build_epoch = 0;       // barriers passed on build_bar so far
+  int blocks_build = 0;
   cudaEvent_t ev_last = nullptr;
   cudaStream_t last_stream = nullptr;
   bool has_last = false;
@@ -187,7 +191,7 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
     cudaError_t e = cudaSuccess;
     for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->roots, &ctx->porder, &ctx->hcomp, &ctx->hcost,
                     &ctx->wide}) {
-      e = grow(p, cap);
+      e = grow(p, cap + 1);  // + 1: q1 is the graph build's [n+1] row-pointer scratch
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
     if (grow(&ctx->est, cap) != cudaSuccess || grow(&ctx->bsum, cap / kScanTile + 2) != cudaSuccess)
@@ -535,11 +539,15 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     return fail(MPLD_ERR_NOMEM, "control block allocation failed");
   }
   cudaMemset(ctx->ctl, 0, sizeof(Control));
-  if (cudaMalloc((void**)&ctx->build_err, sizeof(int)) != cudaSuccess) {
+  ctx->blocks_build = coop_blocks_build(ctx->num_sms);
+  if (ctx->blocks_build <= 0 || cudaMalloc((void**)&ctx->build_err, sizeof(int)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->build_bar, sizeof(unsigned)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->build_tot, sizeof(int) * 3 * (size_t)ctx->blocks_build) != cudaSuccess) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_NOMEM, "control block allocation failed");
   }
   cudaMemset(ctx->build_err, 0, sizeof(int));
+  cudaMemset(ctx->build_bar, 0, sizeof(unsigned));
   if (cudaMalloc((void**)&ctx->wq, sizeof(WorkItem) * 2 * kWQCap) != cudaSuccess ||
       cudaMalloc((void**)&ctx->wq_flag, sizeof(unsigned long long) * 2 * kWQCap) != cudaSuccess ||
       cudaMalloc((void**)&ctx->hslot, sizeof(HeavySlot) * kSlots) != cudaSuccess) {
@@ -603,7 +611,8 @@ void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->bmask, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->roots, (void*)ctx->crec, (void*)ctx->pmask, (void*)ctx->porder, (void*)ctx->hcomp,
-                  (void*)ctx->hcost, (void*)ctx->wide, (void*)ctx->build_err, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
+                  (void*)ctx->hcost, (void*)ctx->wide, (void*)ctx->build_err, (void*)ctx->build_bar,
+                  (void*)ctx->build_tot, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
                   (void*)ctx->est, (void*)ctx->bsum,
                   (void*)ctx->h_lo,
                   (void*)ctx->h_ce_rp, (void*)ctx->h_ce_col, (void*)ctx->h_se_rp, (void*)ctx->h_se_col,
@@ -903,14 +912,31 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
   if (e != cudaSuccess) return cuda_fail(e, "async H2D copy");
   rc = order_after_last(ctx, ks);
   if (rc != MPLD_OK) return rc;
-  if (upper) {  // the CE CSR on the device (scratch: se_rp as the upper row pointer, deg / q0 / bsum)
-    e = launch_ce_from_upper(n, (int)n_ce_up, a.up_deg, a.up_col, a.se_rp, a.ce_rp, a.ce_col, ctx->deg, ctx->q0,
-                             (int*)ctx->bsum, ctx->build_err, ks);
-    if (e != cudaSuccess) return cuda_fail(e, "conflict CSR build");
-  }
-  if (pairs) {  // the SE CSR on the device (scratch: the workspace's deg / q0 / bsum, rewritten later)
-    e = launch_se_from_pairs(n, (int)n_pairs, a.se_pairs, a.se_rp, a.se_col, ctx->deg, ctx->q0, (int*)ctx->bsum, ks);
-    if (e != cudaSuccess) return cuda_fail(e, "stitch CSR build");
+  if (upper || pairs) {  // the CE CSR from its upper triangle and / or the SE CSR from pairs, on the device
+    // (one cooperative launch; scratch: the workspace arrays, rewritten by the hot path later)
+    GraphBuild gb{};
+    gb.n = n;
+    gb.m_up = upper ? (int)n_ce_up : 0;
+    gb.deg_up = upper ? a.up_deg : nullptr;
+    gb.col_up = a.up_col;
+    gb.ce_rp = a.ce_rp;
+    gb.ce_col = a.ce_col;
+    gb.m_se = pairs ? (int)n_pairs : -1;
+    gb.se_pairs = a.se_pairs;
+    gb.se_rp = a.se_rp;
+    gb.se_col = a.se_col;
+    gb.rp_up = ctx->q1;
+    gb.cnt_ce = ctx->deg;
+    gb.cnt_se = ctx->q0;
+    gb.fill_ce = ctx->roots;
+    gb.fill_se = ctx->porder;
+    gb.tot = ctx->build_tot;
+    gb.err = ctx->build_err;
+    gb.bar = ctx->build_bar;
+    gb.epoch0 = ctx->build_epoch;
+    e = launch_graph_build(gb, ks, ctx->blocks_build);
+    if (e != cudaSuccess) return cuda_fail(e, "graph build");
+    if (n > 0) ctx->build_epoch += kBuildBarriers;
   }
   GraphView g{n, n_layouts, a.lo, a.ce_rp, a.ce_col, a.se_rp, a.se_col};
   rc = run_pipeline(ctx, ks, g, k, w_stitch, alpha, (long long)max_steps, flags, a.colors, a.counts, a.cost,

@@ -87,6 +87,9 @@ struct GridBarrier {
   unsigned epoch;
   __device__ __forceinline__ GridBarrier(unsigned* c) : count(c), nblocks(gridDim.x), epoch(0) {}
   __device__ __forceinline__ GridBarrier(unsigned* c, unsigned nb) : count(c), nblocks(nb), epoch(0) {}
+  // a counter that is not reset between launches: this launch's barriers continue at epoch0
+  __device__ __forceinline__ GridBarrier(unsigned* c, unsigned nb, unsigned epoch0)
+      : count(c), nblocks(nb), epoch(epoch0) {}
   __device__ __forceinline__ void sync() {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -273,10 +276,33 @@ cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_s
 cudaError_t configure_search_heavy(int num_sms, int* blocks);  // blocks[3]: resident grids of the heavy kernels (k = 2..4)
 cudaError_t launch_recover(const GraphView& g, Workspace ws, int k, int* colors, Outputs out, cudaStream_t s,
                            int blocks, int threads, bool pdl);
-cudaError_t launch_se_from_pairs(int n, int m, const int* pairs, int* rp, int* col, int* deg, int* fill, int* bsum,
-                                 cudaStream_t s);
-cudaError_t launch_ce_from_upper(int n, int m, const unsigned char* deg_up, const int* col_up, int* rp_up, int* rp,
-                                 int* col, int* full, int* fill, int* bsum, int* err, cudaStream_t s);
+// One cooperative launch building on the device the symmetric CE CSR from its
+// upper triangle (deg_up != NULL) and / or the SE CSR from stitch pairs
+// (m_se >= 0): see kernels_graph.cu mpld_graph_build.
+struct GraphBuild {
+  int n;
+  int m_up;                    // upper-triangle entries (deg_up != NULL)
+  const unsigned char* deg_up;
+  const int* col_up;
+  int* ce_rp;                  // [n+1] out
+  int* ce_col;                 // [2 m_up] out
+  int m_se;                    // stitch pairs (-1: no SE build)
+  const int* se_pairs;
+  int* se_rp;                  // [n+1] out
+  int* se_col;                 // [2 m_se] out
+  int* rp_up;                  // [n+1] scratch
+  int* cnt_ce;                 // [n] scratch: CE row lengths, then the lower entries placed
+  int* cnt_se;                 // [n] scratch: SE row lengths, then the entries placed
+  int* fill_ce;                // [n] scratch
+  int* fill_se;                // [n] scratch
+  int* tot;                    // [3 * blocks] scratch: per-CTA sums
+  int* err;                    // set on invalid input (Workspace::build_err)
+  unsigned* bar;               // grid-barrier counter (never reset: epoch0)
+  unsigned epoch0;
+};
+constexpr unsigned kBuildBarriers = 5;  // grid barriers per mpld_graph_build launch
+cudaError_t launch_graph_build(const GraphBuild& b, cudaStream_t s, int blocks);
+int coop_blocks_build(int num_sms);
 bool recover_tail_available();  // the cluster tail kernel can be launched (cluster size support)
 int simplify_launches();        // kernels launch_simplify_components enqueues (1, or 3 with the cluster tail)
 cudaError_t configure_recover_tail();
