@@ -830,7 +830,11 @@ constexpr int kQueueLow = MPLD_QUEUE_LOW;
 #ifndef MPLD_SEED_INCUMBENT
 #define MPLD_SEED_INCUMBENT 1
 #endif
-constexpr bool kSeedIncumbent = MPLD_SEED_INCUMBENT != 0;  // greedy starting incumbent of heavy components  // the work queue is fed while it holds fewer items than this
+constexpr bool kSeedIncumbent = MPLD_SEED_INCUMBENT != 0;  // greedy starting incumbent of heavy components
+#ifndef MPLD_PAIR_BOUND
+#define MPLD_PAIR_BOUND 1
+#endif
+constexpr bool kPairBound = MPLD_PAIR_BOUND != 0;  // exact mode: the matching term of the lower bound  // the work queue is fed while it holds fewer items than this
 constexpr unsigned kSpillCheck = 64;  // spill / slot-sync checks every this many iterations (power of two),
                                       // from Workspace::spill_iters on
 
@@ -1155,10 +1159,39 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
       live_counts<K, W>(B, U, Z, Ol);
       // bound (R7): the clique deficit is at most the live columns inside
       // cliques, so it is summed only when it can change the key comparison
+      // exact mode may prune with any valid lower bound: R7's, plus (kPairBound)
+      // a matching of adjacent columns whose only live row has the same mask
+      // (each such pair costs >= one more conflict, on edges no other term
+      // charges; pinned by brute force in tests/test_bound_pins.py)
       const int base = cost + kCostUnits * O::popc(Z);
-      const bool undecided = heavy_clique_min<K>() > 0 && key_less<kTwo>(base, P, gcost, gP) &&
-                             !key_less<kTwo>(base + kCostUnits * O::popc(U & ~Z & clu), P, gcost, gP);
-      const int lb = undecided ? base + kCostUnits * clique_deficit<K, W>(B, U, Z, cl, 1, ncl) : base;
+      const W cliq_live = heavy_clique_min<K>() > 0 ? (U & ~Z & clu) : W(0);
+      const int hi_terms = (kPairBound ? (O::popc(Ol) >> 1) : 0) + O::popc(cliq_live);
+      const bool undecided = hi_terms > 0 && key_less<kTwo>(base, P, gcost, gP) &&
+                             !key_less<kTwo>(base + kCostUnits * hi_terms, P, gcost, gP);
+      int lb = base;
+      if (undecided) {
+        W M = 0;  // matched columns
+        int pairs = 0;
+        if (kPairBound) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            const W S = Ol & ~B[c];  // columns whose only live row is r(., c)
+            W T = S;
+            while (T) {
+              const int x = O::ffs(T);
+              T &= T - W(1);
+              const W N = adj[x] & S & ~M;
+              if (N) {
+                const W pb = (W(1) << x) | (W(1) << O::ffs(N));
+                M |= pb;
+                T &= ~pb;
+                ++pairs;
+              }
+            }
+          }
+        }
+        lb = base + kCostUnits * (pairs + clique_deficit<K, W>(B, U & ~M, Z, cl, 1, ncl));
+      }
       const bool leaf = U == 0;
       const bool better = active && en && leaf && key_less<kTwo>(cost, P, gcost, gP);  // Alg. 1 line 5
       const bool ex = active && en && !leaf && key_less<kTwo>(lb, P, gcost, gP);      // bound (R7)

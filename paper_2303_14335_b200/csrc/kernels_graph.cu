@@ -1170,9 +1170,9 @@ __device__ __forceinline__ bool up_entry_ok(const int* col_up, int a, int p, int
 }
 
 // ---------------------------------------------------------------------------
-// The graph build of the compact uploads in ONE cooperative launch (one
-// 1024-thread CTA per SM, five grid barriers): CTA c owns the vertex range
-// [c n / G, (c+1) n / G).
+// The graph build of the compact uploads in ONE cooperative launch (two
+// 1024-thread CTAs per SM, five grid barriers): CTA c owns the vertex range
+// [c n / G, (c+1) n / G), each thread a contiguous sub-range of it.
 //   P1 zero the counters of its range; its sum of deg_up
 //   P2 exclusive scan of deg_up over its range (base = the earlier CTAs'
 //      sums) -> rp_up; for every valid upper entry (v, u): cnt_ce[u]++ (the
@@ -1206,11 +1206,15 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
   __shared__ int s_base[3];
   GridBarrier grid(b.bar, gridDim.x, b.epoch0);
   const int G = gridDim.x, c = blockIdx.x, n = b.n;
+  // CTA c owns [v0, v1); thread t owns the contiguous sub-range [t0, t1) of it,
+  // so one block scan per phase gives every thread its running offset
   const int v0 = (int)((long long)n * c / G), v1 = (int)((long long)n * (c + 1) / G);
+  const int per = (v1 - v0 + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int t0 = min(v0 + (int)threadIdx.x * per, v1), t1 = min(t0 + per, v1);
   const bool ce = b.deg_up != nullptr, se = b.m_se >= 0;
   // P1
   int sum_up = 0;
-  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+  for (int v = t0; v < t1; ++v) {
     if (ce) {
       b.cnt_ce[v] = 0;
       b.fill_ce[v] = 0;
@@ -1221,9 +1225,10 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
       b.fill_se[v] = 0;
     }
   }
+  int excl_up;  // this thread's offset inside the CTA
   {
     int total;
-    block_scan_int(sum_up, s_w, total);
+    excl_up = block_scan_excl(sum_up, s_w, total);
     if (threadIdx.x == 0) b.tot[c] = total;
   }
   grid.sync();
@@ -1235,15 +1240,10 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
       s_base[0] = base;
     }
     __syncthreads();
-    int carry = s_base[0];
+    int a = s_base[0] + excl_up;
     bool bad = false;
-    for (int v00 = v0; v00 < v1; v00 += blockDim.x) {
-      const int v = v00 + threadIdx.x;
-      const int d = v < v1 ? (int)b.deg_up[v] : 0;
-      int total;
-      const int a = carry + block_scan_excl(d, s_w, total);
-      carry += total;
-      if (v >= v1) continue;
+    for (int v = t0; v < t1; ++v) {
+      const int d = b.deg_up[v];
       b.rp_up[v] = a;
       const int e1 = min(a + d, b.m_up);
       bad |= a + d > b.m_up;
@@ -1257,10 +1257,11 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
         }
       }
       if (cnt) atomicAdd(&b.cnt_ce[v], cnt);
+      a += d;
     }
-    if (c == G - 1 && threadIdx.x == 0) {
-      b.rp_up[n] = carry;
-      if (carry != b.m_up) bad = true;
+    if (c == G - 1 && t1 == v1 && t1 > t0) {  // the thread holding the last vertex
+      b.rp_up[n] = a;
+      if (a != b.m_up) bad = true;
     }
     if (bad) atomicOr(b.err, 1);
   }
@@ -1271,16 +1272,17 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
     }
   grid.sync();
   // P3
+  int sc = 0, ss = 0;
+  for (int v = t0; v < t1; ++v) {
+    if (ce) sc += __ldcg(&b.cnt_ce[v]);
+    if (se) ss += __ldcg(&b.cnt_se[v]);
+  }
+  int excl_ce, excl_se;
   {
-    int sc = 0, ss = 0;
-    for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-      if (ce) sc += __ldcg(&b.cnt_ce[v]);
-      if (se) ss += __ldcg(&b.cnt_se[v]);
-    }
     int total;
-    block_scan_int(sc, s_w, total);
+    excl_ce = block_scan_excl(sc, s_w, total);
     if (threadIdx.x == 0) b.tot[G + c] = total;
-    block_scan_int(ss, s_w, total);
+    excl_se = block_scan_excl(ss, s_w, total);
     if (threadIdx.x == 0) b.tot[2 * G + c] = total;
   }
   grid.sync();
@@ -1291,26 +1293,27 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
     s_base[1 + threadIdx.x] = base;
   }
   __syncthreads();
-  for (int q = 0; q < 2; ++q) {
-    if (!(q == 0 ? ce : se)) continue;
-    const int* cnt = q == 0 ? b.cnt_ce : b.cnt_se;
-    int* rp = q == 0 ? b.ce_rp : b.se_rp;
-    int carry = s_base[1 + q];
-    for (int v00 = v0; v00 < v1; v00 += blockDim.x) {
-      const int v = v00 + threadIdx.x;
-      const int d = v < v1 ? __ldcg(&cnt[v]) : 0;
-      int total;
-      const int a = carry + block_scan_excl(d, s_w, total);
-      carry += total;
-      if (v < v1) rp[v] = a;
+  if (ce) {
+    int a = s_base[1] + excl_ce;
+    for (int v = t0; v < t1; ++v) {
+      b.ce_rp[v] = a;
+      a += __ldcg(&b.cnt_ce[v]);
     }
-    if (c == G - 1 && threadIdx.x == 0) rp[n] = carry;
+    if (c == G - 1 && t1 == v1 && t1 > t0) b.ce_rp[n] = a;
+  }
+  if (se) {
+    int a = s_base[2] + excl_se;
+    for (int v = t0; v < t1; ++v) {
+      b.se_rp[v] = a;
+      a += __ldcg(&b.cnt_se[v]);
+    }
+    if (c == G - 1 && t1 == v1 && t1 > t0) b.se_rp[n] = a;
   }
   grid.sync();
   // P5
   if (ce)
-    for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-      const int a = __ldcg(&b.rp_up[v]), e1 = min(__ldcg(&b.rp_up[v + 1]), b.m_up);
+    for (int v = t0; v < t1; ++v) {
+      const int a = __ldcg(&b.rp_up[v]), e1 = min(a + (int)b.deg_up[v], b.m_up);
       int nup = 0;
       for (int p = a; p < e1; ++p) nup += up_entry_ok(b.col_up, a, p, v, n) ? 1 : 0;
       int at = __ldcg(&b.ce_rp[v + 1]) - nup;
@@ -1329,7 +1332,7 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
     }
   grid.sync();
   // P6
-  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+  for (int v = t0; v < t1; ++v) {
     if (ce) {
       const int a = __ldcg(&b.ce_rp[v]);
       build_insertion_sort(b.ce_col, a, a + __ldcg(&b.fill_ce[v]));
@@ -1353,7 +1356,7 @@ cudaError_t launch_graph_build(const GraphBuild& b, cudaStream_t s, int blocks) 
 int coop_blocks_build(int num_sms) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_graph_build, 1024, 0);
-  return std::min(per_sm, 1) * num_sms;
+  return std::min(per_sm, 2) * num_sms;
 }
 
 bool pdl_enabled() { return g_pdl; }

@@ -44,10 +44,11 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 enum KernelId { K_SIMPLIFY = 0, K_DISCOVER, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_PREP, K_SEARCH_WIDE,
-                K_COUNT };
+                K_BUILD, K_COUNT };
 const char* kKernelNames[K_COUNT] = {"mpld_simplify_components", "mpld_component_discover",
                                      "mpld_exact_cover_search", "mpld_exact_cover_search_heavy", "mpld_recover",
-                                     "mpld_evaluate", "mpld_recover_prep", "mpld_exact_cover_search_wide"};
+                                     "mpld_evaluate", "mpld_recover_prep", "mpld_exact_cover_search_wide",
+                                     "mpld_graph_build"};
 
 constexpr int kCoopThreads = 1024;
 #ifndef MPLD_SEPARATE_PREP
@@ -934,8 +935,10 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
     gb.err = ctx->build_err;
     gb.bar = ctx->build_bar;
     gb.epoch0 = ctx->build_epoch;
+    TimedLaunch tb(ctx, K_BUILD, ks);
     e = launch_graph_build(gb, ks, ctx->blocks_build);
     if (e != cudaSuccess) return cuda_fail(e, "graph build");
+    tb.done();
     if (n > 0) ctx->build_epoch += kBuildBarriers;
   }
   GraphView g{n, n_layouts, a.lo, a.ce_rp, a.ce_col, a.se_rp, a.se_col};

@@ -59,6 +59,13 @@ for i in range(N):
 ctx.wait(t - 1)
 ctx.wait(t)
 print("upper: pipelined ms/step", (time.perf_counter() - t0) * 1e3 / N)
+ctx.reset_timing()
+ctx.set_timing(True)
+for i in range(N):
+    ctx.wait(subu(i))
+ctx.set_timing(False)
+kt = ctx.kernel_times()
+print("upper: device us per submit", {k: round(v[0] / v[1] * 1e3, 1) for k, v in kt.items() if v[1]})
 t0 = time.perf_counter()
 ts = []
 for i in range(N):
