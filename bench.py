@@ -589,7 +589,9 @@ def main():
         for _ in range(args.steps):
             step()
         torch.cuda.synchronize()
-        print(json.dumps({"profile_run": True, "stats": st}))
+        dbg = ctx.debug()  # search nodes of the last call: total, heavy (for ncu's instructions per node)
+        print(json.dumps({"profile_run": True, "stats": st, "last_call_nodes": int(dbg[87]),
+                          "last_call_heavy_nodes": int(dbg[85])}))
         return
 
     if world > 1:

@@ -296,7 +296,8 @@ int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* laun
  * out[19] largest per-component step count, out[20..51] per round (0..15) / recovery
  * level (16..31) start stamps, out[52..83] their frontier sizes,
  * out[84] slowest discovery (cycles << 16 | n), out[86] slowest light search
- * (cycles << 24 | steps << 8 | n), out[85,87,88] unused, out[89] the slowest
+ * (cycles << 24 | steps << 8 | n), out[85] search nodes of the warp-parallel
+ * (heavy) search, out[87] search nodes in total, out[88] unused, out[89] the slowest
  * heavy component (cycles), out[90] the slowest heavy warp (cycles over all its
  * components), out[91] the slowest heavy component's size, out[92] component-search seeds,
  * out[93] heavy components, out[94] components, out[95] truncated searches.

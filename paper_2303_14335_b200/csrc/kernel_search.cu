@@ -832,7 +832,7 @@ constexpr int kQueueLow = MPLD_QUEUE_LOW;
 #endif
 constexpr bool kSeedIncumbent = MPLD_SEED_INCUMBENT != 0;  // greedy starting incumbent of heavy components
 #ifndef MPLD_PAIR_BOUND
-#define MPLD_PAIR_BOUND 1
+#define MPLD_PAIR_BOUND 0  // measured slower (configs[2] 1.24-1.34 -> 1.56-1.62 ms, configs[1] +10 us): off
 #endif
 constexpr bool kPairBound = MPLD_PAIR_BOUND != 0;  // exact mode: the matching term of the lower bound  // the work queue is fed while it holds fewer items than this
 constexpr unsigned kSpillCheck = 64;  // spill / slot-sync checks every this many iterations (power of two),
@@ -1863,6 +1863,7 @@ __global__ void __launch_bounds__(32, 8) mpld_exact_cover_search_heavy(GraphView
   }
   if (lane == 0 && acc.steps) {
     atomicAdd(&ctl->steps, acc.steps);
+    atomicAdd(&ctl->steps_heavy, acc.steps);
     atomicMax(&ctl->max_steps_comp, acc.max);
   }
   if (lane == 0 && acc.capped) atomicAdd(&ctl->truncated, acc.capped);

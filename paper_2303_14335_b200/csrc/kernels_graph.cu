@@ -71,6 +71,17 @@ constexpr int kTC = MPLD_CLUSTER;                // CTAs of the recovery's clust
 constexpr int kClusterTailMax = MPLD_CLUSTER_TAIL_ITEMS * kTC * 1024;  // levels up to this size go to the cluster tail
 constexpr int kGroup = MPLD_GROUP;  // frontiers up to kGroup * blockDim items: the first kGroup CTAs, group barriers
 constexpr int kStitchDeg = 1 << 29;  // live degree of stitch vertices: never reaches k (never hidden, R8)
+#ifndef MPLD_PACKED_PRED
+#define MPLD_PACKED_PRED 1
+#endif
+// Recovery state of a hidden vertex v.  Packed (default): ONE 32-bit word in
+// deg[v] = (hidden predecessors still uncoloured) | popped-before bits << 8,
+// bit t = CE entry t of the row (t < 24) pops before v or is kept.  The count
+// fits 8 bits: v had < k live neighbours when it was hidden and every
+// predecessor is one of them, so it is < k <= 4.  Unpacked: the count in
+// deg[v] and 64 bits in bmask[v].  Entries past the mask compare pop keys.
+constexpr bool kPackedPred = MPLD_PACKED_PRED != 0;
+constexpr int kPredBits = kPackedPred ? 24 : 64;
 
 __device__ __forceinline__ void stamp(Control* ctl, int i) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -329,7 +340,7 @@ __device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q,
             const bool before = pop_key(hu[j][t], pu[j][t]) > kv[j];  // popped before v, or kept
             cnt[j] += (hu[j][t] >= 0 && before) ? 1 : 0;
             const int rel = e[j] + t - e0[j];
-            if (rel < 64 && before) bm[j] |= 1ull << rel;
+            if (rel < kPredBits && before) bm[j] |= 1ull << rel;
           } else {
             if (u[j][t] < v[j] && hu[j][t] == -1) seed[j] = false;
             past |= u[j][t] > v[j];
@@ -342,8 +353,12 @@ __device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q,
     for (int j = 0; j < kPF; ++j) {
       if (v[j] >= n || !(mode & (kv[j] == ~0ull ? 1 : 2))) continue;
       if (kv[j] != ~0ull) {
-        w.deg[v[j]] = cnt[j];
-        w.bmask[v[j]] = bm[j];
+        if (kPackedPred) {
+          w.deg[v[j]] = cnt[j] | (int)((unsigned)bm[j] << 8);
+        } else {
+          w.deg[v[j]] = cnt[j];
+          w.bmask[v[j]] = bm[j];
+        }
         if (cnt[j] == 0) cq_push(Q, 1, v[j], &ctl->rq[0], w.q0);
       } else {
         // stitch neighbours (stitch vertices only; rows ascending)
@@ -752,10 +767,11 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
     for (int j = 0; j < kP; ++j) {
       const int i = t0 + j * blockDim.x + threadIdx.x;
       v[j] = i < cnt ? frontier_item(s_in, s_cnt, g_in, i) : -1;
-      bm[j] = v[j] >= 0 ? __ldcg(&w.bmask[v[j]]) : 0ull;
+      bm[j] = v[j] < 0 ? 0ull
+                       : (kPackedPred ? (unsigned long long)((unsigned)__ldcg(&w.deg[v[j]]) >> 8) : __ldcg(&w.bmask[v[j]]));
       e[j] = e0[j] = v[j] >= 0 ? __ldg(&g.ce_rp[v[j]]) : 0;
       e1[j] = v[j] >= 0 ? __ldg(&g.ce_rp[v[j] + 1]) : 0;
-      kv[j] = e1[j] - e0[j] > 64 ? pop_key(__ldcg(&w.hround[v[j]]), __ldcg(&w.prio[v[j]])) : 0ull;  // long rows only
+      kv[j] = e1[j] - e0[j] > kPredBits ? pop_key(__ldcg(&w.hround[v[j]]), __ldcg(&w.prio[v[j]])) : 0ull;  // long rows
       used[j] = 0u;
     }
     while (true) {
@@ -774,7 +790,7 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
 #pragma unroll
         for (int t = 0; t < kNb; ++t) {  // popped before v (or kept): the final pass's bit, past 64 the keys
           const int rel = e[j] + t - e0[j];
-          before[j][t] = u[j][t] >= 0 && (rel < 64 ? ((bm[j] >> rel) & 1ull) != 0ull
+          before[j][t] = u[j][t] >= 0 && (rel < kPredBits ? ((bm[j] >> rel) & 1ull) != 0ull
                                                    : pop_key(__ldcg(&w.hround[u[j][t]]), __ldcg(&w.prio[u[j][t]])) > kv[j]);
         }
 #pragma unroll
@@ -789,7 +805,7 @@ __device__ void recover_level(const GraphView& g, const Workspace& w, int k, int
           if (u[j][t] < 0) continue;
           if (before[j][t]) {
             if (x[j][t] >= 0) used[j] |= 1u << x[j][t];
-          } else if (x[j][t] == 1) {  // v was u's last predecessor
+          } else if ((x[j][t] & 0xff) == 1) {  // v was u's last predecessor
             cq_push(Q, qo, u[j][t], ocnt, oarr);
           }
         }
@@ -927,8 +943,9 @@ template <typename Push>
 __device__ __forceinline__ void recover_vertex(const GraphView& g, const Workspace& w, int k, int* colors, int v,
                                                Push push) {
   const int e0 = __ldg(&g.ce_rp[v]), e1 = __ldg(&g.ce_rp[v + 1]);
-  const unsigned long long bm = __ldcg(&w.bmask[v]);
-  const unsigned long long kv = e1 - e0 > 64 ? pop_key(__ldcg(&w.hround[v]), __ldcg(&w.prio[v])) : 0ull;
+  const unsigned long long bm =
+      kPackedPred ? (unsigned long long)((unsigned)__ldcg(&w.deg[v]) >> 8) : __ldcg(&w.bmask[v]);
+  const unsigned long long kv = e1 - e0 > kPredBits ? pop_key(__ldcg(&w.hround[v]), __ldcg(&w.prio[v])) : 0ull;
   unsigned used = 0u;
   for (int e = e0; e < e1; e += kNb) {
     int u[kNb], x[kNb];
@@ -938,7 +955,7 @@ __device__ __forceinline__ void recover_vertex(const GraphView& g, const Workspa
 #pragma unroll
     for (int t = 0; t < kNb; ++t) {  // popped before v (or kept): the final pass's bit, past 64 the keys
       const int rel = e + t - e0;
-      before[t] = u[t] >= 0 && (rel < 64 ? ((bm >> rel) & 1ull) != 0ull
+      before[t] = u[t] >= 0 && (rel < kPredBits ? ((bm >> rel) & 1ull) != 0ull
                                          : pop_key(__ldcg(&w.hround[u[t]]), __ldcg(&w.prio[u[t]])) > kv);
     }
 #pragma unroll
@@ -948,7 +965,7 @@ __device__ __forceinline__ void recover_vertex(const GraphView& g, const Workspa
       if (u[t] < 0) continue;
       if (before[t]) {
         if (x[t] >= 0) used |= 1u << x[t];
-      } else if (x[t] == 1) {  // v was u's last predecessor
+      } else if ((x[t] & 0xff) == 1) {  // v was u's last predecessor
         push(u[t]);
       }
     }
@@ -1234,10 +1251,11 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
   grid.sync();
   // P2
   if (ce) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // the earlier CTAs' sums, 32 loads in flight
       int base = 0;
-      for (int i = 0; i < c; ++i) base += __ldcg(&b.tot[i]);
-      s_base[0] = base;
+      for (int i = threadIdx.x; i < c; i += 32) base += __ldcg(&b.tot[i]);
+      base = __reduce_add_sync(0xffffffffu, base);
+      if (threadIdx.x == 0) s_base[0] = base;
     }
     __syncthreads();
     int a = s_base[0] + excl_up;
@@ -1287,10 +1305,12 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
   }
   grid.sync();
   // P4
-  if (threadIdx.x < 2) {
+  if (threadIdx.x < 64) {  // warp q: the earlier CTAs' sums of array q
+    const int q = threadIdx.x >> 5;
     int base = 0;
-    for (int i = 0; i < c; ++i) base += __ldcg(&b.tot[(1 + threadIdx.x) * G + i]);
-    s_base[1 + threadIdx.x] = base;
+    for (int i = threadIdx.x & 31; i < c; i += 32) base += __ldcg(&b.tot[(1 + q) * G + i]);
+    base = __reduce_add_sync(0xffffffffu, base);
+    if ((threadIdx.x & 31) == 0) s_base[1 + q] = base;
   }
   __syncthreads();
   if (ce) {

@@ -1063,6 +1063,8 @@ int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
   v[18] = c.n_rounds;
   v[19] = c.max_steps_comp;
   for (int i = 0; i < 8; ++i) v[84 + i] = (int64_t)c.dbg[i];
+  v[85] = (int64_t)c.steps_heavy;
+  v[87] = (int64_t)c.steps;
   v[92] = c.n_seed;
   v[93] = c.n_heavy[0] + c.n_heavy[1];
   v[94] = c.n_comp;

@@ -53,6 +53,7 @@ struct Control {
   alignas(128) int truncated;  // components whose search hit max_steps
   int max_steps_comp;          // largest per-component step count
   unsigned long long steps;    // search nodes entered
+  unsigned long long steps_heavy;  // ... by the warp-parallel (heavy) search
   alignas(128) int n_heavy[2]; // exact mode: components handed to the warp-parallel search, per word class
                                // (32-bit: hcomp[0..), 64-bit: hcomp[n-1], hcomp[n-2], ...; reset per search call)
   int slot_next;               // spilled-component slots handed out (reset with n_heavy)
@@ -151,9 +152,11 @@ struct HeavySlot {
 };
 
 struct Workspace {
-  int* deg;        // live conflict degree (simplification), then hidden-predecessor count (recovery)
+  int* deg;        // live conflict degree (simplification), then the recovery state of a hidden vertex:
+                   // uncoloured hidden predecessors | popped-before bits << 8 (kernels_graph.cu kPackedPred)
   int* hround;     // -1 kept, else the round the vertex was hidden in
-  unsigned long long* bmask;  // recovery: bit t = CE entry t of the row pops before the vertex (or is kept)
+  unsigned long long* bmask;  // recovery, unpacked variant only (MPLD_PACKED_PRED=0): bit t = CE entry t of the
+                              // row pops before the vertex (or is kept)
   unsigned* prio;  // lowbias32(layout-local id), recovery priority (R9)
   int* q0;         // frontier queues (double-buffered)
   int* q1;
