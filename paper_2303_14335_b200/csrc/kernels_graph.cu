@@ -1151,34 +1151,6 @@ __global__ void __launch_bounds__(256) mpld_shard_import(long long m, const int*
 }
 
 // ---------------------------------------------------------------------------
-// Block-wide integer scan (the graph build below): returns the inclusive
-// prefix, `total` the block's sum.
-__device__ __forceinline__ int block_scan_int(int x, int* s_w, int& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int y = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int z = __shfl_up_sync(0xffffffffu, y, o);
-    if (lane >= o) y += z;
-  }
-  if (lane == 31) s_w[wid] = y;
-  __syncthreads();
-  if (wid == 0) {
-    int t = lane < nw ? s_w[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int z = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += z;
-    }
-    if (lane < nw) s_w[lane] = t;
-  }
-  __syncthreads();
-  total = s_w[nw - 1];
-  const int r = y + (wid ? s_w[wid - 1] : 0);  // inclusive
-  __syncthreads();
-  return r;
-}
-
 // An upper-triangle entry p of row v (row start a) is valid iff v < u < n and
 // it is larger than its row predecessor.
 __device__ __forceinline__ bool up_entry_ok(const int* col_up, int a, int p, int v, int n) {
@@ -1188,24 +1160,21 @@ __device__ __forceinline__ bool up_entry_ok(const int* col_up, int a, int p, int
 
 // ---------------------------------------------------------------------------
 // The graph build of the compact uploads in ONE cooperative launch (two
-// 1024-thread CTAs per SM, five grid barriers): CTA c owns the vertex range
-// [c n / G, (c+1) n / G), each thread a contiguous sub-range of it.
-//   P1 zero the counters of its range; its sum of deg_up
-//   P2 exclusive scan of deg_up over its range (base = the earlier CTAs'
-//      sums) -> rp_up; for every valid upper entry (v, u): cnt_ce[u]++ (the
-//      lower entry), cnt_ce[v] += its valid entries; stitch pairs (grid-stride):
-//      cnt_se[u]++, cnt_se[v]++
-//   P3 its sums of cnt_ce and cnt_se
+// 1024-thread CTAs per SM, five grid barriers).  CTA c owns the vertex range
+// [c n / G, (c+1) n / G); each of its warps a contiguous sub-range, walked in
+// chunks of 32 consecutive vertices (coalesced, warp scans).  One counter word
+// per vertex holds both degree counts (CE in the low 24 bits, SE above).
+//   P1 zero the counters; warp / CTA sums of deg_up
+//   P2 scan of deg_up -> rp_up; for every valid upper entry (v, u): count the
+//      lower entry of row u, v's own valid entries; stitch pairs
+//      (grid-stride): count both ends
+//   P3 warp / CTA sums of both degree counts
 //   P4 scans -> ce_rp, se_rp
-//   P5 scatter: lower CE entries by atomics on fill_ce, the upper ones in
-//      order after them; SE entries by atomics on fill_se
-//   P6 sort the lower part of every CE row and every SE row (insertion sort:
-//      rows are short)
-// Validity of an upper entry and error reporting as mpld_up_degrees.
-__device__ __forceinline__ int block_scan_excl(int x, int* s_w, int& total) {
-  return block_scan_int(x, s_w, total) - x;
-}
-
+//   P5 scatter: lower CE entries and SE entries by atomics on the fill word,
+//      the upper CE entries in order after the lower ones
+//   P6 sort the lower part of every CE row with >= 2 of them, every SE row
+//      with >= 2 entries (insertion sort: rows are short)
+// Validity of an upper entry and error reporting as up_entry_ok.
 __device__ __forceinline__ void build_insertion_sort(int* col, int a, int b) {
   for (int i = a + 1; i < b; ++i) {
     const int x = col[i];
@@ -1218,121 +1187,177 @@ __device__ __forceinline__ void build_insertion_sort(int* col, int a, int b) {
   }
 }
 
-__global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
+__device__ __forceinline__ int warp_scan_excl(int x, int& total) {
+  const int lane = threadIdx.x & 31;
+  int y = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int z = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) y += z;
+  }
+  total = __shfl_sync(0xffffffffu, y, 31);
+  return y - x;
+}
+
+constexpr int kCeMask = (1 << 24) - 1;  // CE count in a build counter word; SE count << 24
+
+__global__ void __launch_bounds__(1024, 1) mpld_graph_build(GraphBuild b) {
   __shared__ int s_w[32];
   __shared__ int s_base[3];
   GridBarrier grid(b.bar, gridDim.x, b.epoch0);
   const int G = gridDim.x, c = blockIdx.x, n = b.n;
-  // CTA c owns [v0, v1); thread t owns the contiguous sub-range [t0, t1) of it,
-  // so one block scan per phase gives every thread its running offset
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int v0 = (int)((long long)n * c / G), v1 = (int)((long long)n * (c + 1) / G);
-  const int per = (v1 - v0 + (int)blockDim.x - 1) / (int)blockDim.x;
-  const int t0 = min(v0 + (int)threadIdx.x * per, v1), t1 = min(t0 + per, v1);
+  const int wper = (((v1 - v0) + nw - 1) / nw + 31) & ~31;  // vertices per warp, whole chunks
+  const int w0 = min(v0 + wid * wper, v1), w1 = min(w0 + wper, v1);
   const bool ce = b.deg_up != nullptr, se = b.m_se >= 0;
+  int* cnt = b.cnt_ce;   // CE | SE << 24
+  int* fill = b.fill_ce;
   // P1
-  int sum_up = 0;
-  for (int v = t0; v < t1; ++v) {
-    if (ce) {
-      b.cnt_ce[v] = 0;
-      b.fill_ce[v] = 0;
-      sum_up += b.deg_up[v];
-    }
-    if (se) {
-      b.cnt_se[v] = 0;
-      b.fill_se[v] = 0;
-    }
+  int s_up = 0;
+  for (int v = w0 + lane; v < w1; v += 32) {
+    cnt[v] = 0;
+    fill[v] = 0;
+    if (ce) s_up += b.deg_up[v];
   }
-  int excl_up;  // this thread's offset inside the CTA
-  {
-    int total;
-    excl_up = block_scan_excl(sum_up, s_w, total);
-    if (threadIdx.x == 0) b.tot[c] = total;
+  s_up = __reduce_add_sync(0xffffffffu, s_up);
+  if (lane == 0) s_w[wid] = s_up;
+  __syncthreads();
+  int wbase_up = 0;  // this warp's offset inside the CTA
+  if (threadIdx.x < 32) {
+    int t;
+    const int e = warp_scan_excl(lane < nw ? s_w[lane] : 0, t);
+    if (lane < nw) s_w[lane] = e;
+    if (lane == 0) b.tot[c] = t;
   }
+  __syncthreads();
+  wbase_up = s_w[wid];
+  __syncthreads();
   grid.sync();
   // P2
   if (ce) {
-    if (threadIdx.x < 32) {  // the earlier CTAs' sums, 32 loads in flight
+    if (threadIdx.x < 32) {
       int base = 0;
-      for (int i = threadIdx.x; i < c; i += 32) base += __ldcg(&b.tot[i]);
+      for (int i = lane; i < c; i += 32) base += __ldcg(&b.tot[i]);
       base = __reduce_add_sync(0xffffffffu, base);
-      if (threadIdx.x == 0) s_base[0] = base;
+      if (lane == 0) s_base[0] = base;
     }
     __syncthreads();
-    int a = s_base[0] + excl_up;
+    int carry = s_base[0] + wbase_up;
     bool bad = false;
-    for (int v = t0; v < t1; ++v) {
-      const int d = b.deg_up[v];
+    for (int vv = w0; vv < w1; vv += 32) {
+      const int v = vv + lane;
+      const int d = v < w1 ? (int)b.deg_up[v] : 0;
+      int t;
+      const int a = carry + warp_scan_excl(d, t);
+      carry += t;
+      if (v >= w1) continue;
       b.rp_up[v] = a;
       const int e1 = min(a + d, b.m_up);
       bad |= a + d > b.m_up;
-      int cnt = 0;
+      int k = 0;
       for (int p = a; p < e1; ++p) {
         if (up_entry_ok(b.col_up, a, p, v, n)) {
-          ++cnt;
-          atomicAdd(&b.cnt_ce[__ldg(&b.col_up[p])], 1);
+          ++k;
+          atomicAdd(&cnt[__ldg(&b.col_up[p])], 1);  // the lower entry v of row u
         } else {
           bad = true;
         }
       }
-      if (cnt) atomicAdd(&b.cnt_ce[v], cnt);
-      a += d;
-    }
-    if (c == G - 1 && t1 == v1 && t1 > t0) {  // the thread holding the last vertex
-      b.rp_up[n] = a;
-      if (a != b.m_up) bad = true;
+      if (k) atomicAdd(&cnt[v], k);
+      if (v == n - 1) {  // the last vertex closes the upper row pointer
+        b.rp_up[n] = a + d;
+        if (a + d != b.m_up) bad = true;
+      }
     }
     if (bad) atomicOr(b.err, 1);
   }
   if (se)
     for (int i = c * blockDim.x + threadIdx.x; i < b.m_se; i += G * blockDim.x) {
-      atomicAdd(&b.cnt_se[__ldg(&b.se_pairs[2 * i])], 1);
-      atomicAdd(&b.cnt_se[__ldg(&b.se_pairs[2 * i + 1])], 1);
+      atomicAdd(&cnt[__ldg(&b.se_pairs[2 * i])], 1 << 24);
+      atomicAdd(&cnt[__ldg(&b.se_pairs[2 * i + 1])], 1 << 24);
     }
   grid.sync();
   // P3
   int sc = 0, ss = 0;
-  for (int v = t0; v < t1; ++v) {
-    if (ce) sc += __ldcg(&b.cnt_ce[v]);
-    if (se) ss += __ldcg(&b.cnt_se[v]);
+  for (int v = w0 + lane; v < w1; v += 32) {
+    const int x = __ldcg(&cnt[v]);
+    sc += x & kCeMask;
+    ss += x >> 24;
   }
-  int excl_ce, excl_se;
-  {
-    int total;
-    excl_ce = block_scan_excl(sc, s_w, total);
-    if (threadIdx.x == 0) b.tot[G + c] = total;
-    excl_se = block_scan_excl(ss, s_w, total);
-    if (threadIdx.x == 0) b.tot[2 * G + c] = total;
-  }
-  grid.sync();
-  // P4
-  if (threadIdx.x < 64) {  // warp q: the earlier CTAs' sums of array q
-    const int q = threadIdx.x >> 5;
-    int base = 0;
-    for (int i = threadIdx.x & 31; i < c; i += 32) base += __ldcg(&b.tot[(1 + q) * G + i]);
-    base = __reduce_add_sync(0xffffffffu, base);
-    if ((threadIdx.x & 31) == 0) s_base[1 + q] = base;
+  sc = __reduce_add_sync(0xffffffffu, sc);
+  ss = __reduce_add_sync(0xffffffffu, ss);
+  __shared__ int s_w2[32];
+  if (lane == 0) {
+    s_w[wid] = sc;
+    s_w2[wid] = ss;
   }
   __syncthreads();
-  if (ce) {
-    int a = s_base[1] + excl_ce;
-    for (int v = t0; v < t1; ++v) {
-      b.ce_rp[v] = a;
-      a += __ldcg(&b.cnt_ce[v]);
-    }
-    if (c == G - 1 && t1 == v1 && t1 > t0) b.ce_rp[n] = a;
+  if (threadIdx.x < 32) {
+    int t;
+    int e = warp_scan_excl(lane < nw ? s_w[lane] : 0, t);
+    if (lane < nw) s_w[lane] = e;
+    if (lane == 0) b.tot[G + c] = t;
+    e = warp_scan_excl(lane < nw ? s_w2[lane] : 0, t);
+    if (lane < nw) s_w2[lane] = e;
+    if (lane == 0) b.tot[2 * G + c] = t;
   }
-  if (se) {
-    int a = s_base[2] + excl_se;
-    for (int v = t0; v < t1; ++v) {
-      b.se_rp[v] = a;
-      a += __ldcg(&b.cnt_se[v]);
+  __syncthreads();
+  const int wbase_ce = s_w[wid], wbase_se = s_w2[wid];
+  grid.sync();
+  // P4
+  if (threadIdx.x < 64) {  // warp q: the earlier CTAs' sums of count q
+    const int q = threadIdx.x >> 5;
+    int base = 0;
+    for (int i = lane; i < c; i += 32) base += __ldcg(&b.tot[(1 + q) * G + i]);
+    base = __reduce_add_sync(0xffffffffu, base);
+    if (lane == 0) s_base[1 + q] = base;
+    // the last CTA checks the totals: a count that overflowed its field (a CE
+    // degree >= 2^24, an SE degree >= 128) cannot leave both sums intact
+    if (c == G - 1 && lane == 0) {
+      const int all = base + __ldcg(&b.tot[(1 + q) * G + c]);
+      if (q == 0 && ce && all != 2 * b.m_up) atomicOr(b.err, 1);
+      if (q == 1 && se && all != 2 * b.m_se) atomicOr(b.err, 1);
     }
-    if (c == G - 1 && t1 == v1 && t1 > t0) b.se_rp[n] = a;
+  }
+  __syncthreads();
+  {
+    int cc = s_base[1] + wbase_ce, cs = s_base[2] + wbase_se;
+    for (int vv = w0; vv < w1; vv += 32) {
+      const int v = vv + lane;
+      const int x = v < w1 ? __ldcg(&cnt[v]) : 0;
+      int tc, ts;
+      const int ac = cc + warp_scan_excl(x & kCeMask, tc);
+      const int as = cs + warp_scan_excl(x >> 24, ts);
+      cc += tc;
+      cs += ts;
+      if (v < w1) {
+        if (ce) b.ce_rp[v] = ac;
+        if (se) b.se_rp[v] = as;
+        if (v == n - 1) {
+          if (ce) b.ce_rp[n] = ac + (x & kCeMask);
+          if (se) b.se_rp[n] = as + (x >> 24);
+        }
+      }
+    }
   }
   grid.sync();
-  // P5
+  // P5 (invalid input: an empty CSR instead, so that nothing reads past it;
+  // the error is reported through the simplification)
+  const bool failed = __ldcg(b.err) != 0;
+  if (failed) {
+    for (int v = w0 + lane; v < w1; v += 32) {
+      if (ce) b.ce_rp[v] = 0;
+      if (se) b.se_rp[v] = 0;
+    }
+    if (c == G - 1 && threadIdx.x == 0) {
+      if (ce) b.ce_rp[n] = 0;
+      if (se) b.se_rp[n] = 0;
+    }
+    return;
+  }
   if (ce)
-    for (int v = t0; v < t1; ++v) {
+    for (int v = w0 + lane; v < w1; v += 32) {
       const int a = __ldcg(&b.rp_up[v]), e1 = min(a + (int)b.deg_up[v], b.m_up);
       int nup = 0;
       for (int p = a; p < e1; ++p) nup += up_entry_ok(b.col_up, a, p, v, n) ? 1 : 0;
@@ -1341,23 +1366,24 @@ __global__ void __launch_bounds__(1024) mpld_graph_build(GraphBuild b) {
         if (!up_entry_ok(b.col_up, a, p, v, n)) continue;
         const int u = __ldg(&b.col_up[p]);
         b.ce_col[at++] = u;
-        b.ce_col[__ldcg(&b.ce_rp[u]) + atomicAdd(&b.fill_ce[u], 1)] = v;
+        b.ce_col[__ldcg(&b.ce_rp[u]) + (atomicAdd(&fill[u], 1) & kCeMask)] = v;
       }
     }
   if (se)
     for (int i = c * blockDim.x + threadIdx.x; i < b.m_se; i += G * blockDim.x) {
       const int u = __ldg(&b.se_pairs[2 * i]), v = __ldg(&b.se_pairs[2 * i + 1]);
-      b.se_col[__ldcg(&b.se_rp[u]) + atomicAdd(&b.fill_se[u], 1)] = v;
-      b.se_col[__ldcg(&b.se_rp[v]) + atomicAdd(&b.fill_se[v], 1)] = u;
+      b.se_col[__ldcg(&b.se_rp[u]) + (atomicAdd(&fill[u], 1 << 24) >> 24)] = v;
+      b.se_col[__ldcg(&b.se_rp[v]) + (atomicAdd(&fill[v], 1 << 24) >> 24)] = u;
     }
   grid.sync();
   // P6
-  for (int v = t0; v < t1; ++v) {
-    if (ce) {
+  for (int v = w0 + lane; v < w1; v += 32) {
+    const int f = __ldcg(&fill[v]);
+    if (ce && (f & kCeMask) >= 2) {
       const int a = __ldcg(&b.ce_rp[v]);
-      build_insertion_sort(b.ce_col, a, a + __ldcg(&b.fill_ce[v]));
+      build_insertion_sort(b.ce_col, a, a + (f & kCeMask));
     }
-    if (se) build_insertion_sort(b.se_col, __ldcg(&b.se_rp[v]), __ldcg(&b.se_rp[v + 1]));
+    if (se && (f >> 24) >= 2) build_insertion_sort(b.se_col, __ldcg(&b.se_rp[v]), __ldcg(&b.se_rp[v + 1]));
   }
 }
 

@@ -928,9 +928,7 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
     gb.se_col = a.se_col;
     gb.rp_up = ctx->q1;
     gb.cnt_ce = ctx->deg;
-    gb.cnt_se = ctx->q0;
     gb.fill_ce = ctx->roots;
-    gb.fill_se = ctx->porder;
     gb.tot = ctx->build_tot;
     gb.err = ctx->build_err;
     gb.bar = ctx->build_bar;

@@ -294,10 +294,8 @@ struct GraphBuild {
   int* se_rp;                  // [n+1] out
   int* se_col;                 // [2 m_se] out
   int* rp_up;                  // [n+1] scratch
-  int* cnt_ce;                 // [n] scratch: CE row lengths, then the lower entries placed
-  int* cnt_se;                 // [n] scratch: SE row lengths, then the entries placed
-  int* fill_ce;                // [n] scratch
-  int* fill_se;                // [n] scratch
+  int* cnt_ce;                 // [n] scratch: row lengths, CE | SE << 24
+  int* fill_ce;                // [n] scratch: entries placed, CE | SE << 24
   int* tot;                    // [3 * blocks] scratch: per-CTA sums
   int* err;                    // set on invalid input (Workspace::build_err)
   unsigned* bar;               // grid-barrier counter (never reset: epoch0)
