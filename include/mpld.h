@@ -197,8 +197,10 @@ int mpld_decompose_batch_async(mpld_context* ctx, int32_t n_layouts, const int32
  * (n+1)-entry SE row-pointer array, and the SE CSR is built on the device
  * (degrees, scan, scatter, rows sorted) before the hot path.  Pairs with an id
  * outside [0, n) or u == v are rejected on the host (MPLD_ERR_GRAPH); duplicate
- * pairs and CE ∩ SE are caught by MPLD_FLAG_VALIDATE on the built CSR.  Results
- * are identical to mpld_decompose_batch_async on the same graph. */
+ * pairs and CE ∩ SE are caught by MPLD_FLAG_VALIDATE on the built CSR.  A
+ * vertex with 128 or more stitch pairs is reported as MPLD_ERR_GRAPH (the
+ * device build counts them in 8 bits).  Results are identical to
+ * mpld_decompose_batch_async on the same graph. */
 int mpld_decompose_batch_pairs_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_offsets, int32_t n,
                                      const int32_t* ce_rowptr, const int32_t* ce_col, int64_t n_stitch_pairs,
                                      const int32_t* stitch_pairs, int32_t k, double alpha, int64_t max_steps,

@@ -1354,9 +1354,8 @@ __global__ void __launch_bounds__(1024, 1) mpld_graph_build(GraphBuild b) {
       if (ce) b.ce_rp[n] = 0;
       if (se) b.se_rp[n] = 0;
     }
-    return;
   }
-  if (ce)
+  if (ce && !failed)
     for (int v = w0 + lane; v < w1; v += 32) {
       const int a = __ldcg(&b.rp_up[v]), e1 = min(a + (int)b.deg_up[v], b.m_up);
       int nup = 0;
@@ -1369,14 +1368,15 @@ __global__ void __launch_bounds__(1024, 1) mpld_graph_build(GraphBuild b) {
         b.ce_col[__ldcg(&b.ce_rp[u]) + (atomicAdd(&fill[u], 1) & kCeMask)] = v;
       }
     }
-  if (se)
+  if (se && !failed)
     for (int i = c * blockDim.x + threadIdx.x; i < b.m_se; i += G * blockDim.x) {
       const int u = __ldg(&b.se_pairs[2 * i]), v = __ldg(&b.se_pairs[2 * i + 1]);
       b.se_col[__ldcg(&b.se_rp[u]) + (atomicAdd(&fill[u], 1 << 24) >> 24)] = v;
       b.se_col[__ldcg(&b.se_rp[v]) + (atomicAdd(&fill[v], 1 << 24) >> 24)] = u;
     }
-  grid.sync();
+  grid.sync();  // every CTA passes all kBuildBarriers barriers
   // P6
+  if (failed) return;
   for (int v = w0 + lane; v < w1; v += 32) {
     const int f = __ldcg(&fill[v]);
     if (ce && (f & kCeMask) >= 2) {

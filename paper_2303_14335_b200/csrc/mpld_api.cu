@@ -138,9 +138,8 @@ struct mpld_context {
   // call enqueued on a stream other than the previous call's waits for that
   // call's last operation (ev_last, recorded at the end of every entry point)
   int* build_err = nullptr;  // device flag of the CSR builds from compact uploads (Workspace::build_err)
-  unsigned* build_bar = nullptr;  // grid-barrier counter of mpld_graph_build (never reset)
+  unsigned* build_bar = nullptr;  // grid-barrier counter of mpld_graph_build (zeroed before every build)
   int* build_tot = nullptr;       // [3 * blocks_build] per-CTA sums
-  unsigned build_epoch = 0;       // barriers passed on build_bar so far
   int blocks_build = 0;
   cudaEvent_t ev_last = nullptr;
   cudaStream_t last_stream = nullptr;
@@ -932,12 +931,15 @@ int submit_async(mpld_context* ctx, int32_t n_layouts, const int32_t* layout_off
     gb.tot = ctx->build_tot;
     gb.err = ctx->build_err;
     gb.bar = ctx->build_bar;
-    gb.epoch0 = ctx->build_epoch;
+    gb.epoch0 = 0;
+    // the barrier counter starts every build at zero (a build that never
+    // finished cannot leave later ones waiting)
+    e = cudaMemsetAsync(ctx->build_bar, 0, sizeof(unsigned), ks);
+    if (e != cudaSuccess) return cuda_fail(e, "graph build");
     TimedLaunch tb(ctx, K_BUILD, ks);
     e = launch_graph_build(gb, ks, ctx->blocks_build);
     if (e != cudaSuccess) return cuda_fail(e, "graph build");
     tb.done();
-    if (n > 0) ctx->build_epoch += kBuildBarriers;
   }
   GraphView g{n, n_layouts, a.lo, a.ce_rp, a.ce_col, a.se_rp, a.se_col};
   rc = run_pipeline(ctx, ks, g, k, w_stitch, alpha, (long long)max_steps, flags, a.colors, a.counts, a.cost,

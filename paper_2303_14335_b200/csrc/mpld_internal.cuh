@@ -298,8 +298,8 @@ struct GraphBuild {
   int* fill_ce;                // [n] scratch: entries placed, CE | SE << 24
   int* tot;                    // [3 * blocks] scratch: per-CTA sums
   int* err;                    // set on invalid input (Workspace::build_err)
-  unsigned* bar;               // grid-barrier counter (never reset: epoch0)
-  unsigned epoch0;
+  unsigned* bar;               // grid-barrier counter (zeroed before the launch)
+  unsigned epoch0;             // barriers already counted on it (0)
 };
 constexpr unsigned kBuildBarriers = 5;  // grid barriers per mpld_graph_build launch
 cudaError_t launch_graph_build(const GraphBuild& b, cudaStream_t s, int blocks);

@@ -851,3 +851,24 @@ def test_upper_triangle_entry_point():
     r = ctx.wait(ctx.submit_upper(b.layout_offsets, b.n, deg, col, pairs, k, alpha, 0, mp.MPLD_FLAG_VALIDATE))
     assert np.array_equal(r["colors"], ref["colors"])
     ctx.close()
+
+
+def test_compact_upload_degree_limits():
+    """The device build of the compact uploads counts a vertex's stitch pairs
+    in 8 bits: a vertex with 200 stitch pairs is rejected (MPLD_ERR_GRAPH),
+    one with 60 (a 61-vertex component) is decomposed as the oracle does."""
+    ctx = mp.Context(0, 1 << 10, 1)
+    for d, ok in ((60, True), (200, False)):
+        n = d + 1
+        g = from_edges(n, [], [(0, i) for i in range(1, n)])
+        lo = np.array([0, n], np.int32)
+        deg, col = synth.upper_csr(g)
+        t = ctx.submit_upper(lo, n, deg, col, synth.stitch_pairs(g), 3, 0.1, 0, mp.MPLD_FLAG_VALIDATE)
+        if ok:
+            r = ctx.wait(t)
+            assert np.array_equal(r["colors"], oracle.decompose(g, 3, 0.1, max_steps=0)["colors"])
+        else:
+            with pytest.raises(mp.MPLDError) as ei:
+                ctx.wait(t)
+            assert ei.value.code == 2
+    ctx.close()
