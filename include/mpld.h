@@ -93,6 +93,10 @@ enum mpld_status {
                                * symmetry by two 64-bit multiset hashes (sum H(v,u) == sum H(u,v);
                                * an asymmetric graph passes with probability ~2^-64) */
 
+#define MPLD_FLAG_WHOLE_GRAPH 2u /* run the whole-graph pipeline only (level-synchronous kernels over all
+                                  * vertices) instead of the tile pipeline with it as fallback; results
+                                  * are identical — for A/B measurement and tests */
+
 /* stats[] layout */
 enum mpld_stat {
   MPLD_STAT_COMPONENTS = 0, /* components solved by the exact-cover search (Alg. 1 line 4) */
@@ -299,7 +303,12 @@ int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* laun
  * level (16..31) start stamps, out[52..83] their frontier sizes,
  * out[84] slowest discovery (cycles << 16 | n), out[86] slowest light search
  * (cycles << 24 | steps << 8 | n), out[85] search nodes of the warp-parallel
- * (heavy) search, out[87] search nodes in total, out[88] unused, out[89] the slowest
+ * (heavy) search, out[87] search nodes in total, out[88] the tile pipeline's gate
+ * (0: the tiles took the input; else the reasons the whole-graph pipeline
+ * recomputed it, bits: 1 row pointer / id out of range, 2 a piece larger than a
+ * window, 4 a neighbour outside its piece's window, 8 / 16 / 128 validation
+ * (rows, symmetry, layout offsets), 32 a component > 64 vertices, 64 invalid
+ * compact upload; -1: MPLD_FLAG_WHOLE_GRAPH / phase calls), out[89] the slowest
  * heavy component (cycles), out[90] the slowest heavy warp (cycles over all its
  * components), out[91] the slowest heavy component's size, out[92] component-search seeds,
  * out[93] heavy components, out[94] components, out[95] truncated searches.

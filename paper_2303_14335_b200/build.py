@@ -8,7 +8,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = ["csrc/kernels_graph.cu", "csrc/kernel_search.cu", "csrc/mpld_api.cu"]
+SOURCES = ["csrc/kernels_graph.cu", "csrc/kernel_search.cu", "csrc/kernel_tile.cu", "csrc/mpld_api.cu"]
 LIB = os.path.join(HERE, "lib", "libmpld.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC,-O2", "-shared"]

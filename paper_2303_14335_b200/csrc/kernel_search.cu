@@ -216,6 +216,7 @@ __device__ __forceinline__ void add_counts(const GraphView& g, int v0, int nc, i
 __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(GraphView g, Workspace w, int k,
                                                                               int sharded) {
   pdl_begin();
+  if (gated_off(w)) return;
   __shared__ WarpDisc s_disc[kCompWarps];
   WarpDisc& s = s_disc[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
                                                                            unsigned light_steps, long long* counts,
                                                                            int shard_index, int shard_count) {
   pdl_begin();
+  if (gated_off(w)) return;
   __shared__ LaneLight s_lane[kLaneWarps];
   LaneLight& L = s_lane[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -331,6 +333,7 @@ __global__ void __launch_bounds__(32) mpld_exact_cover_search_wide(GraphView g, 
                                                                    long long max_steps, int* colors,
                                                                    unsigned light_steps, long long* counts) {
   pdl_begin();
+  if (gated_off(w)) return;
   extern __shared__ __align__(16) unsigned char smem[];
   LaneWide& L = *reinterpret_cast<LaneWide*>(smem);
   const int lane = threadIdx.x & 31;
@@ -1350,6 +1353,7 @@ template <int K>
 __global__ void __launch_bounds__(32, 8) mpld_exact_cover_search_heavy(GraphView g, Workspace w, int w_stitch,
                                                                     int* colors, long long* counts) {
   pdl_begin();
+  if (gated_off(w)) return;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_pair[32];
   const int lane = threadIdx.x & 31;

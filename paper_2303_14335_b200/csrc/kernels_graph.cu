@@ -394,6 +394,7 @@ __device__ void final_pass(const GraphView& g, const Workspace& w, CtaQueues& Q,
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_simplify_components(GraphView g, Workspace w, int k,
                                                                     int* colors, long long* counts, int validate,
                                                                     int cluster_rounds, int separate_prep) {
+  if (gated_off(w)) return;  // after the tile pipeline, which took the input
   GridBarrier grid(&w.ctl->bar0);
   __shared__ CtaQueues Q;
   cq_init(Q);
@@ -672,6 +673,7 @@ constexpr int kTQ = 4096;  // frontier slots per CTA and parity of the cluster t
 
 __global__ void __launch_bounds__(1024) mpld_simplify_tail(GraphView g, Workspace w, int k) {
   pdl_begin();
+  if (gated_off(w)) return;
   cg::cluster_group cl = cg::this_cluster();
   __shared__ int s_item[2][kTQ];
   const int tq = min(max(w.tail_slots, 0), kTQ);  // slots in use (MPLD_TAIL_SLOTS lowers it: tests)
@@ -726,6 +728,7 @@ __global__ void __launch_bounds__(1024) mpld_simplify_tail(GraphView g, Workspac
 
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_final_pass(GraphView g, Workspace w, int separate_prep) {
   pdl_begin();
+  if (gated_off(w)) return;
   __shared__ CtaQueues Q;
   cq_init(Q);
   if (__ldcg(&w.ctl->err)) return;
@@ -735,6 +738,7 @@ __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_final_pass(GraphVi
 // The recovery's share of the final pass (predecessor counts, bitmasks, level
 // 0) as its own kernel, on a second stream while the search runs.
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover_prep(GraphView g, Workspace w) {
+  if (gated_off(w)) return;
   __shared__ CtaQueues Q;
   cq_init(Q);
   if (__ldcg(&w.ctl->err)) return;
@@ -859,6 +863,7 @@ __device__ void recover_levels(const GraphView& g, const Workspace& w, int k, in
 __global__ void __launch_bounds__(1024, MPLD_GRAPH_MINB) mpld_recover(GraphView g, Workspace w, int k, int* colors,
                                                                     Outputs out) {
   pdl_begin();
+  if (gated_off(w)) return;
   GridBarrier grid(&w.ctl->bar1);
   __shared__ CtaQueues Q;
   cq_init(Q);
@@ -976,6 +981,7 @@ __device__ __forceinline__ void recover_vertex(const GraphView& g, const Workspa
 
 __global__ void __launch_bounds__(1024) mpld_recover_tail(GraphView g, Workspace w, int k, int* colors, Outputs out) {
   pdl_begin();
+  if (gated_off(w)) return;
   cg::cluster_group cl = cg::this_cluster();
   __shared__ int s_item[2][kTQ];
   const int tq = min(max(w.tail_slots, 0), kTQ);  // slots in use (MPLD_TAIL_SLOTS lowers it: tests)

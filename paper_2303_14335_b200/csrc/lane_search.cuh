@@ -297,6 +297,7 @@ struct LightAcc {
   int maxsteps = 0;
   unsigned trunc = 0;
   unsigned comps = 0;  // components searched (this shard's)
+  unsigned handoff = 0;  // components handed to the warp-parallel search (exact mode)
 };
 
 __device__ __forceinline__ void light_handoff(const GraphView& g, const Workspace& w, int ci, int n, int best_cost) {
@@ -403,6 +404,7 @@ __device__ __forceinline__ void lane_component(const GraphView& g, const Workspa
     colors[kStaged ? L.pk[i][lane] : __ldcg(&w.porder[off + i])] = colour_of<K, W>(bestC, i);
   if (trunc && exact) {
     light_handoff(g, w, ci, n, best_cost);
+    acc.handoff += 1;
   } else {
     if (counts) {  // final colouring: Eq. (1b)/(1c) counts of the component
       int nc = 0, ns = 0;

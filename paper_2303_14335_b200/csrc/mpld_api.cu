@@ -44,11 +44,12 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 enum KernelId { K_SIMPLIFY = 0, K_DISCOVER, K_SEARCH, K_SEARCH_HEAVY, K_RECOVER, K_EVALUATE, K_PREP, K_SEARCH_WIDE,
-                K_BUILD, K_COUNT };
+                K_BUILD, K_TILE, K_TILE_FINISH, K_PIECES, K_COUNT };
 const char* kKernelNames[K_COUNT] = {"mpld_simplify_components", "mpld_component_discover",
                                      "mpld_exact_cover_search", "mpld_exact_cover_search_heavy", "mpld_recover",
                                      "mpld_evaluate", "mpld_recover_prep", "mpld_exact_cover_search_wide",
-                                     "mpld_graph_build"};
+                                     "mpld_graph_build", "mpld_tile_decompose", "mpld_tile_finish",
+                                     "mpld_piece_order"};
 
 constexpr int kCoopThreads = 1024;
 #ifndef MPLD_SEPARATE_PREP
@@ -113,6 +114,13 @@ struct mpld_context {
   int* hcomp = nullptr;
   int* hcost = nullptr;
   int* wide = nullptr;
+  int* t_par = nullptr;  // the tile pipeline's piece order (Workspace::t_*)
+  int* t_cnt = nullptr;
+  int* t_end = nullptr;
+  int* t_pos = nullptr;
+  int* t_perm = nullptr;
+  int* t_pend = nullptr;
+  int blocks_piece = 0;
   WorkItem* wq = nullptr;     // spilled heavy-search work (fixed size)
   unsigned long long* wq_flag = nullptr;
   HeavySlot* hslot = nullptr;
@@ -121,7 +129,11 @@ struct mpld_context {
   unsigned epoch = 0;         // search calls so far (tags wq_flag)
   unsigned spill_iters = 256; // heavy-search spill threshold; MPLD_HEAVY_SPILL overrides (tests of the spill path)
   int tail_slots = 1 << 30;   // cluster-tail frontier slots per CTA (capped at the kernel's); MPLD_TAIL_SLOTS lowers it
-  Control* ctl = nullptr;
+  Control* ctl = nullptr;       // the whole-graph pipeline's control block (ctl[0])
+  Control* ctl_tile = nullptr;  // the tile pipeline's (ctl[1]; one allocation, one reset per call)
+  int blocks_tile = 0;
+  bool gate_active = false;  // enqueuing the whole-graph kernels behind the tile pipeline (Workspace::gate)
+  bool last_tiles = false;   // the last call ran the tile pipeline (diagnostics read its control block)
   // phase-split calls: the prepared graph
   GraphView g{};
   int k = 0;
@@ -190,7 +202,7 @@ int ensure_workspace(mpld_context* ctx, int64_t n, int32_t n_layouts) {
     int64_t cap = std::max<int64_t>(n, ctx->cap_n * 3 / 2);
     cudaError_t e = cudaSuccess;
     for (int** p : {&ctx->deg, &ctx->hround, &ctx->q0, &ctx->q1, &ctx->roots, &ctx->porder, &ctx->hcomp, &ctx->hcost,
-                    &ctx->wide}) {
+                    &ctx->wide, &ctx->t_par, &ctx->t_cnt, &ctx->t_end, &ctx->t_pos, &ctx->t_perm, &ctx->t_pend}) {
       e = grow(p, cap + 1);  // + 1: q1 is the graph build's [n+1] row-pointer scratch
       if (e != cudaSuccess) return fail(MPLD_ERR_NOMEM, "workspace allocation failed");
     }
@@ -272,12 +284,13 @@ Workspace workspace(mpld_context* ctx) {
   return Workspace{ctx->deg,   ctx->hround, ctx->bmask,  ctx->prio,  ctx->q0,    ctx->q1,    ctx->roots,
                    ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->wide,  ctx->ctl,   ctx->wq,
                    ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters, ctx->tail_slots,
-                   ctx->build_err};
+                   ctx->build_err, ctx->gate_active ? &ctx->ctl_tile->gate : nullptr,
+                   ctx->t_par, ctx->t_cnt, ctx->t_end, ctx->t_pos, ctx->t_perm, ctx->t_pend};
 }
 
 // phase 1: validate?, simplification, components (colours initialised to -1)
 int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, uint32_t flags, int* colors,
-                  long long* counts) {
+                  long long* counts, bool reset = true) {
   Workspace ws = workspace(ctx);
   ctx->g = g;
   ctx->k = k;
@@ -287,10 +300,12 @@ int phase_prepare(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, 
   ctx->prepared = true;
   ctx->call_launches = 0;
   // the control block (counters, barrier arrivals, error bits) starts every call at zero
-  cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s);
+  // (behind the tile pipeline: zeroed with its control block at the start of the call)
+  cudaError_t e = reset ? cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s) : cudaSuccess;
   if (e != cudaSuccess) return cuda_fail(e, "control reset");
   TimedLaunch t(ctx, K_SIMPLIFY, s);
-  const int separate_prep = MPLD_SEPARATE_PREP ? 1 : 0;
+  // behind the tile pipeline the recovery's prep runs inside the simplification (no stream fork)
+  const int separate_prep = MPLD_SEPARATE_PREP && !ctx->gate_active ? 1 : 0;
   e = launch_simplify_components(g, ws, k, colors, counts, (flags & MPLD_FLAG_VALIDATE) ? 1 : 0, s,
                                  ctx->blocks_simplify, kCoopThreads, separate_prep);
   if (e != cudaSuccess) return cuda_fail(e, "mpld_simplify_components");
@@ -423,9 +438,80 @@ int phase_finish(mpld_context* ctx, cudaStream_t s, double alpha, int* colors, l
   return MPLD_OK;
 }
 
+// kernels the whole-graph pipeline enqueues for one call
+int whole_graph_launches(long long max_steps) {
+  (void)max_steps;  // one search kernel after the light one: wide (budgeted) or heavy (exact)
+  return simplify_launches() + 3 + (recover_tail_available() ? 2 : 1);
+}
+
+// The fused tile pipeline (kernel_tile.cu): tiles -> heavy / wide search ->
+// recovery of the pending sub-tiles and the outputs; then the whole-graph
+// pipeline, gated: its kernels return at once unless the tiles could not take
+// the input, in which case they recompute every output (identical results).
+int run_tiles(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
+              long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost, long long* stats) {
+  cudaError_t e = cudaMemsetAsync(ctx->ctl, 0, 2 * sizeof(Control), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(counts, 0, sizeof(long long) * 2 * (size_t)g.n_layouts, s);
+  if (e != cudaSuccess) return cuda_fail(e, "control reset");
+  ctx->gate_active = false;
+  Workspace wt = workspace(ctx);
+  wt.ctl = ctx->ctl_tile;
+  wt.epoch = ++ctx->epoch;  // fresh tag for the spilled-work flags of this search
+  TileLaunch tl{w_stitch, max_steps, ctx->light_steps, colors, counts, cost, stats, alpha,
+                5 + whole_graph_launches(max_steps), (flags & MPLD_FLAG_VALIDATE) ? 1 : 0, 0};
+  {
+    TimedLaunch t(ctx, K_PIECES, s);
+    e = launch_piece_order(g, wt, s, ctx->blocks_piece);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_piece_order");
+    t.done();
+  }
+  {
+    TimedLaunch t(ctx, K_TILE, s);
+    e = launch_tile(g, wt, k, tl, s, ctx->blocks_tile, false);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_tile_decompose");
+    t.done();
+  }
+  {  // the components of windows with more than one lane batch (deferred by the tiles)
+    TimedLaunch t(ctx, K_SEARCH, s);
+    e = launch_search(g, wt, k, w_stitch, max_steps, colors, ctx->light_steps, counts, 0, 1, s, ctx->blocks_search,
+                      true);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search");
+    t.done();
+  }
+  if (max_steps > 0) {
+    TimedLaunch t(ctx, K_SEARCH_WIDE, s);
+    e = launch_search_wide(g, wt, k, w_stitch, max_steps, colors, ctx->light_steps, counts, s, ctx->blocks_wide);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_wide");
+    t.done();
+  } else {
+    TimedLaunch t(ctx, K_SEARCH_HEAVY, s);
+    e = launch_search_heavy(g, wt, k, w_stitch, colors, counts, s, ctx->blocks_heavy, true);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_exact_cover_search_heavy");
+    t.done();
+  }
+  tl.finish = 1;
+  {
+    TimedLaunch t(ctx, K_TILE_FINISH, s);
+    e = launch_tile(g, wt, k, tl, s, ctx->blocks_tile, true);
+    if (e != cudaSuccess) return cuda_fail(e, "mpld_tile_finish");
+    t.done();
+  }
+  ctx->gate_active = true;
+  int rc = phase_prepare(ctx, s, g, k, flags, colors, counts, false);
+  if (rc == MPLD_OK) rc = phase_search(ctx, s, w_stitch, max_steps, 0, 1, colors);
+  if (rc == MPLD_OK) rc = phase_finish(ctx, s, alpha, colors, counts, cost, stats);
+  ctx->gate_active = false;
+  if (rc == MPLD_OK) rc = mark_last(ctx, s);
+  ctx->last_tiles = true;
+  return rc;
+}
+
 int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
                  long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost,
                  long long* stats) {
+  if (!(flags & MPLD_FLAG_WHOLE_GRAPH))
+    return run_tiles(ctx, s, g, k, w_stitch, alpha, max_steps, flags, colors, counts, cost, stats);
+  ctx->last_tiles = false;
   int rc = phase_prepare(ctx, s, g, k, flags, colors, counts);
   if (rc == MPLD_OK) rc = phase_search(ctx, s, w_stitch, max_steps, 0, 1, colors);
   if (rc == MPLD_OK) rc = phase_finish(ctx, s, alpha, colors, counts, cost, stats);
@@ -534,11 +620,12 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     delete ctx;
     return fail(MPLD_ERR_CUDA, "device does not support cooperative launch");
   }
-  if (cudaMalloc((void**)&ctx->ctl, sizeof(Control)) != cudaSuccess) {
+  if (cudaMalloc((void**)&ctx->ctl, 2 * sizeof(Control)) != cudaSuccess) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_NOMEM, "control block allocation failed");
   }
-  cudaMemset(ctx->ctl, 0, sizeof(Control));
+  ctx->ctl_tile = ctx->ctl + 1;
+  cudaMemset(ctx->ctl, 0, 2 * sizeof(Control));
   ctx->blocks_build = coop_blocks_build(ctx->num_sms);
   if (ctx->blocks_build <= 0 || cudaMalloc((void**)&ctx->build_err, sizeof(int)) != cudaSuccess ||
       cudaMalloc((void**)&ctx->build_bar, sizeof(unsigned)) != cudaSuccess ||
@@ -575,6 +662,13 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     mpld_context_destroy(ctx);
     return cuda_fail(e, "configure recovery tail");
   }
+  e = configure_tile();
+  if (e != cudaSuccess) {
+    mpld_context_destroy(ctx);
+    return cuda_fail(e, "configure tile pipeline");
+  }
+  ctx->blocks_tile = resident_blocks_tile(ctx->num_sms);
+  ctx->blocks_piece = coop_blocks_piece(ctx->num_sms);
   e = configure_search_heavy(ctx->num_sms, ctx->blocks_heavy);
   if (e == cudaSuccess) e = configure_search_wide(ctx->num_sms, &ctx->blocks_wide);
   if (e != cudaSuccess || ctx->blocks_wide <= 0) {
@@ -584,7 +678,7 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   int min_heavy = ctx->blocks_heavy[0];
   for (int b : ctx->blocks_heavy) min_heavy = std::min(min_heavy, b);
   if (ctx->blocks_simplify <= 0 || ctx->blocks_recover <= 0 || ctx->blocks_search <= 0 || min_heavy <= 0 ||
-      ctx->blocks_discover <= 0) {
+      ctx->blocks_discover <= 0 || ctx->blocks_tile <= 0 || ctx->blocks_piece <= 0) {
     mpld_context_destroy(ctx);
     return fail(MPLD_ERR_CUDA, "occupancy query failed (kernel image missing for this device?)");
   }
@@ -611,7 +705,8 @@ void mpld_context_destroy(mpld_context* ctx) {
   if (!ctx) return;
   for (void* p : {(void*)ctx->deg, (void*)ctx->hround, (void*)ctx->bmask, (void*)ctx->prio, (void*)ctx->q0, (void*)ctx->q1,
                   (void*)ctx->roots, (void*)ctx->crec, (void*)ctx->pmask, (void*)ctx->porder, (void*)ctx->hcomp,
-                  (void*)ctx->hcost, (void*)ctx->wide, (void*)ctx->build_err, (void*)ctx->build_bar,
+                  (void*)ctx->hcost, (void*)ctx->wide, (void*)ctx->t_par, (void*)ctx->t_cnt, (void*)ctx->t_end,
+                  (void*)ctx->t_pos, (void*)ctx->t_perm, (void*)ctx->t_pend, (void*)ctx->build_err, (void*)ctx->build_bar,
                   (void*)ctx->build_tot, (void*)ctx->ctl, (void*)ctx->wq, (void*)ctx->wq_flag, (void*)ctx->hslot,
                   (void*)ctx->est, (void*)ctx->bsum,
                   (void*)ctx->h_lo,
@@ -1050,7 +1145,10 @@ int mpld_kernel_count(void) { return K_COUNT; }
 int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
   if (!ctx || !out || n < 0) return fail(MPLD_ERR_ARG, "bad argument");
   Control c;
-  cudaError_t e = cudaMemcpy(&c, ctx->ctl, sizeof(Control), cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaMemcpy(&c, ctx->ctl_tile, sizeof(Control), cudaMemcpyDeviceToHost);
+  const int64_t gate = ctx->last_tiles ? c.gate : -1;
+  if (e == cudaSuccess && (!ctx->last_tiles || c.gate))  // whole-graph pipeline (alone, or behind a gated tile pass)
+    e = cudaMemcpy(&c, ctx->ctl, sizeof(Control), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "debug copy");
   int64_t v[96];
   for (int i = 0; i < 16; ++i) v[i] = (int64_t)c.t[i];
@@ -1069,6 +1167,7 @@ int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
   v[93] = c.n_heavy[0] + c.n_heavy[1];
   v[94] = c.n_comp;
   v[95] = c.truncated;
+  v[88] = gate;
   for (int i = 0; i < n && i < 96; ++i) out[i] = v[i];
   return MPLD_OK;
 }

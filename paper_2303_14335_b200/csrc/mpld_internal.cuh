@@ -72,6 +72,18 @@ struct Control {
   unsigned long long tr[32];  // diagnostics: per round / level start time (ns)
   int nr[32];                // diagnostics: per round / level frontier size
   alignas(128) unsigned long long dbg[8];  // diagnostics (MPLD_DIAG builds): slowest discovery / search / heavy search
+  // the fused tile pipeline (kernel_tile.cu; its own Control block)
+  alignas(128) int tile_next;  // next tile to take (dynamic tile assignment)
+  alignas(128) int n_pending;  // sub-tiles whose recovery waits for the heavy / wide search (w.q0 / w.q1)
+  int done_tiles;              // last-CTA detection of the finish launch
+  int finish_next;             // next pending sub-tile of the finish launch
+  alignas(128) unsigned long long comp_pool_tile;  // components << 32 | pool words of the tiles' own searches
+                                                   // (taken from the top of the pool; comp_pool: deferred ones)
+  alignas(128) int piece_cursor;  // piece order: positions handed out to pieces
+  alignas(128) unsigned bar_piece;  // grid-barrier arrivals of mpld_piece_order
+  alignas(128) int gate;       // 1: the tile pipeline could not take the input (a piece not closed inside
+                               // its tile's window, a window over capacity, invalid input): the
+                               // whole-graph pipeline runs after it and rewrites every output
 };
 
 #ifndef MPLD_DIAG
@@ -179,7 +191,22 @@ struct Workspace {
   int tail_slots;        // cluster tails: frontier slots per CTA in use (MPLD_TAIL_SLOTS lowers it: tests)
   int* build_err;        // set when a CSR built on the device (upper-triangle upload) saw bad input; the
                          // simplification turns it into MPLD_ERR_GRAPH and clears it
+  const int* gate;       // whole-graph kernels after the tile pipeline: run only if *gate != 0 (nullptr:
+                         // always run)
+  // the tile pipeline's piece order (kernel_tile.cu mpld_piece_order), [n] each
+  int* t_par;   // union-find: parent - v (0 = root)
+  int* t_cnt;   // piece size at its root (then the positions still to hand out)
+  int* t_end;   // end position of the piece, at its root
+  int* t_pos;   // vertex -> position (pieces contiguous)
+  int* t_perm;  // position -> vertex
+  int* t_pend;  // position -> end position of its piece
 };
+
+// The whole-graph kernels return at once when they follow the tile pipeline
+// and it took the input (every thread of the grid reads the same word).
+__device__ __forceinline__ bool gated_off(const Workspace& w) {
+  return w.gate != nullptr && *(volatile const int*)w.gate == 0;
+}
 
 // Layout of vertex v: the l with layout_off[l] <= v < layout_off[l+1] (binary
 // search; the offsets are tiny and stay in L1).
@@ -304,6 +331,32 @@ struct GraphBuild {
 constexpr unsigned kBuildBarriers = 5;  // grid barriers per mpld_graph_build launch
 cudaError_t launch_graph_build(const GraphBuild& b, cudaStream_t s, int blocks);
 int coop_blocks_build(int num_sms);
+
+// The fused tile pipeline (kernel_tile.cu).  finish = 0: every tile
+// (simplification, sub-graphs, light search, recovery); finish = 1: the
+// recovery of the sub-tiles whose components went to the heavy / wide search,
+// then the Eq. (1a) costs and statistics (last CTA).  `launches` is the call's
+// kernel count for MPLD_STAT_LAUNCHES.
+struct TileLaunch {
+  int w_stitch;
+  long long max_steps;
+  unsigned light_steps;
+  int* colors;
+  long long* counts;
+  double* cost;
+  long long* stats;
+  double alpha;
+  int launches;
+  int validate;
+  int finish;
+};
+cudaError_t configure_tile();
+int coop_blocks_piece(int num_sms);
+// the piece order of the tile pipeline (cooperative; see kernel_tile.cu)
+cudaError_t launch_piece_order(const GraphView& g, const Workspace& w, cudaStream_t s, int blocks);
+int resident_blocks_tile(int num_sms);
+cudaError_t launch_tile(const GraphView& g, const Workspace& w, int k, const TileLaunch& t, cudaStream_t s,
+                        int blocks, bool pdl);
 bool recover_tail_available();  // the cluster tail kernel can be launched (cluster size support)
 int simplify_launches();        // kernels launch_simplify_components enqueues (1, or 3 with the cluster tail)
 cudaError_t configure_recover_tail();
