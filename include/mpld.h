@@ -93,9 +93,11 @@ enum mpld_status {
                                * symmetry by two 64-bit multiset hashes (sum H(v,u) == sum H(u,v);
                                * an asymmetric graph passes with probability ~2^-64) */
 
-#define MPLD_FLAG_WHOLE_GRAPH 2u /* run the whole-graph pipeline only (level-synchronous kernels over all
-                                  * vertices) instead of the tile pipeline with it as fallback; results
-                                  * are identical — for A/B measurement and tests */
+#define MPLD_FLAG_TILES 2u /* run the tile pipeline (kernel_tile.cu: piece order, then simplification,
+                            * search and recovery of whole pieces per CTA in shared memory) with the
+                            * whole-graph pipeline gated behind it as the fallback; results are
+                            * identical.  Off by default: measured slower on the
+                            * synthetic configs */
 
 /* stats[] layout */
 enum mpld_stat {
@@ -308,7 +310,7 @@ int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* laun
  * recomputed it, bits: 1 row pointer / id out of range, 2 a piece larger than a
  * window, 4 a neighbour outside its piece's window, 8 / 16 / 128 validation
  * (rows, symmetry, layout offsets), 32 a component > 64 vertices, 64 invalid
- * compact upload; -1: MPLD_FLAG_WHOLE_GRAPH / phase calls), out[89] the slowest
+ * compact upload; -1: the last call ran without MPLD_FLAG_TILES), out[89] the slowest
  * heavy component (cycles), out[90] the slowest heavy warp (cycles over all its
  * components), out[91] the slowest heavy component's size, out[92] component-search seeds,
  * out[93] heavy components, out[94] components, out[95] truncated searches.

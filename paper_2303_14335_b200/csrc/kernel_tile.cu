@@ -14,7 +14,7 @@
 // call — are replaced by:
 //
 //   mpld_piece_order     one cooperative kernel (4 grid barriers): the pieces
-//                        by union-find over CE ∪ SE (roots = minima), then
+//                        by union-find over CE ∪ SE (random-priority roots), then
 //                        positions with every piece contiguous (t_perm /
 //                        t_pos; the order inside a piece is irrelevant: every
 //                        tie-break below compares original ids)
@@ -85,8 +85,9 @@ struct __align__(16) TileSmem {
 
 // ---------------------------------------------------------------------------
 // The piece order.  Union-find on parent offsets (t_par[v] = parent - v, 0 for
-// a root), so a zeroed array is the initial forest; the larger root is hooked
-// under the smaller one, so every root is its piece's minimum.
+// a root), so a zeroed array is the initial forest; the root of larger
+// priority lowbias32(id) is hooked under the other (any root will do: it only
+// names the piece).
 __device__ __forceinline__ int pfind(int* par, int x) {
   while (true) {
     const int d = __ldcg(&par[x]);
@@ -113,9 +114,9 @@ __device__ __forceinline__ void punion(int* par, int a, int b) {
     a = pfind(par, a);
     b = pfind(par, b);
     if (a == b) return;
-    if (a < b) {
-      const int t = a;
-      a = b;
+    if (lowbias32((uint32_t)a) < lowbias32((uint32_t)b)) {  // random priorities: trees of expected
+      const int t = a;                                      // logarithmic depth (minimum-id roots
+      a = b;                                                // chain up along wires)
       b = t;
     }
     if (atomicCAS(&par[a], 0, b - a) == 0) return;
@@ -135,7 +136,7 @@ enum GateBits : int {
 };
 __device__ __forceinline__ void set_gate(Control* ctl, int why) { atomicOr(&ctl->gate, why); }
 
-__global__ void __launch_bounds__(kPieceThreads, 1) mpld_piece_order(GraphView g, Workspace w) {
+__global__ void __launch_bounds__(kPieceThreads, 2) mpld_piece_order(GraphView g, Workspace w) {
   Control* ctl = w.ctl;
   GridBarrier grid(&ctl->bar_piece);
   const int n = g.n;
@@ -362,12 +363,37 @@ __device__ int tile_pass(TileSmem& S, const GraphView& g, const Workspace& w, co
     S.maxn = 0;
     S.pending = 0;
   }
-  for (int i = tid; i < nmax; i += kTT) {
-    const int v = __ldcg(&w.t_perm[s0 + i]);
-    S.orig[i] = v;
-    S.uf[i] = __ldg(&g.ce_rp[v + 1]) - __ldg(&g.ce_rp[v]);  // (row pointers range-checked by the piece order)
-    S.cnt[i] = __ldg(&g.se_rp[v + 1]) - __ldg(&g.se_rp[v]);
-    S.hr[i] = -1;
+  // row starts in the CSR arrays, until the rows are gathered (prio and the
+  // queues are free until step 3)
+  int* gcs = reinterpret_cast<int*>(S.prio);
+  int* gss = reinterpret_cast<int*>(&S.q[0][0]);
+  {
+    constexpr int kPer = kTMaxV / kTT;
+    int vv[kPer], a0[kPer], a1[kPer], b0[kPer], b1[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + j * kTT;
+      vv[j] = i < nmax ? __ldcg(&w.t_perm[s0 + i]) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {  // (row pointers range-checked by the piece order)
+      const int v = max(vv[j], 0);
+      a0[j] = vv[j] >= 0 ? __ldg(&g.ce_rp[v]) : 0;
+      a1[j] = vv[j] >= 0 ? __ldg(&g.ce_rp[v + 1]) : 0;
+      b0[j] = vv[j] >= 0 ? __ldg(&g.se_rp[v]) : 0;
+      b1[j] = vv[j] >= 0 ? __ldg(&g.se_rp[v + 1]) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + j * kTT;
+      if (vv[j] < 0) continue;
+      S.orig[i] = vv[j];
+      S.uf[i] = a1[j] - a0[j];
+      S.cnt[i] = b1[j] - b0[j];
+      gcs[i] = a0[j];
+      gss[i] = b0[j];
+      S.hr[i] = -1;
+    }
   }
   __syncthreads();
   block_scan2(S, S.uf, S.uf, S.cnt, S.cnt, nmax);  // in place: row starts, totals at [nmax]
@@ -386,43 +412,59 @@ __device__ int tile_pass(TileSmem& S, const GraphView& g, const Workspace& w, co
   }
   __syncthreads();
   // ---- 2. the rows, as window indices (every neighbour lies in the window:
-  // pieces are closed); validation (MPLD_FLAG_VALIDATE) on the raw ids
+  // pieces are closed), gathered entry by entry (consecutive entries of a row
+  // on consecutive threads); validation (MPLD_FLAG_VALIDATE) on the raw ids
+  for (int i = tid; i < m; i += kTT) {  // each entry's row, in the entry's slot
+    for (int o = S.rc[i], o1 = S.rc[i + 1]; o < o1; ++o) S.colC[o] = (unsigned short)i;
+    for (int o = S.rs[i], o1 = S.rs[i + 1]; o < o1; ++o) S.colS[o] = (unsigned short)i;
+  }
+  __syncthreads();
   const bool val = a.validate && !finish;
-  for (int i = tid; i < m; i += kTT) {
-    const int v = S.orig[i];
-    const int c0 = __ldg(&g.ce_rp[v]), c1 = __ldg(&g.ce_rp[v + 1]);
-    const int d0 = __ldg(&g.se_rp[v]), d1 = __ldg(&g.se_rp[v + 1]);
-    int prev = -1;
-    for (int e = c0, o = S.rc[i]; e < c1; ++e, ++o) {
-      const int u = __ldg(&g.ce_col[e]);
-      const int p = __ldcg(&w.t_pos[u]) - s0;
-      if ((unsigned)p >= (unsigned)m) atomicOr(&S.bad, kGateOpen);  // asymmetric input
-      S.colC[o] = (unsigned short)min(max(p, 0), m - 1);
+  const int nce = S.rc[m], nse = S.rs[m];
+  for (int o0 = 0; o0 < nce; o0 += 4 * kTT) {
+    int row[4], e[4], u[4], p[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int o = o0 + t * kTT + tid;
+      row[t] = o < nce ? S.colC[o] : -1;
+      e[t] = row[t] >= 0 ? gcs[row[t]] + (o - S.rc[row[t]]) : 0;
+      u[t] = row[t] >= 0 ? __ldg(&g.ce_col[e[t]]) : 0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) p[t] = row[t] >= 0 ? __ldcg(&w.t_pos[u[t]]) - s0 : 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int o = o0 + t * kTT + tid;
+      if (row[t] < 0) continue;
+      if ((unsigned)p[t] >= (unsigned)m) atomicOr(&S.bad, kGateOpen);  // asymmetric input
+      S.colC[o] = (unsigned short)min(max(p[t], 0), m - 1);
       if (val) {
-        if (u == v || u <= prev) atomicOr(&S.bad, kGateInvalid);
-        prev = u;
-        hs[0] += edge_hash(v, u);
-        hs[1] += edge_hash(u, v);
+        const int v = S.orig[row[t]];
+        const bool first = o == S.rc[row[t]];
+        if (u[t] == v || (!first && u[t] <= __ldg(&g.ce_col[e[t] - 1]))) atomicOr(&S.bad, kGateInvalid);
+        hs[0] += edge_hash(v, u[t]);
+        hs[1] += edge_hash(u[t], v);
       }
     }
-    prev = -1;
-    for (int e = d0, o = S.rs[i]; e < d1; ++e, ++o) {
-      const int u = __ldg(&g.se_col[e]);
-      const int p = __ldcg(&w.t_pos[u]) - s0;
-      if ((unsigned)p >= (unsigned)m) atomicOr(&S.bad, kGateOpen);
-      S.colS[o] = (unsigned short)min(max(p, 0), m - 1);
-      if (val) {
-        if (u == v || u <= prev) atomicOr(&S.bad, kGateInvalid);
-        prev = u;
-        hs[2] += edge_hash(v, u);
-        hs[3] += edge_hash(u, v);
-        int lo = c0, hi2 = c1;  // CE ∩ SE: binary search in the CE row
-        while (lo < hi2) {
-          const int mid = (lo + hi2) >> 1;
-          const int y = __ldg(&g.ce_col[mid]);
-          if (y == u) atomicOr(&S.bad, kGateInvalid);
-          if (y < u) lo = mid + 1; else hi2 = mid;
-        }
+  }
+  for (int o = tid; o < nse; o += kTT) {
+    const int r = S.colS[o];
+    const int e = gss[r] + (o - S.rs[r]);
+    const int u = __ldg(&g.se_col[e]);
+    const int p = __ldcg(&w.t_pos[u]) - s0;
+    if ((unsigned)p >= (unsigned)m) atomicOr(&S.bad, kGateOpen);
+    S.colS[o] = (unsigned short)min(max(p, 0), m - 1);
+    if (val) {
+      const int v = S.orig[r];
+      if (u == v || (o > S.rs[r] && u <= __ldg(&g.se_col[e - 1]))) atomicOr(&S.bad, kGateInvalid);
+      hs[2] += edge_hash(v, u);
+      hs[3] += edge_hash(u, v);
+      int lo = gcs[r], hi2 = gcs[r] + (S.rc[r + 1] - S.rc[r]);  // CE ∩ SE: binary search in the CE row
+      while (lo < hi2) {
+        const int mid = (lo + hi2) >> 1;
+        const int y = __ldg(&g.ce_col[mid]);
+        if (y == u) atomicOr(&S.bad, kGateInvalid);
+        if (y < u) lo = mid + 1; else hi2 = mid;
       }
     }
   }
@@ -779,7 +821,7 @@ int coop_blocks_piece(int num_sms) {
   int per = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mpld_piece_order, kPieceThreads, 0) != cudaSuccess)
     return 0;
-  return std::min(per, 1) * num_sms;
+  return std::min(per, 2) * num_sms;
 }
 
 cudaError_t launch_piece_order(const GraphView& g, const Workspace& w, cudaStream_t s, int blocks) {

@@ -509,7 +509,7 @@ int run_tiles(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int 
 int run_pipeline(mpld_context* ctx, cudaStream_t s, const GraphView& g, int k, int w_stitch, double alpha,
                  long long max_steps, uint32_t flags, int* colors, long long* counts, double* cost,
                  long long* stats) {
-  if (!(flags & MPLD_FLAG_WHOLE_GRAPH))
+  if (flags & MPLD_FLAG_TILES)
     return run_tiles(ctx, s, g, k, w_stitch, alpha, max_steps, flags, colors, counts, cost, stats);
   ctx->last_tiles = false;
   int rc = phase_prepare(ctx, s, g, k, flags, colors, counts);

@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("MPLD_LIB") or os.path.join(HERE, "lib", "libmpld.so")
 MPLD_OK = 0
 MPLD_ERR_ARG, MPLD_ERR_GRAPH, MPLD_ERR_COMPONENT, MPLD_ERR_CUDA, MPLD_ERR_NOMEM = 1, 2, 3, 4, 5
 MPLD_FLAG_VALIDATE = 1
-MPLD_FLAG_WHOLE_GRAPH = 2  # whole-graph pipeline only (no tile pass); identical results
+MPLD_FLAG_TILES = 2  # the tile pipeline (whole-graph pipeline gated behind it); identical results
 MPLD_MAX_K = 4
 MPLD_MAX_COMPONENT = 64
 MPLD_COST_UNITS = 1000

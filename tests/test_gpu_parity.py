@@ -242,7 +242,7 @@ def test_device_entry_point_matches_host_entry_point():
     assert np.array_equal(c[:, 0], host["n_conflicts"]) and np.array_equal(c[:, 1], host["n_stitches"])
     assert np.array_equal(cost.cpu().numpy(), host["cost"])
     times = ctx.kernel_times()
-    assert times["mpld_tile_decompose"][1] == 2 and times["mpld_tile_decompose"][0] > 0
+    assert times["mpld_exact_cover_search"][1] == 2 and times["mpld_exact_cover_search"][0] > 0
     ctx.close()
 
 

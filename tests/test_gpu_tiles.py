@@ -1,9 +1,9 @@
-"""The tile pipeline (kernel_tile.cu) and its gate: parity with the CPU oracle
+"""The tile pipeline (kernel_tile.cu, MPLD_FLAG_TILES) and its gate: parity with the CPU oracle
 on inputs the tiles take (windows cut by their shared-memory capacity, pieces
 crossing tile boundaries, the pending sub-tiles of exact mode) and on inputs
 they must hand to the whole-graph pipeline (pieces not local in id space,
 pieces longer than a window), plus the whole-graph pipeline alone
-(MPLD_FLAG_WHOLE_GRAPH) on the same inputs.  Device outputs of both pipelines
+(the default) on the same inputs.  Device outputs of both pipelines
 are compared element by element."""
 from __future__ import annotations
 
@@ -53,7 +53,7 @@ def _device_run(g, k, alpha, max_steps, flags):
 def _check(g, k, alpha, max_steps, expect_gate, ref=None):
     ref = ref or oracle.decompose(g, k, alpha, max_steps=max_steps)
     outs = {}
-    for name, fl in (("tile", mp.MPLD_FLAG_VALIDATE), ("whole", mp.MPLD_FLAG_VALIDATE | mp.MPLD_FLAG_WHOLE_GRAPH)):
+    for name, fl in (("tile", mp.MPLD_FLAG_VALIDATE | mp.MPLD_FLAG_TILES), ("whole", mp.MPLD_FLAG_VALIDATE)):
         got, gate = _device_run(g, k, alpha, max_steps, fl)
         if name == "tile":
             assert gate == expect_gate
@@ -161,9 +161,9 @@ def test_device_outputs_identical_on_the_bench_batch():
         gs, k, alpha = synth.config_graphs(1, seed=10 * r)
         graphs += gs
     b = synth.concat(graphs)
-    a, gate = _device_run(b, k, alpha, 0, mp.MPLD_FLAG_VALIDATE)
+    a, gate = _device_run(b, k, alpha, 0, mp.MPLD_FLAG_VALIDATE | mp.MPLD_FLAG_TILES)
     assert gate == 0
-    w, _ = _device_run(b, k, alpha, 0, mp.MPLD_FLAG_VALIDATE | mp.MPLD_FLAG_WHOLE_GRAPH)
+    w, _ = _device_run(b, k, alpha, 0, mp.MPLD_FLAG_VALIDATE)
     for key in ("colors", "counts", "cost"):
         assert np.array_equal(a[key], w[key]), key
     for key in ("components", "hidden", "rounds", "max_component", "truncated", "error"):
@@ -178,5 +178,5 @@ def test_tiles_reject_invalid_input_like_the_whole_graph_pipeline():
     col[-1] = 5  # row 4 lists 5, row 5 does not list 4
     bad = synth.graph.DecompGraph(g.n, g.ce_rowptr.copy(), col, g.se_rowptr.copy(), g.se_col.copy(), name="asym")
     with pytest.raises(mp.MPLDError) as ei:
-        mp.decompose_graph(bad, 3, 0.1, max_steps=BUDGET, flags=mp.MPLD_FLAG_VALIDATE)
+        mp.decompose_graph(bad, 3, 0.1, max_steps=BUDGET, flags=mp.MPLD_FLAG_VALIDATE | mp.MPLD_FLAG_TILES)
     assert ei.value.code == 2

@@ -33,8 +33,8 @@ def main():
         for it in items:
             d = bench.DeviceItem(it, dev)
             res = {}
-            for name, fl in (("whole", mp.MPLD_FLAG_VALIDATE | mp.MPLD_FLAG_WHOLE_GRAPH),
-                             ("tile", mp.MPLD_FLAG_VALIDATE)):
+            for name, fl in (("whole", mp.MPLD_FLAG_VALIDATE),
+                             ("tile", mp.MPLD_FLAG_VALIDATE | mp.MPLD_FLAG_TILES)):
                 for _ in range(3):
                     d.run(ctx, stream, fl)
                 torch.cuda.synchronize()
