@@ -985,7 +985,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
 // (c, maximal path) is a valid incumbent key that never cuts the canonical
 // optimum (its key is <= (c, path of any leaf of cost c)).
 template <int K, typename W>
-__device__ int warp_greedy_seed(const W* adj, const W* sadj, int n, int w_stitch, unsigned seed, W (&best)[K]) {
+__device__ int warp_greedy_once(const W* adj, const W* sadj, int n, int w_stitch, unsigned seed, W (&best)[K]) {
   using O = WordOps<W>;
   const int lane = threadIdx.x & 31;
   unsigned r = lowbias32(seed * 32u + (unsigned)lane + 0x9e3779b9u);
@@ -1070,6 +1070,23 @@ __device__ int warp_greedy_seed(const W* adj, const W* sadj, int n, int w_stitch
 #pragma unroll
   for (int c = 0; c < K; ++c) best[c] = __shfl_sync(0xffffffffu, C[c], src);
   return mc;
+}
+
+// `rounds` x 32 randomized greedy colourings (Workspace::greedy_rounds), the cheapest kept
+template <int K, typename W>
+__device__ int warp_greedy_seed(const W* adj, const W* sadj, int n, int w_stitch, unsigned seed, int rounds,
+                                W (&best)[K]) {
+  int bc = warp_greedy_once<K, W>(adj, sadj, n, w_stitch, seed, best);
+  for (int i = 1; i < rounds && bc > 0; ++i) {
+    W t[K];
+    const int c = warp_greedy_once<K, W>(adj, sadj, n, w_stitch, seed + 0x10000u * (unsigned)i, t);
+    if (c < bc) {
+      bc = c;
+#pragma unroll
+      for (int q = 0; q < K; ++q) best[q] = t[q];
+    }
+  }
+  return bc;
 }
 
 // The canonical leaf of a colouring: follow the column rule of R5 and take
@@ -1228,7 +1245,8 @@ __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, i
   cur_ncl = u.ncl;
   W gcol[K];
   const int hc = (kSeedIncumbent || !light_leaf) ? warp_greedy_seed<K, W>(s_adj, s_sadj, u.n, w_stitch,
-                                                                          (unsigned)u.ci, gcol)
+                                                                          (unsigned)u.ci + w.greedy_salt,
+                                                                          w.greedy_rounds, gcol)
                                                  : INT_MAX;
   if (!light_leaf) {  // the greedy colouring (renamed into a canonical leaf by leaf_path) is the starting leaf
 #pragma unroll
@@ -1564,8 +1582,11 @@ cudaError_t launch_search_wide(const GraphView& g, Workspace ws, int k, int w_st
 
 template <int K>
 cudaError_t configure_wide_k(int num_sms, int* blocks) {
-  const cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_wide<K>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaneWide));
+  cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_wide<K>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaneWide));
+  if (e == cudaSuccess)  // the whole unified L1 as shared memory (see configure_heavy_k)
+    e = cudaFuncSetAttribute(mpld_exact_cover_search_wide<K>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search_wide<K>, 32, sizeof(LaneWide));
@@ -1607,8 +1628,14 @@ cudaError_t launch_search_heavy(const GraphView& g, Workspace ws, int k, int w_s
 
 template <int K>
 cudaError_t configure_heavy_k(int num_sms, int* blocks) {
-  const cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<K>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem_all(K));
+  cudaError_t e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<K>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)heavy_smem_all(K));
+  // the whole unified L1 as shared memory: the resident-grid size below assumes it, and without
+  // the preference the SM keeps the carveout of the kernel before (measured: configs[2] after the
+  // light kernel 0.93-0.99 ms, after a kernel that had set the maximum 0.45-0.50 ms)
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(mpld_exact_cover_search_heavy<K>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search_heavy<K>, 32, heavy_smem_all(K));
@@ -1632,6 +1659,8 @@ int resident_blocks_discover(int num_sms) {
 
 int resident_blocks_search(int threads, int num_sms) {
   (void)threads;
+  for (auto f : {mpld_exact_cover_search<2>, mpld_exact_cover_search<3>, mpld_exact_cover_search<4>})
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4>, kLaneWarps * 32, 0);
   return per_sm * num_sms;

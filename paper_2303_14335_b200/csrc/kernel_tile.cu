@@ -807,6 +807,9 @@ cudaError_t configure_tile() {
   const int sz = (int)sizeof(TileSmem);
   for (auto f : {mpld_tile_decompose<2>, mpld_tile_decompose<3>, mpld_tile_decompose<4>})
     if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sz);
+  for (auto f : {mpld_tile_decompose<2>, mpld_tile_decompose<3>, mpld_tile_decompose<4>})
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
   return e;
 }
 

@@ -121,6 +121,8 @@ struct mpld_context {
   int* t_perm = nullptr;
   int* t_pend = nullptr;
   int blocks_piece = 0;
+  unsigned greedy_salt = 0;  // MPLD_GREEDY_SALT (experiments)
+  int greedy_rounds = 1;     // MPLD_GREEDY_ROUNDS
   WorkItem* wq = nullptr;     // spilled heavy-search work (fixed size)
   unsigned long long* wq_flag = nullptr;
   HeavySlot* hslot = nullptr;
@@ -284,7 +286,8 @@ Workspace workspace(mpld_context* ctx) {
   return Workspace{ctx->deg,   ctx->hround, ctx->bmask,  ctx->prio,  ctx->q0,    ctx->q1,    ctx->roots,
                    ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->wide,  ctx->ctl,   ctx->wq,
                    ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters, ctx->tail_slots,
-                   ctx->build_err, ctx->gate_active ? &ctx->ctl_tile->gate : nullptr,
+                   ctx->build_err, ctx->greedy_salt, ctx->greedy_rounds,
+                   ctx->gate_active ? &ctx->ctl_tile->gate : nullptr,
                    ctx->t_par, ctx->t_cnt, ctx->t_end, ctx->t_pos, ctx->t_perm, ctx->t_pend};
 }
 
@@ -652,6 +655,11 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
   if (const char* hs = std::getenv("MPLD_HEAVY_SPILL")) {
     const long v = std::strtol(hs, nullptr, 10);
     if (v >= 64) ctx->spill_iters = (unsigned)std::min<long>(v & ~63L, 1L << 30);
+  }
+  if (const char* gs = std::getenv("MPLD_GREEDY_SALT")) ctx->greedy_salt = (unsigned)std::strtoul(gs, nullptr, 10);
+  if (const char* gr = std::getenv("MPLD_GREEDY_ROUNDS")) {
+    const long v = std::strtol(gr, nullptr, 10);
+    if (v >= 1 && v <= 64) ctx->greedy_rounds = (int)v;
   }
   if (const char* ls = std::getenv("MPLD_LIGHT_STEPS")) {
     const long v = std::strtol(ls, nullptr, 10);

@@ -191,6 +191,8 @@ struct Workspace {
   int tail_slots;        // cluster tails: frontier slots per CTA in use (MPLD_TAIL_SLOTS lowers it: tests)
   int* build_err;        // set when a CSR built on the device (upper-triangle upload) saw bad input; the
                          // simplification turns it into MPLD_ERR_GRAPH and clears it
+  unsigned greedy_salt;  // heavy search: seed offset of the greedy starting colourings (MPLD_GREEDY_SALT)
+  int greedy_rounds;     // heavy search: rounds of 32 greedy colourings (MPLD_GREEDY_ROUNDS, default 1)
   const int* gate;       // whole-graph kernels after the tile pipeline: run only if *gate != 0 (nullptr:
                          // always run)
   // the tile pipeline's piece order (kernel_tile.cu mpld_piece_order), [n] each
