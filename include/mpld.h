@@ -314,7 +314,9 @@ int mpld_context_kernel_time(mpld_context* ctx, int i, double* ms, int64_t* laun
  * heavy component (cycles), out[90] the slowest heavy warp (cycles over all its
  * components), out[91] the slowest heavy component's size, out[92] component-search seeds,
  * out[93] heavy components, out[94] components, out[95] truncated searches.
- * Copies min(n, 96). */
+ * Copies min(n, 96); out[96..n) receives the heavy-search trace of MPLD_DIAG_HEAVY
+ * builds (4 words per search unit: ci | n << 32 | item << 48, nodes, start and end
+ * %globaltimer ns), unspecified otherwise. */
 int mpld_context_debug(mpld_context* ctx, int64_t* out, int n);
 
 #ifdef __cplusplus

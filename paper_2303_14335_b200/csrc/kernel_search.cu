@@ -548,6 +548,33 @@ __device__ __forceinline__ void node_at(int j, int depth, const W (&B)[K], const
   }
 }
 
+// The same node N_j rebuilt forward from the lane's start node N_{d0} (the
+// unit's root, or the node the lane took): apply the selected rows of frames
+// d0..j-1.  Identical to node_at; the callers take the shorter direction.
+template <int K, typename W, int D>
+__device__ __forceinline__ void node_from_start(int j, int d0, const W (&C0)[K], const W (&B0)[K], W U0, int cost0,
+                                                const LaneFrames<K, W, D>& F, int lane, const W* adj, const W* sadj,
+                                                int w_stitch, W (&jB)[K], W (&jC)[K], W& jU, int& jcost) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    jB[c] = B0[c];
+    jC[c] = C0[c];
+  }
+  jU = U0;
+  jcost = cost0;
+  for (int d = d0; d < j; ++d) {
+    const int pk = F.pk[d][lane];
+    const int v = pk_v(pk), c = pk_c(pk);
+    const W bit = W(1) << v;
+    const W a = adj[v];
+    jU &= ~bit;
+    const W Cc = pick<K, W>(jC, c);
+    jcost += row_cost<W>(a, sadj[v], Cc, jU, w_stitch);
+    put<K, W>(jC, c, Cc | bit);
+    put<K, W>(jB, c, pick<K, W>(jB, c) | a);
+  }
+}
+
 template <int K, typename W>
 __host__ __device__ constexpr int heavy_depth() {
   return sizeof(W) == 4 ? 32 : 64;
@@ -591,7 +618,8 @@ __device__ __forceinline__ void slot_unlock(HeavySlot* s) {
 template <int K, typename W>
 __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const W (&sC)[K], const W (&sB)[K], W sU,
                                   int scost, int smu, Path sP, int sdepth, int& gcost, Path& gP, bool& mine,
-                                  W (&bestC)[K], unsigned& steps_out, bool& capped_out, bool& spilled) {
+                                  W (&bestC)[K], unsigned& steps_out, bool& capped_out, bool& spilled,
+                                  unsigned* iters_out = nullptr) {
   using O = WordOps<W>;
   constexpr bool kTwo = sizeof(W) == 8;
   const int lane = threadIdx.x & 31;
@@ -619,6 +647,14 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
     B[c] = lane == 0 ? sB[c] : W(0);
   }
   int cost = scost, maxused = smu, depth = sdepth, d0 = sdepth;
+  // the lane's start node N_{d0} (node_from_start)
+  W C0[K], B0[K], U0 = U;
+  int cost0 = scost;
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    C0[c] = C[c];
+    B0[c] = B[c];
+  }
   bool active = lane == 0, enter = lane == 0;
   W f_saved = 0, f_adj = 0, f_sadj = 0;
   int f_cost = 0, f_v = 0, f_c = -1, f_mu = -1, f_lim = 0;
@@ -658,8 +694,12 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           const int j = __ffsll((long long)(open & donatable)) - 1;
           int pk, jc;
           W jU;
-          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
-                                             w_stitch, xB, xC, jU, jc);
+          if (j - d0 < depth - 1 - j)
+            node_from_start<K, W, heavy_depth<K, W>()>(j, d0, C0, B0, U0, cost0, F, lane, adj, sadj, w_stitch, xB,
+                                                       xC, jU, jc);
+          else
+            node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
+                                               w_stitch, xB, xC, jU, jc);
           if (j == depth - 1) {
             pk = pk16(f_v, f_c, f_mu, f_lim);
             f_lim -= 1;
@@ -701,11 +741,11 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
         if (take) {
 #pragma unroll
           for (int c = 0; c < K; ++c) {
-            C[c] = xC[c];
-            B[c] = xB[c];
+            C[c] = C0[c] = xC[c];
+            B[c] = B0[c] = xB[c];
           }
-          U = xU;
-          cost = xcost;
+          U = U0 = xU;
+          cost = cost0 = xcost;
           maxused = xmu;
           P = xP;
           depth = d0 = xd;
@@ -893,6 +933,8 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
 #pragma unroll
               for (int c = 0; c < K; ++c) hs->C[c] = (unsigned long long)u.col[c];
               hs->ci = u.ci;
+              hs->ncl = ncl <= 16 ? ncl : -1;  // (more cliques: the items recompute them)
+              for (int q = 0; q < ncl && q < 16; ++q) hs->cl[q] = (unsigned long long)cl[q];
               __threadfence();
               u.slot = sl;
             }
@@ -919,8 +961,12 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           int at = base + excl;
           W jB[K], jC[K], jU;
           int pk, jc;
-          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
-                                             w_stitch, jB, jC, jU, jc);
+          if (j - d0 < depth - 1 - j)
+            node_from_start<K, W, heavy_depth<K, W>()>(j, d0, C0, B0, U0, cost0, F, lane, adj, sadj, w_stitch, jB,
+                                                       jC, jU, jc);
+          else
+            node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
+                                               w_stitch, jB, jC, jU, jc);
           if (j == depth - 1) {
             pk = pk16(f_v, f_c, f_mu, f_lim);
             f_lim = f_c;  // its children are in the queue now
@@ -973,6 +1019,7 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
   steps_out = tot;
   capped_out = __any_sync(0xffffffffu, capped);
+  if (iters_out) *iters_out = iters;
 }
 
 // A starting incumbent for the exact search ("seeded
@@ -1180,7 +1227,7 @@ __device__ void heavy_unit_done(const GraphView& g, const Workspace& w, const He
 // A heavy component's pool record -> shared memory (masks, clique partition).
 template <int K, typename W>
 __device__ void heavy_load(const Workspace& w, size_t off, int n, W* s_adj, W* s_sadj, W* s_cl, int& ncl,
-                           const int* colors, W (&col)[K]) {
+                           const int* colors, W (&col)[K], const HeavySlot* hs = nullptr) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int c = 0; c < K; ++c) col[c] = 0;
@@ -1200,7 +1247,13 @@ __device__ void heavy_load(const Workspace& w, size_t off, int n, W* s_adj, W* s
     }
   }
   __syncwarp();
-  ncl = heavy_clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, heavy_clique_min<K>()) : 0;
+  const int cached = hs ? __ldcg(&hs->ncl) : -1;
+  if (cached >= 0) {  // a spilled item: the partition its component's first unit stored in the slot
+    ncl = cached;
+    if (lane < ncl) s_cl[lane] = (W)__ldcg(&hs->cl[lane]);
+  } else {
+    ncl = heavy_clique_min<K>() ? clique_partition<W>(s_adj, 1, n, s_cl, 1, heavy_clique_min<K>()) : 0;
+  }
   __syncwarp();
 }
 
@@ -1214,6 +1267,28 @@ struct HeavyAcc {
   int max = 0, capped = 0;
 };
 
+// MPLD_DIAG_HEAVY builds: one trace record per heavy unit (component or spilled
+// item) in Workspace::est (free outside sharded runs): ci | n << 32 | item << 48,
+// nodes, start / end %globaltimer; read back by mpld_context_debug out[96..]
+#ifndef MPLD_DIAG_HEAVY
+#define MPLD_DIAG_HEAVY 0
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void heavy_trace(const Workspace& w, int ci, int n, int item, unsigned long long steps,
+                                            unsigned long long t0) {
+  if (!MPLD_DIAG_HEAVY || (threadIdx.x & 31) != 0) return;
+  const unsigned long long i = atomicAdd(&w.ctl->dbg[7], 1ull);
+  if (4 * i + 3 >= (unsigned long long)w.diag_cap) return;
+  w.est[4 * i] = (unsigned)ci | ((unsigned long long)n << 32) | ((unsigned long long)item << 48);
+  w.est[4 * i + 1] = steps;
+  w.est[4 * i + 2] = t0;
+  w.est[4 * i + 3] = gtimer();
+}
+
 template <int K, typename W>
 __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, int w_stitch, int* colors,
                                 long long* counts, unsigned char* smem, int* s_pair, int& cur_ci, int& cur_ncl,
@@ -1224,6 +1299,7 @@ __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, i
   W* s_adj = (W*)smem;
   W* s_sadj = s_adj + kMaxComp;
   W* s_cl = s_sadj + kMaxComp;
+  const unsigned long long t0 = MPLD_DIAG_HEAVY ? gtimer() : 0ull;
   HeavyUnit<K, W> u;
   u.w_stitch = w_stitch;
   u.cls = cls;
@@ -1268,8 +1344,9 @@ __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, i
   for (int c = 0; c < K; ++c) zero[c] = 0;
   bool mine, capped, spilled;
   unsigned steps;
+  unsigned iters = 0;
   warp_heavy_search<K, W>(u, w, zero, zero, WordOps<W>::full(u.n), 0, -1, Path{0ull, 0ull}, 0, gcost, gP, mine,
-                          bestC, steps, capped, spilled);
+                          bestC, steps, capped, spilled, &iters);
   const int* porder = w.porder + off;
   if (u.slot < 0) {  // searched whole: the final colouring is the warp's best (or the light leaf)
     W fin[K];
@@ -1287,6 +1364,7 @@ __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, i
   } else {
     heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, porder, colors, counts);
   }
+  heavy_trace(w, u.ci, u.n, 0, steps | ((unsigned long long)iters << 32), t0);
   acc.steps += steps;
   acc.max = max(acc.max, (int)min(steps, (unsigned)INT_MAX));
   acc.capped += capped ? 1 : 0;  // per unit (a spilled component may count more than once)
@@ -1303,6 +1381,7 @@ __device__ void heavy_item(const GraphView& g, const Workspace& w, int pos, int 
                            HeavyAcc& acc) {
   constexpr int cls = sizeof(W) == 4 ? 0 : 1;
   const int lane = threadIdx.x & 31;
+  const unsigned long long t0 = MPLD_DIAG_HEAVY ? gtimer() : 0ull;
   W* s_adj = (W*)smem;
   W* s_sadj = s_adj + kMaxComp;
   W* s_cl = s_sadj + kMaxComp;
@@ -1337,7 +1416,7 @@ __device__ void heavy_item(const GraphView& g, const Workspace& w, int pos, int 
     atomicAdd(&w.ctl->wq_read[cls], 1);
   }
   if (u.ci != cur_ci) {  // items of one component mostly follow each other: keep its masks
-    heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, nullptr, u.col);
+    heavy_load<K, W>(w, off, u.n, s_adj, s_sadj, s_cl, u.ncl, nullptr, u.col, hs);
     cur_ci = u.ci;
     cur_ncl = u.ncl;
   }
@@ -1351,8 +1430,11 @@ __device__ void heavy_item(const GraphView& g, const Workspace& w, int pos, int 
   W bestC[K];
   bool mine, capped, spilled;
   unsigned steps;
-  warp_heavy_search<K, W>(u, w, sC, sB, sU, scost, smu, sP, sdepth, gcost, gP, mine, bestC, steps, capped, spilled);
+  unsigned iters = 0;
+  warp_heavy_search<K, W>(u, w, sC, sB, sU, scost, smu, sP, sdepth, gcost, gP, mine, bestC, steps, capped, spilled,
+                          &iters);
   heavy_unit_done<K, W>(g, w, u, gcost, gP, mine, bestC, w.porder + off, colors, counts);
+  heavy_trace(w, u.ci, u.n, 1 + sdepth, steps | ((unsigned long long)iters << 32), t0);
   acc.steps += steps;
   acc.capped += capped ? 1 : 0;
   __syncwarp();

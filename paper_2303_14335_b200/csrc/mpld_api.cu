@@ -286,7 +286,7 @@ Workspace workspace(mpld_context* ctx) {
   return Workspace{ctx->deg,   ctx->hround, ctx->bmask,  ctx->prio,  ctx->q0,    ctx->q1,    ctx->roots,
                    ctx->crec,  ctx->pmask,  ctx->porder, ctx->hcomp, ctx->hcost, ctx->wide,  ctx->ctl,   ctx->wq,
                    ctx->wq_flag, ctx->hslot, ctx->est,  ctx->bsum,  ctx->epoch, ctx->spill_iters, ctx->tail_slots,
-                   ctx->build_err, ctx->greedy_salt, ctx->greedy_rounds,
+                   ctx->build_err, ctx->cap_n, ctx->greedy_salt, ctx->greedy_rounds,
                    ctx->gate_active ? &ctx->ctl_tile->gate : nullptr,
                    ctx->t_par, ctx->t_cnt, ctx->t_end, ctx->t_pos, ctx->t_perm, ctx->t_pend};
 }
@@ -1177,6 +1177,13 @@ int mpld_context_debug(mpld_context* ctx, int64_t* out, int n) {
   v[95] = c.truncated;
   v[88] = gate;
   for (int i = 0; i < n && i < 96; ++i) out[i] = v[i];
+  if (n > 96 && ctx->est) {  // MPLD_DIAG_HEAVY builds: the heavy-search trace (4 words per unit)
+    const int64_t m = std::min<int64_t>(n - 96, std::min<int64_t>(4 * (int64_t)c.dbg[7], ctx->cap_n));
+    if (m > 0) {
+      e = cudaMemcpy(out + 96, ctx->est, sizeof(int64_t) * (size_t)m, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_fail(e, "debug copy");
+    }
+  }
   return MPLD_OK;
 }
 

@@ -160,7 +160,8 @@ struct HeavySlot {
   int bcost, pad0;            // the best cost known (atomicMin, read without the lock: pruning)
   unsigned long long pa, pb, lpa, lpb;
   unsigned long long C[4];    // colour masks of the best leaf
-  int ci, pad[1];             // component (pool record)
+  int ci, ncl;                // component (pool record); its clique partition (R7 bound) for the items:
+  unsigned long long cl[16];  // computed once by the spilling unit instead of once per item
 };
 
 struct Workspace {
@@ -191,6 +192,7 @@ struct Workspace {
   int tail_slots;        // cluster tails: frontier slots per CTA in use (MPLD_TAIL_SLOTS lowers it: tests)
   int* build_err;        // set when a CSR built on the device (upper-triangle upload) saw bad input; the
                          // simplification turns it into MPLD_ERR_GRAPH and clears it
+  long long diag_cap;    // u64 entries of est usable by diagnostics (MPLD_DIAG_HEAVY builds)
   unsigned greedy_salt;  // heavy search: seed offset of the greedy starting colourings (MPLD_GREEDY_SALT)
   int greedy_rounds;     // heavy search: rounds of 32 greedy colourings (MPLD_GREEDY_ROUNDS, default 1)
   const int* gate;       // whole-graph kernels after the tile pipeline: run only if *gate != 0 (nullptr:

@@ -379,10 +379,11 @@ class Context:
     def reset_timing(self):
         _check(lib().mpld_context_reset_timing(self._h))
 
-    def debug(self):
-        """Diagnostics of the last call (include/mpld.h mpld_context_debug)."""
-        out = np.zeros(96, dtype=np.int64)
-        _check(lib().mpld_context_debug(self._h, out.ctypes.data, 96))
+    def debug(self, extra: int = 0):
+        """Diagnostics of the last call (include/mpld.h mpld_context_debug); `extra`
+        more words: the heavy-search trace of MPLD_DIAG_HEAVY builds."""
+        out = np.zeros(96 + int(extra), dtype=np.int64)
+        _check(lib().mpld_context_debug(self._h, out.ctypes.data, 96 + int(extra)))
         return out
 
     def kernel_times(self):
