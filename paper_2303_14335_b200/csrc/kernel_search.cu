@@ -405,7 +405,10 @@ constexpr bool kSeedIncumbent = MPLD_SEED_INCUMBENT != 0;  // greedy starting in
 #define MPLD_PAIR_BOUND 0  // measured slower (configs[2] 1.24-1.34 -> 1.56-1.62 ms, configs[1] +10 us): off
 #endif
 constexpr bool kPairBound = MPLD_PAIR_BOUND != 0;  // exact mode: the matching term of the lower bound  // the work queue is fed while it holds fewer items than this
-constexpr unsigned kSpillCheck = 64;  // spill / slot-sync checks every this many iterations (power of two),
+#ifndef MPLD_SPILL_CHECK
+#define MPLD_SPILL_CHECK 64
+#endif
+constexpr unsigned kSpillCheck = MPLD_SPILL_CHECK;  // spill / slot-sync checks every this many iterations (power of two),
                                       // from Workspace::spill_iters on
 
 struct Path {  // levels 0..31 in a, 32..63 in b; 2 bits per level, level 0 most significant
