@@ -405,6 +405,9 @@ constexpr bool kSeedIncumbent = MPLD_SEED_INCUMBENT != 0;  // greedy starting in
 #define MPLD_PAIR_BOUND 0  // measured slower (configs[2] 1.24-1.34 -> 1.56-1.62 ms, configs[1] +10 us): off
 #endif
 constexpr bool kPairBound = MPLD_PAIR_BOUND != 0;  // exact mode: the matching term of the lower bound  // the work queue is fed while it holds fewer items than this
+#ifndef MPLD_HELPER_DIV
+#define MPLD_HELPER_DIV 2  // helpers waiting for spilled work: gridDim.x / this
+#endif
 #ifndef MPLD_SPILL_CHECK
 #define MPLD_SPILL_CHECK 64
 #endif
@@ -1270,6 +1273,19 @@ struct HeavyAcc {
   int max = 0, capped = 0;
 };
 
+// A unit is finished: count it; the unit that completes the last pending work
+// (every heavy component and every item reserved so far — no unit runs, so no
+// item can be added) raises heavy_finished for the warps waiting for items.
+__device__ __forceinline__ void heavy_unit_finished(Control* ctl, int cls, int n_heavy0, int n_heavy1) {
+  __threadfence();
+  const int d = atomicAdd(&ctl->wq_done[cls], 1) + 1;
+  __threadfence();
+  const int d0 = cls == 0 ? d : *(volatile int*)&ctl->wq_done[0];
+  const int d1 = cls == 1 ? d : *(volatile int*)&ctl->wq_done[1];
+  const int t0 = *(volatile int*)&ctl->wq_tail[0], t1 = *(volatile int*)&ctl->wq_tail[1];
+  if (d0 >= n_heavy0 + t0 && d1 >= n_heavy1 + t1) atomicExch(&ctl->heavy_finished, 1);
+}
+
 // MPLD_DIAG_HEAVY builds: one trace record per heavy unit (component or spilled
 // item) in Workspace::est (free outside sharded runs): ci | n << 32 | item << 48,
 // nodes, start / end %globaltimer; read back by mpld_context_debug out[96..]
@@ -1372,10 +1388,7 @@ __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, i
   acc.max = max(acc.max, (int)min(steps, (unsigned)INT_MAX));
   acc.capped += capped ? 1 : 0;  // per unit (a spilled component may count more than once)
   __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    atomicAdd(&w.ctl->wq_done[cls], 1);
-  }
+  if (lane == 0) heavy_unit_finished(w.ctl, cls, __ldcg(&w.ctl->n_heavy[0]), __ldcg(&w.ctl->n_heavy[1]));
 }
 
 template <int K, typename W>
@@ -1441,10 +1454,7 @@ __device__ void heavy_item(const GraphView& g, const Workspace& w, int pos, int 
   acc.steps += steps;
   acc.capped += capped ? 1 : 0;
   __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    atomicAdd(&w.ctl->wq_done[cls], 1);
-  }
+  if (lane == 0) heavy_unit_finished(w.ctl, cls, __ldcg(&w.ctl->n_heavy[0]), __ldcg(&w.ctl->n_heavy[1]));
 }
 
 // One warp per heavy component, both word classes in one launch: the 64-bit
@@ -1481,11 +1491,14 @@ __global__ void __launch_bounds__(32, 8) mpld_exact_cover_search_heavy(GraphView
   // no component left: stay for spilled work only if some may come (small
   // components never run long; a spill without helpers is still drained by the
   // warps that are running, the spilling one included)
+  // Only the first gridDim.x / MPLD_HELPER_DIV warps stay as helpers: every
+  // waiting warp polls the ring's counters, and a thousand pollers on those
+  // lines slow down the running units' own spill checks and finish counts.
   int leave = 0;
   if (lane == 0)
-    leave = *(volatile int*)&ctl->may_spill == 0 && *(volatile int*)&ctl->wq_tail[0] == 0 &&
-            *(volatile int*)&ctl->wq_tail[1] == 0;
-  unsigned backoff = 32, polls = 0;
+    leave = (*(volatile int*)&ctl->may_spill == 0 || (int)blockIdx.x >= (int)gridDim.x / MPLD_HELPER_DIV) &&
+            *(volatile int*)&ctl->wq_tail[0] == 0 && *(volatile int*)&ctl->wq_tail[1] == 0;
+  unsigned backoff = 32;
   while (!__shfl_sync(0xffffffffu, leave, 0)) {
     int pos = -1, pcls = 0;
     if (lane == 0) {
@@ -1523,13 +1536,8 @@ __global__ void __launch_bounds__(32, 8) mpld_exact_cover_search_heavy(GraphView
       continue;
     }
     // done when every unit (heavy components + items) of both classes has
-    // finished: no unit is running, so no item can be added
-    if (lane == 0 && (++polls & 3) == 0) {
-      const int d0 = *(volatile int*)&ctl->wq_done[0], d1 = *(volatile int*)&ctl->wq_done[1];
-      __threadfence();
-      const int t0 = *(volatile int*)&ctl->wq_tail[0], t1 = *(volatile int*)&ctl->wq_tail[1];
-      leave = d0 >= n_heavy0 + t0 && d1 >= n_heavy1 + t1;
-    }
+    // finished (raised by the unit that finished last: heavy_unit_finished)
+    if (lane == 0) leave = *(volatile int*)&ctl->heavy_finished;
     if (!__shfl_sync(0xffffffffu, leave, 0)) {
       __nanosleep(backoff);
       backoff = min(backoff * 2u, (unsigned)MPLD_POLL_CAP);

@@ -66,6 +66,7 @@ struct Control {
   int wq_done[2];                  // work units (heavy components + items) finished per word class (polled)
   alignas(128) int wq_read[2];     // ... items copied out by their consumers (ring slots free again)
   int spill_refused;               // spills refused (ring full or no slot left): those units ran on alone
+  alignas(128) int heavy_finished; // set by the unit that finishes the last pending work: waiting warps leave
   alignas(128) unsigned long long comp_pool;  // components << 32 | pool words used by this search call (reset with n_heavy)
   alignas(128) unsigned long long vh[4];  // validation: symmetry hashes (CE forward / transposed, SE forward / transposed)
   unsigned long long t[16];  // diagnostics: %globaltimer at phase boundaries (ns)
@@ -146,7 +147,10 @@ __host__ __device__ __forceinline__ unsigned long long partition_estimate(int n,
 // of one component runs long hands its open work to all heavy warps as work
 // items (node states); a slot per spilled component gathers the best key.
 constexpr int kWQCap = 1 << 16;  // ring slots of spilled work items per word class
-constexpr int kHelpersMinN = 16;  // heavy components this large may run long enough to spill
+#ifndef MPLD_HELPERS_MIN_N
+#define MPLD_HELPERS_MIN_N 12
+#endif
+constexpr int kHelpersMinN = MPLD_HELPERS_MIN_N;  // heavy components this large may run long enough to spill
 constexpr int kSlots = 1024;     // spilled components per call
 struct WorkItem {
   int slot, depth, cost, mu;
