@@ -15,6 +15,7 @@
 // (measured on B200: kP = 1, kNb = 4 and one 1024-thread CTA per SM are the
 // fastest; lockstep tiles of 2-3 items per thread lengthen every level).
 #include <algorithm>
+#include <climits>
 #include <cooperative_groups.h>
 
 #include "mpld_internal.cuh"
@@ -1157,40 +1158,54 @@ __global__ void __launch_bounds__(256) mpld_shard_import(long long m, const int*
 }
 
 // ---------------------------------------------------------------------------
-// An upper-triangle entry p of row v (row start a) is valid iff v < u < n and
-// it is larger than its row predecessor.
-__device__ __forceinline__ bool up_entry_ok(const int* col_up, int a, int p, int v, int n) {
-  const int u = __ldg(&col_up[p]);
-  return u > v && u < n && (p == a || u > __ldg(&col_up[p - 1]));
-}
-
-// ---------------------------------------------------------------------------
 // The graph build of the compact uploads in ONE cooperative launch (two
 // 1024-thread CTAs per SM, five grid barriers).  CTA c owns the vertex range
 // [c n / G, (c+1) n / G); each of its warps a contiguous sub-range, walked in
 // chunks of 32 consecutive vertices (coalesced, warp scans).  One counter word
 // per vertex holds both degree counts (CE in the low 24 bits, SE above).
 //   P1 zero the counters; warp / CTA sums of deg_up
-//   P2 scan of deg_up -> rp_up; for every valid upper entry (v, u): count the
-//      lower entry of row u, v's own valid entries; stitch pairs
-//      (grid-stride): count both ends
+//   P2 scan of deg_up -> rp_up; the chunk's upper entries 32 at a time
+//      (coalesced; row by a search over the lanes' offsets): an entry (v, u)
+//      is valid iff v < u < n and it is larger than its row predecessor; every
+//      valid one counts the lower entry of row u and one entry of row v
+//      (aggregated per row); stitch pairs (grid-stride): count both ends
 //   P3 warp / CTA sums of both degree counts
 //   P4 scans -> ce_rp, se_rp
-//   P5 scatter: lower CE entries and SE entries by atomics on the fill word,
-//      the upper CE entries in order after the lower ones
+//   P5 scatter (entry-parallel as P2): lower CE entries and SE entries by
+//      atomics on the fill word, the upper CE entries in order after the lower
+//      ones
 //   P6 sort the lower part of every CE row with >= 2 of them, every SE row
 //      with >= 2 entries (insertion sort: rows are short)
-// Validity of an upper entry and error reporting as up_entry_ok.
-__device__ __forceinline__ void build_insertion_sort(int* col, int a, int b) {
-  for (int i = a + 1; i < b; ++i) {
-    const int x = col[i];
-    int j = i - 1;
-    while (j >= a && col[j] > x) {
-      col[j + 1] = col[j];
-      --j;
+// Rows of up to 8 entries are sorted in registers (all loads issued at once),
+// longer ones in place.
+__device__ __forceinline__ void build_row_sort(int* col, int a, int b) {
+  constexpr int kR = 8;
+  if (b - a > kR) {
+    for (int i = a + 1; i < b; ++i) {
+      const int x = col[i];
+      int j = i - 1;
+      while (j >= a && col[j] > x) {
+        col[j + 1] = col[j];
+        --j;
+      }
+      col[j + 1] = x;
     }
-    col[j + 1] = x;
+    return;
   }
+  int r[kR];
+#pragma unroll
+  for (int i = 0; i < kR; ++i) r[i] = a + i < b ? col[a + i] : INT_MAX;
+#pragma unroll
+  for (int i = 1; i < kR; ++i)  // insertion network on registers
+#pragma unroll
+    for (int j = i; j > 0; --j) {
+      const int lo = min(r[j - 1], r[j]), hi = max(r[j - 1], r[j]);
+      r[j - 1] = lo;
+      r[j] = hi;
+    }
+#pragma unroll
+  for (int i = 0; i < kR; ++i)
+    if (a + i < b) col[a + i] = r[i];
 }
 
 __device__ __forceinline__ int warp_scan_excl(int x, int& total) {
@@ -1203,6 +1218,16 @@ __device__ __forceinline__ int warp_scan_excl(int x, int& total) {
   }
   total = __shfl_sync(0xffffffffu, y, 31);
   return y - x;
+}
+
+// Row of entry i of a warp's chunk: the first lane whose inclusive entry
+// offset exceeds i (lanes without entries are skipped); 32 when i >= total.
+__device__ __forceinline__ int warp_row_of(int incl, int i) {
+  int o = 0;
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1)
+    if (__shfl_sync(0xffffffffu, incl, o + st - 1) <= i) o += st;
+  return min(o, 31);
 }
 
 constexpr int kCeMask = (1 << 24) - 1;  // CE count in a build counter word; SE count << 24
@@ -1255,25 +1280,35 @@ __global__ void __launch_bounds__(1024, 1) mpld_graph_build(GraphBuild b) {
       const int v = vv + lane;
       const int d = v < w1 ? (int)b.deg_up[v] : 0;
       int t;
-      const int a = carry + warp_scan_excl(d, t);
+      const int ex = warp_scan_excl(d, t);
+      const int a = carry + ex;
+      const int base = carry;
       carry += t;
-      if (v >= w1) continue;
-      b.rp_up[v] = a;
-      const int e1 = min(a + d, b.m_up);
-      bad |= a + d > b.m_up;
-      int k = 0;
-      for (int p = a; p < e1; ++p) {
-        if (up_entry_ok(b.col_up, a, p, v, n)) {
-          ++k;
-          atomicAdd(&cnt[__ldg(&b.col_up[p])], 1);  // the lower entry v of row u
-        } else {
-          bad = true;
+      if (v < w1) {
+        b.rp_up[v] = a;
+        bad |= a + d > b.m_up;
+        if (v == n - 1) {  // the last vertex closes the upper row pointer
+          b.rp_up[n] = a + d;
+          if (a + d != b.m_up) bad = true;
         }
       }
-      if (k) atomicAdd(&cnt[v], k);
-      if (v == n - 1) {  // the last vertex closes the upper row pointer
-        b.rp_up[n] = a + d;
-        if (a + d != b.m_up) bad = true;
+      // the chunk's entries 32 at a time (coalesced), each with its row found
+      // by a search over the lanes' inclusive offsets
+      const int incl = ex + d;
+      const int tl = min(t, max(b.m_up - base, 0));
+      for (int i0 = 0; i0 < tl; i0 += 32) {
+        const int i = i0 + lane;
+        const int o = warp_row_of(incl, i);
+        const int ov = vv + o, oex = __shfl_sync(0xffffffffu, ex, o);
+        const int u = i < tl ? __ldg(&b.col_up[base + i]) : 0;
+        int pu = __shfl_up_sync(0xffffffffu, u, 1);
+        if (lane == 0 && i < tl && i > oex) pu = __ldg(&b.col_up[base + i - 1]);
+        const bool ok = i < tl && u > ov && u < n && (i == oex || u > pu);
+        bad |= i < tl && !ok;
+        if (ok) atomicAdd(&cnt[u], 1);  // the lower entry ov of row u
+        const unsigned grp = __match_any_sync(0xffffffffu, i < tl ? ov : -1 - lane);
+        const int k = __popc(__ballot_sync(0xffffffffu, ok) & grp);
+        if (k && lane == __ffs(grp) - 1) atomicAdd(&cnt[ov], k);
       }
     }
     if (bad) atomicOr(b.err, 1);
@@ -1361,17 +1396,26 @@ __global__ void __launch_bounds__(1024, 1) mpld_graph_build(GraphBuild b) {
       if (se) b.se_rp[n] = 0;
     }
   }
-  if (ce && !failed)
-    for (int v = w0 + lane; v < w1; v += 32) {
-      const int a = __ldcg(&b.rp_up[v]), e1 = min(a + (int)b.deg_up[v], b.m_up);
-      int nup = 0;
-      for (int p = a; p < e1; ++p) nup += up_entry_ok(b.col_up, a, p, v, n) ? 1 : 0;
-      int at = __ldcg(&b.ce_rp[v + 1]) - nup;
-      for (int p = a; p < e1; ++p) {
-        if (!up_entry_ok(b.col_up, a, p, v, n)) continue;
-        const int u = __ldg(&b.col_up[p]);
-        b.ce_col[at++] = u;
-        b.ce_col[__ldcg(&b.ce_rp[u]) + (atomicAdd(&fill[u], 1) & kCeMask)] = v;
+  if (ce && !failed)  // every entry is valid here (else the build failed): upper part at the end of row v
+    for (int vv = w0; vv < w1; vv += 32) {
+      const int v = vv + lane;
+      const int d = v < w1 ? (int)b.deg_up[v] : 0;
+      const int a = v < w1 ? __ldcg(&b.rp_up[v]) : 0;
+      const int up0 = v < w1 ? __ldcg(&b.ce_rp[v + 1]) - d : 0;
+      int t;
+      const int ex = warp_scan_excl(d, t);
+      const int incl = ex + d;
+      const int base = __shfl_sync(0xffffffffu, a - ex, 0);  // lane 0 always holds a vertex
+      for (int i0 = 0; i0 < t; i0 += 32) {
+        const int i = i0 + lane;
+        const int o = warp_row_of(incl, i);
+        const int ov = vv + o;
+        const int orow = __shfl_sync(0xffffffffu, up0, o), oex = __shfl_sync(0xffffffffu, ex, o);
+        if (i < t) {
+          const int u = __ldg(&b.col_up[base + i]);
+          b.ce_col[orow + (i - oex)] = u;
+          b.ce_col[__ldcg(&b.ce_rp[u]) + (atomicAdd(&fill[u], 1) & kCeMask)] = ov;
+        }
       }
     }
   if (se && !failed)
@@ -1387,9 +1431,9 @@ __global__ void __launch_bounds__(1024, 1) mpld_graph_build(GraphBuild b) {
     const int f = __ldcg(&fill[v]);
     if (ce && (f & kCeMask) >= 2) {
       const int a = __ldcg(&b.ce_rp[v]);
-      build_insertion_sort(b.ce_col, a, a + (f & kCeMask));
+      build_row_sort(b.ce_col, a, a + (f & kCeMask));
     }
-    if (se && (f >> 24) >= 2) build_insertion_sort(b.se_col, __ldcg(&b.se_rp[v]), __ldcg(&b.se_rp[v + 1]));
+    if (se && (f >> 24) >= 2) build_row_sort(b.se_col, __ldcg(&b.se_rp[v]), __ldcg(&b.se_rp[v + 1]));
   }
 }
 
