@@ -554,33 +554,6 @@ __device__ __forceinline__ void node_at(int j, int depth, const W (&B)[K], const
   }
 }
 
-// The same node N_j rebuilt forward from the lane's start node N_{d0} (the
-// unit's root, or the node the lane took): apply the selected rows of frames
-// d0..j-1.  Identical to node_at; the callers take the shorter direction.
-template <int K, typename W, int D>
-__device__ __forceinline__ void node_from_start(int j, int d0, const W (&C0)[K], const W (&B0)[K], W U0, int cost0,
-                                                const LaneFrames<K, W, D>& F, int lane, const W* adj, const W* sadj,
-                                                int w_stitch, W (&jB)[K], W (&jC)[K], W& jU, int& jcost) {
-#pragma unroll
-  for (int c = 0; c < K; ++c) {
-    jB[c] = B0[c];
-    jC[c] = C0[c];
-  }
-  jU = U0;
-  jcost = cost0;
-  for (int d = d0; d < j; ++d) {
-    const int pk = F.pk[d][lane];
-    const int v = pk_v(pk), c = pk_c(pk);
-    const W bit = W(1) << v;
-    const W a = adj[v];
-    jU &= ~bit;
-    const W Cc = pick<K, W>(jC, c);
-    jcost += row_cost<W>(a, sadj[v], Cc, jU, w_stitch);
-    put<K, W>(jC, c, Cc | bit);
-    put<K, W>(jB, c, pick<K, W>(jB, c) | a);
-  }
-}
-
 template <int K, typename W>
 __host__ __device__ constexpr int heavy_depth() {
   return sizeof(W) == 4 ? 32 : 64;
@@ -653,14 +626,6 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
     B[c] = lane == 0 ? sB[c] : W(0);
   }
   int cost = scost, maxused = smu, depth = sdepth, d0 = sdepth;
-  // the lane's start node N_{d0} (node_from_start)
-  W C0[K], B0[K], U0 = U;
-  int cost0 = scost;
-#pragma unroll
-  for (int c = 0; c < K; ++c) {
-    C0[c] = C[c];
-    B0[c] = B[c];
-  }
   bool active = lane == 0, enter = lane == 0;
   W f_saved = 0, f_adj = 0, f_sadj = 0;
   int f_cost = 0, f_v = 0, f_c = -1, f_mu = -1, f_lim = 0;
@@ -700,12 +665,8 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           const int j = __ffsll((long long)(open & donatable)) - 1;
           int pk, jc;
           W jU;
-          if (j - d0 < depth - 1 - j)
-            node_from_start<K, W, heavy_depth<K, W>()>(j, d0, C0, B0, U0, cost0, F, lane, adj, sadj, w_stitch, xB,
-                                                       xC, jU, jc);
-          else
-            node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
-                                               w_stitch, xB, xC, jU, jc);
+          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
+                                             w_stitch, xB, xC, jU, jc);
           if (j == depth - 1) {
             pk = pk16(f_v, f_c, f_mu, f_lim);
             f_lim -= 1;
@@ -747,11 +708,11 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
         if (take) {
 #pragma unroll
           for (int c = 0; c < K; ++c) {
-            C[c] = C0[c] = xC[c];
-            B[c] = B0[c] = xB[c];
+            C[c] = xC[c];
+            B[c] = xB[c];
           }
-          U = U0 = xU;
-          cost = cost0 = xcost;
+          U = xU;
+          cost = xcost;
           maxused = xmu;
           P = xP;
           depth = d0 = xd;
@@ -967,12 +928,8 @@ __device__ void warp_heavy_search(HeavyUnit<K, W>& u, const Workspace& w, const 
           int at = base + excl;
           W jB[K], jC[K], jU;
           int pk, jc;
-          if (j - d0 < depth - 1 - j)
-            node_from_start<K, W, heavy_depth<K, W>()>(j, d0, C0, B0, U0, cost0, F, lane, adj, sadj, w_stitch, jB,
-                                                       jC, jU, jc);
-          else
-            node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
-                                               w_stitch, jB, jC, jU, jc);
+          node_at<K, W, heavy_depth<K, W>()>(j, depth, B, C, U, f_saved, f_v, f_c, f_cost, F, lane, adj, sadj,
+                                             w_stitch, jB, jC, jU, jc);
           if (j == depth - 1) {
             pk = pk16(f_v, f_c, f_mu, f_lim);
             f_lim = f_c;  // its children are in the queue now
@@ -1279,6 +1236,7 @@ struct HeavyAcc {
 __device__ __forceinline__ void heavy_unit_finished(Control* ctl, int cls, int n_heavy0, int n_heavy1) {
   __threadfence();
   const int d = atomicAdd(&ctl->wq_done[cls], 1) + 1;
+  if (!*(volatile int*)&ctl->may_spill) return;  // no warp waits for spilled work (set before this kernel)
   __threadfence();
   const int d0 = cls == 0 ? d : *(volatile int*)&ctl->wq_done[0];
   const int d1 = cls == 1 ? d : *(volatile int*)&ctl->wq_done[1];
