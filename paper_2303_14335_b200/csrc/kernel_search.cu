@@ -401,6 +401,9 @@ constexpr int kQueueLow = MPLD_QUEUE_LOW;
 #define MPLD_SEED_INCUMBENT 1
 #endif
 constexpr bool kSeedIncumbent = MPLD_SEED_INCUMBENT != 0;  // greedy starting incumbent of heavy components
+#ifndef MPLD_SEED_MIN_N
+#define MPLD_SEED_MIN_N 0  // ... of at least this many vertices (smaller ones start from their light leaf)
+#endif
 #ifndef MPLD_PAIR_BOUND
 #define MPLD_PAIR_BOUND 0  // measured slower (configs[2] 1.24-1.34 -> 1.56-1.62 ms, configs[1] +10 us): off
 #endif
@@ -1297,7 +1300,7 @@ __device__ void heavy_component(const GraphView& g, const Workspace& w, int h, i
   cur_ci = u.ci;
   cur_ncl = u.ncl;
   W gcol[K];
-  const int hc = (kSeedIncumbent || !light_leaf) ? warp_greedy_seed<K, W>(s_adj, s_sadj, u.n, w_stitch,
+  const int hc = ((kSeedIncumbent && u.n >= MPLD_SEED_MIN_N) || !light_leaf) ? warp_greedy_seed<K, W>(s_adj, s_sadj, u.n, w_stitch,
                                                                           (unsigned)u.ci + w.greedy_salt,
                                                                           w.greedy_rounds, gcol)
                                                  : INT_MAX;
