@@ -180,3 +180,12 @@ def test_tiles_reject_invalid_input_like_the_whole_graph_pipeline():
     with pytest.raises(mp.MPLDError) as ei:
         mp.decompose_graph(bad, 3, 0.1, max_steps=BUDGET, flags=mp.MPLD_FLAG_VALIDATE | mp.MPLD_FLAG_TILES)
     assert ei.value.code == 2
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_tiles_every_k_with_stitches(k):
+    """k = 2, 3, 4 with stitch candidates, exact and budgeted: tiles against the
+    oracle and the default pipeline."""
+    g = synth.make_layout(6000, 7000, k=k, stitch_prob=0.6, comp_max=10, density=0.9, seed=40 + k)
+    _check(g, k, 0.1, 0, expect_gate=0)
+    _check(g, k, 0.5, 200, expect_gate=0)
