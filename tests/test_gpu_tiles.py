@@ -184,8 +184,23 @@ def test_tiles_reject_invalid_input_like_the_whole_graph_pipeline():
 
 @pytest.mark.parametrize("k", [2, 3, 4])
 def test_tiles_every_k_with_stitches(k):
-    """k = 2, 3, 4 with stitch candidates, exact and budgeted: tiles against the
-    oracle and the default pipeline."""
-    g = synth.make_layout(6000, 7000, k=k, stitch_prob=0.6, comp_max=10, density=0.9, seed=40 + k)
-    _check(g, k, 0.1, 0, expect_gate=0)
-    _check(g, k, 0.5, 200, expect_gate=0)
+    """k = 2, 3, 4 with stitch candidates, budgeted and (small components)
+    exact: tiles against the oracle and the default pipeline, 150 random
+    layouts in one batch (windows hold several layouts)."""
+    import random
+    rng = random.Random(70 + k)
+    graphs = []
+    for _ in range(150):
+        n = rng.randint(4, 14)
+        ce, se = [], []
+        for u in range(n):
+            for v in range(u + 1, n):
+                r = rng.random()
+                if r < 0.06:
+                    se.append((u, v))
+                elif r < 0.06 + rng.choice([0.2, 0.35]):
+                    ce.append((u, v))
+        graphs.append(from_edges(n, ce, se))
+    b = synth.concat(graphs)
+    _check(b, k, 0.5, 300, expect_gate=0)
+    _check(b, k, 0.1, 0, expect_gate=0)
