@@ -705,6 +705,10 @@ int mpld_context_create(int device, int64_t max_vertices, int32_t max_layouts, m
     return cuda_fail(e, "cudaStreamCreate");
   }
   ctx->blocks_prep = ctx->num_sms;  // one CTA per SM on the second stream, beside the search kernels
+  if (const char* pb = std::getenv("MPLD_PREP_BLOCKS")) {  // experiments: fewer SMs for the prep
+    const long v = std::strtol(pb, nullptr, 10);
+    if (v >= 1 && v <= ctx->num_sms) ctx->blocks_prep = (int)v;
+  }
   *out = ctx;
   return MPLD_OK;
 }
