@@ -170,14 +170,21 @@ constexpr int kLaneWarps = 2;  // warps per CTA of the light search (32-bit word
 #endif
 constexpr bool kStagedLight = MPLD_STAGED_LIGHT != 0;  // coalesced warp staging of the light kernel's records
 
+// A frame holds the word B[c] saved before its row was selected and 12 bits
+// of state.  For 64-bit words (kCompact) the node cost is not stored either:
+// popping back to a frame subtracts its row's cost from the child's (56 KB
+// per warp: four 64-bit lane warps per SM instead of three; the 32-bit light
+// kernel keeps the cost, measured faster there).  After the search the saved
+// rows hold the staged vertex ids.
 template <typename W, int N>
 struct __align__(16) LaneStore {
-  W A[N][32];        // adj[v][lane]
-  W S[N][32];        // sadj[v][lane]
-  W saved[N][32];    // frame d: B[c] before r(v,c) was selected
-  int cost[N][32];   // frame d: cost when the node was entered
-  int pk[N][32];     // frame d: v | (c+1) << 8 | (maxused+1) << 16
-  W cl[N / 2][32];   // clique masks (R7, k >= 4)
+  static constexpr bool kCompact = N > 32;
+  W A[N][32];                        // adj[v][lane]
+  W S[N][32];                        // sadj[v][lane]
+  W saved[N][32];                    // frame d: B[c] before r(v,c) was selected; then vertex ids (warp_stage)
+  int cost[kCompact ? 1 : N][32];    // frame d: cost when the node was entered (not kCompact)
+  unsigned short pk[N][32];          // frame d: v | (c+1) << 6 | (maxused+1) << 9
+  W cl[N / 4][32];                   // clique masks (R7, k >= 4: cliques of >= 4 vertices)
 };
 using LaneLight = LaneStore<unsigned, 32>;
 using LaneWide = LaneStore<unsigned long long, kMaxComp>;
@@ -229,8 +236,8 @@ __device__ unsigned lane_dfs(LaneStore<W, N>& L, int lane, bool valid, int n, in
       if (ex && depth > 0) {  // spill the parent frame
         const int d = depth - 1;
         L.saved[d][lane] = f_saved;
-        L.cost[d][lane] = f_cost;
-        L.pk[d][lane] = f_v | ((f_c + 1) << 8) | ((f_mu + 1) << 16);
+        if (!LaneStore<W, N>::kCompact) L.cost[d][lane] = f_cost;
+        L.pk[d][lane] = (unsigned short)(f_v | ((f_c + 1) << 6) | ((f_mu + 1) << 9));
       }
       const W av = L.A[v][lane], sav = L.S[v][lane];
       f_v = ex ? v : f_v;
@@ -273,14 +280,24 @@ __device__ unsigned lane_dfs(LaneStore<W, N>& L, int lane, bool valid, int n, in
       const bool pop = exh && fd > 0;
       const int pd = max(fd - 1, 0);
       const W ps = L.saved[pd][lane];
-      const int pc = L.cost[pd][lane], ppk = L.pk[pd][lane];
-      const int pv = pop ? (ppk & 0xff) : f_v;
+      const int ppk = L.pk[pd][lane];
+      const int pv = pop ? (ppk & 63) : f_v;
+      const int pcol = max(((ppk >> 6) & 7) - 1, 0);
       const W pa = L.A[pv][lane], psa = L.S[pv][lane];
+      // the parent's cost: the child's minus the parent's row r(pv, pcol), whose
+      // column set C[pcol] \ {pv} and uncovered set U are as when it was selected
+      int pc;
+      if (LaneStore<W, N>::kCompact) {
+        const W pCc = pick<K, W>(C, pcol) & ~(W(1) << pv);
+        pc = f_cost - kCostUnits * O::popc(pa & pCc) - w_stitch * O::popc(psa & ~U & ~pCc);
+      } else {
+        pc = L.cost[pd][lane];
+      }
       f_saved = pop ? ps : f_saved;
       f_cost = pop ? pc : f_cost;
       f_v = pv;
-      f_c = pop ? ((ppk >> 8) & 0xff) - 1 : (nxt ? c : f_c);
-      f_mu = pop ? ((ppk >> 16) & 0xff) - 1 : f_mu;
+      f_c = pop ? ((ppk >> 6) & 7) - 1 : (nxt ? c : f_c);
+      f_mu = pop ? ((ppk >> 9) & 7) - 1 : f_mu;
       f_adj = pop ? pa : f_adj;
       f_sadj = pop ? psa : f_sadj;
       depth = exh ? fd : depth;
@@ -353,9 +370,9 @@ __device__ __forceinline__ void warp_stage(const Workspace& w, LaneStore<W, N>& 
     const unsigned ro = __shfl_sync(0xffffffffu, rel, o);
     const bool so = __shfl_sync(0xffffffffu, store, o);
     if (e < end) {
-      if (kOrder) {  // vertex ids (after the search: the frames' pk rows are free)
+      if (kOrder) {  // vertex ids (after the search: the frames' saved rows are free)
         const int v = __ldcg(&w.porder[base + e]);
-        if (so) L.pk[e - ro][o] = v;
+        if (so) L.saved[e - ro][o] = (W)(unsigned)v;
       } else {  // adj / sadj words
         const ulonglong2 m = __ldcg((const ulonglong2*)&w.pmask[2 * (base + e)]);
         if (so) {
@@ -401,7 +418,7 @@ __device__ __forceinline__ void lane_component(const GraphView& g, const Workspa
   if (kStaged) warp_stage<W, N, true>(w, L, lane, has, valid, off, n);
   if (!valid) return;
   for (int i = 0; i < n; ++i)
-    colors[kStaged ? L.pk[i][lane] : __ldcg(&w.porder[off + i])] = colour_of<K, W>(bestC, i);
+    colors[kStaged ? (int)L.saved[i][lane] : __ldcg(&w.porder[off + i])] = colour_of<K, W>(bestC, i);
   if (trunc && exact) {
     light_handoff(g, w, ci, n, best_cost);
     acc.handoff += 1;
@@ -416,7 +433,7 @@ __device__ __forceinline__ void lane_component(const GraphView& g, const Workspa
       nc >>= 1;
       ns >>= 1;
       if (nc | ns) {
-        const int l = layout_of(g, kStaged ? L.pk[0][lane] : __ldcg(&w.porder[off]));
+        const int l = layout_of(g, kStaged ? (int)L.saved[0][lane] : __ldcg(&w.porder[off]));
         if (nc) atomicAdd((unsigned long long*)&counts[2 * l], (unsigned long long)nc);
         if (ns) atomicAdd((unsigned long long*)&counts[2 * l + 1], (unsigned long long)ns);
       }
