@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(Graph
 }
 
 // The components of more than 32 vertices (listed by the kernel above), one
-// per lane on 64-bit words; one warp per CTA (LaneWide is 72 KB of shared memory).
+// per lane on 64-bit words; one warp per CTA (LaneWide is 56 KB of shared memory: 4 per SM).
 template <int K>
 __global__ void __launch_bounds__(32) mpld_exact_cover_search_wide(GraphView g, Workspace w, int w_stitch,
                                                                    long long max_steps, int* colors,
