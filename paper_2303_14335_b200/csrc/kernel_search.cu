@@ -282,15 +282,19 @@ __global__ void __launch_bounds__(kCompWarps * 32, 16) mpld_component_discover(G
 }
 
 
-template <int K>
+// Cm: compact frames (no stored node cost; budgeted mode's long searches:
+// more resident warps), else the stored cost (exact mode's 48-node searches:
+// fewer instructions per pop)
+template <int K, bool Cm>
 __global__ void __launch_bounds__(kLaneWarps * 32) mpld_exact_cover_search(GraphView g, Workspace w, int w_stitch,
                                                                            long long max_steps, int* colors,
                                                                            unsigned light_steps, long long* counts,
                                                                            int shard_index, int shard_count) {
   pdl_begin();
   if (gated_off(w)) return;
-  __shared__ LaneLight s_lane[kLaneWarps];
-  LaneLight& L = s_lane[threadIdx.x >> 5];
+  using Store = LaneStore<unsigned, 32, Cm>;
+  __shared__ Store s_lane[kLaneWarps];
+  Store& L = s_lane[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   Control* ctl = w.ctl;
   const int n_comp = __ldcg(&ctl->err) ? 0 : (int)(__ldcg(&ctl->comp_pool) >> 32);
@@ -1598,12 +1602,19 @@ cudaError_t launch_partition_scan(const GraphView& g, Workspace ws, cudaStream_t
   return cudaGetLastError();
 }
 
+int g_light_per_sm[2] = {0, 0};  // resident CTAs per SM of the light kernel: [compact frames]
+
 template <int K>
 cudaError_t launch_search_k(const GraphView& g, Workspace ws, int w_stitch, long long max_steps, int* colors,
                             unsigned light_steps, long long* counts, int shard_index, int shard_count, cudaStream_t s,
                             int blocks, bool pdl) {
-  return launch_ex(mpld_exact_cover_search<K>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws, w_stitch,
-                   max_steps, colors, light_steps, counts, shard_index, shard_count);
+  if (max_steps > 0) {  // budgeted: compact frames, its own resident grid (blocks is the stored-cost kernel's)
+    const int nb = g_light_per_sm[0] > 0 ? blocks / g_light_per_sm[0] * g_light_per_sm[1] : blocks;
+    return launch_ex(mpld_exact_cover_search<K, true>, dim3(nb), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws,
+                     w_stitch, max_steps, colors, light_steps, counts, shard_index, shard_count);
+  }
+  return launch_ex(mpld_exact_cover_search<K, false>, dim3(blocks), dim3(kLaneWarps * 32), 0, s, pdl, false, g, ws,
+                   w_stitch, max_steps, colors, light_steps, counts, shard_index, shard_count);
 }
 
 cudaError_t launch_search(const GraphView& g, Workspace ws, int k, int w_stitch, long long max_steps, int* colors,
@@ -1713,10 +1724,14 @@ int resident_blocks_discover(int num_sms) {
 
 int resident_blocks_search(int threads, int num_sms) {
   (void)threads;
-  for (auto f : {mpld_exact_cover_search<2>, mpld_exact_cover_search<3>, mpld_exact_cover_search<4>})
+  for (auto f : {mpld_exact_cover_search<2, false>, mpld_exact_cover_search<3, false>, mpld_exact_cover_search<4, false>,
+                 mpld_exact_cover_search<2, true>, mpld_exact_cover_search<3, true>, mpld_exact_cover_search<4, true>})
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4>, kLaneWarps * 32, 0);
+  int per_sm = 0, per_sm_c = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mpld_exact_cover_search<4, false>, kLaneWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c, mpld_exact_cover_search<4, true>, kLaneWarps * 32, 0);
+  g_light_per_sm[0] = per_sm;
+  g_light_per_sm[1] = per_sm_c > 0 ? per_sm_c : per_sm;
   return per_sm * num_sms;
 }
 

@@ -176,9 +176,9 @@ constexpr bool kStagedLight = MPLD_STAGED_LIGHT != 0;  // coalesced warp staging
 // per warp: four 64-bit lane warps per SM instead of three; the 32-bit light
 // kernel keeps the cost, measured faster there).  After the search the saved
 // rows hold the staged vertex ids.
-template <typename W, int N>
+template <typename W, int N, bool Cm = (N > 32)>
 struct __align__(16) LaneStore {
-  static constexpr bool kCompact = N > 32;
+  static constexpr bool kCompact = Cm;
   W A[N][32];                        // adj[v][lane]
   W S[N][32];                        // sadj[v][lane]
   W saved[N][32];                    // frame d: B[c] before r(v,c) was selected; then vertex ids (warp_stage)
@@ -192,8 +192,8 @@ using LaneWide = LaneStore<unsigned long long, kMaxComp>;
 // The relaxed Algorithm X of R4-R7 with branch and bound, one component per
 // lane (the oracle's node order, incumbent rule and budget); returns the nodes
 // entered and the best leaf's colour masks in bestC.
-template <int K, typename W, int N>
-__device__ unsigned lane_dfs(LaneStore<W, N>& L, int lane, bool valid, int n, int w_stitch, unsigned budget, int ncl,
+template <int K, typename W, int N, bool Cm>
+__device__ unsigned lane_dfs(LaneStore<W, N, Cm>& L, int lane, bool valid, int n, int w_stitch, unsigned budget, int ncl,
                              W clu, W (&bestC)[K], int& best, bool& trunc) {
   using O = WordOps<W>;
   W C[K], B[K];
@@ -236,7 +236,7 @@ __device__ unsigned lane_dfs(LaneStore<W, N>& L, int lane, bool valid, int n, in
       if (ex && depth > 0) {  // spill the parent frame
         const int d = depth - 1;
         L.saved[d][lane] = f_saved;
-        if (!LaneStore<W, N>::kCompact) L.cost[d][lane] = f_cost;
+        if (!Cm) L.cost[d][lane] = f_cost;
         L.pk[d][lane] = (unsigned short)(f_v | ((f_c + 1) << 6) | ((f_mu + 1) << 9));
       }
       const W av = L.A[v][lane], sav = L.S[v][lane];
@@ -287,7 +287,7 @@ __device__ unsigned lane_dfs(LaneStore<W, N>& L, int lane, bool valid, int n, in
       // the parent's cost: the child's minus the parent's row r(pv, pcol), whose
       // column set C[pcol] \ {pv} and uncovered set U are as when it was selected
       int pc;
-      if (LaneStore<W, N>::kCompact) {
+      if (Cm) {
         const W pCc = pick<K, W>(C, pcol) & ~(W(1) << pv);
         pc = f_cost - kCostUnits * O::popc(pa & pCc) - w_stitch * O::popc(psa & ~U & ~pCc);
       } else {
@@ -357,8 +357,8 @@ __device__ __forceinline__ int warp_owner(unsigned rel, unsigned e) {
   return o;
 }
 
-template <typename W, int N, bool kOrder>
-__device__ __forceinline__ void warp_stage(const Workspace& w, LaneStore<W, N>& L, int lane, bool has, bool store,
+template <typename W, int N, bool kOrder, bool Cm>
+__device__ __forceinline__ void warp_stage(const Workspace& w, LaneStore<W, N, Cm>& L, int lane, bool has, bool store,
                                            size_t off, int n) {
   __syncwarp();  // the lanes' earlier accesses to the rows written below (frames / masks) are complete
   const size_t base = __shfl_sync(0xffffffffu, off, 0);  // lane 0 always holds a record
@@ -390,8 +390,8 @@ __device__ __forceinline__ void warp_stage(const Workspace& w, LaneStore<W, N>& 
 // hand-off to the warp-parallel search (exact mode, light budget exceeded).
 // kStaged: the warp's records are consecutive (warp_stage), `has` = the lane
 // holds a record; else each lane reads its own record.
-template <int K, typename W, int N, bool kStaged>
-__device__ __forceinline__ void lane_component(const GraphView& g, const Workspace& w, LaneStore<W, N>& L, int lane,
+template <int K, typename W, int N, bool kStaged, bool Cm>
+__device__ __forceinline__ void lane_component(const GraphView& g, const Workspace& w, LaneStore<W, N, Cm>& L, int lane,
                                                bool has, bool valid, int ci, unsigned long long rec, int w_stitch,
                                                unsigned budget, bool exact, int* colors, long long* counts,
                                                LightAcc& acc) {
