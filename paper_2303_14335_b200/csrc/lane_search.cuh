@@ -117,6 +117,27 @@ __device__ __forceinline__ int clique_deficit(const W (&B)[K], W U, W Z, const W
   return d;
 }
 
+// The same clique term with the cliques in registers (the lane searches: at
+// most N / 4 cliques of >= 4 vertices, zero masks past ncl contribute 0), the
+// loop unrolled up to the warp's largest clique count (no shared-memory loads,
+// no per-clique branch).
+template <int K, typename W, int NQ>
+__device__ __forceinline__ int clique_deficit_reg(const W (&B)[K], W U, W Z, const W (&clr)[NQ], int nq_warp) {
+  using O = WordOps<W>;
+  int d = 0;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    if (q < nq_warp) {
+      const W X = clr[q] & U & ~Z;
+      int live = 0;
+#pragma unroll
+      for (int c = 0; c < K; ++c) live += (X & ~B[c]) ? 1 : 0;
+      d += max(0, O::popc(X) - live);
+    }
+  }
+  return d;
+}
+
 template <int K>
 __host__ __device__ constexpr int heavy_clique_min() {
   return MPLD_HEAVY_CLIQUE > 0 ? MPLD_HEAVY_CLIQUE : clique_min<K>();
@@ -207,7 +228,11 @@ __device__ unsigned lane_dfs(LaneStore<W, N, Cm>& L, int lane, bool valid, int n
   bool active = valid, enter = valid;
   W f_saved = 0, f_adj = 0, f_sadj = 0;
   int f_cost = 0, f_v = 0, f_c = -1, f_mu = -1;
-  const W* cl = &L.cl[0][lane];
+  constexpr int kNQ = N / 4;  // cliques in registers (clique_deficit_reg)
+  W clr[kNQ];
+#pragma unroll
+  for (int q = 0; q < kNQ; ++q) clr[q] = (clique_min<K>() > 0 && q < ncl) ? L.cl[q][lane] : W(0);
+  const int nq_warp = clique_min<K>() > 0 ? (int)__reduce_max_sync(0xffffffffu, (unsigned)ncl) : 0;
   while (__any_sync(0xffffffffu, active)) {
     const bool en = active && enter;
     if (en && ++steps > budget && best != INT_MAX) {  // budget (R7): stop at exactly the oracle's node
@@ -223,7 +248,8 @@ __device__ unsigned lane_dfs(LaneStore<W, N, Cm>& L, int lane, bool valid, int n
       // node order as the oracle; most nodes skip the clique loop)
       const int base = cost + kCostUnits * O::popc(Z);
       const bool undecided = clique_min<K>() > 0 && base < best && base + kCostUnits * O::popc(U & ~Z & clu) >= best;
-      const int lb = undecided ? base + kCostUnits * clique_deficit<K, W>(B, U, Z, cl, 32, ncl) : base;
+      const int lb =
+          undecided ? base + kCostUnits * clique_deficit_reg<K, W, kNQ>(B, U, Z, clr, nq_warp) : base;
       const bool leaf = U == 0;
       const bool better = active && en && leaf && cost < best;  // Alg. 1 line 5, strict improvement
       const bool ex = active && en && !leaf && lb < best;       // bound (R7)
